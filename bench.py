@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""Benchmark of the rehearsal-buffer hot path (update + unbiased global sample + augmented
+batch), BASELINE.json metric "augmented samples/sec (update+global sample)".
+
+Our arm (default): one process per GPU (torchrun for N>1). A step is one engine iteration
+on every rank: insert candidates of m_i, publish occupancy, draw reps(i-1) from the global
+buffer, materialise m'_i = m_i ++ reps(i-1) (one fused sm_100a launch per rank, issued from
+native code over a device-resident input ring larger than L2). value = augmented samples
+produced by all ranks / max-over-ranks device time. e2e = the same through the host-buffer
+C-ABI call (drb_rb_step_host: pinned host m_i in, m'_i back to pinned host memory).
+
+Reference arm (--impl reference): the unmodified reference C++ engine (oracle/_ref,
+compiled from /root/reference sources) — N in-process workers over loopback TCP, each
+doing engine.update(m) + augment(m, reps) — on rank 0's host cores, bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs[1] (the metric's named config), parameters per SURVEY.md §8d:
+# ImageNet-100 shape 224x224x3 uint8, K=100 in 4 class-incremental tasks, b=56, r=7, c=14,
+# |B| = 30% of ImageNet-100 (~130k) spread over 8 GPUs -> 4875 per GPU -> cap 48 per class.
+CONFIGS = {
+    "c2": dict(workload="imagenet100-224x224x3-u8-class-incremental", K=100, T=4, cap=48, S=224 * 224 * 3,
+               dtype="u8", b=56, r=7, c=14),
+    "c1": dict(workload="synthetic-32x32x3-fp32", K=10, T=1, cap=100, S=32 * 32 * 3 * 4, dtype="f32",
+               b=64, r=8, c=14),
+    "c3": dict(workload="imagenet1k-224x224x3-u8-10pct-per-gpu", K=1000, T=4, cap=128, S=224 * 224 * 3,
+               dtype="u8", b=56, r=7, c=14),
+    "c4": dict(workload="imagenet100-224x224x3-fp16-b128", K=100, T=4, cap=48, S=224 * 224 * 3 * 2,
+               dtype="f16", b=128, r=28, c=14),
+    "c5": dict(workload="sensor-128x128x1-fp32", K=50, T=1, cap=40, S=128 * 128 * 4, dtype="f32",
+               b=256, r=32, c=14),
+}
+METRIC = "augmented samples/sec (update+global sample)"
+UNIT = "aug_samples/s"
+
+
+def hbm_bytes_per_step(cfg) -> int:
+    """SURVEY.md §8d algorithmic HBM bytes per rank per iteration: 2*S*(c + r + b)."""
+    return 2 * cfg["S"] * (cfg["c"] + cfg["r"] + cfg["b"])
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_dev{device}_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 6 and parts[0].isdigit():
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def cpu_baseline_sample(cfg, n_workers: int, iters: int, warmup: int):
+    """Reference engine on the host cores (oracle/_ref), else the C port oracle replay."""
+    from oracle.py_oracle import Backend, have_reference
+    from paper_2406_03285_b200.workload import stream_spec
+    spec = stream_spec(cfg["K"], cfg["T"], cfg["b"], cfg["S"], steps_per_task=100, seed=1)
+    ring = 8
+    data = np.stack([np.stack([spec.payload(w, i) for i in range(ring)]) for w in range(n_workers)])
+    labels = np.stack([np.stack([spec.labels(w, i) for i in range(ring)]) for w in range(n_workers)])
+    if have_reference():
+        be = Backend("reference")
+        secs, samples = be.engine_bench(n_workers, cfg["K"], cfg["cap"], cfg["S"], cfg["b"], cfg["c"], cfg["r"],
+                                        1, data, labels, warmup, iters)
+        kind, cores = "reference", 2 * n_workers + (3 * n_workers * (n_workers - 1) if n_workers > 1 else 0)
+        cores = min(cores, os.cpu_count() or 1)
+    else:
+        be = Backend("port")
+        rp = be.replay(n_workers, cfg["K"], cfg["cap"], cfg["S"], cfg["c"], cfg["r"], 1)
+        for i in range(warmup):
+            rp.step(data[:, i % ring], labels[:, i % ring])
+        t0 = time.perf_counter()
+        samples = 0
+        for i in range(iters):
+            _, _, cnt = rp.step(data[:, i % ring], labels[:, i % ring])
+            samples += int(cnt.sum())
+        secs = time.perf_counter() - t0
+        kind, cores = "port", 1
+    return {"value": samples / secs, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{iters} iterations x {n_workers} worker(s) of {cfg['workload']} after {warmup} warm-up "
+                      f"(f32-packed payload, same byte volume), {samples} augmented samples in {secs:.2f}s"}
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    n = args.gpus if args.gpus else world
+    if rank != 0:
+        return 0
+    try:
+        iters = max(1, min(args.steps, args.ref_iters))
+        cb = cpu_baseline_sample(cfg, n, iters, min(args.warmup, 50) if args.warmup else 10)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}), flush=True)
+        return 0
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": n,
+            "steps": iters, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["b"] * n / cb["value"] if cb["value"] else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+            "data": "synthetic", "config": {"workload": cfg["workload"], "K": cfg["K"], "cap": cfg["cap"],
+                                            "b": cfg["b"], "r": cfg["r"], "c": cfg["c"], "S": cfg["S"],
+                                            "n_workers": n},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--ring", type=int, default=64, help="device input batches (>L2 in total)")
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--cpu-iters", type=int, default=300)
+    ap.add_argument("--ref-iters", type=int, default=400)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_03285_b200 as drb
+    from paper_2406_03285_b200.workload import stream_spec
+
+    world, rank, local = dist_env()
+    N = world
+    if args.gpus and args.gpus != world:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("bench.py --gpus N>1 must be launched under torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device(f"cuda:{local}"))
+
+    K, cap, S, b, r, c = cfg["K"], cfg["cap"], cfg["S"], cfg["b"], cfg["r"], cfg["c"]
+    steps_per_task = 100
+    spec = stream_spec(K, cfg["T"], b, S, steps_per_task=steps_per_task, seed=1)
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, rank=rank,
+                               world=N, device=local)
+    if N > 1:
+        blobs = [None] * N
+        dist.all_gather_object(blobs, buf.export_handle())
+        buf.connect(blobs)
+    eng = drb.engine(buf)
+    eng.start()
+
+    ring = args.ring
+    from paper_2406_03285_b200.workload import device_ring
+    data, _ = device_ring(spec, rank, ring, f"cuda:{local}")
+    # Labels follow the class-incremental schedule. The ring of labels is re-drawn per
+    # phase so prefill visits every task (buffers fill) and the timed region sits in one.
+    def labels_for(first):
+        return torch.from_numpy(np.stack([spec.labels(rank, first + i) for i in range(ring)]).astype(np.int32)).cuda(local)
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if N > 1:
+            dist.barrier(device_ids=[local])
+
+    # prefill: every task's classes fill to capacity (replacements dominate afterwards)
+    step = 0
+    prefill = cfg["T"] * steps_per_task
+    while step < prefill:
+        lab = labels_for(step)
+        cnt = min(ring, prefill - step)
+        eng.run(data[:cnt], lab[:cnt], cnt, first=0, stream=stream)
+        step += cnt
+        stream.synchronize()
+    lab = labels_for(step)
+    eng.run(data, lab, args.warmup, first=0, stream=stream)
+    step += args.warmup
+    stream.synchronize()
+    barrier()
+
+    # timed region: K steps, back to back, device-timed (events on the launching stream)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        eng.run(data, lab, args.steps, first=args.warmup, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    step += args.steps
+    if N > 1:
+        tt = torch.tensor([t_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    samples = (b + r) * N * args.steps  # steady state: every rank's m'_i has b + r rows
+    value = samples / (t_ms / 1000.0)
+    ms_per_step = t_ms / args.steps
+
+    # per-launch device time of the (single) step kernel: events bracketing each launch
+    nper = 256
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nper)]
+    barrier()
+    eng.run(data, lab, nper, first=0, stream=stream, events=evs)
+    torch.cuda.synchronize()
+    launch_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(nper)]
+    kernel_ms = float(np.mean(launch_ms))
+    step += nper
+    if N > 1:
+        tt = torch.tensor([kernel_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        kernel_ms = float(tt.item())
+
+    # e2e through the host-buffer C-ABI call (pinned host m_i in, pinned host m'_i out)
+    e2e_steps = args.e2e_steps
+    hring = 4
+    h_data = torch.empty((hring, b, S), dtype=torch.uint8).pin_memory()
+    h_data.copy_(data[:hring].cpu())
+    h_lab = torch.empty((hring, b), dtype=torch.int32).pin_memory()
+    h_lab.copy_(lab[:hring].cpu())
+    h_out = torch.empty((2, b + r, S), dtype=torch.uint8).pin_memory()
+    h_out_l = torch.empty((2, b + r), dtype=torch.int32).pin_memory()
+    h_cnt = torch.zeros(2, dtype=torch.int32).pin_memory()
+    hd, hl, ho, hol, hc = (x.numpy() for x in (h_data, h_lab, h_out, h_out_l, h_cnt))
+    for i in range(8):  # warm
+        eng.update_host(hd[i % hring], hl[i % hring].view(np.uint32), ho[i % 2], hol[i % 2].view(np.uint32),
+                        hc[i % 2:i % 2 + 1].view(np.uint32))
+    eng.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        eng.update_host(hd[i % hring], hl[i % hring].view(np.uint32), ho[i % 2], hol[i % 2].view(np.uint32),
+                        hc[i % 2:i % 2 + 1].view(np.uint32))
+    eng.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if N > 1:
+        tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = (b + r) * N * e2e_steps / e2e_s
+    eng.shutdown()
+
+    peak, peak_kind = peaks()
+    bytes_step = hbm_bytes_per_step(cfg)
+    achieved = bytes_step / (kernel_ms / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_sample(cfg, 1, args.cpu_iters, 20)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "config": {"workload": cfg["workload"], "K": K, "cap": cap, "b": b, "r": r, "c": c, "S": S,
+                       "tasks": cfg["T"], "steps_per_task": steps_per_task,
+                       "parallelism": f"dp{N}" if N > 1 else "single",
+                       "l2": f"inputs larger than L2: {ring}-batch device ring ({ring * b * S / 2**20:.0f} MiB), "
+                             f"slab {K * cap * S / 2**20:.0f} MiB per GPU"},
+            "gpu_launches": args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": b * (S + 4),
+                    "d2h_bytes_per_step": (b + r) * (S + 4) + 4, "steps": e2e_steps},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": bytes_step, "kernel_ms": kernel_ms,
+                         "kernel": "drb_step_kernel"},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,229 @@
+#ifndef DRB_RB_H
+#define DRB_RB_H
+
+/*
+ * drb_rb — C ABI of the B200-native distributed rehearsal buffer (arXiv 2406.03285).
+ *
+ * This is the drop-in boundary for the reference's hot path. The
+ * reference exposes that path only through its C++ API:
+ *   rehearsal_buffer(K, cap) / update_buffer / read_slots / snapshot / total_stored /
+ *   cross_class_evictions          proj/src/buffer/rehearsal_buffer.hpp:60-95
+ *   engine(cfg, rank, ...) / start / update / shutdown / total_wait_ms / drain_timings
+ *                                  proj/src/engine/engine.hpp:53-93
+ *   plan / augment                 proj/src/sampler/sampler.hpp:33-61
+ *   rng_stream                     proj/src/core/rng.hpp:16-51
+ * and its own C ABI (proj/include/drb.h) only has run-level entry points. Every function
+ * below replaces one of those C++ calls (cited per function) and follows the reference C
+ * ABI's conventions: opaque handles, drb_status codes (proj/include/drb.h:33-43), a
+ * thread-local drb_last_error() (proj/src/capi/drb_capi.cpp:15,69-71), NULL arguments ->
+ * DRB_ERR_INVALID_ARGUMENT, exception taxonomy -> status (drb_capi.cpp:29-46).
+ *
+ * No torch types: device buffers are plain device pointers, streams are cudaStream_t
+ * passed as void* (NULL = the handle's own stream).
+ *
+ * Payloads are opaque fixed-size samples of `sample_bytes` bytes (S); labels are uint32.
+ * The reference stores float features; any S that is a multiple of 4 is bit-compatible
+ * with it (bytes packed into floats).
+ */
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(_WIN32)
+#define DRB_RB_API __declspec(dllexport)
+#else
+#define DRB_RB_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef DRB_STATUS_DEFINED
+#define DRB_STATUS_DEFINED
+/* Identical numbering to proj/include/drb.h:33-43. */
+typedef enum drb_status {
+    DRB_OK = 0,
+    DRB_ERR_INVALID_ARGUMENT = 1,
+    DRB_ERR_CONFIG = 2,
+    DRB_ERR_IO = 3,
+    DRB_ERR_TRANSPORT = 4,
+    DRB_ERR_PROTOCOL = 5,
+    DRB_ERR_TRAINING = 6, /* also engine_error, as drb_capi.cpp:40-41 maps it */
+    DRB_ERR_USAGE = 7,
+    DRB_ERR_INTERNAL = 8
+} drb_status;
+#endif
+
+#define DRB_RB_MAX_WORLD 8
+
+/* rng purposes, proj/src/core/rng.hpp:18-26 */
+enum {
+    DRB_PURPOSE_CANDIDATE_SELECTION = 1,
+    DRB_PURPOSE_EVICTION = 2,
+    DRB_PURPOSE_GLOBAL_SAMPLING = 3,
+    DRB_PURPOSE_DATA_SHUFFLE = 4,
+    DRB_PURPOSE_MODEL_INIT = 5,
+    DRB_PURPOSE_SLOT_SUBSTITUTE = 6,
+    DRB_PURPOSE_SYNTH = 7
+};
+
+/* Counter-based stream state: replaces rng_stream (proj/src/core/rng.hpp:16-51).
+ * key = derive_key(...), ctr = number of draws consumed so far. Plain data, host side;
+ * device kernels consume draws and write the advanced counter back. */
+typedef struct drb_rng {
+    uint64_t key;
+    uint64_t ctr;
+} drb_rng;
+
+typedef struct drb_rb drb_rb; /* one rank: HBM slab + occupancy + engine state */
+
+typedef struct drb_rb_config {
+    uint32_t n_classes;       /* K                                   (config.hpp:37) */
+    uint32_t per_class_cap;   /* floor(S_max / K)                    (capacity.cpp:10-18) */
+    uint64_t sample_bytes;    /* S, multiple of 4                                        */
+    uint32_t max_batch;       /* largest |m| ever passed to step/update_buffer (b)       */
+    uint32_t candidate_count; /* c                                   (config.hpp:41)     */
+    uint32_t rep_count;       /* r                                   (config.hpp:40)     */
+    uint32_t rank;            /* worker id                                               */
+    uint32_t world;           /* N <= DRB_RB_MAX_WORLD                                   */
+    uint64_t seed;            /* rng_seed                            (config.hpp:49)     */
+    int32_t device;           /* CUDA device ordinal                                     */
+    uint32_t flags;           /* reserved, 0                                             */
+} drb_rb_config;
+
+/* Per-class insertion report of one update, replaces insertion_report
+ * (proj/src/buffer/rehearsal_buffer.hpp:17-26). Arrays are caller-owned, K entries. */
+typedef struct drb_insertion_report {
+    uint32_t* per_class_appends;
+    uint32_t* per_class_replacements;
+    uint32_t appends;
+    uint32_t replacements;
+} drb_insertion_report;
+
+/* Read request / status, replaces read_request / read_status (rehearsal_buffer.hpp:28-37). */
+typedef struct drb_read_request {
+    uint32_t cls;
+    uint32_t slot;
+} drb_read_request;
+enum { DRB_READ_EXACT = 0, DRB_READ_SUBSTITUTED = 1, DRB_READ_EMPTY = 2 };
+
+/* Global slot reference (owner, cls, slot), replaces slot_ref (proj/src/core/types.hpp:26-32). */
+typedef struct drb_slot_ref {
+    uint32_t owner;
+    uint32_t cls;
+    uint32_t slot;
+} drb_slot_ref;
+
+/* Augmented mini-batch m'_i = m_i ++ reps(i-1), engine-owned device memory.
+ * rows [0, n) are m_i, rows [n, count) the representatives in plan order
+ * (sampler.cpp:234-240). `count` is valid once the step's work on the stream completes
+ * (drb_rb_aug_count). Valid until work enqueued before the next-but-one step call. */
+typedef struct drb_aug {
+    void* data;            /* count x S bytes, contiguous          */
+    uint32_t* labels;      /* count labels                          */
+    uint32_t n;            /* |m_i|                                 */
+    uint32_t ring_slot;    /* pass to drb_rb_aug_count              */
+    uint64_t step;         /* iteration index i                     */
+} drb_aug;
+
+/* ---- library ------------------------------------------------------------------------- */
+DRB_RB_API const char* drb_rb_version(void);
+/* Last error message of the calling thread; never NULL (drb_capi.cpp:69-71). */
+DRB_RB_API const char* drb_rb_last_error(void);
+
+/* ---- rng_stream (proj/src/core/rng.cpp:33-53) ------------------------------------------ */
+/* rng_stream(seed, worker, purpose)                       rng.cpp:33-34 */
+DRB_RB_API drb_status drb_rng_init(drb_rng* s, uint64_t seed, uint32_t worker, uint32_t purpose);
+/* rng_stream::keyed(seed, worker, purpose, k1, k2)        rng.cpp:36-39 */
+DRB_RB_API drb_status drb_rng_keyed(drb_rng* s, uint64_t seed, uint32_t worker, uint32_t purpose,
+                                    uint64_t k1, uint64_t k2);
+/* n draws on the GPU: next_u64 (bound == 0) or bounded(bound) (rng.cpp:41-53); out is host
+ * memory; s->ctr advances exactly as n sequential calls would. */
+DRB_RB_API drb_status drb_rng_draw(drb_rng* s, uint64_t bound, uint64_t n, uint64_t* out,
+                                   int32_t device);
+/* sample_without_replacement(n, k, rng) on the GPU (rehearsal_buffer.cpp:14-26). out: min(n,k). */
+DRB_RB_API drb_status drb_sample_without_replacement(uint32_t n, uint32_t k, drb_rng* s,
+                                                     uint32_t* out, uint32_t* out_k,
+                                                     int32_t device);
+/* plan(want, view, rng) on the GPU (sampler.cpp:65-68). occ: host [n_workers][n_classes].
+ * out: host, capacity min(want, total) refs; *out_count = entries written. */
+DRB_RB_API drb_status drb_plan(uint32_t want, uint32_t n_workers, uint32_t n_classes,
+                               const uint32_t* occ, drb_rng* s, drb_slot_ref* out,
+                               uint32_t* out_count, int32_t device);
+
+/* ---- rehearsal_buffer (proj/src/buffer/rehearsal_buffer.hpp:60-95) --------------------- */
+/* rehearsal_buffer(K, cap) + engine(cfg, rank, ...) storage. config_error on K==0 / cap==0
+ * (rehearsal_buffer.cpp:30-31). */
+DRB_RB_API drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out);
+DRB_RB_API drb_status drb_rb_destroy(drb_rb* h);
+
+/* update_buffer(m, c, cand, evict) (rehearsal_buffer.cpp:37-86). batch/labels: DEVICE
+ * pointers, n samples. Synchronous. usage_error (DRB_ERR_USAGE) on any label >= K, before
+ * any draw. report may be NULL. Not allowed while the engine is started with world > 1. */
+DRB_RB_API drb_status drb_rb_update_buffer(drb_rb* h, const void* batch, const uint32_t* labels,
+                                           uint32_t n, uint32_t c, drb_rng* cand,
+                                           drb_rng* evict, drb_insertion_report* report);
+/* read_slots(requests, substitute_rng) (rehearsal_buffer.cpp:88-142). requests/status: host;
+ * out/out_labels: DEVICE, count rows of S bytes. Synchronous. */
+DRB_RB_API drb_status drb_rb_read_slots(drb_rb* h, const drb_read_request* requests,
+                                        uint32_t count, drb_rng* substitute, void* out,
+                                        uint32_t* out_labels, uint8_t* status);
+/* snapshot() (rehearsal_buffer.cpp:144-152): per_class[K] host, version. */
+DRB_RB_API drb_status drb_rb_snapshot(drb_rb* h, uint32_t* per_class, uint64_t* version);
+DRB_RB_API drb_status drb_rb_total_stored(drb_rb* h, uint64_t* out);
+DRB_RB_API drb_status drb_rb_cross_class_evictions(drb_rb* h, uint64_t* out);
+/* Raw device views for zero-copy consumers: slab [K][cap][S], slab labels [K][cap]. */
+DRB_RB_API drb_status drb_rb_device_views(drb_rb* h, void** slab, uint32_t** slab_labels);
+
+/* ---- multi-rank wiring (replaces worker_mesh + rpc transport, proj/src/runner/mesh.cpp) -- */
+/* Export this rank's peer-shareable region (CUDA IPC handle + metadata) into blob. */
+DRB_RB_API drb_status drb_rb_export_handle(drb_rb* h, void* blob, size_t* len);
+DRB_RB_API size_t drb_rb_handle_size(void);
+/* Map every rank's region; blobs = world blobs of drb_rb_handle_size() bytes in rank order
+ * (the caller does the all-gather, e.g. torch.distributed). */
+DRB_RB_API drb_status drb_rb_connect(drb_rb* h, const void* blobs, size_t blob_len);
+
+/* ---- engine (proj/src/engine/engine.hpp:53-93) ------------------------------------------ */
+DRB_RB_API drb_status drb_rb_start(drb_rb* h);    /* usage_error on double start (engine.cpp:50-52) */
+DRB_RB_API drb_status drb_rb_shutdown(drb_rb* h); /* usage_error before start / twice (:203-206) */
+/* One iteration: `reps = engine.update(m_i); m' = augment(m_i, reps)` fused
+ * (trainer.cpp:109-113). Enqueues on `stream` (device batch/labels): insert candidates of
+ * m_i (round i), publish occupancy version i+1, and materialise m'_i = m_i ++ reps(i-1)
+ * where reps(i-1) = plan(r, view at version i) read at version i — the exact-horizon
+ * semantics of engine.cpp:138-170. out describes m'_i. usage_error before start / after
+ * shutdown; engine_error (DRB_ERR_TRAINING) once a previous round failed. */
+DRB_RB_API drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels,
+                                  uint32_t n, void* stream, drb_aug* out);
+/* Same, with HOST (ideally pinned) buffers: copies m_i in, runs the step, copies m'_i out
+ * into out/out_labels (capacity n + r rows). Asynchronous on the handle's streams;
+ * call drb_rb_synchronize before reading out or *out_count. */
+DRB_RB_API drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels,
+                                       uint32_t n, void* out, uint32_t* out_labels,
+                                       uint32_t* out_count);
+/* `steps` consecutive iterations over a device-resident ring of `ring` input batches
+ * (batch j at batches + j*batch_stride bytes, labels + j*label_stride elements), issued
+ * back to back from native code on `stream`. The throughput-harness analogue of
+ * drb_overlap_bench (proj/include/drb.h:107-114, proj/src/runner/overlap.cpp:83-89, zero
+ * train cost). If step_events is non-NULL it must hold 2*steps cudaEvent_t created by the
+ * caller; launch i is bracketed by events 2i and 2i+1 (per-launch device timing). */
+DRB_RB_API drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride,
+                                 const uint32_t* labels, uint64_t label_stride, uint32_t ring,
+                                 uint32_t n, uint64_t steps, uint64_t first, void* stream,
+                                 void* const* step_events);
+/* Rows of m' for a completed step (blocks on that step's completion). */
+DRB_RB_API drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count);
+DRB_RB_API drb_status drb_rb_synchronize(drb_rb* h);
+/* total_wait_ms (engine.hpp:88): host time blocked waiting for round results. */
+DRB_RB_API drb_status drb_rb_total_wait_ms(drb_rb* h, double* out);
+/* Device-side error word of the last completed step (0 = none). */
+DRB_RB_API drb_status drb_rb_device_error(drb_rb* h, uint32_t* out);
+/* Launch configuration of the step kernel: grid CTAs, threads, dynamic smem. */
+DRB_RB_API drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads,
+                                         uint32_t* smem);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* DRB_RB_H */

@@ -1,0 +1,746 @@
+// C ABI of the B200 rehearsal buffer (include/drb_rb.h). Host C++: allocation, IPC
+// wiring, launch sequencing, error mapping. Conventions follow the reference C ABI
+// (proj/src/capi/drb_capi.cpp:15-59): thread-local last error, status codes, guarded calls.
+
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "drb_internal.cuh"
+
+using namespace drb_b200;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+struct status_error : std::runtime_error {
+    drb_status code;
+    status_error(drb_status c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+[[noreturn]] void fail(drb_status c, const std::string& what) { throw status_error(c, what); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(DRB_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+drb_status guarded(F&& f) {
+    try {
+        f();
+        return DRB_OK;
+    } catch (const status_error& e) {
+        t_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        t_last_error = "out of memory";
+        return DRB_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        t_last_error = e.what();
+        return DRB_ERR_INTERNAL;
+    } catch (...) {
+        t_last_error = "unknown error";
+        return DRB_ERR_INTERNAL;
+    }
+}
+
+#define DRB_REQUIRE(cond)                                           \
+    do {                                                            \
+        if (!(cond)) {                                              \
+            t_last_error = "null argument";                         \
+            return DRB_ERR_INVALID_ARGUMENT;                        \
+        }                                                           \
+    } while (0)
+
+// Host restatement of derive_key (rng.cpp:19-27) — used only to key the device streams.
+uint64_t host_mix64(uint64_t z) {
+    z += kPhi;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+uint64_t derive_key(uint64_t seed, uint64_t worker, uint64_t purpose, uint64_t k1, uint64_t k2) {
+    uint64_t key = host_mix64(seed);
+    key = host_mix64(key ^ (worker * 0xd1342543de82ef95ULL));
+    key = host_mix64(key ^ (purpose * 0xaf251af3b0f025b5ULL));
+    key = host_mix64(key ^ k1);
+    key = host_mix64(key ^ k2);
+    return key;
+}
+
+struct device_guard {
+    int prev = -1;
+    explicit device_guard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev)
+            cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~device_guard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev)
+            cudaSetDevice(prev);
+    }
+};
+
+struct handle_blob {
+    uint32_t magic;
+    uint32_t version;
+    int32_t pid;
+    int32_t device;
+    uint32_t rank;
+    uint32_t world;
+    uint64_t region_bytes;
+    uint64_t region_ptr;  // raw device pointer (same-process peers)
+    cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kBlobMagic = 0x44524232;  // "DRB2"
+
+// Scoped temporary device allocation for the synchronous test-facing calls.
+struct dev_tmp {
+    void* p = nullptr;
+    explicit dev_tmp(size_t bytes) { cuda_check(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
+    ~dev_tmp() { cudaFree(p); }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct drb_rb {
+    drb_rb_config cfg{};
+    RegionLayout layout{};
+    uint32_t smem_bytes = 0;
+    uint32_t grid = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;    // default stream of the handle
+    cudaStream_t h2d = nullptr;       // host-path input copies
+    cudaStream_t d2h = nullptr;       // host-path output copies
+    uint8_t* slab = nullptr;          // [K][cap][S]
+    uint32_t* slab_labels = nullptr;  // [K][cap]
+    uint8_t* region = nullptr;        // own peer-shareable region
+    uint8_t* peers[kMaxWorld] = {};   // every rank's region, mapped here
+    bool peer_opened[kMaxWorld] = {};
+    bool connected = false;
+    DevState* state = nullptr;        // [2]
+    uint32_t cur = 0;                 // state[cur] is current
+    uint64_t ver = 0;                 // occupancy table version index (slot = ver % 3)
+    uint32_t* report = nullptr;       // [2K+2]
+    uint32_t* mailbox = nullptr;      // host-mapped [2*kAugRing]
+    uint32_t* mailbox_dev = nullptr;
+    cudaEvent_t done[kAugRing] = {};  // completion of the step that last wrote each slot
+    cudaEvent_t in_free[2] = {};      // host path: staging slot reusable
+    cudaEvent_t h2d_done[2] = {};
+    uint8_t* stage = nullptr;         // host path: device staging [2][max_batch][S]
+    uint32_t* stage_labels = nullptr; // [2][max_batch]
+    uint64_t cand_key = 0, evict_key = 0, samp_key[kMaxWorld] = {};
+    uint64_t step = 0;
+    bool started = false, shut_down = false;
+    double wait_ms = 0.0;
+    uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+};
+
+namespace {
+
+void check_engine_alive(drb_rb* h) {
+    // Sticky failure of an earlier round (device-written, host-mapped), observed without
+    // blocking. A round whose failure is not yet visible is caught on the device instead
+    // (the next launch sees DevState::error and reports it in its own mailbox slot).
+    const uint32_t e = reinterpret_cast<volatile uint32_t*>(h->mailbox)[2 * kAugRing];
+    if (e)
+        fail(DRB_ERR_TRAINING, "engine: background pipeline dead: round failed with status " +
+                                   std::to_string(e) +
+                                   (e == DRB_ERR_USAGE ? " (label out of range)" : " (peer rendezvous timeout)"));
+}
+
+StepParams base_params(drb_rb* h) {
+    StepParams p{};
+    const auto& c = h->cfg;
+    p.K = c.n_classes;
+    p.cap = c.per_class_cap;
+    p.N = c.world;
+    p.me = c.rank;
+    p.c = c.candidate_count;
+    p.r = c.rep_count;
+    p.nmax = c.max_batch;
+    p.S = c.sample_bytes;
+    p.cand_key = h->cand_key;
+    p.evict_key = h->evict_key;
+    for (int q = 0; q < kMaxWorld; ++q)
+        p.samp_key[q] = h->samp_key[q];
+    p.slab = h->slab;
+    p.slab_labels = h->slab_labels;
+    for (int q = 0; q < kMaxWorld; ++q)
+        p.region[q] = h->peers[q];
+    p.region[c.rank] = h->region;
+    p.off_table = h->layout.off_table;
+    p.off_aug = h->layout.off_aug;
+    p.off_auglab = h->layout.off_auglab;
+    p.aug_slot_bytes = h->layout.aug_slot_bytes;
+    p.auglab_slot_elems = align_up(h->layout.rows * 4, 256) / 4;
+    p.report = h->report;
+    p.mailbox = h->mailbox_dev;
+    p.timeout_ns = h->timeout_ns;
+    p.smem_bytes = h->smem_bytes;
+    return p;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* drb_rb_version(void) { return "drb-b200 0.1.0 (sm_100a)"; }
+
+const char* drb_rb_last_error(void) { return t_last_error.c_str(); }
+
+drb_status drb_rng_init(drb_rng* s, uint64_t seed, uint32_t worker, uint32_t purpose) {
+    DRB_REQUIRE(s);
+    s->key = derive_key(seed, worker, purpose, 0, 0);
+    s->ctr = 0;
+    return DRB_OK;
+}
+
+drb_status drb_rng_keyed(drb_rng* s, uint64_t seed, uint32_t worker, uint32_t purpose,
+                         uint64_t k1, uint64_t k2) {
+    DRB_REQUIRE(s);
+    s->key = derive_key(seed, worker, purpose, k1 + 1, k2 + 1);
+    s->ctr = 0;
+    return DRB_OK;
+}
+
+drb_status drb_rng_draw(drb_rng* s, uint64_t bound, uint64_t n, uint64_t* out, int32_t device) {
+    DRB_REQUIRE(s && (out || n == 0));
+    return guarded([&] {
+        device_guard g(device);
+        dev_tmp d_out(n * 8), d_ctr(8);
+        if (launch_rng_draw(s->key, s->ctr, bound, n, d_out.as<uint64_t>(), d_ctr.as<uint64_t>(), nullptr))
+            fail(DRB_ERR_INTERNAL, "rng_draw launch failed");
+        cuda_check(cudaMemcpy(out, d_out.p, n * 8, cudaMemcpyDeviceToHost), "rng_draw copy");
+        cuda_check(cudaMemcpy(&s->ctr, d_ctr.p, 8, cudaMemcpyDeviceToHost), "rng_draw ctr");
+    });
+}
+
+drb_status drb_sample_without_replacement(uint32_t n, uint32_t k, drb_rng* s, uint32_t* out,
+                                          uint32_t* out_k, int32_t device) {
+    DRB_REQUIRE(s && out_k && (out || k == 0 || n == 0));
+    return guarded([&] {
+        device_guard g(device);
+        const uint32_t kk = k < n ? k : n;
+        dev_tmp d_out(size_t(kk) * 4), d_ctr(8);
+        if (launch_swor(s->key, s->ctr, n, kk, d_out.as<uint32_t>(), d_ctr.as<uint64_t>(), nullptr))
+            fail(DRB_ERR_INTERNAL, "swor launch failed");
+        cuda_check(cudaMemcpy(out, d_out.p, size_t(kk) * 4, cudaMemcpyDeviceToHost), "swor copy");
+        cuda_check(cudaMemcpy(&s->ctr, d_ctr.p, 8, cudaMemcpyDeviceToHost), "swor ctr");
+        *out_k = kk;
+    });
+}
+
+drb_status drb_plan(uint32_t want, uint32_t n_workers, uint32_t n_classes, const uint32_t* occ,
+                    drb_rng* s, drb_slot_ref* out, uint32_t* out_count, int32_t device) {
+    DRB_REQUIRE(occ && s && out_count);
+    return guarded([&] {
+        device_guard g(device);
+        const size_t nk = size_t(n_workers) * n_classes;
+        if (nk == 0)
+            fail(DRB_ERR_USAGE, "plan: empty view");
+        uint64_t total = 0;
+        for (size_t i = 0; i < nk; ++i)
+            total += occ[i];
+        if (total >= (1ull << 31))
+            fail(DRB_ERR_CONFIG, "plan: view larger than 2^31 slots");
+        const uint32_t entries = uint32_t(want < total ? want : total);
+        dev_tmp d_occ(nk * 4), d_out(size_t(entries) * 12), d_cnt(4), d_ctr(8);
+        cuda_check(cudaMemcpy(d_occ.p, occ, nk * 4, cudaMemcpyHostToDevice), "plan occ");
+        if (launch_plan(s->key, s->ctr, want, n_workers, n_classes, d_occ.as<uint32_t>(),
+                        d_out.as<uint32_t>(), d_cnt.as<uint32_t>(), d_ctr.as<uint64_t>(), nullptr))
+            fail(DRB_ERR_INTERNAL, "plan launch failed");
+        uint32_t c = 0;
+        cuda_check(cudaMemcpy(&c, d_cnt.p, 4, cudaMemcpyDeviceToHost), "plan count");
+        if (c && !out)
+            fail(DRB_ERR_INVALID_ARGUMENT, "plan: null output");
+        cuda_check(cudaMemcpy(out, d_out.p, size_t(c) * 12, cudaMemcpyDeviceToHost), "plan out");
+        cuda_check(cudaMemcpy(&s->ctr, d_ctr.p, 8, cudaMemcpyDeviceToHost), "plan ctr");
+        *out_count = c;
+    });
+}
+
+drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
+    DRB_REQUIRE(cfg && out);
+    *out = nullptr;
+    return guarded([&] {
+        const auto& c = *cfg;
+        if (c.n_classes == 0 || c.per_class_cap == 0)
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: class count and per-class capacity must be >= 1");
+        if (c.sample_bytes == 0 || c.sample_bytes % 4)
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: sample_bytes must be a positive multiple of 4");
+        if (c.world == 0 || c.world > kMaxWorld || c.rank >= c.world)
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: need 1 <= world <= 8 and rank < world");
+        if (c.max_batch == 0 || c.max_batch > 4096)
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: max_batch must be in [1, 4096]");
+        if (c.rep_count > 4096 || uint64_t(c.world) * c.rep_count > 4096)
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: world * rep_count must be <= 4096");
+        if (uint64_t(c.world) * c.n_classes * c.per_class_cap >= (1ull << 31))
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K*cap must be < 2^31 slots");
+        const SmemLayout sl = smem_layout(c.world, c.n_classes, c.max_batch, c.rep_count);
+        if (uint64_t(sl.words) * 4 > 200 * 1024)
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K too large for the on-chip view (" +
+                                     std::to_string(sl.words * 4) + " B shared memory)");
+        auto h = new drb_rb();
+        std::unique_ptr<drb_rb> guard_h(h);
+        h->cfg = c;
+        h->layout = region_layout(c.world, c.n_classes, c.sample_bytes, c.max_batch, c.rep_count);
+        h->smem_bytes = sl.words * 4;
+        if (const char* t = std::getenv("DRB_TIMEOUT_MS"))
+            h->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
+        device_guard g(c.device);
+        cuda_check(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, c.device), "sm count");
+        int per_sm = 0;
+        if (step_kernel_max_ctas_per_sm(h->smem_bytes, &per_sm) || per_sm < 1)
+            fail(DRB_ERR_CONFIG, "step kernel does not fit on an SM");
+        h->grid = uint32_t(h->sm_count) * uint32_t(per_sm < 2 ? per_sm : 2);
+        if (const char* gs = std::getenv("DRB_GRID"))
+            h->grid = uint32_t(std::strtoul(gs, nullptr, 10));
+        cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
+        const uint64_t slab_bytes = uint64_t(c.n_classes) * c.per_class_cap * c.sample_bytes;
+        cuda_check(cudaMalloc(&h->slab, slab_bytes), "slab alloc");
+        cuda_check(cudaMalloc(&h->slab_labels, uint64_t(c.n_classes) * c.per_class_cap * 4), "labels alloc");
+        cuda_check(cudaMemset(h->slab_labels, 0, uint64_t(c.n_classes) * c.per_class_cap * 4), "memset");
+        cuda_check(cudaMalloc(&h->region, h->layout.bytes), "region alloc");
+        cuda_check(cudaMemset(h->region, 0, h->layout.bytes), "memset");
+        cuda_check(cudaMalloc(&h->state, 2 * sizeof(DevState)), "state alloc");
+        cuda_check(cudaMemset(h->state, 0, 2 * sizeof(DevState)), "memset");
+        cuda_check(cudaMalloc(&h->report, (2ull * c.n_classes + 2) * 4), "report alloc");
+        cuda_check(cudaHostAlloc(&h->mailbox, 4 * kAugRing * 4, cudaHostAllocMapped), "mailbox");
+        std::memset(h->mailbox, 0, 4 * kAugRing * 4);
+        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->mailbox_dev), h->mailbox, 0), "mailbox map");
+        for (auto& e : h->done)
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaEventCreateWithFlags(&h->in_free[i], cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&h->h2d_done[i], cudaEventDisableTiming), "event");
+        }
+        h->cand_key = derive_key(c.seed, c.rank, DRB_PURPOSE_CANDIDATE_SELECTION, 0, 0);
+        h->evict_key = derive_key(c.seed, c.rank, DRB_PURPOSE_EVICTION, 0, 0);
+        for (uint32_t q = 0; q < kMaxWorld; ++q)
+            h->samp_key[q] = derive_key(c.seed, q, DRB_PURPOSE_GLOBAL_SAMPLING, 0, 0);
+        h->peers[c.rank] = h->region;
+        if (c.world == 1)
+            h->connected = true;
+        cuda_check(cudaDeviceSynchronize(), "create sync");
+        *out = guard_h.release();
+    });
+}
+
+drb_status drb_rb_destroy(drb_rb* h) {
+    if (!h)
+        return DRB_OK;
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        cudaDeviceSynchronize();
+        for (uint32_t w = 0; w < h->cfg.world; ++w)
+            if (h->peer_opened[w])
+                cudaIpcCloseMemHandle(h->peers[w]);
+        cudaFree(h->slab);
+        cudaFree(h->slab_labels);
+        cudaFree(h->region);
+        cudaFree(h->state);
+        cudaFree(h->report);
+        cudaFree(h->stage);
+        cudaFree(h->stage_labels);
+        cudaFreeHost(h->mailbox);
+        for (auto e : h->done)
+            cudaEventDestroy(e);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(h->in_free[i]);
+            cudaEventDestroy(h->h2d_done[i]);
+        }
+        cudaStreamDestroy(h->stream);
+        cudaStreamDestroy(h->h2d);
+        cudaStreamDestroy(h->d2h);
+        delete h;
+    });
+}
+
+drb_status drb_rb_update_buffer(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n,
+                                uint32_t c, drb_rng* cand, drb_rng* evict,
+                                drb_insertion_report* report) {
+    DRB_REQUIRE(h && cand && evict && ((batch && labels) || n == 0));
+    return guarded([&] {
+        if (h->started && h->cfg.world > 1)
+            fail(DRB_ERR_USAGE, "update_buffer: not allowed while a multi-rank engine is running");
+        if (n > h->cfg.max_batch)
+            fail(DRB_ERR_USAGE, "update_buffer: batch larger than max_batch");
+        device_guard g(h->cfg.device);
+        StepParams p = base_params(h);
+        p.n = n;
+        p.c = c;
+        p.batch = static_cast<const uint8_t*>(batch);
+        p.labels = labels;
+        p.cand_key = cand->key;
+        p.evict_key = evict->key;
+        p.cand_ctr0 = cand->ctr;
+        p.evict_ctr0 = evict->ctr;
+        p.mode = kModeUpdate | kModeReport | kModeCtrParams | kModePublish;
+        p.tslot_in = uint32_t(h->ver % kTableRing);
+        p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
+        p.st_in = h->state + h->cur;
+        p.st_out = h->state + (h->cur ^ 1);
+        p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
+        p.mailbox = nullptr;
+        if (launch_step(p, h->grid, h->stream))
+            fail(DRB_ERR_INTERNAL, std::string("step launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        DevState st{};
+        cuda_check(cudaMemcpyAsync(&st, p.st_out, sizeof st, cudaMemcpyDeviceToHost, h->stream), "state copy");
+        std::vector<uint32_t> rep(2ull * h->cfg.n_classes + 2);
+        cuda_check(cudaMemcpyAsync(rep.data(), h->report, rep.size() * 4, cudaMemcpyDeviceToHost, h->stream), "report copy");
+        cuda_check(cudaStreamSynchronize(h->stream), "update_buffer");
+        if (st.error == DRB_ERR_USAGE) {
+            // usage_error is raised before any draw and leaves the buffer untouched
+            // (rehearsal_buffer.cpp:44-47): discard the produced state.
+            fail(DRB_ERR_USAGE, "update_buffer: label out of range (K=" + std::to_string(h->cfg.n_classes) + ")");
+        }
+        h->cur ^= 1;
+        h->ver += 1;
+        cand->ctr = st.cand_ctr;
+        evict->ctr = st.evict_ctr;
+        if (report) {
+            const uint32_t K = h->cfg.n_classes;
+            if (report->per_class_appends)
+                std::memcpy(report->per_class_appends, rep.data(), K * 4);
+            if (report->per_class_replacements)
+                std::memcpy(report->per_class_replacements, rep.data() + K, K * 4);
+            report->appends = rep[2 * K];
+            report->replacements = rep[2 * K + 1];
+        }
+    });
+}
+
+drb_status drb_rb_read_slots(drb_rb* h, const drb_read_request* requests, uint32_t count,
+                             drb_rng* substitute, void* out, uint32_t* out_labels, uint8_t* status) {
+    DRB_REQUIRE(h && substitute && ((requests && out && out_labels && status) || count == 0));
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        dev_tmp d_req(size_t(count) * 8), d_status(count), d_ctr(8);
+        cuda_check(cudaMemcpy(d_req.p, requests, size_t(count) * 8, cudaMemcpyHostToDevice), "req copy");
+        const uint32_t* occ = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_table) +
+                              (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
+                              uint64_t(h->cfg.rank) * h->cfg.n_classes;
+        cuda_check(cudaStreamSynchronize(h->stream), "read_slots order");
+        if (launch_read_slots(h->slab, h->slab_labels, occ, h->cfg.n_classes, h->cfg.per_class_cap,
+                              h->cfg.sample_bytes, d_req.as<uint32_t>(), count, substitute->key,
+                              substitute->ctr, static_cast<uint8_t*>(out), out_labels,
+                              d_status.as<uint8_t>(), d_ctr.as<uint64_t>(), h->stream))
+            fail(DRB_ERR_INTERNAL, "read_slots launch failed");
+        cuda_check(cudaStreamSynchronize(h->stream), "read_slots");
+        cuda_check(cudaMemcpy(status, d_status.p, count, cudaMemcpyDeviceToHost), "status copy");
+        cuda_check(cudaMemcpy(&substitute->ctr, d_ctr.p, 8, cudaMemcpyDeviceToHost), "ctr copy");
+    });
+}
+
+drb_status drb_rb_snapshot(drb_rb* h, uint32_t* per_class, uint64_t* version) {
+    DRB_REQUIRE(h && per_class && version);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        cuda_check(cudaStreamSynchronize(h->stream), "snapshot order");
+        const uint32_t* occ = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_table) +
+                              (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
+                              uint64_t(h->cfg.rank) * h->cfg.n_classes;
+        cuda_check(cudaMemcpy(per_class, occ, h->cfg.n_classes * 4ull, cudaMemcpyDeviceToHost), "snapshot");
+        DevState st{};
+        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        *version = st.version;
+    });
+}
+
+drb_status drb_rb_total_stored(drb_rb* h, uint64_t* out) {
+    DRB_REQUIRE(h && out);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        cuda_check(cudaStreamSynchronize(h->stream), "order");
+        DevState st{};
+        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        *out = st.total;
+    });
+}
+
+drb_status drb_rb_cross_class_evictions(drb_rb* h, uint64_t* out) {
+    DRB_REQUIRE(h && out);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        cuda_check(cudaStreamSynchronize(h->stream), "order");
+        DevState st{};
+        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        *out = st.cross_class;
+    });
+}
+
+drb_status drb_rb_device_views(drb_rb* h, void** slab, uint32_t** slab_labels) {
+    DRB_REQUIRE(h && slab && slab_labels);
+    *slab = h->slab;
+    *slab_labels = h->slab_labels;
+    return DRB_OK;
+}
+
+size_t drb_rb_handle_size(void) { return sizeof(handle_blob); }
+
+drb_status drb_rb_export_handle(drb_rb* h, void* blob, size_t* len) {
+    DRB_REQUIRE(h && blob && len);
+    if (*len < sizeof(handle_blob)) {
+        t_last_error = "export_handle: blob buffer too small";
+        *len = sizeof(handle_blob);
+        return DRB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        handle_blob b{};
+        b.magic = kBlobMagic;
+        b.version = 1;
+        b.pid = int32_t(getpid());
+        b.device = h->cfg.device;
+        b.rank = h->cfg.rank;
+        b.world = h->cfg.world;
+        b.region_bytes = h->layout.bytes;
+        b.region_ptr = reinterpret_cast<uint64_t>(h->region);
+        cuda_check(cudaIpcGetMemHandle(&b.ipc, h->region), "cudaIpcGetMemHandle");
+        std::memcpy(blob, &b, sizeof b);
+        *len = sizeof b;
+    });
+}
+
+drb_status drb_rb_connect(drb_rb* h, const void* blobs, size_t blob_len) {
+    DRB_REQUIRE(h && blobs);
+    return guarded([&] {
+        const auto& c = h->cfg;
+        if (blob_len < sizeof(handle_blob) * c.world)
+            fail(DRB_ERR_INVALID_ARGUMENT, "connect: need world blobs");
+        if (h->started)
+            fail(DRB_ERR_USAGE, "connect: engine already started");
+        device_guard g(c.device);
+        const auto* all = static_cast<const handle_blob*>(blobs);
+        for (uint32_t w = 0; w < c.world; ++w) {
+            const handle_blob& b = all[w];
+            if (b.magic != kBlobMagic || b.rank != w || b.world != c.world ||
+                b.region_bytes != h->layout.bytes)
+                fail(DRB_ERR_CONFIG, "connect: blob " + std::to_string(w) + " does not match this configuration");
+            if (w == c.rank)
+                continue;
+            if (b.pid == int32_t(getpid())) {
+                if (b.device != c.device) {
+                    int can = 0;
+                    cuda_check(cudaDeviceCanAccessPeer(&can, c.device, b.device), "peer query");
+                    if (!can)
+                        fail(DRB_ERR_TRANSPORT, "connect: no peer access between devices");
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                        cuda_check(e, "cudaDeviceEnablePeerAccess");
+                    cudaGetLastError();
+                }
+                h->peers[w] = reinterpret_cast<uint8_t*>(b.region_ptr);
+            } else {
+                void* p = nullptr;
+                cuda_check(cudaIpcOpenMemHandle(&p, b.ipc, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+                h->peers[w] = static_cast<uint8_t*>(p);
+                h->peer_opened[w] = true;
+            }
+        }
+        h->connected = true;
+    });
+}
+
+drb_status drb_rb_start(drb_rb* h) {
+    DRB_REQUIRE(h);
+    return guarded([&] {
+        if (h->started)
+            fail(DRB_ERR_USAGE, "engine: already started");
+        if (!h->connected)
+            fail(DRB_ERR_USAGE, "engine: multi-rank handle not connected");
+        h->started = true;
+    });
+}
+
+drb_status drb_rb_shutdown(drb_rb* h) {
+    DRB_REQUIRE(h);
+    return guarded([&] {
+        if (!h->started)
+            fail(DRB_ERR_USAGE, "engine: shutdown before start");
+        if (h->shut_down)
+            fail(DRB_ERR_USAGE, "engine: double shutdown");
+        h->shut_down = true;
+        device_guard g(h->cfg.device);
+        cuda_check(cudaDeviceSynchronize(), "shutdown drain");
+    });
+}
+
+drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n,
+                       void* stream, drb_aug* out) {
+    DRB_REQUIRE(h && out && ((batch && labels) || n == 0));
+    return guarded([&] {
+        if (h->shut_down)
+            fail(DRB_ERR_USAGE, "engine: update after shutdown");
+        if (!h->started)
+            fail(DRB_ERR_USAGE, "engine: update before start");
+        if (n > h->cfg.max_batch)
+            fail(DRB_ERR_USAGE, "engine: batch larger than max_batch");
+        check_engine_alive(h);
+        device_guard g(h->cfg.device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        StepParams p = base_params(h);
+        p.n = n;
+        p.batch = static_cast<const uint8_t*>(batch);
+        p.labels = labels;
+        p.step = h->step;
+        p.mode = kModeUpdate | kModeAssemble | kModePlan | kModePublish |
+                 (h->cfg.world > 1 ? kModePeers : 0u);
+        p.tslot_in = uint32_t(h->ver % kTableRing);
+        p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
+        p.aslot = uint32_t(h->step % kAugRing);
+        p.st_in = h->state + h->cur;
+        p.st_out = h->state + (h->cur ^ 1);
+        p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
+        if (launch_step(p, h->grid, s))
+            fail(DRB_ERR_INTERNAL, std::string("step launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
+        h->cur ^= 1;
+        h->ver += 1;
+        out->n = n;
+        out->ring_slot = p.aslot;
+        out->step = h->step;
+        const uint32_t row0 = h->cfg.max_batch - n;
+        out->data = h->region + h->layout.off_aug + uint64_t(p.aslot) * h->layout.aug_slot_bytes +
+                    uint64_t(row0) * h->cfg.sample_bytes;
+        out->labels = reinterpret_cast<uint32_t*>(h->region + h->layout.off_auglab) +
+                      uint64_t(p.aslot) * p.auglab_slot_elems + row0;
+        h->step += 1;
+    });
+}
+
+drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, const uint32_t* labels,
+                      uint64_t label_stride, uint32_t ring, uint32_t n, uint64_t steps, uint64_t first,
+                      void* stream, void* const* step_events) {
+    DRB_REQUIRE(h && batches && labels && ring > 0);
+    return guarded([&] {
+        const auto* b = static_cast<const uint8_t*>(batches);
+        drb_aug aug{};
+        for (uint64_t i = 0; i < steps; ++i) {
+            const uint64_t j = (first + i) % ring;
+            if (step_events)
+                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * i]),
+                                           stream ? static_cast<cudaStream_t>(stream) : h->stream), "event");
+            const drb_status st = drb_rb_step(h, b + j * batch_stride, labels + j * label_stride, n, stream, &aug);
+            if (st != DRB_OK)
+                fail(st, t_last_error);
+            if (step_events)
+                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * i + 1]),
+                                           stream ? static_cast<cudaStream_t>(stream) : h->stream), "event");
+        }
+    });
+}
+
+drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n,
+                            void* out, uint32_t* out_labels, uint32_t* out_count) {
+    DRB_REQUIRE(h && out && out_labels && out_count && ((batch && labels) || n == 0));
+    return guarded([&] {
+        if (n > h->cfg.max_batch)
+            fail(DRB_ERR_USAGE, "engine: batch larger than max_batch");
+        device_guard g(h->cfg.device);
+        const auto& c = h->cfg;
+        if (!h->stage) {
+            cuda_check(cudaMalloc(&h->stage, 2ull * c.max_batch * c.sample_bytes), "stage alloc");
+            cuda_check(cudaMalloc(&h->stage_labels, 2ull * c.max_batch * 4), "stage alloc");
+        }
+        // Input copy on its own stream into a 2-deep staging ring so the copy of m_{i+1}
+        // overlaps step i; the output copy of m'_i runs on a third stream (PCIe is duplex).
+        const uint32_t si = uint32_t(h->step & 1);
+        uint8_t* st_b = h->stage + uint64_t(si) * c.max_batch * c.sample_bytes;
+        uint32_t* st_l = h->stage_labels + uint64_t(si) * c.max_batch;
+        cuda_check(cudaStreamWaitEvent(h->h2d, h->in_free[si], 0), "wait");
+        cuda_check(cudaMemcpyAsync(st_b, batch, uint64_t(n) * c.sample_bytes, cudaMemcpyHostToDevice, h->h2d), "h2d");
+        cuda_check(cudaMemcpyAsync(st_l, labels, uint64_t(n) * 4, cudaMemcpyHostToDevice, h->h2d), "h2d");
+        cuda_check(cudaEventRecord(h->h2d_done[si], h->h2d), "event");
+        cuda_check(cudaStreamWaitEvent(h->stream, h->h2d_done[si], 0), "wait");
+        drb_aug aug{};
+        const drb_status st = drb_rb_step(h, st_b, st_l, n, h->stream, &aug);
+        if (st != DRB_OK)
+            fail(st, t_last_error);
+        cuda_check(cudaEventRecord(h->in_free[si], h->stream), "event");
+        cuda_check(cudaStreamWaitEvent(h->d2h, h->done[aug.ring_slot], 0), "wait");
+        const uint64_t rows = uint64_t(n) + c.rep_count;
+        cuda_check(cudaMemcpyAsync(out, aug.data, rows * c.sample_bytes, cudaMemcpyDeviceToHost, h->d2h), "d2h");
+        cuda_check(cudaMemcpyAsync(out_labels, aug.labels, rows * 4, cudaMemcpyDeviceToHost, h->d2h), "d2h");
+        const auto* hdr = reinterpret_cast<const RegionHeader*>(h->region);
+        cuda_check(cudaMemcpyAsync(out_count, &hdr->aug_count[aug.ring_slot], 4, cudaMemcpyDeviceToHost, h->d2h), "d2h");
+        // The next step may reuse this m' slot only after the copy-out drained.
+        cuda_check(cudaEventRecord(h->done[aug.ring_slot], h->d2h), "event");
+        cuda_check(cudaStreamWaitEvent(h->stream, h->done[aug.ring_slot], 0), "wait");
+    });
+}
+
+drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count) {
+    DRB_REQUIRE(h && aug && count);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        const auto t0 = std::chrono::steady_clock::now();
+        cuda_check(cudaEventSynchronize(h->done[aug->ring_slot]), "aug wait");
+        h->wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const volatile uint32_t* mb = h->mailbox;
+        const uint32_t e = mb[kAugRing + aug->ring_slot];
+        *count = mb[aug->ring_slot];
+        if (e)
+            fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(e));
+    });
+}
+
+drb_status drb_rb_synchronize(drb_rb* h) {
+    DRB_REQUIRE(h);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        cuda_check(cudaStreamSynchronize(h->h2d), "sync");
+        cuda_check(cudaStreamSynchronize(h->d2h), "sync");
+        for (auto e : h->done)
+            cuda_check(cudaEventSynchronize(e), "sync");
+    });
+}
+
+drb_status drb_rb_total_wait_ms(drb_rb* h, double* out) {
+    DRB_REQUIRE(h && out);
+    *out = h->wait_ms;
+    return DRB_OK;
+}
+
+drb_status drb_rb_device_error(drb_rb* h, uint32_t* out) {
+    DRB_REQUIRE(h && out);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        DevState st{};
+        cuda_check(cudaStreamSynchronize(h->stream), "order");
+        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        *out = st.error;
+    });
+}
+
+drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads, uint32_t* smem) {
+    DRB_REQUIRE(h && grid && threads && smem);
+    *grid = h->grid;
+    *threads = kThreads;
+    *smem = h->smem_bytes;
+    return DRB_OK;
+}
+
+}  // extern "C"

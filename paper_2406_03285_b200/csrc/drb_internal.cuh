@@ -1,0 +1,160 @@
+// Internal layout shared by the sm_100a kernels (drb_kernels.cu) and the C-ABI host code
+// (drb_capi.cu). Not installed; the public boundary is include/drb_rb.h.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/drb_rb.h"
+
+namespace drb_b200 {
+
+constexpr int kMaxWorld = DRB_RB_MAX_WORLD;
+constexpr int kTableRing = 3;  // occupancy-row versions kept per rank (v % 3); see DESIGN.md §4
+constexpr int kAugRing = 3;    // m' buffers per rank; m'_i valid until step i+2 is enqueued
+constexpr int kThreads = 512;  // step kernel CTA size (16 warps)
+constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
+
+// Mode bits of one step-kernel launch.
+enum : uint32_t {
+    kModeUpdate = 1u << 0,    // S1+S2: insert candidates of m_i
+    kModeAssemble = 1u << 1,  // copy m_i into m'_i rows [0,n)
+    kModePlan = 1u << 2,      // S4+S5: plan(i-1) for every requester, push owned entries
+    kModeReport = 1u << 3,    // write the per-class insertion report
+    kModeCtrParams = 1u << 4, // take cand/evict counters from the params (update_buffer API)
+    kModePublish = 1u << 5,   // write own occupancy row for version i+1
+    kModePeers = 1u << 6,     // multi-rank: publish to / wait for / push into peers
+};
+
+// Device-resident engine state, ping-ponged between consecutive launches.
+struct alignas(16) DevState {
+    uint64_t cand_ctr;
+    uint64_t evict_ctr;
+    uint64_t version;      // mutations applied (rehearsal_buffer.cpp:79)
+    uint64_t total;        // samples stored (m_total)
+    uint64_t cross_class;  // invariant counter, structurally 0 (rehearsal_buffer.hpp:91-95)
+    uint32_t error;        // sticky: DRB_ERR_* of a failed round
+    uint32_t pad;
+    uint64_t samp_ctr[kMaxWorld];  // every requester's global-sampling counter (replicated)
+};
+
+// Peer-shareable region header (one cudaMalloc per rank, exported over CUDA IPC).
+struct alignas(256) RegionHeader {
+    uint64_t occ_flag[kMaxWorld];  // [w]: latest occupancy version rank w published here
+    uint64_t arrive[kMaxWorld];    // [w]: 1 + last step whose pushes from w into me completed
+    uint64_t ticket;               // local: CTA completion tickets (last-CTA detection)
+    uint32_t aug_count[4];         // local: rows of m' per ring slot (device copy)
+    uint64_t pad[13];
+};
+
+struct RegionLayout {
+    uint64_t off_table;     // u32 [kTableRing][N][K]
+    uint64_t off_aug;       // u8  [kAugRing][rows][S]
+    uint64_t off_auglab;    // u32 [kAugRing][rows]
+    uint64_t aug_slot_bytes;
+    uint64_t rows;          // max_batch + r
+    uint64_t bytes;
+};
+
+__host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+inline RegionLayout region_layout(uint32_t N, uint32_t K, uint64_t S, uint32_t max_batch,
+                                  uint32_t r) {
+    RegionLayout L{};
+    uint64_t off = sizeof(RegionHeader);
+    L.off_table = off = align_up(off, 256);
+    off += uint64_t(kTableRing) * N * K * 4;
+    L.rows = uint64_t(max_batch) + r;
+    L.aug_slot_bytes = align_up(L.rows * S, 256);
+    L.off_aug = off = align_up(off, 256);
+    off += kAugRing * L.aug_slot_bytes;
+    L.off_auglab = off = align_up(off, 256);
+    off += uint64_t(kAugRing) * align_up(L.rows * 4, 256);
+    L.bytes = align_up(off, 4096);
+    return L;
+}
+
+struct StepParams {
+    uint32_t K, cap, N, me;
+    uint32_t n, c, r, nmax;
+    uint64_t S;
+    uint64_t step;
+    uint32_t tslot_in, tslot_out;  // table ring slots of versions i and i+1
+    uint32_t aslot;                // m' ring slot of step i
+    uint32_t mode;
+    uint64_t cand_key, evict_key;
+    uint64_t cand_ctr0, evict_ctr0;  // used with kModeCtrParams
+    uint64_t samp_key[kMaxWorld];
+    const uint8_t* batch;
+    const uint32_t* labels;
+    uint8_t* slab;
+    uint32_t* slab_labels;
+    const DevState* st_in;
+    DevState* st_out;
+    uint8_t* region[kMaxWorld];  // every rank's region base, mapped in this process
+    uint64_t off_table, off_aug, off_auglab, aug_slot_bytes, auglab_slot_elems;
+    uint32_t* report;    // [2K + 2]: appends[K], replacements[K], totals[2]
+    uint32_t* mailbox;   // host-mapped: [kAugRing] counts, [kAugRing] errors
+    uint64_t timeout_ns;
+    uint32_t vec16;      // 16-byte vector path legal (S % 16 == 0, aligned bases)
+    uint32_t smem_bytes;
+};
+
+// Dynamic shared-memory carve-up of the step kernel (sizes in 4-byte words).
+struct SmemLayout {
+    uint32_t pre, occ, lab, sel, cand_l, cand_slot, win, idx, plan, cnt, acc, hkey, hfirst,
+        hjob, hmask, pj_src, pj_post, pj_ndst, pj_dst, misc, words;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(uint32_t N, uint32_t K, uint32_t nmax, uint32_t r) {
+    SmemLayout s{};
+    uint32_t w = 0;
+    const uint32_t nr = N * (r ? r : 1);
+#define TAKE(words) (w += ((words) + 3) & ~3u, w - (((words) + 3) & ~3u))
+    s.pre = TAKE(N * K + 1);
+    s.occ = TAKE(K);
+    s.lab = TAKE(nmax);
+    s.sel = TAKE(nmax);
+    s.cand_l = TAKE(nmax);
+    s.cand_slot = TAKE(nmax);
+    s.win = TAKE(2 * nmax);
+    s.idx = TAKE(nmax);
+    s.plan = TAKE(3 * nr);
+    s.cnt = TAKE(N);
+    s.acc = TAKE(nr);
+    uint32_t h = 32;
+    while (h < 2 * nr)
+        h <<= 1;
+    s.hmask = h - 1;
+    s.hkey = TAKE(h);
+    s.hfirst = TAKE(h);
+    s.hjob = TAKE(h);
+    s.pj_src = TAKE(nr);
+    s.pj_post = TAKE(nr);
+    s.pj_ndst = TAKE(nr);
+    s.pj_dst = TAKE(nr * N);
+    s.misc = TAKE(32);
+    s.words = w;
+#undef TAKE
+    return s;
+}
+
+// Launchers (drb_kernels.cu), C++ linkage, used by drb_capi.cu only.
+int launch_step(const StepParams& p, uint32_t grid, void* stream);
+int step_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out);
+int launch_rng_draw(uint64_t key, uint64_t ctr, uint64_t bound, uint64_t n, uint64_t* out_dev,
+                    uint64_t* ctr_out_dev, void* stream);
+int launch_swor(uint64_t key, uint64_t ctr, uint32_t n, uint32_t k, uint32_t* out_dev,
+                uint64_t* ctr_out_dev, void* stream);
+int launch_plan(uint64_t key, uint64_t ctr, uint32_t want, uint32_t n_workers, uint32_t n_classes,
+                const uint32_t* occ_dev, uint32_t* out_dev, uint32_t* count_dev,
+                uint64_t* ctr_out_dev, void* stream);
+int launch_read_slots(const uint8_t* slab, const uint32_t* slab_labels, const uint32_t* occ_dev,
+                      uint32_t K, uint32_t cap, uint64_t S, const uint32_t* req_dev,
+                      uint32_t count, uint64_t key, uint64_t ctr, uint8_t* out,
+                      uint32_t* out_labels, uint8_t* status_dev, uint64_t* ctr_out_dev,
+                      void* stream);
+
+}  // namespace drb_b200
