@@ -268,6 +268,9 @@ def main():
     # per-launch device time of the (single) step kernel: events bracketing each launch
     nper = 256
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nper)]
+    for e in evs:  # torch creates the CUDA event lazily on first record
+        e.record(stream)
+    stream.synchronize()
     barrier()
     eng.run(data, lab, nper, first=0, stream=stream, events=evs)
     torch.cuda.synchronize()

@@ -218,6 +218,9 @@ DRB_RB_API drb_status drb_rb_synchronize(drb_rb* h);
 DRB_RB_API drb_status drb_rb_total_wait_ms(drb_rb* h, double* out);
 /* Device-side error word of the last completed step (0 = none). */
 DRB_RB_API drb_status drb_rb_device_error(drb_rb* h, uint32_t* out);
+/* Diagnostics (DRB_TRACE=1 at create): globaltimer stamps of the last step's phases in
+ * CTA 0 (slots 0-9) and the grid-wide first start / last end (slots 14, 15). */
+DRB_RB_API drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out16);
 /* Launch configuration of the step kernel: grid CTAs, threads, dynamic smem. */
 DRB_RB_API drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads,
                                          uint32_t* smem);

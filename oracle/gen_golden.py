@@ -1,0 +1,123 @@
+#!/usr/bin/env python3
+"""TEST INFRASTRUCTURE: regenerate tests/golden/*.json from the REFERENCE itself
+(oracle/_ref/libdrb_ref.so = the unmodified /root/reference sources + ref_capi.cpp).
+
+Run here (the reference is not on the GPU box):  python oracle/gen_golden.py
+Outputs:
+  tests/golden/kat.json     KAT1-KAT6 + extra rng/swor/plan vectors
+  tests/golden/replay.json  per-step sha256 of every rank's m'_i (bytes ++ labels ++ count)
+                            under the synchronous replay, for small configs at N = 1, 2, 4, 8
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle.py_oracle import Backend, CANDIDATE, EVICTION, GLOBAL_SAMPLING  # noqa: E402
+from paper_2406_03285_b200.workload import stream_spec  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+# (name, N, K, cap, S, b, c, r, seed, T, steps_per_task, steps, short-batch pattern or None)
+REPLAY_CONFIGS = [
+    ("c1_like_n1", 1, 10, 100, 256, 64, 14, 8, 1, 1, 10**9, 220, None),
+    ("engine_cfg_n2", 2, 4, 16, 12, 8, 4, 7, 77, 1, 10**9, 80, None),
+    ("ci_n2", 2, 20, 6, 64, 56, 14, 7, 3, 4, 15, 120, None),
+    ("ci_n4", 4, 12, 5, 32, 24, 14, 7, 5, 3, 10, 100, None),
+    ("ci_n8", 8, 16, 4, 16, 16, 6, 9, 9, 2, 12, 90, None),
+    ("short_n2", 2, 6, 3, 16, 12, 5, 6, 11, 1, 10**9, 60, [12, 3, 0, 12, 1]),
+    ("exhaust_n4", 4, 3, 2, 8, 4, 4, 40, 13, 1, 10**9, 30, None),
+    ("big_r_n2", 2, 8, 8, 16, 40, 33, 33, 17, 2, 20, 60, None),
+]
+
+
+def digest(aug: np.ndarray, lab: np.ndarray, count: int) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(aug[:count]).tobytes())
+    h.update(np.ascontiguousarray(lab[:count].astype(np.uint32)).tobytes())
+    h.update(np.uint32(count).tobytes())
+    return h.hexdigest()
+
+
+def replay_digests(be: Backend, cfg):
+    name, N, K, cap, S, b, c, r, seed, T, spt, steps, pattern = cfg
+    spec = stream_spec(K, T, b, S, steps_per_task=spt, seed=seed)
+    rp = be.replay(N, K, cap, S, c, r, seed)
+    out = []
+    for i in range(steps):
+        n = pattern[i % len(pattern)] if pattern else b
+        data = np.stack([spec.payload(w, i, n) for w in range(N)])
+        labs = np.stack([spec.labels(w, i, n) for w in range(N)])
+        aug, al, cnt = rp.step(data, labs)
+        out.append([digest(aug[w], al[w], int(cnt[w])) for w in range(N)])
+    return out
+
+
+def kat(be: Backend):
+    k = {}
+    k["kat1_next_u64_seed1_w0_candidate"] = [hex(int(x)) for x in be.rng_next(1, 0, CANDIDATE, 4)]
+    k["kat2_bounded100_seed1_w0_eviction"] = be.rng_bounded(1, 0, EVICTION, 100, 8).tolist()
+    k["kat3_swor_64_14"] = be.swor(64, 14, 1).tolist()
+    k["kat4_keyed_7e"] = [hex(int(x)) for x in be.rng_next(1, 0, GLOBAL_SAMPLING, 2, keyed=True, k1=0x7E)]
+    k["kat5_plan"] = be.plan(8, np.array([[4, 0, 6], [10, 3, 0]]), 1).tolist()
+    # extra vectors: rejection-heavy bounds, many (n,k), plans with carried counters
+    k["bounded_big"] = {str(bd): [str(int(x)) for x in be.rng_bounded(3, 1, GLOBAL_SAMPLING, bd, 64)]
+                        for bd in (2**63 + 1, 2**64 - 3, 3 * 2**62)}
+    rng = np.random.default_rng(0)
+    sw = []
+    for _ in range(40):
+        n, kk, seed = int(rng.integers(1, 300)), int(rng.integers(0, 50)), int(rng.integers(0, 2**31))
+        sw.append({"n": n, "k": kk, "seed": seed, "out": be.swor(n, kk, seed).tolist()})
+    k["swor_random"] = sw
+    pl = []
+    for _ in range(30):
+        nw, nk = int(rng.integers(1, 9)), int(rng.integers(1, 30))
+        occ = rng.integers(0, 6, (nw, nk)).astype(np.uint32)
+        want, seed = int(rng.choice([1, 7, 8, 28, 33, 64])), int(rng.integers(0, 2**31))
+        rounds = be.plan(want, occ, seed, 0, GLOBAL_SAMPLING, rounds=3)
+        pl.append({"occ": occ.tolist(), "want": want, "seed": seed, "rounds": [x.tolist() for x in rounds]})
+    k["plan_random"] = pl
+    # KAT6: config-1 single rank, label (64i+j)%10, features[0] = 64i+j (float32)
+    K, cap, b, c, r, S = 10, 100, 64, 14, 8, 16
+    rp = be.replay(1, K, cap, S, c, r, 1)
+    plans, f0 = [], []
+    for i in range(200):
+        feats = np.zeros((b, S // 4), np.float32)
+        feats[:, 0] = 64 * i + np.arange(b)
+        lab = ((64 * i + np.arange(b)) % 10).astype(np.uint32)
+        aug, al, cnt = rp.step(feats.view(np.uint8).reshape(1, b, S), lab[None])
+        plans.append(rp.last_plan(0)[:, 1:].tolist())
+        if i > 0:
+            f0.append(aug[0, b:cnt[0], :4].copy().view(np.float32)[:, 0].astype(int).tolist())
+    feats = np.zeros((b, S // 4), np.float32)
+    aug, al, cnt = rp.step(feats.view(np.uint8).reshape(1, b, S), np.zeros((1, b), np.uint32))
+    f0.append(aug[0, b:cnt[0], :4].copy().view(np.float32)[:, 0].astype(int).tolist())
+    k["kat6_plans_cls_slot"] = plans
+    k["kat6_reps_f0"] = f0  # f0[i] = reps of round i (delivered in m'_{i+1})
+    return k
+
+
+def main():
+    be = Backend("reference")
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "kat.json"), "w") as f:
+        json.dump(kat(be), f)
+    rep = {}
+    for cfg in REPLAY_CONFIGS:
+        rep[cfg[0]] = {"config": dict(zip(["name", "N", "K", "cap", "S", "b", "c", "r", "seed", "T",
+                                           "steps_per_task", "steps", "pattern"], cfg)),
+                       "digests": replay_digests(be, cfg)}
+    with open(os.path.join(OUT, "replay.json"), "w") as f:
+        json.dump(rep, f)
+    print("wrote", os.listdir(OUT))
+
+
+if __name__ == "__main__":
+    main()

@@ -137,6 +137,7 @@ def _load():
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),
+        "drb_rb_trace_read": (st, [vp, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)

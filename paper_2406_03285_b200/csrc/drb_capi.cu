@@ -149,6 +149,7 @@ struct drb_rb {
     uint64_t step = 0;
     bool started = false, shut_down = false;
     double wait_ms = 0.0;
+    unsigned long long* trace = nullptr;  // DRB_TRACE=1: per-step phase timestamps
     uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
 };
 
@@ -194,6 +195,7 @@ StepParams base_params(drb_rb* h) {
     p.mailbox = h->mailbox_dev;
     p.timeout_ns = h->timeout_ns;
     p.smem_bytes = h->smem_bytes;
+    p.trace = h->trace;
     return p;
 }
 
@@ -340,6 +342,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         for (uint32_t q = 0; q < kMaxWorld; ++q)
             h->samp_key[q] = derive_key(c.seed, q, DRB_PURPOSE_GLOBAL_SAMPLING, 0, 0);
         h->peers[c.rank] = h->region;
+        if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
+            cuda_check(cudaMalloc(&h->trace, 16 * 8), "trace alloc");
         if (c.world == 1)
             h->connected = true;
         cuda_check(cudaDeviceSynchronize(), "create sync");
@@ -361,6 +365,7 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaFree(h->region);
         cudaFree(h->state);
         cudaFree(h->report);
+        cudaFree(h->trace);
         cudaFree(h->stage);
         cudaFree(h->stage_labels);
         cudaFreeHost(h->mailbox);
@@ -613,6 +618,10 @@ drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uin
         p.st_in = h->state + h->cur;
         p.st_out = h->state + (h->cur ^ 1);
         p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
+        if (h->trace) {
+            cuda_check(cudaMemsetAsync(h->trace, 0, 16 * 8, s), "trace reset");
+            cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
+        }
         if (launch_step(p, h->grid, s))
             fail(DRB_ERR_INTERNAL, std::string("step launch failed: ") + cudaGetErrorString(cudaGetLastError()));
         cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
@@ -732,6 +741,17 @@ drb_status drb_rb_device_error(drb_rb* h, uint32_t* out) {
         cuda_check(cudaStreamSynchronize(h->stream), "order");
         cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
         *out = st.error;
+    });
+}
+
+drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out16) {
+    DRB_REQUIRE(h && out16);
+    return guarded([&] {
+        if (!h->trace)
+            fail(DRB_ERR_USAGE, "trace_read: run with DRB_TRACE=1");
+        device_guard g(h->cfg.device);
+        cuda_check(cudaDeviceSynchronize(), "trace sync");
+        cuda_check(cudaMemcpy(out16, h->trace, 16 * 8, cudaMemcpyDeviceToHost), "trace copy");
     });
 }
 

@@ -100,12 +100,13 @@ struct StepParams {
     uint64_t timeout_ns;
     uint32_t vec16;      // 16-byte vector path legal (S % 16 == 0, aligned bases)
     uint32_t smem_bytes;
+    unsigned long long* trace;  // optional phase timestamps (CTA 0) + grid min/max, 16 slots
 };
 
 // Dynamic shared-memory carve-up of the step kernel (sizes in 4-byte words).
 struct SmemLayout {
-    uint32_t pre, occ, lab, sel, cand_l, cand_slot, win, idx, plan, cnt, acc, hkey, hfirst,
-        hjob, hmask, pj_src, pj_post, pj_ndst, pj_dst, misc, words;
+    uint32_t pre, pfx, occ, lab, sel, cand_l, cand_slot, win, idx, plan, cnt, acc, pj_src,
+        pj_post, pj_ndst, pj_dst, maskw, misc, words;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(uint32_t N, uint32_t K, uint32_t nmax, uint32_t r) {
@@ -113,29 +114,24 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t N, uint32_t K, uint32
     uint32_t w = 0;
     const uint32_t nr = N * (r ? r : 1);
 #define TAKE(words) (w += ((words) + 3) & ~3u, w - (((words) + 3) & ~3u))
-    s.pre = TAKE(N * K + 1);
+    s.pre = TAKE(N * K);
+    s.pfx = TAKE(N * K + 1);
     s.occ = TAKE(K);
     s.lab = TAKE(nmax);
     s.sel = TAKE(nmax);
     s.cand_l = TAKE(nmax);
     s.cand_slot = TAKE(nmax);
     s.win = TAKE(2 * nmax);
-    s.idx = TAKE(nmax);
+    s.idx = TAKE(nmax < 32 ? 32 : nmax);  // also the 32-entry scratch of warp_select
     s.plan = TAKE(3 * nr);
     s.cnt = TAKE(N);
     s.acc = TAKE(nr);
-    uint32_t h = 32;
-    while (h < 2 * nr)
-        h <<= 1;
-    s.hmask = h - 1;
-    s.hkey = TAKE(h);
-    s.hfirst = TAKE(h);
-    s.hjob = TAKE(h);
     s.pj_src = TAKE(nr);
     s.pj_post = TAKE(nr);
     s.pj_ndst = TAKE(nr);
     s.pj_dst = TAKE(nr * N);
-    s.misc = TAKE(32);
+    s.maskw = TAKE((nmax + 31) / 32);
+    s.misc = TAKE(200);
     s.words = w;
 #undef TAKE
     return s;

@@ -97,17 +97,19 @@ __device__ void warp_select(uint64_t key, uint64_t& ctr, uint32_t n, uint32_t k,
             s = j + static_cast<uint32_t>(v % nj);
         }
         if (__ballot_sync(kFull, !ok) == 0) {
-            int pa = -1, q = -1;
-#pragma unroll
-            for (int m = 0; m < 32; ++m) {
-                const uint32_t sm = __shfl_sync(kFull, s, m);
-                if (m < lane && j < k) {
-                    if (sm == j)
-                        pa = m;
-                    if (sm == s)
-                        q = m;
-                }
-            }
+            // q: latest earlier lane drawing the same target (one match instruction)
+            const unsigned same = __match_any_sync(kFull, s);
+            const unsigned lt = (1u << lane) - 1u;
+            const int q = (j < k && (same & lt)) ? 31 - __clz(same & lt) : -1;
+            // pa(j): latest earlier lane m whose target s_m == j (s_m > m), via smem max
+            int* last = reinterpret_cast<int*>(idx);
+            last[lane] = -1;
+            __syncwarp();
+            if (j < k && s < 32 && s != j)
+                atomicMax(&last[s], lane);
+            __syncwarp();
+            const int pa = j < k ? last[lane] : -1;
+            __syncwarp();
             int par = pa >= 0 ? pa : lane;
 #pragma unroll
             for (int it = 0; it < 5; ++it)
@@ -155,18 +157,10 @@ __device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint32_
         const uint32_t t = base + lane;
         const bool act = t < k;
         const uint32_t L = act ? lab[sel[t]] : 0xffffffffu;
-        uint32_t rho = 0;
-        bool last_of_class = true;
-#pragma unroll
-        for (int m = 0; m < 32; ++m) {
-            const uint32_t lm = __shfl_sync(kFull, L, m);
-            if (act && lm == L) {
-                if (m < lane)
-                    ++rho;
-                if (m > lane)
-                    last_of_class = false;
-            }
-        }
+        // in-batch rank of this candidate within its class, and whether it is the last
+        const unsigned same = __match_any_sync(kFull, L);
+        const uint32_t rho = __popc(same & lt);
+        const bool last_of_class = (same >> lane) == 1u;
         const uint32_t o = act ? occ[L] : 0;
         __syncwarp();
         const bool app = act && (o + rho < cap);
@@ -207,90 +201,101 @@ __device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint32_
     }
 }
 
-// S4 — plan(want, view) (sampler.cpp:39-68) for one requester, one full warp.
-// pre: exclusive prefix of the view's occupancy [N*K] with pre[NK] = total.
+// S4 — plan(want, view) draws (sampler.cpp:39-61) for one requester, one full warp.
 // Draws are bounded(total) on consecutive counters; lane l holds counter ctr+1+l.
 // Rejected draws are skipped, duplicates (of accepted flats or of earlier lanes in the
 // same batch) consume their counter without producing an entry — exactly the
 // `while (|out| < want) { f = bounded(total); if (insert(f)) out.push(locate(f)); }`
-// loop. The counter advances to the draw that completed the plan.
-// Exhaustion (want >= total) lists every slot in flat order with no draws.
-// locate (size_table.cpp:29-39) is a binary search over pre (largest i with pre[i] <= f).
-__device__ uint32_t warp_plan(uint64_t key, uint64_t& ctr, uint32_t want, const uint32_t* pre,
-                              uint32_t NK, uint32_t K, uint32_t* acc, uint32_t* plan) {
+// loop. The counter advances to the draw that completed the plan. Exhaustion
+// (want >= total) lists every slot in flat order with no draws. Returns the entry count;
+// acc[] receives the flat indices in draw order.
+__device__ uint32_t warp_plan_draw(uint64_t key, uint64_t& ctr, uint32_t want, uint32_t total,
+                                   uint32_t* acc) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const uint32_t total = pre[NK];
     if (want == 0 || total == 0)
         return 0;
-    uint32_t cnt;
     if (want >= total) {
-        cnt = total;
+        #pragma unroll 1
         for (uint32_t j = lane; j < total; j += 32)
             acc[j] = j;
-    } else {
-        const uint64_t thr = (0ull - static_cast<uint64_t>(total)) % total;
-        uint32_t got = 0;
-        while (got < want) {
-            const uint64_t v = draw_at(key, ctr + 1 + lane);
-            const bool ok = v >= thr;
-            const uint32_t f = static_cast<uint32_t>(v % total);
-            bool dup = !ok;
-#pragma unroll
-            for (int m = 0; m < 32; ++m) {
-                const uint32_t fm = __shfl_sync(kFull, f, m);
-                const int okm = __shfl_sync(kFull, static_cast<int>(ok), m);
-                if (m < lane && okm && fm == f)
-                    dup = true;
-            }
-            for (uint32_t a = 0; a < got; ++a)
-                if (acc[a] == f)
-                    dup = true;
-            const unsigned nm = __ballot_sync(kFull, !dup);
-            const uint32_t c = __popc(nm);
-            const uint32_t need = want - got;
-            const uint32_t rank = __popc(nm & lt);
-            __syncwarp();
-            if (c >= need) {
-                if (!dup && rank < need)
-                    acc[got + rank] = f;
-                ctr += __fns(nm, 0, need) + 1;
-                got = want;
-            } else {
-                if (!dup)
-                    acc[got + rank] = f;
-                ctr += 32;
-                got += c;
-            }
-            __syncwarp();
-        }
-        cnt = want;
+        __syncwarp();
+        return total;
     }
-    __syncwarp();
+    const uint64_t thr = (0ull - static_cast<uint64_t>(total)) % total;
+    uint32_t got = 0;
+    while (got < want) {
+        const uint64_t v = draw_at(key, ctr + 1 + lane);
+        const bool ok = v >= thr;
+        const uint32_t f = static_cast<uint32_t>(v % total);
+        // duplicate of an earlier valid lane in this batch? (rejected lanes get a unique
+        // key above any flat index, total < 2^31)
+        const unsigned same = __match_any_sync(kFull, ok ? f : 0x80000000u + lane);
+        bool dup = !ok || (same & lt) != 0;
+        for (uint32_t a = 0; a < got; ++a)
+            if (acc[a] == f)
+                dup = true;
+        const unsigned nm = __ballot_sync(kFull, !dup);
+        const uint32_t c = __popc(nm);
+        const uint32_t need = want - got;
+        const uint32_t rank = __popc(nm & lt);
+        __syncwarp();
+        if (c >= need) {
+            if (!dup && rank < need)
+                acc[got + rank] = f;
+            ctr += __fns(nm, 0, need) + 1;
+            got = want;
+        } else {
+            if (!dup)
+                acc[got + rank] = f;
+            ctr += 32;
+            got += c;
+        }
+        __syncwarp();
+    }
+    return want;
+}
+
+// locate (size_table.cpp:29-39): flat -> (owner, class, slot) by binary search over the
+// exclusive prefix pfx[0..NK] (largest i with pfx[i] <= f), one warp.
+__device__ void warp_locate(const uint32_t* acc, uint32_t cnt, const uint32_t* pfx, uint32_t NK,
+                            uint32_t K, uint32_t* plan) {
+    const int lane = threadIdx.x & 31;
     for (uint32_t j = lane; j < cnt; j += 32) {
         const uint32_t f = acc[j];
         uint32_t lo = 0, hi = NK;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (pre[mid] <= f)
+            if (pfx[mid] <= f)
                 lo = mid;
             else
                 hi = mid;
         }
         plan[3 * j] = lo / K;
         plan[3 * j + 1] = lo % K;
-        plan[3 * j + 2] = f - pre[lo];
+        plan[3 * j + 2] = f - pfx[lo];
     }
     __syncwarp();
-    return cnt;
 }
 
-// Block-wide exclusive scan of a[0..n) in place, a[n] = total. All threads participate.
-__device__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n, uint32_t* wtot) {
-    const uint32_t T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t nw = T >> 5;
-    const uint32_t per = (n + T - 1) / T;
-    const uint32_t b0 = min(n, tid * per), b1 = min(n, b0 + per);
+// Sum of a[0..n) by one warp.
+__device__ uint32_t warp_sum(const uint32_t* a, uint32_t n) {
+    const int lane = threadIdx.x & 31;
+    uint32_t s = 0;
+    for (uint32_t i = lane; i < n; i += 32)
+        s += a[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(kFull, s, o);
+    return s;
+}
+
+// Exclusive prefix of a[0..n) into out[0..n] (out[n] = total), one warp: each lane scans a
+// contiguous stripe, then a warp scan of the stripe totals.
+__device__ uint32_t warp_exclusive_scan(const uint32_t* a, uint32_t n, uint32_t* out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t per = (n + 31) / 32;
+    const uint32_t b0 = min(n, lane * per), b1 = min(n, b0 + per);
     uint32_t s = 0;
     for (uint32_t i = b0; i < b1; ++i)
         s += a[i];
@@ -301,472 +306,483 @@ __device__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n, uint32_t* wtot
         if (lane >= static_cast<uint32_t>(o))
             x += y;
     }
-    if (lane == 31)
-        wtot[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < nw ? wtot[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, w, o);
-            if (lane >= static_cast<uint32_t>(o))
-                w += y;
-        }
-        if (lane < nw)
-            wtot[lane] = w;
-    }
-    __syncthreads();
-    uint32_t excl = x - s + (warp ? wtot[warp - 1] : 0);
+    uint32_t excl = x - s;
     for (uint32_t i = b0; i < b1; ++i) {
-        const uint32_t v = a[i];
-        a[i] = excl;
-        excl += v;
+        out[i] = excl;
+        excl += a[i];
     }
-    const uint32_t total = wtot[nw - 1];
-    __syncthreads();
-    if (tid == 0)
-        a[n] = total;
-    __syncthreads();
+    const uint32_t total = __shfl_sync(kFull, x, 31);
+    if (lane == 0)
+        out[n] = total;
+    __syncwarp();
     return total;
 }
 
-// Copy `len` vectors (16 B, or 4 B when !vec16) from src to up to 1+kMaxWorld dsts, then
-// optionally overwrite post_dst with post_src — in that order per vector and per thread,
-// which is what lets a slot be read for a push and overwritten by this round's candidate
-// in the same launch (exact-horizon semantics).
-template <typename V, int U>
-__device__ __forceinline__ void copy_run(const V* src, V* const* dsts, int nd, const V* post_src,
-                                         V* post_dst, uint64_t len, uint32_t first,
-                                         uint32_t stride) {
-    for (uint64_t i = first; i < len; i += uint64_t(stride) * U) {
+// Named barrier 1 over the first `nthreads` threads (the control warps).
+__device__ __forceinline__ void ctl_sync(uint32_t nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+template <typename V>
+__device__ __forceinline__ V ld_vec(const V* p) {
+    if constexpr (sizeof(V) == 16) {
+        const uint4 v = ld_stream(reinterpret_cast<const uint4*>(p));
+        return *reinterpret_cast<const V*>(&v);
+    } else {
+        return __ldg(p);
+    }
+}
+
+// One warp copies dynamically claimed chunks of 32*U vectors out of [lo, hi) (32-bit
+// vector indices). `src(gv)` gives the source address of vector gv; `store(gv, v)` writes
+// it to every destination of its job (and performs the job's trailing overwrite, if any,
+// after those stores — the read-before-write order of a pushed slot). All U loads of a
+// lane are issued before any store (memory-level parallelism).
+template <typename V, int U, typename Src, typename Store>
+__device__ __forceinline__ void warp_copy(uint32_t lo, uint32_t hi, uint32_t* counter, Src src,
+                                          Store store) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (;;) {
+        uint32_t c = 0;
+        if (lane == 0)
+            c = atomicAdd(counter, 1u);
+        c = __shfl_sync(kFull, c, 0);
+        const uint32_t base = lo + c * (32u * U);
+        if (base >= hi)
+            break;
         V r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t x = i + uint64_t(u) * stride;
-            if (x < len) {
-                if constexpr (sizeof(V) == 16)
-                    r[u] = ld_stream(reinterpret_cast<const uint4*>(src + x));
-                else
-                    r[u] = __ldg(src + x);
-            }
+            const uint32_t gv = base + u * 32 + lane;
+            if (gv < hi)
+                r[u] = ld_vec(src(gv));
         }
-        for (int d = 0; d < nd; ++d) {
-            V* dst = dsts[d];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t x = i + uint64_t(u) * stride;
-                if (x < len)
-                    dst[x] = r[u];
-            }
-        }
-        if (post_dst) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t x = i + uint64_t(u) * stride;
-                if (x < len) {
-                    if constexpr (sizeof(V) == 16)
-                        r[u] = ld_stream(reinterpret_cast<const uint4*>(post_src + x));
-                    else
-                        r[u] = __ldg(post_src + x);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t x = i + uint64_t(u) * stride;
-                if (x < len)
-                    post_dst[x] = r[u];
-            }
+        for (int u = 0; u < U; ++u) {
+            const uint32_t gv = base + u * 32 + lane;
+            if (gv < hi)
+                store(gv, r[u]);
         }
     }
 }
 
-// Even split of a virtual vector space [0, jobs*nvec) over the grid; `resolve(job, ...)`
-// yields the byte pointers of one job.
-template <typename V, int U, typename Resolve>
-__device__ __forceinline__ void copy_space(uint32_t jobs, uint64_t nvec, uint32_t first,
-                                           uint32_t stride, uint32_t part, uint32_t parts,
-                                           Resolve resolve) {
-    const uint64_t tv = uint64_t(jobs) * nvec;
-    if (tv == 0)
-        return;
-    uint64_t lo = tv * part / parts, hi = tv * (part + 1) / parts;
-    while (lo < hi) {
-        const uint32_t job = static_cast<uint32_t>(lo / nvec);
-        const uint64_t in_row = lo - uint64_t(job) * nvec;
-        const uint64_t end = min(hi, uint64_t(job + 1) * nvec);
-        const uint8_t* src = nullptr;
-        uint8_t* dst8[1 + kMaxWorld];
-        int nd = 0;
-        const uint8_t* psrc = nullptr;
-        uint8_t* pdst = nullptr;
-        resolve(job, src, dst8, nd, psrc, pdst);
-        V* dsts[1 + kMaxWorld];
-        for (int d = 0; d < nd; ++d)
-            dsts[d] = reinterpret_cast<V*>(dst8[d]) + in_row;
-        copy_run<V, U>(reinterpret_cast<const V*>(src) + in_row, dsts, nd,
-                       psrc ? reinterpret_cast<const V*>(psrc) + in_row : nullptr,
-                       pdst ? reinterpret_cast<V*>(pdst) + in_row : nullptr, end - lo, first,
-                       stride);
-        lo = end;
-    }
+__device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
+    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+        p.trace[slot] = globaltimer();
 }
 
 }  // namespace
 
 // misc[] words (shared)
 enum : uint32_t {
-    kMiscErr = 0,       // error detected this launch
+    kMiscErr = 0,       // rendezvous error this launch
     kMiscBad = 1,       // a label >= K
     kMiscJobs = 2,      // push-job counter
-    kMiscWin = 3,       // winner (candidate-write) job counter
-    kMiscCtr = 4,       // 4 words: cand_ctr, evict_ctr (u64 each)
-    kMiscApp = 8,       // appends
-    kMiscWtot = 12,     // 16 words: scan warp totals
-    kMiscScratch = 12,  // aliases wtot (eviction fallback scratch, used after the scan)
+    kMiscWin = 3,       // candidate-write job counter
+    kMiscChunkA = 4,    // assemble-copy chunk counter
+    kMiscChunkB = 5,    // job-copy chunk counter
+    kMiscScratch = 8,   // 32 words: eviction-draw fallback scratch
+    kMiscState = 40,    // DevState snapshot (sizeof(DevState)/4 words)
+    kMiscMaskP = 72,    // 128 words: push-leader ballot masks (N*r <= 4096)
+    kMiscWords = 200,
 };
+static_assert(sizeof(DevState) % 8 == 0 && 40 + sizeof(DevState) / 4 <= 72, "DevState layout");
 
+// One engine iteration on one rank; see the file comment. Warp roles in every CTA:
+//   control warps [0, CW), CW = N+2, synchronised by named barrier 1:
+//     warp 0      S1 selection + S2 assignment of this rank; leader CTA: round-(i+1)
+//                 state, occupancy publish, slab labels, report
+//     warp 1+q    S4 plan(i-1) of requester q (every rank replicates every requester's
+//                 global-sampling stream so owners know what to push)
+//     warp N+1    prefix of the global view (for locate), concurrent with the draws
+//   copy warps [CW, 16): start the control-independent m_i -> m'_i copy immediately.
+// Then all warps drain the assemble chunks, barrier, and copy the merged candidate-write
+// and push jobs. Multi-rank launches end with the completion handshake.
+template <typename V>
 __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_constant__ StepParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const SmemLayout L = smem_layout(p.N, p.K, p.nmax, p.r);
-    uint32_t* pre = sm + L.pre;
-    uint32_t* occ = sm + L.occ;
+    uint32_t* pre = sm + L.pre;   // raw view occupancy [N*K]
+    uint32_t* pfx = sm + L.pfx;   // exclusive prefix [N*K+1]
+    uint32_t* occ = sm + L.occ;   // own occupancy, updated in place by S2
     uint32_t* lab = sm + L.lab;
     uint32_t* sel = sm + L.sel;
     uint32_t* cand_l = sm + L.cand_l;
     uint32_t* cand_slot = sm + L.cand_slot;
-    uint32_t* win = sm + L.win;  // candidate-write jobs: (batch row, slab row) pairs
-    uint32_t* kind = sm + L.idx; // per candidate: 1 = append (after selection, idx is free)
+    uint32_t* win = sm + L.win;   // candidate-write jobs: (batch row, slab row) pairs
+    uint32_t* kind = sm + L.idx;  // per candidate: 1 = append (idx is free after S1)
     uint32_t* plan = sm + L.plan;
     uint32_t* cnt = sm + L.cnt;
     uint32_t* acc = sm + L.acc;
-    uint32_t* hkey = sm + L.hkey;
-    uint32_t* hfirst = sm + L.hfirst;
-    uint32_t* hjob = sm + L.hjob;
     uint32_t* pj_src = sm + L.pj_src;
     int* pj_post = reinterpret_cast<int*>(sm + L.pj_post);
     uint32_t* pj_ndst = sm + L.pj_ndst;
     uint32_t* pj_dst = sm + L.pj_dst;
     uint32_t* misc = sm + L.misc;
+    DevState* st = reinterpret_cast<DevState*>(misc + kMiscState);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t T = blockDim.x;
     const bool leader = blockIdx.x == 0;
     const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap, r = p.r;
     const uint32_t NK = N * K;
     const uint64_t S = p.S;
+    const uint32_t nvec = static_cast<uint32_t>(S / sizeof(V));
     RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     const bool do_update = p.mode & kModeUpdate;
     const bool do_assemble = p.mode & kModeAssemble;
     const bool do_plan = (p.mode & kModePlan) && p.step > 0;
     const bool do_publish = p.mode & kModePublish;
     const bool multi = (p.mode & kModePeers) && N > 1;
-    constexpr uint32_t kEmpty = 0xffffffffu;
-
-    if (tid < 32)
-        misc[tid] = 0;
-    for (uint32_t x = tid; x <= L.hmask; x += T) {
-        hkey[x] = kEmpty;
-        hfirst[x] = kEmpty;
-    }
-    const uint32_t dead = __ldcg(&p.st_in->error);
-    if (dead) {  // sticky: a failed round kills the engine (engine.cpp:67-68,188-198)
-        if (leader && tid == 0) {
-            *p.st_out = *p.st_in;
-            if (p.mailbox) {
-                volatile uint32_t* mb = p.mailbox;
-                mb[p.aslot] = 0;
-                mb[kAugRing + p.aslot] = dead;
-                mb[2 * kAugRing] = dead;
-            }
-        }
-        return;
-    }
+    const uint32_t CW = N + 2;  // control warps
+    const uint32_t CT = CW * 32;
+    const bool ctl = warp < CW;
+    const uint32_t part = blockIdx.x, parts = gridDim.x;
 
     uint8_t* my_aug = p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
     uint32_t* my_auglab = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
                           uint64_t(p.aslot) * p.auglab_slot_elems;
     const uint32_t row0 = p.nmax - n;  // m'_i occupies rows [nmax-n, nmax+|reps|)
 
-    // Phase A0: loads that need no peer (own occupancy at version i, batch labels).
-    const uint32_t* table = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table);
-    const uint32_t* tin = table + uint64_t(p.tslot_in) * NK;
+    trace_at(p, 0);
+    if (p.trace && tid == 0)
+        atomicMin(p.trace + 14, globaltimer());
+    if (tid < kMiscState)
+        misc[tid] = 0;
     __syncthreads();
-    for (uint32_t x = tid; x < K; x += T)
-        occ[x] = __ldcg(tin + uint64_t(me) * K + x);
-    for (uint32_t x = tid; x < n; x += T) {
-        const uint32_t l = __ldg(p.labels + x);
-        lab[x] = l;
-        if (l >= K)
-            misc[kMiscBad] = 1;
-    }
 
-    // Phase A1: wait for every peer's occupancy row of version i (the size rendezvous,
-    // size_table.cpp:66-100 / engine.cpp:152), bounded by timeout_ns.
-    if (do_plan && multi && tid == 0) {
-        const uint64_t t0 = globaltimer();
-        for (uint32_t w = 0; w < N; ++w) {
-            if (w == me)
+    // The control-independent copy m_i -> m'_i rows [row0, row0+n), claimed in chunks.
+    auto assemble = [&]() {
+        constexpr int U = sizeof(V) == 16 ? 8 : 16;
+        const uint32_t tv = n * nvec;
+        const uint32_t lo = static_cast<uint32_t>(uint64_t(tv) * part / parts);
+        const uint32_t hi = static_cast<uint32_t>(uint64_t(tv) * (part + 1) / parts);
+        const V* src = reinterpret_cast<const V*>(p.batch);
+        V* dst = reinterpret_cast<V*>(my_aug + uint64_t(row0) * S);
+        warp_copy<V, U>(lo, hi, &misc[kMiscChunkA], [&](uint32_t gv) { return src + gv; },
+                        [&](uint32_t gv, const V& v) { dst[gv] = v; });
+    };
+
+    if (ctl) {
+        auto sync = [CT] { ctl_sync(CT); };
+        // ---- one round trip: state, own occupancy row, labels (and the view if N == 1) --
+        const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
+                              uint64_t(p.tslot_in) * NK;
+        if (tid < sizeof(DevState) / 8)
+            reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.st_in) + tid);
+        #pragma unroll 1
+        for (uint32_t x = tid; x < K; x += CT) {
+            const uint32_t o = __ldcg(tin + uint64_t(me) * K + x);
+            occ[x] = o;
+            if (!multi)
+                pre[x] = o;  // N == 1: the view is the own row
+        }
+        #pragma unroll 1
+        for (uint32_t x = tid; x < n; x += CT) {
+            const uint32_t l = __ldg(p.labels + x);
+            lab[x] = l;
+            if (l >= K)
+                misc[kMiscBad] = 1;
+        }
+        // size rendezvous (size_table.cpp:66-100 / engine.cpp:152), bounded by timeout_ns
+        if (do_plan && multi && tid == 0) {
+            const uint64_t t0 = globaltimer();
+            for (uint32_t w = 0; w < N; ++w) {
+                if (w == me)
+                    continue;
+                while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step) {
+                    if (globaltimer() - t0 > p.timeout_ns) {
+                        misc[kMiscErr] = DRB_ERR_TRANSPORT;
+                        break;
+                    }
+                    __nanosleep(32);
+                }
+            }
+        }
+        sync();
+        if (do_plan && multi) {
+            #pragma unroll 1
+            for (uint32_t x = tid; x < NK; x += CT)
+                pre[x] = __ldcg(tin + x);
+            sync();
+        }
+        trace_at(p, 1);
+        const bool dead = st->error != 0;  // sticky: a failed round kills the engine
+        const bool bad = misc[kMiscBad] != 0;  // usage_error before any draw (:44-47)
+        const uint32_t k = (!dead && do_update && !bad && n > 0) ? min(p.c, n) : 0;
+        const bool planning = do_plan && !dead;
+
+        if (warp == 0) {
+            // ---- S1 + S2 of this rank; the leader writes round-(i+1) state right away --
+            uint64_t cand_ctr = (p.mode & kModeCtrParams) ? p.cand_ctr0 : st->cand_ctr;
+            uint64_t evict_ctr = (p.mode & kModeCtrParams) ? p.evict_ctr0 : st->evict_ctr;
+            uint32_t appends = 0;
+            if (k > 0) {
+                warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
+                warp_assign(p.evict_key, evict_ctr, cap, k, sel, lab, occ, cand_l, cand_slot,
+                            misc + kMiscScratch, kind, appends);
+            }
+            trace_at(p, 2);
+            if (leader) {
+                const uint32_t err = dead ? st->error
+                                          : (misc[kMiscErr] | ((bad && do_update) ? DRB_ERR_USAGE : 0u));
+                if (lane == 0) {
+                    DevState* o = p.st_out;
+                    o->cand_ctr = cand_ctr;
+                    o->evict_ctr = evict_ctr;
+                    o->version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
+                    o->total = st->total + appends;
+                    o->cross_class = st->cross_class;
+                    o->error = err;
+                    if (!planning)
+                        for (uint32_t q = 0; q < N; ++q)
+                            o->samp_ctr[q] = st->samp_ctr[q];
+                }
+                #pragma unroll 1
+                for (uint32_t t = lane; t < k; t += 32)  // stored label == class
+                    p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
+                if (do_assemble)
+                    #pragma unroll 1
+                    for (uint32_t x = lane; x < n; x += 32)
+                        my_auglab[row0 + x] = lab[x];
+                if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
+                    uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
+                                     uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
+                    #pragma unroll 1
+                    for (uint32_t x = lane; x < K; x += 32)
+                        tout[x] = occ[x];
+                    if (multi) {
+                        for (uint32_t w = 0; w < N; ++w) {
+                            if (w == me)
+                                continue;
+                            uint32_t* pt = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
+                                           uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
+                            #pragma unroll 1
+                            for (uint32_t x = lane; x < K; x += 32)
+                                pt[x] = occ[x];
+                        }
+                        __threadfence_system();
+                        __syncwarp();
+                        if (lane < N && lane != me) {
+                            RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
+                            st_release_sys(&peer->occ_flag[me], p.step + 1);
+                        }
+                    }
+                }
+                if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
+                    #pragma unroll 1
+                    for (uint32_t x = lane; x < 2 * K + 2; x += 32)
+                        p.report[x] = 0;
+                    __syncwarp();
+                    __threadfence_block();
+                    for (uint32_t t = lane; t < k; t += 32) {
+                        const bool app = kind[t] != 0;
+                        atomicAdd(&p.report[(app ? 0 : K) + cand_l[t]], 1u);
+                        atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
+                    }
+                }
+                if (p.mailbox && lane == 0 && err)
+                    reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
+            }
+        } else if (warp <= N) {
+            // ---- S4 draws of requester q ------------------------------------------------
+            if (planning) {
+                const uint32_t q = warp - 1;
+                uint64_t ctr = st->samp_ctr[q];
+                const uint32_t total = warp_sum(pre, NK);
+                const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
+                if (lane == 0) {
+                    cnt[q] = c;
+                    if (leader)
+                        p.st_out->samp_ctr[q] = ctr;
+                }
+            }
+        } else if (planning) {
+            warp_exclusive_scan(pre, NK, pfx);  // warp N+1
+        }
+        sync();
+        trace_at(p, 3);
+        if (planning && warp >= 1 && warp <= N) {
+            const uint32_t q = warp - 1;
+            warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
+            if (leader && q == me && do_assemble) {
+                #pragma unroll 1
+                for (uint32_t j = lane; j < cnt[q]; j += 32)
+                    my_auglab[p.nmax + j] = plan[3 * (q * r + j) + 1];  // stored label == class
+                if (lane == 0) {
+                    hdr->aug_count[p.aslot] = n + cnt[q];
+                    if (p.mailbox) {
+                        volatile uint32_t* mb = p.mailbox;
+                        mb[p.aslot] = n + cnt[q];
+                        mb[kAugRing + p.aslot] = misc[kMiscErr];
+                    }
+                }
+            }
+        }
+        if (leader && !planning && warp == 0 && lane == 0 && do_assemble) {
+            hdr->aug_count[p.aslot] = n;
+            if (p.mailbox) {
+                volatile uint32_t* mb = p.mailbox;
+                mb[p.aslot] = n;
+                mb[kAugRing + p.aslot] = dead ? st->error : misc[kMiscErr];
+            }
+        }
+        sync();
+        trace_at(p, 4);
+
+        // ---- job construction (identical, deterministic numbering in every CTA: the
+        // grid splits the job space by index, so no atomics decide the order) -------------
+        // push job: one per distinct owned slot over all requesters' plans, numbered in
+        // entry order; its first entry collects every (q, j) that drew the slot; if this
+        // round's winning candidate (last writer in selection order) targets the slot, the
+        // job ends with that overwrite (read at version i, then write — the exact horizon).
+        // candidate-write job: winning candidates whose slot no push job reads this round.
+        const uint32_t NR = planning ? N * r : 0;
+        uint32_t* maskP = misc + kMiscMaskP;  // ballot masks of push leaders, per 32 entries
+        uint32_t* maskW = sm + L.maskw;       // ballot masks of candidate writes
+        for (uint32_t base = warp * 32; base < NR; base += CT) {
+            const uint32_t e = base + lane;
+            bool lead = false;
+            if (e < NR) {
+                const uint32_t q = e / r, j = e - q * r;
+                if (j < cnt[q] && plan[3 * e] == me) {
+                    const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
+                    lead = true;
+                    for (uint32_t q2 = 0; q2 < q && lead; ++q2)
+                        for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
+                            const uint32_t* x = plan + 3 * (q2 * r + j2);
+                            if (x[0] == me && x[1] == cls && x[2] == slot) {
+                                lead = false;
+                                break;
+                            }
+                        }
+                }
+            }
+            const unsigned m = __ballot_sync(kFull, lead);
+            if (lane == 0)
+                maskP[base >> 5] = m;
+        }
+        for (uint32_t base = warp * 32; base < k; base += CT) {
+            const uint32_t t = base + lane;
+            bool w = false;
+            if (t < k) {
+                const uint32_t cl = cand_l[t], cs = cand_slot[t];
+                w = true;
+                for (uint32_t u = t + 1; u < k && w; ++u)
+                    w = !(cand_l[u] == cl && cand_slot[u] == cs);
+                for (uint32_t e = 0; e < NR && w; ++e) {
+                    const uint32_t q = e / r;
+                    w = !((e - q * r) < cnt[q] && plan[3 * e] == me && plan[3 * e + 1] == cl &&
+                          plan[3 * e + 2] == cs);
+                }
+            }
+            const unsigned m = __ballot_sync(kFull, w);
+            if (lane == 0)
+                maskW[base >> 5] = m;
+        }
+        sync();
+        const unsigned lt = (1u << lane) - 1u;
+        for (uint32_t base = warp * 32; base < NR; base += CT) {
+            const unsigned m = maskP[base >> 5];
+            if (!((m >> lane) & 1u))
                 continue;
-            while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step) {
-                if (globaltimer() - t0 > p.timeout_ns) {
-                    misc[kMiscErr] = DRB_ERR_TRANSPORT;
+            uint32_t pj = __popc(m & lt);
+            for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
+                pj += __popc(maskP[b2]);
+            const uint32_t e = base + lane, q = e / r, j = e - q * r;
+            const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
+            uint32_t nd = 0;
+            pj_dst[pj * N + nd++] = (q << 16) | j;
+            for (uint32_t q2 = q + 1; q2 < N; ++q2)
+                for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
+                    const uint32_t* x = plan + 3 * (q2 * r + j2);
+                    if (x[0] == me && x[1] == cls && x[2] == slot) {
+                        pj_dst[pj * N + nd++] = (q2 << 16) | j2;
+                        break;
+                    }
+                }
+            pj_ndst[pj] = nd;
+            pj_src[pj] = cls * cap + slot;
+            int post = -1;
+            for (int t = static_cast<int>(k) - 1; t >= 0; --t)
+                if (cand_l[t] == cls && cand_slot[t] == slot) {
+                    post = static_cast<int>(sel[t]);
                     break;
                 }
-                __nanosleep(64);
-            }
+            pj_post[pj] = post;
         }
-    }
-    __syncthreads();
-    if (do_plan) {
-        for (uint32_t x = tid; x < NK; x += T)
-            pre[x] = __ldcg(tin + x);
-        __syncthreads();
-        block_exclusive_scan(pre, NK, misc + kMiscWtot);
-    }
-    const bool bad = misc[kMiscBad] != 0;  // label >= K: usage_error before any draw (:44-47)
-    const uint32_t k = (do_update && !bad && n > 0) ? min(p.c, n) : 0;
-
-    // Phase B: control decisions, redundantly in every CTA.
-    //   warp 0      : S1 selection + S2 slot assignment of this rank's candidates
-    //   warps 1..N  : S4 plan(i-1) of requester q = warp-1 (each rank replicates every
-    //                 requester's global-sampling stream, so owners know what to push)
-    if (warp == 0) {
-        uint64_t cand_ctr = (p.mode & kModeCtrParams) ? p.cand_ctr0 : p.st_in->cand_ctr;
-        uint64_t evict_ctr = (p.mode & kModeCtrParams) ? p.evict_ctr0 : p.st_in->evict_ctr;
-        uint32_t appends = 0;
-        if (k > 0) {
-            warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
-            warp_assign(p.evict_key, evict_ctr, cap, k, sel, lab, occ, cand_l, cand_slot,
-                        misc + kMiscScratch, kind, appends);
-        }
-        if (lane == 0) {
-            reinterpret_cast<uint64_t*>(misc + kMiscCtr)[0] = cand_ctr;
-            reinterpret_cast<uint64_t*>(misc + kMiscCtr)[1] = evict_ctr;
-            misc[kMiscApp] = appends;
-        }
-    } else if (do_plan && warp <= N) {
-        const uint32_t q = warp - 1;
-        uint64_t ctr = p.st_in->samp_ctr[q];
-        const uint32_t c = warp_plan(p.samp_key[q], ctr, r, pre, NK, K, acc + q * r,
-                                     plan + 3 * q * r);
-        if (lane == 0) {
-            cnt[q] = c;
-            if (leader)
-                p.st_out->samp_ctr[q] = ctr;
-        }
-    }
-    __syncthreads();
-
-    // Phase C: job construction.
-    //  C1: owned plan entries (any requester) insert their slab row into a shared hash
-    //      table keeping the first entry index -> one push job per distinct slot.
-    const uint32_t NR = do_plan ? N * r : 0;
-    for (uint32_t e = tid; e < NR; e += T) {
-        const uint32_t q = e / r, j = e - q * r;
-        if (j < cnt[q] && plan[3 * e] == me) {
-            const uint32_t key = plan[3 * e + 1] * cap + plan[3 * e + 2];
-            uint32_t h = (key * 0x9e3779b1u) & L.hmask;
-            for (;;) {
-                const uint32_t prev = atomicCAS(&hkey[h], kEmpty, key);
-                if (prev == kEmpty || prev == key) {
-                    atomicMin(&hfirst[h], e);
-                    break;
-                }
-                h = (h + 1) & L.hmask;
-            }
-        }
-    }
-    __syncthreads();
-    //  C2: the first entry of each slot allocates the push job.
-    for (uint32_t e = tid; e < NR; e += T) {
-        const uint32_t q = e / r, j = e - q * r;
-        if (j < cnt[q] && plan[3 * e] == me) {
-            const uint32_t key = plan[3 * e + 1] * cap + plan[3 * e + 2];
-            uint32_t h = (key * 0x9e3779b1u) & L.hmask;
-            while (hkey[h] != key)
-                h = (h + 1) & L.hmask;
-            if (hfirst[h] == e) {
-                const uint32_t pj = atomicAdd(&misc[kMiscJobs], 1u);
-                hjob[h] = pj;
-                pj_src[pj] = key;
-                pj_ndst[pj] = 0;
-                pj_post[pj] = -1;
-            }
-        }
-    }
-    __syncthreads();
-    //  C3: every owned entry registers its destination row (requester q, rep j);
-    //      every winning candidate (last writer of its (class, slot) in selection order)
-    //      becomes either a candidate-write job or, if its slot is also read by a push
-    //      this round, the push job's trailing overwrite (read-before-write hazard).
-    for (uint32_t e = tid; e < NR; e += T) {
-        const uint32_t q = e / r, j = e - q * r;
-        if (j < cnt[q] && plan[3 * e] == me) {
-            const uint32_t key = plan[3 * e + 1] * cap + plan[3 * e + 2];
-            uint32_t h = (key * 0x9e3779b1u) & L.hmask;
-            while (hkey[h] != key)
-                h = (h + 1) & L.hmask;
-            const uint32_t pj = hjob[h];
-            const uint32_t slotpos = atomicAdd(&pj_ndst[pj], 1u);
-            pj_dst[pj * N + slotpos] = (q << 16) | j;
-        }
-    }
-    for (uint32_t t = tid; t < k; t += T) {
-        bool winner = true;
-        for (uint32_t u = t + 1; u < k; ++u)
-            if (cand_l[u] == cand_l[t] && cand_slot[u] == cand_slot[t])
-                winner = false;
-        if (!winner)
-            continue;
-        const uint32_t key = cand_l[t] * cap + cand_slot[t];
-        int hazard_job = -1;
-        if (NR) {
-            uint32_t h = (key * 0x9e3779b1u) & L.hmask;
-            while (hkey[h] != kEmpty) {
-                if (hkey[h] == key) {
-                    hazard_job = static_cast<int>(hjob[h]);
-                    break;
-                }
-                h = (h + 1) & L.hmask;
-            }
-        }
-        if (hazard_job >= 0) {
-            pj_post[hazard_job] = static_cast<int>(sel[t]);
-        } else {
-            const uint32_t w = atomicAdd(&misc[kMiscWin], 1u);
+        for (uint32_t base = warp * 32; base < k; base += CT) {
+            const unsigned m = maskW[base >> 5];
+            if (!((m >> lane) & 1u))
+                continue;
+            uint32_t w = __popc(m & lt);
+            for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
+                w += __popc(maskW[b2]);
+            const uint32_t t = base + lane;
             win[2 * w] = sel[t];
-            win[2 * w + 1] = key;
+            win[2 * w + 1] = cand_l[t] * cap + cand_slot[t];
         }
+        if (tid == 0) {
+            uint32_t np = 0, nw = 0;
+            for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
+                np += __popc(maskP[b2]);
+            for (uint32_t b2 = 0; b2 < (k + 31) / 32; ++b2)
+                nw += __popc(maskW[b2]);
+            misc[kMiscJobs] = np;
+            misc[kMiscWin] = nw;
+        }
+        trace_at(p, 5);
     }
+    // copy warps arrive here at once; control warps help drain when done
+    if (do_assemble)
+        assemble();
+    trace_at(p, 9);
     __syncthreads();
+    trace_at(p, 6);
+
+    // ---- merged candidate-write + push jobs (all warps) --------------------------------
     const uint32_t n_win = misc[kMiscWin];
     const uint32_t n_push = misc[kMiscJobs];
-
-    // Phase D (leader CTA): state for round i+1, occupancy publish, m' labels, report.
-    if (leader) {
-        const uint64_t cctr = reinterpret_cast<uint64_t*>(misc + kMiscCtr)[0];
-        const uint64_t ectr = reinterpret_cast<uint64_t*>(misc + kMiscCtr)[1];
-        const uint32_t appends = misc[kMiscApp];
-        const uint32_t err = misc[kMiscErr] | ((bad && do_update) ? DRB_ERR_USAGE : 0u);
-        if (tid == 0) {
-            DevState* o = p.st_out;
-            o->cand_ctr = cctr;
-            o->evict_ctr = ectr;
-            o->version = p.st_in->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
-            o->total = p.st_in->total + appends;
-            o->cross_class = p.st_in->cross_class;
-            o->error = err;
-            if (!do_plan)
-                for (uint32_t q = 0; q < N; ++q)
-                    o->samp_ctr[q] = p.st_in->samp_ctr[q];
-        }
-        for (uint32_t t = tid; t < k; t += T)  // stored label == class (class-partitioned)
-            p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
-        if (do_publish) {  // publish_row(i): version i+1 (engine.cpp:108-136)
-            uint32_t* tout_local = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
-                                   uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
-            for (uint32_t x = tid; x < K; x += T)
-                tout_local[x] = occ[x];
-            if (multi) {
-                for (uint32_t w = 0; w < N; ++w) {
-                    if (w == me)
-                        continue;
-                    uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
-                                     uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
-                    for (uint32_t x = tid; x < K; x += T)
-                        tout[x] = occ[x];
-                }
-                __threadfence_system();
-                __syncthreads();
-                if (tid < N && tid != me) {
-                    RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[tid]);
-                    st_release_sys(&peer->occ_flag[me], p.step + 1);
-                }
-            }
-        }
-        if (do_assemble) {
-            for (uint32_t x = tid; x < n; x += T)
-                my_auglab[row0 + x] = lab[x];
-            const uint32_t mine = do_plan ? cnt[me] : 0;
-            for (uint32_t j = tid; j < mine; j += T)
-                my_auglab[p.nmax + j] = plan[3 * (me * r + j) + 1];
-            if (tid == 0) {
-                hdr->aug_count[p.aslot] = n + mine;
-                if (p.mailbox) {
-                    // m'_i itself is only invalid on a rendezvous failure; a bad label kills
-                    // the engine for the NEXT update (engine.cpp:188-198 then :67-68).
-                    volatile uint32_t* mb = p.mailbox;
-                    mb[p.aslot] = n + mine;
-                    mb[kAugRing + p.aslot] = misc[kMiscErr];
-                    if (err)
-                        mb[2 * kAugRing] = err;
-                }
-            }
-        }
-        if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
-            for (uint32_t x = tid; x < 2 * K + 2; x += T)
-                p.report[x] = 0;
-            __syncthreads();
-            for (uint32_t t = tid; t < k; t += T) {
-                const bool app = kind[t] != 0;
-                atomicAdd(&p.report[(app ? 0 : K) + cand_l[t]], 1u);
-                atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
-            }
-        }
-    }
-
-    // Phase E: byte movement. Three job spaces, each split evenly over the grid:
-    //   assemble : m_i row x            -> m'_i row row0+x                 (n jobs)
-    //   write    : m_i row x (winner)   -> slab[L][slot]                   (n_win jobs)
-    //   push     : slab[cls][slot]      -> m'_i(q) row nmax+j for each requester entry
-    //              that drew it, then (hazard) m_i row -> slab[cls][slot]  (n_push jobs)
-    const uint32_t part = blockIdx.x, parts = gridDim.x;
-    auto run = [&](auto vec_tag) {
-        using V = decltype(vec_tag);
-        const uint64_t nvec = S / sizeof(V);
+    if (n_win + n_push) {
         constexpr int U = sizeof(V) == 16 ? 4 : 8;
-        if (do_assemble)
-            copy_space<V, U>(n, nvec, tid, T, part, parts,
-                             [&](uint32_t job, const uint8_t*& src, uint8_t** d, int& nd,
-                                 const uint8_t*&, uint8_t*&) {
-                                 src = p.batch + uint64_t(job) * S;
-                                 d[0] = my_aug + uint64_t(row0 + job) * S;
-                                 nd = 1;
-                             });
-        copy_space<V, U>(n_win, nvec, tid, T, part, parts,
-                         [&](uint32_t job, const uint8_t*& src, uint8_t** d, int& nd,
-                             const uint8_t*&, uint8_t*&) {
-                             src = p.batch + uint64_t(win[2 * job]) * S;
-                             d[0] = p.slab + uint64_t(win[2 * job + 1]) * S;
-                             nd = 1;
-                         });
-        copy_space<V, U>(n_push, nvec, tid, T, part, parts,
-                         [&](uint32_t job, const uint8_t*& src, uint8_t** d, int& nd,
-                             const uint8_t*& psrc, uint8_t*& pdst) {
-                             src = p.slab + uint64_t(pj_src[job]) * S;
-                             nd = static_cast<int>(pj_ndst[job]);
-                             for (int x = 0; x < nd; ++x) {
-                                 const uint32_t e = pj_dst[job * N + x];
-                                 const uint32_t q = e >> 16, j = e & 0xffffu;
-                                 d[x] = p.region[q] + p.off_aug +
-                                        uint64_t(p.aslot) * p.aug_slot_bytes +
-                                        uint64_t(p.nmax + j) * S;
-                             }
-                             if (pj_post[job] >= 0) {
-                                 psrc = p.batch + uint64_t(pj_post[job]) * S;
-                                 pdst = p.slab + uint64_t(pj_src[job]) * S;
-                             }
-                         });
-    };
-    if (p.vec16)
-        run(uint4{});
-    else
-        run(uint32_t{});
+        const uint32_t tv = (n_win + n_push) * nvec;
+        const uint32_t lo = static_cast<uint32_t>(uint64_t(tv) * part / parts);
+        const uint32_t hi = static_cast<uint32_t>(uint64_t(tv) * (part + 1) / parts);
+        const V* batch = reinterpret_cast<const V*>(p.batch);
+        V* slab = reinterpret_cast<V*>(p.slab);
+        const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
+        warp_copy<V, U>(
+            lo, hi, &misc[kMiscChunkB],
+            [&](uint32_t gv) -> const V* {
+                const uint32_t job = gv / nvec, off = gv - job * nvec;
+                if (job < n_win)
+                    return batch + uint64_t(win[2 * job]) * nvec + off;
+                return slab + uint64_t(pj_src[job - n_win]) * nvec + off;
+            },
+            [&](uint32_t gv, const V& v) {
+                const uint32_t job = gv / nvec, off = gv - job * nvec;
+                if (job < n_win) {
+                    slab[uint64_t(win[2 * job + 1]) * nvec + off] = v;
+                    return;
+                }
+                const uint32_t pj = job - n_win;
+                const uint32_t nd = pj_ndst[pj];
+                #pragma unroll 1
+                for (uint32_t x = 0; x < nd; ++x) {
+                    const uint32_t e = pj_dst[pj * N + x];
+                    const uint32_t q = e >> 16, j = e & 0xffffu;
+                    reinterpret_cast<V*>(p.region[q] + aug_off + uint64_t(p.nmax + j) * S)[off] = v;
+                }
+                const int post = pj_post[pj];
+                if (post >= 0)
+                    slab[uint64_t(pj_src[pj]) * nvec + off] = ld_vec(batch + uint64_t(post) * nvec + off);
+            });
+    }
+    trace_at(p, 7);
 
-    // Phase F (multi-rank): completion handshake. The last CTA of this rank to finish
-    // tells every requester that all pushes of step i into it have landed, then waits
-    // until every owner has done the same for us — so this launch's completion implies
-    // m'_i is complete (the promise resolution of engine.cpp:169).
+    // ---- completion handshake (multi-rank): the last CTA of this rank to finish tells
+    // every requester that all pushes of step i into it have landed, then waits until
+    // every owner has done the same for us — so this launch's completion implies m'_i is
+    // complete (the promise resolution of engine.cpp:169).
     if (do_plan && multi) {
         __threadfence_system();
         __syncthreads();
@@ -790,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_cons
                             to = true;
                             break;
                         }
-                        __nanosleep(64);
+                        __nanosleep(32);
                     }
                 }
                 if (to) {
@@ -804,6 +820,9 @@ __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_cons
             }
         }
     }
+    trace_at(p, 8);
+    if (p.trace && tid == 0)
+        atomicMax(p.trace + 15, globaltimer());
 }
 
 // ---- standalone kernels for the buffer-level API (tests / facade) ----------------------
@@ -836,22 +855,20 @@ __global__ void plan_kernel(uint64_t key, uint64_t ctr, uint32_t want, uint32_t 
     extern __shared__ uint32_t s[];
     const uint32_t NK = NW * K;
     uint32_t* pre = s;
-    uint32_t* wtot = s + NK + 1;
-    uint32_t* acc = wtot + 32;
+    uint32_t* pfx = pre + NK;
+    uint32_t* acc = pfx + NK + 1;
     for (uint32_t x = threadIdx.x; x < NK; x += blockDim.x)
         pre[x] = occ[x];
-    __syncthreads();
-    const uint32_t total = block_exclusive_scan(pre, NK, wtot);
-    const uint32_t cap_entries = min(want, total);
-    uint32_t* pl = acc + (cap_entries ? cap_entries : 1);
-    if (threadIdx.x < 32) {
-        const uint32_t c = warp_plan(key, ctr, want, pre, NK, K, acc, pl);
-        for (uint32_t j = threadIdx.x; j < 3 * c; j += 32)
-            out[j] = pl[j];
-        if (threadIdx.x == 0) {
-            *count = c;
-            *ctr_out = ctr;
-        }
+    __syncwarp();
+    const uint32_t total = warp_exclusive_scan(pre, NK, pfx);
+    const uint32_t c = warp_plan_draw(key, ctr, want, total, acc);
+    uint32_t* pl = acc + (min(want, total) ? min(want, total) : 1);
+    warp_locate(acc, c, pfx, NK, K, pl);
+    for (uint32_t j = threadIdx.x; j < 3 * c; j += 32)
+        out[j] = pl[j];
+    if (threadIdx.x == 0) {
+        *count = c;
+        *ctr_out = ctr;
     }
 }
 
@@ -906,24 +923,25 @@ __global__ void read_slots_kernel(const uint8_t* slab, const uint32_t* slab_labe
 // ---- launchers ------------------------------------------------------------------------
 
 int launch_step(const StepParams& p, uint32_t grid, void* stream) {
-    static bool attr_set = false;
-    static uint32_t attr_bytes = 0;
-    if (!attr_set || p.smem_bytes > attr_bytes) {
-        if (cudaFuncSetAttribute(drb_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static uint32_t attr_bytes[2] = {0, 0};
+    const int which = p.vec16 ? 1 : 0;
+    auto kern = p.vec16 ? drb_step_kernel<uint4> : drb_step_kernel<uint32_t>;
+    if (p.smem_bytes > attr_bytes[which]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(p.smem_bytes)) != cudaSuccess)
             return -1;
-        attr_set = true;
-        attr_bytes = p.smem_bytes;
+        attr_bytes[which] = p.smem_bytes;
     }
-    drb_step_kernel<<<grid, kThreads, p.smem_bytes, static_cast<cudaStream_t>(stream)>>>(p);
+    kern<<<grid, kThreads, p.smem_bytes, static_cast<cudaStream_t>(stream)>>>(p);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int step_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {
-    if (cudaFuncSetAttribute(drb_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_bytes)) != cudaSuccess)
-        return -1;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, drb_step_kernel, kThreads,
+    for (auto kern : {drb_step_kernel<uint4>, drb_step_kernel<uint32_t>})
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem_bytes)) != cudaSuccess)
+            return -1;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, drb_step_kernel<uint4>, kThreads,
                                                          smem_bytes) == cudaSuccess
                ? 0
                : -1;
@@ -948,12 +966,12 @@ int launch_plan(uint64_t key, uint64_t ctr, uint32_t want, uint32_t n_workers, u
                 const uint32_t* occ_dev, uint32_t* out_dev, uint32_t* count_dev,
                 uint64_t* ctr_out_dev, void* stream) {
     const uint32_t NK = n_workers * n_classes;
-    const size_t smem = (size_t(NK) + 1 + 32 + size_t(want + 1) * 4) * 4;
+    const size_t smem = (2 * size_t(NK) + 1 + size_t(want + 1) * 4) * 4;
     if (smem > 200 * 1024)
         return -1;
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    plan_kernel<<<1, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+    plan_kernel<<<1, 32, smem, static_cast<cudaStream_t>(stream)>>>(
         key, ctr, want, n_workers, n_classes, occ_dev, out_dev, count_dev, ctr_out_dev);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

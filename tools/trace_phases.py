@@ -1,0 +1,51 @@
+#!/usr/bin/env python3
+"""Per-phase timeline of the step kernel (DRB_TRACE=1): globaltimer stamps written by CTA 0
+plus the grid-wide first start / last end. Usage: python tools/trace_phases.py [config]"""
+import ctypes as C
+import os
+import sys
+
+os.environ["DRB_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2406_03285_b200 as drb  # noqa: E402
+from paper_2406_03285_b200._lib import check, lib  # noqa: E402
+from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E402
+
+NAMES = {0: "start(cta0)", 1: "loads+rendezvous", 2: "scan", 3: "select/assign/plan", 4: "jobs built",
+         5: "phase D done", 9: "copy warps: assemble share done", 6: "all: after barrier",
+         7: "merged jobs copied", 8: "end(cta0)"}
+
+
+def main():
+    cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+    K, cap, S, b, r, c = cfg["K"], cfg["cap"], cfg["S"], cfg["b"], cfg["r"], cfg["c"]
+    spec = stream_spec(K, cfg["T"], b, S, steps_per_task=100, seed=1)
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1)
+    eng = drb.engine(buf)
+    eng.start()
+    data, lab = device_ring(spec, 0, 16, "cuda:0")
+    for i in range(450):
+        eng.update((data[i % 16], lab[i % 16]))
+    torch.cuda.synchronize()
+    rows = []
+    for i in range(20):
+        eng.update((data[i % 16], lab[i % 16]))
+        t = np.zeros(16, np.uint64)
+        check(lib.drb_rb_trace_read(buf.h, t.ctypes.data))
+        rows.append(t.astype(np.int64))
+    rows = np.stack(rows)
+    t0 = rows[:, 14]
+    print(f"config {sys.argv[1] if len(sys.argv) > 1 else 'c2'}; grid={buf.launch_info()}")
+    for slot in (0, 1, 2, 3, 4, 5, 9, 6, 7, 8):
+        v = rows[:, slot] - t0
+        print(f"  {NAMES[slot]:34s} median {np.median(v) / 1000:7.2f} us")
+    print(f"  {'grid last end':34s} median {np.median(rows[:, 15] - t0) / 1000:7.2f} us")
+
+
+if __name__ == "__main__":
+    main()
