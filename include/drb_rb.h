@@ -211,6 +211,17 @@ DRB_RB_API drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_
                                  const uint32_t* labels, uint64_t label_stride, uint32_t ring,
                                  uint32_t n, uint64_t steps, uint64_t first, void* stream,
                                  void* const* step_events);
+/* The same `steps` iterations captured into a CUDA graph without running them (host
+ * launch cost paid here, once). The handle's iteration state advances as if the steps had
+ * been enqueued: launch the graph exactly once with drb_rb_graph_launch, before any
+ * further step on this handle. */
+typedef struct drb_rb_graph drb_rb_graph;
+DRB_RB_API drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_stride,
+                                           const uint32_t* labels, uint64_t label_stride,
+                                           uint32_t ring, uint32_t n, uint64_t steps,
+                                           uint64_t first, drb_rb_graph** out);
+DRB_RB_API drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream);
+DRB_RB_API drb_status drb_rb_graph_destroy(drb_rb_graph* g);
 /* Rows of m' for a completed step (blocks on that step's completion). */
 DRB_RB_API drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count);
 DRB_RB_API drb_status drb_rb_synchronize(drb_rb* h);
@@ -219,8 +230,9 @@ DRB_RB_API drb_status drb_rb_total_wait_ms(drb_rb* h, double* out);
 /* Device-side error word of the last completed step (0 = none). */
 DRB_RB_API drb_status drb_rb_device_error(drb_rb* h, uint32_t* out);
 /* Diagnostics (DRB_TRACE=1 at create): globaltimer stamps of the last step's phases in
- * CTA 0 (slots 0-9) and the grid-wide first start / last end (slots 14, 15). */
-DRB_RB_API drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out16);
+ * CTA 0 (slots 0-9), CTA 1 (slots 16-25) and the grid-wide first start / last end
+ * (slots 14, 15). out must hold 32 values. */
+DRB_RB_API drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out32);
 /* Launch configuration of the step kernel: grid CTAs, threads, dynamic smem. */
 DRB_RB_API drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads,
                                          uint32_t* smem);

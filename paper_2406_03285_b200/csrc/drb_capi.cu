@@ -138,6 +138,9 @@ struct drb_rb {
     uint32_t cur = 0;                 // state[cur] is current
     uint64_t ver = 0;                 // occupancy table version index (slot = ver % 3)
     uint32_t* report = nullptr;       // [2K+2]
+    uint32_t* plist = nullptr;        // [2][plist_words]: push lists handed between launches
+    uint32_t* wlist = nullptr;        // candidate-write list, planner -> copiers
+    uint64_t seq = 0;                 // launches issued (intra-launch flag values)
     uint32_t* mailbox = nullptr;      // host-mapped [2*kAugRing]
     uint32_t* mailbox_dev = nullptr;
     cudaEvent_t done[kAugRing] = {};  // completion of the step that last wrote each slot
@@ -196,6 +199,8 @@ StepParams base_params(drb_rb* h) {
     p.timeout_ns = h->timeout_ns;
     p.smem_bytes = h->smem_bytes;
     p.trace = h->trace;
+    p.wlist = h->wlist;
+    p.seq = h->seq++;
     return p;
 }
 
@@ -313,7 +318,10 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         int per_sm = 0;
         if (step_kernel_max_ctas_per_sm(h->smem_bytes, &per_sm) || per_sm < 1)
             fail(DRB_ERR_CONFIG, "step kernel does not fit on an SM");
+        // one planner CTA + copier CTAs, one per SM (the grid is a single wave)
         h->grid = uint32_t(h->sm_count) * uint32_t(per_sm < 2 ? per_sm : 2);
+        if (h->grid < 2)
+            h->grid = 2;
         if (const char* gs = std::getenv("DRB_GRID"))
             h->grid = uint32_t(std::strtoul(gs, nullptr, 10));
         cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
@@ -328,6 +336,9 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         cuda_check(cudaMalloc(&h->state, 2 * sizeof(DevState)), "state alloc");
         cuda_check(cudaMemset(h->state, 0, 2 * sizeof(DevState)), "memset");
         cuda_check(cudaMalloc(&h->report, (2ull * c.n_classes + 2) * 4), "report alloc");
+        cuda_check(cudaMalloc(&h->plist, 2ull * plist_words(c.world, c.rep_count) * 4), "plist alloc");
+        cuda_check(cudaMemset(h->plist, 0, 2ull * plist_words(c.world, c.rep_count) * 4), "memset");
+        cuda_check(cudaMalloc(&h->wlist, wlist_words(c.world, c.rep_count, c.max_batch) * 4ull), "wlist alloc");
         cuda_check(cudaHostAlloc(&h->mailbox, 4 * kAugRing * 4, cudaHostAllocMapped), "mailbox");
         std::memset(h->mailbox, 0, 4 * kAugRing * 4);
         cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->mailbox_dev), h->mailbox, 0), "mailbox map");
@@ -343,7 +354,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             h->samp_key[q] = derive_key(c.seed, q, DRB_PURPOSE_GLOBAL_SAMPLING, 0, 0);
         h->peers[c.rank] = h->region;
         if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
-            cuda_check(cudaMalloc(&h->trace, 16 * 8), "trace alloc");
+            cuda_check(cudaMalloc(&h->trace, 32 * 8), "trace alloc");
         if (c.world == 1)
             h->connected = true;
         cuda_check(cudaDeviceSynchronize(), "create sync");
@@ -365,6 +376,8 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaFree(h->region);
         cudaFree(h->state);
         cudaFree(h->report);
+        cudaFree(h->plist);
+        cudaFree(h->wlist);
         cudaFree(h->trace);
         cudaFree(h->stage);
         cudaFree(h->stage_labels);
@@ -615,11 +628,14 @@ drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uin
         p.tslot_in = uint32_t(h->ver % kTableRing);
         p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
         p.aslot = uint32_t(h->step % kAugRing);
+        const uint64_t pw = plist_words(h->cfg.world, h->cfg.rep_count);
+        p.plist_in = h->plist + (h->step & 1) * pw;
+        p.plist_out = h->plist + ((h->step + 1) & 1) * pw;
         p.st_in = h->state + h->cur;
         p.st_out = h->state + (h->cur ^ 1);
         p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
         if (h->trace) {
-            cuda_check(cudaMemsetAsync(h->trace, 0, 16 * 8, s), "trace reset");
+            cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
             cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
         }
         if (launch_step(p, h->grid, s))
@@ -658,6 +674,67 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
                 cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * i + 1]),
                                            stream ? static_cast<cudaStream_t>(stream) : h->stream), "event");
         }
+    });
+}
+
+}  // extern "C"
+
+struct drb_rb_graph {
+    drb_rb* h = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool launched = false;
+};
+
+extern "C" {
+
+drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_stride,
+                                const uint32_t* labels, uint64_t label_stride, uint32_t ring,
+                                uint32_t n, uint64_t steps, uint64_t first, drb_rb_graph** out) {
+    DRB_REQUIRE(h && batches && labels && ring > 0 && out);
+    *out = nullptr;
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        auto gr = std::make_unique<drb_rb_graph>();
+        gr->h = h;
+        cudaStream_t cs = nullptr;
+        cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
+        cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+        const drb_status st = drb_rb_run(h, batches, batch_stride, labels, label_stride, ring, n, steps,
+                                         first, cs, nullptr);
+        const std::string err = t_last_error;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &gr->graph);
+        cudaStreamDestroy(cs);
+        if (st != DRB_OK)
+            fail(st, err);
+        cuda_check(ce, "end capture");
+        cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
+        *out = gr.release();
+    });
+}
+
+drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream) {
+    DRB_REQUIRE(g);
+    return guarded([&] {
+        if (g->launched)
+            fail(DRB_ERR_USAGE, "graph_launch: a prepared run can be launched once");
+        device_guard dg(g->h->cfg.device);
+        cuda_check(cudaGraphLaunch(g->exec, stream ? static_cast<cudaStream_t>(stream) : g->h->stream),
+                   "graph launch");
+        g->launched = true;
+    });
+}
+
+drb_status drb_rb_graph_destroy(drb_rb_graph* g) {
+    if (!g)
+        return DRB_OK;
+    return guarded([&] {
+        device_guard dg(g->h->cfg.device);
+        if (g->exec)
+            cudaGraphExecDestroy(g->exec);
+        if (g->graph)
+            cudaGraphDestroy(g->graph);
+        delete g;
     });
 }
 
@@ -751,7 +828,7 @@ drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out16) {
             fail(DRB_ERR_USAGE, "trace_read: run with DRB_TRACE=1");
         device_guard g(h->cfg.device);
         cuda_check(cudaDeviceSynchronize(), "trace sync");
-        cuda_check(cudaMemcpy(out16, h->trace, 16 * 8, cudaMemcpyDeviceToHost), "trace copy");
+        cuda_check(cudaMemcpy(out16, h->trace, 32 * 8, cudaMemcpyDeviceToHost), "trace copy");
     });
 }
 

@@ -46,7 +46,8 @@ struct alignas(256) RegionHeader {
     uint64_t arrive[kMaxWorld];    // [w]: 1 + last step whose pushes from w into me completed
     uint64_t ticket;               // local: CTA completion tickets (last-CTA detection)
     uint32_t aug_count[4];         // local: rows of m' per ring slot (device copy)
-    uint64_t pad[13];
+    uint64_t wflag;                // local: planner -> copiers, 1 + step whose write list is ready
+    uint64_t pad[12];
 };
 
 struct RegionLayout {
@@ -81,6 +82,7 @@ struct StepParams {
     uint32_t n, c, r, nmax;
     uint64_t S;
     uint64_t step;
+    uint64_t seq;                  // launch sequence number of this handle (intra-launch flag)
     uint32_t tslot_in, tslot_out;  // table ring slots of versions i and i+1
     uint32_t aslot;                // m' ring slot of step i
     uint32_t mode;
@@ -95,6 +97,9 @@ struct StepParams {
     DevState* st_out;
     uint8_t* region[kMaxWorld];  // every rank's region base, mapped in this process
     uint64_t off_table, off_aug, off_auglab, aug_slot_bytes, auglab_slot_elems;
+    const uint32_t* plist_in;  // push list of this launch (built by the previous launch)
+    uint32_t* plist_out;       // push list for the next launch (built by the planner CTA)
+    uint32_t* wlist;           // candidate-write list of this launch (planner -> copiers)
     uint32_t* report;    // [2K + 2]: appends[K], replacements[K], totals[2]
     uint32_t* mailbox;   // host-mapped: [kAugRing] counts, [kAugRing] errors
     uint64_t timeout_ns;
@@ -102,6 +107,23 @@ struct StepParams {
     uint32_t smem_bytes;
     unsigned long long* trace;  // optional phase timestamps (CTA 0) + grid min/max, 16 slots
 };
+
+// Push list handed from launch i (leader CTA, plan(i)) to launch i+1 (all copy CTAs):
+// the owned entries of every requester's plan, one job per distinct slab slot, in a
+// deterministic order. u32 words: [0] njobs, [1] reps drawn for this rank (cnt_me),
+// [2..3] pad, src[MJ] (slab row = cls*cap+slot), ndst[MJ], dst[MJ*N] ((q << 16) | j).
+__host__ __device__ inline uint32_t plist_mj(uint32_t N, uint32_t r) { return N * (r ? r : 1); }
+__host__ __device__ inline uint32_t plist_words(uint32_t N, uint32_t r) {
+    const uint32_t mj = plist_mj(N, r);
+    return 4 + mj * (2 + N);
+}
+
+// Candidate-write list, planner -> copiers within one launch. u32 words: [0] n_win,
+// [1..1+2*nmax) (batch row, slab row) pairs, then post[MJ] (int: batch row overwriting
+// push job j's slot after the push read, or -1).
+__host__ __device__ inline uint32_t wlist_words(uint32_t N, uint32_t r, uint32_t nmax) {
+    return 1 + 2 * nmax + plist_mj(N, r);
+}
 
 // Dynamic shared-memory carve-up of the step kernel (sizes in 4-byte words).
 struct SmemLayout {
@@ -131,7 +153,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t N, uint32_t K, uint32
     s.pj_ndst = TAKE(nr);
     s.pj_dst = TAKE(nr * N);
     s.maskw = TAKE((nmax + 31) / 32);
-    s.misc = TAKE(200);
+    s.misc = TAKE(208);
     s.words = w;
 #undef TAKE
     return s;

@@ -318,11 +318,6 @@ __device__ uint32_t warp_exclusive_scan(const uint32_t* a, uint32_t n, uint32_t*
     return total;
 }
 
-// Named barrier 1 over the first `nthreads` threads (the control warps).
-__device__ __forceinline__ void ctl_sync(uint32_t nthreads) {
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
 template <typename V>
 __device__ __forceinline__ V ld_vec(const V* p) {
     if constexpr (sizeof(V) == 16) {
@@ -354,8 +349,9 @@ __device__ __forceinline__ void warp_copy(uint32_t lo, uint32_t hi, uint32_t* co
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t gv = base + u * 32 + lane;
-            if (gv < hi)
-                r[u] = ld_vec(src(gv));
+            const V* a = gv < hi ? src(gv) : nullptr;
+            if (a)
+                r[u] = ld_vec(a);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -366,9 +362,10 @@ __device__ __forceinline__ void warp_copy(uint32_t lo, uint32_t hi, uint32_t* co
     }
 }
 
+// Diagnostics: CTA 0 (planner) stamps slots 0-9, CTA 1 (first copier) slots 16-25.
 __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
-    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0)
-        p.trace[slot] = globaltimer();
+    if (p.trace && blockIdx.x < 2 && (threadIdx.x & 31) == 0)
+        p.trace[slot + 16 * blockIdx.x] = globaltimer();
 }
 
 }  // namespace
@@ -380,41 +377,66 @@ enum : uint32_t {
     kMiscJobs = 2,      // push-job counter
     kMiscWin = 3,       // candidate-write job counter
     kMiscChunkA = 4,    // assemble-copy chunk counter
-    kMiscChunkB = 5,    // job-copy chunk counter
+    kMiscChunkB = 5,    // push-copy chunk counter
+    kMiscChunkC = 6,    // candidate-write chunk counter
+    kMiscK = 7,         // candidates selected this round
+    kMiscCtr = 200,     // 4 words: cand_ctr, evict_ctr (u64 each)
+    kMiscApp = 204,     // appends
     kMiscScratch = 8,   // 32 words: eviction-draw fallback scratch
     kMiscState = 40,    // DevState snapshot (sizeof(DevState)/4 words)
     kMiscMaskP = 72,    // 128 words: push-leader ballot masks (N*r <= 4096)
-    kMiscWords = 200,
+    kMiscWords = 208,
 };
 static_assert(sizeof(DevState) % 8 == 0 && 40 + sizeof(DevState) / 4 <= 72, "DevState layout");
 
-// One engine iteration on one rank; see the file comment. Warp roles in every CTA:
-//   control warps [0, CW), CW = N+2, synchronised by named barrier 1:
-//     warp 0      S1 selection + S2 assignment of this rank; leader CTA: round-(i+1)
-//                 state, occupancy publish, slab labels, report
-//     warp 1+q    S4 plan(i-1) of requester q (every rank replicates every requester's
-//                 global-sampling stream so owners know what to push)
-//     warp N+1    prefix of the global view (for locate), concurrent with the draws
-//   copy warps [CW, 16): start the control-independent m_i -> m'_i copy immediately.
-// Then all warps drain the assemble chunks, barrier, and copy the merged candidate-write
-// and push jobs. Multi-rank launches end with the completion handshake.
+// Named barrier helpers (barrier 0 is __syncthreads).
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One engine iteration i on one rank: a cooperative launch (all CTAs co-resident),
+// software-pipelined across launches.
+//
+//  CTA 0 ("planner", no bulk copies):
+//    S1+S2 of round i (select + assign) and the candidate-write list of round i, handed
+//    to the copiers through global memory + a release/acquire flag; then round-(i+1)
+//    state, occupancy row v=i+1 published (local + peers), m'_i labels/count; then the
+//    size rendezvous for v=i+1, S4 plan(i) for every requester, and the PUSH LIST for
+//    launch i+1 (owned plan entries, one job per distinct slab slot).
+//  CTAs 1.. ("copiers", all 16 warps copy):
+//    phase 1 — m_i -> m'_i rows (needs nothing) and the pushes of plan(i-1) read at
+//              version i (push list built by launch i-1);
+//    phase 2 — after the planner's flag: candidate writes of round i; a slot that a
+//              push of this launch read is overwritten by the SAME CTA that pushed it
+//              (read-before-write: exact-horizon semantics), the rest spread over the grid.
+// No decision of round i gates the copy of the (b + r) rows of m'_i.
 template <typename V>
 __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_constant__ StepParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const SmemLayout L = smem_layout(p.N, p.K, p.nmax, p.r);
-    uint32_t* pre = sm + L.pre;   // raw view occupancy [N*K]
-    uint32_t* pfx = sm + L.pfx;   // exclusive prefix [N*K+1]
+    uint32_t* pre = sm + L.pre;   // planner: view occupancy v=i+1 [N*K]
+    uint32_t* pfx = sm + L.pfx;   // planner: exclusive prefix [N*K+1]
     uint32_t* occ = sm + L.occ;   // own occupancy, updated in place by S2
     uint32_t* lab = sm + L.lab;
     uint32_t* sel = sm + L.sel;
     uint32_t* cand_l = sm + L.cand_l;
     uint32_t* cand_slot = sm + L.cand_slot;
-    uint32_t* win = sm + L.win;   // candidate-write jobs: (batch row, slab row) pairs
+    uint32_t* win = sm + L.win;   // copiers: candidate-write jobs (batch row, slab row)
     uint32_t* kind = sm + L.idx;  // per candidate: 1 = append (idx is free after S1)
     uint32_t* plan = sm + L.plan;
     uint32_t* cnt = sm + L.cnt;
     uint32_t* acc = sm + L.acc;
-    uint32_t* pj_src = sm + L.pj_src;
+    uint32_t* pj_src = sm + L.pj_src;   // this launch's push jobs
     int* pj_post = reinterpret_cast<int*>(sm + L.pj_post);
     uint32_t* pj_ndst = sm + L.pj_ndst;
     uint32_t* pj_dst = sm + L.pj_dst;
@@ -422,368 +444,436 @@ __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_cons
     DevState* st = reinterpret_cast<DevState*>(misc + kMiscState);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool leader = blockIdx.x == 0;
+    const unsigned lt = (1u << lane) - 1u;
+    const bool planner = blockIdx.x == 0;
     const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap, r = p.r;
     const uint32_t NK = N * K;
+    const uint32_t MJ = plist_mj(N, r);
     const uint64_t S = p.S;
     const uint32_t nvec = static_cast<uint32_t>(S / sizeof(V));
     RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     const bool do_update = p.mode & kModeUpdate;
     const bool do_assemble = p.mode & kModeAssemble;
-    const bool do_plan = (p.mode & kModePlan) && p.step > 0;
+    const bool do_plan = p.mode & kModePlan;                   // build the push list for i+1
+    const bool do_push = do_plan && p.step > 0 && p.plist_in;  // pushes of plan(i-1)
     const bool do_publish = p.mode & kModePublish;
     const bool multi = (p.mode & kModePeers) && N > 1;
-    const uint32_t CW = N + 2;  // control warps
-    const uint32_t CT = CW * 32;
-    const bool ctl = warp < CW;
-    const uint32_t part = blockIdx.x, parts = gridDim.x;
+    const uint32_t part = blockIdx.x - 1, parts = gridDim.x - 1;  // copier partition
+    const uint32_t aslot_next = (p.aslot + 1) % kAugRing;
+    const uint32_t n_push = do_push ? __ldcg(p.plist_in) : 0;    // uniform, L2 hit
 
     uint8_t* my_aug = p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
-    uint32_t* my_auglab = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
-                          uint64_t(p.aslot) * p.auglab_slot_elems;
+    uint32_t* auglab = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab);
     const uint32_t row0 = p.nmax - n;  // m'_i occupies rows [nmax-n, nmax+|reps|)
+    const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
+                          uint64_t(p.tslot_in) * NK;
 
     trace_at(p, 0);
     if (p.trace && tid == 0)
         atomicMin(p.trace + 14, globaltimer());
     if (tid < kMiscState)
         misc[tid] = 0;
-    __syncthreads();
 
-    // The control-independent copy m_i -> m'_i rows [row0, row0+n), claimed in chunks.
-    auto assemble = [&]() {
-        constexpr int U = sizeof(V) == 16 ? 8 : 16;
-        const uint32_t tv = n * nvec;
-        const uint32_t lo = static_cast<uint32_t>(uint64_t(tv) * part / parts);
-        const uint32_t hi = static_cast<uint32_t>(uint64_t(tv) * (part + 1) / parts);
-        const V* src = reinterpret_cast<const V*>(p.batch);
-        V* dst = reinterpret_cast<V*>(my_aug + uint64_t(row0) * S);
-        warp_copy<V, U>(lo, hi, &misc[kMiscChunkA], [&](uint32_t gv) { return src + gv; },
-                        [&](uint32_t gv, const V& v) { dst[gv] = v; });
-    };
-
-    if (ctl) {
-        auto sync = [CT] { ctl_sync(CT); };
-        // ---- one round trip: state, own occupancy row, labels (and the view if N == 1) --
-        const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
-                              uint64_t(p.tslot_in) * NK;
+    if (planner) {
+        // =============================== planner CTA ================================
         if (tid < sizeof(DevState) / 8)
-            reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.st_in) + tid);
-        #pragma unroll 1
-        for (uint32_t x = tid; x < K; x += CT) {
-            const uint32_t o = __ldcg(tin + uint64_t(me) * K + x);
-            occ[x] = o;
-            if (!multi)
-                pre[x] = o;  // N == 1: the view is the own row
-        }
-        #pragma unroll 1
-        for (uint32_t x = tid; x < n; x += CT) {
+            reinterpret_cast<uint64_t*>(st)[tid] =
+                __ldcg(reinterpret_cast<const uint64_t*>(p.st_in) + tid);
+#pragma unroll 1
+        for (uint32_t x = tid; x < K; x += kThreads)
+            occ[x] = __ldcg(tin + uint64_t(me) * K + x);
+#pragma unroll 1
+        for (uint32_t x = tid; x < n_push; x += kThreads)
+            pj_src[x] = __ldcg(p.plist_in + 4 + x);
+        int any_bad = 0;
+#pragma unroll 1
+        for (uint32_t x = tid; x < n; x += kThreads) {
             const uint32_t l = __ldg(p.labels + x);
             lab[x] = l;
-            if (l >= K)
-                misc[kMiscBad] = 1;
+            any_bad |= l >= K;
         }
-        // size rendezvous (size_table.cpp:66-100 / engine.cpp:152), bounded by timeout_ns
-        if (do_plan && multi && tid == 0) {
-            const uint64_t t0 = globaltimer();
-            for (uint32_t w = 0; w < N; ++w) {
-                if (w == me)
-                    continue;
-                while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step) {
-                    if (globaltimer() - t0 > p.timeout_ns) {
-                        misc[kMiscErr] = DRB_ERR_TRANSPORT;
-                        break;
-                    }
-                    __nanosleep(32);
-                }
-            }
-        }
-        sync();
-        if (do_plan && multi) {
-            #pragma unroll 1
-            for (uint32_t x = tid; x < NK; x += CT)
-                pre[x] = __ldcg(tin + x);
-            sync();
-        }
-        trace_at(p, 1);
-        const bool dead = st->error != 0;  // sticky: a failed round kills the engine
-        const bool bad = misc[kMiscBad] != 0;  // usage_error before any draw (:44-47)
-        const uint32_t k = (!dead && do_update && !bad && n > 0) ? min(p.c, n) : 0;
+        const bool bad = __syncthreads_or(any_bad) != 0;  // usage_error before any draw (:44-47)
+        const bool dead = st->error != 0;       // sticky: a failed round kills the engine
         const bool planning = do_plan && !dead;
-
+        trace_at(p, 1);
         if (warp == 0) {
-            // ---- S1 + S2 of this rank; the leader writes round-(i+1) state right away --
+            // ---- S1 + S2 of round i -------------------------------------------------------
+            const uint32_t k = (!dead && do_update && !bad && n > 0) ? min(p.c, n) : 0;
             uint64_t cand_ctr = (p.mode & kModeCtrParams) ? p.cand_ctr0 : st->cand_ctr;
             uint64_t evict_ctr = (p.mode & kModeCtrParams) ? p.evict_ctr0 : st->evict_ctr;
             uint32_t appends = 0;
             if (k > 0) {
+                trace_at(p, 10);
                 warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
+                trace_at(p, 11);
                 warp_assign(p.evict_key, evict_ctr, cap, k, sel, lab, occ, cand_l, cand_slot,
                             misc + kMiscScratch, kind, appends);
+                trace_at(p, 12);
             }
+            // ---- candidate-write list for the copiers: winners (last writer of each
+            //      (class, slot) in selection order) not read by a push of this launch;
+            //      a pushed winner slot becomes that push job's trailing overwrite -------
+            uint32_t* wl = p.wlist;
+            uint32_t n_win = 0;
+#pragma unroll 1
+            for (uint32_t base = 0; base < k; base += 32) {
+                const uint32_t t = base + lane;
+                bool w = false;
+                uint32_t key = 0;
+                if (t < k) {
+                    key = cand_l[t] * cap + cand_slot[t];
+                    w = true;
+#pragma unroll 1
+                    for (uint32_t u = t + 1; u < k && w; ++u)
+                        w = cand_l[u] * cap + cand_slot[u] != key;
+#pragma unroll 1
+                    for (uint32_t x = 0; x < n_push && w; ++x)
+                        w = pj_src[x] != key;
+                }
+                const unsigned m = __ballot_sync(kFull, w);
+                if (w) {
+                    const uint32_t pos = n_win + __popc(m & lt);
+                    wl[1 + 2 * pos] = sel[t];
+                    wl[2 + 2 * pos] = key;
+                }
+                n_win += __popc(m);
+            }
+#pragma unroll 1
+            for (uint32_t x = lane; x < n_push; x += 32) {
+                int post = -1;
+#pragma unroll 1
+                for (int t = static_cast<int>(k) - 1; t >= 0; --t)
+                    if (cand_l[t] * cap + cand_slot[t] == pj_src[x]) {
+                        post = static_cast<int>(sel[t]);
+                        break;
+                    }
+                wl[1 + 2 * p.nmax + x] = static_cast<uint32_t>(post);
+            }
+            if (lane == 0)
+                wl[0] = n_win;
+            __syncwarp();  // orders every lane's list writes before lane 0's release
+            if (lane == 0)
+                st_release_gpu(&hdr->wflag, p.seq + 1);
             trace_at(p, 2);
-            if (leader) {
-                const uint32_t err = dead ? st->error
-                                          : (misc[kMiscErr] | ((bad && do_update) ? DRB_ERR_USAGE : 0u));
-                if (lane == 0) {
-                    DevState* o = p.st_out;
-                    o->cand_ctr = cand_ctr;
-                    o->evict_ctr = evict_ctr;
-                    o->version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
-                    o->total = st->total + appends;
-                    o->cross_class = st->cross_class;
-                    o->error = err;
-                    if (!planning)
-                        for (uint32_t q = 0; q < N; ++q)
-                            o->samp_ctr[q] = st->samp_ctr[q];
-                }
-                #pragma unroll 1
-                for (uint32_t t = lane; t < k; t += 32)  // stored label == class
-                    p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
-                if (do_assemble)
-                    #pragma unroll 1
-                    for (uint32_t x = lane; x < n; x += 32)
-                        my_auglab[row0 + x] = lab[x];
-                if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
-                    uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
-                                     uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
-                    #pragma unroll 1
-                    for (uint32_t x = lane; x < K; x += 32)
-                        tout[x] = occ[x];
-                    if (multi) {
-                        for (uint32_t w = 0; w < N; ++w) {
-                            if (w == me)
-                                continue;
-                            uint32_t* pt = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
-                                           uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
-                            #pragma unroll 1
-                            for (uint32_t x = lane; x < K; x += 32)
-                                pt[x] = occ[x];
-                        }
-                        __threadfence_system();
-                        __syncwarp();
-                        if (lane < N && lane != me) {
-                            RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
-                            st_release_sys(&peer->occ_flag[me], p.step + 1);
-                        }
-                    }
-                }
-                if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
-                    #pragma unroll 1
-                    for (uint32_t x = lane; x < 2 * K + 2; x += 32)
-                        p.report[x] = 0;
-                    __syncwarp();
-                    __threadfence_block();
-                    for (uint32_t t = lane; t < k; t += 32) {
-                        const bool app = kind[t] != 0;
-                        atomicAdd(&p.report[(app ? 0 : K) + cand_l[t]], 1u);
-                        atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
-                    }
-                }
-                if (p.mailbox && lane == 0 && err)
-                    reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
+
+            // ---- round-(i+1) state, slab labels, publish, m'_i labels, report ----------
+            const uint32_t err = dead ? st->error : ((bad && do_update) ? DRB_ERR_USAGE : 0u);
+            if (lane == 0) {
+                DevState* o = p.st_out;
+                o->cand_ctr = cand_ctr;
+                o->evict_ctr = evict_ctr;
+                o->version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
+                o->total = st->total + appends;
+                o->cross_class = st->cross_class;
+                o->error = err;
+                if (!planning)
+                    for (uint32_t q = 0; q < N; ++q)
+                        o->samp_ctr[q] = st->samp_ctr[q];
             }
-        } else if (warp <= N) {
-            // ---- S4 draws of requester q ------------------------------------------------
-            if (planning) {
+#pragma unroll 1
+            for (uint32_t t = lane; t < k; t += 32)  // stored label == class
+                p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
+            if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
+                uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
+                                 uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
+#pragma unroll 1
+                for (uint32_t x = lane; x < K; x += 32)
+                    tout[x] = occ[x];
+                if (multi) {
+#pragma unroll 1
+                    for (uint32_t w = 0; w < N; ++w) {
+                        if (w == me)
+                            continue;
+                        uint32_t* pt = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
+                                       uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
+#pragma unroll 1
+                        for (uint32_t x = lane; x < K; x += 32)
+                            pt[x] = occ[x];
+                    }
+                    __threadfence_system();
+                    __syncwarp();
+                    if (lane < N && lane != me) {
+                        RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
+                        st_release_sys(&peer->occ_flag[me], p.step + 1);
+                    }
+                }
+            }
+            if (do_assemble) {  // m'_i labels of rows [row0, row0+n) and its row count
+                uint32_t* al = auglab + uint64_t(p.aslot) * p.auglab_slot_elems;
+#pragma unroll 1
+                for (uint32_t x = lane; x < n; x += 32)
+                    al[row0 + x] = lab[x];
+                if (lane == 0) {
+                    const uint32_t mine = do_push ? __ldcg(p.plist_in + 1) : 0;
+                    hdr->aug_count[p.aslot] = n + mine;
+                    if (p.mailbox) {
+                        volatile uint32_t* mb = p.mailbox;
+                        mb[p.aslot] = n + mine;
+                        mb[kAugRing + p.aslot] = dead ? st->error : 0u;
+                    }
+                }
+            }
+            if (p.mailbox && lane == 0 && err)
+                reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
+            if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
+#pragma unroll 1
+                for (uint32_t x = lane; x < 2 * K + 2; x += 32)
+                    p.report[x] = 0;
+                __syncwarp();
+                __threadfence_block();
+#pragma unroll 1
+                for (uint32_t t = lane; t < k; t += 32) {
+                    const bool app = kind[t] != 0;
+                    atomicAdd(&p.report[(app ? 0 : K) + cand_l[t]], 1u);
+                    atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
+                }
+            }
+#pragma unroll 1
+            for (uint32_t x = lane; x < K; x += 32)  // own row of the view v = i+1
+                pre[uint64_t(me) * K + x] = occ[x];
+        } else if (planning && multi && warp == 1) {
+            // size rendezvous for v = i+1 (size_table.cpp:66-100 / engine.cpp:152)
+            if (lane == 0) {
+                const uint64_t t0 = globaltimer();
+                for (uint32_t w = 0; w < N; ++w) {
+                    if (w == me)
+                        continue;
+                    while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step + 1) {
+                        if (globaltimer() - t0 > p.timeout_ns) {
+                            misc[kMiscErr] = DRB_ERR_TRANSPORT;
+                            break;
+                        }
+                        __nanosleep(32);
+                    }
+                }
+            }
+            __syncwarp();
+            const uint32_t* tv1 = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
+                                  uint64_t(p.tslot_out) * NK;
+#pragma unroll 1
+            for (uint32_t x = lane; x < NK; x += 32)
+                if (x / K != me)
+                    pre[x] = __ldcg(tv1 + x);
+        }
+        __syncthreads();
+        trace_at(p, 3);
+        if (planning) {
+            // ---- S4 plan(i) for every requester (warps 1..N), prefix (warp N+1) --------
+            if (warp >= 1 && warp <= N) {
                 const uint32_t q = warp - 1;
                 uint64_t ctr = st->samp_ctr[q];
                 const uint32_t total = warp_sum(pre, NK);
                 const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
                 if (lane == 0) {
                     cnt[q] = c;
-                    if (leader)
-                        p.st_out->samp_ctr[q] = ctr;
+                    p.st_out->samp_ctr[q] = ctr;
+                }
+            } else if (warp == N + 1) {
+                warp_exclusive_scan(pre, NK, pfx);
+            }
+            __syncthreads();
+            if (warp >= 1 && warp <= N) {
+                const uint32_t q = warp - 1;
+                warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
+                if (q == me && do_assemble) {  // labels of m'_{i+1}'s reps (stored label == class)
+                    uint32_t* al = auglab + uint64_t(aslot_next) * p.auglab_slot_elems;
+#pragma unroll 1
+                    for (uint32_t j = lane; j < cnt[q]; j += 32)
+                        al[p.nmax + j] = plan[3 * (q * r + j) + 1];
                 }
             }
-        } else if (planning) {
-            warp_exclusive_scan(pre, NK, pfx);  // warp N+1
-        }
-        sync();
-        trace_at(p, 3);
-        if (planning && warp >= 1 && warp <= N) {
-            const uint32_t q = warp - 1;
-            warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
-            if (leader && q == me && do_assemble) {
-                #pragma unroll 1
-                for (uint32_t j = lane; j < cnt[q]; j += 32)
-                    my_auglab[p.nmax + j] = plan[3 * (q * r + j) + 1];  // stored label == class
-                if (lane == 0) {
-                    hdr->aug_count[p.aslot] = n + cnt[q];
-                    if (p.mailbox) {
-                        volatile uint32_t* mb = p.mailbox;
-                        mb[p.aslot] = n + cnt[q];
-                        mb[kAugRing + p.aslot] = misc[kMiscErr];
-                    }
-                }
-            }
-        }
-        if (leader && !planning && warp == 0 && lane == 0 && do_assemble) {
-            hdr->aug_count[p.aslot] = n;
-            if (p.mailbox) {
-                volatile uint32_t* mb = p.mailbox;
-                mb[p.aslot] = n;
-                mb[kAugRing + p.aslot] = dead ? st->error : misc[kMiscErr];
-            }
-        }
-        sync();
-        trace_at(p, 4);
-
-        // ---- job construction (identical, deterministic numbering in every CTA: the
-        // grid splits the job space by index, so no atomics decide the order) -------------
-        // push job: one per distinct owned slot over all requesters' plans, numbered in
-        // entry order; its first entry collects every (q, j) that drew the slot; if this
-        // round's winning candidate (last writer in selection order) targets the slot, the
-        // job ends with that overwrite (read at version i, then write — the exact horizon).
-        // candidate-write job: winning candidates whose slot no push job reads this round.
-        const uint32_t NR = planning ? N * r : 0;
-        uint32_t* maskP = misc + kMiscMaskP;  // ballot masks of push leaders, per 32 entries
-        uint32_t* maskW = sm + L.maskw;       // ballot masks of candidate writes
-        for (uint32_t base = warp * 32; base < NR; base += CT) {
-            const uint32_t e = base + lane;
-            bool lead = false;
-            if (e < NR) {
-                const uint32_t q = e / r, j = e - q * r;
-                if (j < cnt[q] && plan[3 * e] == me) {
-                    const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-                    lead = true;
-                    for (uint32_t q2 = 0; q2 < q && lead; ++q2)
-                        for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
-                            const uint32_t* x = plan + 3 * (q2 * r + j2);
-                            if (x[0] == me && x[1] == cls && x[2] == slot) {
-                                lead = false;
-                                break;
+            __syncthreads();
+            trace_at(p, 4);
+            // ---- push list for launch i+1: owned entries, one job per distinct slot,
+            //      numbered in entry order (ballots), dests = every (q, j) drawing it ----
+            const uint32_t NR = N * r;
+            uint32_t* maskP = misc + kMiscMaskP;
+            uint32_t* out = p.plist_out;
+            for (uint32_t base = warp * 32; base < NR; base += kThreads) {
+                const uint32_t e = base + lane;
+                bool lead = false;
+                if (e < NR) {
+                    const uint32_t q = e / r, j = e - q * r;
+                    if (j < cnt[q] && plan[3 * e] == me) {
+                        const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
+                        lead = true;
+#pragma unroll 1
+                        for (uint32_t q2 = 0; q2 < q && lead; ++q2)
+#pragma unroll 1
+                            for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
+                                const uint32_t* x = plan + 3 * (q2 * r + j2);
+                                if (x[0] == me && x[1] == cls && x[2] == slot) {
+                                    lead = false;
+                                    break;
+                                }
                             }
-                        }
-                }
-            }
-            const unsigned m = __ballot_sync(kFull, lead);
-            if (lane == 0)
-                maskP[base >> 5] = m;
-        }
-        for (uint32_t base = warp * 32; base < k; base += CT) {
-            const uint32_t t = base + lane;
-            bool w = false;
-            if (t < k) {
-                const uint32_t cl = cand_l[t], cs = cand_slot[t];
-                w = true;
-                for (uint32_t u = t + 1; u < k && w; ++u)
-                    w = !(cand_l[u] == cl && cand_slot[u] == cs);
-                for (uint32_t e = 0; e < NR && w; ++e) {
-                    const uint32_t q = e / r;
-                    w = !((e - q * r) < cnt[q] && plan[3 * e] == me && plan[3 * e + 1] == cl &&
-                          plan[3 * e + 2] == cs);
-                }
-            }
-            const unsigned m = __ballot_sync(kFull, w);
-            if (lane == 0)
-                maskW[base >> 5] = m;
-        }
-        sync();
-        const unsigned lt = (1u << lane) - 1u;
-        for (uint32_t base = warp * 32; base < NR; base += CT) {
-            const unsigned m = maskP[base >> 5];
-            if (!((m >> lane) & 1u))
-                continue;
-            uint32_t pj = __popc(m & lt);
-            for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
-                pj += __popc(maskP[b2]);
-            const uint32_t e = base + lane, q = e / r, j = e - q * r;
-            const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-            uint32_t nd = 0;
-            pj_dst[pj * N + nd++] = (q << 16) | j;
-            for (uint32_t q2 = q + 1; q2 < N; ++q2)
-                for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
-                    const uint32_t* x = plan + 3 * (q2 * r + j2);
-                    if (x[0] == me && x[1] == cls && x[2] == slot) {
-                        pj_dst[pj * N + nd++] = (q2 << 16) | j2;
-                        break;
                     }
                 }
-            pj_ndst[pj] = nd;
-            pj_src[pj] = cls * cap + slot;
-            int post = -1;
-            for (int t = static_cast<int>(k) - 1; t >= 0; --t)
-                if (cand_l[t] == cls && cand_slot[t] == slot) {
-                    post = static_cast<int>(sel[t]);
-                    break;
+                const unsigned m = __ballot_sync(kFull, lead);
+                if (lane == 0)
+                    maskP[base >> 5] = m;
+            }
+            __syncthreads();
+            for (uint32_t base = warp * 32; base < NR; base += kThreads) {
+                const unsigned m = maskP[base >> 5];
+                if (!((m >> lane) & 1u))
+                    continue;
+                uint32_t pj = __popc(m & lt);
+#pragma unroll 1
+                for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
+                    pj += __popc(maskP[b2]);
+                const uint32_t e = base + lane, q = e / r, j = e - q * r;
+                const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
+                uint32_t nd = 0;
+                out[4 + 2 * MJ + pj * N + nd++] = (q << 16) | j;
+#pragma unroll 1
+                for (uint32_t q2 = q + 1; q2 < N; ++q2)
+#pragma unroll 1
+                    for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
+                        const uint32_t* x = plan + 3 * (q2 * r + j2);
+                        if (x[0] == me && x[1] == cls && x[2] == slot) {
+                            out[4 + 2 * MJ + pj * N + nd++] = (q2 << 16) | j2;
+                            break;
+                        }
+                    }
+                out[4 + pj] = cls * cap + slot;
+                out[4 + MJ + pj] = nd;
+            }
+            if (tid == 0) {
+                uint32_t np = 0;
+#pragma unroll 1
+                for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
+                    np += __popc(maskP[b2]);
+                out[0] = np;
+                out[1] = cnt[me];
+                if (misc[kMiscErr]) {  // rendezvous failure: the engine is dead from here
+                    atomicOr(&p.st_out->error, misc[kMiscErr]);
+                    if (p.mailbox)
+                        reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[kMiscErr];
                 }
-            pj_post[pj] = post;
-        }
-        for (uint32_t base = warp * 32; base < k; base += CT) {
-            const unsigned m = maskW[base >> 5];
-            if (!((m >> lane) & 1u))
-                continue;
-            uint32_t w = __popc(m & lt);
-            for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
-                w += __popc(maskW[b2]);
-            const uint32_t t = base + lane;
-            win[2 * w] = sel[t];
-            win[2 * w + 1] = cand_l[t] * cap + cand_slot[t];
-        }
-        if (tid == 0) {
-            uint32_t np = 0, nw = 0;
-            for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
-                np += __popc(maskP[b2]);
-            for (uint32_t b2 = 0; b2 < (k + 31) / 32; ++b2)
-                nw += __popc(maskW[b2]);
-            misc[kMiscJobs] = np;
-            misc[kMiscWin] = nw;
+            }
+        } else if (do_plan && tid == 0 && p.plist_out) {
+            p.plist_out[0] = 0;
+            p.plist_out[1] = 0;
         }
         trace_at(p, 5);
-    }
-    // copy warps arrive here at once; control warps help drain when done
-    if (do_assemble)
-        assemble();
-    trace_at(p, 9);
-    __syncthreads();
-    trace_at(p, 6);
-
-    // ---- merged candidate-write + push jobs (all warps) --------------------------------
-    const uint32_t n_win = misc[kMiscWin];
-    const uint32_t n_push = misc[kMiscJobs];
-    if (n_win + n_push) {
-        constexpr int U = sizeof(V) == 16 ? 4 : 8;
-        const uint32_t tv = (n_win + n_push) * nvec;
-        const uint32_t lo = static_cast<uint32_t>(uint64_t(tv) * part / parts);
-        const uint32_t hi = static_cast<uint32_t>(uint64_t(tv) * (part + 1) / parts);
+    } else {
+        // =============================== copier CTAs ================================
+        // Phase 1 is ONE chunked vector space: [assemble: n rows of m_i][pushes: n_push
+        // jobs]; each CTA owns a fixed slice of it (the hazard overwrites of phase 2 reuse
+        // that slice), warps claim 32*U-vector chunks dynamically inside the slice.
         const V* batch = reinterpret_cast<const V*>(p.batch);
         V* slab = reinterpret_cast<V*>(p.slab);
-        const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
-        warp_copy<V, U>(
-            lo, hi, &misc[kMiscChunkB],
-            [&](uint32_t gv) -> const V* {
-                const uint32_t job = gv / nvec, off = gv - job * nvec;
-                if (job < n_win)
+        const uint32_t av = do_assemble ? n * nvec : 0;   // assemble vectors
+        const uint32_t tv1 = av + n_push * nvec;
+        const uint32_t lo1 = static_cast<uint32_t>(uint64_t(tv1) * part / parts);
+        const uint32_t hi1 = static_cast<uint32_t>(uint64_t(tv1) * (part + 1) / parts);
+        if (warp == 0 && lo1 < hi1 && hi1 > av) {
+            // this CTA's slice reaches the push jobs: stage them (overlaps the copy)
+#pragma unroll 1
+            for (uint32_t x = lane; x < n_push; x += 32) {
+                pj_src[x] = __ldcg(p.plist_in + 4 + x);
+                const uint32_t nd = __ldcg(p.plist_in + 4 + MJ + x);
+                pj_ndst[x] = nd;
+#pragma unroll 1
+                for (uint32_t d = 0; d < nd; ++d)
+                    pj_dst[x * N + d] = __ldcg(p.plist_in + 4 + 2 * MJ + x * N + d);
+            }
+            __syncwarp();
+            __threadfence_block();
+        }
+        __syncthreads();  // chunk counters zeroed; push jobs staged
+        {
+            constexpr int U = sizeof(V) == 16 ? 8 : 16;
+            V* asm_dst = reinterpret_cast<V*>(my_aug + uint64_t(row0) * S);
+            const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
+            warp_copy<V, U>(
+                lo1, hi1, &misc[kMiscChunkA],
+                [&](uint32_t gv) -> const V* {
+                    if (gv < av)
+                        return batch + gv;
+                    const uint32_t pv = gv - av, job = pv / nvec, off = pv - job * nvec;
+                    return slab + uint64_t(pj_src[job]) * nvec + off;
+                },
+                [&](uint32_t gv, const V& v) {
+                    if (gv < av) {
+                        asm_dst[gv] = v;
+                        return;
+                    }
+                    const uint32_t pv = gv - av, job = pv / nvec, off = pv - job * nvec;
+                    const uint32_t nd = pj_ndst[job];
+#pragma unroll 1
+                    for (uint32_t x = 0; x < nd; ++x) {
+                        const uint32_t e = pj_dst[job * N + x];
+                        const uint32_t q = e >> 16, j = e & 0xffffu;
+                        reinterpret_cast<V*>(p.region[q] + aug_off + uint64_t(p.nmax + j) * S)[off] = v;
+                    }
+                });
+        }
+        trace_at(p, 6);
+        // ---- wait for the planner's candidate-write list -------------------------------
+        if (tid == 0 && (do_update || do_push)) {
+            const uint64_t t0 = globaltimer();
+            while (ld_acquire_gpu(&hdr->wflag) < p.seq + 1) {
+                if (globaltimer() - t0 > p.timeout_ns)
+                    break;  // planner lost: leave the slab untouched (engine error set by host)
+                __nanosleep(20);
+            }
+        }
+        __syncthreads();
+        const uint32_t* wl = p.wlist;
+        const uint32_t n_win = (do_update || do_push) ? __ldcg(wl) : 0;
+        // the push jobs in this CTA's slice (hazard overwrites) and the candidate writes
+        const uint32_t pj_lo = lo1 > av ? (lo1 - av) / nvec : 0;
+        const uint32_t pj_hi = hi1 > av ? (hi1 - av + nvec - 1) / nvec : 0;
+#pragma unroll 1
+        for (uint32_t x = tid; x < 2 * n_win; x += kThreads)
+            win[x] = __ldcg(wl + 1 + x);
+#pragma unroll 1
+        for (uint32_t x = pj_lo + tid; x < pj_hi; x += kThreads)
+            pj_post[x] = static_cast<int>(__ldcg(wl + 1 + 2 * p.nmax + x));
+        __syncthreads();
+        trace_at(p, 7);
+        // ---- phase 2, ONE pass: [hazard overwrites of this CTA's push slice (post >= 0)]
+        //      then [candidate writes spread over the grid] --------------------------------
+        {
+            constexpr int U = sizeof(V) == 16 ? 4 : 8;
+            const uint32_t plo = lo1 > av ? lo1 - av : 0, phi = hi1 > av ? hi1 - av : 0;
+            const uint32_t nh = phi - plo;  // this CTA's pushed vectors (candidates for posts)
+            const uint32_t tvw = n_win * nvec;
+            const uint32_t wlo = static_cast<uint32_t>(uint64_t(tvw) * part / parts);
+            const uint32_t whi = static_cast<uint32_t>(uint64_t(tvw) * (part + 1) / parts);
+            const uint32_t tot = nh + (whi - wlo);
+            warp_copy<V, U>(
+                0, tot, &misc[kMiscChunkC],
+                [&](uint32_t gv) -> const V* {
+                    if (gv < nh) {
+                        const uint32_t pv = plo + gv, job = pv / nvec, off = pv - job * nvec;
+                        const int post = pj_post[job];
+                        return post >= 0 ? batch + uint64_t(post) * nvec + off : nullptr;
+                    }
+                    const uint32_t wv = wlo + gv - nh, job = wv / nvec, off = wv - job * nvec;
                     return batch + uint64_t(win[2 * job]) * nvec + off;
-                return slab + uint64_t(pj_src[job - n_win]) * nvec + off;
-            },
-            [&](uint32_t gv, const V& v) {
-                const uint32_t job = gv / nvec, off = gv - job * nvec;
-                if (job < n_win) {
+                },
+                [&](uint32_t gv, const V& v) {
+                    if (gv < nh) {
+                        const uint32_t pv = plo + gv, job = pv / nvec, off = pv - job * nvec;
+                        if (pj_post[job] >= 0)
+                            slab[uint64_t(pj_src[job]) * nvec + off] = v;
+                        return;
+                    }
+                    const uint32_t wv = wlo + gv - nh, job = wv / nvec, off = wv - job * nvec;
                     slab[uint64_t(win[2 * job + 1]) * nvec + off] = v;
-                    return;
-                }
-                const uint32_t pj = job - n_win;
-                const uint32_t nd = pj_ndst[pj];
-                #pragma unroll 1
-                for (uint32_t x = 0; x < nd; ++x) {
-                    const uint32_t e = pj_dst[pj * N + x];
-                    const uint32_t q = e >> 16, j = e & 0xffffu;
-                    reinterpret_cast<V*>(p.region[q] + aug_off + uint64_t(p.nmax + j) * S)[off] = v;
-                }
-                const int post = pj_post[pj];
-                if (post >= 0)
-                    slab[uint64_t(pj_src[pj]) * nvec + off] = ld_vec(batch + uint64_t(post) * nvec + off);
-            });
+                });
+        }
+        trace_at(p, 8);
     }
-    trace_at(p, 7);
 
     // ---- completion handshake (multi-rank): the last CTA of this rank to finish tells
     // every requester that all pushes of step i into it have landed, then waits until
     // every owner has done the same for us — so this launch's completion implies m'_i is
     // complete (the promise resolution of engine.cpp:169).
-    if (do_plan && multi) {
+    if (do_push && multi) {
         __threadfence_system();
         __syncthreads();
         if (tid == 0) {
@@ -820,7 +910,6 @@ __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_cons
             }
         }
     }
-    trace_at(p, 8);
     if (p.trace && tid == 0)
         atomicMax(p.trace + 15, globaltimer());
 }
@@ -932,8 +1021,19 @@ int launch_step(const StepParams& p, uint32_t grid, void* stream) {
             return -1;
         attr_bytes[which] = p.smem_bytes;
     }
-    kern<<<grid, kThreads, p.smem_bytes, static_cast<cudaStream_t>(stream)>>>(p);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    // Cooperative: the copier CTAs wait for the planner CTA's flag inside the launch, so
+    // every CTA must be co-resident (one CTA per SM, a single wave).
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p) == cudaSuccess ? 0 : -1;
 }
 
 int step_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {

@@ -295,6 +295,27 @@ class augmented_batch:
         return d[self.n:], l[self.n:]
 
 
+class prepared_run:
+    """A captured multi-iteration run (CUDA graph). Keeps its input rings alive."""
+
+    def __init__(self, g: C.c_void_p, keep):
+        self.g, self._keep = g, keep
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        check(lib.drb_rb_graph_launch(self.g, C.c_void_p(stream.cuda_stream) if stream is not None else None))
+
+    def close(self) -> None:
+        if self.g and self.g.value:
+            check(lib.drb_rb_graph_destroy(self.g))
+            self.g = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class engine:
     """engine(cfg, rank, buffer, ...) (engine.hpp:53-93) over a rehearsal_buffer handle."""
 
@@ -345,6 +366,19 @@ class engine:
         check(lib.drb_rb_run(self.buffer.h, data_ring.data_ptr(), data_ring.stride(0), label_ring.data_ptr(),
                              label_ring.stride(0), B, n, steps, first, C.c_void_p(s.cuda_stream), ev))
         self.iteration += steps
+
+    def prepare_run(self, data_ring: torch.Tensor, label_ring: torch.Tensor, steps: int,
+                    first: int = 0) -> "prepared_run":
+        """Capture `steps` iterations (as run()) into a CUDA graph; launch it once, in order."""
+        B, n = int(data_ring.shape[0]), int(data_ring.shape[1])
+        if label_ring.shape[0] != B:
+            raise _lib.usage_error("prepare_run: data and label rings must have the same length")
+        g = C.c_void_p()
+        check(lib.drb_rb_graph_prepare(self.buffer.h, data_ring.data_ptr(), data_ring.stride(0),
+                                       label_ring.data_ptr(), label_ring.stride(0), B, n, steps, first,
+                                       C.byref(g)))
+        self.iteration += steps
+        return prepared_run(g, (data_ring, label_ring))
 
     def synchronize(self) -> None:
         check(lib.drb_rb_synchronize(self.buffer.h))

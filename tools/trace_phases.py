@@ -16,9 +16,11 @@ import paper_2406_03285_b200 as drb  # noqa: E402
 from paper_2406_03285_b200._lib import check, lib  # noqa: E402
 from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E402
 
-NAMES = {0: "start(cta0)", 1: "loads+rendezvous", 2: "scan", 3: "select/assign/plan", 4: "jobs built",
-         5: "phase D done", 9: "copy warps: assemble share done", 6: "all: after barrier",
-         7: "merged jobs copied", 8: "end(cta0)"}
+NAMES = {0: "planner start", 1: "planner loads", 10: "planner S1 start", 11: "planner S1 done",
+         12: "planner S2 done", 2: "planner write list published", 3: "planner rendezvous v=i+1",
+         4: "planner plan(i)+locate", 5: "planner push list written",
+         16: "copier start", 22: "copier phase 1 done", 23: "copier write list loaded",
+         24: "copier phase 2 done"}
 
 
 def main():
@@ -35,16 +37,26 @@ def main():
     rows = []
     for i in range(20):
         eng.update((data[i % 16], lab[i % 16]))
-        t = np.zeros(16, np.uint64)
+        t = np.zeros(32, np.uint64)
         check(lib.drb_rb_trace_read(buf.h, t.ctypes.data))
         rows.append(t.astype(np.int64))
     rows = np.stack(rows)
     t0 = rows[:, 14]
     print(f"config {sys.argv[1] if len(sys.argv) > 1 else 'c2'}; grid={buf.launch_info()}")
-    for slot in (0, 1, 2, 3, 4, 5, 9, 6, 7, 8):
+    for slot in (0, 1, 10, 11, 12, 2, 3, 4, 5, 16, 22, 23, 24):
         v = rows[:, slot] - t0
         print(f"  {NAMES[slot]:34s} median {np.median(v) / 1000:7.2f} us")
     print(f"  {'grid last end':34s} median {np.median(rows[:, 15] - t0) / 1000:7.2f} us")
+    # host submission rate of the native multi-step loop (no sync inside)
+    import time
+    lab_ring = lab
+    torch.cuda.synchronize()
+    t0h = time.perf_counter()
+    eng.run(data, lab_ring, 2000)
+    t1h = time.perf_counter()
+    torch.cuda.synchronize()
+    t2h = time.perf_counter()
+    print(f"  host submit {1e6 * (t1h - t0h) / 2000:.2f} us/step, wall incl. drain {1e6 * (t2h - t0h) / 2000:.2f} us/step (trace on)")
 
 
 if __name__ == "__main__":
