@@ -233,6 +233,10 @@ DRB_RB_API drb_status drb_rb_device_error(drb_rb* h, uint32_t* out);
  * CTA 0 (slots 0-9), CTA 1 (slots 16-25) and the grid-wide first start / last end
  * (slots 14, 15). out must hold 32 values. */
 DRB_RB_API drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out32);
+/* Diagnostics (DRB_TIMELINE=<steps> at create): per step s (ring of `steps`), per kernel
+ * kind (0 sel, 1 plan, 2 copy) the grid-wide [first start, last end] globaltimer stamps at
+ * out[(s*3 + kind)*2 + {0,1}]. out = NULL queries *steps only. */
+DRB_RB_API drb_status drb_rb_timeline_read(drb_rb* h, uint64_t* out, uint32_t* steps);
 /* Launch configuration of the step kernel: grid CTAs, threads, dynamic smem. */
 DRB_RB_API drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads,
                                          uint32_t* smem);

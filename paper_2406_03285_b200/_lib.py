@@ -141,6 +141,7 @@ def _load():
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),
         "drb_rb_trace_read": (st, [vp, vp]),
+        "drb_rb_timeline_read": (st, [vp, vp, P(u32)]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)

@@ -122,10 +122,12 @@ struct dev_tmp {
 struct drb_rb {
     drb_rb_config cfg{};
     RegionLayout layout{};
-    uint32_t smem_bytes = 0;
-    uint32_t grid = 0;
+    uint32_t copy_smem = 0;           // dynamic smem of the copy kernel
+    uint32_t grid = 0;                // copy-kernel CTAs (one wave)
     int sm_count = 0;
-    cudaStream_t stream = nullptr;    // default stream of the handle
+    cudaStream_t stream = nullptr;    // default stream of the handle (copy kernel)
+    cudaStream_t s_sel = nullptr;     // selection chain sel(i)
+    cudaStream_t s_plan = nullptr;    // planning chain plan(i)
     cudaStream_t h2d = nullptr;       // host-path input copies
     cudaStream_t d2h = nullptr;       // host-path output copies
     uint8_t* slab = nullptr;          // [K][cap][S]
@@ -134,25 +136,35 @@ struct drb_rb {
     uint8_t* peers[kMaxWorld] = {};   // every rank's region, mapped here
     bool peer_opened[kMaxWorld] = {};
     bool connected = false;
-    DevState* state = nullptr;        // [2]
-    uint32_t cur = 0;                 // state[cur] is current
+    SelState* sel = nullptr;          // [2], sel[cur_sel] is current
+    PlanState* plan = nullptr;        // [2], plan[cur_plan] is current
+    uint32_t cur_sel = 0, cur_plan = 0;
     uint64_t ver = 0;                 // occupancy table version index (slot = ver % 3)
     uint32_t* report = nullptr;       // [2K+2]
-    uint32_t* plist = nullptr;        // [2][plist_words]: push lists handed between launches
-    uint32_t* wlist = nullptr;        // candidate-write list, planner -> copiers
-    uint64_t seq = 0;                 // launches issued (intra-launch flag values)
-    uint32_t* mailbox = nullptr;      // host-mapped [2*kAugRing]
+    uint32_t* plist = nullptr;        // [kListRing][plist_words]: P_i, plan(i-1) -> copy(i)
+    uint32_t* wlist = nullptr;        // [kListRing][wlist_words]: W_i, sel(i) -> copy(i)
+    uint32_t* mailbox = nullptr;      // host-mapped [4*kAugRing]
     uint32_t* mailbox_dev = nullptr;
-    cudaEvent_t done[kAugRing] = {};  // completion of the step that last wrote each slot
+    static constexpr int kEv = 8;
+    cudaEvent_t ev_user[kEv] = {}, ev_sel[kEv] = {}, ev_plan[kEv] = {}, ev_copy[kEv] = {};
+    cudaEvent_t done[kAugRing] = {};  // completion of the copy that last wrote each m' slot
     cudaEvent_t in_free[2] = {};      // host path: staging slot reusable
     cudaEvent_t h2d_done[2] = {};
     uint8_t* stage = nullptr;         // host path: device staging [2][max_batch][S]
     uint32_t* stage_labels = nullptr; // [2][max_batch]
     uint64_t cand_key = 0, evict_key = 0, samp_key[kMaxWorld] = {};
     uint64_t step = 0;
+    uint64_t seq = 0;
+    uint64_t dep_floor = 0;           // steps below this completed before a graph capture
+    cudaStream_t last_copy_stream = nullptr;
+    uint64_t ver0 = 0;                // engine: table version / state parities at start()
+    uint32_t sel_par0 = 0, plan_par0 = 0;
+    bool use_pdl = false;             // DRB_PDL=1
     bool started = false, shut_down = false;
     double wait_ms = 0.0;
     unsigned long long* trace = nullptr;  // DRB_TRACE=1: per-step phase timestamps
+    unsigned long long* timeline = nullptr;  // DRB_TIMELINE=<steps>: per-kernel start/end
+    uint32_t timeline_steps = 0;
     uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
 };
 
@@ -197,10 +209,17 @@ StepParams base_params(drb_rb* h) {
     p.report = h->report;
     p.mailbox = h->mailbox_dev;
     p.timeout_ns = h->timeout_ns;
-    p.smem_bytes = h->smem_bytes;
+    p.smem_bytes = h->copy_smem;
     p.trace = h->trace;
-    p.wlist = h->wlist;
+    p.timeline = h->timeline;
+    p.timeline_steps = h->timeline_steps ? h->timeline_steps : 1;
     p.seq = h->seq++;
+    p.tslot_in = uint32_t(h->ver % kTableRing);
+    p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
+    p.sel_in = h->sel + h->cur_sel;
+    p.sel_out = h->sel + (h->cur_sel ^ 1);
+    p.plan_in = h->plan + h->cur_plan;
+    p.plan_out = h->plan + (h->cur_plan ^ 1);
     return p;
 }
 
@@ -302,29 +321,28 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: world * rep_count must be <= 4096");
         if (uint64_t(c.world) * c.n_classes * c.per_class_cap >= (1ull << 31))
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K*cap must be < 2^31 slots");
-        const SmemLayout sl = smem_layout(c.world, c.n_classes, c.max_batch, c.rep_count);
-        if (uint64_t(sl.words) * 4 > 200 * 1024)
+        const uint32_t plan_bytes = plan_smem_bytes(c.world, c.n_classes, c.rep_count);
+        if (plan_bytes > 200 * 1024 || sel_smem_bytes(c.n_classes, c.max_batch) > 200 * 1024)
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K too large for the on-chip view (" +
-                                     std::to_string(sl.words * 4) + " B shared memory)");
+                                     std::to_string(plan_bytes) + " B shared memory)");
         auto h = new drb_rb();
         std::unique_ptr<drb_rb> guard_h(h);
         h->cfg = c;
         h->layout = region_layout(c.world, c.n_classes, c.sample_bytes, c.max_batch, c.rep_count);
-        h->smem_bytes = sl.words * 4;
+        h->copy_smem = copy_smem(c.world, c.rep_count, c.max_batch).words * 4;
         if (const char* t = std::getenv("DRB_TIMEOUT_MS"))
             h->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
         device_guard g(c.device);
         cuda_check(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, c.device), "sm count");
         int per_sm = 0;
-        if (step_kernel_max_ctas_per_sm(h->smem_bytes, &per_sm) || per_sm < 1)
-            fail(DRB_ERR_CONFIG, "step kernel does not fit on an SM");
-        // one planner CTA + copier CTAs, one per SM (the grid is a single wave)
-        h->grid = uint32_t(h->sm_count) * uint32_t(per_sm < 2 ? per_sm : 2);
-        if (h->grid < 2)
-            h->grid = 2;
+        if (copy_kernel_max_ctas_per_sm(h->copy_smem, &per_sm) || per_sm < 1)
+            fail(DRB_ERR_CONFIG, "copy kernel does not fit on an SM");
+        h->grid = uint32_t(h->sm_count);  // one copy CTA per SM: a single wave
         if (const char* gs = std::getenv("DRB_GRID"))
             h->grid = uint32_t(std::strtoul(gs, nullptr, 10));
         cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&h->s_sel, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&h->s_plan, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
         const uint64_t slab_bytes = uint64_t(c.n_classes) * c.per_class_cap * c.sample_bytes;
@@ -333,17 +351,23 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         cuda_check(cudaMemset(h->slab_labels, 0, uint64_t(c.n_classes) * c.per_class_cap * 4), "memset");
         cuda_check(cudaMalloc(&h->region, h->layout.bytes), "region alloc");
         cuda_check(cudaMemset(h->region, 0, h->layout.bytes), "memset");
-        cuda_check(cudaMalloc(&h->state, 2 * sizeof(DevState)), "state alloc");
-        cuda_check(cudaMemset(h->state, 0, 2 * sizeof(DevState)), "memset");
+        cuda_check(cudaMalloc(&h->sel, 2 * sizeof(SelState)), "state alloc");
+        cuda_check(cudaMemset(h->sel, 0, 2 * sizeof(SelState)), "memset");
+        cuda_check(cudaMalloc(&h->plan, 2 * sizeof(PlanState)), "state alloc");
+        cuda_check(cudaMemset(h->plan, 0, 2 * sizeof(PlanState)), "memset");
         cuda_check(cudaMalloc(&h->report, (2ull * c.n_classes + 2) * 4), "report alloc");
-        cuda_check(cudaMalloc(&h->plist, 2ull * plist_words(c.world, c.rep_count) * 4), "plist alloc");
-        cuda_check(cudaMemset(h->plist, 0, 2ull * plist_words(c.world, c.rep_count) * 4), "memset");
-        cuda_check(cudaMalloc(&h->wlist, wlist_words(c.world, c.rep_count, c.max_batch) * 4ull), "wlist alloc");
+        cuda_check(cudaMalloc(&h->plist, uint64_t(kListRing) * plist_words(c.world, c.rep_count) * 4), "plist alloc");
+        cuda_check(cudaMemset(h->plist, 0, uint64_t(kListRing) * plist_words(c.world, c.rep_count) * 4), "memset");
+        cuda_check(cudaMalloc(&h->wlist, uint64_t(kListRing) * wlist_words(c.max_batch) * 4), "wlist alloc");
+        cuda_check(cudaMemset(h->wlist, 0, uint64_t(kListRing) * wlist_words(c.max_batch) * 4), "memset");
         cuda_check(cudaHostAlloc(&h->mailbox, 4 * kAugRing * 4, cudaHostAllocMapped), "mailbox");
         std::memset(h->mailbox, 0, 4 * kAugRing * 4);
         cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->mailbox_dev), h->mailbox, 0), "mailbox map");
         for (auto& e : h->done)
             cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        for (int i = 0; i < drb_rb::kEv; ++i)
+            for (cudaEvent_t* e : {&h->ev_user[i], &h->ev_sel[i], &h->ev_plan[i], &h->ev_copy[i]})
+                cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
         for (int i = 0; i < 2; ++i) {
             cuda_check(cudaEventCreateWithFlags(&h->in_free[i], cudaEventDisableTiming), "event");
             cuda_check(cudaEventCreateWithFlags(&h->h2d_done[i], cudaEventDisableTiming), "event");
@@ -353,6 +377,20 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         for (uint32_t q = 0; q < kMaxWorld; ++q)
             h->samp_key[q] = derive_key(c.seed, q, DRB_PURPOSE_GLOBAL_SAMPLING, 0, 0);
         h->peers[c.rank] = h->region;
+        if (const char* tl = std::getenv("DRB_TIMELINE")) {
+            h->timeline_steps = uint32_t(std::strtoul(tl, nullptr, 10));
+            if (h->timeline_steps) {
+                cuda_check(cudaMalloc(&h->timeline, h->timeline_steps * 6ull * 8), "timeline alloc");
+                std::vector<unsigned long long> init(h->timeline_steps * 6ull);
+                for (size_t x = 0; x < init.size(); x += 2) {
+                    init[x] = ~0ull;
+                    init[x + 1] = 0;
+                }
+                cuda_check(cudaMemcpy(h->timeline, init.data(), init.size() * 8, cudaMemcpyHostToDevice), "timeline init");
+            }
+        }
+        if (const char* pd = std::getenv("DRB_PDL"); pd && pd[0] == '1')
+            h->use_pdl = true;
         if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
             cuda_check(cudaMalloc(&h->trace, 32 * 8), "trace alloc");
         if (c.world == 1)
@@ -374,21 +412,28 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaFree(h->slab);
         cudaFree(h->slab_labels);
         cudaFree(h->region);
-        cudaFree(h->state);
+        cudaFree(h->sel);
+        cudaFree(h->plan);
         cudaFree(h->report);
         cudaFree(h->plist);
         cudaFree(h->wlist);
         cudaFree(h->trace);
+        cudaFree(h->timeline);
         cudaFree(h->stage);
         cudaFree(h->stage_labels);
         cudaFreeHost(h->mailbox);
         for (auto e : h->done)
             cudaEventDestroy(e);
+        for (int i = 0; i < drb_rb::kEv; ++i)
+            for (cudaEvent_t e : {h->ev_user[i], h->ev_sel[i], h->ev_plan[i], h->ev_copy[i]})
+                cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
             cudaEventDestroy(h->in_free[i]);
             cudaEventDestroy(h->h2d_done[i]);
         }
         cudaStreamDestroy(h->stream);
+        cudaStreamDestroy(h->s_sel);
+        cudaStreamDestroy(h->s_plan);
         cudaStreamDestroy(h->h2d);
         cudaStreamDestroy(h->d2h);
         delete h;
@@ -400,8 +445,8 @@ drb_status drb_rb_update_buffer(drb_rb* h, const void* batch, const uint32_t* la
                                 drb_insertion_report* report) {
     DRB_REQUIRE(h && cand && evict && ((batch && labels) || n == 0));
     return guarded([&] {
-        if (h->started && h->cfg.world > 1)
-            fail(DRB_ERR_USAGE, "update_buffer: not allowed while a multi-rank engine is running");
+        if (h->started)
+            fail(DRB_ERR_USAGE, "update_buffer: the buffer is driven by its engine once started");
         if (n > h->cfg.max_batch)
             fail(DRB_ERR_USAGE, "update_buffer: batch larger than max_batch");
         device_guard g(h->cfg.device);
@@ -415,16 +460,15 @@ drb_status drb_rb_update_buffer(drb_rb* h, const void* batch, const uint32_t* la
         p.cand_ctr0 = cand->ctr;
         p.evict_ctr0 = evict->ctr;
         p.mode = kModeUpdate | kModeReport | kModeCtrParams | kModePublish;
-        p.tslot_in = uint32_t(h->ver % kTableRing);
-        p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
-        p.st_in = h->state + h->cur;
-        p.st_out = h->state + (h->cur ^ 1);
+        p.wlist = h->wlist;
+        p.plist_in = nullptr;
+        p.plist_out = nullptr;
         p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
         p.mailbox = nullptr;
-        if (launch_step(p, h->grid, h->stream))
-            fail(DRB_ERR_INTERNAL, std::string("step launch failed: ") + cudaGetErrorString(cudaGetLastError()));
-        DevState st{};
-        cuda_check(cudaMemcpyAsync(&st, p.st_out, sizeof st, cudaMemcpyDeviceToHost, h->stream), "state copy");
+        if (launch_sel(p, h->stream) || launch_copy(p, h->grid, h->stream, false))
+            fail(DRB_ERR_INTERNAL, std::string("update launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        SelState st{};
+        cuda_check(cudaMemcpyAsync(&st, p.sel_out, sizeof st, cudaMemcpyDeviceToHost, h->stream), "state copy");
         std::vector<uint32_t> rep(2ull * h->cfg.n_classes + 2);
         cuda_check(cudaMemcpyAsync(rep.data(), h->report, rep.size() * 4, cudaMemcpyDeviceToHost, h->stream), "report copy");
         cuda_check(cudaStreamSynchronize(h->stream), "update_buffer");
@@ -433,7 +477,7 @@ drb_status drb_rb_update_buffer(drb_rb* h, const void* batch, const uint32_t* la
             // (rehearsal_buffer.cpp:44-47): discard the produced state.
             fail(DRB_ERR_USAGE, "update_buffer: label out of range (K=" + std::to_string(h->cfg.n_classes) + ")");
         }
-        h->cur ^= 1;
+        h->cur_sel ^= 1;
         h->ver += 1;
         cand->ctr = st.cand_ctr;
         evict->ctr = st.evict_ctr;
@@ -459,7 +503,7 @@ drb_status drb_rb_read_slots(drb_rb* h, const drb_read_request* requests, uint32
         const uint32_t* occ = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_table) +
                               (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
                               uint64_t(h->cfg.rank) * h->cfg.n_classes;
-        cuda_check(cudaStreamSynchronize(h->stream), "read_slots order");
+        cuda_check(cudaDeviceSynchronize(), "read_slots order");
         if (launch_read_slots(h->slab, h->slab_labels, occ, h->cfg.n_classes, h->cfg.per_class_cap,
                               h->cfg.sample_bytes, d_req.as<uint32_t>(), count, substitute->key,
                               substitute->ctr, static_cast<uint8_t*>(out), out_labels,
@@ -475,13 +519,13 @@ drb_status drb_rb_snapshot(drb_rb* h, uint32_t* per_class, uint64_t* version) {
     DRB_REQUIRE(h && per_class && version);
     return guarded([&] {
         device_guard g(h->cfg.device);
-        cuda_check(cudaStreamSynchronize(h->stream), "snapshot order");
+        cuda_check(cudaDeviceSynchronize(), "snapshot order");
         const uint32_t* occ = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_table) +
                               (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
                               uint64_t(h->cfg.rank) * h->cfg.n_classes;
         cuda_check(cudaMemcpy(per_class, occ, h->cfg.n_classes * 4ull, cudaMemcpyDeviceToHost), "snapshot");
-        DevState st{};
-        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        SelState st{};
+        cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
         *version = st.version;
     });
 }
@@ -490,9 +534,9 @@ drb_status drb_rb_total_stored(drb_rb* h, uint64_t* out) {
     DRB_REQUIRE(h && out);
     return guarded([&] {
         device_guard g(h->cfg.device);
-        cuda_check(cudaStreamSynchronize(h->stream), "order");
-        DevState st{};
-        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        cuda_check(cudaDeviceSynchronize(), "order");
+        SelState st{};
+        cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
         *out = st.total;
     });
 }
@@ -501,9 +545,9 @@ drb_status drb_rb_cross_class_evictions(drb_rb* h, uint64_t* out) {
     DRB_REQUIRE(h && out);
     return guarded([&] {
         device_guard g(h->cfg.device);
-        cuda_check(cudaStreamSynchronize(h->stream), "order");
-        DevState st{};
-        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
+        cuda_check(cudaDeviceSynchronize(), "order");
+        SelState st{};
+        cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
         *out = st.cross_class;
     });
 }
@@ -589,6 +633,9 @@ drb_status drb_rb_start(drb_rb* h) {
         if (!h->connected)
             fail(DRB_ERR_USAGE, "engine: multi-rank handle not connected");
         h->started = true;
+        h->ver0 = h->ver - h->step;  // iteration i uses table version ver0 + i
+        h->sel_par0 = h->cur_sel;
+        h->plan_par0 = h->cur_plan;
     });
 }
 
@@ -605,53 +652,128 @@ drb_status drb_rb_shutdown(drb_rb* h) {
     });
 }
 
-drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n,
-                       void* stream, drb_aug* out) {
-    DRB_REQUIRE(h && out && ((batch && labels) || n == 0));
-    return guarded([&] {
-        if (h->shut_down)
-            fail(DRB_ERR_USAGE, "engine: update after shutdown");
-        if (!h->started)
-            fail(DRB_ERR_USAGE, "engine: update before start");
-        if (n > h->cfg.max_batch)
-            fail(DRB_ERR_USAGE, "engine: batch larger than max_batch");
-        check_engine_alive(h);
-        device_guard g(h->cfg.device);
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
-        StepParams p = base_params(h);
-        p.n = n;
-        p.batch = static_cast<const uint8_t*>(batch);
-        p.labels = labels;
-        p.step = h->step;
-        p.mode = kModeUpdate | kModeAssemble | kModePlan | kModePublish |
-                 (h->cfg.world > 1 ? kModePeers : 0u);
-        p.tslot_in = uint32_t(h->ver % kTableRing);
-        p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
-        p.aslot = uint32_t(h->step % kAugRing);
-        const uint64_t pw = plist_words(h->cfg.world, h->cfg.rep_count);
-        p.plist_in = h->plist + (h->step & 1) * pw;
-        p.plist_out = h->plist + ((h->step + 1) & 1) * pw;
-        p.st_in = h->state + h->cur;
-        p.st_out = h->state + (h->cur ^ 1);
-        p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
-        if (h->trace) {
-            cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
-            cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
-        }
-        if (launch_step(p, h->grid, s))
-            fail(DRB_ERR_INTERNAL, std::string("step launch failed: ") + cudaGetErrorString(cudaGetLastError()));
-        cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
-        h->cur ^= 1;
-        h->ver += 1;
+namespace {
+
+// Parameters of engine iteration i (every slot / parity is a function of i, so the three
+// kernels of an iteration may be issued at different times).
+StepParams iter_params(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n) {
+    StepParams p = base_params(h);
+    const uint64_t v = h->ver0 + i;
+    p.tslot_in = uint32_t(v % kTableRing);
+    p.tslot_out = uint32_t((v + 1) % kTableRing);
+    p.sel_in = h->sel + ((h->sel_par0 + i) & 1);
+    p.sel_out = h->sel + ((h->sel_par0 + i + 1) & 1);
+    p.plan_in = h->plan + ((h->plan_par0 + i) & 1);
+    p.plan_out = h->plan + ((h->plan_par0 + i + 1) & 1);
+    p.n = n;
+    p.batch = static_cast<const uint8_t*>(batch);
+    p.labels = labels;
+    p.step = i;
+    p.seq = i;
+    p.mode = kModeUpdate | kModeAssemble | kModePlan | kModePublish | (h->cfg.world > 1 ? kModePeers : 0u);
+    p.aslot = uint32_t(i % kAugRing);
+    const uint64_t pw = plist_words(h->cfg.world, h->cfg.rep_count);
+    const uint64_t ww = wlist_words(h->cfg.max_batch);
+    p.plist_in = h->plist + (i % kListRing) * pw;         // P_i, built by plan(i-1)
+    p.plist_out = h->plist + ((i + 1) % kListRing) * pw;  // P_{i+1}, built by plan(i)
+    p.wlist = h->wlist + (i % kListRing) * ww;            // W_i
+    p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
+    return p;
+}
+
+constexpr int kE = drb_rb::kEv;
+inline int ev_of(uint64_t i) { return int(i % kE); }
+
+// sel(i) on s_sel: W slot i%4 free once copy(i-4) read it; table slot (i+1)%6 (own row
+// v=i+1) free once plan(i-4) read it (peers' rows are ordered by the copy handshake);
+// optionally after the caller's prior work on `caller` (m_i produced, m'_{i-3} consumed).
+void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
+                 cudaStream_t caller, bool wait_caller) {
+    StepParams p = iter_params(h, i, batch, labels, n);
+    if (wait_caller) {
+        cuda_check(cudaEventRecord(h->ev_user[ev_of(i)], caller), "event");
+        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_user[ev_of(i)], 0), "wait");
+    }
+    if (i >= h->dep_floor + 4) {
+        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - 4)], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_plan[ev_of(i - 4)], 0), "wait");
+    }
+    if (launch_sel(p, h->s_sel))
+        fail(DRB_ERR_INTERNAL, std::string("sel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    cuda_check(cudaEventRecord(h->ev_sel[ev_of(i)], h->s_sel), "event");
+    h->ver = h->ver0 + i + 1;
+    h->cur_sel = uint32_t((h->sel_par0 + i + 1) & 1);
+}
+
+// plan(i) on s_plan: own row v=i+1 from sel(i); P slot (i+1)%4 free once copy(i-3) read it.
+void enqueue_plan(drb_rb* h, uint64_t i) {
+    StepParams p = iter_params(h, i, nullptr, nullptr, 0);
+    cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_sel[ev_of(i)], 0), "wait");
+    if (i >= h->dep_floor + 3)
+        cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_copy[ev_of(i - 3)], 0), "wait");
+    if (launch_plan_next(p, h->s_plan))
+        fail(DRB_ERR_INTERNAL, std::string("plan launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    cuda_check(cudaEventRecord(h->ev_plan[ev_of(i)], h->s_plan), "event");
+    h->cur_plan = uint32_t((h->plan_par0 + i + 1) & 1);
+}
+
+// copy(i) on `s`: W_i from sel(i), P_i from plan(i-1), slab writes of round i-1 from copy(i-1).
+void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
+                  cudaStream_t s, bool first_of_run, drb_aug* out) {
+    StepParams p = iter_params(h, i, batch, labels, n);
+    if (h->trace) {
+        cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
+        cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
+    }
+    cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i)], 0), "wait");
+    const bool have1 = i >= h->dep_floor + 1;
+    if (have1)
+        cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i - 1)], 0), "wait");
+    // (measured: PDL between copies delays the event-gated plan chain; off by default)
+    const bool pdl = h->use_pdl && !first_of_run && s == h->last_copy_stream && have1;
+    if (have1 && s != h->last_copy_stream)
+        cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i - 1)], 0), "wait");
+    if (launch_copy(p, h->grid, s, pdl))
+        fail(DRB_ERR_INTERNAL, std::string("copy launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    cuda_check(cudaEventRecord(h->ev_copy[ev_of(i)], s), "event");
+    cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
+    h->last_copy_stream = s;
+    if (out) {
         out->n = n;
         out->ring_slot = p.aslot;
-        out->step = h->step;
+        out->step = i;
         const uint32_t row0 = h->cfg.max_batch - n;
         out->data = h->region + h->layout.off_aug + uint64_t(p.aslot) * h->layout.aug_slot_bytes +
                     uint64_t(row0) * h->cfg.sample_bytes;
         out->labels = reinterpret_cast<uint32_t*>(h->region + h->layout.off_auglab) +
                       uint64_t(p.aslot) * p.auglab_slot_elems + row0;
-        h->step += 1;
+    }
+    h->step = i + 1;
+}
+
+void check_step_args(drb_rb* h, uint32_t n) {
+    if (h->shut_down)
+        fail(DRB_ERR_USAGE, "engine: update after shutdown");
+    if (!h->started)
+        fail(DRB_ERR_USAGE, "engine: update before start");
+    if (n > h->cfg.max_batch)
+        fail(DRB_ERR_USAGE, "engine: batch larger than max_batch");
+    check_engine_alive(h);
+}
+
+}  // namespace
+
+drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n,
+                       void* stream, drb_aug* out) {
+    DRB_REQUIRE(h && out && ((batch && labels) || n == 0));
+    return guarded([&] {
+        check_step_args(h, n);
+        device_guard g(h->cfg.device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        const uint64_t i = h->step;
+        enqueue_sel(h, i, batch, labels, n, s, true);
+        enqueue_plan(h, i);
+        enqueue_copy(h, i, batch, labels, n, s, true, out);
     });
 }
 
@@ -660,19 +782,32 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
                       void* stream, void* const* step_events) {
     DRB_REQUIRE(h && batches && labels && ring > 0);
     return guarded([&] {
+        check_step_args(h, n);
+        device_guard g(h->cfg.device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
         const auto* b = static_cast<const uint8_t*>(batches);
-        drb_aug aug{};
-        for (uint64_t i = 0; i < steps; ++i) {
-            const uint64_t j = (first + i) % ring;
+        auto bat = [&](uint64_t k) { return b + ((first + k) % ring) * batch_stride; };
+        auto lab = [&](uint64_t k) { return labels + ((first + k) % ring) * label_stride; };
+        const uint64_t i0 = h->step, end = i0 + steps;
+        if (steps == 0)
+            return;
+        // Skewed issue order (software pipeline over a resident input ring): sel runs two
+        // iterations ahead, plan one, so neither chain waits behind a copy in launch order.
+        // Only the first iteration waits for the caller's prior work.
+        enqueue_sel(h, i0, bat(0), lab(0), n, s, true);
+        if (i0 + 1 < end)
+            enqueue_sel(h, i0 + 1, bat(1), lab(1), n, s, false);
+        enqueue_plan(h, i0);
+        for (uint64_t i = i0; i < end; ++i) {
+            if (i + 2 < end)
+                enqueue_sel(h, i + 2, bat(i + 2 - i0), lab(i + 2 - i0), n, s, false);
+            if (i + 1 < end)
+                enqueue_plan(h, i + 1);
             if (step_events)
-                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * i]),
-                                           stream ? static_cast<cudaStream_t>(stream) : h->stream), "event");
-            const drb_status st = drb_rb_step(h, b + j * batch_stride, labels + j * label_stride, n, stream, &aug);
-            if (st != DRB_OK)
-                fail(st, t_last_error);
+                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * (i - i0)]), s), "event");
+            enqueue_copy(h, i, bat(i - i0), lab(i - i0), n, s, i == i0, nullptr);
             if (step_events)
-                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * i + 1]),
-                                           stream ? static_cast<cudaStream_t>(stream) : h->stream), "event");
+                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * (i - i0) + 1]), s), "event");
         }
     });
 }
@@ -697,18 +832,30 @@ drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_s
         device_guard g(h->cfg.device);
         auto gr = std::make_unique<drb_rb_graph>();
         gr->h = h;
+        // everything issued so far completes first, so the captured steps depend only on
+        // each other (no waits on events recorded outside the capture)
+        cuda_check(cudaDeviceSynchronize(), "capture prologue");
+        h->dep_floor = h->step;
         cudaStream_t cs = nullptr;
         cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
         cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
-        const drb_status st = drb_rb_run(h, batches, batch_stride, labels, label_stride, ring, n, steps,
-                                         first, cs, nullptr);
+        drb_status st = drb_rb_run(h, batches, batch_stride, labels, label_stride, ring, n, steps,
+                                   first, cs, nullptr);
         const std::string err = t_last_error;
+        if (st == DRB_OK && steps > 0) {  // join the forked sel/plan streams into the capture
+            const int e = int((h->step - 1) % drb_rb::kEv);
+            if (cudaStreamWaitEvent(cs, h->ev_plan[e], 0) != cudaSuccess)
+                st = DRB_ERR_INTERNAL;
+        }
         const cudaError_t ce = cudaStreamEndCapture(cs, &gr->graph);
         cudaStreamDestroy(cs);
         if (st != DRB_OK)
             fail(st, err);
         cuda_check(ce, "end capture");
         cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
+        // events recorded during the capture are graph-internal: later steps must not wait
+        // on them (graph_launch orders the handle's streams after the whole graph instead)
+        h->dep_floor = h->step;
         *out = gr.release();
     });
 }
@@ -719,8 +866,12 @@ drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream) {
         if (g->launched)
             fail(DRB_ERR_USAGE, "graph_launch: a prepared run can be launched once");
         device_guard dg(g->h->cfg.device);
-        cuda_check(cudaGraphLaunch(g->exec, stream ? static_cast<cudaStream_t>(stream) : g->h->stream),
-                   "graph launch");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->h->stream;
+        cuda_check(cudaGraphLaunch(g->exec, s), "graph launch");
+        cuda_check(cudaEventRecord(g->h->ev_user[0], s), "event");
+        for (cudaStream_t o : {g->h->stream, g->h->s_sel, g->h->s_plan})
+            if (o != s)
+                cuda_check(cudaStreamWaitEvent(o, g->h->ev_user[0], 0), "wait");
         g->launched = true;
     });
 }
@@ -797,6 +948,8 @@ drb_status drb_rb_synchronize(drb_rb* h) {
     return guarded([&] {
         device_guard g(h->cfg.device);
         cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        cuda_check(cudaStreamSynchronize(h->s_sel), "sync");
+        cuda_check(cudaStreamSynchronize(h->s_plan), "sync");
         cuda_check(cudaStreamSynchronize(h->h2d), "sync");
         cuda_check(cudaStreamSynchronize(h->d2h), "sync");
         for (auto e : h->done)
@@ -814,10 +967,12 @@ drb_status drb_rb_device_error(drb_rb* h, uint32_t* out) {
     DRB_REQUIRE(h && out);
     return guarded([&] {
         device_guard g(h->cfg.device);
-        DevState st{};
-        cuda_check(cudaStreamSynchronize(h->stream), "order");
-        cuda_check(cudaMemcpy(&st, h->state + h->cur, sizeof st, cudaMemcpyDeviceToHost), "state");
-        *out = st.error;
+        SelState st{};
+        PlanState pst{};
+        cuda_check(cudaDeviceSynchronize(), "order");
+        cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
+        cuda_check(cudaMemcpy(&pst, h->plan + h->cur_plan, sizeof pst, cudaMemcpyDeviceToHost), "state");
+        *out = st.error ? st.error : pst.error;
     });
 }
 
@@ -832,11 +987,23 @@ drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out16) {
     });
 }
 
+drb_status drb_rb_timeline_read(drb_rb* h, uint64_t* out, uint32_t* steps) {
+    DRB_REQUIRE(h && steps);
+    return guarded([&] {
+        *steps = h->timeline_steps;
+        if (!h->timeline || !out)
+            return;
+        device_guard g(h->cfg.device);
+        cuda_check(cudaDeviceSynchronize(), "timeline sync");
+        cuda_check(cudaMemcpy(out, h->timeline, h->timeline_steps * 6ull * 8, cudaMemcpyDeviceToHost), "timeline copy");
+    });
+}
+
 drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads, uint32_t* smem) {
     DRB_REQUIRE(h && grid && threads && smem);
     *grid = h->grid;
     *threads = kThreads;
-    *smem = h->smem_bytes;
+    *smem = h->copy_smem;
     return DRB_OK;
 }
 

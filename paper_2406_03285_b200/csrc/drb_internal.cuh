@@ -12,7 +12,8 @@
 namespace drb_b200 {
 
 constexpr int kMaxWorld = DRB_RB_MAX_WORLD;
-constexpr int kTableRing = 3;  // occupancy-row versions kept per rank (v % 3); see DESIGN.md §4
+constexpr int kTableRing = 6;  // occupancy-row versions kept per rank (v % 6); see DESIGN.md §4
+constexpr int kListRing = 4;   // W_i / P_i slots: sel and plan may run up to 4 iterations ahead
 constexpr int kAugRing = 3;    // m' buffers per rank; m'_i valid until step i+2 is enqueued
 constexpr int kThreads = 512;  // step kernel CTA size (16 warps)
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
@@ -28,8 +29,10 @@ enum : uint32_t {
     kModePeers = 1u << 6,     // multi-rank: publish to / wait for / push into peers
 };
 
-// Device-resident engine state, ping-ponged between consecutive launches.
-struct alignas(16) DevState {
+// Device-resident engine state, ping-ponged between consecutive iterations. The
+// selection chain (sel kernel) and the planning chain (plan kernel) own separate state so
+// that round i+1's selection can run while round i is still being planned / copied.
+struct alignas(16) SelState {
     uint64_t cand_ctr;
     uint64_t evict_ctr;
     uint64_t version;      // mutations applied (rehearsal_buffer.cpp:79)
@@ -37,7 +40,12 @@ struct alignas(16) DevState {
     uint64_t cross_class;  // invariant counter, structurally 0 (rehearsal_buffer.hpp:91-95)
     uint32_t error;        // sticky: DRB_ERR_* of a failed round
     uint32_t pad;
+};
+
+struct alignas(16) PlanState {
     uint64_t samp_ctr[kMaxWorld];  // every requester's global-sampling counter (replicated)
+    uint32_t error;
+    uint32_t pad[3];
 };
 
 // Peer-shareable region header (one cudaMalloc per rank, exported over CUDA IPC).
@@ -93,19 +101,23 @@ struct StepParams {
     const uint32_t* labels;
     uint8_t* slab;
     uint32_t* slab_labels;
-    const DevState* st_in;
-    DevState* st_out;
+    const SelState* sel_in;
+    SelState* sel_out;
+    const PlanState* plan_in;
+    PlanState* plan_out;
     uint8_t* region[kMaxWorld];  // every rank's region base, mapped in this process
     uint64_t off_table, off_aug, off_auglab, aug_slot_bytes, auglab_slot_elems;
-    const uint32_t* plist_in;  // push list of this launch (built by the previous launch)
-    uint32_t* plist_out;       // push list for the next launch (built by the planner CTA)
-    uint32_t* wlist;           // candidate-write list of this launch (planner -> copiers)
+    const uint32_t* plist_in;  // copy(i): push list P_i (built by plan(i-1))
+    uint32_t* plist_out;       // plan(i): push list P_{i+1}
+    uint32_t* wlist;           // sel(i) writes / copy(i) reads the candidate-write list W_i
     uint32_t* report;    // [2K + 2]: appends[K], replacements[K], totals[2]
     uint32_t* mailbox;   // host-mapped: [kAugRing] counts, [kAugRing] errors
     uint64_t timeout_ns;
     uint32_t vec16;      // 16-byte vector path legal (S % 16 == 0, aligned bases)
     uint32_t smem_bytes;
     unsigned long long* trace;  // optional phase timestamps (CTA 0) + grid min/max, 16 slots
+    unsigned long long* timeline;  // optional per-kernel [start, end] per step (kind 0 sel, 1 plan, 2 copy)
+    uint32_t timeline_steps;       // ring length of the timeline (entries = steps * 3)
 };
 
 // Push list handed from launch i (leader CTA, plan(i)) to launch i+1 (all copy CTAs):
@@ -118,50 +130,73 @@ __host__ __device__ inline uint32_t plist_words(uint32_t N, uint32_t r) {
     return 4 + mj * (2 + N);
 }
 
-// Candidate-write list, planner -> copiers within one launch. u32 words: [0] n_win,
-// [1..1+2*nmax) (batch row, slab row) pairs, then post[MJ] (int: batch row overwriting
-// push job j's slot after the push read, or -1).
-__host__ __device__ inline uint32_t wlist_words(uint32_t N, uint32_t r, uint32_t nmax) {
-    return 1 + 2 * nmax + plist_mj(N, r);
-}
+// Candidate-write list W_i, sel(i) -> copy(i). u32 words: [0] n_win, then (batch row,
+// slab row) pairs of round i's winning candidates (last writer of each (class, slot)).
+__host__ __device__ inline uint32_t wlist_words(uint32_t nmax) { return 2 + 2 * nmax; }
 
-// Dynamic shared-memory carve-up of the step kernel (sizes in 4-byte words).
-struct SmemLayout {
-    uint32_t pre, pfx, occ, lab, sel, cand_l, cand_slot, win, idx, plan, cnt, acc, pj_src,
-        pj_post, pj_ndst, pj_dst, maskw, misc, words;
+// Dynamic shared-memory carve-ups (4-byte words) of the three iteration kernels.
+#define DRB_TAKE(words) (w += ((words) + 3) & ~3u, w - (((words) + 3) & ~3u))
+struct SelSmem {
+    uint32_t occ, lab, sel, cand_l, cand_slot, kind, misc, words;
 };
-
-__host__ __device__ inline SmemLayout smem_layout(uint32_t N, uint32_t K, uint32_t nmax, uint32_t r) {
-    SmemLayout s{};
+__host__ __device__ inline SelSmem sel_smem(uint32_t K, uint32_t nmax) {
+    SelSmem s{};
     uint32_t w = 0;
-    const uint32_t nr = N * (r ? r : 1);
-#define TAKE(words) (w += ((words) + 3) & ~3u, w - (((words) + 3) & ~3u))
-    s.pre = TAKE(N * K);
-    s.pfx = TAKE(N * K + 1);
-    s.occ = TAKE(K);
-    s.lab = TAKE(nmax);
-    s.sel = TAKE(nmax);
-    s.cand_l = TAKE(nmax);
-    s.cand_slot = TAKE(nmax);
-    s.win = TAKE(2 * nmax);
-    s.idx = TAKE(nmax < 32 ? 32 : nmax);  // also the 32-entry scratch of warp_select
-    s.plan = TAKE(3 * nr);
-    s.cnt = TAKE(N);
-    s.acc = TAKE(nr);
-    s.pj_src = TAKE(nr);
-    s.pj_post = TAKE(nr);
-    s.pj_ndst = TAKE(nr);
-    s.pj_dst = TAKE(nr * N);
-    s.maskw = TAKE((nmax + 31) / 32);
-    s.misc = TAKE(208);
+    const uint32_t n32 = nmax < 32 ? 32 : nmax;
+    s.occ = DRB_TAKE(K);
+    s.lab = DRB_TAKE(nmax);
+    s.sel = DRB_TAKE(n32);
+    s.cand_l = DRB_TAKE(nmax);
+    s.cand_slot = DRB_TAKE(nmax);
+    s.kind = DRB_TAKE(n32);  // also the 32-entry scratch of warp_select
+    s.misc = DRB_TAKE(64);
     s.words = w;
-#undef TAKE
     return s;
 }
+struct PlanSmem {
+    uint32_t pre, pfx, plan, cnt, acc, misc, words;
+};
+__host__ __device__ inline PlanSmem plan_smem(uint32_t N, uint32_t K, uint32_t r) {
+    PlanSmem s{};
+    uint32_t w = 0;
+    const uint32_t mj = plist_mj(N, r);
+    s.pre = DRB_TAKE(N * K);
+    s.pfx = DRB_TAKE(N * K + 1);
+    s.plan = DRB_TAKE(3 * mj);
+    s.cnt = DRB_TAKE(N);
+    s.acc = DRB_TAKE(mj);
+    s.misc = DRB_TAKE(64 + (mj + 31) / 32);
+    s.words = w;
+    return s;
+}
+struct CopySmem {
+    uint32_t pj_src, pj_ndst, pj_dst, pj_post, win, misc, words;
+};
+__host__ __device__ inline CopySmem copy_smem(uint32_t N, uint32_t r, uint32_t nmax) {
+    CopySmem s{};
+    uint32_t w = 0;
+    const uint32_t mj = plist_mj(N, r);
+    s.pj_src = DRB_TAKE(mj);
+    s.pj_ndst = DRB_TAKE(mj);
+    s.pj_dst = DRB_TAKE(mj * N);
+    s.pj_post = DRB_TAKE(mj);
+    s.win = DRB_TAKE(2 * nmax);
+    s.misc = DRB_TAKE(32 + (nmax + 31) / 32);
+    s.words = w;
+    return s;
+}
+#undef DRB_TAKE
 
 // Launchers (drb_kernels.cu), C++ linkage, used by drb_capi.cu only.
-int launch_step(const StepParams& p, uint32_t grid, void* stream);
-int step_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out);
+int launch_sel(const StepParams& p, void* stream);
+int launch_plan_next(const StepParams& p, void* stream);
+// pdl: the previous kernel on `stream` is this handle's copy of the previous iteration, so
+// the launch may overlap its tail (programmatic dependent launch).
+int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl);
+int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out);
+uint32_t sel_smem_bytes(uint32_t K, uint32_t nmax);
+uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r);
+uint32_t plan_threads(uint32_t N);
 int launch_rng_draw(uint64_t key, uint64_t ctr, uint64_t bound, uint64_t n, uint64_t* out_dev,
                     uint64_t* ctr_out_dev, void* stream);
 int launch_swor(uint64_t key, uint64_t ctr, uint32_t n, uint32_t k, uint32_t* out_dev,

@@ -362,512 +362,561 @@ __device__ __forceinline__ void warp_copy(uint32_t lo, uint32_t hi, uint32_t* co
     }
 }
 
-// Diagnostics: CTA 0 (planner) stamps slots 0-9, CTA 1 (first copier) slots 16-25.
+// Diagnostics: sel / plan stamp slots 0-8, copy CTA 0 slots 16-19 (DRB_TRACE=1).
+// Timeline (DRB_TIMELINE=<steps>): grid-wide first start / last end of each kernel of
+// each step, as globaltimer ns; works inside CUDA graphs.
+__device__ __forceinline__ void tl_mark(const StepParams& p, int kind, bool end) {
+    if (p.timeline && threadIdx.x == 0) {
+        unsigned long long* e = p.timeline + 2 * ((p.step % p.timeline_steps) * 3 + kind);
+        if (end)
+            atomicMax(e + 1, globaltimer());
+        else
+            atomicMin(e, globaltimer());
+    }
+}
+
 __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
-    if (p.trace && blockIdx.x < 2 && (threadIdx.x & 31) == 0)
-        p.trace[slot + 16 * blockIdx.x] = globaltimer();
+    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+        p.trace[slot] = globaltimer();
 }
 
 }  // namespace
 
-// misc[] words (shared)
-enum : uint32_t {
-    kMiscErr = 0,       // rendezvous error this launch
-    kMiscBad = 1,       // a label >= K
-    kMiscJobs = 2,      // push-job counter
-    kMiscWin = 3,       // candidate-write job counter
-    kMiscChunkA = 4,    // assemble-copy chunk counter
-    kMiscChunkB = 5,    // push-copy chunk counter
-    kMiscChunkC = 6,    // candidate-write chunk counter
-    kMiscK = 7,         // candidates selected this round
-    kMiscCtr = 200,     // 4 words: cand_ctr, evict_ctr (u64 each)
-    kMiscApp = 204,     // appends
-    kMiscScratch = 8,   // 32 words: eviction-draw fallback scratch
-    kMiscState = 40,    // DevState snapshot (sizeof(DevState)/4 words)
-    kMiscMaskP = 72,    // 128 words: push-leader ballot masks (N*r <= 4096)
-    kMiscWords = 208,
-};
-static_assert(sizeof(DevState) % 8 == 0 && 40 + sizeof(DevState) / 4 <= 72, "DevState layout");
+// ======================================================================================
+// One engine iteration i on one rank is three kernels, pipelined across iterations
+// (DESIGN.md §3):
+//   sel(i)   1 CTA  : S1+S2 of round i (rehearsal_buffer.cpp:14-86), the candidate-write
+//                     list W_i, round-(i+1) selection state, occupancy row v=i+1 published
+//                     (engine.cpp:108-136)                        — chained only on sel(i-1)
+//   plan(i)  1 CTA  : size rendezvous v=i+1 (size_table.cpp:66-100), S4 plan(i) for every
+//                     requester (sampler.cpp:39-68), the push list P_{i+1}, labels of
+//                     m'_{i+1}'s representatives                  — chained only on plan(i-1)
+//   copy(i)  grid   : m'_i = m_i ++ reps(i-1) (sampler.cpp:234-240): m_i -> m'_i, pushes of
+//                     P_i (slots read at version i into each requester's m'_i), then the
+//                     writes of W_i into the slab, a pushed slot only after its push read
+// so copy(i) starts with every list it needs already in memory, and sel(i+1) / plan(i)
+// run concurrently with copy(i) on their own streams.
+// ======================================================================================
 
-// Named barrier helpers (barrier 0 is __syncthreads).
-__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
+constexpr uint32_t kSelThreads = 128;
 
-__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// One engine iteration i on one rank: a cooperative launch (all CTAs co-resident),
-// software-pipelined across launches.
-//
-//  CTA 0 ("planner", no bulk copies):
-//    S1+S2 of round i (select + assign) and the candidate-write list of round i, handed
-//    to the copiers through global memory + a release/acquire flag; then round-(i+1)
-//    state, occupancy row v=i+1 published (local + peers), m'_i labels/count; then the
-//    size rendezvous for v=i+1, S4 plan(i) for every requester, and the PUSH LIST for
-//    launch i+1 (owned plan entries, one job per distinct slab slot).
-//  CTAs 1.. ("copiers", all 16 warps copy):
-//    phase 1 — m_i -> m'_i rows (needs nothing) and the pushes of plan(i-1) read at
-//              version i (push list built by launch i-1);
-//    phase 2 — after the planner's flag: candidate writes of round i; a slot that a
-//              push of this launch read is overwritten by the SAME CTA that pushed it
-//              (read-before-write: exact-horizon semantics), the rest spread over the grid.
-// No decision of round i gates the copy of the (b + r) rows of m'_i.
-template <typename V>
-__global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_constant__ StepParams p) {
+__global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_constant__ StepParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
-    const SmemLayout L = smem_layout(p.N, p.K, p.nmax, p.r);
-    uint32_t* pre = sm + L.pre;   // planner: view occupancy v=i+1 [N*K]
-    uint32_t* pfx = sm + L.pfx;   // planner: exclusive prefix [N*K+1]
-    uint32_t* occ = sm + L.occ;   // own occupancy, updated in place by S2
+    const SelSmem L = sel_smem(p.K, p.nmax);
+    uint32_t* occ = sm + L.occ;
     uint32_t* lab = sm + L.lab;
     uint32_t* sel = sm + L.sel;
     uint32_t* cand_l = sm + L.cand_l;
     uint32_t* cand_slot = sm + L.cand_slot;
-    uint32_t* win = sm + L.win;   // copiers: candidate-write jobs (batch row, slab row)
-    uint32_t* kind = sm + L.idx;  // per candidate: 1 = append (idx is free after S1)
-    uint32_t* plan = sm + L.plan;
-    uint32_t* cnt = sm + L.cnt;
-    uint32_t* acc = sm + L.acc;
-    uint32_t* pj_src = sm + L.pj_src;   // this launch's push jobs
-    int* pj_post = reinterpret_cast<int*>(sm + L.pj_post);
-    uint32_t* pj_ndst = sm + L.pj_ndst;
-    uint32_t* pj_dst = sm + L.pj_dst;
+    uint32_t* kind = sm + L.kind;
     uint32_t* misc = sm + L.misc;
-    DevState* st = reinterpret_cast<DevState*>(misc + kMiscState);
+    SelState* st = reinterpret_cast<SelState*>(misc + 16);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const bool planner = blockIdx.x == 0;
-    const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap, r = p.r;
+    const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap;
     const uint32_t NK = N * K;
-    const uint32_t MJ = plist_mj(N, r);
-    const uint64_t S = p.S;
-    const uint32_t nvec = static_cast<uint32_t>(S / sizeof(V));
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     const bool do_update = p.mode & kModeUpdate;
-    const bool do_assemble = p.mode & kModeAssemble;
-    const bool do_plan = p.mode & kModePlan;                   // build the push list for i+1
-    const bool do_push = do_plan && p.step > 0 && p.plist_in;  // pushes of plan(i-1)
     const bool do_publish = p.mode & kModePublish;
     const bool multi = (p.mode & kModePeers) && N > 1;
-    const uint32_t part = blockIdx.x - 1, parts = gridDim.x - 1;  // copier partition
-    const uint32_t aslot_next = (p.aslot + 1) % kAugRing;
-    const uint32_t n_push = do_push ? __ldcg(p.plist_in) : 0;    // uniform, L2 hit
-
-    uint8_t* my_aug = p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
-    uint32_t* auglab = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab);
-    const uint32_t row0 = p.nmax - n;  // m'_i occupies rows [nmax-n, nmax+|reps|)
     const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
-                          uint64_t(p.tslot_in) * NK;
-
+                          uint64_t(p.tslot_in) * NK + uint64_t(me) * K;
     trace_at(p, 0);
-    if (p.trace && tid == 0)
-        atomicMin(p.trace + 14, globaltimer());
-    if (tid < kMiscState)
-        misc[tid] = 0;
-
-    if (planner) {
-        // =============================== planner CTA ================================
-        if (tid < sizeof(DevState) / 8)
-            reinterpret_cast<uint64_t*>(st)[tid] =
-                __ldcg(reinterpret_cast<const uint64_t*>(p.st_in) + tid);
+    tl_mark(p, 0, false);
+    // one round trip: state, own occupancy row (version i), labels of m_i
+    if (tid < sizeof(SelState) / 8)
+        reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.sel_in) + tid);
 #pragma unroll 1
-        for (uint32_t x = tid; x < K; x += kThreads)
-            occ[x] = __ldcg(tin + uint64_t(me) * K + x);
+    for (uint32_t x = tid; x < K; x += kSelThreads)
+        occ[x] = __ldcg(tin + x);
+    int any_bad = 0;
 #pragma unroll 1
-        for (uint32_t x = tid; x < n_push; x += kThreads)
-            pj_src[x] = __ldcg(p.plist_in + 4 + x);
-        int any_bad = 0;
+    for (uint32_t x = tid; x < n; x += kSelThreads) {
+        const uint32_t l = __ldg(p.labels + x);
+        lab[x] = l;
+        any_bad |= l >= K;
+    }
+    const bool bad = __syncthreads_or(any_bad) != 0;  // usage_error before any draw (:44-47)
+    if (warp != 0)
+        return;
+    trace_at(p, 1);
+    const bool dead = st->error != 0;  // sticky: a failed round kills the engine
+    const uint32_t k = (!dead && do_update && !bad && n > 0) ? min(p.c, n) : 0;
+    uint64_t cand_ctr = (p.mode & kModeCtrParams) ? p.cand_ctr0 : st->cand_ctr;
+    uint64_t evict_ctr = (p.mode & kModeCtrParams) ? p.evict_ctr0 : st->evict_ctr;
+    uint32_t appends = 0;
+    if (k > 0) {
+        warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
+        trace_at(p, 2);
+        warp_assign(p.evict_key, evict_ctr, cap, k, sel, lab, occ, cand_l, cand_slot, misc + 32, kind,
+                    appends);
+    }
+    trace_at(p, 3);
+    // W_i: winners = last writer of each (class, slot) in selection order, ballot-ordered
+    uint32_t* wl = p.wlist;
+    uint32_t n_win = 0;
 #pragma unroll 1
-        for (uint32_t x = tid; x < n; x += kThreads) {
-            const uint32_t l = __ldg(p.labels + x);
-            lab[x] = l;
-            any_bad |= l >= K;
+    for (uint32_t base = 0; base < k; base += 32) {
+        const uint32_t t = base + lane;
+        bool w = false;
+        uint32_t key = 0;
+        if (t < k) {
+            key = cand_l[t] * cap + cand_slot[t];
+            w = true;
+#pragma unroll 1
+            for (uint32_t u = t + 1; u < k && w; ++u)
+                w = cand_l[u] * cap + cand_slot[u] != key;
         }
-        const bool bad = __syncthreads_or(any_bad) != 0;  // usage_error before any draw (:44-47)
-        const bool dead = st->error != 0;       // sticky: a failed round kills the engine
-        const bool planning = do_plan && !dead;
-        trace_at(p, 1);
-        if (warp == 0) {
-            // ---- S1 + S2 of round i -------------------------------------------------------
-            const uint32_t k = (!dead && do_update && !bad && n > 0) ? min(p.c, n) : 0;
-            uint64_t cand_ctr = (p.mode & kModeCtrParams) ? p.cand_ctr0 : st->cand_ctr;
-            uint64_t evict_ctr = (p.mode & kModeCtrParams) ? p.evict_ctr0 : st->evict_ctr;
-            uint32_t appends = 0;
-            if (k > 0) {
-                trace_at(p, 10);
-                warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
-                trace_at(p, 11);
-                warp_assign(p.evict_key, evict_ctr, cap, k, sel, lab, occ, cand_l, cand_slot,
-                            misc + kMiscScratch, kind, appends);
-                trace_at(p, 12);
-            }
-            // ---- candidate-write list for the copiers: winners (last writer of each
-            //      (class, slot) in selection order) not read by a push of this launch;
-            //      a pushed winner slot becomes that push job's trailing overwrite -------
-            uint32_t* wl = p.wlist;
-            uint32_t n_win = 0;
+        const unsigned m = __ballot_sync(kFull, w);
+        if (w) {
+            const uint32_t pos = n_win + __popc(m & lt);
+            wl[2 + 2 * pos] = sel[t];
+            wl[3 + 2 * pos] = key;
+        }
+        n_win += __popc(m);
+    }
+    if (lane == 0)
+        wl[0] = n_win;
+    // round-(i+1) selection state
+    const uint32_t err = dead ? st->error : ((bad && do_update) ? DRB_ERR_USAGE : 0u);
+    if (lane == 0) {
+        SelState* o = p.sel_out;
+        o->cand_ctr = cand_ctr;
+        o->evict_ctr = evict_ctr;
+        o->version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
+        o->total = st->total + appends;
+        o->cross_class = st->cross_class;
+        o->error = err;
+        if (p.mailbox && err)
+            reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
+    }
 #pragma unroll 1
-            for (uint32_t base = 0; base < k; base += 32) {
-                const uint32_t t = base + lane;
-                bool w = false;
-                uint32_t key = 0;
-                if (t < k) {
-                    key = cand_l[t] * cap + cand_slot[t];
-                    w = true;
+    for (uint32_t t = lane; t < k; t += 32)  // stored label == class (class-partitioned)
+        p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
+    if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
+        uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
+                         uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
 #pragma unroll 1
-                    for (uint32_t u = t + 1; u < k && w; ++u)
-                        w = cand_l[u] * cap + cand_slot[u] != key;
+        for (uint32_t x = lane; x < K; x += 32)
+            tout[x] = occ[x];
+        if (multi) {
 #pragma unroll 1
-                    for (uint32_t x = 0; x < n_push && w; ++x)
-                        w = pj_src[x] != key;
-                }
-                const unsigned m = __ballot_sync(kFull, w);
-                if (w) {
-                    const uint32_t pos = n_win + __popc(m & lt);
-                    wl[1 + 2 * pos] = sel[t];
-                    wl[2 + 2 * pos] = key;
-                }
-                n_win += __popc(m);
-            }
-#pragma unroll 1
-            for (uint32_t x = lane; x < n_push; x += 32) {
-                int post = -1;
-#pragma unroll 1
-                for (int t = static_cast<int>(k) - 1; t >= 0; --t)
-                    if (cand_l[t] * cap + cand_slot[t] == pj_src[x]) {
-                        post = static_cast<int>(sel[t]);
-                        break;
-                    }
-                wl[1 + 2 * p.nmax + x] = static_cast<uint32_t>(post);
-            }
-            if (lane == 0)
-                wl[0] = n_win;
-            __syncwarp();  // orders every lane's list writes before lane 0's release
-            if (lane == 0)
-                st_release_gpu(&hdr->wflag, p.seq + 1);
-            trace_at(p, 2);
-
-            // ---- round-(i+1) state, slab labels, publish, m'_i labels, report ----------
-            const uint32_t err = dead ? st->error : ((bad && do_update) ? DRB_ERR_USAGE : 0u);
-            if (lane == 0) {
-                DevState* o = p.st_out;
-                o->cand_ctr = cand_ctr;
-                o->evict_ctr = evict_ctr;
-                o->version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
-                o->total = st->total + appends;
-                o->cross_class = st->cross_class;
-                o->error = err;
-                if (!planning)
-                    for (uint32_t q = 0; q < N; ++q)
-                        o->samp_ctr[q] = st->samp_ctr[q];
-            }
-#pragma unroll 1
-            for (uint32_t t = lane; t < k; t += 32)  // stored label == class
-                p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
-            if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
-                uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
-                                 uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
+            for (uint32_t w = 0; w < N; ++w) {
+                if (w == me)
+                    continue;
+                uint32_t* pt = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
+                               uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
 #pragma unroll 1
                 for (uint32_t x = lane; x < K; x += 32)
-                    tout[x] = occ[x];
-                if (multi) {
-#pragma unroll 1
-                    for (uint32_t w = 0; w < N; ++w) {
-                        if (w == me)
-                            continue;
-                        uint32_t* pt = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
-                                       uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
-#pragma unroll 1
-                        for (uint32_t x = lane; x < K; x += 32)
-                            pt[x] = occ[x];
-                    }
-                    __threadfence_system();
-                    __syncwarp();
-                    if (lane < N && lane != me) {
-                        RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
-                        st_release_sys(&peer->occ_flag[me], p.step + 1);
-                    }
-                }
+                    pt[x] = occ[x];
             }
-            if (do_assemble) {  // m'_i labels of rows [row0, row0+n) and its row count
-                uint32_t* al = auglab + uint64_t(p.aslot) * p.auglab_slot_elems;
-#pragma unroll 1
-                for (uint32_t x = lane; x < n; x += 32)
-                    al[row0 + x] = lab[x];
-                if (lane == 0) {
-                    const uint32_t mine = do_push ? __ldcg(p.plist_in + 1) : 0;
-                    hdr->aug_count[p.aslot] = n + mine;
-                    if (p.mailbox) {
-                        volatile uint32_t* mb = p.mailbox;
-                        mb[p.aslot] = n + mine;
-                        mb[kAugRing + p.aslot] = dead ? st->error : 0u;
-                    }
-                }
-            }
-            if (p.mailbox && lane == 0 && err)
-                reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
-            if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
-#pragma unroll 1
-                for (uint32_t x = lane; x < 2 * K + 2; x += 32)
-                    p.report[x] = 0;
-                __syncwarp();
-                __threadfence_block();
-#pragma unroll 1
-                for (uint32_t t = lane; t < k; t += 32) {
-                    const bool app = kind[t] != 0;
-                    atomicAdd(&p.report[(app ? 0 : K) + cand_l[t]], 1u);
-                    atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
-                }
-            }
-#pragma unroll 1
-            for (uint32_t x = lane; x < K; x += 32)  // own row of the view v = i+1
-                pre[uint64_t(me) * K + x] = occ[x];
-        } else if (planning && multi && warp == 1) {
-            // size rendezvous for v = i+1 (size_table.cpp:66-100 / engine.cpp:152)
-            if (lane == 0) {
-                const uint64_t t0 = globaltimer();
-                for (uint32_t w = 0; w < N; ++w) {
-                    if (w == me)
-                        continue;
-                    while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step + 1) {
-                        if (globaltimer() - t0 > p.timeout_ns) {
-                            misc[kMiscErr] = DRB_ERR_TRANSPORT;
-                            break;
-                        }
-                        __nanosleep(32);
-                    }
-                }
-            }
+            __threadfence_system();
             __syncwarp();
-            const uint32_t* tv1 = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
-                                  uint64_t(p.tslot_out) * NK;
-#pragma unroll 1
-            for (uint32_t x = lane; x < NK; x += 32)
-                if (x / K != me)
-                    pre[x] = __ldcg(tv1 + x);
+            if (lane < N && lane != me) {
+                RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
+                st_release_sys(&peer->occ_flag[me], p.step + 1);
+            }
         }
-        __syncthreads();
-        trace_at(p, 3);
-        if (planning) {
-            // ---- S4 plan(i) for every requester (warps 1..N), prefix (warp N+1) --------
-            if (warp >= 1 && warp <= N) {
-                const uint32_t q = warp - 1;
-                uint64_t ctr = st->samp_ctr[q];
-                const uint32_t total = warp_sum(pre, NK);
-                const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
-                if (lane == 0) {
-                    cnt[q] = c;
-                    p.st_out->samp_ctr[q] = ctr;
+    }
+    if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
+#pragma unroll 1
+        for (uint32_t x = lane; x < 2 * K + 2; x += 32)
+            p.report[x] = 0;
+        __syncwarp();
+        __threadfence_block();
+#pragma unroll 1
+        for (uint32_t t = lane; t < k; t += 32) {
+            const bool app = kind[t] != 0;
+            atomicAdd(&p.report[(app ? 0 : K) + cand_l[t]], 1u);
+            atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
+        }
+    }
+    trace_at(p, 4);
+    tl_mark(p, 0, true);
+}
+
+__global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const PlanSmem L = plan_smem(p.N, p.K, p.r);
+    uint32_t* pre = sm + L.pre;
+    uint32_t* pfx = sm + L.pfx;
+    uint32_t* plan = sm + L.plan;
+    uint32_t* cnt = sm + L.cnt;
+    uint32_t* acc = sm + L.acc;
+    uint32_t* misc = sm + L.misc;
+    PlanState* st = reinterpret_cast<PlanState*>(misc + 16);
+    uint32_t* maskP = misc + 64;
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, T = blockDim.x;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t N = p.N, K = p.K, me = p.me, cap = p.cap, r = p.r;
+    const uint32_t NK = N * K;
+    const uint32_t MJ = plist_mj(N, r);
+    const bool multi = (p.mode & kModePeers) && N > 1;
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
+    trace_at(p, 5);
+    tl_mark(p, 1, false);
+    if (tid < sizeof(PlanState) / 8)
+        reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.plan_in) + tid);
+    if (tid == 0)
+        misc[0] = 0;
+    // size rendezvous for v = i+1 (size_table.cpp:66-100 / engine.cpp:152): every peer's
+    // row of this version, bounded by timeout_ns; the own row came from sel(i)
+    if (multi && tid == 0) {
+        const uint64_t t0 = globaltimer();
+        for (uint32_t w = 0; w < N; ++w) {
+            if (w == me)
+                continue;
+            while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step + 1) {
+                if (globaltimer() - t0 > p.timeout_ns) {
+                    misc[0] = DRB_ERR_TRANSPORT;
+                    break;
                 }
-            } else if (warp == N + 1) {
-                warp_exclusive_scan(pre, NK, pfx);
+                __nanosleep(32);
             }
-            __syncthreads();
-            if (warp >= 1 && warp <= N) {
-                const uint32_t q = warp - 1;
-                warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
-                if (q == me && do_assemble) {  // labels of m'_{i+1}'s reps (stored label == class)
-                    uint32_t* al = auglab + uint64_t(aslot_next) * p.auglab_slot_elems;
+        }
+    }
+    __syncthreads();
+    const uint32_t* tv1 = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
+                          uint64_t(p.tslot_out) * NK;
 #pragma unroll 1
-                    for (uint32_t j = lane; j < cnt[q]; j += 32)
-                        al[p.nmax + j] = plan[3 * (q * r + j) + 1];
-                }
-            }
-            __syncthreads();
-            trace_at(p, 4);
-            // ---- push list for launch i+1: owned entries, one job per distinct slot,
-            //      numbered in entry order (ballots), dests = every (q, j) drawing it ----
-            const uint32_t NR = N * r;
-            uint32_t* maskP = misc + kMiscMaskP;
-            uint32_t* out = p.plist_out;
-            for (uint32_t base = warp * 32; base < NR; base += kThreads) {
-                const uint32_t e = base + lane;
-                bool lead = false;
-                if (e < NR) {
-                    const uint32_t q = e / r, j = e - q * r;
-                    if (j < cnt[q] && plan[3 * e] == me) {
-                        const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-                        lead = true;
+    for (uint32_t x = tid; x < NK; x += T)
+        pre[x] = __ldcg(tv1 + x);
+    __syncthreads();
+    trace_at(p, 6);
+    const bool dead = st->error != 0;
+    uint32_t* out = p.plist_out;
+    if (dead) {
+        if (tid < sizeof(PlanState) / 8)
+            reinterpret_cast<uint64_t*>(p.plan_out)[tid] = reinterpret_cast<const uint64_t*>(st)[tid];
+        if (tid == 0) {
+            out[0] = 0;
+            out[1] = 0;
+        }
+        tl_mark(p, 1, true);
+        return;
+    }
+    // S4 plan(i): warps 1..N draw for requester q = warp-1; warp 0 builds the prefix
+    if (warp >= 1 && warp <= N) {
+        const uint32_t q = warp - 1;
+        uint64_t ctr = st->samp_ctr[q];
+        const uint32_t total = warp_sum(pre, NK);
+        const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
+        if (lane == 0) {
+            cnt[q] = c;
+            p.plan_out->samp_ctr[q] = ctr;
+        }
+    } else if (warp == 0) {
+        warp_exclusive_scan(pre, NK, pfx);
+    }
+    __syncthreads();
+    if (warp >= 1 && warp <= N) {
+        const uint32_t q = warp - 1;
+        warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
+        if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
+            uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
+                           uint64_t((p.aslot + 1) % kAugRing) * p.auglab_slot_elems;
 #pragma unroll 1
-                        for (uint32_t q2 = 0; q2 < q && lead; ++q2)
-#pragma unroll 1
-                            for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
-                                const uint32_t* x = plan + 3 * (q2 * r + j2);
-                                if (x[0] == me && x[1] == cls && x[2] == slot) {
-                                    lead = false;
-                                    break;
-                                }
-                            }
-                    }
-                }
-                const unsigned m = __ballot_sync(kFull, lead);
-                if (lane == 0)
-                    maskP[base >> 5] = m;
-            }
-            __syncthreads();
-            for (uint32_t base = warp * 32; base < NR; base += kThreads) {
-                const unsigned m = maskP[base >> 5];
-                if (!((m >> lane) & 1u))
-                    continue;
-                uint32_t pj = __popc(m & lt);
-#pragma unroll 1
-                for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
-                    pj += __popc(maskP[b2]);
-                const uint32_t e = base + lane, q = e / r, j = e - q * r;
+            for (uint32_t j = lane; j < cnt[q]; j += 32)
+                al[p.nmax + j] = plan[3 * (q * r + j) + 1];
+        }
+    }
+    __syncthreads();
+    trace_at(p, 7);
+    // P_{i+1}: owned entries, one job per distinct slot numbered in entry order (ballots),
+    // destinations = every (requester q, rep j) that drew the slot
+    const uint32_t NR = N * r;
+    for (uint32_t base = warp * 32; base < NR; base += T) {
+        const uint32_t e = base + lane;
+        bool lead = false;
+        if (e < NR) {
+            const uint32_t q = e / r, j = e - q * r;
+            if (j < cnt[q] && plan[3 * e] == me) {
                 const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-                uint32_t nd = 0;
-                out[4 + 2 * MJ + pj * N + nd++] = (q << 16) | j;
+                lead = true;
 #pragma unroll 1
-                for (uint32_t q2 = q + 1; q2 < N; ++q2)
+                for (uint32_t q2 = 0; q2 < q && lead; ++q2)
 #pragma unroll 1
                     for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
                         const uint32_t* x = plan + 3 * (q2 * r + j2);
                         if (x[0] == me && x[1] == cls && x[2] == slot) {
-                            out[4 + 2 * MJ + pj * N + nd++] = (q2 << 16) | j2;
+                            lead = false;
                             break;
                         }
                     }
-                out[4 + pj] = cls * cap + slot;
-                out[4 + MJ + pj] = nd;
             }
-            if (tid == 0) {
-                uint32_t np = 0;
+        }
+        const unsigned m = __ballot_sync(kFull, lead);
+        if (lane == 0)
+            maskP[base >> 5] = m;
+    }
+    __syncthreads();
+    for (uint32_t base = warp * 32; base < NR; base += T) {
+        const unsigned m = maskP[base >> 5];
+        if (!((m >> lane) & 1u))
+            continue;
+        uint32_t pj = __popc(m & lt);
 #pragma unroll 1
-                for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
-                    np += __popc(maskP[b2]);
-                out[0] = np;
-                out[1] = cnt[me];
-                if (misc[kMiscErr]) {  // rendezvous failure: the engine is dead from here
-                    atomicOr(&p.st_out->error, misc[kMiscErr]);
-                    if (p.mailbox)
-                        reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[kMiscErr];
+        for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
+            pj += __popc(maskP[b2]);
+        const uint32_t e = base + lane, q = e / r, j = e - q * r;
+        const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
+        uint32_t nd = 0;
+        out[4 + 2 * MJ + pj * N + nd++] = (q << 16) | j;
+#pragma unroll 1
+        for (uint32_t q2 = q + 1; q2 < N; ++q2)
+#pragma unroll 1
+            for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
+                const uint32_t* x = plan + 3 * (q2 * r + j2);
+                if (x[0] == me && x[1] == cls && x[2] == slot) {
+                    out[4 + 2 * MJ + pj * N + nd++] = (q2 << 16) | j2;
+                    break;
                 }
             }
-        } else if (do_plan && tid == 0 && p.plist_out) {
-            p.plist_out[0] = 0;
-            p.plist_out[1] = 0;
-        }
-        trace_at(p, 5);
-    } else {
-        // =============================== copier CTAs ================================
-        // Phase 1 is ONE chunked vector space: [assemble: n rows of m_i][pushes: n_push
-        // jobs]; each CTA owns a fixed slice of it (the hazard overwrites of phase 2 reuse
-        // that slice), warps claim 32*U-vector chunks dynamically inside the slice.
-        const V* batch = reinterpret_cast<const V*>(p.batch);
-        V* slab = reinterpret_cast<V*>(p.slab);
-        const uint32_t av = do_assemble ? n * nvec : 0;   // assemble vectors
-        const uint32_t tv1 = av + n_push * nvec;
-        const uint32_t lo1 = static_cast<uint32_t>(uint64_t(tv1) * part / parts);
-        const uint32_t hi1 = static_cast<uint32_t>(uint64_t(tv1) * (part + 1) / parts);
-        if (warp == 0 && lo1 < hi1 && hi1 > av) {
-            // this CTA's slice reaches the push jobs: stage them (overlaps the copy)
+        out[4 + pj] = cls * cap + slot;
+        out[4 + MJ + pj] = nd;
+    }
+    if (tid == 0) {
+        uint32_t np = 0;
 #pragma unroll 1
-            for (uint32_t x = lane; x < n_push; x += 32) {
-                pj_src[x] = __ldcg(p.plist_in + 4 + x);
-                const uint32_t nd = __ldcg(p.plist_in + 4 + MJ + x);
-                pj_ndst[x] = nd;
+        for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
+            np += __popc(maskP[b2]);
+        out[0] = np;
+        out[1] = cnt[me];
+        p.plan_out->error = misc[0];
+        if (misc[0] && p.mailbox)  // rendezvous failure: the engine is dead from here
+            reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[0];
+    }
+    trace_at(p, 8);
+    tl_mark(p, 1, true);
+}
+
+// copy(i): every CTA owns fixed slices of three vector spaces —
+//   A: m_i -> m'_i rows [nmax-n, nmax)                                  (n rows)
+//   B: [pushes of P_i: slab slot -> every requester's m'_i row nmax+j |
+//       writes of W_i whose slot no push reads: m_i row -> slab slot]
+//   C: writes of W_i whose slot a push reads (hazard), over this CTA's push slice of B,
+//      after a barrier — read at version i, then overwritten (exact horizon).
+// Warps claim 32*U-vector chunks of a slice dynamically.
+template <typename V>
+__global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_constant__ StepParams p) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const CopySmem L = copy_smem(p.N, p.r, p.nmax);
+    uint32_t* pj_src = sm + L.pj_src;
+    uint32_t* pj_ndst = sm + L.pj_ndst;
+    uint32_t* pj_dst = sm + L.pj_dst;
+    int* pj_post = reinterpret_cast<int*>(sm + L.pj_post);
+    uint32_t* win = sm + L.win;  // non-hazard writes first, then hazard ones (compacted)
+    uint32_t* misc = sm + L.misc;
+    uint32_t* maskw = misc + 32;
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t N = p.N, me = p.me, n = p.n;
+    const uint32_t MJ = plist_mj(N, p.r);
+    const uint64_t S = p.S;
+    const uint32_t nvec = static_cast<uint32_t>(S / sizeof(V));
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
+    const bool do_assemble = p.mode & kModeAssemble;
+    const bool do_push = (p.mode & kModePlan) && p.step > 0 && p.plist_in;
+    const bool do_update = p.mode & kModeUpdate;
+    const bool multi = (p.mode & kModePeers) && N > 1;
+    const uint32_t part = blockIdx.x, parts = gridDim.x;
+    const V* batch = reinterpret_cast<const V*>(p.batch);
+    V* slab = reinterpret_cast<V*>(p.slab);
+    const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
+    const uint32_t row0 = p.nmax - n;
+
+    trace_at(p, 16);
+    tl_mark(p, 2, false);
+    // Programmatic dependent launch: the next copy may be scheduled as soon as SMs free up;
+    // it runs its independent part (m_{i+1} -> m'_{i+1}) before waiting for this grid.
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (p.trace && tid == 0)
+        atomicMin(p.trace + 14, globaltimer());
+    volatile uint32_t* ready = misc + 6;
+    if (tid < 16)
+        misc[tid] = 0;
+    __syncthreads();  // chunk counters / ready flag zeroed
+    // This CTA's slices: A = m_i -> m'_i (known at once), B = pushes of P_i + safe writes
+    // of W_i (known once warp 0 staged the lists AND the previous copy grid finished —
+    // its slab writes are what P_i's pushes read). One chunk counter walks A then B.
+    constexpr int UA = sizeof(V) == 16 ? 8 : 16;
+    constexpr int UB = sizeof(V) == 16 ? 4 : 8;
+    const uint32_t tva = do_assemble ? n * nvec : 0;
+    const uint32_t alo = static_cast<uint32_t>(uint64_t(tva) * part / parts);
+    const uint32_t ahi = static_cast<uint32_t>(uint64_t(tva) * (part + 1) / parts);
+    const uint32_t a_chunks = (ahi - alo + 32 * UA - 1) / (32 * UA);
+    if (warp == 0) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // previous copy complete
+        // stage P_i and W_i; hazard = a winner whose slot a push job reads
+        const uint32_t n_push = do_push ? __ldcg(p.plist_in) : 0;
+        const uint32_t n_win = do_update ? __ldcg(p.wlist) : 0;
 #pragma unroll 1
-                for (uint32_t d = 0; d < nd; ++d)
-                    pj_dst[x * N + d] = __ldcg(p.plist_in + 4 + 2 * MJ + x * N + d);
-            }
-            __syncwarp();
-            __threadfence_block();
+        for (uint32_t x = lane; x < n_push; x += 32) {
+            pj_src[x] = __ldcg(p.plist_in + 4 + x);
+            const uint32_t nd = __ldcg(p.plist_in + 4 + MJ + x);
+            pj_ndst[x] = nd;
+#pragma unroll 1
+            for (uint32_t d = 0; d < nd; ++d)
+                pj_dst[x * N + d] = __ldcg(p.plist_in + 4 + 2 * MJ + x * N + d);
+            pj_post[x] = -1;
         }
-        __syncthreads();  // chunk counters zeroed; push jobs staged
-        {
-            constexpr int U = sizeof(V) == 16 ? 8 : 16;
-            V* asm_dst = reinterpret_cast<V*>(my_aug + uint64_t(row0) * S);
-            const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
-            warp_copy<V, U>(
-                lo1, hi1, &misc[kMiscChunkA],
-                [&](uint32_t gv) -> const V* {
-                    if (gv < av)
-                        return batch + gv;
-                    const uint32_t pv = gv - av, job = pv / nvec, off = pv - job * nvec;
-                    return slab + uint64_t(pj_src[job]) * nvec + off;
-                },
-                [&](uint32_t gv, const V& v) {
-                    if (gv < av) {
-                        asm_dst[gv] = v;
-                        return;
+        __syncwarp();
+        uint32_t nw_safe = 0;
+#pragma unroll 1
+        for (uint32_t base = 0; base < n_win; base += 32) {
+            const uint32_t t = base + lane;
+            uint32_t row = 0, key = 0;
+            int hz = -1;
+            if (t < n_win) {
+                row = __ldcg(p.wlist + 2 + 2 * t);
+                key = __ldcg(p.wlist + 3 + 2 * t);
+#pragma unroll 1
+                for (uint32_t x = 0; x < n_push; ++x)
+                    if (pj_src[x] == key) {
+                        hz = static_cast<int>(x);
+                        break;
                     }
-                    const uint32_t pv = gv - av, job = pv / nvec, off = pv - job * nvec;
+                if (hz >= 0)
+                    pj_post[hz] = static_cast<int>(row);
+            }
+            const unsigned m = __ballot_sync(kFull, t < n_win && hz < 0);
+            if (t < n_win && hz < 0) {
+                const uint32_t pos = nw_safe + __popc(m & lt);
+                win[2 * pos] = row;
+                win[2 * pos + 1] = key;
+            }
+            nw_safe += __popc(m);
+        }
+        if (lane == 0) {
+            misc[0] = n_push;
+            misc[1] = nw_safe;
+        }
+        if (blockIdx.x == 0 && do_assemble) {
+            // m'_i labels of rows [row0, row0+n) and its row count n + |reps(i-1)|
+            uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
+                           uint64_t(p.aslot) * p.auglab_slot_elems;
+#pragma unroll 1
+            for (uint32_t x = lane; x < n; x += 32)
+                al[row0 + x] = __ldg(p.labels + x);
+            if (lane == 0) {
+                const uint32_t mine = do_push ? __ldcg(p.plist_in + 1) : 0;
+                hdr->aug_count[p.aslot] = n + mine;
+                if (p.mailbox) {
+                    volatile uint32_t* mb = p.mailbox;
+                    mb[p.aslot] = n + mine;
+                    mb[kAugRing + p.aslot] = 0;
+                }
+            }
+        }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0)
+            *ready = 1;
+    }
+    V* asm_dst = reinterpret_cast<V*>(p.region[me] + aug_off + uint64_t(row0) * S);
+    uint32_t n_push = 0, pv_tot = 0, blo = 0, bhi = 0;
+    bool have_b = false;
+    for (;;) {
+        uint32_t c = 0;
+        if (lane == 0)
+            c = atomicAdd(&misc[4], 1u);
+        c = __shfl_sync(kFull, c, 0);
+        if (c < a_chunks) {  // ---- A chunk --------------------------------------------
+            const uint32_t base = alo + c * (32u * UA);
+            V r[UA];
+#pragma unroll
+            for (int u = 0; u < UA; ++u) {
+                const uint32_t gv = base + u * 32 + lane;
+                if (gv < ahi)
+                    r[u] = ld_vec(batch + gv);
+            }
+#pragma unroll
+            for (int u = 0; u < UA; ++u) {
+                const uint32_t gv = base + u * 32 + lane;
+                if (gv < ahi)
+                    asm_dst[gv] = r[u];
+            }
+            continue;
+        }
+        if (!have_b) {  // lists staged (warp 0), previous grid done
+            while (*ready == 0)
+                __nanosleep(20);
+            __threadfence_block();
+            n_push = misc[0];
+            const uint32_t n_safe = misc[1];
+            pv_tot = n_push * nvec;
+            const uint32_t tvb = pv_tot + n_safe * nvec;
+            blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
+            bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
+            have_b = true;
+        }
+        const uint32_t base = blo + (c - a_chunks) * (32u * UB);
+        if (base >= bhi)
+            break;
+        // ---- B chunk: pushes of P_i (slab -> every requester's m'_i) + safe writes ------
+        V r[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const uint32_t gv = base + u * 32 + lane;
+            if (gv < bhi) {
+                if (gv < pv_tot) {
+                    const uint32_t job = gv / nvec, off = gv - job * nvec;
+                    r[u] = ld_vec(slab + uint64_t(pj_src[job]) * nvec + off);
+                } else {
+                    const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
+                    r[u] = ld_vec(batch + uint64_t(win[2 * job]) * nvec + off);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const uint32_t gv = base + u * 32 + lane;
+            if (gv < bhi) {
+                if (gv < pv_tot) {
+                    const uint32_t job = gv / nvec, off = gv - job * nvec;
                     const uint32_t nd = pj_ndst[job];
 #pragma unroll 1
                     for (uint32_t x = 0; x < nd; ++x) {
                         const uint32_t e = pj_dst[job * N + x];
                         const uint32_t q = e >> 16, j = e & 0xffffu;
-                        reinterpret_cast<V*>(p.region[q] + aug_off + uint64_t(p.nmax + j) * S)[off] = v;
+                        reinterpret_cast<V*>(p.region[q] + aug_off + uint64_t(p.nmax + j) * S)[off] = r[u];
                     }
-                });
-        }
-        trace_at(p, 6);
-        // ---- wait for the planner's candidate-write list -------------------------------
-        if (tid == 0 && (do_update || do_push)) {
-            const uint64_t t0 = globaltimer();
-            while (ld_acquire_gpu(&hdr->wflag) < p.seq + 1) {
-                if (globaltimer() - t0 > p.timeout_ns)
-                    break;  // planner lost: leave the slab untouched (engine error set by host)
-                __nanosleep(20);
+                } else {
+                    const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
+                    slab[uint64_t(win[2 * job + 1]) * nvec + off] = r[u];
+                }
             }
         }
-        __syncthreads();
-        const uint32_t* wl = p.wlist;
-        const uint32_t n_win = (do_update || do_push) ? __ldcg(wl) : 0;
-        // the push jobs in this CTA's slice (hazard overwrites) and the candidate writes
-        const uint32_t pj_lo = lo1 > av ? (lo1 - av) / nvec : 0;
-        const uint32_t pj_hi = hi1 > av ? (hi1 - av + nvec - 1) / nvec : 0;
-#pragma unroll 1
-        for (uint32_t x = tid; x < 2 * n_win; x += kThreads)
-            win[x] = __ldcg(wl + 1 + x);
-#pragma unroll 1
-        for (uint32_t x = pj_lo + tid; x < pj_hi; x += kThreads)
-            pj_post[x] = static_cast<int>(__ldcg(wl + 1 + 2 * p.nmax + x));
-        __syncthreads();
-        trace_at(p, 7);
-        // ---- phase 2, ONE pass: [hazard overwrites of this CTA's push slice (post >= 0)]
-        //      then [candidate writes spread over the grid] --------------------------------
-        {
-            constexpr int U = sizeof(V) == 16 ? 4 : 8;
-            const uint32_t plo = lo1 > av ? lo1 - av : 0, phi = hi1 > av ? hi1 - av : 0;
-            const uint32_t nh = phi - plo;  // this CTA's pushed vectors (candidates for posts)
-            const uint32_t tvw = n_win * nvec;
-            const uint32_t wlo = static_cast<uint32_t>(uint64_t(tvw) * part / parts);
-            const uint32_t whi = static_cast<uint32_t>(uint64_t(tvw) * (part + 1) / parts);
-            const uint32_t tot = nh + (whi - wlo);
-            warp_copy<V, U>(
-                0, tot, &misc[kMiscChunkC],
-                [&](uint32_t gv) -> const V* {
-                    if (gv < nh) {
-                        const uint32_t pv = plo + gv, job = pv / nvec, off = pv - job * nvec;
-                        const int post = pj_post[job];
-                        return post >= 0 ? batch + uint64_t(post) * nvec + off : nullptr;
-                    }
-                    const uint32_t wv = wlo + gv - nh, job = wv / nvec, off = wv - job * nvec;
-                    return batch + uint64_t(win[2 * job]) * nvec + off;
-                },
-                [&](uint32_t gv, const V& v) {
-                    if (gv < nh) {
-                        const uint32_t pv = plo + gv, job = pv / nvec, off = pv - job * nvec;
-                        if (pj_post[job] >= 0)
-                            slab[uint64_t(pj_src[job]) * nvec + off] = v;
-                        return;
-                    }
-                    const uint32_t wv = wlo + gv - nh, job = wv / nvec, off = wv - job * nvec;
-                    slab[uint64_t(win[2 * job + 1]) * nvec + off] = v;
-                });
-        }
-        trace_at(p, 8);
     }
+    trace_at(p, 18);
+    // ---- C: hazard writes over this CTA's push slice (after its reads) -------------------
+    __syncthreads();
+    if (!have_b) {
+        n_push = misc[0];
+        pv_tot = n_push * nvec;
+        const uint32_t tvb = pv_tot + misc[1] * nvec;
+        blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
+        bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
+    }
+    const uint32_t clo = blo, chi = min(bhi, pv_tot);
+    bool any_post = false;
+    if (clo < chi) {
+        const uint32_t j0 = clo / nvec, j1 = (chi - 1) / nvec;
+        for (uint32_t j = j0; j <= j1; ++j)
+            any_post |= pj_post[j] >= 0;
+    }
+    if (__syncthreads_or(any_post)) {
+#pragma unroll 1
+        for (uint32_t gv = clo + tid; gv < chi; gv += kThreads) {
+            const uint32_t job = gv / nvec, off = gv - job * nvec;
+            const int post = pj_post[job];
+            if (post >= 0)
+                slab[uint64_t(pj_src[job]) * nvec + off] = ld_vec(batch + uint64_t(post) * nvec + off);
+        }
+    }
+    trace_at(p, 19);
 
     // ---- completion handshake (multi-rank): the last CTA of this rank to finish tells
     // every requester that all pushes of step i into it have landed, then waits until
@@ -899,19 +948,18 @@ __global__ void __launch_bounds__(kThreads, 1) drb_step_kernel(const __grid_cons
                         __nanosleep(32);
                     }
                 }
-                if (to) {
-                    atomicOr(&p.st_out->error, static_cast<uint32_t>(DRB_ERR_TRANSPORT));
-                    if (p.mailbox) {
-                        volatile uint32_t* mb = p.mailbox;
-                        mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
-                        mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
-                    }
+                if (to && p.mailbox) {
+                    volatile uint32_t* mb = p.mailbox;
+                    mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
+                    mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
                 }
             }
         }
     }
     if (p.trace && tid == 0)
         atomicMax(p.trace + 15, globaltimer());
+    __syncthreads();
+    tl_mark(p, 2, true);
 }
 
 // ---- standalone kernels for the buffer-level API (tests / facade) ----------------------
@@ -1011,37 +1059,65 @@ __global__ void read_slots_kernel(const uint8_t* slab, const uint32_t* slab_labe
 
 // ---- launchers ------------------------------------------------------------------------
 
-int launch_step(const StepParams& p, uint32_t grid, void* stream) {
-    static uint32_t attr_bytes[2] = {0, 0};
-    const int which = p.vec16 ? 1 : 0;
-    auto kern = p.vec16 ? drb_step_kernel<uint4> : drb_step_kernel<uint32_t>;
-    if (p.smem_bytes > attr_bytes[which]) {
+uint32_t sel_smem_bytes(uint32_t K, uint32_t nmax) { return sel_smem(K, nmax).words * 4; }
+uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r) { return plan_smem(N, K, r).words * 4; }
+uint32_t plan_threads(uint32_t N) { return 32 * (N + 1 < 3 ? 3 : N + 1); }
+
+namespace {
+int set_smem(const void* kern, uint32_t bytes, uint32_t* cache) {
+    if (bytes > *cache) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(p.smem_bytes)) != cudaSuccess)
+                                 static_cast<int>(bytes)) != cudaSuccess)
             return -1;
-        attr_bytes[which] = p.smem_bytes;
+        *cache = bytes;
     }
-    // Cooperative: the copier CTAs wait for the planner CTA's flag inside the launch, so
-    // every CTA must be co-resident (one CTA per SM, a single wave).
+    return 0;
+}
+}  // namespace
+
+int launch_sel(const StepParams& p, void* stream) {
+    static uint32_t cache = 0;
+    const uint32_t smem = sel_smem_bytes(p.K, p.nmax);
+    if (set_smem(reinterpret_cast<const void*>(drb_sel_kernel), smem, &cache))
+        return -1;
+    drb_sel_kernel<<<1, kSelThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_plan_next(const StepParams& p, void* stream) {
+    static uint32_t cache = 0;
+    const uint32_t smem = plan_smem_bytes(p.N, p.K, p.r);
+    if (set_smem(reinterpret_cast<const void*>(drb_plan_next_kernel), smem, &cache))
+        return -1;
+    drb_plan_next_kernel<<<1, plan_threads(p.N), smem, static_cast<cudaStream_t>(stream)>>>(p);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl) {
+    static uint32_t cache[2] = {0, 0};
+    const int which = p.vec16 ? 1 : 0;
+    auto kern = p.vec16 ? drb_copy_kernel<uint4> : drb_copy_kernel<uint32_t>;
+    if (set_smem(reinterpret_cast<const void*>(kern), p.smem_bytes, &cache[which]))
+        return -1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, p) == cudaSuccess ? 0 : -1;
 }
 
-int step_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {
-    for (auto kern : {drb_step_kernel<uint4>, drb_step_kernel<uint32_t>})
+int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {
+    for (auto kern : {drb_copy_kernel<uint4>, drb_copy_kernel<uint32_t>})
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem_bytes)) != cudaSuccess)
             return -1;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, drb_step_kernel<uint4>, kThreads,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, drb_copy_kernel<uint4>, kThreads,
                                                          smem_bytes) == cudaSuccess
                ? 0
                : -1;

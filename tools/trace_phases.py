@@ -16,11 +16,10 @@ import paper_2406_03285_b200 as drb  # noqa: E402
 from paper_2406_03285_b200._lib import check, lib  # noqa: E402
 from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E402
 
-NAMES = {0: "planner start", 1: "planner loads", 10: "planner S1 start", 11: "planner S1 done",
-         12: "planner S2 done", 2: "planner write list published", 3: "planner rendezvous v=i+1",
-         4: "planner plan(i)+locate", 5: "planner push list written",
-         16: "copier start", 22: "copier phase 1 done", 23: "copier write list loaded",
-         24: "copier phase 2 done"}
+NAMES = {0: "sel start", 1: "sel loads", 2: "sel S1 done", 3: "sel S2 done", 4: "sel end",
+         5: "plan start", 6: "plan view loaded", 7: "plan draws+locate", 8: "plan end",
+         16: "copy start", 17: "copy A (m_i -> m') done", 18: "copy B (push+write) done",
+         19: "copy C (hazard) done"}
 
 
 def main():
@@ -41,9 +40,9 @@ def main():
         check(lib.drb_rb_trace_read(buf.h, t.ctypes.data))
         rows.append(t.astype(np.int64))
     rows = np.stack(rows)
-    t0 = rows[:, 14]
+    t0 = rows[:, 0]
     print(f"config {sys.argv[1] if len(sys.argv) > 1 else 'c2'}; grid={buf.launch_info()}")
-    for slot in (0, 1, 10, 11, 12, 2, 3, 4, 5, 16, 22, 23, 24):
+    for slot in (0, 1, 2, 3, 4, 5, 6, 7, 8, 16, 17, 18, 19):
         v = rows[:, slot] - t0
         print(f"  {NAMES[slot]:34s} median {np.median(v) / 1000:7.2f} us")
     print(f"  {'grid last end':34s} median {np.median(rows[:, 15] - t0) / 1000:7.2f} us")
