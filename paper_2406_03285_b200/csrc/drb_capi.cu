@@ -724,6 +724,7 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
     if (h->trace) {
         cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
         cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
+        cuda_check(cudaMemsetAsync(h->trace + 21, 0xff, 16, s), "trace reset");
     }
     cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i)], 0), "wait");
     const bool have1 = i >= h->dep_floor + 1;

@@ -170,18 +170,17 @@ __host__ __device__ inline PlanSmem plan_smem(uint32_t N, uint32_t K, uint32_t r
     return s;
 }
 struct CopySmem {
-    uint32_t pj_src, pj_ndst, pj_dst, pj_post, win, misc, words;
+    uint32_t praw, wraw, pj_post, win, misc, words;
 };
 __host__ __device__ inline CopySmem copy_smem(uint32_t N, uint32_t r, uint32_t nmax) {
     CopySmem s{};
     uint32_t w = 0;
     const uint32_t mj = plist_mj(N, r);
-    s.pj_src = DRB_TAKE(mj);
-    s.pj_ndst = DRB_TAKE(mj);
-    s.pj_dst = DRB_TAKE(mj * N);
+    s.praw = DRB_TAKE(plist_words(N, r));   // P_i verbatim
+    s.wraw = DRB_TAKE(wlist_words(nmax));   // W_i verbatim
     s.pj_post = DRB_TAKE(mj);
     s.win = DRB_TAKE(2 * nmax);
-    s.misc = DRB_TAKE(32 + (nmax + 31) / 32);
+    s.misc = DRB_TAKE(32);
     s.words = w;
     return s;
 }

@@ -702,13 +702,15 @@ template <typename V>
 __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_constant__ StepParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const CopySmem L = copy_smem(p.N, p.r, p.nmax);
-    uint32_t* pj_src = sm + L.pj_src;
-    uint32_t* pj_ndst = sm + L.pj_ndst;
-    uint32_t* pj_dst = sm + L.pj_dst;
+    uint32_t* praw = sm + L.praw;
+    uint32_t* wraw = sm + L.wraw;
+    const uint32_t MJ0 = plist_mj(p.N, p.r);
+    const uint32_t* pj_src = praw + 4;
+    const uint32_t* pj_ndst = praw + 4 + MJ0;
+    const uint32_t* pj_dst = praw + 4 + 2 * MJ0;
     int* pj_post = reinterpret_cast<int*>(sm + L.pj_post);
-    uint32_t* win = sm + L.win;  // non-hazard writes first, then hazard ones (compacted)
+    uint32_t* win = sm + L.win;  // candidate writes whose slot no push reads (compacted)
     uint32_t* misc = sm + L.misc;
-    uint32_t* maskw = misc + 32;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -737,7 +739,25 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     volatile uint32_t* ready = misc + 6;
     if (tid < 16)
         misc[tid] = 0;
-    __syncthreads();  // chunk counters / ready flag zeroed
+    const uint32_t pw = do_push ? plist_words(N, p.r) : 0;
+    const uint32_t ww = do_update ? wlist_words(p.nmax) : 0;
+    if (warp == 0) {
+        // issue the list loads (async, straight into shared memory) before any bulk
+        // traffic of this CTA, so they are not queued behind it
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // previous copy complete
+#pragma unroll 1
+        for (uint32_t x = lane; x < pw; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(praw + x))),
+                         "l"(p.plist_in + x)
+                         : "memory");
+#pragma unroll 1
+        for (uint32_t x = lane; x < ww; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(wraw + x))),
+                         "l"(p.wlist + x)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __syncthreads();  // chunk counters / ready flag zeroed; list loads issued
     // This CTA's slices: A = m_i -> m'_i (known at once), B = pushes of P_i + safe writes
     // of W_i (known once warp 0 staged the lists AND the previous copy grid finished —
     // its slab writes are what P_i's pushes read). One chunk counter walks A then B.
@@ -748,21 +768,15 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     const uint32_t ahi = static_cast<uint32_t>(uint64_t(tva) * (part + 1) / parts);
     const uint32_t a_chunks = (ahi - alo + 32 * UA - 1) / (32 * UA);
     if (warp == 0) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // previous copy complete
-        // stage P_i and W_i; hazard = a winner whose slot a push job reads
-        const uint32_t n_push = do_push ? __ldcg(p.plist_in) : 0;
-        const uint32_t n_win = do_update ? __ldcg(p.wlist) : 0;
-#pragma unroll 1
-        for (uint32_t x = lane; x < n_push; x += 32) {
-            pj_src[x] = __ldcg(p.plist_in + 4 + x);
-            const uint32_t nd = __ldcg(p.plist_in + 4 + MJ + x);
-            pj_ndst[x] = nd;
-#pragma unroll 1
-            for (uint32_t d = 0; d < nd; ++d)
-                pj_dst[x * N + d] = __ldcg(p.plist_in + 4 + 2 * MJ + x * N + d);
-            pj_post[x] = -1;
-        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
+        const uint32_t n_push = do_push ? praw[0] : 0;
+        const uint32_t n_win = do_update ? wraw[0] : 0;
+#pragma unroll 1
+        for (uint32_t x = lane; x < n_push; x += 32)
+            pj_post[x] = -1;
+        __syncwarp();
+        // hazard = a winner whose slot a push job reads: it becomes that job's overwrite
         uint32_t nw_safe = 0;
 #pragma unroll 1
         for (uint32_t base = 0; base < n_win; base += 32) {
@@ -770,8 +784,8 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             uint32_t row = 0, key = 0;
             int hz = -1;
             if (t < n_win) {
-                row = __ldcg(p.wlist + 2 + 2 * t);
-                key = __ldcg(p.wlist + 3 + 2 * t);
+                row = wraw[2 + 2 * t];
+                key = wraw[3 + 2 * t];
 #pragma unroll 1
                 for (uint32_t x = 0; x < n_push; ++x)
                     if (pj_src[x] == key) {
@@ -793,6 +807,11 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             misc[0] = n_push;
             misc[1] = nw_safe;
         }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0)
+            *ready = 1;
+        trace_at(p, 20);
         if (blockIdx.x == 0 && do_assemble) {
             // m'_i labels of rows [row0, row0+n) and its row count n + |reps(i-1)|
             uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
@@ -801,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             for (uint32_t x = lane; x < n; x += 32)
                 al[row0 + x] = __ldg(p.labels + x);
             if (lane == 0) {
-                const uint32_t mine = do_push ? __ldcg(p.plist_in + 1) : 0;
+                const uint32_t mine = do_push ? praw[1] : 0;
                 hdr->aug_count[p.aslot] = n + mine;
                 if (p.mailbox) {
                     volatile uint32_t* mb = p.mailbox;
@@ -810,10 +829,6 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
                 }
             }
         }
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0)
-            *ready = 1;
     }
     V* asm_dst = reinterpret_cast<V*>(p.region[me] + aug_off + uint64_t(row0) * S);
     uint32_t n_push = 0, pv_tot = 0, blo = 0, bhi = 0;
@@ -841,6 +856,8 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             continue;
         }
         if (!have_b) {  // lists staged (warp 0), previous grid done
+            if (p.trace && blockIdx.x == 0 && lane == 0)
+                atomicMin(p.trace + 21, globaltimer());
             while (*ready == 0)
                 __nanosleep(20);
             __threadfence_block();
@@ -890,16 +907,12 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             }
         }
     }
-    trace_at(p, 18);
-    // ---- C: hazard writes over this CTA's push slice (after its reads) -------------------
-    __syncthreads();
-    if (!have_b) {
-        n_push = misc[0];
-        pv_tot = n_push * nvec;
-        const uint32_t tvb = pv_tot + misc[1] * nvec;
-        blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
-        bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
+    if (p.trace && blockIdx.x == 0 && lane == 0) {
+        atomicMin(p.trace + 22, globaltimer());  // first warp out of the chunk loop
+        atomicMax(p.trace + 18, globaltimer());  // last warp out
     }
+    // ---- C: hazard writes over this CTA's push slice, after ALL its reads (barrier only
+    //      when this CTA has one; the condition is uniform: it reads staged lists) --------
     const uint32_t clo = blo, chi = min(bhi, pv_tot);
     bool any_post = false;
     if (clo < chi) {
@@ -907,7 +920,8 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         for (uint32_t j = j0; j <= j1; ++j)
             any_post |= pj_post[j] >= 0;
     }
-    if (__syncthreads_or(any_post)) {
+    if (any_post) {
+        __syncthreads();
 #pragma unroll 1
         for (uint32_t gv = clo + tid; gv < chi; gv += kThreads) {
             const uint32_t job = gv / nvec, off = gv - job * nvec;
@@ -958,8 +972,10 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     }
     if (p.trace && tid == 0)
         atomicMax(p.trace + 15, globaltimer());
-    __syncthreads();
-    tl_mark(p, 2, true);
+    if (p.timeline) {
+        __syncthreads();
+        tl_mark(p, 2, true);
+    }
 }
 
 // ---- standalone kernels for the buffer-level API (tests / facade) ----------------------

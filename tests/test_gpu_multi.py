@@ -1,0 +1,98 @@
+"""Multi-rank engine on several GPUs vs the synchronous-replay oracle.
+
+Single process, one rehearsal_buffer per device (peer access over NVLink); every rank's
+augmented batch must be bit-exact against oracle/drb_oracle.c's N-rank replay, including
+the cross-GPU pushes of representatives owned by other ranks.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.py_oracle import Backend
+from paper_2406_03285_b200.workload import stream_spec
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def make_world(drb, N, K, cap, S, b, c, r, seed):
+    bufs = [drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed, rank=w,
+                                 world=N, device=w) for w in range(N)]
+    blobs = [bf.export_handle() for bf in bufs]
+    for bf in bufs:
+        bf.connect(blobs)
+    engs = [drb.engine(bf) for bf in bufs]
+    for e in engs:
+        e.start()
+    return bufs, engs
+
+
+def run_multi(drb, N, K, cap, S, b, c, r, seed, steps, T=1, spt=10**9, pattern=None, ring_run=False):
+    bufs, engs = make_world(drb, N, K, cap, S, b, c, r, seed)
+    spec = stream_spec(K, T, b, S, steps_per_task=spt, seed=seed)
+    rep = Backend("port").replay(N, K, cap, S, c, r, seed)
+    streams = [torch.cuda.Stream(device=w) for w in range(N)]
+    for i in range(steps):
+        n = pattern[i % len(pattern)] if pattern else b
+        data = np.stack([spec.payload(w, i, n) for w in range(N)])
+        labs = np.stack([spec.labels(w, i, n) for w in range(N)])
+        o, ol, oc = rep.step(data, labs)
+        augs = []
+        for w in range(N):  # enqueue every rank before waiting on any (they rendezvous)
+            with torch.cuda.device(w):
+                m = (torch.from_numpy(data[w]).cuda(w), torch.from_numpy(labs[w].astype(np.int32)).cuda(w))
+                torch.cuda.synchronize(w)
+                augs.append(engs[w].update(m, stream=streams[w]))
+        for w in range(N):
+            d, l = augs[w].tensors()
+            cnt = augs[w].count()
+            assert cnt == int(oc[w]), (i, w)
+            assert np.array_equal(l.cpu().numpy().astype(np.uint32), ol[w, :cnt]), (i, w)
+            assert np.array_equal(d.cpu().numpy(), o[w, :cnt]), (i, w)
+    for e in engs:
+        e.shutdown()
+    return bufs
+
+
+def ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+def test_multi_rank_parity_small(N):
+    if ngpu() < N:
+        pytest.skip(f"needs {N} GPUs")
+    import paper_2406_03285_b200 as drb
+    run_multi(drb, N, K=12, cap=5, S=64, b=24, c=14, r=7, seed=5, steps=40, T=3, spt=10)
+
+
+def test_multi_rank_parity_c2_shape():
+    if ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2406_03285_b200 as drb
+    run_multi(drb, 2, K=100, cap=48, S=150528, b=56, c=14, r=7, seed=1, steps=60, T=4, spt=15)
+
+
+def test_multi_rank_short_batches_and_exhaustion():
+    if ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2406_03285_b200 as drb
+    run_multi(drb, 2, K=6, cap=3, S=16, b=12, c=5, r=40, seed=11, steps=30, pattern=[12, 3, 0, 12, 1])
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_multi_process_ipc_parity(N):
+    """torchrun, one process per GPU, regions mapped with CUDA IPC handles."""
+    if ngpu() < N:
+        pytest.skip(f"needs {N} GPUs")
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    worker = os.path.join(os.path.dirname(__file__), "mp", "ipc_parity_worker.py")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={N}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", worker]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]

@@ -18,8 +18,9 @@ from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E40
 
 NAMES = {0: "sel start", 1: "sel loads", 2: "sel S1 done", 3: "sel S2 done", 4: "sel end",
          5: "plan start", 6: "plan view loaded", 7: "plan draws+locate", 8: "plan end",
-         16: "copy start", 17: "copy A (m_i -> m') done", 18: "copy B (push+write) done",
-         19: "copy C (hazard) done"}
+         16: "copy start (cta0)", 20: "copy lists staged", 21: "copy first B chunk",
+         22: "copy first warp done", 18: "copy last warp done", 19: "copy end (cta0)", 14: "copy grid first start",
+         15: "copy grid last end"}
 
 
 def main():
@@ -40,9 +41,9 @@ def main():
         check(lib.drb_rb_trace_read(buf.h, t.ctypes.data))
         rows.append(t.astype(np.int64))
     rows = np.stack(rows)
-    t0 = rows[:, 0]
+    t0 = rows[:, 14]
     print(f"config {sys.argv[1] if len(sys.argv) > 1 else 'c2'}; grid={buf.launch_info()}")
-    for slot in (0, 1, 2, 3, 4, 5, 6, 7, 8, 16, 17, 18, 19):
+    for slot in (0, 1, 2, 3, 4, 5, 6, 7, 8, 14, 16, 20, 21, 22, 18, 19, 15):
         v = rows[:, slot] - t0
         print(f"  {NAMES[slot]:34s} median {np.median(v) / 1000:7.2f} us")
     print(f"  {'grid last end':34s} median {np.median(rows[:, 15] - t0) / 1000:7.2f} us")
