@@ -104,9 +104,12 @@ struct handle_blob {
     uint32_t world;
     uint64_t region_bytes;
     uint64_t region_ptr;  // raw device pointer (same-process peers)
+    uint64_t slab_bytes;
+    uint64_t slab_ptr;
     cudaIpcMemHandle_t ipc;
+    cudaIpcMemHandle_t slab_ipc;  // the slab: peers pull representatives from it
 };
-constexpr uint32_t kBlobMagic = 0x44524232;  // "DRB2"
+constexpr uint32_t kBlobMagic = 0x44524233;  // "DRB3"
 
 // Scoped temporary device allocation for the synchronous test-facing calls.
 struct dev_tmp {
@@ -135,6 +138,8 @@ struct drb_rb {
     uint8_t* region = nullptr;        // own peer-shareable region
     uint8_t* peers[kMaxWorld] = {};   // every rank's region, mapped here
     bool peer_opened[kMaxWorld] = {};
+    uint8_t* slab_peers[kMaxWorld] = {};  // every rank's slab, mapped here
+    bool slab_opened[kMaxWorld] = {};
     bool connected = false;
     SelState* sel = nullptr;          // [2], sel[cur_sel] is current
     PlanState* plan = nullptr;        // [2], plan[cur_plan] is current
@@ -198,9 +203,12 @@ StepParams base_params(drb_rb* h) {
         p.samp_key[q] = h->samp_key[q];
     p.slab = h->slab;
     p.slab_labels = h->slab_labels;
-    for (int q = 0; q < kMaxWorld; ++q)
+    for (int q = 0; q < kMaxWorld; ++q) {
         p.region[q] = h->peers[q];
+        p.slab_peer[q] = h->slab_peers[q];
+    }
     p.region[c.rank] = h->region;
+    p.slab_peer[c.rank] = h->slab;
     p.off_table = h->layout.off_table;
     p.off_aug = h->layout.off_aug;
     p.off_auglab = h->layout.off_auglab;
@@ -377,6 +385,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         for (uint32_t q = 0; q < kMaxWorld; ++q)
             h->samp_key[q] = derive_key(c.seed, q, DRB_PURPOSE_GLOBAL_SAMPLING, 0, 0);
         h->peers[c.rank] = h->region;
+        h->slab_peers[c.rank] = h->slab;
         if (const char* tl = std::getenv("DRB_TIMELINE")) {
             h->timeline_steps = uint32_t(std::strtoul(tl, nullptr, 10));
             if (h->timeline_steps) {
@@ -406,9 +415,12 @@ drb_status drb_rb_destroy(drb_rb* h) {
     return guarded([&] {
         device_guard g(h->cfg.device);
         cudaDeviceSynchronize();
-        for (uint32_t w = 0; w < h->cfg.world; ++w)
+        for (uint32_t w = 0; w < h->cfg.world; ++w) {
             if (h->peer_opened[w])
                 cudaIpcCloseMemHandle(h->peers[w]);
+            if (h->slab_opened[w])
+                cudaIpcCloseMemHandle(h->slab_peers[w]);
+        }
         cudaFree(h->slab);
         cudaFree(h->slab_labels);
         cudaFree(h->region);
@@ -579,7 +591,10 @@ drb_status drb_rb_export_handle(drb_rb* h, void* blob, size_t* len) {
         b.world = h->cfg.world;
         b.region_bytes = h->layout.bytes;
         b.region_ptr = reinterpret_cast<uint64_t>(h->region);
+        b.slab_bytes = uint64_t(h->cfg.n_classes) * h->cfg.per_class_cap * h->cfg.sample_bytes;
+        b.slab_ptr = reinterpret_cast<uint64_t>(h->slab);
         cuda_check(cudaIpcGetMemHandle(&b.ipc, h->region), "cudaIpcGetMemHandle");
+        cuda_check(cudaIpcGetMemHandle(&b.slab_ipc, h->slab), "cudaIpcGetMemHandle (slab)");
         std::memcpy(blob, &b, sizeof b);
         *len = sizeof b;
     });
@@ -614,11 +629,17 @@ drb_status drb_rb_connect(drb_rb* h, const void* blobs, size_t blob_len) {
                     cudaGetLastError();
                 }
                 h->peers[w] = reinterpret_cast<uint8_t*>(b.region_ptr);
+                h->slab_peers[w] = reinterpret_cast<uint8_t*>(b.slab_ptr);
             } else {
                 void* p = nullptr;
                 cuda_check(cudaIpcOpenMemHandle(&p, b.ipc, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
                 h->peers[w] = static_cast<uint8_t*>(p);
                 h->peer_opened[w] = true;
+                void* q = nullptr;
+                cuda_check(cudaIpcOpenMemHandle(&q, b.slab_ipc, cudaIpcMemLazyEnablePeerAccess),
+                           "cudaIpcOpenMemHandle (slab)");
+                h->slab_peers[w] = static_cast<uint8_t*>(q);
+                h->slab_opened[w] = true;
             }
         }
         h->connected = true;

@@ -51,11 +51,13 @@ struct alignas(16) PlanState {
 // Peer-shareable region header (one cudaMalloc per rank, exported over CUDA IPC).
 struct alignas(256) RegionHeader {
     uint64_t occ_flag[kMaxWorld];  // [w]: latest occupancy version rank w published here
-    uint64_t arrive[kMaxWorld];    // [w]: 1 + last step whose pushes from w into me completed
+    uint64_t done[kMaxWorld];      // [w]: 1 + last iteration whose copy rank w completed
+                                   //      (its slab writes of that round are visible)
+    uint64_t readdone[kMaxWorld];  // [w]: 1 + last iteration whose pulls rank w completed
     uint64_t ticket;               // local: CTA completion tickets (last-CTA detection)
+    uint64_t rticket;              // local: CTA tickets after the pull phase
     uint32_t aug_count[4];         // local: rows of m' per ring slot (device copy)
-    uint64_t wflag;                // local: planner -> copiers, 1 + step whose write list is ready
-    uint64_t pad[12];
+    uint64_t pad[2];
 };
 
 struct RegionLayout {
@@ -106,6 +108,7 @@ struct StepParams {
     const PlanState* plan_in;
     PlanState* plan_out;
     uint8_t* region[kMaxWorld];  // every rank's region base, mapped in this process
+    const uint8_t* slab_peer[kMaxWorld];  // every rank's slab, mapped in this process
     uint64_t off_table, off_aug, off_auglab, aug_slot_bytes, auglab_slot_elems;
     const uint32_t* plist_in;  // copy(i): push list P_i (built by plan(i-1))
     uint32_t* plist_out;       // plan(i): push list P_{i+1}
@@ -120,14 +123,17 @@ struct StepParams {
     uint32_t timeline_steps;       // ring length of the timeline (entries = steps * 3)
 };
 
-// Push list handed from launch i (leader CTA, plan(i)) to launch i+1 (all copy CTAs):
-// the owned entries of every requester's plan, one job per distinct slab slot, in a
-// deterministic order. u32 words: [0] njobs, [1] reps drawn for this rank (cnt_me),
-// [2..3] pad, src[MJ] (slab row = cls*cap+slot), ndst[MJ], dst[MJ*N] ((q << 16) | j).
+// Pull list handed from plan(i-1) to copy(i). u32 words:
+//   [0] cnt      — this rank's representatives of round i-1 (= rows pulled into m'_i)
+//   [1] n_remote — rows of MY slab that other requesters read this round
+//   [2..3] pad
+//   owner[R], row[R]      this rank's plan in draw order (pulled into m'_i row nmax+j);
+//                         row = cls*cap + slot in the owner's slab          (R = max(r,1))
+//   rrow[MJ], rmask[MJ]   remote-read rows of my slab, bit w = requester w reads it
 __host__ __device__ inline uint32_t plist_mj(uint32_t N, uint32_t r) { return N * (r ? r : 1); }
+__host__ __device__ inline uint32_t plist_r(uint32_t r) { return r ? r : 1; }
 __host__ __device__ inline uint32_t plist_words(uint32_t N, uint32_t r) {
-    const uint32_t mj = plist_mj(N, r);
-    return 4 + mj * (2 + N);
+    return 4 + 2 * plist_r(r) + 2 * plist_mj(N, r);
 }
 
 // Candidate-write list W_i, sel(i) -> copy(i). u32 words: [0] n_win, then (batch row,
@@ -170,16 +176,16 @@ __host__ __device__ inline PlanSmem plan_smem(uint32_t N, uint32_t K, uint32_t r
     return s;
 }
 struct CopySmem {
-    uint32_t praw, wraw, pj_post, win, misc, words;
+    uint32_t praw, wraw, post, win, defer, misc, words;
 };
 __host__ __device__ inline CopySmem copy_smem(uint32_t N, uint32_t r, uint32_t nmax) {
     CopySmem s{};
     uint32_t w = 0;
-    const uint32_t mj = plist_mj(N, r);
-    s.praw = DRB_TAKE(plist_words(N, r));   // P_i verbatim
+    s.praw = DRB_TAKE(plist_words(N, r));   // pull list verbatim
     s.wraw = DRB_TAKE(wlist_words(nmax));   // W_i verbatim
-    s.pj_post = DRB_TAKE(mj);
-    s.win = DRB_TAKE(2 * nmax);
+    s.post = DRB_TAKE(plist_r(r));          // per pulled rep: local overwrite after the read
+    s.win = DRB_TAKE(2 * nmax);             // candidate writes nobody reads this round
+    s.defer = DRB_TAKE(3 * nmax);           // writes to rows remote requesters read
     s.misc = DRB_TAKE(32);
     s.words = w;
     return s;

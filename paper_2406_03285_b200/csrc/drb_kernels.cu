@@ -64,6 +64,12 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// No ordering of earlier stores (a release would wait for every store of the copy to be
+// acknowledged): for flags that only announce completed LOADS.
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -623,19 +629,33 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
     }
     __syncthreads();
     trace_at(p, 7);
-    // P_{i+1}: owned entries, one job per distinct slot numbered in entry order (ballots),
-    // destinations = every (requester q, rep j) that drew the slot
+    // Pull list for copy(i+1): (a) this rank's own plan in draw order — it reads every
+    // representative itself, from the owner's slab (local or over NVLink); (b) the rows of
+    // MY slab that other requesters read, deduplicated in entry order (ballots), with the
+    // set of readers — a write of round i+1 to such a row must wait for those reads.
+    const uint32_t R = plist_r(r);
+    const uint32_t mine = cnt[me];
+#pragma unroll 1
+    for (uint32_t j = tid; j < mine; j += T) {
+        const uint32_t* x = plan + 3 * (me * r + j);
+        out[4 + j] = x[0];
+        out[4 + R + j] = x[1] * cap + x[2];
+    }
     const uint32_t NR = N * r;
+    uint32_t* rrow = out + 4 + 2 * R;
+    uint32_t* rmask = rrow + MJ;
     for (uint32_t base = warp * 32; base < NR; base += T) {
         const uint32_t e = base + lane;
         bool lead = false;
         if (e < NR) {
             const uint32_t q = e / r, j = e - q * r;
-            if (j < cnt[q] && plan[3 * e] == me) {
+            if (q != me && j < cnt[q] && plan[3 * e] == me) {
                 const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
                 lead = true;
 #pragma unroll 1
-                for (uint32_t q2 = 0; q2 < q && lead; ++q2)
+                for (uint32_t q2 = 0; q2 < q && lead; ++q2) {
+                    if (q2 == me)
+                        continue;
 #pragma unroll 1
                     for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
                         const uint32_t* x = plan + 3 * (q2 * r + j2);
@@ -644,6 +664,7 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
                             break;
                         }
                     }
+                }
             }
         }
         const unsigned m = __ballot_sync(kFull, lead);
@@ -655,34 +676,36 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
         const unsigned m = maskP[base >> 5];
         if (!((m >> lane) & 1u))
             continue;
-        uint32_t pj = __popc(m & lt);
+        uint32_t pos = __popc(m & lt);
 #pragma unroll 1
         for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
-            pj += __popc(maskP[b2]);
-        const uint32_t e = base + lane, q = e / r, j = e - q * r;
+            pos += __popc(maskP[b2]);
+        const uint32_t e = base + lane, q = e / r;
         const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-        uint32_t nd = 0;
-        out[4 + 2 * MJ + pj * N + nd++] = (q << 16) | j;
+        uint32_t readers = 1u << q;
 #pragma unroll 1
-        for (uint32_t q2 = q + 1; q2 < N; ++q2)
+        for (uint32_t q2 = q + 1; q2 < N; ++q2) {
+            if (q2 == me)
+                continue;
 #pragma unroll 1
             for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
                 const uint32_t* x = plan + 3 * (q2 * r + j2);
                 if (x[0] == me && x[1] == cls && x[2] == slot) {
-                    out[4 + 2 * MJ + pj * N + nd++] = (q2 << 16) | j2;
+                    readers |= 1u << q2;
                     break;
                 }
             }
-        out[4 + pj] = cls * cap + slot;
-        out[4 + MJ + pj] = nd;
+        }
+        rrow[pos] = cls * cap + slot;
+        rmask[pos] = readers;
     }
     if (tid == 0) {
-        uint32_t np = 0;
+        uint32_t nrem = 0;
 #pragma unroll 1
         for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
-            np += __popc(maskP[b2]);
-        out[0] = np;
-        out[1] = cnt[me];
+            nrem += __popc(maskP[b2]);
+        out[0] = mine;
+        out[1] = nrem;
         p.plan_out->error = misc[0];
         if (misc[0] && p.mailbox)  // rendezvous failure: the engine is dead from here
             reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[0];
@@ -691,60 +714,96 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
     tl_mark(p, 1, true);
 }
 
-// copy(i): every CTA owns fixed slices of three vector spaces —
-//   A: m_i -> m'_i rows [nmax-n, nmax)                                  (n rows)
-//   B: [pushes of P_i: slab slot -> every requester's m'_i row nmax+j |
-//       writes of W_i whose slot no push reads: m_i row -> slab slot]
-//   C: writes of W_i whose slot a push reads (hazard), over this CTA's push slice of B,
-//      after a barrier — read at version i, then overwritten (exact horizon).
-// Warps claim 32*U-vector chunks of a slice dynamically.
+__device__ __forceinline__ uint4 ld_cg16(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <typename V>
+__device__ __forceinline__ V ld_pull(const V* p) {  // possibly a peer's memory (NVLink)
+    if constexpr (sizeof(V) == 16) {
+        const uint4 v = ld_cg16(reinterpret_cast<const uint4*>(p));
+        return *reinterpret_cast<const V*>(&v);
+    } else {
+        return __ldcg(p);
+    }
+}
+
+// Spin (thread-level) until *flag >= want or the timeout; returns false on timeout.
+__device__ bool wait_flag(const uint64_t* flag, uint64_t want, uint64_t timeout_ns) {
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_sys(flag) < want) {
+        if (globaltimer() - t0 > timeout_ns)
+            return false;
+        __nanosleep(32);
+    }
+    return true;
+}
+
+// copy(i): m'_i = m_i ++ reps(i-1) and the slab writes of round i. Every CTA owns fixed
+// slices of the vector spaces below; warps claim 32*U-vector chunks of a slice dynamically.
+//   A  m_i -> m'_i rows [nmax-n, nmax)                                   (n rows)
+//   B  pulls: rep j of this rank <- owner's slab row (local or a peer's over NVLink, read
+//      at version i: the owner finished copy(i-1)) into m'_i row nmax+j; plus the
+//      candidate writes of W_i nobody reads this round
+//   C  a write to a row this rank itself pulled: by the same CTA, after the pull (barrier)
+//   D  a write to a row a remote requester pulls: after that requester's pulls completed
+// Multi-rank signals (peer headers, release/acquire .sys): readdone[me] after the last
+// CTA's B phase, done[me] after the last CTA's writes — the only cross-rank waits are
+// "owner finished copy(i-1)" before pulling from it and the rare D case.
 template <typename V>
 __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_constant__ StepParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const CopySmem L = copy_smem(p.N, p.r, p.nmax);
     uint32_t* praw = sm + L.praw;
     uint32_t* wraw = sm + L.wraw;
-    const uint32_t MJ0 = plist_mj(p.N, p.r);
-    const uint32_t* pj_src = praw + 4;
-    const uint32_t* pj_ndst = praw + 4 + MJ0;
-    const uint32_t* pj_dst = praw + 4 + 2 * MJ0;
-    int* pj_post = reinterpret_cast<int*>(sm + L.pj_post);
-    uint32_t* win = sm + L.win;  // candidate writes whose slot no push reads (compacted)
+    int* post = reinterpret_cast<int*>(sm + L.post);
+    uint32_t* win = sm + L.win;
+    uint32_t* defer = sm + L.defer;
     uint32_t* misc = sm + L.misc;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t N = p.N, me = p.me, n = p.n;
-    const uint32_t MJ = plist_mj(N, p.r);
+    const uint32_t R = plist_r(p.r), MJ = plist_mj(N, p.r);
     const uint64_t S = p.S;
     const uint32_t nvec = static_cast<uint32_t>(S / sizeof(V));
     RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     const bool do_assemble = p.mode & kModeAssemble;
-    const bool do_push = (p.mode & kModePlan) && p.step > 0 && p.plist_in;
+    const bool do_pull = (p.mode & kModePlan) && p.step > 0 && p.plist_in;
     const bool do_update = p.mode & kModeUpdate;
     const bool multi = (p.mode & kModePeers) && N > 1;
     const uint32_t part = blockIdx.x, parts = gridDim.x;
     const V* batch = reinterpret_cast<const V*>(p.batch);
     V* slab = reinterpret_cast<V*>(p.slab);
     const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
+    V* my_aug = reinterpret_cast<V*>(p.region[me] + aug_off);
     const uint32_t row0 = p.nmax - n;
+    const uint32_t* owner = praw + 4;
+    const uint32_t* prow = praw + 4 + R;
+    const uint32_t* rrow = praw + 4 + 2 * R;
+    const uint32_t* rmask = rrow + MJ;
 
     trace_at(p, 16);
     tl_mark(p, 2, false);
-    // Programmatic dependent launch: the next copy may be scheduled as soon as SMs free up;
-    // it runs its independent part (m_{i+1} -> m'_{i+1}) before waiting for this grid.
     asm volatile("griddepcontrol.launch_dependents;");
     if (p.trace && tid == 0)
         atomicMin(p.trace + 14, globaltimer());
     volatile uint32_t* ready = misc + 6;
     if (tid < 16)
         misc[tid] = 0;
-    const uint32_t pw = do_push ? plist_words(N, p.r) : 0;
+    const uint32_t pw = do_pull ? plist_words(N, p.r) : 0;
     const uint32_t ww = do_update ? wlist_words(p.nmax) : 0;
     if (warp == 0) {
-        // issue the list loads (async, straight into shared memory) before any bulk
-        // traffic of this CTA, so they are not queued behind it
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // previous copy complete
+        // list loads first (async into shared memory), before any bulk traffic of this CTA
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        // copy(i-1) of this rank is complete (kernel boundary: its slab writes are visible),
+        // so peers may pull round-i representatives from our slab: done[me] = i everywhere
+        if (multi && blockIdx.x == 0 && lane < N)
+            st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[lane])->done[me], p.step);
 #pragma unroll 1
         for (uint32_t x = lane; x < pw; x += 32)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(praw + x))),
@@ -758,9 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __syncthreads();  // chunk counters / ready flag zeroed; list loads issued
-    // This CTA's slices: A = m_i -> m'_i (known at once), B = pushes of P_i + safe writes
-    // of W_i (known once warp 0 staged the lists AND the previous copy grid finished —
-    // its slab writes are what P_i's pushes read). One chunk counter walks A then B.
+
     constexpr int UA = sizeof(V) == 16 ? 8 : 16;
     constexpr int UB = sizeof(V) == 16 ? 4 : 8;
     const uint32_t tva = do_assemble ? n * nvec : 0;
@@ -770,42 +827,89 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     if (warp == 0) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
-        const uint32_t n_push = do_push ? praw[0] : 0;
+        const uint32_t cnt = do_pull ? praw[0] : 0;
+        const uint32_t nrem = (do_pull && multi) ? praw[1] : 0;
         const uint32_t n_win = do_update ? wraw[0] : 0;
+        // round-i writes: to a row this rank pulls -> post on that pull (C); to a row a
+        // remote requester pulls -> deferred (D); otherwise a plain write (B)
 #pragma unroll 1
-        for (uint32_t x = lane; x < n_push; x += 32)
-            pj_post[x] = -1;
+        for (uint32_t j = lane; j < cnt; j += 32)
+            post[j] = -1;
         __syncwarp();
-        // hazard = a winner whose slot a push job reads: it becomes that job's overwrite
-        uint32_t nw_safe = 0;
+        uint32_t n_safe = 0, n_def = 0;
 #pragma unroll 1
         for (uint32_t base = 0; base < n_win; base += 32) {
             const uint32_t t = base + lane;
-            uint32_t row = 0, key = 0;
-            int hz = -1;
+            uint32_t row = 0, key = 0, readers = 0;
+            bool local_hz = false;
             if (t < n_win) {
                 row = wraw[2 + 2 * t];
                 key = wraw[3 + 2 * t];
 #pragma unroll 1
-                for (uint32_t x = 0; x < n_push; ++x)
-                    if (pj_src[x] == key) {
-                        hz = static_cast<int>(x);
+                for (uint32_t j = 0; j < cnt; ++j)
+                    if (owner[j] == me && prow[j] == key) {
+                        post[j] = static_cast<int>(row);
+                        local_hz = true;
                         break;
                     }
-                if (hz >= 0)
-                    pj_post[hz] = static_cast<int>(row);
+#pragma unroll 1
+                for (uint32_t x = 0; x < nrem; ++x)
+                    if (rrow[x] == key) {
+                        readers = rmask[x];
+                        break;
+                    }
             }
-            const unsigned m = __ballot_sync(kFull, t < n_win && hz < 0);
-            if (t < n_win && hz < 0) {
-                const uint32_t pos = nw_safe + __popc(m & lt);
+            const bool safe = t < n_win && !local_hz && readers == 0;
+            const bool def = t < n_win && readers != 0;
+            const unsigned ms = __ballot_sync(kFull, safe);
+            const unsigned md = __ballot_sync(kFull, def);
+            if (safe) {
+                const uint32_t pos = n_safe + __popc(ms & lt);
                 win[2 * pos] = row;
                 win[2 * pos + 1] = key;
             }
-            nw_safe += __popc(m);
+            if (def) {  // (a local hazard that is also remote-read: D after the local read
+                        //  — D runs after this CTA's barrier anyway)
+                const uint32_t pos = n_def + __popc(md & lt);
+                defer[3 * pos] = row;
+                defer[3 * pos + 1] = key;
+                defer[3 * pos + 2] = readers;
+            }
+            n_safe += __popc(ms);
+            n_def += __popc(md);
+        }
+        // a local-hazard row that is also remote-read is written in D only
+        if (n_def) {
+#pragma unroll 1
+            for (uint32_t j = lane; j < cnt; j += 32)
+                if (post[j] >= 0)
+#pragma unroll 1
+                    for (uint32_t x = 0; x < n_def; ++x)
+                        if (defer[3 * x + 1] == prow[j] && owner[j] == me)
+                            post[j] = -1;
+        }
+        // pulls from a peer need that owner's copy(i-1) complete (its slab at version i)
+        if (multi && cnt) {
+            uint32_t need = 0;
+            for (uint32_t j = lane; j < cnt; j += 32)
+                if (owner[j] != me)
+                    need |= 1u << owner[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                need |= __shfl_xor_sync(kFull, need, o);
+            bool ok = true;
+            if (lane < N && ((need >> lane) & 1u))
+                ok = wait_flag(&hdr->done[lane], p.step, p.timeout_ns);
+            if (__any_sync(kFull, !ok) && lane == 0 && p.mailbox) {
+                volatile uint32_t* mb = p.mailbox;
+                mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
+                mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
+            }
         }
         if (lane == 0) {
-            misc[0] = n_push;
-            misc[1] = nw_safe;
+            misc[0] = cnt;
+            misc[1] = n_safe;
+            misc[2] = n_def;
         }
         __syncwarp();
         __threadfence_block();
@@ -820,18 +924,17 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             for (uint32_t x = lane; x < n; x += 32)
                 al[row0 + x] = __ldg(p.labels + x);
             if (lane == 0) {
-                const uint32_t mine = do_push ? praw[1] : 0;
-                hdr->aug_count[p.aslot] = n + mine;
+                hdr->aug_count[p.aslot] = n + cnt;
                 if (p.mailbox) {
                     volatile uint32_t* mb = p.mailbox;
-                    mb[p.aslot] = n + mine;
+                    mb[p.aslot] = n + cnt;
                     mb[kAugRing + p.aslot] = 0;
                 }
             }
         }
     }
-    V* asm_dst = reinterpret_cast<V*>(p.region[me] + aug_off + uint64_t(row0) * S);
-    uint32_t n_push = 0, pv_tot = 0, blo = 0, bhi = 0;
+    V* asm_dst = my_aug + uint64_t(row0) * nvec;
+    uint32_t cnt = 0, pv_tot = 0, blo = 0, bhi = 0;
     bool have_b = false;
     for (;;) {
         uint32_t c = 0;
@@ -840,31 +943,30 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         c = __shfl_sync(kFull, c, 0);
         if (c < a_chunks) {  // ---- A chunk --------------------------------------------
             const uint32_t base = alo + c * (32u * UA);
-            V r[UA];
+            V rg[UA];
 #pragma unroll
             for (int u = 0; u < UA; ++u) {
                 const uint32_t gv = base + u * 32 + lane;
                 if (gv < ahi)
-                    r[u] = ld_vec(batch + gv);
+                    rg[u] = ld_vec(batch + gv);
             }
 #pragma unroll
             for (int u = 0; u < UA; ++u) {
                 const uint32_t gv = base + u * 32 + lane;
                 if (gv < ahi)
-                    asm_dst[gv] = r[u];
+                    asm_dst[gv] = rg[u];
             }
             continue;
         }
-        if (!have_b) {  // lists staged (warp 0), previous grid done
+        if (!have_b) {  // lists staged and peers ready (warp 0)
             if (p.trace && blockIdx.x == 0 && lane == 0)
                 atomicMin(p.trace + 21, globaltimer());
             while (*ready == 0)
                 __nanosleep(20);
             __threadfence_block();
-            n_push = misc[0];
-            const uint32_t n_safe = misc[1];
-            pv_tot = n_push * nvec;
-            const uint32_t tvb = pv_tot + n_safe * nvec;
+            cnt = misc[0];
+            pv_tot = cnt * nvec;
+            const uint32_t tvb = pv_tot + misc[1] * nvec;
             blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
             bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
             have_b = true;
@@ -872,18 +974,18 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         const uint32_t base = blo + (c - a_chunks) * (32u * UB);
         if (base >= bhi)
             break;
-        // ---- B chunk: pushes of P_i (slab -> every requester's m'_i) + safe writes ------
-        V r[UB];
+        // ---- B chunk: pulls into m'_i + plain candidate writes ---------------------------
+        V rg[UB];
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
             const uint32_t gv = base + u * 32 + lane;
             if (gv < bhi) {
                 if (gv < pv_tot) {
-                    const uint32_t job = gv / nvec, off = gv - job * nvec;
-                    r[u] = ld_vec(slab + uint64_t(pj_src[job]) * nvec + off);
+                    const uint32_t j = gv / nvec, off = gv - j * nvec;
+                    rg[u] = ld_pull(reinterpret_cast<const V*>(p.slab_peer[owner[j]]) + uint64_t(prow[j]) * nvec + off);
                 } else {
                     const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
-                    r[u] = ld_vec(batch + uint64_t(win[2 * job]) * nvec + off);
+                    rg[u] = ld_vec(batch + uint64_t(win[2 * job]) * nvec + off);
                 }
             }
         }
@@ -892,17 +994,11 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             const uint32_t gv = base + u * 32 + lane;
             if (gv < bhi) {
                 if (gv < pv_tot) {
-                    const uint32_t job = gv / nvec, off = gv - job * nvec;
-                    const uint32_t nd = pj_ndst[job];
-#pragma unroll 1
-                    for (uint32_t x = 0; x < nd; ++x) {
-                        const uint32_t e = pj_dst[job * N + x];
-                        const uint32_t q = e >> 16, j = e & 0xffffu;
-                        reinterpret_cast<V*>(p.region[q] + aug_off + uint64_t(p.nmax + j) * S)[off] = r[u];
-                    }
+                    const uint32_t j = gv / nvec, off = gv - j * nvec;
+                    my_aug[uint64_t(p.nmax + j) * nvec + off] = rg[u];
                 } else {
                     const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
-                    slab[uint64_t(win[2 * job + 1]) * nvec + off] = r[u];
+                    slab[uint64_t(win[2 * job + 1]) * nvec + off] = rg[u];
                 }
             }
         }
@@ -911,64 +1007,66 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         atomicMin(p.trace + 22, globaltimer());  // first warp out of the chunk loop
         atomicMax(p.trace + 18, globaltimer());  // last warp out
     }
-    // ---- C: hazard writes over this CTA's push slice, after ALL its reads (barrier only
-    //      when this CTA has one; the condition is uniform: it reads staged lists) --------
+    // ---- C: writes to rows this CTA pulled, after ALL its pulls (barrier only when this
+    //      CTA has one; the condition is uniform: it reads staged lists) ------------------
     const uint32_t clo = blo, chi = min(bhi, pv_tot);
     bool any_post = false;
     if (clo < chi) {
         const uint32_t j0 = clo / nvec, j1 = (chi - 1) / nvec;
         for (uint32_t j = j0; j <= j1; ++j)
-            any_post |= pj_post[j] >= 0;
+            any_post |= post[j] >= 0;
     }
     if (any_post) {
         __syncthreads();
 #pragma unroll 1
         for (uint32_t gv = clo + tid; gv < chi; gv += kThreads) {
-            const uint32_t job = gv / nvec, off = gv - job * nvec;
-            const int post = pj_post[job];
-            if (post >= 0)
-                slab[uint64_t(pj_src[job]) * nvec + off] = ld_vec(batch + uint64_t(post) * nvec + off);
+            const uint32_t j = gv / nvec, off = gv - j * nvec;
+            const int pr = post[j];
+            if (pr >= 0)
+                slab[uint64_t(prow[j]) * nvec + off] = ld_vec(batch + uint64_t(pr) * nvec + off);
         }
     }
     trace_at(p, 19);
-
-    // ---- completion handshake (multi-rank): the last CTA of this rank to finish tells
-    // every requester that all pushes of step i into it have landed, then waits until
-    // every owner has done the same for us — so this launch's completion implies m'_i is
-    // complete (the promise resolution of engine.cpp:169).
-    if (do_push && multi) {
-        __threadfence_system();
+    if (multi) {
+        const uint32_t n_def = misc[2];
+        // ---- pulls of this rank done -> readdone[me] at every peer (last CTA). The pulled
+        //      values were consumed before the barrier, so a relaxed ticket suffices; the
+        //      flag itself is a release store (no bulk fence on the stores of the copy).
         __syncthreads();
         if (tid == 0) {
-            const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->ticket), 1ull);
+            const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->rticket), 1ull);
             if ((t + 1) % gridDim.x == 0) {
-                __threadfence_system();
-                for (uint32_t w = 0; w < N; ++w) {
-                    if (w == me)
-                        continue;
-                    RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[w]);
-                    st_release_sys(&peer->arrive[me], p.step + 1);
-                }
-                const uint64_t t0 = globaltimer();
-                bool to = false;
-                for (uint32_t w = 0; w < N && !to; ++w) {
-                    if (w == me)
-                        continue;
-                    while (ld_acquire_sys(&hdr->arrive[w]) < p.step + 1) {
-                        if (globaltimer() - t0 > p.timeout_ns) {
-                            to = true;
-                            break;
-                        }
-                        __nanosleep(32);
-                    }
-                }
-                if (to && p.mailbox) {
-                    volatile uint32_t* mb = p.mailbox;
-                    mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
-                    mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
-                }
+                if (p.trace)
+                    p.trace[23] = globaltimer();
+                for (uint32_t w = 0; w < N; ++w)
+                    st_relaxed_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->readdone[me], p.step + 1);
             }
         }
+        // ---- D: writes to rows remote requesters pull, after their pulls ------------------
+        if (n_def) {
+            if (tid == 0) {
+                uint32_t readers = 1u << me;  // own pulls of the row too (other CTAs)
+                for (uint32_t x = 0; x < n_def; ++x)
+                    readers |= defer[3 * x + 2];
+                for (uint32_t w = 0; w < N; ++w)
+                    if (((readers >> w) & 1u) && !wait_flag(&hdr->readdone[w], p.step + 1, p.timeout_ns) &&
+                        p.mailbox) {
+                        volatile uint32_t* mb = p.mailbox;
+                        mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
+                        mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
+                    }
+            }
+            __syncthreads();
+            const uint32_t tvd = n_def * nvec;
+            const uint32_t dlo = static_cast<uint32_t>(uint64_t(tvd) * part / parts);
+            const uint32_t dhi = static_cast<uint32_t>(uint64_t(tvd) * (part + 1) / parts);
+#pragma unroll 1
+            for (uint32_t gv = dlo + tid; gv < dhi; gv += kThreads) {
+                const uint32_t x = gv / nvec, off = gv - x * nvec;
+                slab[uint64_t(defer[3 * x + 1]) * nvec + off] = ld_vec(batch + uint64_t(defer[3 * x]) * nvec + off);
+            }
+        }
+        // (done[me] = i+1 is published by copy(i+1) at its start)
     }
     if (p.trace && tid == 0)
         atomicMax(p.trace + 15, globaltimer());
