@@ -206,7 +206,8 @@ DRB_RB_API drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint3
  * back to back from native code on `stream`. The throughput-harness analogue of
  * drb_overlap_bench (proj/include/drb.h:107-114, proj/src/runner/overlap.cpp:83-89, zero
  * train cost). If step_events is non-NULL it must hold 2*steps cudaEvent_t created by the
- * caller; launch i is bracketed by events 2i and 2i+1 (per-launch device timing). */
+ * caller; iteration i's copy kernel (the dominant one) is bracketed by events 2i and 2i+1,
+ * recorded after its dependencies resolved (per-launch device timing). */
 DRB_RB_API drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride,
                                  const uint32_t* labels, uint64_t label_stride, uint32_t ring,
                                  uint32_t n, uint64_t steps, uint64_t first, void* stream,
@@ -219,7 +220,8 @@ typedef struct drb_rb_graph drb_rb_graph;
 DRB_RB_API drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_stride,
                                            const uint32_t* labels, uint64_t label_stride,
                                            uint32_t ring, uint32_t n, uint64_t steps,
-                                           uint64_t first, drb_rb_graph** out);
+                                           uint64_t first, void* const* step_events,
+                                           drb_rb_graph** out);
 DRB_RB_API drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream);
 DRB_RB_API drb_status drb_rb_graph_destroy(drb_rb_graph* g);
 /* Rows of m' for a completed step (blocks on that step's completion). */

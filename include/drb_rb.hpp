@@ -1,0 +1,283 @@
+// drb_rb.hpp — header-only C++ facade over the C ABI (drb_rb.h), mirroring the reference's
+// hot-path C++ API so call sites port one-to-one:
+//
+//   reference (proj/src/...)                          this facade (namespace drb::b200)
+//   rng_stream(seed, worker, purpose)  core/rng.hpp   rng_stream(seed, worker, purpose)
+//   rng_stream::keyed(...)                            rng_stream::keyed(...)
+//   sample_without_replacement(n, k, rng)             sample_without_replacement(n, k, rng)
+//   rehearsal_buffer(K, cap)   buffer/rehearsal_buffer.hpp:62
+//                                                     rehearsal_buffer(config)  (S, max batch,
+//                                                     c, r, rank, world, device fixed at creation)
+//   update_buffer(m, c, cand, evict)                  update_buffer(device_batch, c, cand, evict)
+//   read_slots(requests, substitute_rng)              read_slots(requests, substitute_rng, out...)
+//   snapshot() / total_stored() / cross_class_evictions()   same
+//   plan(want, view, rng)      sampler/sampler.hpp:33 plan(want, view, rng)
+//   engine(cfg, rank, buffer, table, client)  engine/engine.hpp:53
+//                                                     engine(rehearsal_buffer&)
+//   engine::start / update / shutdown / total_wait_ms        same; update() returns the fused
+//                                                     augmented batch m'_i = m_i ++ reps(i-1)
+//   augment(m, reps)           sampler/sampler.hpp:61 augmented_batch (already m ++ reps)
+//
+// Errors are thrown as the reference's exception taxonomy (proj/src/core/errors.hpp):
+// config_error, usage_error, transport_error, engine_error; anything else drb_error.
+// Device memory is plain device pointers: the caller owns batches, the engine owns m'.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "drb_rb.h"
+
+namespace drb::b200 {
+
+struct drb_error : std::runtime_error {
+    drb_status status;
+    drb_error(drb_status s, const std::string& w) : std::runtime_error(w), status(s) {}
+};
+struct config_error : drb_error {
+    using drb_error::drb_error;
+};
+struct usage_error : drb_error {
+    using drb_error::drb_error;
+};
+struct transport_error : drb_error {
+    using drb_error::drb_error;
+};
+struct engine_error : drb_error {
+    using drb_error::drb_error;
+};
+
+inline void check(drb_status s) {
+    if (s == DRB_OK)
+        return;
+    const std::string msg = drb_rb_last_error();
+    switch (s) {
+    case DRB_ERR_CONFIG: throw config_error(s, msg);
+    case DRB_ERR_USAGE: throw usage_error(s, msg);
+    case DRB_ERR_TRANSPORT: throw transport_error(s, msg);
+    case DRB_ERR_TRAINING: throw engine_error(s, msg);
+    default: throw drb_error(s, msg);
+    }
+}
+
+class rng_stream {
+public:
+    enum class purpose : std::uint32_t {
+        candidate_selection = 1,
+        eviction = 2,
+        global_sampling = 3,
+        data_shuffle = 4,
+        model_init = 5,
+        slot_substitute = 6,
+        synth = 7,
+    };
+    rng_stream(std::uint64_t seed, std::uint32_t worker, purpose p, int device = 0) : device_(device) {
+        check(drb_rng_init(&s_, seed, worker, static_cast<std::uint32_t>(p)));
+    }
+    static rng_stream keyed(std::uint64_t seed, std::uint32_t worker, purpose p, std::uint64_t k1,
+                            std::uint64_t k2 = 0, int device = 0) {
+        rng_stream r(seed, worker, p, device);
+        check(drb_rng_keyed(&r.s_, seed, worker, static_cast<std::uint32_t>(p), k1, k2));
+        return r;
+    }
+    std::uint64_t next_u64() {
+        std::uint64_t v = 0;
+        check(drb_rng_draw(&s_, 0, 1, &v, device_));
+        return v;
+    }
+    std::uint64_t bounded(std::uint64_t n) {
+        if (n == 0)
+            throw usage_error(DRB_ERR_USAGE, "bounded: n must be nonzero");
+        std::uint64_t v = 0;
+        check(drb_rng_draw(&s_, n, 1, &v, device_));
+        return v;
+    }
+    std::uint64_t counter() const { return s_.ctr; }
+    drb_rng* raw() { return &s_; }
+    int device() const { return device_; }
+
+private:
+    drb_rng s_{};
+    int device_ = 0;
+};
+
+inline std::vector<std::uint32_t> sample_without_replacement(std::uint32_t n, std::uint32_t k, rng_stream& rng) {
+    std::vector<std::uint32_t> out(k < n ? k : n);
+    std::uint32_t got = 0;
+    check(drb_sample_without_replacement(n, k, rng.raw(), out.data(), &got, rng.device()));
+    out.resize(got);
+    return out;
+}
+
+struct slot_ref {
+    std::uint32_t owner = 0, cls = 0, slot = 0;
+    bool operator==(const slot_ref&) const = default;
+};
+
+struct sampling_plan {
+    std::vector<slot_ref> entries;
+};
+
+// plan(want, view, rng): view = occupancy[n_workers][n_classes] (sampler.cpp:65-68)
+inline sampling_plan plan(std::uint32_t want, const std::vector<std::vector<std::uint32_t>>& view, rng_stream& rng) {
+    const std::uint32_t nw = static_cast<std::uint32_t>(view.size());
+    const std::uint32_t nk = nw ? static_cast<std::uint32_t>(view[0].size()) : 0;
+    std::vector<std::uint32_t> flat;
+    std::uint64_t total = 0;
+    for (const auto& row : view)
+        for (auto o : row) {
+            flat.push_back(o);
+            total += o;
+        }
+    sampling_plan p;
+    p.entries.resize(want < total ? want : total);
+    std::uint32_t got = 0;
+    check(drb_plan(want, nw, nk, flat.data(), rng.raw(), reinterpret_cast<drb_slot_ref*>(p.entries.data()), &got,
+                   rng.device()));
+    p.entries.resize(got);
+    return p;
+}
+
+struct device_batch {  // a mini-batch resident in device memory
+    const void* data = nullptr;        // n x S bytes
+    const std::uint32_t* labels = nullptr;
+    std::uint32_t n = 0;
+};
+
+struct insertion_report {
+    std::vector<std::uint32_t> per_class_appends, per_class_replacements;
+    std::uint32_t appends = 0, replacements = 0;
+};
+
+struct occupancy_snapshot {
+    std::vector<std::uint32_t> per_class;
+    std::uint64_t version = 0;
+    std::uint64_t total() const {
+        std::uint64_t t = 0;
+        for (auto o : per_class)
+            t += o;
+        return t;
+    }
+};
+
+class rehearsal_buffer {
+public:
+    explicit rehearsal_buffer(const drb_rb_config& cfg) : cfg_(cfg) { check(drb_rb_create(&cfg_, &h_)); }
+    rehearsal_buffer(std::uint32_t n_classes, std::uint32_t per_class_cap, std::uint64_t sample_bytes,
+                     std::uint32_t max_batch = 64, std::uint32_t c = 14, std::uint32_t r = 7, std::uint64_t seed = 1,
+                     int device = 0)
+        : rehearsal_buffer(drb_rb_config{n_classes, per_class_cap, sample_bytes, max_batch, c, r, 0, 1, seed, device, 0}) {}
+    ~rehearsal_buffer() {
+        if (h_)
+            drb_rb_destroy(h_);
+    }
+    rehearsal_buffer(const rehearsal_buffer&) = delete;
+    rehearsal_buffer& operator=(const rehearsal_buffer&) = delete;
+
+    insertion_report update_buffer(const device_batch& m, std::uint32_t candidate_count, rng_stream& cand,
+                                   rng_stream& evict) {
+        insertion_report rep;
+        rep.per_class_appends.assign(cfg_.n_classes, 0);
+        rep.per_class_replacements.assign(cfg_.n_classes, 0);
+        drb_insertion_report r{rep.per_class_appends.data(), rep.per_class_replacements.data(), 0, 0};
+        check(drb_rb_update_buffer(h_, m.data, m.labels, m.n, candidate_count, cand.raw(), evict.raw(), &r));
+        rep.appends = r.appends;
+        rep.replacements = r.replacements;
+        return rep;
+    }
+    occupancy_snapshot snapshot() const {
+        occupancy_snapshot s;
+        s.per_class.assign(cfg_.n_classes, 0);
+        check(drb_rb_snapshot(h_, s.per_class.data(), &s.version));
+        return s;
+    }
+    std::uint64_t total_stored() const {
+        std::uint64_t v = 0;
+        check(drb_rb_total_stored(h_, &v));
+        return v;
+    }
+    std::uint64_t cross_class_evictions() const {
+        std::uint64_t v = 0;
+        check(drb_rb_cross_class_evictions(h_, &v));
+        return v;
+    }
+    // read_slots: out / out_labels are device buffers of requests.size() rows
+    std::vector<std::uint8_t> read_slots(const std::vector<drb_read_request>& requests, rng_stream& substitute,
+                                         void* out, std::uint32_t* out_labels) {
+        std::vector<std::uint8_t> status(requests.size());
+        check(drb_rb_read_slots(h_, requests.data(), static_cast<std::uint32_t>(requests.size()), substitute.raw(),
+                                out, out_labels, status.data()));
+        return status;
+    }
+    std::vector<std::uint8_t> export_handle() const {
+        std::vector<std::uint8_t> blob(drb_rb_handle_size());
+        std::size_t len = blob.size();
+        check(drb_rb_export_handle(h_, blob.data(), &len));
+        return blob;
+    }
+    void connect(const std::vector<std::uint8_t>& all_blobs) { check(drb_rb_connect(h_, all_blobs.data(), all_blobs.size())); }
+    std::uint32_t n_classes() const { return cfg_.n_classes; }
+    std::uint32_t per_class_cap() const { return cfg_.per_class_cap; }
+    drb_rb* raw() const { return h_; }
+
+private:
+    drb_rb_config cfg_{};
+    drb_rb* h_ = nullptr;
+};
+
+// m'_i = m_i ++ reps(i-1), engine-owned; valid until work enqueued before update(i+2).
+class augmented_batch {
+public:
+    augmented_batch(drb_rb* h, const drb_aug& a) : h_(h), a_(a) {}
+    const void* data() const { return a_.data; }
+    const std::uint32_t* labels() const { return a_.labels; }
+    std::uint32_t batch_rows() const { return a_.n; }
+    std::uint32_t count() const {  // blocks until this iteration's m' is complete
+        std::uint32_t c = 0;
+        check(drb_rb_aug_count(h_, &a_, &c));
+        return c;
+    }
+    std::uint32_t reps() const { return count() - a_.n; }
+
+private:
+    drb_rb* h_;
+    drb_aug a_;
+};
+
+class engine {
+public:
+    explicit engine(rehearsal_buffer& b) : b_(b) {}
+    ~engine() {
+        if (started_ && !shut_)
+            drb_rb_shutdown(b_.raw());
+    }
+    void start() {
+        check(drb_rb_start(b_.raw()));
+        started_ = true;
+    }
+    // engine.update(m) fused with augment(m, reps) (trainer.cpp:109-113); stream: cudaStream_t
+    augmented_batch update(const device_batch& m, void* stream = nullptr) {
+        drb_aug a{};
+        check(drb_rb_step(b_.raw(), m.data, m.labels, m.n, stream, &a));
+        return augmented_batch(b_.raw(), a);
+    }
+    void shutdown() {
+        check(drb_rb_shutdown(b_.raw()));
+        shut_ = true;
+    }
+    double total_wait_ms() const {
+        double v = 0;
+        check(drb_rb_total_wait_ms(b_.raw(), &v));
+        return v;
+    }
+    void synchronize() { check(drb_rb_synchronize(b_.raw())); }
+
+private:
+    rehearsal_buffer& b_;
+    bool started_ = false, shut_ = false;
+};
+
+}  // namespace drb::b200

@@ -740,7 +740,8 @@ void enqueue_plan(drb_rb* h, uint64_t i) {
 
 // copy(i) on `s`: W_i from sel(i), P_i from plan(i-1), slab writes of round i-1 from copy(i-1).
 void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
-                  cudaStream_t s, bool first_of_run, drb_aug* out) {
+                  cudaStream_t s, bool first_of_run, drb_aug* out, cudaEvent_t ev_begin = nullptr,
+                  cudaEvent_t ev_end = nullptr) {
     StepParams p = iter_params(h, i, batch, labels, n);
     if (h->trace) {
         cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
@@ -755,8 +756,17 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
     const bool pdl = h->use_pdl && !first_of_run && s == h->last_copy_stream && have1;
     if (have1 && s != h->last_copy_stream)
         cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i - 1)], 0), "wait");
+    // timing events after every dependency: they bracket the copy kernel alone. External
+    // records stay real (timeable) records when captured into a graph.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(s, &cap), "capture query");
+    const unsigned rec_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+    if (ev_begin)
+        cuda_check(cudaEventRecordWithFlags(ev_begin, s, rec_flags), "event");
     if (launch_copy(p, h->grid, s, pdl))
         fail(DRB_ERR_INTERNAL, std::string("copy launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    if (ev_end)
+        cuda_check(cudaEventRecordWithFlags(ev_end, s, rec_flags), "event");
     cuda_check(cudaEventRecord(h->ev_copy[ev_of(i)], s), "event");
     cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
     h->last_copy_stream = s;
@@ -825,11 +835,9 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
                 enqueue_sel(h, i + 2, bat(i + 2 - i0), lab(i + 2 - i0), n, s, false);
             if (i + 1 < end)
                 enqueue_plan(h, i + 1);
-            if (step_events)
-                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * (i - i0)]), s), "event");
-            enqueue_copy(h, i, bat(i - i0), lab(i - i0), n, s, i == i0, nullptr);
-            if (step_events)
-                cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(step_events[2 * (i - i0) + 1]), s), "event");
+            enqueue_copy(h, i, bat(i - i0), lab(i - i0), n, s, i == i0, nullptr,
+                         step_events ? static_cast<cudaEvent_t>(step_events[2 * (i - i0)]) : nullptr,
+                         step_events ? static_cast<cudaEvent_t>(step_events[2 * (i - i0) + 1]) : nullptr);
         }
     });
 }
@@ -847,7 +855,8 @@ extern "C" {
 
 drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_stride,
                                 const uint32_t* labels, uint64_t label_stride, uint32_t ring,
-                                uint32_t n, uint64_t steps, uint64_t first, drb_rb_graph** out) {
+                                uint32_t n, uint64_t steps, uint64_t first, void* const* step_events,
+                                drb_rb_graph** out) {
     DRB_REQUIRE(h && batches && labels && ring > 0 && out);
     *out = nullptr;
     return guarded([&] {
@@ -862,7 +871,7 @@ drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_s
         cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
         cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
         drb_status st = drb_rb_run(h, batches, batch_stride, labels, label_stride, ring, n, steps,
-                                   first, cs, nullptr);
+                                   first, cs, step_events);
         const std::string err = t_last_error;
         if (st == DRB_OK && steps > 0) {  // join the forked sel/plan streams into the capture
             const int e = int((h->step - 1) % drb_rb::kEv);

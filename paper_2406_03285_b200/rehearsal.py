@@ -368,14 +368,18 @@ class engine:
         self.iteration += steps
 
     def prepare_run(self, data_ring: torch.Tensor, label_ring: torch.Tensor, steps: int,
-                    first: int = 0) -> "prepared_run":
-        """Capture `steps` iterations (as run()) into a CUDA graph; launch it once, in order."""
+                    first: int = 0, events=None) -> "prepared_run":
+        """Capture `steps` iterations (as run()) into a CUDA graph; launch it once, in order.
+        events: optional 2*steps torch.cuda.Event (timing) bracketing each copy kernel."""
         B, n = int(data_ring.shape[0]), int(data_ring.shape[1])
         if label_ring.shape[0] != B:
             raise _lib.usage_error("prepare_run: data and label rings must have the same length")
+        ev = None
+        if events is not None:
+            ev = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
         g = C.c_void_p()
         check(lib.drb_rb_graph_prepare(self.buffer.h, data_ring.data_ptr(), data_ring.stride(0),
-                                       label_ring.data_ptr(), label_ring.stride(0), B, n, steps, first,
+                                       label_ring.data_ptr(), label_ring.stride(0), B, n, steps, first, ev,
                                        C.byref(g)))
         self.iteration += steps
         return prepared_run(g, (data_ring, label_ring))

@@ -25,9 +25,8 @@ def main():
     spec = stream_spec(K, 2, b, S, steps_per_task=20, seed=seed)
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed, rank=rank,
                                world=world, device=local)
-    blobs = [None] * world
-    dist.all_gather_object(blobs, buf.export_handle())
-    buf.connect(blobs)
+    from paper_2406_03285_b200.dist import connect_world
+    connect_world(buf)
     eng = drb.engine(buf)
     eng.start()
     rep = Backend("port").replay(world, K, cap, S, c, r, seed)
