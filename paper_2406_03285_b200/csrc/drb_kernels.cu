@@ -933,74 +933,97 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             }
         }
     }
+    // ---- A + B with a static per-thread schedule: every thread issues its A loads at
+    //      once, then (lists ready) its B loads, and only then stores — both memory
+    //      latencies overlap. Thread t handles vectors lo + t + k*512 of each slice.
     V* asm_dst = my_aug + uint64_t(row0) * nvec;
-    uint32_t cnt = 0, pv_tot = 0, blo = 0, bhi = 0;
-    bool have_b = false;
-    for (;;) {
-        uint32_t c = 0;
-        if (lane == 0)
-            c = atomicAdd(&misc[4], 1u);
-        c = __shfl_sync(kFull, c, 0);
-        if (c < a_chunks) {  // ---- A chunk --------------------------------------------
-            const uint32_t base = alo + c * (32u * UA);
-            V rg[UA];
-#pragma unroll
-            for (int u = 0; u < UA; ++u) {
-                const uint32_t gv = base + u * 32 + lane;
-                if (gv < ahi)
-                    rg[u] = ld_vec(batch + gv);
-            }
-#pragma unroll
-            for (int u = 0; u < UA; ++u) {
-                const uint32_t gv = base + u * 32 + lane;
-                if (gv < ahi)
-                    asm_dst[gv] = rg[u];
-            }
-            continue;
+    constexpr int KA = sizeof(V) == 16 ? 8 : 16;  // A vectors in flight per thread
+    constexpr int KB = sizeof(V) == 16 ? 4 : 8;   // B vectors in flight per thread
+    const uint32_t T = kThreads;
+    (void)a_chunks;
+    auto b_src = [&](uint32_t gv, uint32_t pv_tot) -> const V* {
+        if (gv < pv_tot) {
+            const uint32_t j = gv / nvec, off = gv - j * nvec;
+            return reinterpret_cast<const V*>(p.slab_peer[praw[4 + j]]) + uint64_t(praw[4 + R + j]) * nvec + off;
         }
-        if (!have_b) {  // lists staged and peers ready (warp 0)
-            if (p.trace && blockIdx.x == 0 && lane == 0)
-                atomicMin(p.trace + 21, globaltimer());
-            while (*ready == 0)
-                __nanosleep(20);
-            __threadfence_block();
-            cnt = misc[0];
-            pv_tot = cnt * nvec;
-            const uint32_t tvb = pv_tot + misc[1] * nvec;
-            blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
-            bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
-            have_b = true;
+        const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
+        return batch + uint64_t(win[2 * job]) * nvec + off;
+    };
+    auto b_store = [&](uint32_t gv, uint32_t pv_tot, const V& v) {
+        if (gv < pv_tot) {
+            const uint32_t j = gv / nvec, off = gv - j * nvec;
+            my_aug[uint64_t(p.nmax + j) * nvec + off] = v;
+        } else {
+            const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
+            slab[uint64_t(win[2 * job + 1]) * nvec + off] = v;
         }
-        const uint32_t base = blo + (c - a_chunks) * (32u * UB);
-        if (base >= bhi)
-            break;
-        // ---- B chunk: pulls into m'_i + plain candidate writes ---------------------------
-        V rg[UB];
+    };
+    V ra[KA];
+    uint32_t a_next = alo + tid;
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-            const uint32_t gv = base + u * 32 + lane;
-            if (gv < bhi) {
-                if (gv < pv_tot) {
-                    const uint32_t j = gv / nvec, off = gv - j * nvec;
-                    rg[u] = ld_pull(reinterpret_cast<const V*>(p.slab_peer[owner[j]]) + uint64_t(prow[j]) * nvec + off);
-                } else {
-                    const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
-                    rg[u] = ld_vec(batch + uint64_t(win[2 * job]) * nvec + off);
-                }
-            }
+    for (int k = 0; k < KA; ++k) {
+        const uint32_t gv = a_next + k * T;
+        if (gv < ahi)
+            ra[k] = ld_vec(batch + gv);
+    }
+    // lists staged (warp 0) -> B bounds
+    if (p.trace && blockIdx.x == 0 && lane == 0)
+        atomicMin(p.trace + 21, globaltimer());
+    while (*ready == 0)
+        __nanosleep(20);
+    __threadfence_block();
+    const uint32_t cnt = misc[0];
+    const uint32_t pv_tot = cnt * nvec;
+    const uint32_t tvb = pv_tot + misc[1] * nvec;
+    const uint32_t blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
+    const uint32_t bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
+    V rb[KB];
+    uint32_t b_next = blo + tid;
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+        const uint32_t gv = b_next + k * T;
+        if (gv < bhi)
+            rb[k] = ld_pull(b_src(gv, pv_tot));
+    }
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+        const uint32_t gv = a_next + k * T;
+        if (gv < ahi)
+            asm_dst[gv] = ra[k];
+    }
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+        const uint32_t gv = b_next + k * T;
+        if (gv < bhi)
+            b_store(gv, pv_tot, rb[k]);
+    }
+    // larger slices: further rounds
+    for (a_next += KA * T; a_next < ahi; a_next += KA * T) {
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const uint32_t gv = a_next + k * T;
+            if (gv < ahi)
+                ra[k] = ld_vec(batch + gv);
         }
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-            const uint32_t gv = base + u * 32 + lane;
-            if (gv < bhi) {
-                if (gv < pv_tot) {
-                    const uint32_t j = gv / nvec, off = gv - j * nvec;
-                    my_aug[uint64_t(p.nmax + j) * nvec + off] = rg[u];
-                } else {
-                    const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
-                    slab[uint64_t(win[2 * job + 1]) * nvec + off] = rg[u];
-                }
-            }
+        for (int k = 0; k < KA; ++k) {
+            const uint32_t gv = a_next + k * T;
+            if (gv < ahi)
+                asm_dst[gv] = ra[k];
+        }
+    }
+    for (b_next += KB * T; b_next < bhi; b_next += KB * T) {
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            const uint32_t gv = b_next + k * T;
+            if (gv < bhi)
+                rb[k] = ld_pull(b_src(gv, pv_tot));
+        }
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            const uint32_t gv = b_next + k * T;
+            if (gv < bhi)
+                b_store(gv, pv_tot, rb[k]);
         }
     }
     if (p.trace && blockIdx.x == 0 && lane == 0) {
