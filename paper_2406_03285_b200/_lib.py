@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdrb_b200.so")
+LIB_PATH = os.environ.get("DRB_LIB") or os.path.join(HERE, "libdrb_b200.so")  # DRB_LIB: A/B experiments
 
 DRB_OK = 0
 DRB_ERR_INVALID_ARGUMENT = 1

@@ -126,6 +126,7 @@ struct drb_rb {
     drb_rb_config cfg{};
     RegionLayout layout{};
     uint32_t copy_smem = 0;           // dynamic smem of the copy kernel
+    uint32_t solo_smem = 0;           // kSoloSmem unless DRB_SOLO=0
     uint32_t grid = 0;                // copy-kernel CTAs (one wave)
     int sm_count = 0;
     cudaStream_t stream = nullptr;    // default stream of the handle (copy kernel)
@@ -218,6 +219,9 @@ StepParams base_params(drb_rb* h) {
     p.mailbox = h->mailbox_dev;
     p.timeout_ns = h->timeout_ns;
     p.smem_bytes = h->copy_smem;
+    p.solo_smem = h->solo_smem;
+    static const uint32_t dbg = std::getenv("DRB_DBG") ? uint32_t(std::strtoul(std::getenv("DRB_DBG"), nullptr, 0)) : 0u;
+    p.dbg = dbg;
     p.trace = h->trace;
     p.timeline = h->timeline;
     p.timeline_steps = h->timeline_steps ? h->timeline_steps : 1;
@@ -338,6 +342,11 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         h->cfg = c;
         h->layout = region_layout(c.world, c.n_classes, c.sample_bytes, c.max_batch, c.rep_count);
         h->copy_smem = copy_smem(c.world, c.rep_count, c.max_batch).words * 4;
+        {
+            const char* so = std::getenv("DRB_SOLO");  // DRB_SOLO=0: let the kernels share SMs
+            h->solo_smem = (so && so[0] == '0') ? 0u : kSoloSmem;
+            h->copy_smem = std::max(h->copy_smem, h->solo_smem);
+        }
         if (const char* t = std::getenv("DRB_TIMEOUT_MS"))
             h->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
         device_guard g(c.device);
@@ -345,7 +354,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         int per_sm = 0;
         if (copy_kernel_max_ctas_per_sm(h->copy_smem, &per_sm) || per_sm < 1)
             fail(DRB_ERR_CONFIG, "copy kernel does not fit on an SM");
-        h->grid = uint32_t(h->sm_count);  // one copy CTA per SM: a single wave
+        // one copy CTA per SM (a single wave), minus the two SMs sel and plan run on
+        h->grid = uint32_t(h->sm_count) - ((h->solo_smem && h->sm_count > 4) ? 2u : 0u);
         if (const char* gs = std::getenv("DRB_GRID"))
             h->grid = uint32_t(std::strtoul(gs, nullptr, 10));
         cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
@@ -389,12 +399,11 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         if (const char* tl = std::getenv("DRB_TIMELINE")) {
             h->timeline_steps = uint32_t(std::strtoul(tl, nullptr, 10));
             if (h->timeline_steps) {
-                cuda_check(cudaMalloc(&h->timeline, h->timeline_steps * 6ull * 8), "timeline alloc");
-                std::vector<unsigned long long> init(h->timeline_steps * 6ull);
-                for (size_t x = 0; x < init.size(); x += 2) {
-                    init[x] = ~0ull;
-                    init[x + 1] = 0;
-                }
+                cuda_check(cudaMalloc(&h->timeline, h->timeline_steps * uint64_t(kTlStride) * 8), "timeline alloc");
+                std::vector<unsigned long long> init(h->timeline_steps * uint64_t(kTlStride), 0ull);
+                for (size_t x = 0; x < init.size(); x += kTlStride)
+                    for (int k = 0; k < 6; k += 2)
+                        init[x + k] = ~0ull;
                 cuda_check(cudaMemcpy(h->timeline, init.data(), init.size() * 8, cudaMemcpyHostToDevice), "timeline init");
             }
         }
@@ -1026,7 +1035,7 @@ drb_status drb_rb_timeline_read(drb_rb* h, uint64_t* out, uint32_t* steps) {
             return;
         device_guard g(h->cfg.device);
         cuda_check(cudaDeviceSynchronize(), "timeline sync");
-        cuda_check(cudaMemcpy(out, h->timeline, h->timeline_steps * 6ull * 8, cudaMemcpyDeviceToHost), "timeline copy");
+        cuda_check(cudaMemcpy(out, h->timeline, h->timeline_steps * uint64_t(kTlStride) * 8, cudaMemcpyDeviceToHost), "timeline copy");
     });
 }
 

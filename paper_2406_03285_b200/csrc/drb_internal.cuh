@@ -14,6 +14,15 @@ namespace drb_b200 {
 constexpr int kMaxWorld = DRB_RB_MAX_WORLD;
 constexpr int kTableRing = 6;  // occupancy-row versions kept per rank (v % 6); see DESIGN.md §4
 constexpr int kListRing = 4;   // W_i / P_i slots: sel and plan may run up to 4 iterations ahead
+// Every iteration kernel (sel, plan, copy) reserves at least this much dynamic shared
+// memory, so no two of them are ever resident on one SM: sel and plan are latency-bound
+// single-CTA kernels and, next to a copy CTA, their shared/global instructions queue behind
+// the copy's memory traffic in the SM's LSU pipe. The copy grid leaves two SMs for them.
+constexpr uint32_t kSoloSmem = 116u * 1024u;
+// DRB_TIMELINE=<steps> record per step: [0,6) kernel start/end, [8,32) phase stamps of
+// CTA 0, then kTlCtaSlots stamps for each of up to kTlMaxCtas copy CTAs.
+constexpr uint32_t kTlCtaSlots = 8, kTlMaxCtas = 160;
+constexpr uint32_t kTlStride = 32 + kTlCtaSlots * kTlMaxCtas;
 constexpr int kAugRing = 3;    // m' buffers per rank; m'_i valid until step i+2 is enqueued
 constexpr int kThreads = 512;  // step kernel CTA size (16 warps)
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
@@ -118,6 +127,8 @@ struct StepParams {
     uint64_t timeout_ns;
     uint32_t vec16;      // 16-byte vector path legal (S % 16 == 0, aligned bases)
     uint32_t smem_bytes;
+    uint32_t solo_smem;
+    uint32_t dbg;        // DRB_DBG experiment bits (0 in production)  // sel / plan dynamic smem floor (kSoloSmem or 0), see below
     unsigned long long* trace;  // optional phase timestamps (CTA 0) + grid min/max, 16 slots
     unsigned long long* timeline;  // optional per-kernel [start, end] per step (kind 0 sel, 1 plan, 2 copy)
     uint32_t timeline_steps;       // ring length of the timeline (entries = steps * 3)
@@ -176,7 +187,7 @@ __host__ __device__ inline PlanSmem plan_smem(uint32_t N, uint32_t K, uint32_t r
     return s;
 }
 struct CopySmem {
-    uint32_t praw, wraw, post, win, defer, misc, words;
+    uint32_t praw, wraw, post, win, defer, rowmap, misc, words;
 };
 __host__ __device__ inline CopySmem copy_smem(uint32_t N, uint32_t r, uint32_t nmax) {
     CopySmem s{};
@@ -186,9 +197,27 @@ __host__ __device__ inline CopySmem copy_smem(uint32_t N, uint32_t r, uint32_t n
     s.post = DRB_TAKE(plist_r(r));          // per pulled rep: local overwrite after the read
     s.win = DRB_TAKE(2 * nmax);             // candidate writes nobody reads this round
     s.defer = DRB_TAKE(3 * nmax);           // writes to rows remote requesters read
+    s.rowmap = DRB_TAKE(nmax);              // batch row -> slab row of its safe write, or -1
     s.misc = DRB_TAKE(32);
     s.words = w;
     return s;
+}
+// TMA copy kernel: the copy lists (CopySmem) + mbarriers + a ring of kTmaChunk-byte stages
+// (A: batch slice, B: pulls / safe writes, C: the round-i bytes of pulled rows).
+constexpr uint32_t kTmaThreads = 64;
+constexpr uint32_t kTmaChunk = 16384;
+constexpr uint32_t kTmaStagesA = 6, kTmaStagesB = 2;
+constexpr uint32_t kTmaStages = kTmaStagesA + kTmaStagesB;  // C mirrors B: ring slots [kTmaStages, +B)
+struct TmaSmem {
+    uint32_t bars, ring, bytes;  // byte offsets
+};
+__host__ __device__ inline TmaSmem tma_smem(uint32_t N, uint32_t r, uint32_t nmax) {
+    TmaSmem t{};
+    const uint32_t lists = copy_smem(N, r, nmax).words * 4;
+    t.bars = (lists + 127u) & ~127u;
+    t.ring = t.bars + 128u * ((8u * (kTmaStages + kTmaStagesB) + 127u) / 128u);
+    t.bytes = t.ring + (kTmaStages + kTmaStagesB) * kTmaChunk;
+    return t;
 }
 #undef DRB_TAKE
 

@@ -373,7 +373,7 @@ __device__ __forceinline__ void warp_copy(uint32_t lo, uint32_t hi, uint32_t* co
 // each step, as globaltimer ns; works inside CUDA graphs.
 __device__ __forceinline__ void tl_mark(const StepParams& p, int kind, bool end) {
     if (p.timeline && threadIdx.x == 0) {
-        unsigned long long* e = p.timeline + 2 * ((p.step % p.timeline_steps) * 3 + kind);
+        unsigned long long* e = p.timeline + (p.step % p.timeline_steps) * kTlStride + 2 * kind;
         if (end)
             atomicMax(e + 1, globaltimer());
         else
@@ -381,9 +381,22 @@ __device__ __forceinline__ void tl_mark(const StepParams& p, int kind, bool end)
     }
 }
 
+// per-CTA copy stamps (timeline mode): slot s of this CTA, written by the calling thread
+__device__ __forceinline__ void cta_mark(const StepParams& p, int slot) {
+    if (p.timeline && blockIdx.x < kTlMaxCtas) {
+        uint64_t t;  // "memory": not reordered with the surrounding loads / stores
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+        p.timeline[(p.step % p.timeline_steps) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = t;
+    }
+}
+
 __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
-    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0)
-        p.trace[slot] = globaltimer();
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
+        if (p.trace)
+            p.trace[slot] = globaltimer();
+        if (p.timeline)  // phase stamps of the pipelined run: slots 8.. of the step's record
+            p.timeline[(p.step % p.timeline_steps) * kTlStride + 8 + slot] = globaltimer();
+    }
 }
 
 }  // namespace
@@ -743,6 +756,155 @@ __device__ bool wait_flag(const uint64_t* flag, uint64_t want, uint64_t timeout_
     return true;
 }
 
+// Copy CTA, warp 0: wait for the staged lists (cp.async), classify W_i's writes — safe
+// (rowmap when fused into A, else `win` jobs), local hazard C (`post`), remote-read D
+// (`defer`) — wait for the owners of remote pulls (done >= i), publish misc[0..2] and the
+// ready flag; CTA 0 also writes m'_i's batch labels and row count.
+struct CopyLists {
+    uint32_t *praw, *wraw, *win, *defer, *misc;
+    int *post, *rowmap;
+    volatile uint32_t* ready;
+};
+__device__ void copy_parse_lists(const StepParams& p, const CopyLists& cl, bool do_pull, bool do_update,
+                                 bool multi, bool fuse) {
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t N = p.N, me = p.me, n = p.n;
+    const uint32_t R = plist_r(p.r), MJ = plist_mj(N, p.r);
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
+    const uint32_t row0 = p.nmax - n;
+    uint32_t* praw = cl.praw;
+    uint32_t* wraw = cl.wraw;
+    uint32_t* win = cl.win;
+    uint32_t* defer = cl.defer;
+    uint32_t* misc = cl.misc;
+    int* post = cl.post;
+    int* rowmap = cl.rowmap;
+    volatile uint32_t* ready = cl.ready;
+    const uint32_t* owner = praw + 4;
+    const uint32_t* prow = praw + 4 + R;
+    const uint32_t* rrow = praw + 4 + 2 * R;
+    const uint32_t* rmask = rrow + MJ;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    const uint32_t cnt = do_pull ? praw[0] : 0;
+    const uint32_t nrem = (do_pull && multi) ? praw[1] : 0;
+    const uint32_t n_win = do_update ? wraw[0] : 0;
+    // round-i writes: to a row this rank pulls -> post on that pull (C); to a row a
+    // remote requester pulls -> deferred (D); otherwise a plain write (B)
+#pragma unroll 1
+    for (uint32_t j = lane; j < cnt; j += 32)
+        post[j] = -1;
+    __syncwarp();
+    uint32_t n_safe = 0, n_def = 0;
+#pragma unroll 1
+    for (uint32_t base = 0; base < n_win; base += 32) {
+        const uint32_t t = base + lane;
+        uint32_t row = 0, key = 0, readers = 0;
+        bool local_hz = false;
+        if (t < n_win) {
+            row = wraw[2 + 2 * t];
+            key = wraw[3 + 2 * t];
+#pragma unroll 1
+            for (uint32_t j = 0; j < cnt; ++j)
+                if (owner[j] == me && prow[j] == key) {
+                    post[j] = static_cast<int>(row);
+                    local_hz = true;
+                    break;
+                }
+#pragma unroll 1
+            for (uint32_t x = 0; x < nrem; ++x)
+                if (rrow[x] == key) {
+                    readers = rmask[x];
+                    break;
+                }
+        }
+        const bool safe = t < n_win && !local_hz && readers == 0;
+        const bool def = t < n_win && readers != 0;
+        const unsigned ms = __ballot_sync(kFull, safe);
+        const unsigned md = __ballot_sync(kFull, def);
+        if (safe) {
+            const uint32_t pos = n_safe + __popc(ms & lt);
+            win[2 * pos] = row;
+            win[2 * pos + 1] = key;
+        }
+        if (def) {  // (a local hazard that is also remote-read: D after the local read
+                    //  — D runs after this CTA's barrier anyway)
+            const uint32_t pos = n_def + __popc(md & lt);
+            defer[3 * pos] = row;
+            defer[3 * pos + 1] = key;
+            defer[3 * pos + 2] = readers;
+        }
+        n_safe += __popc(ms);
+        n_def += __popc(md);
+    }
+    // a local-hazard row that is also remote-read is written in D only
+    if (n_def) {
+#pragma unroll 1
+        for (uint32_t j = lane; j < cnt; j += 32)
+            if (post[j] >= 0)
+#pragma unroll 1
+                for (uint32_t x = 0; x < n_def; ++x)
+                    if (defer[3 * x + 1] == prow[j] && owner[j] == me)
+                        post[j] = -1;
+    }
+    // pulls from a peer need that owner's copy(i-1) complete (its slab at version i)
+    if (multi && cnt) {
+        uint32_t need = 0;
+        for (uint32_t j = lane; j < cnt; j += 32)
+            if (owner[j] != me)
+                need |= 1u << owner[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            need |= __shfl_xor_sync(kFull, need, o);
+        bool ok = true;
+        if (lane < N && ((need >> lane) & 1u))
+            ok = wait_flag(&hdr->done[lane], p.step, p.timeout_ns);
+        if (__any_sync(kFull, !ok) && lane == 0 && p.mailbox) {
+            volatile uint32_t* mb = p.mailbox;
+            mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
+            mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
+        }
+    }
+    if (fuse) {
+#pragma unroll 1
+        for (uint32_t x = lane; x < n; x += 32)
+            rowmap[x] = -1;
+        __syncwarp();
+#pragma unroll 1
+        for (uint32_t x = lane; x < n_safe; x += 32)
+            rowmap[win[2 * x]] = static_cast<int>(win[2 * x + 1]);
+    }
+    if (lane == 0) {
+        misc[0] = cnt;
+        misc[1] = fuse ? 0u : n_safe;
+        misc[2] = n_def;
+    }
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) {
+        *ready = 1;
+        cta_mark(p, 1);
+    }
+    trace_at(p, 20);
+    if (blockIdx.x == 0 && (p.mode & kModeAssemble)) {
+        // m'_i labels of rows [row0, row0+n) and its row count n + |reps(i-1)|
+        uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
+                       uint64_t(p.aslot) * p.auglab_slot_elems;
+#pragma unroll 1
+        for (uint32_t x = lane; x < n; x += 32)
+            al[row0 + x] = __ldg(p.labels + x);
+        if (lane == 0) {
+            hdr->aug_count[p.aslot] = n + cnt;
+            if (p.mailbox) {
+                volatile uint32_t* mb = p.mailbox;
+                mb[p.aslot] = n + cnt;
+                mb[kAugRing + p.aslot] = 0;
+            }
+        }
+    }
+}
+
 // copy(i): m'_i = m_i ++ reps(i-1) and the slab writes of round i. Every CTA owns fixed
 // slices of the vector spaces below; warps claim 32*U-vector chunks of a slice dynamically.
 //   A  m_i -> m'_i rows [nmax-n, nmax)                                   (n rows)
@@ -763,6 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     int* post = reinterpret_cast<int*>(sm + L.post);
     uint32_t* win = sm + L.win;
     uint32_t* defer = sm + L.defer;
+    int* rowmap = reinterpret_cast<int*>(sm + L.rowmap);
     uint32_t* misc = sm + L.misc;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -789,6 +952,8 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
 
     trace_at(p, 16);
     tl_mark(p, 2, false);
+    if (threadIdx.x == 0)
+        cta_mark(p, 0);
     asm volatile("griddepcontrol.launch_dependents;");
     if (p.trace && tid == 0)
         atomicMin(p.trace + 14, globaltimer());
@@ -818,129 +983,46 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     }
     __syncthreads();  // chunk counters / ready flag zeroed; list loads issued
 
-    constexpr int UA = sizeof(V) == 16 ? 8 : 16;
-    constexpr int UB = sizeof(V) == 16 ? 4 : 8;
-    const uint32_t tva = do_assemble ? n * nvec : 0;
-    const uint32_t alo = static_cast<uint32_t>(uint64_t(tva) * part / parts);
-    const uint32_t ahi = static_cast<uint32_t>(uint64_t(tva) * (part + 1) / parts);
-    const uint32_t a_chunks = (ahi - alo + 32 * UA - 1) / (32 * UA);
-    if (warp == 0) {
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
-        const uint32_t cnt = do_pull ? praw[0] : 0;
-        const uint32_t nrem = (do_pull && multi) ? praw[1] : 0;
-        const uint32_t n_win = do_update ? wraw[0] : 0;
-        // round-i writes: to a row this rank pulls -> post on that pull (C); to a row a
-        // remote requester pulls -> deferred (D); otherwise a plain write (B)
-#pragma unroll 1
-        for (uint32_t j = lane; j < cnt; j += 32)
-            post[j] = -1;
-        __syncwarp();
-        uint32_t n_safe = 0, n_def = 0;
-#pragma unroll 1
-        for (uint32_t base = 0; base < n_win; base += 32) {
-            const uint32_t t = base + lane;
-            uint32_t row = 0, key = 0, readers = 0;
-            bool local_hz = false;
-            if (t < n_win) {
-                row = wraw[2 + 2 * t];
-                key = wraw[3 + 2 * t];
-#pragma unroll 1
-                for (uint32_t j = 0; j < cnt; ++j)
-                    if (owner[j] == me && prow[j] == key) {
-                        post[j] = static_cast<int>(row);
-                        local_hz = true;
-                        break;
-                    }
-#pragma unroll 1
-                for (uint32_t x = 0; x < nrem; ++x)
-                    if (rrow[x] == key) {
-                        readers = rmask[x];
-                        break;
-                    }
-            }
-            const bool safe = t < n_win && !local_hz && readers == 0;
-            const bool def = t < n_win && readers != 0;
-            const unsigned ms = __ballot_sync(kFull, safe);
-            const unsigned md = __ballot_sync(kFull, def);
-            if (safe) {
-                const uint32_t pos = n_safe + __popc(ms & lt);
-                win[2 * pos] = row;
-                win[2 * pos + 1] = key;
-            }
-            if (def) {  // (a local hazard that is also remote-read: D after the local read
-                        //  — D runs after this CTA's barrier anyway)
-                const uint32_t pos = n_def + __popc(md & lt);
-                defer[3 * pos] = row;
-                defer[3 * pos + 1] = key;
-                defer[3 * pos + 2] = readers;
-            }
-            n_safe += __popc(ms);
-            n_def += __popc(md);
-        }
-        // a local-hazard row that is also remote-read is written in D only
-        if (n_def) {
-#pragma unroll 1
-            for (uint32_t j = lane; j < cnt; j += 32)
-                if (post[j] >= 0)
-#pragma unroll 1
-                    for (uint32_t x = 0; x < n_def; ++x)
-                        if (defer[3 * x + 1] == prow[j] && owner[j] == me)
-                            post[j] = -1;
-        }
-        // pulls from a peer need that owner's copy(i-1) complete (its slab at version i)
-        if (multi && cnt) {
-            uint32_t need = 0;
-            for (uint32_t j = lane; j < cnt; j += 32)
-                if (owner[j] != me)
-                    need |= 1u << owner[j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                need |= __shfl_xor_sync(kFull, need, o);
-            bool ok = true;
-            if (lane < N && ((need >> lane) & 1u))
-                ok = wait_flag(&hdr->done[lane], p.step, p.timeout_ns);
-            if (__any_sync(kFull, !ok) && lane == 0 && p.mailbox) {
-                volatile uint32_t* mb = p.mailbox;
-                mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
-                mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
-            }
-        }
-        if (lane == 0) {
-            misc[0] = cnt;
-            misc[1] = n_safe;
-            misc[2] = n_def;
-        }
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0)
-            *ready = 1;
-        trace_at(p, 20);
-        if (blockIdx.x == 0 && do_assemble) {
-            // m'_i labels of rows [row0, row0+n) and its row count n + |reps(i-1)|
-            uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
-                           uint64_t(p.aslot) * p.auglab_slot_elems;
-#pragma unroll 1
-            for (uint32_t x = lane; x < n; x += 32)
-                al[row0 + x] = __ldg(p.labels + x);
-            if (lane == 0) {
-                hdr->aug_count[p.aslot] = n + cnt;
-                if (p.mailbox) {
-                    volatile uint32_t* mb = p.mailbox;
-                    mb[p.aslot] = n + cnt;
-                    mb[kAugRing + p.aslot] = 0;
-                }
-            }
-        }
-    }
-    // ---- A + B with a static per-thread schedule: every thread issues its A loads at
-    //      once, then (lists ready) its B loads, and only then stores — both memory
-    //      latencies overlap. Thread t handles vectors lo + t + k*512 of each slice.
-    V* asm_dst = my_aug + uint64_t(row0) * nvec;
+    // ---- A + B with a static per-thread schedule: every thread (warp 0 included) issues
+    //      its A loads at once, then (lists ready) its B loads, and only then stores — both
+    //      memory latencies overlap. Thread t handles vectors lo + t + k*512 of each slice.
+    //      A's stores also perform the safe candidate writes of W_i (batch row -> slab row,
+    //      rowmap) from the same registers; B is then the pulls only.
     constexpr int KA = sizeof(V) == 16 ? 8 : 16;  // A vectors in flight per thread
     constexpr int KB = sizeof(V) == 16 ? 4 : 8;   // B vectors in flight per thread
     const uint32_t T = kThreads;
-    (void)a_chunks;
+    const uint32_t tva = do_assemble ? n * nvec : 0;
+    const uint32_t alo = static_cast<uint32_t>(uint64_t(tva) * part / parts);
+    const uint32_t ahi = static_cast<uint32_t>(uint64_t(tva) * (part + 1) / parts);
+    const V* batch_v = batch;
+    V ra[KA];
+    uint32_t a_next = alo + tid;
+    const bool lists_first = p.dbg & 4;  // every warp waits for the lists before its A loads
+    const bool late0 = ((p.dbg & 2) && warp == 0) || lists_first;
+    if ((p.dbg >> 8) && warp != 0)
+        __nanosleep(p.dbg >> 8);
+    if (!late0) {
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const uint32_t gv = a_next + k * T;
+            if (gv < ahi)
+                ra[k] = ld_vec(batch_v + gv);
+        }
+    }
+    const bool fuse = do_assemble && !(p.dbg & 1);  // safe writes ride on A (else: B jobs)
+    if (warp == 0)
+        copy_parse_lists(p, CopyLists{praw, wraw, win, defer, misc, post, rowmap, ready}, do_pull, do_update,
+                         multi, fuse);
+    V* asm_dst = my_aug + uint64_t(row0) * nvec;
+    auto a_store = [&](uint32_t gv, const V& v) {
+        asm_dst[gv] = v;
+        if (fuse) {
+            const uint32_t row = gv / nvec;
+            const int key = rowmap[row];
+            if (key >= 0)
+                slab[uint64_t(key) * nvec + (gv - row * nvec)] = v;
+        }
+    };
     auto b_src = [&](uint32_t gv, uint32_t pv_tot) -> const V* {
         if (gv < pv_tot) {
             const uint32_t j = gv / nvec, off = gv - j * nvec;
@@ -958,13 +1040,19 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
             slab[uint64_t(win[2 * job + 1]) * nvec + off] = v;
         }
     };
-    V ra[KA];
-    uint32_t a_next = alo + tid;
+    if (tid == 32)
+        cta_mark(p, 2);  // warp 1: A loads issued
+    if (lists_first) {
+        while (*ready == 0)
+            __nanosleep(20);
+    }
+    if (late0) {
 #pragma unroll
-    for (int k = 0; k < KA; ++k) {
-        const uint32_t gv = a_next + k * T;
-        if (gv < ahi)
-            ra[k] = ld_vec(batch + gv);
+        for (int k = 0; k < KA; ++k) {
+            const uint32_t gv = a_next + k * T;
+            if (gv < ahi)
+                ra[k] = ld_vec(batch_v + gv);
+        }
     }
     // lists staged (warp 0) -> B bounds
     if (p.trace && blockIdx.x == 0 && lane == 0)
@@ -972,6 +1060,8 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     while (*ready == 0)
         __nanosleep(20);
     __threadfence_block();
+    if (tid == 32)
+        cta_mark(p, 3);  // warp 1 past the lists-ready wait
     const uint32_t cnt = misc[0];
     const uint32_t pv_tot = cnt * nvec;
     const uint32_t tvb = pv_tot + misc[1] * nvec;
@@ -985,18 +1075,24 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         if (gv < bhi)
             rb[k] = ld_pull(b_src(gv, pv_tot));
     }
+    if (tid == 32)
+        cta_mark(p, 4);  // B loads issued
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
         const uint32_t gv = a_next + k * T;
         if (gv < ahi)
-            asm_dst[gv] = ra[k];
+            a_store(gv, ra[k]);
     }
+    if (tid == 32)
+        cta_mark(p, 5);  // A data in, stores issued
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
         const uint32_t gv = b_next + k * T;
         if (gv < bhi)
             b_store(gv, pv_tot, rb[k]);
     }
+    if (tid == 32)
+        cta_mark(p, 6);  // B data in, stores issued
     // larger slices: further rounds
     for (a_next += KA * T; a_next < ahi; a_next += KA * T) {
 #pragma unroll
@@ -1009,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
         for (int k = 0; k < KA; ++k) {
             const uint32_t gv = a_next + k * T;
             if (gv < ahi)
-                asm_dst[gv] = ra[k];
+                a_store(gv, ra[k]);
         }
     }
     for (b_next += KB * T; b_next < bhi; b_next += KB * T) {
@@ -1096,6 +1192,289 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
+        if (tid == 0)
+            cta_mark(p, 7);
+    }
+}
+
+// ---- TMA bulk-copy path (S % 16 == 0) ---------------------------------------------------
+// The same copy(i) as drb_copy_kernel, moved with the SM's TMA engine instead of LSU
+// loads/stores: 1-D cp.async.bulk global->shared (mbarrier completion) and
+// shared->global (bulk groups). Bytes in flight per SM are bounded by the shared-memory
+// ring (kTmaStages x kTmaChunk), not by the L1 miss-tracking capacity that throttles
+// 16-byte vector loads; two elected threads issue everything:
+//   warp 1 lane 0  A: batch slice -> ring -> m'_i rows, then (lists parsed) the same ring
+//                  bytes -> slab rows of the safe W_i winners (rowmap)
+//   warp 0         staged lists (copy_parse_lists), then lane 0: B pulls owner slab ->
+//                  ring -> m'_i rep rows; C: a round-i write to a pulled row is loaded
+//                  alongside and stored only after the pull's load completed;
+//                  non-fused safe writes (update_buffer without assembly)
+//   all            D (remote-read rows, multi-GPU) after the readers' readdone, LSU path
+__device__ __forceinline__ uint64_t min64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n selp.u32 %0, 1, 0, q;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst_smem)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __grid_constant__ StepParams p) {
+    extern __shared__ __align__(128) uint32_t sm[];
+    const CopySmem L = copy_smem(p.N, p.r, p.nmax);
+    uint32_t* praw = sm + L.praw;
+    uint32_t* wraw = sm + L.wraw;
+    int* post = reinterpret_cast<int*>(sm + L.post);
+    uint32_t* win = sm + L.win;
+    uint32_t* defer = sm + L.defer;
+    int* rowmap = reinterpret_cast<int*>(sm + L.rowmap);
+    uint32_t* misc = sm + L.misc;
+    const TmaSmem T = tma_smem(p.N, p.r, p.nmax);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm) + T.bars);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sm) + T.ring;
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t N = p.N, me = p.me, n = p.n;
+    const uint32_t R = plist_r(p.r);
+    const uint64_t S = p.S;
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
+    const bool do_assemble = p.mode & kModeAssemble;
+    const bool do_pull = (p.mode & kModePlan) && p.step > 0 && p.plist_in;
+    const bool do_update = p.mode & kModeUpdate;
+    const bool multi = (p.mode & kModePeers) && N > 1;
+    const uint32_t part = blockIdx.x, parts = gridDim.x;
+    const uint8_t* batch = reinterpret_cast<const uint8_t*>(p.batch);
+    uint8_t* slab = reinterpret_cast<uint8_t*>(p.slab);
+    uint8_t* my_aug = p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
+    const uint32_t row0 = p.nmax - n;
+    const uint32_t* owner = praw + 4;
+    const uint32_t* prow = praw + 4 + R;
+    volatile uint32_t* ready = misc + 6;
+
+    tl_mark(p, 2, false);
+    if (tid == 0)
+        cta_mark(p, 0);
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (tid < 16)
+        misc[tid] = 0;
+    if (tid == 0 || tid == 32) {  // each engine thread owns its barriers
+        const uint32_t b0 = tid == 0 ? kTmaStagesA : 0, b1 = tid == 0 ? kTmaStages + kTmaStagesB : kTmaStagesA;
+        for (uint32_t b = b0; b < b1; ++b)
+            mbar_init(bars + b, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const uint32_t pw = do_pull ? plist_words(N, p.r) : 0;
+    const uint32_t ww = do_update ? wlist_words(p.nmax) : 0;
+    if (warp == 0) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (multi && blockIdx.x == 0 && lane < N)
+            st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[lane])->done[me], p.step);
+#pragma unroll 1
+        for (uint32_t x = lane; x < pw; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(praw + x)), "l"(p.plist_in + x)
+                         : "memory");
+#pragma unroll 1
+        for (uint32_t x = lane; x < ww; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wraw + x)), "l"(p.wlist + x)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __syncthreads();  // misc / ready zeroed, barriers initialised, list loads issued
+
+    const uint32_t CH = kTmaChunk;
+    if (warp == 1) {
+        // ---- A engine: batch bytes [alo, ahi) of this CTA -> m'_i (+ safe slab rows) ----
+        if (lane == 0) {
+            const uint64_t a16 = do_assemble ? (uint64_t(n) * S) >> 4 : 0;
+            const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
+            const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
+            uint8_t* dst = my_aug + uint64_t(row0) * S;
+            uint32_t ph_base = 0;  // uses of each A barrier so far (parity)
+            bool lists = false;
+            for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
+                const uint32_t w1 = min(nA, w0 + kTmaStagesA);
+                if (w0 > 0)
+                    bulk_wait_read_all();  // the ring's previous window has been stored
+                for (uint32_t k = w0; k < w1; ++k) {
+                    const uint64_t off = alo + uint64_t(k) * CH;
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                    uint64_t* bar = bars + (k - w0);
+                    mbar_expect_tx(bar, len);
+                    bulk_load(ring + (k - w0) * CH, batch + off, len, bar);
+                }
+                if (w0 == 0 && tid == 32)
+                    cta_mark(p, 2);
+                for (uint32_t k = w0; k < w1; ++k) {  // m'_i rows as soon as each piece lands
+                    const uint64_t off = alo + uint64_t(k) * CH;
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                    mbar_wait(bars + (k - w0), ph_base & 1);
+                    bulk_store(dst + off, ring + (k - w0) * CH, len);
+                }
+                bulk_commit();
+                if (w0 == 0)
+                    cta_mark(p, 5);
+                if (!lists) {
+                    while (*ready == 0)
+                        __nanosleep(20);
+                    __threadfence_block();
+                    lists = true;
+                    cta_mark(p, 3);
+                }
+                for (uint32_t k = w0; k < w1; ++k) {  // safe W_i winners among these rows
+                    uint64_t off = alo + uint64_t(k) * CH;
+                    const uint64_t end = off + min64(CH, ahi - off);
+                    while (off < end) {
+                        const uint32_t row = static_cast<uint32_t>(off / S);
+                        const uint64_t rend = min64(end, uint64_t(row + 1) * S);
+                        const int key = rowmap[row];
+                        if (key >= 0)
+                            bulk_store(slab + uint64_t(key) * S + (off - uint64_t(row) * S),
+                                       ring + (k - w0) * CH + (off - (alo + uint64_t(k) * CH)),
+                                       static_cast<uint32_t>(rend - off));
+                        off = rend;
+                    }
+                }
+                bulk_commit();
+                ++ph_base;
+            }
+            bulk_wait_read_all();
+            cta_mark(p, 6);
+        }
+    } else if (warp == 0) {
+        copy_parse_lists(p, CopyLists{praw, wraw, win, defer, misc, post, rowmap, ready}, do_pull, do_update,
+                         multi, do_assemble);
+        if (tid == 0)
+            cta_mark(p, 1);
+        if (lane == 0) {
+            // ---- B engine: pulls (+ C after each pull's read) and non-fused safe writes ----
+            uint8_t* ringB = ring + kTmaStagesA * CH;
+            uint8_t* ringC = ring + kTmaStages * CH;
+            uint64_t* barB = bars + kTmaStagesA;
+            uint64_t* barC = bars + kTmaStages;
+            const uint32_t cnt = misc[0];
+            const uint64_t pv = uint64_t(cnt) * S;
+            const uint64_t sv = do_assemble ? 0 : uint64_t(misc[1]) * S;
+            const uint64_t b16 = (pv + sv) >> 4;
+            const uint64_t blo = (b16 * part / parts) << 4, bhi = (b16 * (part + 1) / parts) << 4;
+            uint32_t use = 0;   // window count (B barrier parity)
+            uint32_t cpar = 0;  // C barrier parities (bit x), armed only with a hazard
+            uint64_t off = blo;
+            while (off < bhi) {
+                // one window: up to kTmaStagesB pieces, each inside one row and <= CH
+                uint64_t poff[kTmaStagesB];
+                uint32_t plen[kTmaStagesB], m = 0;
+                while (m < kTmaStagesB && off < bhi) {
+                    const bool is_pull = off < pv;
+                    const uint64_t base = is_pull ? 0 : pv;
+                    const uint32_t j = static_cast<uint32_t>((off - base) / S);
+                    const uint64_t rend = min64(min64(bhi, is_pull ? pv : pv + sv), base + uint64_t(j + 1) * S);
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, rend - off));
+                    poff[m] = off;
+                    plen[m] = len;
+                    const uint64_t o = off - base - uint64_t(j) * S;
+                    const uint8_t* src = is_pull ? p.slab_peer[owner[j]] + uint64_t(prow[j]) * S + o
+                                                 : batch + uint64_t(win[2 * j]) * S + o;
+                    mbar_expect_tx(barB + m, len);
+                    bulk_load(ringB + m * CH, src, len, barB + m);
+                    if (is_pull && post[j] >= 0) {  // C: the new round-i bytes of the pulled row
+                        mbar_expect_tx(barC + m, len);
+                        bulk_load(ringC + m * CH, batch + uint64_t(post[j]) * S + o, len, barC + m);
+                    }
+                    off += len;
+                    ++m;
+                }
+                if (use == 0 && tid == 0)
+                    cta_mark(p, 4);
+                for (uint32_t x = 0; x < m; ++x) {
+                    const bool is_pull = poff[x] < pv;
+                    const uint64_t base = is_pull ? 0 : pv;
+                    const uint32_t j = static_cast<uint32_t>((poff[x] - base) / S);
+                    const uint64_t o = poff[x] - base - uint64_t(j) * S;
+                    mbar_wait(barB + x, use & 1);  // the pull's read of the slab row is complete
+                    if (is_pull) {
+                        bulk_store(my_aug + uint64_t(p.nmax + j) * S + o, ringB + x * CH, plen[x]);
+                        if (post[j] >= 0) {
+                            mbar_wait(barC + x, (cpar >> x) & 1u);
+                            cpar ^= 1u << x;
+                            bulk_store(slab + uint64_t(prow[j]) * S + o, ringC + x * CH, plen[x]);
+                        }
+                    } else {
+                        bulk_store(slab + uint64_t(win[2 * j + 1]) * S + o, ringB + x * CH, plen[x]);
+                    }
+                }
+                bulk_commit();
+                bulk_wait_read_all();  // the ring is reused by the next window
+                ++use;
+            }
+        }
+    }
+    __syncthreads();  // all pulls of this CTA read, all bulk stores issued and sourced
+    if (multi) {
+        const uint32_t n_def = misc[2];
+        if (tid == 0) {
+            const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->rticket), 1ull);
+            if ((t + 1) % gridDim.x == 0)
+                for (uint32_t w = 0; w < N; ++w)
+                    st_relaxed_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->readdone[me], p.step + 1);
+        }
+        if (n_def) {  // D: rows remote requesters pull, after their pulls (LSU path, rare)
+            if (tid == 0) {
+                uint32_t readers = 1u << me;
+                for (uint32_t x = 0; x < n_def; ++x)
+                    readers |= defer[3 * x + 2];
+                for (uint32_t w = 0; w < N; ++w)
+                    if (((readers >> w) & 1u) && !wait_flag(&hdr->readdone[w], p.step + 1, p.timeout_ns) &&
+                        p.mailbox) {
+                        volatile uint32_t* mb = p.mailbox;
+                        mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
+                        mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
+                    }
+            }
+            __syncthreads();
+            const uint32_t nvec = static_cast<uint32_t>(S / 16);
+            const uint32_t tvd = n_def * nvec;
+            const uint32_t dlo = static_cast<uint32_t>(uint64_t(tvd) * part / parts);
+            const uint32_t dhi = static_cast<uint32_t>(uint64_t(tvd) * (part + 1) / parts);
+            const uint4* bv = reinterpret_cast<const uint4*>(batch);
+            uint4* sv = reinterpret_cast<uint4*>(slab);
+#pragma unroll 1
+            for (uint32_t gv = dlo + tid; gv < dhi; gv += blockDim.x) {
+                const uint32_t x = gv / nvec, o = gv - x * nvec;
+                sv[uint64_t(defer[3 * x + 1]) * nvec + o] = ld_vec(bv + uint64_t(defer[3 * x]) * nvec + o);
+            }
+        }
+    }
+    if (p.timeline) {
+        __syncthreads();
+        tl_mark(p, 2, true);
+        if (tid == 0)
+            cta_mark(p, 7);
     }
 }
 
@@ -1201,7 +1580,13 @@ uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r) { return plan_smem(
 uint32_t plan_threads(uint32_t N) { return 32 * (N + 1 < 3 ? 3 : N + 1); }
 
 namespace {
+constexpr int kMaxDevices = 64;
+// cudaFuncSetAttribute is per device: `cache` holds kMaxDevices entries
 int set_smem(const void* kern, uint32_t bytes, uint32_t* cache) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return -1;
+    cache += dev;
     if (bytes > *cache) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)) != cudaSuccess)
@@ -1213,33 +1598,35 @@ int set_smem(const void* kern, uint32_t bytes, uint32_t* cache) {
 }  // namespace
 
 int launch_sel(const StepParams& p, void* stream) {
-    static uint32_t cache = 0;
-    const uint32_t smem = sel_smem_bytes(p.K, p.nmax);
-    if (set_smem(reinterpret_cast<const void*>(drb_sel_kernel), smem, &cache))
+    static uint32_t cache[kMaxDevices] = {};
+    const uint32_t smem = max(sel_smem_bytes(p.K, p.nmax), p.solo_smem);
+    if (set_smem(reinterpret_cast<const void*>(drb_sel_kernel), smem, cache))
         return -1;
     drb_sel_kernel<<<1, kSelThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_plan_next(const StepParams& p, void* stream) {
-    static uint32_t cache = 0;
-    const uint32_t smem = plan_smem_bytes(p.N, p.K, p.r);
-    if (set_smem(reinterpret_cast<const void*>(drb_plan_next_kernel), smem, &cache))
+    static uint32_t cache[kMaxDevices] = {};
+    const uint32_t smem = max(plan_smem_bytes(p.N, p.K, p.r), p.solo_smem);
+    if (set_smem(reinterpret_cast<const void*>(drb_plan_next_kernel), smem, cache))
         return -1;
     drb_plan_next_kernel<<<1, plan_threads(p.N), smem, static_cast<cudaStream_t>(stream)>>>(p);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl) {
-    static uint32_t cache[2] = {0, 0};
-    const int which = p.vec16 ? 1 : 0;
-    auto kern = p.vec16 ? drb_copy_kernel<uint4> : drb_copy_kernel<uint32_t>;
-    if (set_smem(reinterpret_cast<const void*>(kern), p.smem_bytes, &cache[which]))
+    static uint32_t cache[3][kMaxDevices] = {};
+    const bool tma = p.vec16 && !(p.dbg & 16);  // DRB_DBG bit 4: LSU kernel instead of TMA
+    const int which = tma ? 2 : (p.vec16 ? 1 : 0);
+    auto kern = tma ? drb_copy_tma_kernel : (p.vec16 ? drb_copy_kernel<uint4> : drb_copy_kernel<uint32_t>);
+    const uint32_t smem = tma ? max(p.smem_bytes, tma_smem(p.N, p.r, p.nmax).bytes) : p.smem_bytes;
+    if (set_smem(reinterpret_cast<const void*>(kern), smem, cache[which]))
         return -1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.blockDim = dim3(tma ? kTmaThreads : kThreads);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1250,10 +1637,11 @@ int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl) {
 }
 
 int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {
-    for (auto kern : {drb_copy_kernel<uint4>, drb_copy_kernel<uint32_t>})
+    for (auto kern : {drb_copy_kernel<uint4>, drb_copy_kernel<uint32_t>}) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem_bytes)) != cudaSuccess)
             return -1;
+    }
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, drb_copy_kernel<uint4>, kThreads,
                                                          smem_bytes) == cudaSuccess
                ? 0

@@ -6,7 +6,7 @@ import os
 import sys
 
 STEPS = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-os.environ["DRB_TIMELINE"] = str(4096)
+os.environ["DRB_TIMELINE"] = str(1024)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -31,9 +31,13 @@ g.launch()
 torch.cuda.synchronize()
 n = C.c_uint32(0)
 check(lib.drb_rb_timeline_read(buf.h, None, C.byref(n)))
-t = np.zeros(n.value * 6, np.uint64)
+W = 32 + 8 * 160
+t = np.zeros(n.value * W, np.uint64)
 check(lib.drb_rb_timeline_read(buf.h, t.ctypes.data, C.byref(n)))
-t = t.reshape(n.value, 3, 2).astype(np.int64)
+t = t.reshape(n.value, W).astype(np.int64)
+ph = t[:, 8:32]
+cta = t[:, 32:].reshape(n.value, 160, 8)
+t = t[:, :6].reshape(n.value, 3, 2)
 rows = [(first + i) % n.value for i in range(STEPS)]
 t0 = t[rows[0], 2, 0]
 print(f"{'step':>5} {'sel':>17} {'plan':>17} {'copy':>17}  (us from first copy start)")
@@ -51,3 +55,29 @@ for k, name in ((0, "sel"), (1, "plan")):
     s_ = np.array([t[row, k, 0] for row in rows]); e_ = np.array([t[row, k, 1] for row in rows])
     print(f"{name}: duration median {np.median(e_ - s_) / 1e3:.2f} us; start after copy(i-1) end median "
           f"{np.median(s_[1:] - ce[:-1]) / 1e3:.2f} us; end before copy(i) start median {np.median(cs - e_) / 1e3:.2f} us")
+
+# phase stamps (CTA 0; trace slot s -> timeline word 8+s), medians relative to kernel start
+PH = {"sel": [0, 1, 2, 3, 4], "plan": [5, 6, 7, 8], "copy(cta0)": [16, 20, 19]}
+NM = {0: "start", 1: "loads", 2: "S1", 3: "S2", 4: "end", 5: "start", 6: "view", 7: "draw+locate", 8: "end",
+      16: "start", 20: "lists", 19: "end"}
+for name, slots in PH.items():
+    base = np.array([ph[row, slots[0]] for row in rows])
+    parts = []
+    for s_ in slots[1:]:
+        v = np.array([ph[row, s_] for row in rows])
+        ok = (v > 0) & (base > 0)
+        parts.append(f"{NM[s_]} +{np.median(v[ok] - base[ok]) / 1e3:.2f}" if ok.any() else f"{NM[s_]} -")
+    print(f"{name} phases (us after start): " + ", ".join(parts))
+
+# per-CTA copy stamps relative to the copy's first CTA start, medians over steps
+CN = ["start", "lists", "A issued", "ready(w1)", "B issued", "A stored", "B stored", "end"]
+grid = int(((cta[rows[0], :, 0]) > 0).sum())
+rel = []
+for row in rows[8:]:
+    c = cta[row, :grid].astype(np.float64)
+    rel.append((c - c[:, 0].min()) / 1e3)
+rel = np.array(rel)  # steps x ctas x 8
+print(f"copy CTAs: {grid}; per-slot over CTAs (median step): p10 / p50 / p90 / max  [us from first CTA start]")
+for k, nm in enumerate(CN):
+    v = np.median(rel[:, :, k], axis=0)
+    print(f"  {nm:10s} {np.percentile(v, 10):6.2f} {np.percentile(v, 50):6.2f} {np.percentile(v, 90):6.2f} {v.max():6.2f}")
