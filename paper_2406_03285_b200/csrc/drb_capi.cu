@@ -151,7 +151,7 @@ struct drb_rb {
     uint32_t* wlist = nullptr;        // [kListRing][wlist_words]: W_i, sel(i) -> copy(i)
     uint32_t* mailbox = nullptr;      // host-mapped [4*kAugRing]
     uint32_t* mailbox_dev = nullptr;
-    static constexpr int kEv = 8;
+    static constexpr int kEv = 16;  // >= kListRing + 1: per-iteration events in flight
     cudaEvent_t ev_user[kEv] = {}, ev_sel[kEv] = {}, ev_plan[kEv] = {}, ev_copy[kEv] = {};
     cudaEvent_t done[kAugRing] = {};  // completion of the copy that last wrote each m' slot
     cudaEvent_t in_free[2] = {};      // host path: staging slot reusable
@@ -165,7 +165,13 @@ struct drb_rb {
     cudaStream_t last_copy_stream = nullptr;
     uint64_t ver0 = 0;                // engine: table version / state parities at start()
     uint32_t sel_par0 = 0, plan_par0 = 0;
-    bool use_pdl = false;             // DRB_PDL=1
+    uint32_t dbg_bits = 0;            // DRB_DBG experiment bits (0 in production)
+    bool use_persist = true;
+    bool last_run_persistent = false; // the latest drb_rb_run was one persistent launch          // drb_rb_run as one persistent cooperative launch; DRB_PERSIST=0 off
+    RunCtl* runctl = nullptr;         // device counters of the persistent run
+    cudaEvent_t run_end = nullptr;
+    uint64_t prewaited = 0;           // 1 + the iteration whose sel/plan the copy stream already waited for
+    bool use_pdl = true;              // copy(i+1) launched programmatically behind copy(i); DRB_PDL=0 off
     bool started = false, shut_down = false;
     double wait_ms = 0.0;
     unsigned long long* trace = nullptr;  // DRB_TRACE=1: per-step phase timestamps
@@ -344,7 +350,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         h->copy_smem = copy_smem(c.world, c.rep_count, c.max_batch).words * 4;
         {
             const char* so = std::getenv("DRB_SOLO");  // DRB_SOLO=0: let the kernels share SMs
-            h->solo_smem = (so && so[0] == '0') ? 0u : kSoloSmem;
+            h->solo_smem = (so && so[0] == '0') ? 0u
+                                                : solo_smem_for(tma_smem(c.world, c.rep_count, c.max_batch).bytes);
             h->copy_smem = std::max(h->copy_smem, h->solo_smem);
         }
         if (const char* t = std::getenv("DRB_TIMEOUT_MS"))
@@ -407,10 +414,23 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
                 cuda_check(cudaMemcpy(h->timeline, init.data(), init.size() * 8, cudaMemcpyHostToDevice), "timeline init");
             }
         }
-        if (const char* pd = std::getenv("DRB_PDL"); pd && pd[0] == '1')
-            h->use_pdl = true;
+        if (const char* db = std::getenv("DRB_DBG"))
+            h->dbg_bits = uint32_t(std::strtoul(db, nullptr, 0));
+        if (const char* pd = std::getenv("DRB_PDL"); pd && pd[0] == '0')
+            h->use_pdl = false;
+        if (const char* pe = std::getenv("DRB_PERSIST"); pe && pe[0] == '0')
+            h->use_persist = false;
+        cuda_check(cudaMalloc(&h->runctl, sizeof(RunCtl)), "run state alloc");
+        cuda_check(cudaEventCreateWithFlags(&h->run_end, cudaEventDisableTiming), "event");
         if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
             cuda_check(cudaMalloc(&h->trace, 32 * 8), "trace alloc");
+        if (h->dbg_bits & 64) {
+            int occ = 0;
+            const uint32_t tb = tma_smem(c.world, c.rep_count, c.max_batch).bytes;
+            copy_tma_occupancy(tb, &occ);
+            std::fprintf(stderr, "drb: tma copy smem %u B, %d CTA/SM; sel/plan floor %u B; grid %u\n", tb, occ,
+                         h->solo_smem, h->grid);
+        }
         if (c.world == 1)
             h->connected = true;
         cuda_check(cudaDeviceSynchronize(), "create sync");
@@ -454,6 +474,10 @@ drb_status drb_rb_destroy(drb_rb* h) {
         }
         cudaStreamDestroy(h->stream);
         cudaStreamDestroy(h->s_sel);
+        if (h->runctl)
+            cudaFree(h->runctl);
+        if (h->run_end)
+            cudaEventDestroy(h->run_end);
         cudaStreamDestroy(h->s_plan);
         cudaStreamDestroy(h->h2d);
         cudaStreamDestroy(h->d2h);
@@ -704,8 +728,8 @@ StepParams iter_params(drb_rb* h, uint64_t i, const void* batch, const uint32_t*
     p.aslot = uint32_t(i % kAugRing);
     const uint64_t pw = plist_words(h->cfg.world, h->cfg.rep_count);
     const uint64_t ww = wlist_words(h->cfg.max_batch);
-    p.plist_in = h->plist + (i % kListRing) * pw;         // P_i, built by plan(i-1)
-    p.plist_out = h->plist + ((i + 1) % kListRing) * pw;  // P_{i+1}, built by plan(i)
+    p.plist_in = h->plist + (i % kListRing) * pw;   // X_i, built by plan(i), read by copy(i)
+    p.plist_out = h->plist + (i % kListRing) * pw;
     p.wlist = h->wlist + (i % kListRing) * ww;            // W_i
     p.vec16 = (p.S % 16 == 0) && (n == 0 || aligned16(batch));
     return p;
@@ -714,7 +738,7 @@ StepParams iter_params(drb_rb* h, uint64_t i, const void* batch, const uint32_t*
 constexpr int kE = drb_rb::kEv;
 inline int ev_of(uint64_t i) { return int(i % kE); }
 
-// sel(i) on s_sel: W slot i%4 free once copy(i-4) read it; table slot (i+1)%6 (own row
+// sel(i) on s_sel: W slot i%8 free once copy(i-8) read it; table slot (i+1)%6 (own row
 // v=i+1) free once plan(i-4) read it (peers' rows are ordered by the copy handshake);
 // optionally after the caller's prior work on `caller` (m_i produced, m'_{i-3} consumed).
 void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
@@ -724,44 +748,56 @@ void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* label
         cuda_check(cudaEventRecord(h->ev_user[ev_of(i)], caller), "event");
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_user[ev_of(i)], 0), "wait");
     }
-    if (i >= h->dep_floor + 4) {
-        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - 4)], 0), "wait");
+    if (i >= h->dep_floor + kListRing)
+        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
+    if (i >= h->dep_floor + 4)
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_plan[ev_of(i - 4)], 0), "wait");
-    }
-    if (launch_sel(p, h->s_sel))
+    if (launch_sel(p, h->s_sel, h->use_pdl && (h->dbg_bits & 256)))  // DRB_DBG bit 8: PDL sel chain
         fail(DRB_ERR_INTERNAL, std::string("sel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     cuda_check(cudaEventRecord(h->ev_sel[ev_of(i)], h->s_sel), "event");
     h->ver = h->ver0 + i + 1;
     h->cur_sel = uint32_t((h->sel_par0 + i + 1) & 1);
 }
 
-// plan(i) on s_plan: own row v=i+1 from sel(i); P slot (i+1)%4 free once copy(i-3) read it.
+// plan(i) on s_plan: own row v=i+1 from sel(i); X slot i%8 free once copy(i-8) read it.
 void enqueue_plan(drb_rb* h, uint64_t i) {
     StepParams p = iter_params(h, i, nullptr, nullptr, 0);
     cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_sel[ev_of(i)], 0), "wait");
-    if (i >= h->dep_floor + 3)
-        cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_copy[ev_of(i - 3)], 0), "wait");
-    if (launch_plan_next(p, h->s_plan))
+    if (i >= h->dep_floor + kListRing)
+        cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
+    if (launch_plan_next(p, h->s_plan, h->use_pdl && (h->dbg_bits & 256)))
         fail(DRB_ERR_INTERNAL, std::string("plan launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     cuda_check(cudaEventRecord(h->ev_plan[ev_of(i)], h->s_plan), "event");
     h->cur_plan = uint32_t((h->plan_par0 + i + 1) & 1);
 }
 
-// copy(i) on `s`: W_i from sel(i), P_i from plan(i-1), slab writes of round i-1 from copy(i-1).
+// copy(i) on `s`: W_i from sel(i), X_i from plan(i), slab writes of round i-1 and the reps
+// rows of m'_i from copy(i-1).
+// prewait_next (inside a run, with copy(i+1) to follow on `s`): s also waits here for
+// sel(i+1) / plan(i+1), so copy(i+1)'s only new dependency is copy(i) itself — the edge a
+// programmatic (PDL) launch can overlap (sel/plan run iterations ahead; this costs nothing).
 void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
                   cudaStream_t s, bool first_of_run, drb_aug* out, cudaEvent_t ev_begin = nullptr,
-                  cudaEvent_t ev_end = nullptr) {
+                  cudaEvent_t ev_end = nullptr, bool prewait_next = false) {
     StepParams p = iter_params(h, i, batch, labels, n);
     if (h->trace) {
         cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
         cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
         cuda_check(cudaMemsetAsync(h->trace + 21, 0xff, 16, s), "trace reset");
     }
-    cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i)], 0), "wait");
+    const bool prewaited = !first_of_run && h->prewaited == i + 1 && s == h->last_copy_stream;
+    if (!prewaited) {
+        cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i)], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i)], 0), "wait");
+    }
+    if (prewait_next) {
+        cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i + 1)], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i + 1)], 0), "wait");
+    }
+    h->prewaited = prewait_next ? i + 2 : 0;  // (i+1) + 1: 0 means none
     const bool have1 = i >= h->dep_floor + 1;
-    if (have1)
-        cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i - 1)], 0), "wait");
-    // (measured: PDL between copies delays the event-gated plan chain; off by default)
+    // PDL only between this handle's own consecutive copies inside one run: the copy's
+    // pre-wait prologue reads m_i, which must not be the output of an arbitrary predecessor.
     const bool pdl = h->use_pdl && !first_of_run && s == h->last_copy_stream && have1;
     if (have1 && s != h->last_copy_stream)
         cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i - 1)], 0), "wait");
@@ -790,6 +826,64 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
                       uint64_t(p.aslot) * p.auglab_slot_elems + row0;
     }
     h->step = i + 1;
+}
+
+// drb_rb_run as one persistent cooperative launch: the prior iterations (their
+// sel / plan / copy kernels on any stream) complete first; afterwards every engine stream
+// orders behind the run and later steps wait on no per-iteration event of it.
+void enqueue_persistent_run(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
+                            uint64_t label_stride, uint32_t ring, uint32_t n, uint64_t steps, uint64_t first,
+                            cudaStream_t s) {
+    const uint64_t i0 = h->step, end = i0 + steps;
+    if (i0 >= h->dep_floor + 1) {
+        cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i0 - 1)], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i0 - 1)], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i0 - 1)], 0), "wait");
+    }
+    RunParams rp{};
+    rp.base = iter_params(h, i0, batches, labels, n);
+    rp.batches = batches;
+    rp.batch_stride = batch_stride;
+    rp.labels = labels;
+    rp.label_stride = label_stride;
+    rp.first = first;
+    rp.i0 = i0;
+    rp.steps = steps;
+    rp.ver0 = h->ver0;
+    rp.sel_base = h->sel;
+    rp.plan_base = h->plan;
+    rp.plist_base = h->plist;
+    rp.wlist_base = h->wlist;
+    rp.ctl = h->runctl;
+    rp.ring = ring;
+    rp.n = n;
+    rp.sel_par0 = h->sel_par0;
+    rp.plan_par0 = h->plan_par0;
+    rp.pw = plist_words(h->cfg.world, h->cfg.rep_count);
+    rp.ww = wlist_words(h->cfg.max_batch);
+    const uint32_t grid = uint32_t(h->sm_count);
+    rp.copy_ctas = grid - 2;
+    cuda_check(cudaMemsetAsync(h->runctl, 0, sizeof(RunCtl), s), "run state reset");
+    if (launch_run(rp, grid, s))
+        fail(DRB_ERR_INTERNAL, std::string("persistent run launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(s, &cap), "capture query");
+    if (cap != cudaStreamCaptureStatusActive) {  // (a captured run: graph_launch orders the streams)
+        cuda_check(cudaEventRecord(h->run_end, s), "event");
+        for (cudaStream_t o : {h->stream, h->s_sel, h->s_plan})
+            if (o != s)
+                cuda_check(cudaStreamWaitEvent(o, h->run_end, 0), "wait");
+        for (auto& e : h->done)
+            cuda_check(cudaEventRecord(e, s), "event");
+    }
+    h->last_run_persistent = true;
+    h->ver = h->ver0 + end;
+    h->cur_sel = uint32_t((h->sel_par0 + end) & 1);
+    h->cur_plan = uint32_t((h->plan_par0 + end) & 1);
+    h->dep_floor = end;
+    h->prewaited = 0;
+    h->last_copy_stream = s;
+    h->step = end;
 }
 
 void check_step_args(drb_rb* h, uint32_t n) {
@@ -832,6 +926,12 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
         const uint64_t i0 = h->step, end = i0 + steps;
         if (steps == 0)
             return;
+        const bool vec = (h->cfg.sample_bytes % 16 == 0) && aligned16(batches) && (batch_stride % 16 == 0);
+        h->last_run_persistent = false;
+        if (h->use_persist && !step_events && vec && h->sm_count > 2) {
+            enqueue_persistent_run(h, b, batch_stride, labels, label_stride, ring, n, steps, first, s);
+            return;
+        }
         // Skewed issue order (software pipeline over a resident input ring): sel runs two
         // iterations ahead, plan one, so neither chain waits behind a copy in launch order.
         // Only the first iteration waits for the caller's prior work.
@@ -846,7 +946,8 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
                 enqueue_plan(h, i + 1);
             enqueue_copy(h, i, bat(i - i0), lab(i - i0), n, s, i == i0, nullptr,
                          step_events ? static_cast<cudaEvent_t>(step_events[2 * (i - i0)]) : nullptr,
-                         step_events ? static_cast<cudaEvent_t>(step_events[2 * (i - i0) + 1]) : nullptr);
+                         step_events ? static_cast<cudaEvent_t>(step_events[2 * (i - i0) + 1]) : nullptr,
+                         h->use_pdl && !(h->dbg_bits & 32) && i + 1 < end);
         }
     });
 }
@@ -882,7 +983,7 @@ drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_s
         drb_status st = drb_rb_run(h, batches, batch_stride, labels, label_stride, ring, n, steps,
                                    first, cs, step_events);
         const std::string err = t_last_error;
-        if (st == DRB_OK && steps > 0) {  // join the forked sel/plan streams into the capture
+        if (st == DRB_OK && steps > 0 && !h->last_run_persistent) {  // join the forked sel/plan streams
             const int e = int((h->step - 1) % drb_rb::kEv);
             if (cudaStreamWaitEvent(cs, h->ev_plan[e], 0) != cudaSuccess)
                 st = DRB_ERR_INTERNAL;
@@ -892,6 +993,8 @@ drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_s
         if (st != DRB_OK)
             fail(st, err);
         cuda_check(ce, "end capture");
+        if (const char* dot = std::getenv("DRB_GRAPH_DOT"))  // diagnostics: the captured DAG
+            cudaGraphDebugDotPrint(gr->graph, dot, cudaGraphDebugDotFlagsVerbose);
         cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
         // events recorded during the capture are graph-internal: later steps must not wait
         // on them (graph_launch orders the handle's streams after the whole graph instead)

@@ -13,15 +13,19 @@ namespace drb_b200 {
 
 constexpr int kMaxWorld = DRB_RB_MAX_WORLD;
 constexpr int kTableRing = 6;  // occupancy-row versions kept per rank (v % 6); see DESIGN.md §4
-constexpr int kListRing = 4;   // W_i / P_i slots: sel and plan may run up to 4 iterations ahead
-// Every iteration kernel (sel, plan, copy) reserves at least this much dynamic shared
-// memory, so no two of them are ever resident on one SM: sel and plan are latency-bound
-// single-CTA kernels and, next to a copy CTA, their shared/global instructions queue behind
-// the copy's memory traffic in the SM's LSU pipe. The copy grid leaves two SMs for them.
+constexpr int kListRing = 8;   // W_i / X_i slots: sel and plan may run up to 8 iterations ahead
+// sel and plan reserve at least this much dynamic shared memory, so neither is ever resident
+// next to a copy CTA: they are latency-bound single-CTA kernels and, next to a copy CTA,
+// their shared/global instructions queue behind the copy's memory traffic. The copy grid
+// leaves two SMs for them. The TMA copy kernel stays small enough (<= kSmSmem/2 - 1 KB) for
+// two copy CTAs — copy(i) and the programmatically launched copy(i+1) — to share an SM;
+// solo_smem_for() raises the floor so that sel/plan + one such copy CTA exceed the SM.
 constexpr uint32_t kSoloSmem = 116u * 1024u;
+constexpr uint32_t kSmSmem = 228u * 1024u;      // shared memory per SM (sm_100)
+constexpr uint32_t kCtaReserved = 1024u;        // per-CTA system reservation
 // DRB_TIMELINE=<steps> record per step: [0,6) kernel start/end, [8,32) phase stamps of
 // CTA 0, then kTlCtaSlots stamps for each of up to kTlMaxCtas copy CTAs.
-constexpr uint32_t kTlCtaSlots = 8, kTlMaxCtas = 160;
+constexpr uint32_t kTlCtaSlots = 16, kTlMaxCtas = 160;
 constexpr uint32_t kTlStride = 32 + kTlCtaSlots * kTlMaxCtas;
 constexpr int kAugRing = 3;    // m' buffers per rank; m'_i valid until step i+2 is enqueued
 constexpr int kThreads = 512;  // step kernel CTA size (16 warps)
@@ -60,13 +64,12 @@ struct alignas(16) PlanState {
 // Peer-shareable region header (one cudaMalloc per rank, exported over CUDA IPC).
 struct alignas(256) RegionHeader {
     uint64_t occ_flag[kMaxWorld];  // [w]: latest occupancy version rank w published here
-    uint64_t done[kMaxWorld];      // [w]: 1 + last iteration whose copy rank w completed
-                                   //      (its slab writes of that round are visible)
-    uint64_t readdone[kMaxWorld];  // [w]: 1 + last iteration whose pulls rank w completed
+    uint64_t pushdone[kMaxWorld];  // [w]: 1 + last iteration whose pushes rank w completed
+                                   //      (its reps rows of my m'_{i+1} have landed)
     uint64_t ticket;               // local: CTA completion tickets (last-CTA detection)
-    uint64_t rticket;              // local: CTA tickets after the pull phase
     uint32_t aug_count[4];         // local: rows of m' per ring slot (device copy)
-    uint64_t pad[2];
+    uint32_t repcnt[4];            // local: |reps| already written into m' ring slot s
+    uint64_t pad[4];
 };
 
 struct RegionLayout {
@@ -134,18 +137,43 @@ struct StepParams {
     uint32_t timeline_steps;       // ring length of the timeline (entries = steps * 3)
 };
 
-// Pull list handed from plan(i-1) to copy(i). u32 words:
-//   [0] cnt      — this rank's representatives of round i-1 (= rows pulled into m'_i)
-//   [1] n_remote — rows of MY slab that other requesters read this round
+// Persistent multi-iteration run (drb_rb_run over a device-resident input ring):
+// one cooperative launch, CTA 0 runs the sel chain, CTA 1 the plan chain, CTAs 2.. the copies,
+// handing iterations over through these device counters (run-relative k+1, zeroed per run).
+struct alignas(64) RunCtl {
+    uint64_t sel_done;   // sel of run iteration k finished (W_i, state, own row v=i+1)
+    uint64_t plan_done;  // plan of k finished (X_i)
+    uint64_t b_done;     // every copy CTA's slab writes and pushes of k are complete (in order)
+    uint32_t error;      // sticky: a wait timed out -> every role leaves its loop
+    uint32_t pad[9];
+    uint32_t ticket[8];  // copy-CTA arrivals of iteration k in slot k % 8 (CTAs drift < 8 iterations)
+};
+
+struct RunParams {
+    StepParams base;  // iteration i0 (host iter_params); per-iteration fields patched on device
+    const uint8_t* batches;
+    uint64_t batch_stride;
+    const uint32_t* labels;
+    uint64_t label_stride;
+    uint64_t first, i0, steps, ver0;
+    SelState* sel_base;
+    PlanState* plan_base;
+    uint32_t* plist_base;
+    uint32_t* wlist_base;
+    RunCtl* ctl;
+    uint32_t ring, n, sel_par0, plan_par0, pw, ww, copy_ctas, pad;
+};
+constexpr uint32_t kRunThreads = 32 * (kMaxWorld + 1);  // >= plan_threads(N), >= kSelThreads
+
+// Push list X_i, plan(i) -> copy(i). u32 words:
+//   [0] cnt      — |reps_me(i)|: representative rows of my m'_{i+1}
+//   [1] n_jobs   — entries of plan(i), over every requester, whose slot this rank owns
 //   [2..3] pad
-//   owner[R], row[R]      this rank's plan in draw order (pulled into m'_i row nmax+j);
-//                         row = cls*cap + slot in the owner's slab          (R = max(r,1))
-//   rrow[MJ], rmask[MJ]   remote-read rows of my slab, bit w = requester w reads it
+//   dst[MJ]      (requester q << 24) | position j: the bytes go to q's m'_{i+1} row nmax+j
+//   row[MJ]      slot as cls*cap + slot in my slab                       (MJ = N*max(r,1))
 __host__ __device__ inline uint32_t plist_mj(uint32_t N, uint32_t r) { return N * (r ? r : 1); }
 __host__ __device__ inline uint32_t plist_r(uint32_t r) { return r ? r : 1; }
-__host__ __device__ inline uint32_t plist_words(uint32_t N, uint32_t r) {
-    return 4 + 2 * plist_r(r) + 2 * plist_mj(N, r);
-}
+__host__ __device__ inline uint32_t plist_words(uint32_t N, uint32_t r) { return 4 + 2 * plist_mj(N, r); }
 
 // Candidate-write list W_i, sel(i) -> copy(i). u32 words: [0] n_win, then (batch row,
 // slab row) pairs of round i's winning candidates (last writer of each (class, slot)).
@@ -187,27 +215,27 @@ __host__ __device__ inline PlanSmem plan_smem(uint32_t N, uint32_t K, uint32_t r
     return s;
 }
 struct CopySmem {
-    uint32_t praw, wraw, post, win, defer, rowmap, misc, words;
+    uint32_t xraw, wraw, jsrc, rowmap, misc, words;
 };
 __host__ __device__ inline CopySmem copy_smem(uint32_t N, uint32_t r, uint32_t nmax) {
     CopySmem s{};
     uint32_t w = 0;
-    s.praw = DRB_TAKE(plist_words(N, r));   // pull list verbatim
-    s.wraw = DRB_TAKE(wlist_words(nmax));   // W_i verbatim
-    s.post = DRB_TAKE(plist_r(r));          // per pulled rep: local overwrite after the read
-    s.win = DRB_TAKE(2 * nmax);             // candidate writes nobody reads this round
-    s.defer = DRB_TAKE(3 * nmax);           // writes to rows remote requesters read
-    s.rowmap = DRB_TAKE(nmax);              // batch row -> slab row of its safe write, or -1
+    s.xraw = DRB_TAKE(plist_words(N, r));  // push list X_i verbatim
+    s.wraw = DRB_TAKE(wlist_words(nmax));  // W_i verbatim
+    s.jsrc = DRB_TAKE(plist_mj(N, r));     // per job: source row (bit 31: batch row, else slab)
+    s.rowmap = DRB_TAKE(nmax);             // batch row -> slab row of its W_i write, or -1
     s.misc = DRB_TAKE(32);
     s.words = w;
     return s;
 }
 // TMA copy kernel: the copy lists (CopySmem) + mbarriers + a ring of kTmaChunk-byte stages
-// (A: batch slice, B: pulls / safe writes, C: the round-i bytes of pulled rows).
+// (A: batch slice, B: push jobs / non-fused writes).
 constexpr uint32_t kTmaThreads = 64;
-constexpr uint32_t kTmaChunk = 16384;
-constexpr uint32_t kTmaStagesA = 6, kTmaStagesB = 2;
-constexpr uint32_t kTmaStages = kTmaStagesA + kTmaStagesB;  // C mirrors B: ring slots [kTmaStages, +B)
+constexpr uint32_t kTmaChunk = 8192;
+// A holds a CTA's whole batch slice at the c2 shape (56 x 150528 B / 146 CTAs = 57.7 KB), so
+// copy(i+1) can load and store it to m'_{i+1} while copy(i) still runs (PDL)
+constexpr uint32_t kTmaStagesA = 8, kTmaStagesB = 4;
+constexpr uint32_t kTmaStages = kTmaStagesA + kTmaStagesB;
 struct TmaSmem {
     uint32_t bars, ring, bytes;  // byte offsets
 };
@@ -215,19 +243,59 @@ __host__ __device__ inline TmaSmem tma_smem(uint32_t N, uint32_t r, uint32_t nma
     TmaSmem t{};
     const uint32_t lists = copy_smem(N, r, nmax).words * 4;
     t.bars = (lists + 127u) & ~127u;
-    t.ring = t.bars + 128u * ((8u * (kTmaStages + kTmaStagesB) + 127u) / 128u);
-    t.bytes = t.ring + (kTmaStages + kTmaStagesB) * kTmaChunk;
+    t.ring = t.bars + 128u * ((8u * kTmaStages + 127u) / 128u);
+    t.bytes = t.ring + kTmaStages * kTmaChunk;
     return t;
 }
+// Persistent run kernel (drb_run_kernel): one carve-up serves every role — sel (+ a second
+// label buffer), plan, and the copy role's lists, barriers, A ring and B arena (byte offsets).
+// At least kSoloSmem so exactly one CTA lands on each SM.
+struct RunSmem {
+    uint32_t lists2, prevw, paddr, bars, ring_a, arena, arena_bytes, bytes;
+};
+__host__ __device__ inline RunSmem run_smem(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax) {
+    RunSmem s{};
+    const uint32_t lists = copy_smem(N, r, nmax).words * 4;
+    const uint32_t lw = (plist_words(N, r) + wlist_words(nmax)) * 4;  // second list buffer
+    s.lists2 = (lists + 15u) & ~15u;
+    s.prevw = (s.lists2 + lw + 15u) & ~15u;
+    s.paddr = (s.prevw + nmax * 4u + 15u) & ~15u;  // per B piece: source, destination (u64)
+    s.bars = (s.paddr + 16u * (plist_mj(N, r) + nmax) + 127u) & ~127u;
+    s.ring_a = s.bars + 128u;
+    s.arena = s.ring_a + kTmaStagesA * kTmaChunk;
+    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax) * 4, plan_b = plan_smem(N, K, r).words * 4;
+    const uint32_t ctl = sel_b > plan_b ? sel_b : plan_b;
+    const uint32_t want = 200u * 1024u;  // total target; the arena takes what the rest leaves
+    s.arena_bytes = want > s.arena + 16384u ? want - s.arena : 16384u;
+    s.bytes = s.arena + s.arena_bytes;
+    if (s.bytes < ctl)
+        s.bytes = ctl;
+    if (s.bytes < kSoloSmem)
+        s.bytes = kSoloSmem;
+    return s;
+}
 #undef DRB_TAKE
+// sel/plan shared-memory floor: with the TMA copy kernel at `copy_bytes`, one sel/plan CTA
+// plus one copy CTA must not fit on one SM.
+__host__ __device__ inline uint32_t solo_smem_for(uint32_t copy_bytes) {
+    const uint32_t need = kSmSmem - copy_bytes;  // + 2 reservations > kSmSmem
+    const uint32_t lo = need > kSoloSmem ? need : kSoloSmem;
+    return lo > 227u * 1024u ? 227u * 1024u : lo;
+}
 
 // Launchers (drb_kernels.cu), C++ linkage, used by drb_capi.cu only.
-int launch_sel(const StepParams& p, void* stream);
-int launch_plan_next(const StepParams& p, void* stream);
+// pdl: launched programmatically behind the previous kernel of the same chain on `stream`
+// (its prologue overlaps that kernel; griddepcontrol.wait orders the dependent part).
+int launch_sel(const StepParams& p, void* stream, bool pdl = false);
+int launch_plan_next(const StepParams& p, void* stream, bool pdl = false);
 // pdl: the previous kernel on `stream` is this handle's copy of the previous iteration, so
 // the launch may overlap its tail (programmatic dependent launch).
 int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl);
 int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out);
+int copy_tma_occupancy(uint32_t smem_bytes, int* out);  // CTAs per SM of the TMA copy kernel
+// persistent run: dynamic smem, and the cooperative launch (grid = copy_ctas + 2)
+uint32_t run_smem_bytes(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax);
+int launch_run(const RunParams& rp, uint32_t grid, void* stream);
 uint32_t sel_smem_bytes(uint32_t K, uint32_t nmax);
 uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r);
 uint32_t plan_threads(uint32_t N);

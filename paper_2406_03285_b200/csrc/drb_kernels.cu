@@ -1,18 +1,18 @@
 // sm_100a kernels of the distributed rehearsal buffer (arXiv 2406.03285 hot path).
 //
-// One launch of drb_step_kernel is one engine iteration i on one rank:
-//   * S1+S2 update_buffer(m_i)          proj/src/buffer/rehearsal_buffer.cpp:14-86
-//   * publish occupancy row v=i+1       proj/src/engine/engine.cpp:108-136
-//   * S4 plan(i-1) for every requester  proj/src/sampler/sampler.cpp:39-68 (+ locate,
-//                                       proj/src/sampler/size_table.cpp:29-39)
-//   * S5 push owned plan entries (read at version i, before this round's overwrites)
-//     into each requester's m'_i rows   proj/src/sampler/sampler.cpp:111-232 (fetch) and
-//                                       proj/src/engine/engine.cpp:215-251 (serve_sample)
-//   * augment: m'_i = m_i ++ reps(i-1)  proj/src/sampler/sampler.cpp:234-240
+// One engine iteration i on one rank is three kernels:
+//   * sel(i):  S1+S2 update_buffer(m_i)          proj/src/buffer/rehearsal_buffer.cpp:14-86
+//              publish occupancy row v=i+1       proj/src/engine/engine.cpp:108-136
+//   * plan(i): size rendezvous v=i+1             proj/src/sampler/size_table.cpp:66-100
+//              S4 plan(i) for every requester    proj/src/sampler/sampler.cpp:39-68 (+ locate,
+//                                                proj/src/sampler/size_table.cpp:29-39)
+//   * copy(i): m_i -> m'_i, the slab writes of round i, and S5: every owned slot of plan(i)
+//              at version i+1 pushed into its requester's m'_{i+1}
+//                                                proj/src/sampler/sampler.cpp:111-232 (fetch),
+//                                                proj/src/engine/engine.cpp:215-251 (serve),
+//              so m'_i = m_i ++ reps(i-1)        proj/src/sampler/sampler.cpp:234-240
 // The RNG decisions are bit-identical to proj/src/core/rng.cpp:12-53 and are evaluated
 // warp-parallel over consecutive counters (exact rejection semantics; see warp_* below).
-// Every CTA recomputes the (tiny) control decisions redundantly so no grid-wide barrier
-// is needed; the byte movement is spread evenly over all CTAs as 16-byte vectors.
 
 #include <cuda_runtime.h>
 
@@ -62,12 +62,6 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// No ordering of earlier stores (a release would wait for every store of the copy to be
-// acknowledged): for flags that only announce completed LOADS.
-__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -334,40 +328,6 @@ __device__ __forceinline__ V ld_vec(const V* p) {
     }
 }
 
-// One warp copies dynamically claimed chunks of 32*U vectors out of [lo, hi) (32-bit
-// vector indices). `src(gv)` gives the source address of vector gv; `store(gv, v)` writes
-// it to every destination of its job (and performs the job's trailing overwrite, if any,
-// after those stores — the read-before-write order of a pushed slot). All U loads of a
-// lane are issued before any store (memory-level parallelism).
-template <typename V, int U, typename Src, typename Store>
-__device__ __forceinline__ void warp_copy(uint32_t lo, uint32_t hi, uint32_t* counter, Src src,
-                                          Store store) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (;;) {
-        uint32_t c = 0;
-        if (lane == 0)
-            c = atomicAdd(counter, 1u);
-        c = __shfl_sync(kFull, c, 0);
-        const uint32_t base = lo + c * (32u * U);
-        if (base >= hi)
-            break;
-        V r[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t gv = base + u * 32 + lane;
-            const V* a = gv < hi ? src(gv) : nullptr;
-            if (a)
-                r[u] = ld_vec(a);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t gv = base + u * 32 + lane;
-            if (gv < hi)
-                store(gv, r[u]);
-        }
-    }
-}
-
 // Diagnostics: sel / plan stamp slots 0-8, copy CTA 0 slots 16-19 (DRB_TRACE=1).
 // Timeline (DRB_TIMELINE=<steps>): grid-wide first start / last end of each kernel of
 // each step, as globaltimer ns; works inside CUDA graphs.
@@ -391,7 +351,8 @@ __device__ __forceinline__ void cta_mark(const StepParams& p, int slot) {
 }
 
 __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
+    // CTA 0 (sel, plan and the copy's first CTA); CTA 1 too: the plan role of a persistent run
+    if (blockIdx.x <= 1 && (threadIdx.x & 31) == 0) {
         if (p.trace)
             p.trace[slot] = globaltimer();
         if (p.timeline)  // phase stamps of the pipelined run: slots 8.. of the step's record
@@ -408,56 +369,48 @@ __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
 //                     list W_i, round-(i+1) selection state, occupancy row v=i+1 published
 //                     (engine.cpp:108-136)                        — chained only on sel(i-1)
 //   plan(i)  1 CTA  : size rendezvous v=i+1 (size_table.cpp:66-100), S4 plan(i) for every
-//                     requester (sampler.cpp:39-68), the push list P_{i+1}, labels of
+//                     requester (sampler.cpp:39-68), the push list X_i, labels of
 //                     m'_{i+1}'s representatives                  — chained only on plan(i-1)
-//   copy(i)  grid   : m'_i = m_i ++ reps(i-1) (sampler.cpp:234-240): m_i -> m'_i, pushes of
-//                     P_i (slots read at version i into each requester's m'_i), then the
-//                     writes of W_i into the slab, a pushed slot only after its push read
-// so copy(i) starts with every list it needs already in memory, and sel(i+1) / plan(i)
+//   copy(i)  grid   : m_i -> m'_i rows, W_i into the slab, and the pushes of X_i (slots at
+//                     version i+1 into each requester's m'_{i+1})
+// so copy(i) starts with every list it needs already in memory, and sel(i+1) / plan(i+1)
 // run concurrently with copy(i) on their own streams.
 // ======================================================================================
 
 constexpr uint32_t kSelThreads = 128;
 
-__global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_constant__ StepParams p) {
-    extern __shared__ __align__(16) uint32_t sm[];
+struct SelView {  // sel's shared-memory arrays (sel_smem carve-up)
+    uint32_t *occ, *lab, *sel, *cand_l, *cand_slot, *kind, *misc;
+    SelState* st;
+};
+__device__ __forceinline__ SelView sel_view(uint32_t* sm, const StepParams& p) {
     const SelSmem L = sel_smem(p.K, p.nmax);
-    uint32_t* occ = sm + L.occ;
-    uint32_t* lab = sm + L.lab;
-    uint32_t* sel = sm + L.sel;
-    uint32_t* cand_l = sm + L.cand_l;
-    uint32_t* cand_slot = sm + L.cand_slot;
-    uint32_t* kind = sm + L.kind;
-    uint32_t* misc = sm + L.misc;
-    SelState* st = reinterpret_cast<SelState*>(misc + 16);
+    SelView v;
+    v.occ = sm + L.occ;
+    v.lab = sm + L.lab;
+    v.sel = sm + L.sel;
+    v.cand_l = sm + L.cand_l;
+    v.cand_slot = sm + L.cand_slot;
+    v.kind = sm + L.kind;
+    v.misc = sm + L.misc;
+    v.st = reinterpret_cast<SelState*>(v.misc + 16);
+    return v;
+}
 
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// sel(i) after its loads (one full warp): S1+S2 on occ (own occupancy row, version i, updated
+// in place to version i+1) and lab (labels of m_i, `bad` if any is >= K), the candidate-write
+// list W_i, the round-(i+1) selection state (p.sel_out, and *v.st in place), stored slot
+// labels, the published occupancy row v=i+1 and the insertion report.
+__device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
+    const uint32_t lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap;
     const uint32_t NK = N * K;
     const bool do_update = p.mode & kModeUpdate;
     const bool do_publish = p.mode & kModePublish;
     const bool multi = (p.mode & kModePeers) && N > 1;
-    const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
-                          uint64_t(p.tslot_in) * NK + uint64_t(me) * K;
-    trace_at(p, 0);
-    tl_mark(p, 0, false);
-    // one round trip: state, own occupancy row (version i), labels of m_i
-    if (tid < sizeof(SelState) / 8)
-        reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.sel_in) + tid);
-#pragma unroll 1
-    for (uint32_t x = tid; x < K; x += kSelThreads)
-        occ[x] = __ldcg(tin + x);
-    int any_bad = 0;
-#pragma unroll 1
-    for (uint32_t x = tid; x < n; x += kSelThreads) {
-        const uint32_t l = __ldg(p.labels + x);
-        lab[x] = l;
-        any_bad |= l >= K;
-    }
-    const bool bad = __syncthreads_or(any_bad) != 0;  // usage_error before any draw (:44-47)
-    if (warp != 0)
-        return;
+    SelState* st = v.st;
+    uint32_t *occ = v.occ, *sel = v.sel, *cand_l = v.cand_l, *cand_slot = v.cand_slot, *kind = v.kind;
     trace_at(p, 1);
     const bool dead = st->error != 0;  // sticky: a failed round kills the engine
     const uint32_t k = (!dead && do_update && !bad && n > 0) ? min(p.c, n) : 0;
@@ -467,7 +420,7 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
     if (k > 0) {
         warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
         trace_at(p, 2);
-        warp_assign(p.evict_key, evict_ctr, cap, k, sel, lab, occ, cand_l, cand_slot, misc + 32, kind,
+        warp_assign(p.evict_key, evict_ctr, cap, k, sel, v.lab, occ, cand_l, cand_slot, v.misc + 32, kind,
                     appends);
     }
     trace_at(p, 3);
@@ -479,7 +432,11 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
         const uint32_t t = base + lane;
         bool w = false;
         uint32_t key = 0;
-        if (t < k) {
+        if (k <= 32) {  // one match: no later candidate of the same (class, slot)
+            key = t < k ? cand_l[t] * cap + cand_slot[t] : 0x80000000u + lane;  // slots < 2^31
+            const unsigned same = __match_any_sync(kFull, key);
+            w = t < k && (same >> lane) == 1u;
+        } else if (t < k) {
             key = cand_l[t] * cap + cand_slot[t];
             w = true;
 #pragma unroll 1
@@ -498,14 +455,18 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
         wl[0] = n_win;
     // round-(i+1) selection state
     const uint32_t err = dead ? st->error : ((bad && do_update) ? DRB_ERR_USAGE : 0u);
+    __syncwarp();
     if (lane == 0) {
-        SelState* o = p.sel_out;
-        o->cand_ctr = cand_ctr;
-        o->evict_ctr = evict_ctr;
-        o->version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
-        o->total = st->total + appends;
-        o->cross_class = st->cross_class;
-        o->error = err;
+        SelState o;
+        o.cand_ctr = cand_ctr;
+        o.evict_ctr = evict_ctr;
+        o.version = st->version + k;  // one per mutation (rehearsal_buffer.cpp:79)
+        o.total = st->total + appends;
+        o.cross_class = st->cross_class;
+        o.error = err;
+        o.pad = 0;
+        *p.sel_out = o;
+        *st = o;
         if (p.mailbox && err)
             reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
     }
@@ -550,31 +511,184 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
             atomicAdd(&p.report[2 * K + (app ? 0 : 1)], 1u);
         }
     }
+    __syncwarp();
     trace_at(p, 4);
+}
+
+// labels of m_i into v.lab (all threads of the CTA, stride T); returns this thread's "bad"
+__device__ __forceinline__ int sel_load_labels(const StepParams& p, const SelView& v, uint32_t T) {
+    int any_bad = 0;
+#pragma unroll 1
+    for (uint32_t x = threadIdx.x; x < p.n; x += T) {
+        const uint32_t l = __ldg(p.labels + x);
+        v.lab[x] = l;
+        any_bad |= l >= p.K;
+    }
+    return any_bad;
+}
+
+__global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_constant__ StepParams p) {
+    extern __shared__ __align__(128) uint32_t sm[];
+    const SelView v = sel_view(sm, p);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[p.me] + p.off_table) +
+                          uint64_t(p.tslot_in) * p.N * p.K + uint64_t(p.me) * p.K;
+    trace_at(p, 0);
+    tl_mark(p, 0, false);
+    // No griddepcontrol.launch_dependents here (nor in plan): a copy launched with the PDL
+    // attribute turns ALL its captured in-edges programmatic, and copy(i) reads W_i / X_i
+    // before its griddepcontrol.wait — so sel/plan must trigger their dependents only by
+    // completing. (Measured: PDL on the sel/plan chains themselves does not pay either.)
+    // Under PDL the labels of m_i would load while sel(i-1) still runs; state and the own
+    // occupancy row (version i) come from sel(i-1) and load after griddepcontrol.wait.
+    const int any_bad = sel_load_labels(p, v, kSelThreads);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid < sizeof(SelState) / 8)
+        reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.sel_in) + tid);
+#pragma unroll 1
+    for (uint32_t x = tid; x < p.K; x += kSelThreads)
+        v.occ[x] = __ldcg(tin + x);
+    const bool bad = __syncthreads_or(any_bad) != 0;  // usage_error before any draw (:44-47)
+    if (warp != 0)
+        return;
+    sel_core(p, v, bad);
     tl_mark(p, 0, true);
 }
 
-__global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
-    extern __shared__ __align__(16) uint32_t sm[];
+struct PlanView {  // plan's shared-memory arrays (plan_smem carve-up)
+    uint32_t *pre, *pfx, *plan, *cnt, *acc, *misc, *maskP;
+    PlanState* st;
+};
+__device__ __forceinline__ PlanView plan_view(uint32_t* sm, const StepParams& p) {
     const PlanSmem L = plan_smem(p.N, p.K, p.r);
-    uint32_t* pre = sm + L.pre;
-    uint32_t* pfx = sm + L.pfx;
-    uint32_t* plan = sm + L.plan;
-    uint32_t* cnt = sm + L.cnt;
-    uint32_t* acc = sm + L.acc;
-    uint32_t* misc = sm + L.misc;
-    PlanState* st = reinterpret_cast<PlanState*>(misc + 16);
-    uint32_t* maskP = misc + 64;
+    PlanView v;
+    v.pre = sm + L.pre;
+    v.pfx = sm + L.pfx;
+    v.plan = sm + L.plan;
+    v.cnt = sm + L.cnt;
+    v.acc = sm + L.acc;
+    v.misc = sm + L.misc;
+    v.st = reinterpret_cast<PlanState*>(v.misc + 16);
+    v.maskP = v.misc + 64;
+    return v;
+}
 
+// plan(i) after the size rendezvous (all threads of the CTA, blockDim >= 32*(N+1)): the view
+// v=i+1 from the table, S4 for every requester (p.plan_out and *v.st updated in place),
+// labels of m'_{i+1}'s reps, the push list X_i. v.misc[0] = rendezvous status.
+__device__ void plan_core(const StepParams& p, const PlanView& v) {
+    uint32_t *pre = v.pre, *pfx = v.pfx, *plan = v.plan, *cnt = v.cnt, *acc = v.acc, *misc = v.misc,
+             *maskP = v.maskP;
+    PlanState* st = v.st;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, T = blockDim.x;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t N = p.N, K = p.K, me = p.me, cap = p.cap, r = p.r;
     const uint32_t NK = N * K;
     const uint32_t MJ = plist_mj(N, r);
+    const uint32_t* tv1 = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
+                          uint64_t(p.tslot_out) * NK;
+#pragma unroll 1
+    for (uint32_t x = tid; x < NK; x += T)
+        pre[x] = __ldcg(tv1 + x);
+    __syncthreads();
+    trace_at(p, 6);
+    const bool dead = st->error != 0;
+    uint32_t* out = p.plist_out;
+    if (dead) {
+        if (tid < sizeof(PlanState) / 8)
+            reinterpret_cast<uint64_t*>(p.plan_out)[tid] = reinterpret_cast<const uint64_t*>(st)[tid];
+        if (tid == 0) {
+            out[0] = 0;
+            out[1] = 0;
+        }
+        return;
+    }
+    // S4 plan(i): warps 1..N draw for requester q = warp-1; warp 0 builds the prefix
+    if (warp >= 1 && warp <= N) {
+        const uint32_t q = warp - 1;
+        uint64_t ctr = st->samp_ctr[q];
+        const uint32_t total = warp_sum(pre, NK);
+        const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
+        if (lane == 0) {
+            cnt[q] = c;
+            p.plan_out->samp_ctr[q] = ctr;
+            st->samp_ctr[q] = ctr;
+        }
+    } else if (warp == 0) {
+        warp_exclusive_scan(pre, NK, pfx);
+    }
+    __syncthreads();
+    if (warp >= 1 && warp <= N) {
+        const uint32_t q = warp - 1;
+        warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
+        if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
+            uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
+                           uint64_t((p.aslot + 1) % kAugRing) * p.auglab_slot_elems;
+#pragma unroll 1
+            for (uint32_t j = lane; j < cnt[q]; j += 32)
+                al[p.nmax + j] = plan[3 * (q * r + j) + 1];
+        }
+    }
+    __syncthreads();
+    trace_at(p, 7);
+    // Push list X_i for copy(i): every entry (q, j) of plan(i), over all requesters q (own
+    // plan included), whose slot this rank owns, in (q, j) order. copy(i) stores the slot's
+    // version-(i+1) bytes into q's m'_{i+1} row nmax+j (sampler.cpp:111-232 serve + fetch,
+    // as one-sided stores from the owner).
+    const uint32_t NR = N * r;
+    uint32_t* jdst = out + 4;
+    uint32_t* jrow = out + 4 + MJ;
+    for (uint32_t base = warp * 32; base < NR; base += T) {
+        const uint32_t e = base + lane;
+        bool own = false;
+        if (e < NR) {
+            const uint32_t q = e / r, j = e - q * r;
+            own = j < cnt[q] && plan[3 * e] == me;
+        }
+        const unsigned m = __ballot_sync(kFull, own);
+        if (lane == 0)
+            maskP[base >> 5] = m;
+    }
+    __syncthreads();
+    for (uint32_t base = warp * 32; base < NR; base += T) {
+        const unsigned m = maskP[base >> 5];
+        if (!((m >> lane) & 1u))
+            continue;
+        uint32_t pos = __popc(m & lt);
+#pragma unroll 1
+        for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
+            pos += __popc(maskP[b2]);
+        const uint32_t e = base + lane, q = e / r, j = e - q * r;
+        jdst[pos] = (q << 24) | j;
+        jrow[pos] = plan[3 * e + 1] * cap + plan[3 * e + 2];
+    }
+    if (tid == 0) {
+        uint32_t nj = 0;
+#pragma unroll 1
+        for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
+            nj += __popc(maskP[b2]);
+        out[0] = cnt[me];
+        out[1] = nj;
+        p.plan_out->error = misc[0];
+        st->error = misc[0];
+        if (misc[0] && p.mailbox)  // rendezvous failure: the engine is dead from here
+            reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[0];
+    }
+    trace_at(p, 8);
+}
+
+__global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
+    extern __shared__ __align__(128) uint32_t sm[];
+    const PlanView v = plan_view(sm, p);
+    uint32_t* misc = v.misc;
+    PlanState* st = v.st;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t N = p.N, me = p.me;
     const bool multi = (p.mode & kModePeers) && N > 1;
     RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     trace_at(p, 5);
     tl_mark(p, 1, false);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // plan(i-1): the sampling counters
     if (tid < sizeof(PlanState) / 8)
         reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.plan_in) + tid);
     if (tid == 0)
@@ -596,153 +710,8 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
         }
     }
     __syncthreads();
-    const uint32_t* tv1 = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
-                          uint64_t(p.tslot_out) * NK;
-#pragma unroll 1
-    for (uint32_t x = tid; x < NK; x += T)
-        pre[x] = __ldcg(tv1 + x);
-    __syncthreads();
-    trace_at(p, 6);
-    const bool dead = st->error != 0;
-    uint32_t* out = p.plist_out;
-    if (dead) {
-        if (tid < sizeof(PlanState) / 8)
-            reinterpret_cast<uint64_t*>(p.plan_out)[tid] = reinterpret_cast<const uint64_t*>(st)[tid];
-        if (tid == 0) {
-            out[0] = 0;
-            out[1] = 0;
-        }
-        tl_mark(p, 1, true);
-        return;
-    }
-    // S4 plan(i): warps 1..N draw for requester q = warp-1; warp 0 builds the prefix
-    if (warp >= 1 && warp <= N) {
-        const uint32_t q = warp - 1;
-        uint64_t ctr = st->samp_ctr[q];
-        const uint32_t total = warp_sum(pre, NK);
-        const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
-        if (lane == 0) {
-            cnt[q] = c;
-            p.plan_out->samp_ctr[q] = ctr;
-        }
-    } else if (warp == 0) {
-        warp_exclusive_scan(pre, NK, pfx);
-    }
-    __syncthreads();
-    if (warp >= 1 && warp <= N) {
-        const uint32_t q = warp - 1;
-        warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
-        if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
-            uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
-                           uint64_t((p.aslot + 1) % kAugRing) * p.auglab_slot_elems;
-#pragma unroll 1
-            for (uint32_t j = lane; j < cnt[q]; j += 32)
-                al[p.nmax + j] = plan[3 * (q * r + j) + 1];
-        }
-    }
-    __syncthreads();
-    trace_at(p, 7);
-    // Pull list for copy(i+1): (a) this rank's own plan in draw order — it reads every
-    // representative itself, from the owner's slab (local or over NVLink); (b) the rows of
-    // MY slab that other requesters read, deduplicated in entry order (ballots), with the
-    // set of readers — a write of round i+1 to such a row must wait for those reads.
-    const uint32_t R = plist_r(r);
-    const uint32_t mine = cnt[me];
-#pragma unroll 1
-    for (uint32_t j = tid; j < mine; j += T) {
-        const uint32_t* x = plan + 3 * (me * r + j);
-        out[4 + j] = x[0];
-        out[4 + R + j] = x[1] * cap + x[2];
-    }
-    const uint32_t NR = N * r;
-    uint32_t* rrow = out + 4 + 2 * R;
-    uint32_t* rmask = rrow + MJ;
-    for (uint32_t base = warp * 32; base < NR; base += T) {
-        const uint32_t e = base + lane;
-        bool lead = false;
-        if (e < NR) {
-            const uint32_t q = e / r, j = e - q * r;
-            if (q != me && j < cnt[q] && plan[3 * e] == me) {
-                const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-                lead = true;
-#pragma unroll 1
-                for (uint32_t q2 = 0; q2 < q && lead; ++q2) {
-                    if (q2 == me)
-                        continue;
-#pragma unroll 1
-                    for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
-                        const uint32_t* x = plan + 3 * (q2 * r + j2);
-                        if (x[0] == me && x[1] == cls && x[2] == slot) {
-                            lead = false;
-                            break;
-                        }
-                    }
-                }
-            }
-        }
-        const unsigned m = __ballot_sync(kFull, lead);
-        if (lane == 0)
-            maskP[base >> 5] = m;
-    }
-    __syncthreads();
-    for (uint32_t base = warp * 32; base < NR; base += T) {
-        const unsigned m = maskP[base >> 5];
-        if (!((m >> lane) & 1u))
-            continue;
-        uint32_t pos = __popc(m & lt);
-#pragma unroll 1
-        for (uint32_t b2 = 0; b2 < (base >> 5); ++b2)
-            pos += __popc(maskP[b2]);
-        const uint32_t e = base + lane, q = e / r;
-        const uint32_t cls = plan[3 * e + 1], slot = plan[3 * e + 2];
-        uint32_t readers = 1u << q;
-#pragma unroll 1
-        for (uint32_t q2 = q + 1; q2 < N; ++q2) {
-            if (q2 == me)
-                continue;
-#pragma unroll 1
-            for (uint32_t j2 = 0; j2 < cnt[q2]; ++j2) {
-                const uint32_t* x = plan + 3 * (q2 * r + j2);
-                if (x[0] == me && x[1] == cls && x[2] == slot) {
-                    readers |= 1u << q2;
-                    break;
-                }
-            }
-        }
-        rrow[pos] = cls * cap + slot;
-        rmask[pos] = readers;
-    }
-    if (tid == 0) {
-        uint32_t nrem = 0;
-#pragma unroll 1
-        for (uint32_t b2 = 0; b2 < (NR + 31) / 32; ++b2)
-            nrem += __popc(maskP[b2]);
-        out[0] = mine;
-        out[1] = nrem;
-        p.plan_out->error = misc[0];
-        if (misc[0] && p.mailbox)  // rendezvous failure: the engine is dead from here
-            reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[0];
-    }
-    trace_at(p, 8);
+    plan_core(p, v);
     tl_mark(p, 1, true);
-}
-
-__device__ __forceinline__ uint4 ld_cg16(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-}
-
-template <typename V>
-__device__ __forceinline__ V ld_pull(const V* p) {  // possibly a peer's memory (NVLink)
-    if constexpr (sizeof(V) == 16) {
-        const uint4 v = ld_cg16(reinterpret_cast<const uint4*>(p));
-        return *reinterpret_cast<const V*>(&v);
-    } else {
-        return __ldcg(p);
-    }
 }
 
 // Spin (thread-level) until *flag >= want or the timeout; returns false on timeout.
@@ -756,129 +725,67 @@ __device__ bool wait_flag(const uint64_t* flag, uint64_t want, uint64_t timeout_
     return true;
 }
 
-// Copy CTA, warp 0: wait for the staged lists (cp.async), classify W_i's writes — safe
-// (rowmap when fused into A, else `win` jobs), local hazard C (`post`), remote-read D
-// (`defer`) — wait for the owners of remote pulls (done >= i), publish misc[0..2] and the
-// ready flag; CTA 0 also writes m'_i's batch labels and row count.
-struct CopyLists {
-    uint32_t *praw, *wraw, *win, *defer, *misc;
-    int *post, *rowmap;
-    volatile uint32_t* ready;
-};
-__device__ void copy_parse_lists(const StepParams& p, const CopyLists& cl, bool do_pull, bool do_update,
-                                 bool multi, bool fuse) {
+__device__ __forceinline__ void mailbox_fail(const StepParams& p, uint32_t err) {
+    if (p.mailbox) {
+        volatile uint32_t* mb = p.mailbox;
+        mb[kAugRing + p.aslot] = err;
+        mb[2 * kAugRing] = err;
+    }
+}
+
+// ---- copy(i) ------------------------------------------------------------------------------
+// m'_i = m_i ++ reps(i-1) is assembled by two launches: copy(i) writes m_i's rows, and
+// copy(i-1) of every owner already wrote reps(i-1) into m'_i's representative rows. A rep
+// of plan(i) is the content of its slot at version i+1 (S5), i.e. after round i's writes:
+// for a slot in W_i that is the winning candidate's batch row, otherwise the slab row as it
+// is now (round i does not touch it). So copy(i) reads every slot it serves *while* it
+// writes W_i — no read-before-write hazard exists — and stores the bytes straight into the
+// requester's m'_{i+1} row nmax+j: its own (HBM) or a peer's (P2P stores over NVLink).
+//   A  m_i -> m'_i rows [nmax-n, nmax); a batch row that won a slot also -> its slab row
+//   B  push jobs of X_i (plan(i)): version-(i+1) slot bytes -> requester's m'_{i+1} row;
+//      without assembly (update_buffer API) the W_i writes instead
+// Cross-rank: after its pushes complete, the last CTA of copy(i) release-stores
+// pushdone[me] = i+1 into every peer's header; copy(i) does not finish before every
+// peer's pushdone >= i (their reps(i-1) rows of m'_i landed). Nothing waits on a peer
+// before moving bytes.
+
+// Copy CTA, warp 0: wait for the staged lists (cp.async), resolve each push job's source
+// (winner batch row if its slot is written this round, else the slab row) and the
+// batch-row -> slab-row map of the fused W_i writes; publish misc[0..1] and the ready flag.
+__device__ void copy_parse(const StepParams& p, const uint32_t* xraw, const uint32_t* wraw, uint32_t* jsrc,
+                           int* rowmap, uint32_t* misc, volatile uint32_t* ready, bool do_push, bool do_update,
+                           bool fuse) {
     const uint32_t lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    const uint32_t N = p.N, me = p.me, n = p.n;
-    const uint32_t R = plist_r(p.r), MJ = plist_mj(N, p.r);
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
-    const uint32_t row0 = p.nmax - n;
-    uint32_t* praw = cl.praw;
-    uint32_t* wraw = cl.wraw;
-    uint32_t* win = cl.win;
-    uint32_t* defer = cl.defer;
-    uint32_t* misc = cl.misc;
-    int* post = cl.post;
-    int* rowmap = cl.rowmap;
-    volatile uint32_t* ready = cl.ready;
-    const uint32_t* owner = praw + 4;
-    const uint32_t* prow = praw + 4 + R;
-    const uint32_t* rrow = praw + 4 + 2 * R;
-    const uint32_t* rmask = rrow + MJ;
+    const uint32_t MJ = plist_mj(p.N, p.r);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
-    const uint32_t cnt = do_pull ? praw[0] : 0;
-    const uint32_t nrem = (do_pull && multi) ? praw[1] : 0;
+    const uint32_t nj = do_push ? xraw[1] : 0;
     const uint32_t n_win = do_update ? wraw[0] : 0;
-    // round-i writes: to a row this rank pulls -> post on that pull (C); to a row a
-    // remote requester pulls -> deferred (D); otherwise a plain write (B)
+    const uint32_t* jrow = xraw + 4 + MJ;
 #pragma unroll 1
-    for (uint32_t j = lane; j < cnt; j += 32)
-        post[j] = -1;
-    __syncwarp();
-    uint32_t n_safe = 0, n_def = 0;
+    for (uint32_t x = lane; x < nj; x += 32) {
+        const uint32_t row = jrow[x];
+        uint32_t src = row;
 #pragma unroll 1
-    for (uint32_t base = 0; base < n_win; base += 32) {
-        const uint32_t t = base + lane;
-        uint32_t row = 0, key = 0, readers = 0;
-        bool local_hz = false;
-        if (t < n_win) {
-            row = wraw[2 + 2 * t];
-            key = wraw[3 + 2 * t];
-#pragma unroll 1
-            for (uint32_t j = 0; j < cnt; ++j)
-                if (owner[j] == me && prow[j] == key) {
-                    post[j] = static_cast<int>(row);
-                    local_hz = true;
-                    break;
-                }
-#pragma unroll 1
-            for (uint32_t x = 0; x < nrem; ++x)
-                if (rrow[x] == key) {
-                    readers = rmask[x];
-                    break;
-                }
-        }
-        const bool safe = t < n_win && !local_hz && readers == 0;
-        const bool def = t < n_win && readers != 0;
-        const unsigned ms = __ballot_sync(kFull, safe);
-        const unsigned md = __ballot_sync(kFull, def);
-        if (safe) {
-            const uint32_t pos = n_safe + __popc(ms & lt);
-            win[2 * pos] = row;
-            win[2 * pos + 1] = key;
-        }
-        if (def) {  // (a local hazard that is also remote-read: D after the local read
-                    //  — D runs after this CTA's barrier anyway)
-            const uint32_t pos = n_def + __popc(md & lt);
-            defer[3 * pos] = row;
-            defer[3 * pos + 1] = key;
-            defer[3 * pos + 2] = readers;
-        }
-        n_safe += __popc(ms);
-        n_def += __popc(md);
-    }
-    // a local-hazard row that is also remote-read is written in D only
-    if (n_def) {
-#pragma unroll 1
-        for (uint32_t j = lane; j < cnt; j += 32)
-            if (post[j] >= 0)
-#pragma unroll 1
-                for (uint32_t x = 0; x < n_def; ++x)
-                    if (defer[3 * x + 1] == prow[j] && owner[j] == me)
-                        post[j] = -1;
-    }
-    // pulls from a peer need that owner's copy(i-1) complete (its slab at version i)
-    if (multi && cnt) {
-        uint32_t need = 0;
-        for (uint32_t j = lane; j < cnt; j += 32)
-            if (owner[j] != me)
-                need |= 1u << owner[j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            need |= __shfl_xor_sync(kFull, need, o);
-        bool ok = true;
-        if (lane < N && ((need >> lane) & 1u))
-            ok = wait_flag(&hdr->done[lane], p.step, p.timeout_ns);
-        if (__any_sync(kFull, !ok) && lane == 0 && p.mailbox) {
-            volatile uint32_t* mb = p.mailbox;
-            mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
-            mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
-        }
+        for (uint32_t t = 0; t < n_win; ++t)  // winners hold distinct slots
+            if (wraw[3 + 2 * t] == row) {
+                src = 0x80000000u | wraw[2 + 2 * t];
+                break;
+            }
+        jsrc[x] = src;
     }
     if (fuse) {
 #pragma unroll 1
-        for (uint32_t x = lane; x < n; x += 32)
+        for (uint32_t x = lane; x < p.n; x += 32)
             rowmap[x] = -1;
         __syncwarp();
 #pragma unroll 1
-        for (uint32_t x = lane; x < n_safe; x += 32)
-            rowmap[win[2 * x]] = static_cast<int>(win[2 * x + 1]);
+        for (uint32_t t = lane; t < n_win; t += 32)
+            rowmap[wraw[2 + 2 * t]] = static_cast<int>(wraw[3 + 2 * t]);
     }
     if (lane == 0) {
-        misc[0] = cnt;
-        misc[1] = fuse ? 0u : n_safe;
-        misc[2] = n_def;
+        misc[0] = nj;
+        misc[1] = fuse ? 0u : n_win;
     }
     __syncwarp();
     __threadfence_block();
@@ -887,308 +794,170 @@ __device__ void copy_parse_lists(const StepParams& p, const CopyLists& cl, bool 
         cta_mark(p, 1);
     }
     trace_at(p, 20);
-    if (blockIdx.x == 0 && (p.mode & kModeAssemble)) {
-        // m'_i labels of rows [row0, row0+n) and its row count n + |reps(i-1)|
-        uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
-                       uint64_t(p.aslot) * p.auglab_slot_elems;
+}
+
+// CTA 0, warp 0, after griddepcontrol.wait: m'_i's batch labels, its row count
+// n + |reps(i-1)| (|reps(i-1)| left by copy(i-1) in repcnt) and |reps(i)| for copy(i+1).
+__device__ void copy_counts(const StepParams& p, const uint32_t* xraw) {
+    const uint32_t lane = threadIdx.x & 31;
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[p.me]);
+    const uint32_t row0 = p.nmax - p.n;
+    uint32_t* al = reinterpret_cast<uint32_t*>(p.region[p.me] + p.off_auglab) + uint64_t(p.aslot) * p.auglab_slot_elems;
 #pragma unroll 1
-        for (uint32_t x = lane; x < n; x += 32)
-            al[row0 + x] = __ldg(p.labels + x);
-        if (lane == 0) {
-            hdr->aug_count[p.aslot] = n + cnt;
-            if (p.mailbox) {
-                volatile uint32_t* mb = p.mailbox;
-                mb[p.aslot] = n + cnt;
-                mb[kAugRing + p.aslot] = 0;
-            }
+    for (uint32_t x = lane; x < p.n; x += 32)
+        al[row0 + x] = __ldg(p.labels + x);
+    if (lane == 0) {
+        const uint32_t prev = p.step > 0 ? hdr->repcnt[p.aslot] : 0u;
+        hdr->aug_count[p.aslot] = p.n + prev;
+        hdr->repcnt[(p.aslot + 1) % kAugRing] = xraw[0];
+        if (p.mailbox) {
+            volatile uint32_t* mb = p.mailbox;
+            mb[p.aslot] = p.n + prev;
+            mb[kAugRing + p.aslot] = 0;
         }
     }
 }
 
-// copy(i): m'_i = m_i ++ reps(i-1) and the slab writes of round i. Every CTA owns fixed
-// slices of the vector spaces below; warps claim 32*U-vector chunks of a slice dynamically.
-//   A  m_i -> m'_i rows [nmax-n, nmax)                                   (n rows)
-//   B  pulls: rep j of this rank <- owner's slab row (local or a peer's over NVLink, read
-//      at version i: the owner finished copy(i-1)) into m'_i row nmax+j; plus the
-//      candidate writes of W_i nobody reads this round
-//   C  a write to a row this rank itself pulled: by the same CTA, after the pull (barrier)
-//   D  a write to a row a remote requester pulls: after that requester's pulls completed
-// Multi-rank signals (peer headers, release/acquire .sys): readdone[me] after the last
-// CTA's B phase, done[me] after the last CTA's writes — the only cross-rank waits are
-// "owner finished copy(i-1)" before pulling from it and the rare D case.
+// Multi-rank completion of copy(i), after every CTA's pushes are complete and fenced:
+// the last CTA announces pushdone[me] = i+1 to every peer; CTA 0 holds the kernel until
+// every peer's reps(i-1) rows of m'_i have landed (pushdone >= i).
+__device__ void copy_finish_peers(const StepParams& p) {
+    const uint32_t tid = threadIdx.x, N = p.N, me = p.me;
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
+    if (tid == 0) {
+        const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->ticket), 1ull);
+        if ((t + 1) % gridDim.x == 0) {
+            __threadfence_system();
+            for (uint32_t w = 0; w < N; ++w)
+                if (w != me)
+                    st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->pushdone[me], p.step + 1);
+        }
+    }
+    if (blockIdx.x == 0 && tid < 32 && p.step > 0) {
+        bool ok = true;
+        if (tid < N && tid != me)
+            ok = wait_flag(&hdr->pushdone[tid], p.step, p.timeout_ns);
+        if (__any_sync(kFull, !ok) && tid == 0)
+            mailbox_fail(p, DRB_ERR_TRANSPORT);
+    }
+}
+
+__device__ __forceinline__ uint8_t* push_dst(const StepParams& p, uint32_t dst, uint32_t next_slot) {
+    const uint32_t q = dst >> 24, j = dst & 0xffffffu;
+    return p.region[q] + p.off_aug + uint64_t(next_slot) * p.aug_slot_bytes + uint64_t(p.nmax + j) * p.S;
+}
+
+// LSU path (any S % 4 == 0): grid-stride vector copies over the same lists.
 template <typename V>
 __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_constant__ StepParams p) {
-    extern __shared__ __align__(16) uint32_t sm[];
+    extern __shared__ __align__(128) uint32_t sm[];
     const CopySmem L = copy_smem(p.N, p.r, p.nmax);
-    uint32_t* praw = sm + L.praw;
+    uint32_t* xraw = sm + L.xraw;
     uint32_t* wraw = sm + L.wraw;
-    int* post = reinterpret_cast<int*>(sm + L.post);
-    uint32_t* win = sm + L.win;
-    uint32_t* defer = sm + L.defer;
+    uint32_t* jsrc = sm + L.jsrc;
     int* rowmap = reinterpret_cast<int*>(sm + L.rowmap);
     uint32_t* misc = sm + L.misc;
+    volatile uint32_t* ready = misc + 6;
 
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const uint32_t N = p.N, me = p.me, n = p.n;
-    const uint32_t R = plist_r(p.r), MJ = plist_mj(N, p.r);
     const uint64_t S = p.S;
     const uint32_t nvec = static_cast<uint32_t>(S / sizeof(V));
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     const bool do_assemble = p.mode & kModeAssemble;
-    const bool do_pull = (p.mode & kModePlan) && p.step > 0 && p.plist_in;
+    const bool do_push = (p.mode & kModePlan) && p.plist_in;
     const bool do_update = p.mode & kModeUpdate;
     const bool multi = (p.mode & kModePeers) && N > 1;
     const uint32_t part = blockIdx.x, parts = gridDim.x;
     const V* batch = reinterpret_cast<const V*>(p.batch);
     V* slab = reinterpret_cast<V*>(p.slab);
-    const uint64_t aug_off = p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
-    V* my_aug = reinterpret_cast<V*>(p.region[me] + aug_off);
-    const uint32_t row0 = p.nmax - n;
-    const uint32_t* owner = praw + 4;
-    const uint32_t* prow = praw + 4 + R;
-    const uint32_t* rrow = praw + 4 + 2 * R;
-    const uint32_t* rmask = rrow + MJ;
+    V* asm_dst = reinterpret_cast<V*>(p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes) +
+                 uint64_t(p.nmax - n) * nvec;
+    const uint32_t next_slot = (p.aslot + 1) % kAugRing;
+    const uint32_t* jdst = xraw + 4;
 
-    trace_at(p, 16);
     tl_mark(p, 2, false);
-    if (threadIdx.x == 0)
+    if (tid == 0)
         cta_mark(p, 0);
     asm volatile("griddepcontrol.launch_dependents;");
-    if (p.trace && tid == 0)
-        atomicMin(p.trace + 14, globaltimer());
-    volatile uint32_t* ready = misc + 6;
     if (tid < 16)
         misc[tid] = 0;
-    const uint32_t pw = do_pull ? plist_words(N, p.r) : 0;
+    const uint32_t pw = do_push ? plist_words(N, p.r) : 0;
     const uint32_t ww = do_update ? wlist_words(p.nmax) : 0;
     if (warp == 0) {
-        // list loads first (async into shared memory), before any bulk traffic of this CTA
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        // copy(i-1) of this rank is complete (kernel boundary: its slab writes are visible),
-        // so peers may pull round-i representatives from our slab: done[me] = i everywhere
-        if (multi && blockIdx.x == 0 && lane < N)
-            st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[lane])->done[me], p.step);
 #pragma unroll 1
-        for (uint32_t x = lane; x < pw; x += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(praw + x))),
+        for (uint32_t x = tid; x < pw; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(xraw + x))),
                          "l"(p.plist_in + x)
                          : "memory");
 #pragma unroll 1
-        for (uint32_t x = lane; x < ww; x += 32)
+        for (uint32_t x = tid; x < ww; x += 32)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(wraw + x))),
                          "l"(p.wlist + x)
                          : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    __syncthreads();  // chunk counters / ready flag zeroed; list loads issued
-
-    // ---- A + B with a static per-thread schedule: every thread (warp 0 included) issues
-    //      its A loads at once, then (lists ready) its B loads, and only then stores — both
-    //      memory latencies overlap. Thread t handles vectors lo + t + k*512 of each slice.
-    //      A's stores also perform the safe candidate writes of W_i (batch row -> slab row,
-    //      rowmap) from the same registers; B is then the pulls only.
-    constexpr int KA = sizeof(V) == 16 ? 8 : 16;  // A vectors in flight per thread
-    constexpr int KB = sizeof(V) == 16 ? 4 : 8;   // B vectors in flight per thread
-    const uint32_t T = kThreads;
+    __syncthreads();
+    const bool fuse = do_assemble;
+    if (warp == 0) {
+        copy_parse(p, xraw, wraw, jsrc, rowmap, misc, ready, do_push, do_update, fuse);
+        if (blockIdx.x == 0 && do_assemble) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            copy_counts(p, xraw);
+        }
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // copy(i-1) complete (slab at version i)
+    // A: m_i -> m'_i (+ fused W_i slab writes)
     const uint32_t tva = do_assemble ? n * nvec : 0;
     const uint32_t alo = static_cast<uint32_t>(uint64_t(tva) * part / parts);
     const uint32_t ahi = static_cast<uint32_t>(uint64_t(tva) * (part + 1) / parts);
-    const V* batch_v = batch;
-    V ra[KA];
-    uint32_t a_next = alo + tid;
-    const bool lists_first = p.dbg & 4;  // every warp waits for the lists before its A loads
-    const bool late0 = ((p.dbg & 2) && warp == 0) || lists_first;
-    if ((p.dbg >> 8) && warp != 0)
-        __nanosleep(p.dbg >> 8);
-    if (!late0) {
+    constexpr int U = sizeof(V) == 16 ? 4 : 8;
+#pragma unroll 1
+    for (uint32_t g0 = alo + tid; g0 < ahi; g0 += U * kThreads) {
+        V v[U];
 #pragma unroll
-        for (int k = 0; k < KA; ++k) {
-            const uint32_t gv = a_next + k * T;
-            if (gv < ahi)
-                ra[k] = ld_vec(batch_v + gv);
-        }
-    }
-    const bool fuse = do_assemble && !(p.dbg & 1);  // safe writes ride on A (else: B jobs)
-    if (warp == 0)
-        copy_parse_lists(p, CopyLists{praw, wraw, win, defer, misc, post, rowmap, ready}, do_pull, do_update,
-                         multi, fuse);
-    V* asm_dst = my_aug + uint64_t(row0) * nvec;
-    auto a_store = [&](uint32_t gv, const V& v) {
-        asm_dst[gv] = v;
-        if (fuse) {
-            const uint32_t row = gv / nvec;
-            const int key = rowmap[row];
-            if (key >= 0)
-                slab[uint64_t(key) * nvec + (gv - row * nvec)] = v;
-        }
-    };
-    auto b_src = [&](uint32_t gv, uint32_t pv_tot) -> const V* {
-        if (gv < pv_tot) {
-            const uint32_t j = gv / nvec, off = gv - j * nvec;
-            return reinterpret_cast<const V*>(p.slab_peer[praw[4 + j]]) + uint64_t(praw[4 + R + j]) * nvec + off;
-        }
-        const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
-        return batch + uint64_t(win[2 * job]) * nvec + off;
-    };
-    auto b_store = [&](uint32_t gv, uint32_t pv_tot, const V& v) {
-        if (gv < pv_tot) {
-            const uint32_t j = gv / nvec, off = gv - j * nvec;
-            my_aug[uint64_t(p.nmax + j) * nvec + off] = v;
-        } else {
-            const uint32_t wv = gv - pv_tot, job = wv / nvec, off = wv - job * nvec;
-            slab[uint64_t(win[2 * job + 1]) * nvec + off] = v;
-        }
-    };
-    if (tid == 32)
-        cta_mark(p, 2);  // warp 1: A loads issued
-    if (lists_first) {
-        while (*ready == 0)
-            __nanosleep(20);
-    }
-    if (late0) {
+        for (int u = 0; u < U; ++u)
+            if (g0 + u * kThreads < ahi)
+                v[u] = ld_vec(batch + g0 + u * kThreads);
 #pragma unroll
-        for (int k = 0; k < KA; ++k) {
-            const uint32_t gv = a_next + k * T;
-            if (gv < ahi)
-                ra[k] = ld_vec(batch_v + gv);
+        for (int u = 0; u < U; ++u) {
+            const uint32_t gv = g0 + u * kThreads;
+            if (gv < ahi) {
+                asm_dst[gv] = v[u];
+                const uint32_t row = gv / nvec;
+                const int key = rowmap[row];
+                if (key >= 0)
+                    slab[uint64_t(key) * nvec + (gv - row * nvec)] = v[u];
+            }
         }
     }
-    // lists staged (warp 0) -> B bounds
-    if (p.trace && blockIdx.x == 0 && lane == 0)
-        atomicMin(p.trace + 21, globaltimer());
-    while (*ready == 0)
-        __nanosleep(20);
-    __threadfence_block();
     if (tid == 32)
-        cta_mark(p, 3);  // warp 1 past the lists-ready wait
-    const uint32_t cnt = misc[0];
-    const uint32_t pv_tot = cnt * nvec;
-    const uint32_t tvb = pv_tot + misc[1] * nvec;
+        cta_mark(p, 5);
+    // B: push jobs, then (no assembly) the W_i writes
+    const uint32_t nj = misc[0], nw = misc[1];
+    const uint32_t pv = nj * nvec;
+    const uint32_t tvb = pv + nw * nvec;
     const uint32_t blo = static_cast<uint32_t>(uint64_t(tvb) * part / parts);
     const uint32_t bhi = static_cast<uint32_t>(uint64_t(tvb) * (part + 1) / parts);
-    V rb[KB];
-    uint32_t b_next = blo + tid;
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-        const uint32_t gv = b_next + k * T;
-        if (gv < bhi)
-            rb[k] = ld_pull(b_src(gv, pv_tot));
-    }
-    if (tid == 32)
-        cta_mark(p, 4);  // B loads issued
-#pragma unroll
-    for (int k = 0; k < KA; ++k) {
-        const uint32_t gv = a_next + k * T;
-        if (gv < ahi)
-            a_store(gv, ra[k]);
-    }
-    if (tid == 32)
-        cta_mark(p, 5);  // A data in, stores issued
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-        const uint32_t gv = b_next + k * T;
-        if (gv < bhi)
-            b_store(gv, pv_tot, rb[k]);
-    }
-    if (tid == 32)
-        cta_mark(p, 6);  // B data in, stores issued
-    // larger slices: further rounds
-    for (a_next += KA * T; a_next < ahi; a_next += KA * T) {
-#pragma unroll
-        for (int k = 0; k < KA; ++k) {
-            const uint32_t gv = a_next + k * T;
-            if (gv < ahi)
-                ra[k] = ld_vec(batch + gv);
-        }
-#pragma unroll
-        for (int k = 0; k < KA; ++k) {
-            const uint32_t gv = a_next + k * T;
-            if (gv < ahi)
-                a_store(gv, ra[k]);
-        }
-    }
-    for (b_next += KB * T; b_next < bhi; b_next += KB * T) {
-#pragma unroll
-        for (int k = 0; k < KB; ++k) {
-            const uint32_t gv = b_next + k * T;
-            if (gv < bhi)
-                rb[k] = ld_pull(b_src(gv, pv_tot));
-        }
-#pragma unroll
-        for (int k = 0; k < KB; ++k) {
-            const uint32_t gv = b_next + k * T;
-            if (gv < bhi)
-                b_store(gv, pv_tot, rb[k]);
-        }
-    }
-    if (p.trace && blockIdx.x == 0 && lane == 0) {
-        atomicMin(p.trace + 22, globaltimer());  // first warp out of the chunk loop
-        atomicMax(p.trace + 18, globaltimer());  // last warp out
-    }
-    // ---- C: writes to rows this CTA pulled, after ALL its pulls (barrier only when this
-    //      CTA has one; the condition is uniform: it reads staged lists) ------------------
-    const uint32_t clo = blo, chi = min(bhi, pv_tot);
-    bool any_post = false;
-    if (clo < chi) {
-        const uint32_t j0 = clo / nvec, j1 = (chi - 1) / nvec;
-        for (uint32_t j = j0; j <= j1; ++j)
-            any_post |= post[j] >= 0;
-    }
-    if (any_post) {
-        __syncthreads();
 #pragma unroll 1
-        for (uint32_t gv = clo + tid; gv < chi; gv += kThreads) {
-            const uint32_t j = gv / nvec, off = gv - j * nvec;
-            const int pr = post[j];
-            if (pr >= 0)
-                slab[uint64_t(prow[j]) * nvec + off] = ld_vec(batch + uint64_t(pr) * nvec + off);
+    for (uint32_t gv = blo + tid; gv < bhi; gv += kThreads) {
+        if (gv < pv) {
+            const uint32_t x = gv / nvec, o = gv - x * nvec;
+            const uint32_t s = jsrc[x];
+            const V* src = (s >> 31) ? batch + uint64_t(s & 0x7fffffffu) * nvec : slab + uint64_t(s) * nvec;
+            reinterpret_cast<V*>(push_dst(p, jdst[x], next_slot))[o] = ld_vec(src + o);
+        } else {
+            const uint32_t t = (gv - pv) / nvec, o = (gv - pv) - t * nvec;
+            slab[uint64_t(wraw[3 + 2 * t]) * nvec + o] = ld_vec(batch + uint64_t(wraw[2 + 2 * t]) * nvec + o);
         }
     }
-    trace_at(p, 19);
+    if (tid == 32)
+        cta_mark(p, 6);
     if (multi) {
-        const uint32_t n_def = misc[2];
-        // ---- pulls of this rank done -> readdone[me] at every peer (last CTA). The pulled
-        //      values were consumed before the barrier, so a relaxed ticket suffices; the
-        //      flag itself is a release store (no bulk fence on the stores of the copy).
+        __threadfence_system();  // this thread's pushes, before the CTA's ticket
         __syncthreads();
-        if (tid == 0) {
-            const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->rticket), 1ull);
-            if ((t + 1) % gridDim.x == 0) {
-                if (p.trace)
-                    p.trace[23] = globaltimer();
-                for (uint32_t w = 0; w < N; ++w)
-                    st_relaxed_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->readdone[me], p.step + 1);
-            }
-        }
-        // ---- D: writes to rows remote requesters pull, after their pulls ------------------
-        if (n_def) {
-            if (tid == 0) {
-                uint32_t readers = 1u << me;  // own pulls of the row too (other CTAs)
-                for (uint32_t x = 0; x < n_def; ++x)
-                    readers |= defer[3 * x + 2];
-                for (uint32_t w = 0; w < N; ++w)
-                    if (((readers >> w) & 1u) && !wait_flag(&hdr->readdone[w], p.step + 1, p.timeout_ns) &&
-                        p.mailbox) {
-                        volatile uint32_t* mb = p.mailbox;
-                        mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
-                        mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
-                    }
-            }
-            __syncthreads();
-            const uint32_t tvd = n_def * nvec;
-            const uint32_t dlo = static_cast<uint32_t>(uint64_t(tvd) * part / parts);
-            const uint32_t dhi = static_cast<uint32_t>(uint64_t(tvd) * (part + 1) / parts);
-#pragma unroll 1
-            for (uint32_t gv = dlo + tid; gv < dhi; gv += kThreads) {
-                const uint32_t x = gv / nvec, off = gv - x * nvec;
-                slab[uint64_t(defer[3 * x + 1]) * nvec + off] = ld_vec(batch + uint64_t(defer[3 * x]) * nvec + off);
-            }
-        }
-        // (done[me] = i+1 is published by copy(i+1) at its start)
+        copy_finish_peers(p);
     }
-    if (p.trace && tid == 0)
-        atomicMax(p.trace + 15, globaltimer());
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
@@ -1198,18 +967,18 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
 }
 
 // ---- TMA bulk-copy path (S % 16 == 0) ---------------------------------------------------
-// The same copy(i) as drb_copy_kernel, moved with the SM's TMA engine instead of LSU
-// loads/stores: 1-D cp.async.bulk global->shared (mbarrier completion) and
-// shared->global (bulk groups). Bytes in flight per SM are bounded by the shared-memory
-// ring (kTmaStages x kTmaChunk), not by the L1 miss-tracking capacity that throttles
-// 16-byte vector loads; two elected threads issue everything:
-//   warp 1 lane 0  A: batch slice -> ring -> m'_i rows, then (lists parsed) the same ring
-//                  bytes -> slab rows of the safe W_i winners (rowmap)
-//   warp 0         staged lists (copy_parse_lists), then lane 0: B pulls owner slab ->
-//                  ring -> m'_i rep rows; C: a round-i write to a pulled row is loaded
-//                  alongside and stored only after the pull's load completed;
-//                  non-fused safe writes (update_buffer without assembly)
-//   all            D (remote-read rows, multi-GPU) after the readers' readdone, LSU path
+// The same copy(i) moved by the SM's TMA engine: 1-D cp.async.bulk global->shared
+// (mbarrier completion) and shared->global (bulk groups), so the bytes in flight per SM
+// are bounded by the shared-memory ring, not by the L1 miss-tracking capacity that
+// throttles 16-byte vector loads. Two elected threads issue everything:
+//   warp 1 lane 0  A: batch slice -> ring -> m'_i rows; after griddepcontrol.wait the same
+//                  ring bytes -> slab rows of the W_i winners (rowmap)
+//   warp 0         staged lists (copy_parse), CTA 0's counts; lane 0 B: push jobs
+//                  (slot bytes -> ring -> requester's m'_{i+1} row, local HBM or a peer's)
+//                  and, without assembly, the W_i writes
+// Everything before griddepcontrol.wait (list staging and parsing, A's loads and m'_i
+// stores) is independent of copy(i-1), so under PDL it overlaps copy(i-1)'s tail: the
+// kernel is sized (<= half an SM's shared memory) for two co-resident CTAs.
 __device__ __forceinline__ uint64_t min64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
@@ -1221,15 +990,33 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+// Wait for phase `parity` of barrier b to complete. Bounded: a bulk copy that never lands
+// (a fault) must not hang the GPU — after timeout_ns the wait gives up and returns false.
+__device__ __forceinline__ bool mbar_wait(uint64_t* b, uint32_t parity, uint64_t timeout_ns = 4000000000ull) {
     uint32_t ok = 0;
-    while (!ok)
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0;; ++spin) {
         asm volatile(
             "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n selp.u32 %0, 1, 0, q;\n}"
             : "=r"(ok)
             : "r"(smem_u32(b)), "r"(parity)
             : "memory");
+        if (ok)
+            return true;
+        if (spin == 64)
+            t0 = globaltimer();
+        else if (spin > 64 && (spin & 63) == 0 && globaltimer() - t0 > timeout_ns)
+            return false;
+    }
 }
+// Per-barrier phase bits of an engine thread: barrier x of a ring is waited on with bit x,
+// which then flips (a partially used window leaves the other barriers' phases alone).
+__device__ __forceinline__ uint32_t take_phase(uint32_t& bits, uint32_t x) {
+    const uint32_t ph = (bits >> x) & 1u;
+    bits ^= 1u << x;
+    return ph;
+}
+
 __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst_smem)),
@@ -1243,15 +1030,14 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __grid_constant__ StepParams p) {
     extern __shared__ __align__(128) uint32_t sm[];
     const CopySmem L = copy_smem(p.N, p.r, p.nmax);
-    uint32_t* praw = sm + L.praw;
+    uint32_t* xraw = sm + L.xraw;
     uint32_t* wraw = sm + L.wraw;
-    int* post = reinterpret_cast<int*>(sm + L.post);
-    uint32_t* win = sm + L.win;
-    uint32_t* defer = sm + L.defer;
+    uint32_t* jsrc = sm + L.jsrc;
     int* rowmap = reinterpret_cast<int*>(sm + L.rowmap);
     uint32_t* misc = sm + L.misc;
     const TmaSmem T = tma_smem(p.N, p.r, p.nmax);
@@ -1260,20 +1046,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t N = p.N, me = p.me, n = p.n;
-    const uint32_t R = plist_r(p.r);
     const uint64_t S = p.S;
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     const bool do_assemble = p.mode & kModeAssemble;
-    const bool do_pull = (p.mode & kModePlan) && p.step > 0 && p.plist_in;
+    const bool do_push = (p.mode & kModePlan) && p.plist_in;
     const bool do_update = p.mode & kModeUpdate;
     const bool multi = (p.mode & kModePeers) && N > 1;
     const uint32_t part = blockIdx.x, parts = gridDim.x;
     const uint8_t* batch = reinterpret_cast<const uint8_t*>(p.batch);
     uint8_t* slab = reinterpret_cast<uint8_t*>(p.slab);
     uint8_t* my_aug = p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
+    const uint32_t next_slot = (p.aslot + 1) % kAugRing;
     const uint32_t row0 = p.nmax - n;
-    const uint32_t* owner = praw + 4;
-    const uint32_t* prow = praw + 4 + R;
+    const uint32_t* jdst = xraw + 4;
     volatile uint32_t* ready = misc + 6;
 
     tl_mark(p, 2, false);
@@ -1283,21 +1067,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
     if (tid < 16)
         misc[tid] = 0;
     if (tid == 0 || tid == 32) {  // each engine thread owns its barriers
-        const uint32_t b0 = tid == 0 ? kTmaStagesA : 0, b1 = tid == 0 ? kTmaStages + kTmaStagesB : kTmaStagesA;
+        const uint32_t b0 = tid == 0 ? kTmaStagesA : 0, b1 = tid == 0 ? kTmaStages : kTmaStagesA;
         for (uint32_t b = b0; b < b1; ++b)
             mbar_init(bars + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    const uint32_t pw = do_pull ? plist_words(N, p.r) : 0;
+    const uint32_t pw = do_push ? plist_words(N, p.r) : 0;
     const uint32_t ww = do_update ? wlist_words(p.nmax) : 0;
     if (warp == 0) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (multi && blockIdx.x == 0 && lane < N)
-            st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[lane])->done[me], p.step);
 #pragma unroll 1
         for (uint32_t x = lane; x < pw; x += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(praw + x)), "l"(p.plist_in + x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xraw + x)), "l"(p.plist_in + x)
                          : "memory");
 #pragma unroll 1
         for (uint32_t x = lane; x < ww; x += 32)
@@ -1306,16 +1087,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __syncthreads();  // misc / ready zeroed, barriers initialised, list loads issued
+    if (tid == 32)
+        cta_mark(p, 8);
 
     const uint32_t CH = kTmaChunk;
     if (warp == 1) {
-        // ---- A engine: batch bytes [alo, ahi) of this CTA -> m'_i (+ safe slab rows) ----
+        // ---- A engine: batch bytes [alo, ahi) of this CTA -> m'_i (+ W_i winners' slab rows) ----
         if (lane == 0) {
-            const uint64_t a16 = do_assemble ? (uint64_t(n) * S) >> 4 : 0;
+            const uint64_t a16 = (do_assemble && !(p.dbg & 128)) ? (uint64_t(n) * S) >> 4 : 0;  // 128: no bytes
             const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
             const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
             uint8_t* dst = my_aug + uint64_t(row0) * S;
-            uint32_t ph_base = 0;  // uses of each A barrier so far (parity)
+            uint32_t ph_bits = 0;  // phase of each A barrier
             bool lists = false;
             for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
                 const uint32_t w1 = min(nA, w0 + kTmaStagesA);
@@ -1328,25 +1111,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
                     mbar_expect_tx(bar, len);
                     bulk_load(ring + (k - w0) * CH, batch + off, len, bar);
                 }
-                if (w0 == 0 && tid == 32)
+                if (w0 == 0)
                     cta_mark(p, 2);
                 for (uint32_t k = w0; k < w1; ++k) {  // m'_i rows as soon as each piece lands
                     const uint64_t off = alo + uint64_t(k) * CH;
                     const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
-                    mbar_wait(bars + (k - w0), ph_base & 1);
+                    if (!mbar_wait(bars + (k - w0), take_phase(ph_bits, k - w0)))
+                        mailbox_fail(p, DRB_ERR_INTERNAL);
+                    if (k == 0)
+                        cta_mark(p, 11);
                     bulk_store(dst + off, ring + (k - w0) * CH, len);
                 }
                 bulk_commit();
                 if (w0 == 0)
                     cta_mark(p, 5);
-                if (!lists) {
+                if (!lists) {  // slab rows: after copy(i-1) (its reads of them) and the lists
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
                     while (*ready == 0)
                         __nanosleep(20);
                     __threadfence_block();
                     lists = true;
                     cta_mark(p, 3);
                 }
-                for (uint32_t k = w0; k < w1; ++k) {  // safe W_i winners among these rows
+                for (uint32_t k = w0; k < w1; ++k) {  // W_i winners among these rows
                     uint64_t off = alo + uint64_t(k) * CH;
                     const uint64_t end = off + min64(CH, ahi - off);
                     while (off < end) {
@@ -1361,121 +1148,552 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
                     }
                 }
                 bulk_commit();
-                ++ph_base;
             }
             bulk_wait_read_all();
             cta_mark(p, 6);
         }
     } else if (warp == 0) {
-        copy_parse_lists(p, CopyLists{praw, wraw, win, defer, misc, post, rowmap, ready}, do_pull, do_update,
-                         multi, do_assemble);
-        if (tid == 0)
-            cta_mark(p, 1);
+        copy_parse(p, xraw, wraw, jsrc, rowmap, misc, ready, do_push, do_update, do_assemble);
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // copy(i-1) complete: slab at version i
+        if (lane == 0)
+            cta_mark(p, 10);
+        if (blockIdx.x == 0 && do_assemble)
+            copy_counts(p, xraw);
         if (lane == 0) {
-            // ---- B engine: pulls (+ C after each pull's read) and non-fused safe writes ----
+            // ---- B engine: push jobs (+ non-fused W_i writes) ----
             uint8_t* ringB = ring + kTmaStagesA * CH;
-            uint8_t* ringC = ring + kTmaStages * CH;
             uint64_t* barB = bars + kTmaStagesA;
-            uint64_t* barC = bars + kTmaStages;
-            const uint32_t cnt = misc[0];
-            const uint64_t pv = uint64_t(cnt) * S;
-            const uint64_t sv = do_assemble ? 0 : uint64_t(misc[1]) * S;
-            const uint64_t b16 = (pv + sv) >> 4;
+            const uint32_t nj = misc[0];
+            const uint64_t pv = uint64_t(nj) * S;
+            const uint64_t sv = uint64_t(misc[1]) * S;
+            const uint64_t b16 = (p.dbg & 128) ? 0 : (pv + sv) >> 4;
             const uint64_t blo = (b16 * part / parts) << 4, bhi = (b16 * (part + 1) / parts) << 4;
-            uint32_t use = 0;   // window count (B barrier parity)
-            uint32_t cpar = 0;  // C barrier parities (bit x), armed only with a hazard
+            uint32_t use = 0;      // window count
+            uint32_t ph_bits = 0;  // phase of each B barrier
             uint64_t off = blo;
             while (off < bhi) {
                 // one window: up to kTmaStagesB pieces, each inside one row and <= CH
                 uint64_t poff[kTmaStagesB];
                 uint32_t plen[kTmaStagesB], m = 0;
                 while (m < kTmaStagesB && off < bhi) {
-                    const bool is_pull = off < pv;
-                    const uint64_t base = is_pull ? 0 : pv;
+                    const bool is_job = off < pv;
+                    const uint64_t base = is_job ? 0 : pv;
                     const uint32_t j = static_cast<uint32_t>((off - base) / S);
-                    const uint64_t rend = min64(min64(bhi, is_pull ? pv : pv + sv), base + uint64_t(j + 1) * S);
+                    const uint64_t rend = min64(bhi, base + uint64_t(j + 1) * S);
                     const uint32_t len = static_cast<uint32_t>(min64(CH, rend - off));
+                    const uint64_t o = off - base - uint64_t(j) * S;
+                    const uint8_t* src;
+                    if (is_job) {
+                        const uint32_t s = jsrc[j];
+                        src = ((s >> 31) ? batch + uint64_t(s & 0x7fffffffu) * S : slab + uint64_t(s) * S) + o;
+                    } else {
+                        src = batch + uint64_t(wraw[2 + 2 * j]) * S + o;
+                    }
                     poff[m] = off;
                     plen[m] = len;
-                    const uint64_t o = off - base - uint64_t(j) * S;
-                    const uint8_t* src = is_pull ? p.slab_peer[owner[j]] + uint64_t(prow[j]) * S + o
-                                                 : batch + uint64_t(win[2 * j]) * S + o;
                     mbar_expect_tx(barB + m, len);
                     bulk_load(ringB + m * CH, src, len, barB + m);
-                    if (is_pull && post[j] >= 0) {  // C: the new round-i bytes of the pulled row
-                        mbar_expect_tx(barC + m, len);
-                        bulk_load(ringC + m * CH, batch + uint64_t(post[j]) * S + o, len, barC + m);
-                    }
                     off += len;
                     ++m;
                 }
-                if (use == 0 && tid == 0)
+                if (use == 0)
                     cta_mark(p, 4);
                 for (uint32_t x = 0; x < m; ++x) {
-                    const bool is_pull = poff[x] < pv;
-                    const uint64_t base = is_pull ? 0 : pv;
+                    const bool is_job = poff[x] < pv;
+                    const uint64_t base = is_job ? 0 : pv;
                     const uint32_t j = static_cast<uint32_t>((poff[x] - base) / S);
                     const uint64_t o = poff[x] - base - uint64_t(j) * S;
-                    mbar_wait(barB + x, use & 1);  // the pull's read of the slab row is complete
-                    if (is_pull) {
-                        bulk_store(my_aug + uint64_t(p.nmax + j) * S + o, ringB + x * CH, plen[x]);
-                        if (post[j] >= 0) {
-                            mbar_wait(barC + x, (cpar >> x) & 1u);
-                            cpar ^= 1u << x;
-                            bulk_store(slab + uint64_t(prow[j]) * S + o, ringC + x * CH, plen[x]);
-                        }
-                    } else {
-                        bulk_store(slab + uint64_t(win[2 * j + 1]) * S + o, ringB + x * CH, plen[x]);
-                    }
+                    uint8_t* dst = is_job ? push_dst(p, jdst[j], next_slot) + o
+                                          : slab + uint64_t(wraw[3 + 2 * j]) * S + o;
+                    if (!mbar_wait(barB + x, take_phase(ph_bits, x)))
+                        mailbox_fail(p, DRB_ERR_INTERNAL);
+                    bulk_store(dst, ringB + x * CH, plen[x]);
                 }
                 bulk_commit();
                 bulk_wait_read_all();  // the ring is reused by the next window
                 ++use;
             }
-        }
-    }
-    __syncthreads();  // all pulls of this CTA read, all bulk stores issued and sourced
-    if (multi) {
-        const uint32_t n_def = misc[2];
-        if (tid == 0) {
-            const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->rticket), 1ull);
-            if ((t + 1) % gridDim.x == 0)
-                for (uint32_t w = 0; w < N; ++w)
-                    st_relaxed_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->readdone[me], p.step + 1);
-        }
-        if (n_def) {  // D: rows remote requesters pull, after their pulls (LSU path, rare)
-            if (tid == 0) {
-                uint32_t readers = 1u << me;
-                for (uint32_t x = 0; x < n_def; ++x)
-                    readers |= defer[3 * x + 2];
-                for (uint32_t w = 0; w < N; ++w)
-                    if (((readers >> w) & 1u) && !wait_flag(&hdr->readdone[w], p.step + 1, p.timeout_ns) &&
-                        p.mailbox) {
-                        volatile uint32_t* mb = p.mailbox;
-                        mb[kAugRing + p.aslot] = DRB_ERR_TRANSPORT;
-                        mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
-                    }
-            }
-            __syncthreads();
-            const uint32_t nvec = static_cast<uint32_t>(S / 16);
-            const uint32_t tvd = n_def * nvec;
-            const uint32_t dlo = static_cast<uint32_t>(uint64_t(tvd) * part / parts);
-            const uint32_t dhi = static_cast<uint32_t>(uint64_t(tvd) * (part + 1) / parts);
-            const uint4* bv = reinterpret_cast<const uint4*>(batch);
-            uint4* sv = reinterpret_cast<uint4*>(slab);
-#pragma unroll 1
-            for (uint32_t gv = dlo + tid; gv < dhi; gv += blockDim.x) {
-                const uint32_t x = gv / nvec, o = gv - x * nvec;
-                sv[uint64_t(defer[3 * x + 1]) * nvec + o] = ld_vec(bv + uint64_t(defer[3 * x]) * nvec + o);
+            cta_mark(p, 9);
+            if (multi) {  // the pushes are complete before the CTA's ticket
+                bulk_wait_all();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence_system();
             }
         }
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();  // all bulk stores of this CTA issued and sourced
+    if (multi)
+        copy_finish_peers(p);
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
         if (tid == 0)
             cta_mark(p, 7);
     }
+}
+
+// ---- persistent run (drb_rb_run over a resident input ring) --------------------------------
+// One cooperative launch for `steps` iterations (all CTAs co-resident): CTA 0 loops the sel
+// chain, CTA 1 the plan chain, CTAs 2.. the copies; the hand-offs that the three-kernel
+// path expresses as launches and stream events become device counters in RunCtl. The
+// selection / sampling state stays in shared memory across iterations, the next labels are
+// fetched while the current selection runs, and nothing is launched per iteration. Every
+// decision is the same code as the three-kernel path (sel_core, plan_core, copy_parse, the
+// push-at-source copy), so the outputs are bit-identical.
+//   sel(k)   waits B(k-8) (W slot), plan(k-4) (table slot); multi-rank B(k-3) of every rank
+//            (the pushes into the m' slot that plan(k)'s requesters refill)
+//   plan(k)  waits sel(k), B(k-8) (X slot), peers' occupancy rows v=i+1
+//   A(k)     (batch -> m'_i) waits B(k-3) (bounded run-ahead)
+//   B(k)     (W_i writes, X_i pushes, by byte column) waits sel(k), plan(k) only
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// *f >= want, or false once the run failed / the wait timed out (then the run is failed).
+__device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, bool sys) {
+    const uint64_t t0 = globaltimer();
+    for (;;) {
+        const uint64_t v = sys ? ld_acquire_sys(f) : ld_acquire_gpu(f);
+        if (v >= want)
+            return true;
+        if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+            return false;
+        if (globaltimer() - t0 > rp.base.timeout_ns) {
+            atomicExch(&rp.ctl->error, DRB_ERR_TRANSPORT);
+            if (rp.base.mailbox) {
+                volatile uint32_t* mb = rp.base.mailbox;
+                mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
+            }
+            return false;
+        }
+        __nanosleep(20);
+    }
+}
+__device__ __forceinline__ uint64_t back(uint64_t k, uint64_t d) { return k >= d ? k - d : 0; }
+
+// StepParams of run iteration k (= engine iteration i0 + k), as iter_params() on the host
+__device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t k) {
+    const uint64_t i = rp.i0 + k, v = rp.ver0 + i;
+    p.tslot_in = static_cast<uint32_t>(v % kTableRing);
+    p.tslot_out = static_cast<uint32_t>((v + 1) % kTableRing);
+    p.sel_in = rp.sel_base + ((rp.sel_par0 + i) & 1);
+    p.sel_out = rp.sel_base + ((rp.sel_par0 + i + 1) & 1);
+    p.plan_in = rp.plan_base + ((rp.plan_par0 + i) & 1);
+    p.plan_out = rp.plan_base + ((rp.plan_par0 + i + 1) & 1);
+    const uint64_t slot = (rp.first + k) % rp.ring;
+    p.batch = rp.batches + slot * rp.batch_stride;
+    p.labels = rp.labels + slot * rp.label_stride;
+    p.n = rp.n;
+    p.step = i;
+    p.seq = i;
+    p.aslot = static_cast<uint32_t>(i % kAugRing);
+    p.plist_in = rp.plist_base + (i % kListRing) * rp.pw;
+    p.plist_out = const_cast<uint32_t*>(p.plist_in);
+    p.wlist = rp.wlist_base + (i % kListRing) * rp.ww;
+}
+
+// per-CTA timeline stamp of engine iteration i (timeline mode), any thread
+__device__ __forceinline__ void run_mark(const RunParams& rp, uint64_t i, int slot) {
+    const StepParams& p = rp.base;
+    if (p.timeline && blockIdx.x < kTlMaxCtas)
+        p.timeline[(i % p.timeline_steps) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = globaltimer();
+}
+
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Waits on run counters keep the last value seen, so a satisfied wait costs no memory trip.
+struct SeenFlag {
+    const uint64_t* f;
+    uint64_t seen;
+};
+__device__ __forceinline__ bool wait_seen(SeenFlag& s, uint64_t want, const RunParams& rp, bool sys = false) {
+    if (s.seen >= want)
+        return true;
+    if (!run_wait(s.f, want, rp, sys))
+        return false;
+    s.seen = sys ? ld_acquire_sys(s.f) : ld_acquire_gpu(s.f);
+    return true;
+}
+
+// CTA 0: the sel chain. Warp 0 runs sel(k) while warps 1-3 fetch the labels of m_{k+1}.
+__device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    if (tid >= kSelThreads)
+        return;
+    const StepParams& b = rp.base;
+    const uint32_t N = b.N, me = b.me;
+    const bool multi = (b.mode & kModePeers) && N > 1;
+    SelView v = sel_view(sm, b);
+    uint32_t* lab2 = sm + sel_smem(b.K, b.nmax).words;  // second label buffer (prefetch)
+    uint32_t* labs[2] = {v.lab, lab2};
+    if (tid == 0) {
+        sp = b;
+        run_patch(sp, rp, 0);
+    }
+    named_bar(1, kSelThreads);
+    {  // state and the own occupancy row at the start of the run (written before the launch)
+        const uint32_t* tin = reinterpret_cast<const uint32_t*>(sp.region[me] + sp.off_table) +
+                              uint64_t(sp.tslot_in) * N * sp.K + uint64_t(me) * sp.K;
+        if (tid < sizeof(SelState) / 8)
+            reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.sel_in) + tid);
+        for (uint32_t x = tid; x < sp.K; x += kSelThreads)
+            v.occ[x] = __ldcg(tin + x);
+        if (tid == 0)
+            flag[2] = 0;
+        named_bar(1, kSelThreads);
+        if (sel_load_labels(sp, v, kSelThreads))
+            atomicOr(&flag[2], 1u);
+    }
+    SeenFlag bdone{&rp.ctl->b_done, 0}, pdone{&rp.ctl->plan_done, 0};
+    const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(b.region[me]);
+#pragma unroll 1
+    for (uint64_t k = 0; k < rp.steps; ++k) {
+        if (tid == 0) {
+            if (k > 0)
+                run_patch(sp, rp, k);
+            bool ok = wait_seen(bdone, back(k, multi ? 2 : kListRing - 1), rp) && wait_seen(pdone, back(k, 3), rp);
+            for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-3) complete
+                if (w != me && sp.step >= 3)
+                    ok = run_wait(&hdr->pushdone[w], sp.step - 2, rp, true);
+            flag[1] = ok ? 0u : 1u;
+            flag[0] = flag[2];  // "bad" of m_k's labels
+            flag[3] = 0;
+        }
+        named_bar(1, kSelThreads);
+        if (flag[1])
+            return;
+        v.lab = labs[k & 1];
+        if (warp == 0) {
+            tl_mark(sp, 0, false);
+            trace_at(sp, 0);
+            sel_core(sp, v, flag[0] != 0);
+            __syncwarp();
+            if (tid == 0) {  // release: the warp's W_i / state / row stores precede it
+                st_release_gpu(&rp.ctl->sel_done, k + 1);
+                tl_mark(sp, 0, true);
+            }
+        } else if (k + 1 < rp.steps) {  // labels of m_{k+1}
+            const uint64_t slot = (rp.first + k + 1) % rp.ring;
+            const uint32_t* lp = rp.labels + slot * rp.label_stride;
+            int bad = 0;
+            for (uint32_t x = tid - 32; x < rp.n; x += kSelThreads - 32) {
+                const uint32_t l = __ldg(lp + x);
+                labs[(k + 1) & 1][x] = l;
+                bad |= l >= sp.K;
+            }
+            if (bad)
+                atomicOr(&flag[3], 1u);
+        }
+        named_bar(1, kSelThreads);
+        if (tid == 0)
+            flag[2] = flag[3];
+    }
+}
+
+// CTA 1: the plan chain.
+__device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
+    const uint32_t tid = threadIdx.x, N = rp.base.N, me = rp.base.me;
+    const bool multi = (rp.base.mode & kModePeers) && N > 1;
+    const PlanView v = plan_view(sm, rp.base);
+    if (tid == 0) {
+        sp = rp.base;
+        run_patch(sp, rp, 0);
+    }
+    __syncthreads();
+    if (tid < sizeof(PlanState) / 8)
+        reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.plan_in) + tid);
+    SeenFlag sdone{&rp.ctl->sel_done, 0}, bdone{&rp.ctl->b_done, 0};
+    const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(rp.base.region[me]);
+#pragma unroll 1
+    for (uint64_t k = 0; k < rp.steps; ++k) {
+        if (tid == 0) {
+            if (k > 0)
+                run_patch(sp, rp, k);
+            bool ok = wait_seen(sdone, k + 1, rp) && wait_seen(bdone, back(k, kListRing - 1), rp);
+            // size rendezvous v = i+1 (size_table.cpp:66-100): every peer's row
+            for (uint32_t w = 0; ok && multi && w < N; ++w)
+                if (w != me)
+                    ok = run_wait(&hdr->occ_flag[w], sp.step + 1, rp, true);
+            flag[1] = ok ? 0u : 1u;
+            v.misc[0] = 0;
+        }
+        __syncthreads();
+        if (flag[1])
+            return;
+        tl_mark(sp, 1, false);
+        trace_at(sp, 5);
+        plan_core(sp, v);
+        __syncthreads();
+        if (tid == 0) {  // release after the CTA barrier: X_i and the state precede it
+            st_release_gpu(&rp.ctl->plan_done, k + 1);
+            tl_mark(sp, 1, true);
+        }
+    }
+}
+
+// B(k) of a copy CTA is complete: fence, arrive. Copy CTAs are not in lockstep, so arrivals
+// are counted per iteration (slot k % 8); the last arrival of k releases b_done = k+1 once
+// b_done = k (in order) and, multi-rank, pushdone = i+1 at every peer.
+__device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t k, bool multi) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk stores, for generic-proxy readers
+    uint32_t* t = &rp.ctl->ticket[k & 7];
+    uint32_t old;
+    if (multi)  // acq_rel: the last arrival's releases below cover every arrival's stores
+        asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    else
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    if (old + 1 == rp.copy_ctas) {
+        *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+8
+        if (!run_wait(&rp.ctl->b_done, k, rp, false))
+            return;
+        if (multi)
+            for (uint32_t w = 0; w < p.N; ++w)
+                if (w != p.me)
+                    st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->pushdone[p.me], rp.i0 + k + 1);
+        st_release_gpu(&rp.ctl->b_done, k + 1);
+    }
+}
+
+// CTAs 2..: copies. Warp 1 lane 0 streams m_i -> m'_i (flat slice of the batch bytes), at
+// most two iterations ahead of the completed B. Warp 0 does B on a fixed COLUMN of every
+// row — bytes [c0, c1) of each slab row it writes (W_i) and each slot it pushes (X_i) — so
+// every read and write of a given slab byte happens in this one CTA, in program order:
+// there is no grid-wide hand-off between iterations. The one cross-iteration hazard (a
+// slot pushed in k that B(k-1) wrote) waits for this CTA's previous stores to complete.
+__device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams& sp) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp >= 2)
+        return;
+    const StepParams& b = rp.base;
+    const CopySmem L = copy_smem(b.N, b.r, b.nmax);
+    uint32_t* xraw = sm + L.xraw;
+    uint32_t* wraw = sm + L.wraw;
+    uint32_t* jsrc = sm + L.jsrc;
+    int* rowmap = reinterpret_cast<int*>(sm + L.rowmap);
+    uint32_t* misc = sm + L.misc;
+    const RunSmem R = run_smem(b.N, b.K, b.r, b.nmax);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm) + R.bars);
+    uint8_t* ringA = reinterpret_cast<uint8_t*>(sm) + R.ring_a;
+    uint8_t* arena = reinterpret_cast<uint8_t*>(sm) + R.arena;
+    uint32_t* prevw = sm + R.prevw;  // slab rows of W_{k-1}
+    const uint32_t part = blockIdx.x - 2, parts = rp.copy_ctas;
+    const uint64_t S = b.S;
+    const bool multi = (b.mode & kModePeers) && b.N > 1;
+    const uint32_t CH = kTmaChunk;
+    if (tid == 0 || tid == 32) {
+        const uint32_t b0 = tid == 0 ? kTmaStagesA : 0, b1 = tid == 0 ? kTmaStagesA + 1 : kTmaStagesA;
+        for (uint32_t x = b0; x < b1; ++x)
+            mbar_init(bars + x, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
+        if (lane != 0)
+            return;
+        const uint64_t a16 = (uint64_t(rp.n) * S) >> 4;
+        const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
+        const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
+        const uint32_t row0 = b.nmax - rp.n;
+        uint32_t ph_bits = 0;  // phase of each A barrier
+        SeenFlag bdone{&rp.ctl->b_done, 0};
+#pragma unroll 1
+        for (uint64_t k = 0; k < rp.steps; ++k) {
+            if (!wait_seen(bdone, back(k, 2), rp))
+                break;
+            const uint64_t i = rp.i0 + k;
+            run_mark(rp, i, 2);
+            // m'_i's rows were last written by A(k-3): those stores are complete (every bulk
+            // group but the newest — A(k-1)'s last window — has finished)
+            asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+            const uint8_t* batch = rp.batches + ((rp.first + k) % rp.ring) * rp.batch_stride;
+            uint8_t* dst = b.region[b.me] + b.off_aug + (i % kAugRing) * b.aug_slot_bytes + uint64_t(row0) * S;
+            for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
+                const uint32_t w1 = min(nA, w0 + kTmaStagesA);
+                bulk_wait_read_all();  // the ring's previous window has been stored
+                for (uint32_t x = w0; x < w1; ++x) {
+                    const uint64_t off = alo + uint64_t(x) * CH;
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                    mbar_expect_tx(bars + (x - w0), len);
+                    bulk_load(ringA + (x - w0) * CH, batch + off, len, bars + (x - w0));
+                }
+                for (uint32_t x = w0; x < w1; ++x) {
+                    const uint64_t off = alo + uint64_t(x) * CH;
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                    if (!mbar_wait(bars + (x - w0), take_phase(ph_bits, x - w0), rp.base.timeout_ns))
+                        atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
+                    bulk_store(dst + off, ringA + (x - w0) * CH, len);
+                }
+                bulk_commit();
+            }
+            run_mark(rp, i, 5);
+        }
+        bulk_wait_all();
+        return;
+    }
+    // ---- warp 0: lists, counts, B engine on this CTA's column ----------------------------
+    // The lists of k+1 are staged (cp.async, second buffer) while B(k) moves bytes; every
+    // lane issues its own pieces' bulk copies (addresses resolved lane-parallel first).
+    volatile uint32_t* ready = misc + 6;
+    uint64_t* barB = bars + kTmaStagesA;
+    uint64_t* paddr = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm) + R.paddr);
+    uint32_t* xbuf[2] = {xraw, reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(sm) + R.lists2)};
+    uint32_t* wbuf[2] = {wraw, xbuf[1] + plist_words(b.N, b.r)};
+    uint32_t phB = 0;
+    const uint64_t c16 = S >> 4;
+    const uint64_t c0 = (c16 * part / parts) << 4, c1 = (c16 * (part + 1) / parts) << 4;
+    const uint32_t clen = static_cast<uint32_t>(c1 - c0);
+    const uint32_t per_win = clen ? R.arena_bytes / clen : 0;  // pieces per arena window
+    const uint32_t pw = plist_words(b.N, b.r), ww = wlist_words(b.nmax);
+    SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0};
+    uint32_t nprev = 0;
+    auto stage = [&](uint64_t kk) {  // cp.async of iteration kk's X / W lists into buffer kk & 1
+        const uint64_t i = rp.i0 + kk;
+        const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
+        const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
+        uint32_t* xd = xbuf[kk & 1];
+        uint32_t* wd = wbuf[kk & 1];
+        for (uint32_t x = lane; x < pw; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xd + x)), "l"(xs + x) : "memory");
+        for (uint32_t x = lane; x < ww; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wd + x)), "l"(ws + x) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (lane == 0)
+        sp = b;
+    bool staged = false;  // lists of the current k already issued
+#pragma unroll 1
+    for (uint64_t k = 0; k < rp.steps; ++k) {
+        bool ok = true;
+        if (lane == 0) {
+            run_patch(sp, rp, k);
+            ok = wait_seen(sdone, k + 1, rp) && wait_seen(pdone, k + 1, rp);
+        }
+        if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
+            break;
+        __syncwarp();  // sp (lane 0) visible to the warp
+        tl_mark(sp, 2, false);
+        if (lane == 0)
+            cta_mark(sp, 0);
+        if (!staged)
+            stage(k);
+        uint32_t* xr = xbuf[k & 1];
+        uint32_t* wr = wbuf[k & 1];
+        copy_parse(sp, xr, wr, jsrc, rowmap, misc, ready, true, true, false);
+        // next iteration's lists, if sel/plan already finished it (cached counters)
+        staged = false;
+        if (k + 1 < rp.steps) {
+            bool nx = false;
+            if (lane == 0)
+                nx = sdone.seen >= k + 2 && pdone.seen >= k + 2;
+            if (__shfl_sync(kFull, nx ? 1 : 0, 0)) {
+                stage(k + 1);
+                staged = true;
+            }
+        }
+        if (part == 0)
+            copy_counts(sp, xr);
+        const uint32_t nj = misc[0], nw = misc[1];
+        const uint32_t pieces = clen ? nj + nw : 0;
+        // piece addresses (lane-parallel); a slot pushed now that B(k-1) wrote is a hazard
+        bool hazard = false;
+        {
+            const uint8_t* batch = sp.batch;
+            uint8_t* slab = reinterpret_cast<uint8_t*>(sp.slab);
+            const uint32_t next_slot = (sp.aslot + 1) % kAugRing;
+            for (uint32_t x = lane; x < pieces; x += 32) {
+                const uint8_t* src;
+                uint8_t* dst;
+                if (x < nj) {
+                    const uint32_t s_ = jsrc[x];
+                    src = ((s_ >> 31) ? batch + uint64_t(s_ & 0x7fffffffu) * S : slab + uint64_t(s_) * S) + c0;
+                    dst = push_dst(sp, xr[4 + x], next_slot) + c0;
+                    if (!(s_ >> 31))
+                        for (uint32_t t = 0; t < nprev; ++t)
+                            hazard |= prevw[t] == s_;
+                } else {
+                    src = batch + uint64_t(wr[2 + 2 * (x - nj)]) * S + c0;
+                    dst = slab + uint64_t(wr[3 + 2 * (x - nj)]) * S + c0;
+                }
+                paddr[2 * x] = reinterpret_cast<uint64_t>(src);
+                paddr[2 * x + 1] = reinterpret_cast<uint64_t>(dst);
+            }
+        }
+        hazard = __any_sync(kFull, hazard);
+        __syncwarp();
+        bool drained = false;
+        auto drain = [&]() {  // B(k-1)'s stores (every lane's groups) complete, then arrive
+            bulk_wait_all();
+            __syncwarp();
+            if (lane == 0) {
+                cta_mark(sp, 7);
+                if (k > 0)
+                    run_b_arrive(rp, sp, k - 1, multi);
+                cta_mark(sp, 8);
+            }
+            drained = true;
+        };
+        if (hazard || pieces == 0)
+            drain();
+        for (uint32_t p0 = 0; p0 < pieces; p0 += per_win) {
+            const uint32_t p1 = min(pieces, p0 + per_win);
+            if (p0 > 0) {
+                bulk_wait_read_all();  // arena reuse
+                __syncwarp();
+            }
+            if (lane == 0)
+                mbar_expect_tx(barB, (p1 - p0) * clen);
+            for (uint32_t x = p0 + lane; x < p1; x += 32)
+                bulk_load(arena + (x - p0) * clen, reinterpret_cast<const void*>(paddr[2 * x]), clen, barB);
+            if (lane == 0)
+                cta_mark(sp, 3);
+            if (!drained)  // B(k-1)'s stores complete while these loads fly
+                drain();
+            if (!mbar_wait(barB, take_phase(phB, 0), rp.base.timeout_ns))
+                atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
+            if (lane == 0)
+                cta_mark(sp, 6);
+            for (uint32_t x = p0 + lane; x < p1; x += 32)
+                bulk_store(reinterpret_cast<void*>(paddr[2 * x + 1]), arena + (x - p0) * clen, clen);
+            bulk_commit();
+        }
+        if (lane == 0)
+            cta_mark(sp, 4);
+        // W_k's slab rows for the next iteration's hazard check
+        nprev = nw;
+        for (uint32_t t = lane; t < nw; t += 32)
+            prevw[t] = wr[3 + 2 * t];
+        bulk_wait_read_all();  // arena free before the next iteration's loads
+        if (lane == 0)
+            cta_mark(sp, 9);
+        __syncwarp();
+    }
+    if (rp.steps > 0 && !*reinterpret_cast<volatile uint32_t*>(&rp.ctl->error)) {
+        bulk_wait_all();
+        __syncwarp();
+        if (lane == 0)
+            run_b_arrive(rp, sp, rp.steps - 1, multi);
+    }
+}
+
+__global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_constant__ RunParams rp) {
+    extern __shared__ __align__(128) uint32_t sm[];
+    __shared__ StepParams sp;
+    __shared__ uint32_t flag[4];
+    if (blockIdx.x == 0)
+        run_sel_role(rp, sm, sp, flag);
+    else if (blockIdx.x == 1)
+        run_plan_role(rp, sm, sp, flag);
+    else
+        run_copy_role(rp, sm, sp);
 }
 
 // ---- standalone kernels for the buffer-level API (tests / facade) ----------------------
@@ -1591,28 +1809,49 @@ int set_smem(const void* kern, uint32_t bytes, uint32_t* cache) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)) != cudaSuccess)
             return -1;
+        // one carveout (all shared memory) for every iteration kernel, so the residency
+        // arithmetic of solo_smem_for() holds and no SM reconfigures between them
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+            return -1;
         *cache = bytes;
     }
     return 0;
 }
 }  // namespace
 
-int launch_sel(const StepParams& p, void* stream) {
+namespace {
+int launch_ex(const void* kern, uint32_t grid, uint32_t threads, uint32_t smem, void* stream, bool pdl,
+              const StepParams& p) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void* args[] = {const_cast<StepParams*>(&p)};
+    return cudaLaunchKernelExC(&cfg, kern, args) == cudaSuccess ? 0 : -1;
+}
+}  // namespace
+
+int launch_sel(const StepParams& p, void* stream, bool pdl) {
     static uint32_t cache[kMaxDevices] = {};
     const uint32_t smem = max(sel_smem_bytes(p.K, p.nmax), p.solo_smem);
     if (set_smem(reinterpret_cast<const void*>(drb_sel_kernel), smem, cache))
         return -1;
-    drb_sel_kernel<<<1, kSelThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    return launch_ex(reinterpret_cast<const void*>(drb_sel_kernel), 1, kSelThreads, smem, stream, pdl, p);
 }
 
-int launch_plan_next(const StepParams& p, void* stream) {
+int launch_plan_next(const StepParams& p, void* stream, bool pdl) {
     static uint32_t cache[kMaxDevices] = {};
     const uint32_t smem = max(plan_smem_bytes(p.N, p.K, p.r), p.solo_smem);
     if (set_smem(reinterpret_cast<const void*>(drb_plan_next_kernel), smem, cache))
         return -1;
-    drb_plan_next_kernel<<<1, plan_threads(p.N), smem, static_cast<cudaStream_t>(stream)>>>(p);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    return launch_ex(reinterpret_cast<const void*>(drb_plan_next_kernel), 1, plan_threads(p.N), smem, stream, pdl,
+                     p);
 }
 
 int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl) {
@@ -1620,7 +1859,8 @@ int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl) {
     const bool tma = p.vec16 && !(p.dbg & 16);  // DRB_DBG bit 4: LSU kernel instead of TMA
     const int which = tma ? 2 : (p.vec16 ? 1 : 0);
     auto kern = tma ? drb_copy_tma_kernel : (p.vec16 ? drb_copy_kernel<uint4> : drb_copy_kernel<uint32_t>);
-    const uint32_t smem = tma ? max(p.smem_bytes, tma_smem(p.N, p.r, p.nmax).bytes) : p.smem_bytes;
+    // the TMA kernel is sized for two co-resident CTAs (copy(i) + copy(i+1) under PDL)
+    const uint32_t smem = tma ? tma_smem(p.N, p.r, p.nmax).bytes : p.smem_bytes;
     if (set_smem(reinterpret_cast<const void*>(kern), smem, cache[which]))
         return -1;
     cudaLaunchConfig_t cfg{};
@@ -1634,6 +1874,42 @@ int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, p) == cudaSuccess ? 0 : -1;
+}
+
+uint32_t run_smem_bytes(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax) {
+    return run_smem(N, K, r, nmax).bytes;
+}
+
+int launch_run(const RunParams& rp, uint32_t grid, void* stream) {
+    static uint32_t cache[kMaxDevices] = {};
+    // one CTA per SM (each copy CTA owns an SM's share of HBM bandwidth)
+    const uint32_t smem = run_smem_bytes(rp.base.N, rp.base.K, rp.base.r, rp.base.nmax);
+    if (smem > 227u * 1024u)
+        return -1;
+    if (set_smem(reinterpret_cast<const void*>(drb_run_kernel), smem, cache))
+        return -1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kRunThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the roles spin on each other
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, drb_run_kernel, rp) == cudaSuccess ? 0 : -1;
+}
+
+int copy_tma_occupancy(uint32_t smem_bytes, int* out) {
+    if (cudaFuncSetAttribute(drb_copy_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_bytes)) != cudaSuccess ||
+        cudaFuncSetAttribute(drb_copy_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+        return -1;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, drb_copy_tma_kernel, kTmaThreads, smem_bytes) ==
+                   cudaSuccess
+               ? 0
+               : -1;
 }
 
 int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {

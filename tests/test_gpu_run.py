@@ -1,0 +1,108 @@
+"""Multi-iteration runs over a device-resident input ring (drb_rb_run, the bench path).
+
+The persistent cooperative launch (default) and the three-kernel path (DRB_PERSIST=0) must
+leave the engine exactly where the synchronous-replay oracle is after the same batches:
+slab bytes, stored labels, occupancy and version, and every later update() step's m'
+(whose representative rows the run's last iteration pushed) bit-exact. Runs are also
+captured into CUDA graphs (prepare_run) and interleaved with single steps.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.py_oracle import Backend
+from paper_2406_03285_b200.workload import stream_spec
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["persistent", "three-kernel"])
+def drb(request, monkeypatch):
+    import paper_2406_03285_b200 as drb
+    monkeypatch.setenv("DRB_PERSIST", "1" if request.param == "persistent" else "0")
+    return drb
+
+
+def dev(data, labels):
+    return (torch.from_numpy(np.ascontiguousarray(data)).cuda(),
+            torch.from_numpy(np.ascontiguousarray(labels).astype(np.int32)).cuda())
+
+
+def check_step(eng, rep, data, lab, where):
+    o, ol, oc = rep.step(data[None], lab[None])
+    aug = eng.update(dev(data, lab))
+    d, l = aug.tensors()
+    cnt = aug.count()
+    assert cnt == int(oc[0]), where
+    assert np.array_equal(l.cpu().numpy().astype(np.uint32), ol[0, :cnt]), where
+    assert np.array_equal(d.cpu().numpy(), o[0, :cnt]), where
+
+
+def check_state(buf, rep, K, cap, where):
+    occ, ver, slab, sl = rep.dump(0)
+    snap = buf.snapshot()
+    assert np.array_equal(np.asarray(snap.per_class, np.uint32), occ), where
+    assert snap.version == ver, where
+    d, l = buf.slab()
+    d = d.cpu().numpy().reshape(K, cap, -1)
+    l = l.cpu().numpy().reshape(K, cap).astype(np.uint32)
+    for k in range(K):  # only occupied slots are defined
+        assert np.array_equal(d[k, :occ[k]], slab[k, :occ[k]]), (where, k)
+        assert np.array_equal(l[k, :occ[k]], sl[k, :occ[k]]), (where, k)
+
+
+def ring_parity(drb, K, cap, S, b, c, r, seed, pre, runs, post, ring, T=2, spt=7, graph=False):
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed)
+    eng = drb.engine(buf)
+    eng.start()
+    rep = Backend("port").replay(1, K, cap, S, c, r, seed)
+    spec = stream_spec(K, T, b, S, steps_per_task=spt, seed=seed)
+    i = 0
+    for _ in range(pre):
+        check_step(eng, rep, spec.payload(0, i), spec.labels(0, i), ("pre", i))
+        i += 1
+    for run_no, (steps, first) in enumerate(runs):
+        rd = np.stack([spec.payload(0, 1000 * (run_no + 1) + x) for x in range(ring)])
+        rl = np.stack([spec.labels(0, 1000 * (run_no + 1) + x) for x in range(ring)])
+        data_ring, lab_ring = dev(rd, rl)
+        if graph:
+            g = eng.prepare_run(data_ring, lab_ring, steps, first=first)
+            g.launch()
+        else:
+            eng.run(data_ring, lab_ring, steps, first=first)
+        for k in range(steps):
+            rep.step(rd[(first + k) % ring][None], rl[(first + k) % ring][None])
+        torch.cuda.synchronize()
+        if graph:
+            g.close()
+        check_state(buf, rep, K, cap, ("run", run_no))
+        for _ in range(post):
+            check_step(eng, rep, spec.payload(0, i), spec.labels(0, i), ("post", run_no, i))
+            i += 1
+    assert eng.device_error() == 0
+    eng.shutdown()
+
+
+def test_run_small(drb):
+    ring_parity(drb, K=10, cap=6, S=64, b=24, c=14, r=7, seed=3, pre=3, runs=[(20, 0), (9, 5)], post=4, ring=5)
+
+
+def test_run_from_start_and_replacement_heavy(drb):
+    # run as the very first iterations (reps(-1) empty), tiny capacity -> replacements and
+    # reps pushed from slots written in the same round (winner batch rows)
+    ring_parity(drb, K=4, cap=2, S=32, b=16, c=12, r=5, seed=9, pre=0, runs=[(30, 2)], post=5, ring=3, T=1)
+
+
+def test_run_exhaustion_r_ge_total(drb):
+    ring_parity(drb, K=3, cap=2, S=48, b=8, c=3, r=40, seed=4, pre=1, runs=[(12, 0)], post=3, ring=4, T=1)
+
+
+def test_run_c2_sample_shape(drb):
+    # 224x224x3 u8 samples, b=56, r=7, c=14 (c2), fewer classes to keep the slab dump small
+    ring_parity(drb, K=12, cap=8, S=150528, b=56, c=14, r=7, seed=1, pre=2, runs=[(40, 0)], post=3, ring=6,
+                T=3, spt=10)
+
+
+def test_run_graph_captured(drb):
+    ring_parity(drb, K=10, cap=6, S=64, b=24, c=14, r=7, seed=8, pre=2, runs=[(25, 1), (7, 0)], post=3, ring=6,
+                graph=True)

@@ -1,12 +1,14 @@
 """CPU, world_size 2 (gloo): the host-side multi-rank logic.
 
 1. exchange_blobs: the handle all-gather used to wire ranks (dist.py).
-2. A CPU model of the distributed protocol the kernels implement (DESIGN.md §4): every
+2. A CPU model of the distributed protocol the kernels implement (DESIGN.md §3-4): every
    rank keeps only its own buffer, exchanges occupancy rows, replicates every requester's
-   global-sampling stream to plan for all of them, derives its PULL list (own plan) and its
-   REMOTE-READ set (rows of its slab others read, with reader masks), exchanges exactly
-   those rows (standing in for the NVLink pulls), reads before writing (exact horizon) —
-   and must reproduce the N-rank synchronous replay oracle bit for bit.
+   global-sampling stream to plan for all of them, derives its PUSH list (every entry of
+   any requester's plan(i) whose slot it owns), resolves each slot's version-(i+1) bytes
+   the way copy(i) does — the winning candidate's batch row if round i wrote the slot
+   (W_i), else the slab row untouched by round i — and sends exactly those rows to their
+   requesters (standing in for the NVLink stores) — and must reproduce the N-rank
+   synchronous replay oracle bit for bit.
 """
 import os
 import socket
@@ -92,45 +94,57 @@ def _worker(rank, world, port, q):
         spec = stream_spec(K, 2, b, S, steps_per_task=12, seed=seed)
         buf = OracleBuffer(K, cap, S)
         cand, evict = buf.stream(seed, rank, CANDIDATE), buf.stream(seed, rank, EVICTION)
+        # shadow buffer, same decisions (same labels and streams), payload = (round, batch row)
+        # tags: the slots it shows written in round i are W_i (last writer per slot)
+        tag = OracleBuffer(K, cap, 8)
+        tcand, tevict = type(cand).from_buffer_copy(cand), type(evict).from_buffer_copy(evict)
         samp = [stream(seed, w, 3) for w in range(world)]  # every requester, replicated
         replay = Backend("port").replay(world, K, cap, S, c, r, seed)
-        pull_list, remote_rows = [], {}
+        reps, rep_labels = [], []  # reps(i-1): the rows of m'_i pushed during round i-1
         bad = 0
         for i in range(steps):
             data = np.stack([spec.payload(w, i) for w in range(world)])
             labs = np.stack([spec.labels(w, i) for w in range(world)])
             o, ol, oc = replay.step(data, labs)
-            # (a) pulls of plan(i-1) at version i: owners publish exactly their remote-read rows
-            mine_rows = {row: buf.slab[row // cap, row % cap].copy() for row in remote_rows}
-            gathered = [None] * world
-            dist.all_gather_object(gathered, mine_rows)
-            reps, rep_labels = [], []
-            for owner, row in pull_list:
-                src = buf.slab[row // cap, row % cap] if owner == rank else gathered[owner][row]
-                reps.append(src.copy())
-                rep_labels.append(row // cap)
-            # (b) round-i update of the own buffer only
-            rc, _, _ = buf.update_buffer(data[rank], labs[rank], c, cand, evict)
-            assert rc == 0
-            # (c) occupancy rows v = i+1 (the size rendezvous)
-            rows = [None] * world
-            dist.all_gather_object(rows, buf.occ.copy())
-            view = np.stack(rows).astype(np.uint32)
-            # (d) plan(i) for every requester -> own pull list + remote-read set
-            plans = [plan(r, view, samp[w]) for w in range(world)]
-            pull_list = [(ow, cl * cap + sl) for (ow, cl, sl) in plans[rank]]
-            remote_rows = {}
-            for w in range(world):
-                if w != rank:
-                    for (ow, cl, sl) in plans[w]:
-                        if ow == rank:
-                            remote_rows[cl * cap + sl] = remote_rows.get(cl * cap + sl, 0) | (1 << w)
             # m'_i = m_i ++ reps(i-1)
             got = np.concatenate([data[rank]] + ([np.stack(reps)] if reps else []))
             got_l = np.concatenate([labs[rank], np.array(rep_labels, np.uint32)])
             n = int(oc[rank])
             if not (len(got) == n and np.array_equal(got, o[rank, :n]) and np.array_equal(got_l, ol[rank, :n])):
                 bad += 1
+            # (a) round-i update of the own buffer only (copy(i) reads the slab as it was)
+            before = buf.slab.copy()
+            rc, _, _ = buf.update_buffer(data[rank], labs[rank], c, cand, evict)
+            assert rc == 0
+            tags = np.zeros((len(labs[rank]), 8), np.uint8)
+            tags[:, :4] = np.arange(len(labs[rank]), dtype=np.uint32).view(np.uint8).reshape(-1, 4)
+            tags[:, 4:] = np.full(len(labs[rank]), i + 1, np.uint32).view(np.uint8).reshape(-1, 4)
+            rc, _, _ = tag.update_buffer(tags, labs[rank], c, tcand, tevict)
+            assert rc == 0
+            tv = tag.slab.view(np.uint32).reshape(K, cap, 2)
+            # (b) occupancy rows v = i+1 (the size rendezvous)
+            rows = [None] * world
+            dist.all_gather_object(rows, buf.occ.copy())
+            view = np.stack(rows).astype(np.uint32)
+            # (c) plan(i) for every requester; push every owned entry at version i+1
+            plans = [plan(r, view, samp[w]) for w in range(world)]
+            out = {}
+            for w in range(world):
+                for j, (ow, cl, sl) in enumerate(plans[w]):
+                    if ow != rank:
+                        continue
+                    won = tv[cl, sl, 1] == i + 1
+                    src = data[rank][tv[cl, sl, 0]] if won else before[cl, sl]
+                    out.setdefault(w, []).append((j, src.copy()))
+            gathered = [None] * world
+            dist.all_gather_object(gathered, out)
+            mine = {}
+            for g in gathered:
+                for j, row in g.get(rank, []):
+                    mine[j] = row
+            assert sorted(mine) == list(range(len(plans[rank])))
+            reps = [mine[j] for j in range(len(plans[rank]))]
+            rep_labels = [cl for (_, cl, _) in plans[rank]]
         t = torch.tensor([bad])
         dist.all_reduce(t)
         q.put((rank, int(t.item())))
@@ -139,7 +153,7 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.parametrize("world", [2])
-def test_pull_protocol_model_matches_replay(world):
+def test_push_protocol_model_matches_replay(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()

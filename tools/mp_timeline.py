@@ -43,9 +43,10 @@ g.launch()
 torch.cuda.synchronize()
 n = C.c_uint32(0)
 check(lib.drb_rb_timeline_read(buf.h, None, C.byref(n)))
-t = np.zeros(n.value * 6, np.uint64)
+W = 32 + 16 * 160  # kTlStride words per step (drb_internal.cuh)
+t = np.zeros(n.value * W, np.uint64)
 check(lib.drb_rb_timeline_read(buf.h, t.ctypes.data, C.byref(n)))
-t = t.reshape(n.value, 3, 2).astype(np.int64)
+t = t.reshape(n.value, W)[:, :6].reshape(n.value, 3, 2).astype(np.int64)
 rows = [(first + i) % n.value for i in range(STEPS)]
 mine = np.stack([t[row] for row in rows])  # [STEPS, 3, 2]
 allt = [None] * world

@@ -31,12 +31,12 @@ g.launch()
 torch.cuda.synchronize()
 n = C.c_uint32(0)
 check(lib.drb_rb_timeline_read(buf.h, None, C.byref(n)))
-W = 32 + 8 * 160
+W = 32 + 16 * 160
 t = np.zeros(n.value * W, np.uint64)
 check(lib.drb_rb_timeline_read(buf.h, t.ctypes.data, C.byref(n)))
 t = t.reshape(n.value, W).astype(np.int64)
 ph = t[:, 8:32]
-cta = t[:, 32:].reshape(n.value, 160, 8)
+cta = t[:, 32:].reshape(n.value, 160, 16)
 t = t[:, :6].reshape(n.value, 3, 2)
 rows = [(first + i) % n.value for i in range(STEPS)]
 t0 = t[rows[0], 2, 0]
@@ -70,7 +70,8 @@ for name, slots in PH.items():
     print(f"{name} phases (us after start): " + ", ".join(parts))
 
 # per-CTA copy stamps relative to the copy's first CTA start, medians over steps
-CN = ["start", "lists", "A issued", "ready(w1)", "B issued", "A stored", "B stored", "end"]
+CN = ["start", "lists", "A issued", "A wait+ready", "B issued", "A m' stored", "A done", "end", "prologue", "B done",
+      "B wait", "A 1st land"]
 grid = int(((cta[rows[0], :, 0]) > 0).sum())
 rel = []
 for row in rows[8:]:
