@@ -166,7 +166,7 @@ struct drb_rb {
     uint64_t ver0 = 0;                // engine: table version / state parities at start()
     uint32_t sel_par0 = 0, plan_par0 = 0;
     uint32_t dbg_bits = 0;            // DRB_DBG experiment bits (0 in production)
-    bool use_persist = true;
+    bool use_persist = false;         // drb_rb_run as one persistent cooperative launch (DRB_PERSIST=1)
     bool last_run_persistent = false; // the latest drb_rb_run was one persistent launch          // drb_rb_run as one persistent cooperative launch; DRB_PERSIST=0 off
     RunCtl* runctl = nullptr;         // device counters of the persistent run
     cudaEvent_t run_end = nullptr;
@@ -418,8 +418,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             h->dbg_bits = uint32_t(std::strtoul(db, nullptr, 0));
         if (const char* pd = std::getenv("DRB_PDL"); pd && pd[0] == '0')
             h->use_pdl = false;
-        if (const char* pe = std::getenv("DRB_PERSIST"); pe && pe[0] == '0')
-            h->use_persist = false;
+        if (const char* pe = std::getenv("DRB_PERSIST"))
+            h->use_persist = pe[0] == '1';
         cuda_check(cudaMalloc(&h->runctl, sizeof(RunCtl)), "run state alloc");
         cuda_check(cudaEventCreateWithFlags(&h->run_end, cudaEventDisableTiming), "event");
         if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
