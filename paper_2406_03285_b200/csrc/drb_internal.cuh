@@ -66,10 +66,9 @@ struct alignas(256) RegionHeader {
     uint64_t occ_flag[kMaxWorld];  // [w]: latest occupancy version rank w published here
     uint64_t pushdone[kMaxWorld];  // [w]: 1 + last iteration whose pushes rank w completed
                                    //      (its reps rows of my m'_{i+1} have landed)
-    uint64_t ticket;               // local: CTA completion tickets (last-CTA detection)
     uint32_t aug_count[4];         // local: rows of m' per ring slot (device copy)
     uint32_t repcnt[4];            // local: |reps| already written into m' ring slot s
-    uint64_t pad[4];
+    uint64_t pad[5];
 };
 
 struct RegionLayout {

@@ -490,8 +490,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
                 for (uint32_t x = lane; x < K; x += 32)
                     pt[x] = occ[x];
             }
-            __threadfence_system();
-            __syncwarp();
+            __syncwarp();  // the warp's row stores precede each lane's release below
             if (lane < N && lane != me) {
                 RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
                 st_release_sys(&peer->occ_flag[me], p.step + 1);
@@ -818,28 +817,30 @@ __device__ void copy_counts(const StepParams& p, const uint32_t* xraw) {
     }
 }
 
-// Multi-rank completion of copy(i), after every CTA's pushes are complete and fenced:
-// the last CTA announces pushdone[me] = i+1 to every peer; CTA 0 holds the kernel until
-// every peer's reps(i-1) rows of m'_i have landed (pushdone >= i).
-__device__ void copy_finish_peers(const StepParams& p) {
-    const uint32_t tid = threadIdx.x, N = p.N, me = p.me;
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
-    if (tid == 0) {
-        const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->ticket), 1ull);
-        if ((t + 1) % gridDim.x == 0) {
-            __threadfence_system();
-            for (uint32_t w = 0; w < N; ++w)
-                if (w != me)
-                    st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[w])->pushdone[me], p.step + 1);
-        }
-    }
-    if (blockIdx.x == 0 && tid < 32 && p.step > 0) {
-        bool ok = true;
-        if (tid < N && tid != me)
-            ok = wait_flag(&hdr->pushdone[tid], p.step, p.timeout_ns);
-        if (__any_sync(kFull, !ok) && tid == 0)
-            mailbox_fail(p, DRB_ERR_TRANSPORT);
-    }
+// Multi-rank hand-off of the pushes, in copy(i) (CTA 0, warp 0):
+//   start (after griddepcontrol.wait: copy(i-1) complete, so are its stores into the peers'
+//     m'_i — kernel completion): pushdone[me] = i at every peer, after a system fence;
+//   end: wait until every peer announced pushdone >= i (their reps(i-1) rows of my m'_i
+//     landed) — m'_i is complete when copy(i) is.
+__device__ void copy_announce_peers(const StepParams& p) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (p.step == 0)
+        return;
+    __threadfence_system();
+    __syncwarp();
+    if (lane < p.N && lane != p.me)
+        st_release_sys(&reinterpret_cast<RegionHeader*>(p.region[lane])->pushdone[p.me], p.step);
+}
+__device__ void copy_wait_peers(const StepParams& p) {
+    const uint32_t lane = threadIdx.x & 31;
+    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[p.me]);
+    if (p.step == 0)
+        return;
+    bool ok = true;
+    if (lane < p.N && lane != p.me)
+        ok = wait_flag(&hdr->pushdone[lane], p.step, p.timeout_ns);
+    if (__any_sync(kFull, !ok) && lane == 0)
+        mailbox_fail(p, DRB_ERR_TRANSPORT);
 }
 
 __device__ __forceinline__ uint8_t* push_dst(const StepParams& p, uint32_t dst, uint32_t next_slot) {
@@ -900,9 +901,12 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     const bool fuse = do_assemble;
     if (warp == 0) {
         copy_parse(p, xraw, wraw, jsrc, rowmap, misc, ready, do_push, do_update, fuse);
-        if (blockIdx.x == 0 && do_assemble) {
+        if (blockIdx.x == 0) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            copy_counts(p, xraw);
+            if (multi)
+                copy_announce_peers(p);
+            if (do_assemble)
+                copy_counts(p, xraw);
         }
     }
     __syncthreads();
@@ -953,11 +957,8 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     }
     if (tid == 32)
         cta_mark(p, 6);
-    if (multi) {
-        __threadfence_system();  // this thread's pushes, before the CTA's ticket
-        __syncthreads();
-        copy_finish_peers(p);
-    }
+    if (multi && blockIdx.x == 0 && warp == 0)
+        copy_wait_peers(p);
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
@@ -1157,6 +1158,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
         asm volatile("griddepcontrol.wait;" ::: "memory");  // copy(i-1) complete: slab at version i
         if (lane == 0)
             cta_mark(p, 10);
+        if (multi && blockIdx.x == 0)
+            copy_announce_peers(p);
         if (blockIdx.x == 0 && do_assemble)
             copy_counts(p, xraw);
         if (lane == 0) {
@@ -1214,17 +1217,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
                 ++use;
             }
             cta_mark(p, 9);
-            if (multi) {  // the pushes are complete before the CTA's ticket
-                bulk_wait_all();
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                __threadfence_system();
-            }
         }
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();  // all bulk stores of this CTA issued and sourced
-    if (multi)
-        copy_finish_peers(p);
+    if (multi && blockIdx.x == 0 && warp == 0)
+        copy_wait_peers(p);
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
