@@ -294,26 +294,29 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         kernel_ms = float(tt.item())
 
-    # e2e through the host-buffer C-ABI call (pinned host m_i in, pinned host m'_i out)
+    # e2e through the host-buffer C-ABI call drb_rb_step_host: pinned host m_i in, m'_i
+    # assembled in place in the caller's buffer (rows [0, b) are m_i, the r representative
+    # rows and their labels come back over PCIe) — reps = update(m); m' = augment(m, reps)
     e2e_steps = args.e2e_steps
     hring = 4
-    h_data = torch.empty((hring, b, S), dtype=torch.uint8).pin_memory()
-    h_data.copy_(data[:hring].cpu())
-    h_lab = torch.empty((hring, b), dtype=torch.int32).pin_memory()
-    h_lab.copy_(lab[:hring].cpu())
-    h_out = torch.empty((2, b + r, S), dtype=torch.uint8).pin_memory()
-    h_out_l = torch.empty((2, b + r), dtype=torch.int32).pin_memory()
-    h_cnt = torch.zeros(2, dtype=torch.int32).pin_memory()
-    hd, hl, ho, hol, hc = (x.numpy() for x in (h_data, h_lab, h_out, h_out_l, h_cnt))
+    h_slot = torch.empty((hring, b + r, S), dtype=torch.uint8).pin_memory()
+    h_slot[:, :b].copy_(data[:hring].cpu())
+    h_lab = torch.empty((hring, b + r), dtype=torch.int32).pin_memory()
+    h_lab[:, :b].copy_(lab[:hring].cpu())
+    h_cnt = torch.zeros(hring, dtype=torch.int32).pin_memory()
+    hs, hl, hc = (x.numpy() for x in (h_slot, h_lab, h_cnt))
+
+    def host_step(i):
+        k = i % hring
+        eng.update_host(hs[k][:b], hl[k][:b].view(np.uint32), hs[k], hl[k].view(np.uint32),
+                        hc[k:k + 1].view(np.uint32))
     for i in range(8):  # warm
-        eng.update_host(hd[i % hring], hl[i % hring].view(np.uint32), ho[i % 2], hol[i % 2].view(np.uint32),
-                        hc[i % 2:i % 2 + 1].view(np.uint32))
+        host_step(i)
     eng.synchronize()
     barrier()
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        eng.update_host(hd[i % hring], hl[i % hring].view(np.uint32), ho[i % 2], hol[i % 2].view(np.uint32),
-                        hc[i % 2:i % 2 + 1].view(np.uint32))
+        host_step(i)
     eng.synchronize()
     e2e_s = time.perf_counter() - t0
     if N > 1:
@@ -323,6 +326,11 @@ def main():
     e2e_value = (b + r) * N * e2e_steps / e2e_s
     eng.shutdown()
 
+    persistent = os.environ.get("DRB_PERSIST", "0") == "1" and not args.no_graph
+    # our kernels inside the timed region: sel + plan + copy per step (three-kernel path,
+    # captured in one CUDA graph), or one cooperative launch for the whole run (DRB_PERSIST=1)
+    launches = 1 if persistent else 3 * args.steps
+    launch_mode = "persistent-cooperative" if persistent else ("cuda-graph" if not args.no_graph else "direct")
     peak, peak_kind = peaks()
     bytes_step = hbm_bytes_per_step(cfg)
     # The copy kernel is the only bulk kernel and runs back to back, one launch per step, so
@@ -356,14 +364,15 @@ def main():
                        "parallelism": f"dp{N}" if N > 1 else "single",
                        "l2": f"inputs larger than L2: {ring}-batch device ring ({ring * b * S / 2**20:.0f} MiB), "
                              f"slab {K * cap * S / 2**20:.0f} MiB per GPU"},
-            "gpu_launches": args.steps,
-            "launch_mode": "cuda-graph" if not args.no_graph else "direct",
+            "gpu_launches": launches,
+            "launch_mode": launch_mode,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": b * (S + 4),
-                    "d2h_bytes_per_step": (b + r) * (S + 4) + 4, "steps": e2e_steps},
+                    "d2h_bytes_per_step": r * (S + 4) + 4, "steps": e2e_steps,
+                    "api": "drb_rb_step_host, m' assembled in place in the caller's pinned batch buffer"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": bytes_step, "kernel_ms": ms_per_step,
-                         "kernel": "drb_copy_kernel", "timing": "CUDA events over the timed region / K launches",
+                         "kernel": "drb_copy_tma_kernel", "timing": "CUDA events over the timed region / K steps",
                          "kernel_ms_event_bracketed": kernel_ms,
                          "bytes_formula": "2*S*(b+r+c) per rank per iteration (SURVEY.md 8d)"},
             "cpu_baseline": cpu,

@@ -197,7 +197,10 @@ DRB_RB_API drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* 
                                   uint32_t n, void* stream, drb_aug* out);
 /* Same, with HOST (ideally pinned) buffers: copies m_i in, runs the step, copies m'_i out
  * into out/out_labels (capacity n + r rows). Asynchronous on the handle's streams;
- * call drb_rb_synchronize before reading out or *out_count. */
+ * call drb_rb_synchronize before reading out or *out_count.
+ * In place (out == batch and out_labels == labels, capacity n + r rows): m_i's rows are
+ * already where m'_i keeps them, so only reps(i-1) (rows [n, n+|reps|)) and their labels
+ * come back — `augment(m, reps)` (sampler.cpp:234-240) without the host-side copy of m. */
 DRB_RB_API drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels,
                                        uint32_t n, void* out, uint32_t* out_labels,
                                        uint32_t* out_count);

@@ -752,7 +752,7 @@ void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* label
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
     if (i >= h->dep_floor + 4)
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_plan[ev_of(i - 4)], 0), "wait");
-    if (launch_sel(p, h->s_sel, h->use_pdl && (h->dbg_bits & 256)))  // DRB_DBG bit 8: PDL sel chain
+    if (launch_sel(p, h->s_sel, h->use_pdl && (h->dbg_bits & 768)))  // DRB_DBG bits 8/9: PDL sel chain
         fail(DRB_ERR_INTERNAL, std::string("sel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     cuda_check(cudaEventRecord(h->ev_sel[ev_of(i)], h->s_sel), "event");
     h->ver = h->ver0 + i + 1;
@@ -765,7 +765,7 @@ void enqueue_plan(drb_rb* h, uint64_t i) {
     cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_sel[ev_of(i)], 0), "wait");
     if (i >= h->dep_floor + kListRing)
         cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
-    if (launch_plan_next(p, h->s_plan, h->use_pdl && (h->dbg_bits & 256)))
+    if (launch_plan_next(p, h->s_plan, h->use_pdl && (h->dbg_bits & 768)))
         fail(DRB_ERR_INTERNAL, std::string("plan launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     cuda_check(cudaEventRecord(h->ev_plan[ev_of(i)], h->s_plan), "event");
     h->cur_plan = uint32_t((h->plan_par0 + i + 1) & 1);
@@ -1060,9 +1060,16 @@ drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels
             fail(st, t_last_error);
         cuda_check(cudaEventRecord(h->in_free[si], h->stream), "event");
         cuda_check(cudaStreamWaitEvent(h->d2h, h->done[aug.ring_slot], 0), "wait");
-        const uint64_t rows = uint64_t(n) + c.rep_count;
-        cuda_check(cudaMemcpyAsync(out, aug.data, rows * c.sample_bytes, cudaMemcpyDeviceToHost, h->d2h), "d2h");
-        cuda_check(cudaMemcpyAsync(out_labels, aug.labels, rows * 4, cudaMemcpyDeviceToHost, h->d2h), "d2h");
+        // in place: the caller's batch rows already are m'_i's first n rows; only the
+        // representatives (at most r rows, fixed offset n) travel back
+        const bool in_place = out == batch && out_labels == labels;
+        const uint64_t skip = in_place ? n : 0;
+        const uint64_t rows = uint64_t(n) + c.rep_count - skip;
+        cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(out) + skip * c.sample_bytes,
+                                   static_cast<const uint8_t*>(aug.data) + skip * c.sample_bytes,
+                                   rows * c.sample_bytes, cudaMemcpyDeviceToHost, h->d2h), "d2h");
+        cuda_check(cudaMemcpyAsync(out_labels + skip, aug.labels + skip, rows * 4, cudaMemcpyDeviceToHost, h->d2h),
+                   "d2h");
         const auto* hdr = reinterpret_cast<const RegionHeader*>(h->region);
         cuda_check(cudaMemcpyAsync(out_count, &hdr->aug_count[aug.ring_slot], 4, cudaMemcpyDeviceToHost, h->d2h), "d2h");
         // The next step may reuse this m' slot only after the copy-out drained.

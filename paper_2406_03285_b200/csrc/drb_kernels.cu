@@ -48,6 +48,32 @@ __device__ uint64_t bounded_seq(uint64_t key, uint64_t& ctr, uint64_t n) {
     }
 }
 
+// Exact v mod d for a 32-bit d, without the generic 64-bit division routine: with
+// m = floor((2^64-1)/d) (one division, shared by every lane that reduces by the same d),
+// q = umulhi(v, m) undershoots floor(v/d) by at most 2. The rejection threshold of
+// bounded(d) is (2^64 - d) mod d = reduce(0 - d) (rng.cpp:45-53).
+struct reducer {
+    uint64_t d, m;
+    __device__ explicit reducer(uint64_t d_) : d(d_), m(~0ull / d_) {}
+    __device__ __forceinline__ uint64_t mod(uint64_t v) const {
+        uint64_t r = v - __umul64hi(v, m) * d;
+        r = r >= d ? r - d : r;
+        return r >= d ? r - d : r;
+    }
+    __device__ __forceinline__ uint64_t thr() const { return mod(0ull - d); }
+};
+// v mod d for d < 2^16 from three 32-bit remainders: v = hi*2^32 + lo and
+// (hi mod d)*(2^32 mod d) < 2^32.
+__device__ __forceinline__ uint32_t mod_small(uint64_t v, uint32_t d) {
+    const uint32_t c = (0u - d) % d;  // 2^32 mod d
+    const uint32_t hi = static_cast<uint32_t>(v >> 32) % d, lo = static_cast<uint32_t>(v) % d;
+    return ((hi * c) % d + lo) % d;
+}
+__device__ __forceinline__ uint32_t thr_small(uint32_t d) {  // 2^64 mod d = (2^32 mod d)^2 mod d
+    const uint32_t c = (0u - d) % d;
+    return (c * c) % d;
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -85,16 +111,15 @@ __device__ void warp_select(uint64_t key, uint64_t& ctr, uint32_t n, uint32_t k,
     const int lane = threadIdx.x & 31;
     if (k == 0)
         return;
-    if (k <= 32) {
+    if (k <= 32 && n < 65536u) {  // (mod_small needs n < 2^16; max_batch <= 4096)
         const uint32_t j = lane;
         uint32_t s = 0xffffffffu;
         bool ok = true;
-        if (j < k) {
-            const uint64_t nj = n - j;
-            const uint64_t thr = (0ull - nj) % nj;
+        if (j < k) {  // n <= 4096 (max_batch): 32-bit remainders
+            const uint32_t nj = n - j;
             const uint64_t v = draw_at(key, ctr + 1 + j);
-            ok = v >= thr;
-            s = j + static_cast<uint32_t>(v % nj);
+            ok = v >= thr_small(nj);
+            s = j + mod_small(v, nj);
         }
         if (__ballot_sync(kFull, !ok) == 0) {
             // q: latest earlier lane drawing the same target (one match instruction)
@@ -150,7 +175,8 @@ __device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint32_
                             uint32_t* cand_l, uint32_t* cand_slot, uint32_t* scratch,
                             uint32_t* kind, uint32_t& appends) {
     const int lane = threadIdx.x & 31;
-    const uint64_t thr = (0ull - static_cast<uint64_t>(cap)) % cap;
+    const reducer red(cap);
+    const uint64_t thr = red.thr();
     const unsigned lt = (1u << lane) - 1u;
     appends = 0;
     for (uint32_t base = 0; base < k; base += 32) {
@@ -173,7 +199,7 @@ __device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint32_
             const uint64_t v = draw_at(ekey, ectr + 1 + lane);
             const unsigned vmask = __ballot_sync(kFull, v >= thr);
             if (static_cast<uint32_t>(__popc(vmask)) >= R) {
-                const uint32_t val = static_cast<uint32_t>(v % cap);
+                const uint32_t val = static_cast<uint32_t>(red.mod(v));
                 const int pos = rep ? static_cast<int>(__fns(vmask, 0, e + 1)) : 0;
                 const uint32_t got = __shfl_sync(kFull, val, pos);
                 if (rep)
@@ -222,12 +248,13 @@ __device__ uint32_t warp_plan_draw(uint64_t key, uint64_t& ctr, uint32_t want, u
         __syncwarp();
         return total;
     }
-    const uint64_t thr = (0ull - static_cast<uint64_t>(total)) % total;
+    const reducer red(total);
+    const uint64_t thr = red.thr();
     uint32_t got = 0;
     while (got < want) {
         const uint64_t v = draw_at(key, ctr + 1 + lane);
         const bool ok = v >= thr;
-        const uint32_t f = static_cast<uint32_t>(v % total);
+        const uint32_t f = static_cast<uint32_t>(red.mod(v));
         // duplicate of an earlier valid lane in this batch? (rejected lanes get a unique
         // key above any flat index, total < 2^31)
         const unsigned same = __match_any_sync(kFull, ok ? f : 0x80000000u + lane);
@@ -551,6 +578,11 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
     if (warp != 0)
         return;
     sel_core(p, v, bad);
+    if (p.dbg & 512) {  // experiment: trigger dependents once every output is visible
+        __threadfence();
+        __syncwarp();
+        asm volatile("griddepcontrol.launch_dependents;");
+    }
     tl_mark(p, 0, true);
 }
 
@@ -710,6 +742,11 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
     }
     __syncthreads();
     plan_core(p, v);
+    if (p.dbg & 512) {
+        __threadfence();
+        __syncthreads();
+        asm volatile("griddepcontrol.launch_dependents;");
+    }
     tl_mark(p, 1, true);
 }
 

@@ -25,7 +25,7 @@ def dev(data, labels):
             torch.from_numpy(np.ascontiguousarray(labels).astype(np.int32)).cuda())
 
 
-def run_parity(drb, K, cap, S, b, c, r, seed, steps, spec=None, n_of=None, host=False):
+def run_parity(drb, K, cap, S, b, c, r, seed, steps, spec=None, n_of=None, host=False, inplace=False):
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed)
     eng = drb.engine(buf)
     eng.start()
@@ -40,7 +40,14 @@ def run_parity(drb, K, cap, S, b, c, r, seed, steps, spec=None, n_of=None, host=
         lab = spec.labels(0, i, n)
         data = spec.payload(0, i, n)
         o, ol, oc = rep.step(data[None], lab[None])
-        if host:
+        if host and inplace:  # m' assembled in the caller's batch buffer (capacity n + r rows)
+            slot = np.zeros((n + r, S), np.uint8)
+            slot_l = np.zeros(n + r, np.uint32)
+            slot[:n], slot_l[:n] = data, lab
+            eng.update_host(slot[:n], slot_l[:n], slot, slot_l, cnt)
+            eng.synchronize()
+            got, got_l, got_c = slot[: cnt[0]], slot_l[: cnt[0]].astype(np.int64), int(cnt[0])
+        elif host:
             eng.update_host(data, lab, out, out_l, cnt)
             eng.synchronize()
             got, got_l, got_c = out[: cnt[0]], out_l[: cnt[0]].astype(np.int64), int(cnt[0])
@@ -96,6 +103,11 @@ def test_engine_class_incremental_c2_full_size(drb):
     """BASELINE config 2 shape on one rank: 224x224x3 u8, K=100 (4 tasks), cap=48, b=56, r=7, c=14."""
     spec = stream_spec(100, 4, 56, 150528, steps_per_task=30, seed=1)
     run_parity(drb, 100, 48, 150528, 56, 14, 7, seed=1, steps=130, spec=spec)
+
+
+def test_engine_host_path_in_place(drb):
+    run_parity(drb, 10, 5, 96, 32, 14, 8, 4, 30, host=True, inplace=True,
+               n_of=lambda i: [32, 7, 0, 32, 1][i % 5])
 
 
 def test_engine_host_path(drb):
