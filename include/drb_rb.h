@@ -152,6 +152,20 @@ DRB_RB_API drb_status drb_plan(uint32_t want, uint32_t n_workers, uint32_t n_cla
                                const uint32_t* occ, drb_rng* s, drb_slot_ref* out,
                                uint32_t* out_count, int32_t device);
 
+/* Global-sampling bias test (drb_bias_test, proj/include/drb.h:91-97; the procedure of
+ * proj/src/runner/bias.cpp:35-154): every rank of an n_workers mesh freezes its share of
+ * `fill` samples (labels i % K, all inserted), rank 0 draws `draws` plans of rep_count from
+ * its global-sampling stream of `seed` — on the GPU — and the per-slot hit counts are tested
+ * against uniform with Pearson's chi-square (make_bias_report, metrics.cpp:90-107; p-value
+ * = Q(df/2, stat/2), stats.cpp:54-96). biased_control != 0 plans over rank 0's own slots only
+ * (plan_local_only, sampler.cpp:70-83), the negative control. counts: NULL or `fill`
+ * entries (one per slot, flat worker-major order). config_error when fill < n_workers,
+ * usage_error when draws == 0 (zero expected count). */
+DRB_RB_API drb_status drb_rb_bias_test(uint32_t n_workers, uint32_t n_classes, uint32_t rep_count,
+                                       uint64_t seed, uint64_t draws, uint64_t fill, int biased_control,
+                                       uint64_t* counts, double* statistic, double* p_value,
+                                       int32_t device);
+
 /* ---- rehearsal_buffer (proj/src/buffer/rehearsal_buffer.hpp:60-95) --------------------- */
 /* rehearsal_buffer(K, cap) + engine(cfg, rank, ...) storage. config_error on K==0 / cap==0
  * (rehearsal_buffer.cpp:30-31). */

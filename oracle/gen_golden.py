@@ -7,6 +7,10 @@ Outputs:
   tests/golden/kat.json     KAT1-KAT6 + extra rng/swor/plan vectors
   tests/golden/replay.json  per-step sha256 of every rank's m'_i (bytes ++ labels ++ count)
                             under the synchronous replay, for small configs at N = 1, 2, 4, 8
+  tests/golden/bias.json    the bias test of proj/tests/acceptance.cpp:205-227 (K=10, r=7,
+                            seed=5, 1e5 draws; N=2 fill 40, N=4 fill 80, local-only control):
+                            sha256 of the reference's per-slot counts, its chi-square
+                            statistic and p-value (make_bias_report)
 """
 from __future__ import annotations
 
@@ -104,6 +108,24 @@ def kat(be: Backend):
     return k
 
 
+BIAS_CONFIGS = [("n2", 2, 40, False), ("n4", 4, 80, False), ("control", 2, 40, True)]
+BIAS_K, BIAS_R, BIAS_SEED = 10, 7, 5
+
+
+def bias(be, draws):
+    from oracle.py_oracle import bias_counts, bias_view, reference_bias_report
+    out = {}
+    for name, N, fill, control in BIAS_CONFIGS:
+        occ = bias_view(N, BIAS_K, fill)
+        counts = bias_counts(be, occ, BIAS_R, BIAS_SEED, draws, control)
+        st, p = reference_bias_report(counts, BIAS_R, draws)
+        out[name] = {"N": N, "K": BIAS_K, "r": BIAS_R, "seed": BIAS_SEED, "fill": fill, "local_only": control,
+                     "draws": draws, "occ": occ.tolist(),
+                     "counts_sha256": hashlib.sha256(counts.astype("<u8").tobytes()).hexdigest(),
+                     "counts_head": counts[:16].tolist(), "statistic": st, "p_value": p}
+    return out
+
+
 def main():
     be = Backend("reference")
     os.makedirs(OUT, exist_ok=True)
@@ -116,6 +138,8 @@ def main():
                        "digests": replay_digests(be, cfg)}
     with open(os.path.join(OUT, "replay.json"), "w") as f:
         json.dump(rep, f)
+    with open(os.path.join(OUT, "bias.json"), "w") as f:
+        json.dump({"draws_1e5": bias(be, 100000), "draws_2000": bias(be, 2000)}, f, indent=1)
     print("wrote", os.listdir(OUT))
 
 

@@ -212,5 +212,43 @@ class OracleBuffer:
         return rc, app, rep
 
 
+# ---- global-sampling bias test (proj/src/runner/bias.cpp:35-154), test infrastructure -----
+def bias_view(N: int, K: int, fill: int) -> np.ndarray:
+    """Frozen occupancy after the fill phase (bias.cpp:42-45,84-89): rank w inserts
+    fill/N (+1 for w < fill % N) samples labelled i % K, all appended (capacity covers it)."""
+    occ = np.zeros((N, K), np.uint32)
+    for w in range(N):
+        here = fill // N + (1 if w < fill % N else 0)
+        for c in range(K):
+            occ[w, c] = here // K + (1 if c < here % K else 0)
+    return occ
+
+
+def bias_counts(be: "Backend", occ: np.ndarray, r: int, seed: int, draws: int, local_only: bool) -> np.ndarray:
+    """Per-slot hit counts of `draws` plans on rank 0's global-sampling stream (bias.cpp:
+    104-133); the biased control plans over rank 0's own slots only (plan_local_only,
+    sampler.cpp:70-83 == plan over the one-row view). Slots are counted in flat order."""
+    total = int(occ.sum())
+    view = occ[:1] if local_only else occ
+    plans = be.plan(r, view, seed, 0, GLOBAL_SAMPLING, rounds=draws)
+    pre = np.concatenate([[0], np.cumsum(occ.reshape(-1).astype(np.int64))])
+    K = occ.shape[1]
+    flat = np.concatenate([pre[p[:, 0].astype(np.int64) * K + p[:, 1]] + p[:, 2] for p in plans if len(p)])
+    return np.bincount(flat, minlength=total).astype(np.uint64)
+
+
+def reference_bias_report(counts: np.ndarray, r: int, draws: int):
+    """make_bias_report of the reference itself (metrics.cpp:90-107) -> (statistic, p)."""
+    lib = C.CDLL(REF_LIB)
+    f = lib.ref_bias_report
+    f.restype = C.c_int
+    f.argtypes = [_u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    st, p = C.c_double(0), C.c_double(0)
+    rc = f(np.ascontiguousarray(counts, np.uint64), len(counts), r, draws, C.byref(st), C.byref(p))
+    if rc:
+        raise ValueError("make_bias_report failed")
+    return st.value, p.value
+
+
 def have_reference() -> bool:
     return os.path.exists(REF_LIB)

@@ -20,6 +20,7 @@
 #include "core/errors.hpp"
 #include "core/rng.hpp"
 #include "engine/engine.hpp"
+#include "metrics/metrics.hpp"
 #include "runner/mesh.hpp"
 #include "sampler/sampler.hpp"
 #include "sampler/size_table.hpp"
@@ -347,6 +348,20 @@ int ref_engine_bench(std::uint32_t N, std::uint32_t K, std::uint32_t cap, std::u
         *samples = total;
         return 0;
     } catch (const std::exception&) {
+        return 8;
+    }
+}
+
+// make_bias_report (proj/src/metrics/metrics.cpp:90-107): Pearson chi-square of per-slot
+// hit counts against uniform, p-value by the reference's gamma_q (stats.cpp:54-96).
+int ref_bias_report(const std::uint64_t* counts, std::uint64_t n, std::uint64_t rep_count,
+                    std::uint64_t draws, double* statistic, double* p_value) {
+    try {
+        const auto r = make_bias_report(std::span<const std::uint64_t>(counts, n), rep_count, draws);
+        *statistic = r.statistic;
+        *p_value = r.p_value;
+        return 0;
+    } catch (...) {
         return 8;
     }
 }

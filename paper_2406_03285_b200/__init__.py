@@ -6,12 +6,13 @@ built library raises ImportError — there is no CPU fallback.
 """
 from ._lib import (config_error, drb_error, engine_error, invalid_argument, transport_error,  # noqa: F401
                    usage_error)
-from .rehearsal import (augment, augmented_batch, engine, insertion_report, occupancy_snapshot,  # noqa: F401
+from .rehearsal import (augment, augmented_batch, bias_report, bias_test, engine, insertion_report, occupancy_snapshot,  # noqa: F401
                         plan, read_entry, rehearsal_buffer, rng_stream, sample_without_replacement,
                         sampling_plan)
 
 __all__ = [
-    "rehearsal_buffer", "engine", "rng_stream", "plan", "augment", "sample_without_replacement",
+    "rehearsal_buffer", "engine", "rng_stream", "plan", "augment", "sample_without_replacement", "bias_test",
+    "bias_report",
     "augmented_batch", "insertion_report", "occupancy_snapshot", "read_entry", "sampling_plan",
     "config_error", "usage_error", "engine_error", "transport_error", "invalid_argument", "drb_error",
 ]

@@ -140,6 +140,7 @@ def _load():
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),
+        "drb_rb_bias_test": (st, [u32, u32, u32, u64, u64, u64, i32, vp, P(C.c_double), P(C.c_double), i32]),
         "drb_rb_trace_read": (st, [vp, vp]),
         "drb_rb_timeline_read": (st, [vp, vp, P(u32)]),
     }

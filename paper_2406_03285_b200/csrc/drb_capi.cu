@@ -6,6 +6,7 @@
 #include <unistd.h>
 
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -319,6 +320,93 @@ drb_status drb_plan(uint32_t want, uint32_t n_workers, uint32_t n_classes, const
         cuda_check(cudaMemcpy(out, d_out.p, size_t(c) * 12, cudaMemcpyDeviceToHost), "plan out");
         cuda_check(cudaMemcpy(&s->ctr, d_ctr.p, 8, cudaMemcpyDeviceToHost), "plan ctr");
         *out_count = c;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Regularized upper incomplete gamma Q(a, x): the power series of P for x < a + 1, else the
+// modified-Lentz continued fraction of Q (the same split as proj/src/metrics/stats.cpp).
+double gamma_q(double a, double x) {
+    if (x <= 0.0)
+        return 1.0;
+    const double front = std::exp(-x + a * std::log(x) - std::lgamma(a));
+    if (x < a + 1.0) {
+        double term = 1.0 / a, sum = term;
+        for (int n = 1; n < 100000; ++n) {
+            term *= x / (a + n);
+            sum += term;
+            if (std::fabs(term) < std::fabs(sum) * 1e-17)
+                break;
+        }
+        return 1.0 - sum * front;
+    }
+    const double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int i = 1; i < 100000; ++i) {
+        const double an = -i * (i - a);
+        b += 2.0;
+        d = an * d + b;
+        if (std::fabs(d) < tiny)
+            d = tiny;
+        c = b + an / c;
+        if (std::fabs(c) < tiny)
+            c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (std::fabs(del - 1.0) < 1e-16)
+            break;
+    }
+    return front * h;
+}
+
+}  // namespace
+
+extern "C" {
+
+drb_status drb_rb_bias_test(uint32_t n_workers, uint32_t n_classes, uint32_t rep_count, uint64_t seed,
+                            uint64_t draws, uint64_t fill, int biased_control, uint64_t* counts,
+                            double* statistic, double* p_value, int32_t device) {
+    DRB_REQUIRE(statistic && p_value);
+    return guarded([&] {
+        if (n_workers == 0 || n_workers > kMaxWorld || n_classes == 0)
+            fail(DRB_ERR_CONFIG, "bias test: need 1 <= n_workers <= 8 and n_classes >= 1");
+        if (fill < n_workers)  // bias.cpp:37-38
+            fail(DRB_ERR_CONFIG, "bias test: fill must provide at least one sample per worker");
+        if (fill >= (1ull << 31))
+            fail(DRB_ERR_CONFIG, "bias test: fill larger than 2^31 slots");
+        if (draws == 0 || rep_count == 0)  // make_bias_report: zero expected count per slot
+            fail(DRB_ERR_USAGE, "bias test: zero expected count per slot");
+        // frozen view after the fill phase (bias.cpp:42-45,84-89): all inserted
+        uint64_t total0 = 0;
+        for (uint32_t c = 0; c < n_classes; ++c) {
+            const uint64_t here = fill / n_workers + (0 < fill % n_workers ? 1 : 0);
+            total0 += here / n_classes + (c < here % n_classes ? 1 : 0);
+        }
+        const uint64_t total = fill;  // sum over ranks of fill_here
+        device_guard g(device);
+        dev_tmp d_counts(total * 8), d_ctr(8);
+        cuda_check(cudaMemset(d_counts.p, 0, total * 8), "bias counts");
+        const uint64_t key = derive_key(seed, 0, DRB_PURPOSE_GLOBAL_SAMPLING, 0, 0);
+        if (launch_bias_counts(key, rep_count, uint32_t(biased_control ? total0 : total), draws,
+                               d_counts.as<unsigned long long>(), d_ctr.as<uint64_t>(), nullptr))
+            fail(DRB_ERR_INTERNAL, std::string("bias launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        std::vector<uint64_t> obs(total);
+        cuda_check(cudaMemcpy(obs.data(), d_counts.p, total * 8, cudaMemcpyDeviceToHost), "bias counts copy");
+        if (counts)
+            std::memcpy(counts, obs.data(), total * 8);
+        // Pearson chi-square against uniform (metrics.cpp:90-107)
+        const double expected = double(rep_count) * double(draws) / double(total);
+        double stat = 0.0;
+        for (uint64_t x = 0; x < total; ++x) {
+            const double diff = double(obs[x]) - expected;
+            stat += diff * diff / expected;
+        }
+        *statistic = stat;
+        *p_value = total > 1 ? gamma_q(double(total - 1) / 2.0, stat / 2.0) : 1.0;
     });
 }
 

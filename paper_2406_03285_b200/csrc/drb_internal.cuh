@@ -298,6 +298,8 @@ int launch_run(const RunParams& rp, uint32_t grid, void* stream);
 uint32_t sel_smem_bytes(uint32_t K, uint32_t nmax);
 uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r);
 uint32_t plan_threads(uint32_t N);
+int launch_bias_counts(uint64_t key, uint32_t want, uint32_t total_draw, uint64_t draws,
+                       unsigned long long* counts_dev, uint64_t* ctr_out_dev, void* stream);
 int launch_rng_draw(uint64_t key, uint64_t ctr, uint64_t bound, uint64_t n, uint64_t* out_dev,
                     uint64_t* ctr_out_dev, void* stream);
 int launch_swor(uint64_t key, uint64_t ctr, uint32_t n, uint32_t k, uint32_t* out_dev,

@@ -1731,6 +1731,30 @@ __global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_co
         run_copy_role(rp, sm, sp);
 }
 
+// ---- global-sampling bias test (proj/src/runner/bias.cpp:104-133) -----------------------
+// One warp replays rank 0's global-sampling stream plan after plan — each plan's first
+// counter is where the previous one stopped, so the draws are inherently sequential — and
+// counts the slots hit, indexed by flat slot (worker-major, class, slot: the order of
+// size_table::view::locate). total_draw = the view's total, or rank 0's own total for the
+// biased control (plan_local_only, sampler.cpp:70-83: its flats are rank 0's slots).
+__global__ void bias_counts_kernel(uint64_t key, uint32_t want, uint32_t total_draw, uint64_t draws,
+                                   unsigned long long* counts, uint64_t* ctr_out) {
+    extern __shared__ __align__(16) uint32_t acc[];
+    const uint32_t lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32)
+        return;
+    uint64_t ctr = 0;
+#pragma unroll 1
+    for (uint64_t d = 0; d < draws; ++d) {
+        const uint32_t c = warp_plan_draw(key, ctr, want, total_draw, acc);
+        for (uint32_t j = lane; j < c; j += 32)
+            atomicAdd(counts + acc[j], 1ull);
+        __syncwarp();
+    }
+    if (lane == 0)
+        *ctr_out = ctr;
+}
+
 // ---- standalone kernels for the buffer-level API (tests / facade) ----------------------
 
 __global__ void rng_draw_kernel(uint64_t key, uint64_t ctr, uint64_t bound, uint64_t n,
@@ -1957,6 +1981,17 @@ int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out) {
                                                          smem_bytes) == cudaSuccess
                ? 0
                : -1;
+}
+
+int launch_bias_counts(uint64_t key, uint32_t want, uint32_t total_draw, uint64_t draws,
+                       unsigned long long* counts_dev, uint64_t* ctr_out_dev, void* stream) {
+    const size_t smem = (size_t(want) + 32) * 4;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(bias_counts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        return -1;
+    bias_counts_kernel<<<1, 32, smem, static_cast<cudaStream_t>(stream)>>>(key, want, total_draw, draws, counts_dev,
+                                                                            ctr_out_dev);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_rng_draw(uint64_t key, uint64_t ctr, uint64_t bound, uint64_t n, uint64_t* out_dev,

@@ -1,0 +1,139 @@
+"""Asynchronous overlap of the rehearsal engine with a real training step.
+
+The reference measures this with `run_overlap_bench` (proj/src/runner/overlap.cpp:39-120,
+acceptance criterion 5 of proj/tests/acceptance.cpp:229-256): calibrate the background round
+cost, run a training stub of >= 10x that cost after every `engine.update(m)`, and require the
+mean time the trainer waits for its augmented batch to stay under 5% of the iteration.
+
+Here the trainer is a real GPU training step (forward, backward and SGD update of a small
+convolutional classifier on m'_i, bf16 autocast) on its own CUDA stream, and the engine's
+three kernels run on theirs. update(m_{i+1}) is enqueued one iteration ahead, so round i+1's
+selection, sampling and copy run while step i trains; the train stream only waits on the
+event of m'_i. Everything is timed on the device:
+  background_ms      engine alone, device time per update
+  train_ms           the training step alone on a resident batch
+  iteration_ms       the overlapped loop, per iteration (train stream events)
+  wait_ms            iteration_ms - train_ms: what the trainer lost to the engine
+                     (waiting for m'_i, and SM / HBM contention)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.nn as nn
+
+
+@dataclass
+class overlap_result:  # overlap_stats (proj/include/drb.h:70-77)
+    train_cost_ms: float
+    background_ms: float
+    mean_wait_ms: float
+    mean_iteration_ms: float
+    iterations: int
+
+    @property
+    def wait_fraction(self) -> float:
+        return self.mean_wait_ms / self.mean_iteration_ms if self.mean_iteration_ms > 0 else 0.0
+
+
+class conv_classifier(nn.Module):
+    """The consumer: a small CNN over H x W x C uint8 samples (channels-last bytes)."""
+
+    def __init__(self, hw: int, ch: int, n_classes: int, width: int = 64, depth: int = 4):
+        super().__init__()
+        self.hw, self.ch = hw, ch
+        layers, c = [], ch
+        for i in range(depth):
+            layers += [nn.Conv2d(c, width * (2 ** min(i, 2)), 3, stride=2, padding=1), nn.ReLU(inplace=True)]
+            c = width * (2 ** min(i, 2))
+        self.body = nn.Sequential(*layers)
+        self.head = nn.Linear(c, n_classes)
+
+    def forward(self, x_u8: torch.Tensor) -> torch.Tensor:
+        x = x_u8.view(-1, self.hw, self.hw, self.ch).permute(0, 3, 1, 2).float().div_(255.0)
+        x = x.contiguous(memory_format=torch.channels_last)
+        return self.head(self.body(x).mean(dim=(2, 3)))
+
+
+def make_train_step(model: nn.Module, lr: float = 0.01):
+    opt = torch.optim.SGD(model.parameters(), lr=lr, momentum=0.9)
+    loss_fn = nn.CrossEntropyLoss()
+
+    def step(data_u8: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = loss_fn(model(data_u8), labels.long())
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        opt.step()
+        return loss
+
+    return step
+
+
+def run_overlap_bench(eng, data_ring: torch.Tensor, label_ring: torch.Tensor, train_step, iterations: int,
+                      calib: int = 60) -> overlap_result:
+    """eng: a started engine; data_ring [B, n, S] u8 / label_ring [B, n] int32 on its device."""
+    dev = data_ring.device
+    B = data_ring.shape[0]
+    s_eng = torch.cuda.Stream(device=dev)
+    s_train = torch.cuda.Stream(device=dev)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    # background: engine alone (device time per update, steady state)
+    with torch.cuda.stream(s_eng):
+        for i in range(calib):
+            eng.update((data_ring[i % B], label_ring[i % B]), stream=s_eng)
+    torch.cuda.synchronize(dev)
+    e0, e1 = ev(), ev()
+    e0.record(s_eng)
+    for i in range(calib):
+        eng.update((data_ring[i % B], label_ring[i % B]), stream=s_eng)
+    e1.record(s_eng)
+    torch.cuda.synchronize(dev)
+    background_ms = e0.elapsed_time(e1) / calib
+
+    # training step alone, on a resident augmented batch
+    aug = eng.update((data_ring[0], label_ring[0]), stream=s_eng)
+    d, l = aug.tensors()
+    d, l = d.clone(), l.clone()
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(s_train):
+        for _ in range(5):
+            train_step(d, l)
+    torch.cuda.synchronize(dev)
+    e0.record(s_train)
+    with torch.cuda.stream(s_train):
+        for _ in range(min(iterations, 100)):
+            train_step(d, l)
+    e1.record(s_train)
+    torch.cuda.synchronize(dev)
+    train_ms = e0.elapsed_time(e1) / min(iterations, 100)
+
+    # overlapped loop: update(m_{i+1}) is enqueued before step i trains on m'_i
+    ready = [torch.cuda.Event() for _ in range(3)]
+
+    def enqueue(i):
+        a = eng.update((data_ring[i % B], label_ring[i % B]), stream=s_eng)
+        ready[i % 3].record(s_eng)
+        return a
+
+    pending = enqueue(0)
+    torch.cuda.synchronize(dev)
+    e0.record(s_train)
+    for i in range(iterations):
+        cur = pending
+        s_train.wait_event(ready[i % 3])
+        # m'_i stays valid until update(m_{i+2}) is enqueued; the next update is i+1, and
+        # the one after waits on the train stream (s_eng waits for step i's reads below)
+        pending = enqueue(i + 1)
+        with torch.cuda.stream(s_train):
+            dd, ll = cur.tensors_nowait()
+            train_step(dd, ll)
+        s_eng.wait_stream(s_train)  # step i read m'_i before update(m_{i+2}) may reuse its slot
+    e1.record(s_train)
+    torch.cuda.synchronize(dev)
+    iteration_ms = e0.elapsed_time(e1) / iterations
+    return overlap_result(train_ms, background_ms, max(0.0, iteration_ms - train_ms), iteration_ms, iterations)

@@ -121,6 +121,23 @@ def plan(want: int, view: np.ndarray, rng: rng_stream, device: int = 0) -> sampl
     return sampling_plan(out[: got.value].copy())
 
 
+@dataclass
+class bias_report:
+    statistic: float
+    p_value: float
+    counts: np.ndarray  # per-slot hits, flat worker-major order
+
+
+def bias_test(n_workers: int, n_classes: int, rep_count: int, seed: int, draws: int, fill: int,
+              biased_control: bool = False, device: int = 0) -> bias_report:
+    """drb_bias_test (drb.h:91-97, bias.cpp:35-154) with the plans drawn on the GPU."""
+    counts = np.zeros(max(fill, 1), np.uint64)
+    st, p = C.c_double(0), C.c_double(0)
+    check(lib.drb_rb_bias_test(n_workers, n_classes, rep_count, seed, draws, fill, 1 if biased_control else 0,
+                               counts.ctypes.data, C.byref(st), C.byref(p), device))
+    return bias_report(float(st.value), float(p.value), counts[:fill])
+
+
 def augment(m: Tuple[torch.Tensor, torch.Tensor], reps: Tuple[torch.Tensor, torch.Tensor]):
     """m then reps (sampler.cpp:234-240). The engine already produces this layout in place;
     this standalone form concatenates two device batches."""
@@ -282,6 +299,14 @@ class augmented_batch:
             check(lib.drb_rb_aug_count(self.eng.buffer.h, C.byref(self.aug), C.byref(c)))
             self._count = int(c.value)
         return self._count
+
+    def tensors_nowait(self) -> Tuple[torch.Tensor, torch.Tensor]:
+        """Views of the n + r rows m'_i has in steady state (the global buffer holds >= r
+        slots), without waiting on the host: consumers order on the device (stream events)."""
+        b = self.eng.buffer
+        rows = self.n + b.r
+        return (_view(self.aug.data, (rows, b.S), "|u1", b.device, self),
+                _view(self.aug.labels, (rows,), "<i4", b.device, self))
 
     def tensors(self) -> Tuple[torch.Tensor, torch.Tensor]:
         b = self.eng.buffer

@@ -123,3 +123,17 @@ def test_schedule_stream_matches_reference_rng():
     assert [s.bounded(97) for _ in range(50)] == R.rng_bounded(5, 0, 4, 97, 50, keyed=True, k1=0xABCD).tolist()
     sched = make_schedule(100, 4, 1)
     assert sorted(sum(sched, [])) == list(range(100)) and [len(t) for t in sched] == [25] * 4
+
+
+def test_port_bias_counts_match_reference_golden():
+    """The C restatement's bias-test counts (plan rounds on rank 0's stream) against the
+    reference's, tests/golden/bias.json (oracle/gen_golden.py, bias.cpp:104-133)."""
+    import hashlib
+    from oracle.py_oracle import Backend, bias_counts, bias_view
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "bias.json")))["draws_2000"]
+    be = Backend("port")
+    for name, g in gold.items():
+        occ = bias_view(g["N"], g["K"], g["fill"])
+        assert occ.tolist() == g["occ"], name
+        c = bias_counts(be, occ, g["r"], g["seed"], g["draws"], g["local_only"])
+        assert hashlib.sha256(c.astype("<u8").tobytes()).hexdigest() == g["counts_sha256"], name
