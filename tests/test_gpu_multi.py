@@ -96,3 +96,40 @@ def test_multi_process_ipc_parity(N):
            "--master-addr=127.0.0.1", f"--master-port={port}", worker]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+
+
+def test_stalled_peer_times_out_without_hanging(monkeypatch):
+    """A peer that stops calling update: the reference degrades after its
+    rendezvous timeout (size_table.cpp:66-100); here every cross-rank wait is bounded
+    (DRB_TIMEOUT_MS), the round fails with a sticky transport error, the augmented batch
+    reports it, the engine is dead for later updates (engine.cpp:67-68,74-80), and shutdown
+    still drains — the GPU is not left spinning."""
+    if ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    import time
+
+    import paper_2406_03285_b200 as drb
+    monkeypatch.setenv("DRB_TIMEOUT_MS", "300")
+    K, cap, S, b, c, r = 8, 4, 64, 16, 6, 5
+    bufs, engs = make_world(drb, 2, K, cap, S, b, c, r, seed=3)
+    spec = stream_spec(K, 1, b, S, steps_per_task=10**9, seed=3)
+    streams = [torch.cuda.Stream(device=w) for w in range(2)]
+
+    def upd(w, i):
+        with torch.cuda.device(w):
+            m = (torch.from_numpy(spec.payload(w, i)).cuda(w),
+                 torch.from_numpy(spec.labels(w, i).astype(np.int32)).cuda(w))
+            return engs[w].update(m, stream=streams[w])
+    for i in range(4):  # healthy rounds
+        a = [upd(w, i) for w in range(2)]
+        assert [x.count() for x in a] == [b + r if i else b] * 2
+    t0 = time.time()
+    lone = upd(0, 4)  # rank 1 stalls: never enqueues round 4
+    with pytest.raises(drb.engine_error):
+        lone.count()
+    assert time.time() - t0 < 30
+    with pytest.raises(drb.engine_error):
+        upd(0, 5)
+    assert engs[0].device_error() != 0
+    for e in engs:
+        e.shutdown()
