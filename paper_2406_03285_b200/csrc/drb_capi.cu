@@ -135,6 +135,7 @@ struct drb_rb {
     cudaStream_t s_plan = nullptr;    // planning chain plan(i)
     cudaStream_t h2d = nullptr;       // host-path input copies
     cudaStream_t d2h = nullptr;       // host-path output copies
+    cudaStream_t s_wait = nullptr;    // multi-rank: peers_wait(i) -> "m'_i ready", off the copy chain
     uint8_t* slab = nullptr;          // [K][cap][S]
     uint32_t* slab_labels = nullptr;  // [K][cap]
     uint8_t* region = nullptr;        // own peer-shareable region
@@ -458,6 +459,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         cuda_check(cudaStreamCreateWithFlags(&h->s_plan, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&h->s_wait, cudaStreamNonBlocking), "stream");
         const uint64_t slab_bytes = uint64_t(c.n_classes) * c.per_class_cap * c.sample_bytes;
         cuda_check(cudaMalloc(&h->slab, slab_bytes), "slab alloc");
         cuda_check(cudaMalloc(&h->slab_labels, uint64_t(c.n_classes) * c.per_class_cap * 4), "labels alloc");
@@ -569,6 +571,7 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaStreamDestroy(h->s_plan);
         cudaStreamDestroy(h->h2d);
         cudaStreamDestroy(h->d2h);
+        cudaStreamDestroy(h->s_wait);
         delete h;
     });
 }
@@ -633,10 +636,13 @@ drb_status drb_rb_read_slots(drb_rb* h, const drb_read_request* requests, uint32
         device_guard g(h->cfg.device);
         dev_tmp d_req(size_t(count) * 8), d_status(count), d_ctr(8);
         cuda_check(cudaMemcpy(d_req.p, requests, size_t(count) * 8, cudaMemcpyHostToDevice), "req copy");
-        const uint32_t* occ = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_table) +
+        const uint64_t* row = reinterpret_cast<const uint64_t*>(h->region + h->layout.off_table) +
                               (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
                               uint64_t(h->cfg.rank) * h->cfg.n_classes;
         cuda_check(cudaDeviceSynchronize(), "read_slots order");
+        dev_tmp d_occ(size_t(h->cfg.n_classes) * 4);  // the counts of the versioned words
+        cuda_check(cudaMemcpy2D(d_occ.p, 4, row, 8, 4, h->cfg.n_classes, cudaMemcpyDeviceToDevice), "occ copy");
+        const uint32_t* occ = d_occ.as<uint32_t>();
         if (launch_read_slots(h->slab, h->slab_labels, occ, h->cfg.n_classes, h->cfg.per_class_cap,
                               h->cfg.sample_bytes, d_req.as<uint32_t>(), count, substitute->key,
                               substitute->ctr, static_cast<uint8_t*>(out), out_labels,
@@ -653,10 +659,10 @@ drb_status drb_rb_snapshot(drb_rb* h, uint32_t* per_class, uint64_t* version) {
     return guarded([&] {
         device_guard g(h->cfg.device);
         cuda_check(cudaDeviceSynchronize(), "snapshot order");
-        const uint32_t* occ = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_table) +
+        const uint64_t* row = reinterpret_cast<const uint64_t*>(h->region + h->layout.off_table) +
                               (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
                               uint64_t(h->cfg.rank) * h->cfg.n_classes;
-        cuda_check(cudaMemcpy(per_class, occ, h->cfg.n_classes * 4ull, cudaMemcpyDeviceToHost), "snapshot");
+        cuda_check(cudaMemcpy2D(per_class, 4, row, 8, 4, h->cfg.n_classes, cudaMemcpyDeviceToHost), "snapshot");
         SelState st{};
         cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
         *version = st.version;
@@ -826,8 +832,8 @@ StepParams iter_params(drb_rb* h, uint64_t i, const void* batch, const uint32_t*
 constexpr int kE = drb_rb::kEv;
 inline int ev_of(uint64_t i) { return int(i % kE); }
 
-// sel(i) on s_sel: W slot i%8 free once copy(i-8) read it; table slot (i+1)%6 (own row
-// v=i+1) free once plan(i-4) read it (peers' rows are ordered by the copy handshake);
+// sel(i) on s_sel: table slot (i+1)%6 (own row v=i+1) free once plan(i-4) read it (a peer's
+// plan(i-6) precedes its copy(i-6), which precedes my sel(i) through the rendezvous);
 // optionally after the caller's prior work on `caller` (m_i produced, m'_{i-3} consumed).
 void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
                  cudaStream_t caller, bool wait_caller) {
@@ -836,11 +842,17 @@ void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* label
         cuda_check(cudaEventRecord(h->ev_user[ev_of(i)], caller), "event");
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_user[ev_of(i)], 0), "wait");
     }
+    // W slot i%8: copy(i-8) read it. Multi-rank: copy(i-6) complete before sel(i)
+    // publishes — every plan(i) entry is pushed into an m' slot whose previous pushes
+    // (reps(i-6), any owner) must have landed; each owner orders them before its own sel(i),
+    // and plan(i) of every rank waits for all sel(i) rows. (One rank: stream order.)
     if (i >= h->dep_floor + kListRing)
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
+    if (h->cfg.world > 1 && i >= h->dep_floor + kAugRing)
+        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - kAugRing)], 0), "wait");
     if (i >= h->dep_floor + 4)
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_plan[ev_of(i - 4)], 0), "wait");
-    if (launch_sel(p, h->s_sel, h->use_pdl && (h->dbg_bits & 768)))  // DRB_DBG bits 8/9: PDL sel chain
+    if (launch_sel(p, h->s_sel, h->use_pdl && (h->dbg_bits & 256)))  // DRB_DBG bit 8: PDL sel chain
         fail(DRB_ERR_INTERNAL, std::string("sel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     cuda_check(cudaEventRecord(h->ev_sel[ev_of(i)], h->s_sel), "event");
     h->ver = h->ver0 + i + 1;
@@ -853,7 +865,7 @@ void enqueue_plan(drb_rb* h, uint64_t i) {
     cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_sel[ev_of(i)], 0), "wait");
     if (i >= h->dep_floor + kListRing)
         cuda_check(cudaStreamWaitEvent(h->s_plan, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
-    if (launch_plan_next(p, h->s_plan, h->use_pdl && (h->dbg_bits & 768)))
+    if (launch_plan_next(p, h->s_plan, h->use_pdl && (h->dbg_bits & 256)))
         fail(DRB_ERR_INTERNAL, std::string("plan launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     cuda_check(cudaEventRecord(h->ev_plan[ev_of(i)], h->s_plan), "event");
     h->cur_plan = uint32_t((h->plan_par0 + i + 1) & 1);
@@ -864,10 +876,16 @@ void enqueue_plan(drb_rb* h, uint64_t i) {
 // prewait_next (inside a run, with copy(i+1) to follow on `s`): s also waits here for
 // sel(i+1) / plan(i+1), so copy(i+1)'s only new dependency is copy(i) itself — the edge a
 // programmatic (PDL) launch can overlap (sel/plan run iterations ahead; this costs nothing).
+// batch_ready: the caller's event after m_i was produced (single steps run their copies on
+// the handle's own stream). ready_wait: multi-rank single steps follow the copy with
+// peers_wait(i) on s_wait; done[slot] ("m'_i ready") is recorded after it.
 void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labels, uint32_t n,
                   cudaStream_t s, bool first_of_run, drb_aug* out, cudaEvent_t ev_begin = nullptr,
-                  cudaEvent_t ev_end = nullptr, bool prewait_next = false) {
+                  cudaEvent_t ev_end = nullptr, bool prewait_next = false, cudaEvent_t batch_ready = nullptr,
+                  bool ready_wait = false) {
     StepParams p = iter_params(h, i, batch, labels, n);
+    if (batch_ready)
+        cuda_check(cudaStreamWaitEvent(s, batch_ready, 0), "wait");
     if (h->trace) {
         cuda_check(cudaMemsetAsync(h->trace, 0, 32 * 8, s), "trace reset");
         cuda_check(cudaMemsetAsync(h->trace + 14, 0xff, 8, s), "trace reset");
@@ -901,7 +919,14 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
     if (ev_end)
         cuda_check(cudaEventRecordWithFlags(ev_end, s, rec_flags), "event");
     cuda_check(cudaEventRecord(h->ev_copy[ev_of(i)], s), "event");
-    cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
+    if (ready_wait && (p.mode & kModePeers) && i > 0) {
+        cuda_check(cudaStreamWaitEvent(h->s_wait, h->ev_copy[ev_of(i)], 0), "wait");
+        if (launch_peers_wait(p, h->s_wait))
+            fail(DRB_ERR_INTERNAL, std::string("peers_wait launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        cuda_check(cudaEventRecord(h->done[p.aslot], h->s_wait), "event record");
+    } else {
+        cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
+    }
     h->last_copy_stream = s;
     if (out) {
         out->n = n;
@@ -996,7 +1021,13 @@ drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uin
         const uint64_t i = h->step;
         enqueue_sel(h, i, batch, labels, n, s, true);
         enqueue_plan(h, i);
-        enqueue_copy(h, i, batch, labels, n, s, true, out);
+        // the copies run on the handle's stream, one behind the other (PDL: copy(i)'s batch
+        // part overlaps copy(i-1)'s tail); the caller's stream waits for "m'_i ready"
+        const bool chained = h->last_copy_stream == h->stream && i >= h->dep_floor + 1;
+        enqueue_copy(h, i, batch, labels, n, h->stream, !chained, out, nullptr, nullptr, false,
+                     h->ev_user[ev_of(i)], true);
+        if (s != h->stream || h->cfg.world > 1)
+            cuda_check(cudaStreamWaitEvent(s, h->done[i % kAugRing], 0), "wait");
     });
 }
 

@@ -27,7 +27,10 @@ constexpr uint32_t kCtaReserved = 1024u;        // per-CTA system reservation
 // CTA 0, then kTlCtaSlots stamps for each of up to kTlMaxCtas copy CTAs.
 constexpr uint32_t kTlCtaSlots = 16, kTlMaxCtas = 160;
 constexpr uint32_t kTlStride = 32 + kTlCtaSlots * kTlMaxCtas;
-constexpr int kAugRing = 3;    // m' buffers per rank; m'_i valid until step i+2 is enqueued
+// m' buffers per rank. The API promises m'_i until step i+2 is enqueued; the slot is reused
+// by step i+6 (batch rows) and by the pushes of reps(i+5) — a deep ring lets sel(i) order the
+// multi-rank pushes behind copy(i-6) instead of copy(i-3), off the pipeline's critical path.
+constexpr int kAugRing = 6;
 constexpr int kThreads = 512;  // step kernel CTA size (16 warps)
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
 
@@ -62,17 +65,17 @@ struct alignas(16) PlanState {
 };
 
 // Peer-shareable region header (one cudaMalloc per rank, exported over CUDA IPC).
+static_assert(kAugRing <= 8, "RegionHeader sizes aug_count / repcnt for 8 slots");
 struct alignas(256) RegionHeader {
-    uint64_t occ_flag[kMaxWorld];  // [w]: latest occupancy version rank w published here
     uint64_t pushdone[kMaxWorld];  // [w]: 1 + last iteration whose pushes rank w completed
                                    //      (its reps rows of my m'_{i+1} have landed)
-    uint32_t aug_count[4];         // local: rows of m' per ring slot (device copy)
-    uint32_t repcnt[4];            // local: |reps| already written into m' ring slot s
-    uint64_t pad[5];
+    uint32_t aug_count[8];         // local: rows of m' per ring slot (device copy)
+    uint32_t repcnt[8];            // local: |reps| already written into m' ring slot s
+    uint64_t pad[9];
 };
 
 struct RegionLayout {
-    uint64_t off_table;     // u32 [kTableRing][N][K]
+    uint64_t off_table;     // u64 [kTableRing][N][K] occupancy words: version << 32 | occ
     uint64_t off_aug;       // u8  [kAugRing][rows][S]
     uint64_t off_auglab;    // u32 [kAugRing][rows]
     uint64_t aug_slot_bytes;
@@ -82,12 +85,21 @@ struct RegionLayout {
 
 __host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+// An occupancy-table word carries its row version (i+1 for round i's row) next to the count,
+// so a reader recognises a current word by itself: a publisher's plain 8-byte stores need no
+// fence and no separate flag (one NVLink trip instead of store + release + acknowledgement).
+__host__ __device__ inline uint64_t occ_word(uint64_t version, uint32_t occ) {
+    return (uint64_t(uint32_t(version)) << 32) | occ;
+}
+__host__ __device__ inline uint32_t occ_of(uint64_t w) { return uint32_t(w); }
+__host__ __device__ inline bool occ_is(uint64_t w, uint64_t version) { return uint32_t(w >> 32) == uint32_t(version); }
+
 inline RegionLayout region_layout(uint32_t N, uint32_t K, uint64_t S, uint32_t max_batch,
                                   uint32_t r) {
     RegionLayout L{};
     uint64_t off = sizeof(RegionHeader);
     L.off_table = off = align_up(off, 256);
-    off += uint64_t(kTableRing) * N * K * 4;
+    off += uint64_t(kTableRing) * N * K * 8;
     L.rows = uint64_t(max_batch) + r;
     L.aug_slot_bytes = align_up(L.rows * S, 256);
     L.off_aug = off = align_up(off, 256);
@@ -291,6 +303,8 @@ int launch_plan_next(const StepParams& p, void* stream, bool pdl = false);
 // the launch may overlap its tail (programmatic dependent launch).
 int launch_copy(const StepParams& p, uint32_t grid, void* stream, bool pdl);
 int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out);
+// multi-rank: wait (one warp) until every peer's pushes into m'_i landed (pushdone >= i)
+int launch_peers_wait(const StepParams& p, void* stream);
 int copy_tma_occupancy(uint32_t smem_bytes, int* out);  // CTAs per SM of the TMA copy kernel
 // persistent run: dynamic smem, and the cooperative launch (grid = copy_ctas + 2)
 uint32_t run_smem_bytes(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax);

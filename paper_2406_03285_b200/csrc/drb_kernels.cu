@@ -406,6 +406,17 @@ __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
 
 constexpr uint32_t kSelThreads = 128;
 
+// Spin (thread-level) until *flag >= want or the timeout; returns false on timeout.
+__device__ bool wait_flag(const uint64_t* flag, uint64_t want, uint64_t timeout_ns) {
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_sys(flag) < want) {
+        if (globaltimer() - t0 > timeout_ns)
+            return false;
+        __nanosleep(32);
+    }
+    return true;
+}
+
 struct SelView {  // sel's shared-memory arrays (sel_smem carve-up)
     uint32_t *occ, *lab, *sel, *cand_l, *cand_slot, *kind, *misc;
     SelState* st;
@@ -501,26 +512,30 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
     for (uint32_t t = lane; t < k; t += 32)  // stored label == class (class-partitioned)
         p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
     if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
-        uint32_t* tout = reinterpret_cast<uint32_t*>(p.region[me] + p.off_table) +
+        uint64_t* tout = reinterpret_cast<uint64_t*>(p.region[me] + p.off_table) +
                          uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
 #pragma unroll 1
         for (uint32_t x = lane; x < K; x += 32)
-            tout[x] = occ[x];
+            tout[x] = occ_word(p.step + 1, occ[x]);
         if (multi) {
+            // Every peer finished copy(i-6) (it announced pushdone >= i-5): its plan(i-6) no
+            // longer reads the table slot this row overwrites, and its pushes into the m'
+            // slot that plan(i) refills have landed. Normally long true: sel runs ahead.
+            if (p.step >= kAugRing && lane < N && lane != me &&
+                !wait_flag(&reinterpret_cast<const RegionHeader*>(p.region[me])->pushdone[lane],
+                           p.step - (kAugRing - 1), p.timeout_ns) &&
+                p.mailbox)
+                reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = DRB_ERR_TRANSPORT;
+            __syncwarp();
 #pragma unroll 1
             for (uint32_t w = 0; w < N; ++w) {
                 if (w == me)
                     continue;
-                uint32_t* pt = reinterpret_cast<uint32_t*>(p.region[w] + p.off_table) +
+                uint64_t* pt = reinterpret_cast<uint64_t*>(p.region[w] + p.off_table) +
                                uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
 #pragma unroll 1
-                for (uint32_t x = lane; x < K; x += 32)
-                    pt[x] = occ[x];
-            }
-            __syncwarp();  // the warp's row stores precede each lane's release below
-            if (lane < N && lane != me) {
-                RegionHeader* peer = reinterpret_cast<RegionHeader*>(p.region[lane]);
-                st_release_sys(&peer->occ_flag[me], p.step + 1);
+                for (uint32_t x = lane; x < K; x += 32)  // self-validating words: no flag, no fence
+                    pt[x] = occ_word(p.step + 1, occ[x]);
             }
         }
     }
@@ -557,7 +572,7 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
     extern __shared__ __align__(128) uint32_t sm[];
     const SelView v = sel_view(sm, p);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
-    const uint32_t* tin = reinterpret_cast<const uint32_t*>(p.region[p.me] + p.off_table) +
+    const uint64_t* tin = reinterpret_cast<const uint64_t*>(p.region[p.me] + p.off_table) +
                           uint64_t(p.tslot_in) * p.N * p.K + uint64_t(p.me) * p.K;
     trace_at(p, 0);
     tl_mark(p, 0, false);
@@ -573,16 +588,11 @@ __global__ void __launch_bounds__(kSelThreads) drb_sel_kernel(const __grid_const
         reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.sel_in) + tid);
 #pragma unroll 1
     for (uint32_t x = tid; x < p.K; x += kSelThreads)
-        v.occ[x] = __ldcg(tin + x);
+        v.occ[x] = occ_of(__ldcg(tin + x));
     const bool bad = __syncthreads_or(any_bad) != 0;  // usage_error before any draw (:44-47)
     if (warp != 0)
         return;
     sel_core(p, v, bad);
-    if (p.dbg & 512) {  // experiment: trigger dependents once every output is visible
-        __threadfence();
-        __syncwarp();
-        asm volatile("griddepcontrol.launch_dependents;");
-    }
     tl_mark(p, 0, true);
 }
 
@@ -616,11 +626,29 @@ __device__ void plan_core(const StepParams& p, const PlanView& v) {
     const uint32_t N = p.N, K = p.K, me = p.me, cap = p.cap, r = p.r;
     const uint32_t NK = N * K;
     const uint32_t MJ = plist_mj(N, r);
-    const uint32_t* tv1 = reinterpret_cast<const uint32_t*>(p.region[me] + p.off_table) +
+    // size rendezvous for v = i+1 (size_table.cpp:66-100 / engine.cpp:152): every word of
+    // every row at this version (own row from sel(i); peers' rows land over NVLink),
+    // bounded by timeout_ns
+    const uint64_t* tv1 = reinterpret_cast<const uint64_t*>(p.region[me] + p.off_table) +
                           uint64_t(p.tslot_out) * NK;
+    {
+        uint64_t t0 = 0;
 #pragma unroll 1
-    for (uint32_t x = tid; x < NK; x += T)
-        pre[x] = __ldcg(tv1 + x);
+        for (uint32_t x = tid; x < NK; x += T) {
+            uint64_t w = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
+            while (!occ_is(w, p.step + 1)) {
+                if (t0 == 0)
+                    t0 = globaltimer();
+                else if (globaltimer() - t0 > p.timeout_ns) {
+                    misc[0] = DRB_ERR_TRANSPORT;
+                    break;
+                }
+                __nanosleep(32);
+                w = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
+            }
+            pre[x] = occ_of(w);
+        }
+    }
     __syncthreads();
     trace_at(p, 6);
     const bool dead = st->error != 0;
@@ -714,9 +742,6 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
     uint32_t* misc = v.misc;
     PlanState* st = v.st;
     const uint32_t tid = threadIdx.x;
-    const uint32_t N = p.N, me = p.me;
-    const bool multi = (p.mode & kModePeers) && N > 1;
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[me]);
     trace_at(p, 5);
     tl_mark(p, 1, false);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // plan(i-1): the sampling counters
@@ -724,41 +749,9 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
         reinterpret_cast<uint64_t*>(st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(p.plan_in) + tid);
     if (tid == 0)
         misc[0] = 0;
-    // size rendezvous for v = i+1 (size_table.cpp:66-100 / engine.cpp:152): every peer's
-    // row of this version, bounded by timeout_ns; the own row came from sel(i)
-    if (multi && tid == 0) {
-        const uint64_t t0 = globaltimer();
-        for (uint32_t w = 0; w < N; ++w) {
-            if (w == me)
-                continue;
-            while (ld_acquire_sys(&hdr->occ_flag[w]) < p.step + 1) {
-                if (globaltimer() - t0 > p.timeout_ns) {
-                    misc[0] = DRB_ERR_TRANSPORT;
-                    break;
-                }
-                __nanosleep(32);
-            }
-        }
-    }
     __syncthreads();
-    plan_core(p, v);
-    if (p.dbg & 512) {
-        __threadfence();
-        __syncthreads();
-        asm volatile("griddepcontrol.launch_dependents;");
-    }
+    plan_core(p, v);  // (the size rendezvous is plan_core's versioned view load)
     tl_mark(p, 1, true);
-}
-
-// Spin (thread-level) until *flag >= want or the timeout; returns false on timeout.
-__device__ bool wait_flag(const uint64_t* flag, uint64_t want, uint64_t timeout_ns) {
-    const uint64_t t0 = globaltimer();
-    while (ld_acquire_sys(flag) < want) {
-        if (globaltimer() - t0 > timeout_ns)
-            return false;
-        __nanosleep(32);
-    }
-    return true;
 }
 
 __device__ __forceinline__ void mailbox_fail(const StepParams& p, uint32_t err) {
@@ -854,11 +847,13 @@ __device__ void copy_counts(const StepParams& p, const uint32_t* xraw) {
     }
 }
 
-// Multi-rank hand-off of the pushes, in copy(i) (CTA 0, warp 0):
-//   start (after griddepcontrol.wait: copy(i-1) complete, so are its stores into the peers'
-//     m'_i — kernel completion): pushdone[me] = i at every peer, after a system fence;
-//   end: wait until every peer announced pushdone >= i (their reps(i-1) rows of my m'_i
-//     landed) — m'_i is complete when copy(i) is.
+// Multi-rank hand-off of the pushes:
+//   copy(i) start (CTA 0, warp 0, after griddepcontrol.wait: copy(i-1) complete, so are its
+//     stores into the peers' m'_i — kernel completion): pushdone[me] = i at every peer,
+//     after a system fence;
+//   peers_wait(i), a one-warp kernel off the copy chain: every peer announced pushdone >= i
+//     (their reps(i-1) rows of my m'_i landed). The consumer's "m'_i ready" event follows it,
+//     so no copy ever waits on a peer's progress.
 __device__ void copy_announce_peers(const StepParams& p) {
     const uint32_t lane = threadIdx.x & 31;
     if (p.step == 0)
@@ -878,6 +873,11 @@ __device__ void copy_wait_peers(const StepParams& p) {
         ok = wait_flag(&hdr->pushdone[lane], p.step, p.timeout_ns);
     if (__any_sync(kFull, !ok) && lane == 0)
         mailbox_fail(p, DRB_ERR_TRANSPORT);
+}
+
+__global__ void peers_wait_kernel(const __grid_constant__ StepParams p) {
+    if (threadIdx.x < 32)
+        copy_wait_peers(p);
 }
 
 __device__ __forceinline__ uint8_t* push_dst(const StepParams& p, uint32_t dst, uint32_t next_slot) {
@@ -994,8 +994,6 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     }
     if (tid == 32)
         cta_mark(p, 6);
-    if (multi && blockIdx.x == 0 && warp == 0)
-        copy_wait_peers(p);
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
@@ -1258,8 +1256,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();  // all bulk stores of this CTA issued and sourced
-    if (multi && blockIdx.x == 0 && warp == 0)
-        copy_wait_peers(p);
     if (p.timeline) {
         __syncthreads();
         tl_mark(p, 2, true);
@@ -1276,7 +1272,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
 // fetched while the current selection runs, and nothing is launched per iteration. Every
 // decision is the same code as the three-kernel path (sel_core, plan_core, copy_parse, the
 // push-at-source copy), so the outputs are bit-identical.
-//   sel(k)   waits B(k-8) (W slot), plan(k-4) (table slot); multi-rank B(k-3) of every rank
+//   sel(k)   waits B(k-8) (W slot), plan(k-4) (table slot); multi-rank B(k-6) of every rank
 //            (the pushes into the m' slot that plan(k)'s requesters refill)
 //   plan(k)  waits sel(k), B(k-8) (X slot), peers' occupancy rows v=i+1
 //   A(k)     (batch -> m'_i) waits B(k-3) (bounded run-ahead)
@@ -1375,12 +1371,12 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
     }
     named_bar(1, kSelThreads);
     {  // state and the own occupancy row at the start of the run (written before the launch)
-        const uint32_t* tin = reinterpret_cast<const uint32_t*>(sp.region[me] + sp.off_table) +
+        const uint64_t* tin = reinterpret_cast<const uint64_t*>(sp.region[me] + sp.off_table) +
                               uint64_t(sp.tslot_in) * N * sp.K + uint64_t(me) * sp.K;
         if (tid < sizeof(SelState) / 8)
             reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.sel_in) + tid);
         for (uint32_t x = tid; x < sp.K; x += kSelThreads)
-            v.occ[x] = __ldcg(tin + x);
+            v.occ[x] = occ_of(__ldcg(tin + x));
         if (tid == 0)
             flag[2] = 0;
         named_bar(1, kSelThreads);
@@ -1394,10 +1390,10 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
         if (tid == 0) {
             if (k > 0)
                 run_patch(sp, rp, k);
-            bool ok = wait_seen(bdone, back(k, multi ? 2 : kListRing - 1), rp) && wait_seen(pdone, back(k, 3), rp);
-            for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-3) complete
-                if (w != me && sp.step >= 3)
-                    ok = run_wait(&hdr->pushdone[w], sp.step - 2, rp, true);
+            bool ok = wait_seen(bdone, back(k, multi ? kAugRing - 1 : kListRing - 1), rp) && wait_seen(pdone, back(k, 3), rp);
+            for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-6) complete (m' slot)
+                if (w != me && sp.step >= kAugRing)
+                    ok = run_wait(&hdr->pushdone[w], sp.step - kAugRing + 1, rp, true);
             flag[1] = ok ? 0u : 1u;
             flag[0] = flag[2];  // "bad" of m_k's labels
             flag[3] = 0;
@@ -1435,8 +1431,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
 
 // CTA 1: the plan chain.
 __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
-    const uint32_t tid = threadIdx.x, N = rp.base.N, me = rp.base.me;
-    const bool multi = (rp.base.mode & kModePeers) && N > 1;
+    const uint32_t tid = threadIdx.x;
     const PlanView v = plan_view(sm, rp.base);
     if (tid == 0) {
         sp = rp.base;
@@ -1446,17 +1441,12 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
     if (tid < sizeof(PlanState) / 8)
         reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.plan_in) + tid);
     SeenFlag sdone{&rp.ctl->sel_done, 0}, bdone{&rp.ctl->b_done, 0};
-    const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(rp.base.region[me]);
 #pragma unroll 1
     for (uint64_t k = 0; k < rp.steps; ++k) {
         if (tid == 0) {
             if (k > 0)
                 run_patch(sp, rp, k);
-            bool ok = wait_seen(sdone, k + 1, rp) && wait_seen(bdone, back(k, kListRing - 1), rp);
-            // size rendezvous v = i+1 (size_table.cpp:66-100): every peer's row
-            for (uint32_t w = 0; ok && multi && w < N; ++w)
-                if (w != me)
-                    ok = run_wait(&hdr->occ_flag[w], sp.step + 1, rp, true);
+            const bool ok = wait_seen(sdone, k + 1, rp) && wait_seen(bdone, back(k, kListRing - 1), rp);
             flag[1] = ok ? 0u : 1u;
             v.misc[0] = 0;
         }
@@ -1958,6 +1948,11 @@ int launch_run(const RunParams& rp, uint32_t grid, void* stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, drb_run_kernel, rp) == cudaSuccess ? 0 : -1;
+}
+
+int launch_peers_wait(const StepParams& p, void* stream) {
+    peers_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(p);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int copy_tma_occupancy(uint32_t smem_bytes, int* out) {

@@ -46,7 +46,8 @@ check(lib.drb_rb_timeline_read(buf.h, None, C.byref(n)))
 W = 32 + 16 * 160  # kTlStride words per step (drb_internal.cuh)
 t = np.zeros(n.value * W, np.uint64)
 check(lib.drb_rb_timeline_read(buf.h, t.ctypes.data, C.byref(n)))
-t = t.reshape(n.value, W)[:, :6].reshape(n.value, 3, 2).astype(np.int64)
+full = t.reshape(n.value, W).astype(np.int64)
+t = full[:, :6].reshape(n.value, 3, 2)
 rows = [(first + i) % n.value for i in range(STEPS)]
 mine = np.stack([t[row] for row in rows])  # [STEPS, 3, 2]
 allt = [None] * world
@@ -70,4 +71,18 @@ if rank == 0:
             m = allt[w][i] - t0[w]
             cells.append(" ".join(f"{m[k,0]/1e3:6.1f}-{m[k,1]/1e3:6.1f}" for k in range(3)))
         print(f"{first+i:4d} | " + " | ".join(cells))
+# per-CTA copy stamps of this rank (slots as in tools/timeline.py), medians over steps
+CN = {0: "start", 2: "A issued", 11: "A 1st land", 5: "A m' stored", 1: "lists", 10: "B wait", 3: "A wait+ready",
+      4: "B issued", 9: "B done", 6: "A done", 7: "end"}
+cta = full[:, 32:].reshape(n.value, 160, 16)
+grid = int((cta[rows[8], :, 0] > 0).sum())
+rel = np.array([(cta[row, :grid].astype(np.float64) - cta[row, :grid, 0].min()) / 1e3 for row in rows[8:]])
+lines = [f"rank {rank} copy CTA stamps (us from first CTA start, median step, p50 / p90 over CTAs):"]
+for k, nm in CN.items():
+    v = np.median(rel[:, :, k], axis=0)
+    lines.append(f"  {nm:12s} {np.percentile(v, 50):6.2f} {np.percentile(v, 90):6.2f}")
+allc = [None] * world
+dist.all_gather_object(allc, "\n".join(lines))
+if rank == 0:
+    print("\n".join(allc))
 dist.destroy_process_group()
