@@ -326,9 +326,9 @@ def main():
     e2e_value = (b + r) * N * e2e_steps / e2e_s
     eng.shutdown()
 
-    persistent = os.environ.get("DRB_PERSIST", "0") == "1" and not args.no_graph
+    persistent = os.environ.get("DRB_PERSIST", "1") != "0" and not args.no_graph
     # our kernels inside the timed region: sel + plan + copy per step (three-kernel path,
-    # captured in one CUDA graph), or one cooperative launch for the whole run (DRB_PERSIST=1)
+    # captured in one CUDA graph, DRB_PERSIST=0), or one cooperative launch for the whole run
     launches = 1 if persistent else 3 * args.steps
     launch_mode = "persistent-cooperative" if persistent else ("cuda-graph" if not args.no_graph else "direct")
     peak, peak_kind = peaks()

@@ -168,8 +168,8 @@ struct drb_rb {
     uint64_t ver0 = 0;                // engine: table version / state parities at start()
     uint32_t sel_par0 = 0, plan_par0 = 0;
     uint32_t dbg_bits = 0;            // DRB_DBG experiment bits (0 in production)
-    bool use_persist = false;         // drb_rb_run as one persistent cooperative launch (DRB_PERSIST=1)
-    bool last_run_persistent = false; // the latest drb_rb_run was one persistent launch          // drb_rb_run as one persistent cooperative launch; DRB_PERSIST=0 off
+    bool use_persist = true;          // drb_rb_run as one persistent cooperative launch (DRB_PERSIST=0 off)
+    bool last_run_persistent = false; // the latest drb_rb_run was one persistent launch
     RunCtl* runctl = nullptr;         // device counters of the persistent run
     cudaEvent_t run_end = nullptr;
     uint64_t prewaited = 0;           // 1 + the iteration whose sel/plan the copy stream already waited for
@@ -1216,6 +1216,14 @@ drb_status drb_rb_synchronize(drb_rb* h) {
     DRB_REQUIRE(h);
     return guarded([&] {
         device_guard g(h->cfg.device);
+        if (h->dbg_bits & 1024) {  // diagnostics of the last persistent run
+            cudaDeviceSynchronize();
+            RunCtl rc{};
+            cudaMemcpy(&rc, h->runctl, sizeof rc, cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "drb run: sel %llu plan %llu b %llu error %u where site %u k %u\n",
+                         (unsigned long long)rc.sel_done, (unsigned long long)rc.plan_done,
+                         (unsigned long long)rc.b_done, rc.error, rc.where >> 24, rc.where & 0xffffff);
+        }
         cuda_check(cudaStreamSynchronize(h->stream), "sync");
         cuda_check(cudaStreamSynchronize(h->s_sel), "sync");
         cuda_check(cudaStreamSynchronize(h->s_plan), "sync");

@@ -156,7 +156,8 @@ struct alignas(64) RunCtl {
     uint64_t plan_done;  // plan of k finished (X_i)
     uint64_t b_done;     // every copy CTA's slab writes and pushes of k are complete (in order)
     uint32_t error;      // sticky: a wait timed out -> every role leaves its loop
-    uint32_t pad[9];
+    uint32_t where;      // diagnostics: the wait that failed first (site << 24 | k)
+    uint32_t pad[8];
     uint32_t ticket[8];  // copy-CTA arrivals of iteration k in slot k % 8 (CTAs drift < 8 iterations)
 };
 
@@ -174,7 +175,7 @@ struct RunParams {
     RunCtl* ctl;
     uint32_t ring, n, sel_par0, plan_par0, pw, ww, copy_ctas, pad;
 };
-constexpr uint32_t kRunThreads = 32 * (kMaxWorld + 1);  // >= plan_threads(N), >= kSelThreads
+constexpr uint32_t kRunThreads = 32 * (kMaxWorld + 2);  // plan_threads(N) + a helper warp, >= kSelThreads
 
 // Push list X_i, plan(i) -> copy(i). u32 words:
 //   [0] cnt      — |reps_me(i)|: representative rows of my m'_{i+1}
@@ -262,25 +263,39 @@ __host__ __device__ inline TmaSmem tma_smem(uint32_t N, uint32_t r, uint32_t nma
 // label buffer), plan, and the copy role's lists, barriers, A ring and B arena (byte offsets).
 // At least kSoloSmem so exactly one CTA lands on each SM.
 struct RunSmem {
-    uint32_t lists2, prevw, paddr, bars, ring_a, arena, arena_bytes, bytes;
+    uint32_t bars, ring_a, wrows, flags;  // shared by the copy role's warps
+    uint32_t xraw[2], wraw[2], jsrc[2], misc[2], paddr[2], arena[2];  // per B warp (k even / odd)
+    uint32_t arena_bytes, bytes;
 };
 __host__ __device__ inline RunSmem run_smem(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax) {
     RunSmem s{};
-    const uint32_t lists = copy_smem(N, r, nmax).words * 4;
-    const uint32_t lw = (plist_words(N, r) + wlist_words(nmax)) * 4;  // second list buffer
-    s.lists2 = (lists + 15u) & ~15u;
-    s.prevw = (s.lists2 + lw + 15u) & ~15u;
-    s.paddr = (s.prevw + nmax * 4u + 15u) & ~15u;  // per B piece: source, destination (u64)
-    s.bars = (s.paddr + 16u * (plist_mj(N, r) + nmax) + 127u) & ~127u;
-    s.ring_a = s.bars + 128u;
-    s.arena = s.ring_a + kTmaStagesA * kTmaChunk;
-    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax) * 4, plan_b = plan_smem(N, K, r).words * 4;
+    const uint32_t MJ = plist_mj(N, r);
+    uint32_t off = 0;
+    auto take = [&](uint32_t bytes, uint32_t align) {
+        off = (off + align - 1) / align * align;
+        const uint32_t at = off;
+        off += bytes;
+        return at;
+    };
+    s.bars = take(128, 128);
+    s.flags = take(128, 16);
+    s.wrows = take(4 * (nmax + 1) * 4, 16);  // W_k's slab rows, slot k % 4 (count first)
+    for (int w = 0; w < 2; ++w) {
+        s.xraw[w] = take(plist_words(N, r) * 4, 16);
+        s.wraw[w] = take(wlist_words(nmax) * 4, 16);
+        s.jsrc[w] = take(MJ * 4, 16);
+        s.misc[w] = take(32 * 4, 16);
+        s.paddr[w] = take(16 * (MJ + nmax), 16);
+    }
+    s.ring_a = take(kTmaStagesA * kTmaChunk, 128);
+    const uint32_t want = 200u * 1024u;  // total target; the two arenas take what is left
+    const uint32_t left = want > off + 2 * 16384u ? want - off : 2 * 16384u;
+    s.arena_bytes = (left / 2) & ~127u;
+    s.arena[0] = take(s.arena_bytes, 128);
+    s.arena[1] = take(s.arena_bytes, 128);
+    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax + 8) * 4, plan_b = plan_smem(N, K, r).words * 4;
     const uint32_t ctl = sel_b > plan_b ? sel_b : plan_b;
-    const uint32_t want = 200u * 1024u;  // total target; the arena takes what the rest leaves
-    s.arena_bytes = want > s.arena + 16384u ? want - s.arena : 16384u;
-    s.bytes = s.arena + s.arena_bytes;
-    if (s.bytes < ctl)
-        s.bytes = ctl;
+    s.bytes = off > ctl ? off : ctl;
     if (s.bytes < kSoloSmem)
         s.bytes = kSoloSmem;
     return s;

@@ -614,14 +614,23 @@ __device__ __forceinline__ PlanView plan_view(uint32_t* sm, const StepParams& p)
     return v;
 }
 
-// plan(i) after the size rendezvous (all threads of the CTA, blockDim >= 32*(N+1)): the view
+// __syncthreads (bar 0) or a named barrier over the first `threads` threads
+__device__ __forceinline__ void cta_bar(uint32_t bar, uint32_t threads) {
+    if (bar == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(threads) : "memory");
+}
+
+// plan(i) after the size rendezvous (threads [0, T), T >= 32*(N+1), synchronising on barrier
+// `bar` — 0 for __syncthreads): the view
 // v=i+1 from the table, S4 for every requester (p.plan_out and *v.st updated in place),
 // labels of m'_{i+1}'s reps, the push list X_i. v.misc[0] = rendezvous status.
-__device__ void plan_core(const StepParams& p, const PlanView& v) {
+__device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, uint32_t bar) {
     uint32_t *pre = v.pre, *pfx = v.pfx, *plan = v.plan, *cnt = v.cnt, *acc = v.acc, *misc = v.misc,
              *maskP = v.maskP;
     PlanState* st = v.st;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, T = blockDim.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t N = p.N, K = p.K, me = p.me, cap = p.cap, r = p.r;
     const uint32_t NK = N * K;
@@ -649,7 +658,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v) {
             pre[x] = occ_of(w);
         }
     }
-    __syncthreads();
+    cta_bar(bar, T);
     trace_at(p, 6);
     const bool dead = st->error != 0;
     uint32_t* out = p.plist_out;
@@ -676,7 +685,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v) {
     } else if (warp == 0) {
         warp_exclusive_scan(pre, NK, pfx);
     }
-    __syncthreads();
+    cta_bar(bar, T);
     if (warp >= 1 && warp <= N) {
         const uint32_t q = warp - 1;
         warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
@@ -688,7 +697,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v) {
                 al[p.nmax + j] = plan[3 * (q * r + j) + 1];
         }
     }
-    __syncthreads();
+    cta_bar(bar, T);
     trace_at(p, 7);
     // Push list X_i for copy(i): every entry (q, j) of plan(i), over all requesters q (own
     // plan included), whose slot this rank owns, in (q, j) order. copy(i) stores the slot's
@@ -708,7 +717,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v) {
         if (lane == 0)
             maskP[base >> 5] = m;
     }
-    __syncthreads();
+    cta_bar(bar, T);
     for (uint32_t base = warp * 32; base < NR; base += T) {
         const unsigned m = maskP[base >> 5];
         if (!((m >> lane) & 1u))
@@ -750,7 +759,7 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
     if (tid == 0)
         misc[0] = 0;
     __syncthreads();
-    plan_core(p, v);  // (the size rendezvous is plan_core's versioned view load)
+    plan_core(p, v, blockDim.x, 0);  // (the size rendezvous is plan_core's versioned view load)
     tl_mark(p, 1, true);
 }
 
@@ -1296,7 +1305,8 @@ __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, 
         if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
             return false;
         if (globaltimer() - t0 > rp.base.timeout_ns) {
-            atomicExch(&rp.ctl->error, DRB_ERR_TRANSPORT);
+            if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_TRANSPORT)) == 0)
+                rp.ctl->where = (9u << 24) | uint32_t(want & 0xffffff);
             if (rp.base.mailbox) {
                 volatile uint32_t* mb = rp.base.mailbox;
                 mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
@@ -1354,7 +1364,47 @@ __device__ __forceinline__ bool wait_seen(SeenFlag& s, uint64_t want, const RunP
     return true;
 }
 
-// CTA 0: the sel chain. Warp 0 runs sel(k) while warps 1-3 fetch the labels of m_{k+1}.
+__device__ __forceinline__ void st_release_cta(volatile unsigned long long* p, uint64_t v) {
+    asm volatile("st.release.cta.shared.u64 [%0], %1;" ::"r"(smem_u32(const_cast<unsigned long long*>(p))), "l"(v)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_cta(const volatile unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.cta.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(const_cast<unsigned long long*>(p)))
+                 : "memory");
+    return v;
+}
+
+// A publisher warp (lane 0) for a control CTA: whenever the compute warps hand over
+// iteration k (smem `ready` = k+1, release at CTA scope), it release-stores the run counter
+// (`done` = k+1, GPU scope — this is the store that waits for the compute warps' global
+// writes to be acknowledged, so they don't) and refreshes the counters the compute warps
+// check next (`seen`, acquire).
+__device__ void run_publisher(const RunParams& rp, volatile unsigned long long* ready, uint64_t* done,
+                              volatile unsigned long long* seen, const uint64_t* s0, const uint64_t* s1) {
+    for (uint64_t k = 0; k < rp.steps; ++k) {
+        uint64_t t0 = 0;
+        for (uint32_t spin = 0; ld_acquire_cta(ready) < k + 1; ++spin) {
+            if ((spin & 63) == 63) {
+                if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+                    return;
+                const uint64_t now = globaltimer();
+                if (t0 == 0)
+                    t0 = now;
+                else if (now - t0 > 2 * rp.base.timeout_ns)
+                    return;
+            }
+            seen[0] = ld_acquire_gpu(s0);  // keep the compute warps' view fresh while waiting
+            seen[1] = ld_acquire_gpu(s1);
+        }
+        st_release_gpu(done, k + 1);
+        seen[0] = ld_acquire_gpu(s0);
+        seen[1] = ld_acquire_gpu(s1);
+    }
+}
+
+// CTA 0: the sel chain. Warp 0 runs sel(k), warps 2-3 fetch the labels of m_{k+1}, warp 1
+// publishes sel_done and keeps b_done / plan_done fresh in shared memory.
 __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     if (tid >= kSelThreads)
@@ -1365,9 +1415,14 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
     SelView v = sel_view(sm, b);
     uint32_t* lab2 = sm + sel_smem(b.K, b.nmax).words;  // second label buffer (prefetch)
     uint32_t* labs[2] = {v.lab, lab2};
+    volatile unsigned long long* seen =  // [0] b_done, [1] plan_done as last loaded; [2] ready
+        reinterpret_cast<volatile unsigned long long*>(sm + ((sel_smem(b.K, b.nmax).words + b.nmax + 1) & ~1u));
     if (tid == 0) {
         sp = b;
         run_patch(sp, rp, 0);
+        seen[0] = 0;
+        seen[1] = 0;
+        seen[2] = 0;
     }
     named_bar(1, kSelThreads);
     {  // state and the own occupancy row at the start of the run (written before the launch)
@@ -1382,15 +1437,28 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
         named_bar(1, kSelThreads);
         if (sel_load_labels(sp, v, kSelThreads))
             atomicOr(&flag[2], 1u);
+        named_bar(1, kSelThreads);
     }
-    SeenFlag bdone{&rp.ctl->b_done, 0}, pdone{&rp.ctl->plan_done, 0};
+    if (warp == 1) {
+        if (tid == 32)
+            run_publisher(rp, seen + 2, &rp.ctl->sel_done, seen, &rp.ctl->b_done, &rp.ctl->plan_done);
+        return;
+    }
     const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(b.region[me]);
 #pragma unroll 1
-    for (uint64_t k = 0; k < rp.steps; ++k) {
+    for (uint64_t k = 0; k < rp.steps; ++k) {  // warps 0, 2, 3 (barrier 1, 96 threads)
         if (tid == 0) {
+            run_mark(rp, rp.i0 + k, 0);
             if (k > 0)
                 run_patch(sp, rp, k);
-            bool ok = wait_seen(bdone, back(k, multi ? kAugRing - 1 : kListRing - 1), rp) && wait_seen(pdone, back(k, 3), rp);
+            // W slot (k-8) / m' slot (multi, k-6) / table slot (plan(k-4)) free
+            const uint64_t wb = back(k, multi ? kAugRing - 1 : kListRing - 1), wp = back(k, 3);
+            bool ok = true;
+            if (seen[0] < wb)
+                ok = run_wait(&rp.ctl->b_done, wb, rp, false);
+            if (ok && seen[1] < wp)
+                ok = run_wait(&rp.ctl->plan_done, wp, rp, false);
+            run_mark(rp, rp.i0 + k, 1);
             for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-6) complete (m' slot)
                 if (w != me && sp.step >= kAugRing)
                     ok = run_wait(&hdr->pushdone[w], sp.step - kAugRing + 1, rp, true);
@@ -1398,24 +1466,27 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             flag[0] = flag[2];  // "bad" of m_k's labels
             flag[3] = 0;
         }
-        named_bar(1, kSelThreads);
+        named_bar(1, 96);
         if (flag[1])
             return;
         v.lab = labs[k & 1];
         if (warp == 0) {
             tl_mark(sp, 0, false);
             trace_at(sp, 0);
+            if (tid == 0)
+                run_mark(rp, rp.i0 + k, 2);
             sel_core(sp, v, flag[0] != 0);
             __syncwarp();
-            if (tid == 0) {  // release: the warp's W_i / state / row stores precede it
-                st_release_gpu(&rp.ctl->sel_done, k + 1);
+            if (tid == 0) {
+                st_release_cta(seen + 2, k + 1);  // hand sel(k) to the publisher
+                run_mark(rp, rp.i0 + k, 3);
                 tl_mark(sp, 0, true);
             }
-        } else if (k + 1 < rp.steps) {  // labels of m_{k+1}
+        } else if (k + 1 < rp.steps) {  // warps 2-3: labels of m_{k+1}
             const uint64_t slot = (rp.first + k + 1) % rp.ring;
             const uint32_t* lp = rp.labels + slot * rp.label_stride;
             int bad = 0;
-            for (uint32_t x = tid - 32; x < rp.n; x += kSelThreads - 32) {
+            for (uint32_t x = tid - 64; x < rp.n; x += kSelThreads - 64) {
                 const uint32_t l = __ldg(lp + x);
                 labs[(k + 1) & 1][x] = l;
                 bad |= l >= sp.K;
@@ -1423,43 +1494,65 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             if (bad)
                 atomicOr(&flag[3], 1u);
         }
-        named_bar(1, kSelThreads);
-        if (tid == 0)
+        named_bar(1, 96);
+        if (tid == 0) {
             flag[2] = flag[3];
+            run_mark(rp, rp.i0 + k, 4);
+        }
     }
 }
 
-// CTA 1: the plan chain.
+// CTA 1: the plan chain. plan_core runs on the first plan_threads(N) threads (named barrier
+// 3); a helper warp publishes plan_done and keeps sel_done / b_done fresh.
 __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const PlanView v = plan_view(sm, rp.base);
+    const uint32_t T = 32 * (rp.base.N + 1 < 3 ? 3 : rp.base.N + 1);  // plan_threads(N) <= kRunThreads - 32
+    const uint32_t helper = kRunThreads / 32 - 1;
+    volatile unsigned long long* seen = reinterpret_cast<volatile unsigned long long*>(flag + 2);  // [0] sel, [1] b, [2] ready
     if (tid == 0) {
         sp = rp.base;
         run_patch(sp, rp, 0);
+        seen[0] = 0;
+        seen[1] = 0;
+        seen[2] = 0;
     }
     __syncthreads();
+    if (warp == helper) {
+        if ((tid & 31) == 0)
+            run_publisher(rp, seen + 2, &rp.ctl->plan_done, seen, &rp.ctl->sel_done, &rp.ctl->b_done);
+        return;
+    }
+    if (tid >= T)
+        return;
     if (tid < sizeof(PlanState) / 8)
         reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.plan_in) + tid);
-    SeenFlag sdone{&rp.ctl->sel_done, 0}, bdone{&rp.ctl->b_done, 0};
 #pragma unroll 1
     for (uint64_t k = 0; k < rp.steps; ++k) {
         if (tid == 0) {
+            run_mark(rp, rp.i0 + k, 0);
             if (k > 0)
                 run_patch(sp, rp, k);
-            const bool ok = wait_seen(sdone, k + 1, rp) && wait_seen(bdone, back(k, kListRing - 1), rp);
+            bool ok = true;
+            if (seen[0] < k + 1)  // sel(k)
+                ok = run_wait(&rp.ctl->sel_done, k + 1, rp, false);
+            if (ok && seen[1] < back(k, kListRing - 1))  // X slot: B(k-8) complete
+                ok = run_wait(&rp.ctl->b_done, back(k, kListRing - 1), rp, false);
+            run_mark(rp, rp.i0 + k, 1);
             flag[1] = ok ? 0u : 1u;
             v.misc[0] = 0;
         }
-        __syncthreads();
+        cta_bar(3, T);
         if (flag[1])
             return;
         tl_mark(sp, 1, false);
         trace_at(sp, 5);
-        plan_core(sp, v);
-        __syncthreads();
-        if (tid == 0) {  // release after the CTA barrier: X_i and the state precede it
-            st_release_gpu(&rp.ctl->plan_done, k + 1);
+        plan_core(sp, v, T, 3);
+        cta_bar(3, T);
+        if (tid == 0) {
+            st_release_cta(seen + 2, k + 1);  // hand plan(k) to the publisher
             tl_mark(sp, 1, true);
+            run_mark(rp, rp.i0 + k, 3);
         }
     }
 }
@@ -1493,110 +1586,72 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
 // every read and write of a given slab byte happens in this one CTA, in program order:
 // there is no grid-wide hand-off between iterations. The one cross-iteration hazard (a
 // slot pushed in k that B(k-1) wrote) waits for this CTA's previous stores to complete.
-__device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams& sp) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (warp >= 2)
-        return;
+// Cross-warp progress of a copy CTA's B engines (shared memory, per iteration parity).
+struct BFlags {
+    unsigned long long landed[2];    // k+1: B(k)'s loads landed (its reads are done)
+    unsigned long long complete[2];  // k+1: B(k)'s stores complete
+    unsigned long long parsed[4];    // k+1 in slot k % 4: W_k's slab rows published in wrows[k % 4]
+    unsigned long long counted;      // k+1: m'_i's counts written (part 0)
+};
+// Bounded like every other wait: gives up once the run failed or after timeout_ns (then
+// fails the run, recording `site` and the iteration), so no role can spin forever.
+__device__ bool smem_wait_ge(const volatile unsigned long long* f, uint64_t want, const RunParams& rp,
+                             uint32_t site, uint64_t k) {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0; *f < want; ++spin) {
+        if ((spin & 255) == 255) {
+            if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+                return false;
+            const uint64_t now = globaltimer();
+            if (t0 == 0)
+                t0 = now;
+            else if (now - t0 > rp.base.timeout_ns) {
+                if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
+                    rp.ctl->where = (site << 24) | uint32_t(k & 0xffffff);
+                return false;
+            }
+        }
+        __nanosleep(20);
+    }
+    return true;
+}
+
+// One B engine (a warp) of a copy CTA, for the iterations k = first, first+2, ...: the W_k
+// writes and X_k pushes on this CTA's byte column [c0, c1). The two B warps alternate, so
+// B(k+1) issues its loads while B(k) drains; what must stay ordered between consecutive
+// iterations on the same slab bytes is ordered through BFlags:
+//   a slot pushed in k that W_{k-1} wrote        -> B(k-1)'s stores complete first
+//   a W_k row that X_{k-1} read                  -> B(k-1)'s loads landed before k's stores
+//   a W_k row that W_{k-1} also wrote            -> B(k-1)'s stores complete first
+__device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, StepParams& sp, uint32_t wsel) {
+    const uint32_t lane = threadIdx.x & 31;
     const StepParams& b = rp.base;
-    const CopySmem L = copy_smem(b.N, b.r, b.nmax);
-    uint32_t* xraw = sm + L.xraw;
-    uint32_t* wraw = sm + L.wraw;
-    uint32_t* jsrc = sm + L.jsrc;
-    int* rowmap = reinterpret_cast<int*>(sm + L.rowmap);
-    uint32_t* misc = sm + L.misc;
-    const RunSmem R = run_smem(b.N, b.K, b.r, b.nmax);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm) + R.bars);
-    uint8_t* ringA = reinterpret_cast<uint8_t*>(sm) + R.ring_a;
-    uint8_t* arena = reinterpret_cast<uint8_t*>(sm) + R.arena;
-    uint32_t* prevw = sm + R.prevw;  // slab rows of W_{k-1}
+    uint8_t* base8 = reinterpret_cast<uint8_t*>(sm);
+    uint32_t* xraw = reinterpret_cast<uint32_t*>(base8 + R.xraw[wsel]);
+    uint32_t* wraw = reinterpret_cast<uint32_t*>(base8 + R.wraw[wsel]);
+    uint32_t* jsrc = reinterpret_cast<uint32_t*>(base8 + R.jsrc[wsel]);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(base8 + R.misc[wsel]);
+    uint64_t* paddr = reinterpret_cast<uint64_t*>(base8 + R.paddr[wsel]);
+    uint8_t* arena = base8 + R.arena[wsel];
+    uint32_t* wrows = reinterpret_cast<uint32_t*>(base8 + R.wrows);
+    volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
+    uint64_t* barB = reinterpret_cast<uint64_t*>(base8 + R.bars) + kTmaStagesA + wsel;
+    volatile uint32_t* ready = misc + 6;
     const uint32_t part = blockIdx.x - 2, parts = rp.copy_ctas;
     const uint64_t S = b.S;
     const bool multi = (b.mode & kModePeers) && b.N > 1;
-    const uint32_t CH = kTmaChunk;
-    if (tid == 0 || tid == 32) {
-        const uint32_t b0 = tid == 0 ? kTmaStagesA : 0, b1 = tid == 0 ? kTmaStagesA + 1 : kTmaStagesA;
-        for (uint32_t x = b0; x < b1; ++x)
-            mbar_init(bars + x, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (warp == 1) {
-        // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
-        if (lane != 0)
-            return;
-        const uint64_t a16 = (uint64_t(rp.n) * S) >> 4;
-        const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
-        const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
-        const uint32_t row0 = b.nmax - rp.n;
-        uint32_t ph_bits = 0;  // phase of each A barrier
-        SeenFlag bdone{&rp.ctl->b_done, 0};
-#pragma unroll 1
-        for (uint64_t k = 0; k < rp.steps; ++k) {
-            if (!wait_seen(bdone, back(k, 2), rp))
-                break;
-            const uint64_t i = rp.i0 + k;
-            run_mark(rp, i, 2);
-            // m'_i's rows were last written by A(k-3): those stores are complete (every bulk
-            // group but the newest — A(k-1)'s last window — has finished)
-            asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
-            const uint8_t* batch = rp.batches + ((rp.first + k) % rp.ring) * rp.batch_stride;
-            uint8_t* dst = b.region[b.me] + b.off_aug + (i % kAugRing) * b.aug_slot_bytes + uint64_t(row0) * S;
-            for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
-                const uint32_t w1 = min(nA, w0 + kTmaStagesA);
-                bulk_wait_read_all();  // the ring's previous window has been stored
-                for (uint32_t x = w0; x < w1; ++x) {
-                    const uint64_t off = alo + uint64_t(x) * CH;
-                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
-                    mbar_expect_tx(bars + (x - w0), len);
-                    bulk_load(ringA + (x - w0) * CH, batch + off, len, bars + (x - w0));
-                }
-                for (uint32_t x = w0; x < w1; ++x) {
-                    const uint64_t off = alo + uint64_t(x) * CH;
-                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
-                    if (!mbar_wait(bars + (x - w0), take_phase(ph_bits, x - w0), rp.base.timeout_ns))
-                        atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
-                    bulk_store(dst + off, ringA + (x - w0) * CH, len);
-                }
-                bulk_commit();
-            }
-            run_mark(rp, i, 5);
-        }
-        bulk_wait_all();
-        return;
-    }
-    // ---- warp 0: lists, counts, B engine on this CTA's column ----------------------------
-    // The lists of k+1 are staged (cp.async, second buffer) while B(k) moves bytes; every
-    // lane issues its own pieces' bulk copies (addresses resolved lane-parallel first).
-    volatile uint32_t* ready = misc + 6;
-    uint64_t* barB = bars + kTmaStagesA;
-    uint64_t* paddr = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm) + R.paddr);
-    uint32_t* xbuf[2] = {xraw, reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(sm) + R.lists2)};
-    uint32_t* wbuf[2] = {wraw, xbuf[1] + plist_words(b.N, b.r)};
-    uint32_t phB = 0;
     const uint64_t c16 = S >> 4;
     const uint64_t c0 = (c16 * part / parts) << 4, c1 = (c16 * (part + 1) / parts) << 4;
     const uint32_t clen = static_cast<uint32_t>(c1 - c0);
-    const uint32_t per_win = clen ? R.arena_bytes / clen : 0;  // pieces per arena window
-    const uint32_t pw = plist_words(b.N, b.r), ww = wlist_words(b.nmax);
+    const uint32_t per_win = clen ? R.arena_bytes / clen : 0;
+    const uint32_t pw = plist_words(b.N, b.r), ww = wlist_words(b.nmax), nslot = b.nmax + 1;
     SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0};
-    uint32_t nprev = 0;
-    auto stage = [&](uint64_t kk) {  // cp.async of iteration kk's X / W lists into buffer kk & 1
-        const uint64_t i = rp.i0 + kk;
-        const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
-        const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
-        uint32_t* xd = xbuf[kk & 1];
-        uint32_t* wd = wbuf[kk & 1];
-        for (uint32_t x = lane; x < pw; x += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xd + x)), "l"(xs + x) : "memory");
-        for (uint32_t x = lane; x < ww; x += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wd + x)), "l"(ws + x) : "memory");
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
+    uint32_t phB = 0;
+    int64_t prev_k = -1;  // this warp's previous iteration (stores not yet drained)
     if (lane == 0)
         sp = b;
-    bool staged = false;  // lists of the current k already issued
 #pragma unroll 1
-    for (uint64_t k = 0; k < rp.steps; ++k) {
+    for (uint64_t k = wsel; k < rp.steps; k += 2) {
         bool ok = true;
         if (lane == 0) {
             run_patch(sp, rp, k);
@@ -1604,32 +1659,64 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams& sp)
         }
         if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
             break;
-        __syncwarp();  // sp (lane 0) visible to the warp
+        __syncwarp();
         tl_mark(sp, 2, false);
         if (lane == 0)
             cta_mark(sp, 0);
-        if (!staged)
-            stage(k);
-        uint32_t* xr = xbuf[k & 1];
-        uint32_t* wr = wbuf[k & 1];
-        copy_parse(sp, xr, wr, jsrc, rowmap, misc, ready, true, true, false);
-        // next iteration's lists, if sel/plan already finished it (cached counters)
-        staged = false;
-        if (k + 1 < rp.steps) {
-            bool nx = false;
-            if (lane == 0)
-                nx = sdone.seen >= k + 2 && pdone.seen >= k + 2;
-            if (__shfl_sync(kFull, nx ? 1 : 0, 0)) {
-                stage(k + 1);
-                staged = true;
-            }
-        }
-        if (part == 0)
-            copy_counts(sp, xr);
+        const uint64_t i = rp.i0 + k;
+        const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
+        const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
+        for (uint32_t x = lane; x < pw; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xraw + x)), "l"(xs + x) : "memory");
+        for (uint32_t x = lane; x < ww; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wraw + x)), "l"(ws + x) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        copy_parse(sp, xraw, wraw, jsrc, nullptr, misc, ready, true, true, false);
         const uint32_t nj = misc[0], nw = misc[1];
+        uint32_t* wk = wrows + (k & 3) * nslot;  // publish W_k's rows for B(k+1)
+        for (uint32_t t = lane; t < nw; t += 32)
+            wk[1 + t] = wraw[3 + 2 * t];
+        if (lane == 0)
+            wk[0] = nw;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0)
+            fl->parsed[k & 3] = k + 1;
+        if (part == 0) {  // m'_i's counts after m'_{i-1}'s (repcnt hand-off)
+            if (lane == 0 && k > 0)
+                smem_wait_ge(&fl->counted, k, rp, 1, k);
+            __syncwarp();
+            copy_counts(sp, xraw);
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0)
+                fl->counted = k + 1;
+        }
+        if (lane == 0)
+            cta_mark(sp, 10);
+        // W_{k-1} (the other warp's) for the hazard checks
+        bool push_hz = false, w_hz = false;
+        if (k > 0) {
+            if (lane == 0)
+                smem_wait_ge(&fl->parsed[(k - 1) & 3], k, rp, 2, k);
+            __syncwarp();
+            if (lane == 0)
+                cta_mark(sp, 11);
+            const uint32_t* wp = wrows + ((k - 1) & 3) * nslot;
+            const uint32_t np = wp[0];
+            for (uint32_t x = lane; x < nj; x += 32) {
+                const uint32_t s_ = jsrc[x];
+                if (!(s_ >> 31))
+                    for (uint32_t t = 0; t < np; ++t)
+                        push_hz |= wp[1 + t] == s_;
+            }
+            for (uint32_t t = lane; t < nw; t += 32)
+                for (uint32_t u = 0; u < np; ++u)
+                    w_hz |= wp[1 + u] == wk[1 + t];
+            push_hz = __any_sync(kFull, push_hz);
+            w_hz = __any_sync(kFull, w_hz);
+        }
         const uint32_t pieces = clen ? nj + nw : 0;
-        // piece addresses (lane-parallel); a slot pushed now that B(k-1) wrote is a hazard
-        bool hazard = false;
         {
             const uint8_t* batch = sp.batch;
             uint8_t* slab = reinterpret_cast<uint8_t*>(sp.slab);
@@ -1640,34 +1727,37 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams& sp)
                 if (x < nj) {
                     const uint32_t s_ = jsrc[x];
                     src = ((s_ >> 31) ? batch + uint64_t(s_ & 0x7fffffffu) * S : slab + uint64_t(s_) * S) + c0;
-                    dst = push_dst(sp, xr[4 + x], next_slot) + c0;
-                    if (!(s_ >> 31))
-                        for (uint32_t t = 0; t < nprev; ++t)
-                            hazard |= prevw[t] == s_;
+                    dst = push_dst(sp, xraw[4 + x], next_slot) + c0;
                 } else {
-                    src = batch + uint64_t(wr[2 + 2 * (x - nj)]) * S + c0;
-                    dst = slab + uint64_t(wr[3 + 2 * (x - nj)]) * S + c0;
+                    src = batch + uint64_t(wraw[2 + 2 * (x - nj)]) * S + c0;
+                    dst = slab + uint64_t(wraw[3 + 2 * (x - nj)]) * S + c0;
                 }
                 paddr[2 * x] = reinterpret_cast<uint64_t>(src);
                 paddr[2 * x + 1] = reinterpret_cast<uint64_t>(dst);
             }
         }
-        hazard = __any_sync(kFull, hazard);
         __syncwarp();
+        if (lane == 0)
+            cta_mark(sp, 12);
         bool drained = false;
-        auto drain = [&]() {  // B(k-1)'s stores (every lane's groups) complete, then arrive
+        auto drain = [&]() {  // this warp's previous iteration (k-2): stores complete, arrive
             bulk_wait_all();
             __syncwarp();
-            if (lane == 0) {
-                cta_mark(sp, 7);
-                if (k > 0)
-                    run_b_arrive(rp, sp, k - 1, multi);
-                cta_mark(sp, 8);
+            if (lane == 0 && prev_k >= 0) {
+                fl->complete[prev_k & 1] = uint64_t(prev_k) + 1;
+                run_b_arrive(rp, sp, uint64_t(prev_k), multi);
             }
+            prev_k = -1;
             drained = true;
         };
-        if (hazard || pieces == 0)
+        if (push_hz) {  // B(k-1)'s W stores land before these loads read the rows. Drain own
+                        // k-2 first: the other warp may be waiting for it (no wait cycle).
             drain();
+            if (lane == 0)
+                smem_wait_ge(&fl->complete[(k - 1) & 1], k, rp, 3, k);
+            __syncwarp();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (uint32_t p0 = 0; p0 < pieces; p0 += per_win) {
             const uint32_t p1 = min(pieces, p0 + per_win);
             if (p0 > 0) {
@@ -1680,43 +1770,127 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams& sp)
                 bulk_load(arena + (x - p0) * clen, reinterpret_cast<const void*>(paddr[2 * x]), clen, barB);
             if (lane == 0)
                 cta_mark(sp, 3);
-            if (!drained)  // B(k-1)'s stores complete while these loads fly
+            if (!drained)
                 drain();
             if (!mbar_wait(barB, take_phase(phB, 0), rp.base.timeout_ns))
                 atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
-            if (lane == 0)
+            if (p1 == pieces && lane == 0)
+                fl->landed[k & 1] = k + 1;
+            if (lane == 0) {
                 cta_mark(sp, 6);
+                if (k > 0)  // B(k-1) finished reading the rows W_k overwrites
+                    smem_wait_ge(&fl->landed[(k - 1) & 1], k, rp, 4, k);
+                if (k > 0 && w_hz)  // and its own writes to them land first
+                    smem_wait_ge(&fl->complete[(k - 1) & 1], k, rp, 5, k);
+            }
+            __syncwarp();
             for (uint32_t x = p0 + lane; x < p1; x += 32)
                 bulk_store(reinterpret_cast<void*>(paddr[2 * x + 1]), arena + (x - p0) * clen, clen);
             bulk_commit();
         }
+        if (!drained)
+            drain();
+        if (pieces == 0 && lane == 0)
+            fl->landed[k & 1] = k + 1;
+        prev_k = int64_t(k);
         if (lane == 0)
             cta_mark(sp, 4);
-        // W_k's slab rows for the next iteration's hazard check
-        nprev = nw;
-        for (uint32_t t = lane; t < nw; t += 32)
-            prevw[t] = wr[3 + 2 * t];
-        bulk_wait_read_all();  // arena free before the next iteration's loads
+        bulk_wait_read_all();  // arena free before this warp's next iteration
+        __syncwarp();
         if (lane == 0)
             cta_mark(sp, 9);
-        __syncwarp();
     }
-    if (rp.steps > 0 && !*reinterpret_cast<volatile uint32_t*>(&rp.ctl->error)) {
+    if (prev_k >= 0 && !*reinterpret_cast<volatile uint32_t*>(&rp.ctl->error)) {
         bulk_wait_all();
         __syncwarp();
-        if (lane == 0)
-            run_b_arrive(rp, sp, rp.steps - 1, multi);
+        if (lane == 0) {
+            fl->complete[prev_k & 1] = uint64_t(prev_k) + 1;
+            run_b_arrive(rp, sp, uint64_t(prev_k), multi);
+        }
     }
+}
+
+// CTAs 2..: copies. Warp 1 lane 0 streams m_i -> m'_i (flat slice of the batch bytes), at
+// most two iterations ahead of the completed B. Warps 0 and 2 do B (even / odd iterations)
+// on a fixed COLUMN of every row — bytes [c0, c1) of each slab row written (W_i) and each
+// slot pushed (X_i) — so every access to a given slab byte is in this one CTA: there is no
+// grid-wide hand-off between iterations.
+__device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp >= 3)
+        return;
+    const StepParams& b = rp.base;
+    const RunSmem R = run_smem(b.N, b.K, b.r, b.nmax);
+    uint8_t* base8 = reinterpret_cast<uint8_t*>(sm);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base8 + R.bars);
+    uint8_t* ringA = base8 + R.ring_a;
+    const uint32_t part = blockIdx.x - 2, parts = rp.copy_ctas;
+    const uint64_t S = b.S;
+    const uint32_t CH = kTmaChunk;
+    if (tid < sizeof(BFlags) / 8)
+        reinterpret_cast<unsigned long long*>(base8 + R.flags)[tid] = 0;
+    if (tid == 32) {
+        for (uint32_t x = 0; x < kTmaStagesA + 2; ++x)
+            mbar_init(bars + x, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    named_bar(2, 96);
+    if (warp == 0 || warp == 2) {
+        run_b_warp(rp, sm, R, sp2[warp >> 1], warp >> 1);
+        return;
+    }
+    // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
+    if (lane != 0)
+        return;
+    const uint64_t a16 = (uint64_t(rp.n) * S) >> 4;
+    const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
+    const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
+    const uint32_t row0 = b.nmax - rp.n;
+    uint32_t ph_bits = 0;  // phase of each A barrier
+    SeenFlag bdone{&rp.ctl->b_done, 0};
+#pragma unroll 1
+    for (uint64_t k = 0; k < rp.steps; ++k) {
+        if (!wait_seen(bdone, back(k, 2), rp))
+            break;
+        const uint64_t i = rp.i0 + k;
+        run_mark(rp, i, 2);
+        // m'_i's rows were last written by A(k-6): those stores are complete (every bulk
+        // group but the newest — A(k-1)'s last window — has finished)
+        asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+        const uint8_t* batch = rp.batches + ((rp.first + k) % rp.ring) * rp.batch_stride;
+        uint8_t* dst = b.region[b.me] + b.off_aug + (i % kAugRing) * b.aug_slot_bytes + uint64_t(row0) * S;
+        for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
+            const uint32_t w1 = min(nA, w0 + kTmaStagesA);
+            bulk_wait_read_all();  // the ring's previous window has been stored
+            for (uint32_t x = w0; x < w1; ++x) {
+                const uint64_t off = alo + uint64_t(x) * CH;
+                const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                mbar_expect_tx(bars + (x - w0), len);
+                bulk_load(ringA + (x - w0) * CH, batch + off, len, bars + (x - w0));
+            }
+            for (uint32_t x = w0; x < w1; ++x) {
+                const uint64_t off = alo + uint64_t(x) * CH;
+                const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                if (!mbar_wait(bars + (x - w0), take_phase(ph_bits, x - w0), rp.base.timeout_ns))
+                    atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
+                bulk_store(dst + off, ringA + (x - w0) * CH, len);
+            }
+            bulk_commit();
+        }
+        run_mark(rp, i, 5);
+    }
+    bulk_wait_all();
 }
 
 __global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_constant__ RunParams rp) {
     extern __shared__ __align__(128) uint32_t sm[];
-    __shared__ StepParams sp;
-    __shared__ uint32_t flag[4];
+    __shared__ StepParams sp[2];
+    __shared__ __align__(8) uint32_t flag[8];  // [0..1] role flags, [2..7] the plan role's counters
     if (blockIdx.x == 0)
-        run_sel_role(rp, sm, sp, flag);
+        run_sel_role(rp, sm, sp[0], flag);
     else if (blockIdx.x == 1)
-        run_plan_role(rp, sm, sp, flag);
+        run_plan_role(rp, sm, sp[0], flag);
     else
         run_copy_role(rp, sm, sp);
 }

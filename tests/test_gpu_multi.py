@@ -133,3 +133,54 @@ def test_stalled_peer_times_out_without_hanging(monkeypatch):
     assert engs[0].device_error() != 0
     for e in engs:
         e.shutdown()
+
+
+@pytest.mark.parametrize("persist", ["1", "0"])
+def test_multi_rank_ring_runs(monkeypatch, persist):
+    """Multi-iteration runs over device rings on every rank (the bench path, persistent kernel
+    and three-kernel graph path): after the runs, every rank's later update() steps — whose
+    representative rows the runs' last pushes delivered — are bit-exact vs the N-rank replay."""
+    if ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2406_03285_b200 as drb
+    monkeypatch.setenv("DRB_PERSIST", persist)
+    monkeypatch.setenv("DRB_TIMEOUT_MS", "5000")
+    N = min(ngpu(), 4)
+    K, cap, S, b, c, r, seed, ring, steps = 12, 5, 1024, 24, 14, 7, 13, 5, 60
+    bufs, engs = make_world(drb, N, K, cap, S, b, c, r, seed)
+    spec = stream_spec(K, 3, b, S, steps_per_task=10, seed=seed)
+    rep = Backend("port").replay(N, K, cap, S, c, r, seed)
+    rd = [np.stack([spec.payload(w, 500 + x) for x in range(ring)]) for w in range(N)]
+    rl = [np.stack([spec.labels(w, 500 + x) for x in range(ring)]) for w in range(N)]
+    rings = []
+    for w in range(N):
+        with torch.cuda.device(w):
+            rings.append((torch.from_numpy(rd[w]).cuda(w), torch.from_numpy(rl[w].astype(np.int32)).cuda(w)))
+    for w in range(N):  # every rank's run in flight at once (they rendezvous on the device)
+        with torch.cuda.device(w):
+            engs[w].run(rings[w][0], rings[w][1], steps, first=1)
+    for k in range(steps):
+        rep.step(np.stack([rd[w][(1 + k) % ring] for w in range(N)]),
+                 np.stack([rl[w][(1 + k) % ring] for w in range(N)]))
+    for w in range(N):
+        torch.cuda.synchronize(w)
+    streams = [torch.cuda.Stream(device=w) for w in range(N)]
+    for i in range(3):
+        data = np.stack([spec.payload(w, i) for w in range(N)])
+        labs = np.stack([spec.labels(w, i) for w in range(N)])
+        o, ol, oc = rep.step(data, labs)
+        augs = []
+        for w in range(N):
+            with torch.cuda.device(w):
+                m = (torch.from_numpy(data[w]).cuda(w), torch.from_numpy(labs[w].astype(np.int32)).cuda(w))
+                torch.cuda.synchronize(w)
+                augs.append(engs[w].update(m, stream=streams[w]))
+        for w in range(N):
+            d, l = augs[w].tensors()
+            cnt = augs[w].count()
+            assert cnt == int(oc[w]), (i, w)
+            assert np.array_equal(l.cpu().numpy().astype(np.uint32), ol[w, :cnt]), (i, w)
+            assert np.array_equal(d.cpu().numpy(), o[w, :cnt]), (i, w)
+    for e in engs:
+        assert e.device_error() == 0
+        e.shutdown()

@@ -39,8 +39,9 @@ t = t.reshape(n.value, W).astype(np.int64)
 rows = [(first + i) % n.value for i in range(STEPS)]
 cta = t[:, 32:].reshape(n.value, 160, 16)
 ncta = torch.cuda.get_device_properties(0).multi_processor_count
-NAMES = {0: "B start", 1: "lists parsed", 3: "B loads issued", 7: "prev drained", 8: "arrived", 6: "B loads landed",
-         4: "B stores issued", 9: "B iter end", 2: "A start", 5: "A end"}
+NAMES = {0: "B start", 1: "lists parsed", 10: "W published", 11: "W(k-1) seen", 12: "addresses", 3: "B loads issued",
+         7: "prev drained", 8: "arrived", 6: "B loads landed", 4: "B stores issued", 9: "B iter end", 2: "A start",
+         5: "A end"}
 sel = rows[8:-2]
 print(f"{'stamp':16s} median over copy CTAs / iterations, us after the CTA's B start")
 for s_, nm in NAMES.items():
@@ -60,3 +61,10 @@ for name, a, e in (("sel", 0, 4), ("plan", 5, 8)):
     st = [ph[row, a] for row in rows]
     print(f"{name}: duration {np.median(d):.2f} us, period {np.median(np.diff(st)) / 1e3:.2f} us; "
           f"start vs B start (median CTA) {np.median([(ph[row, a] - np.median(cta[row, 2:ncta, 0])) / 1e3 for row in sel]):.2f} us")
+
+# control CTAs: CTA 0 (sel) stamps 0 loop top, 1 flags ok, 2 sel_core start, 3 sel_core end, 4 loop end;
+# CTA 1 (plan) 0 loop top, 1 flags ok, 3 released. Medians relative to the loop top.
+for c, nm, slots in ((0, "sel", (1, 2, 3, 4)), (1, "plan", (1, 3))):
+    rel = {s_: np.median([(cta[row, c, s_] - cta[row, c, 0]) / 1e3 for row in sel]) for s_ in slots}
+    per = np.median(np.diff([cta[row, c, 0] for row in rows])) / 1e3
+    print(f"{nm} CTA: loop period {per:.2f} us; " + ", ".join(f"stamp{s_} +{v:.2f}" for s_, v in rel.items()))
