@@ -327,6 +327,24 @@ def main():
     eng.shutdown()
 
     persistent = os.environ.get("DRB_PERSIST", "1") != "0" and not args.no_graph
+    # PCIe ceiling of the e2e leg: the same H2D + D2H bytes as one step, plain pinned copies
+    h2d_b, d2h_b = b * (S + 4), r * (S + 4) + 4
+    pin_in = torch.empty(h2d_b, dtype=torch.uint8).pin_memory()
+    pin_out = torch.empty(d2h_b, dtype=torch.uint8).pin_memory()
+    dev_in = torch.empty(h2d_b, dtype=torch.uint8, device=f"cuda:{local}")
+    dev_out = torch.empty(d2h_b, dtype=torch.uint8, device=f"cuda:{local}")
+    s_in, s_out = torch.cuda.Stream(device=local), torch.cuda.Stream(device=local)
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            with torch.cuda.stream(s_in):
+                dev_in.copy_(pin_in, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                pin_out.copy_(dev_out, non_blocking=True)
+        torch.cuda.synchronize()
+        pcie_s = time.perf_counter() - t0
+    pcie_steps_per_s = e2e_steps / pcie_s
     # our kernels inside the timed region: sel + plan + copy per step (three-kernel path,
     # captured in one CUDA graph, DRB_PERSIST=0), or one cooperative launch for the whole run
     launches = 1 if persistent else 3 * args.steps
@@ -366,14 +384,22 @@ def main():
                              f"slab {K * cap * S / 2**20:.0f} MiB per GPU"},
             "gpu_launches": launches,
             "launch_mode": launch_mode,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": b * (S + 4),
-                    "d2h_bytes_per_step": r * (S + 4) + 4, "steps": e2e_steps,
-                    "api": "drb_rb_step_host, m' assembled in place in the caller's pinned batch buffer"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
+                    "d2h_bytes_per_step": d2h_b, "steps": e2e_steps,
+                    "api": "drb_rb_step_host, m' assembled in place in the caller's pinned batch buffer",
+                    "pcie_ceiling": {"value": (b + r) * N * pcie_steps_per_s, "unit": UNIT,
+                                     "h2d_gbs": h2d_b * pcie_steps_per_s / 1e9,
+                                     "how": "the same per-step H2D and D2H bytes as plain pinned cudaMemcpyAsync "
+                                            "on two streams, no kernels"}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "algorithmic_bytes_per_launch": bytes_step, "kernel_ms": ms_per_step,
-                         "kernel": "drb_copy_tma_kernel", "timing": "CUDA events over the timed region / K steps",
-                         "kernel_ms_event_bracketed": kernel_ms,
+                         "algorithmic_bytes_per_step": bytes_step,
+                         "algorithmic_bytes_per_launch": bytes_step * (args.steps if persistent else 1),
+                         "kernel_ms_per_step": ms_per_step,
+                         "kernel": "drb_run_kernel" if persistent else "drb_copy_tma_kernel",
+                         "timing": ("one persistent launch = the whole timed region (K steps); CUDA events on its "
+                                    "stream / K" if persistent else "CUDA events over the timed region / K steps"),
+                         "three_kernel_copy_ms_event_bracketed": kernel_ms,
                          "bytes_formula": "2*S*(b+r+c) per rank per iteration (SURVEY.md 8d)"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
