@@ -323,6 +323,8 @@ int or_replay_dump(void* p, uint32_t w, uint32_t* occ, uint64_t* version, uint8_
     replay* h = (replay*)p;
     memcpy(occ, h->occ + (size_t)w * h->K, h->K * 4);
     *version = h->version[w];
+    if (!slab || !slab_labels)  /* occupancy and version only */
+        return 0;
     for (uint32_t k = 0; k < h->K; ++k)
         for (uint32_t s = 0; s < h->cap; ++s) {
             const size_t i = (size_t)k * h->cap + s;

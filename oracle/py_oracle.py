@@ -30,6 +30,12 @@ _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 
 
+def _nullable(nd):
+    """An ndpointer argtype that also accepts None (NULL)."""
+    return type(nd.__name__ + "_or_null", (nd,),
+                {"from_param": classmethod(lambda cls, obj: None if obj is None else nd.from_param(obj))})
+
+
 def _bind(lib, prefix):
     u32, u64, i32, vp = C.c_uint32, C.c_uint64, C.c_int, C.c_void_p
     sig = {
@@ -42,7 +48,7 @@ def _bind(lib, prefix):
         "replay_step": (i32, [vp, _u8p, _u32p, u32, _u8p, _u32p, _u32p]),
         "replay_last_plan": (u32, [vp, u32, _u32p]),
         "replay_last_report": (i32, [vp, u32, _u32p, _u32p, _u32p]),
-        "replay_dump": (i32, [vp, u32, _u32p, _u64p, _u8p, _u32p]),
+        "replay_dump": (i32, [vp, u32, _u32p, _u64p, _nullable(_u8p), _nullable(_u32p)]),
     }
     fns = {}
     for name, (res, args) in sig.items():
@@ -161,9 +167,13 @@ class Replay:
         self.be.f["replay_last_report"](self.h, w, a, rp, t)
         return a, rp, t
 
-    def dump(self, w):
+    def dump(self, w, occupancy_only=False):
         occ = np.zeros(self.K, np.uint32)
         ver = np.zeros(1, np.uint64)
+        if occupancy_only:
+            assert self.be.kind == "port"
+            self.be.f["replay_dump"](self.h, w, occ, ver, None, None)
+            return occ, int(ver[0]), None, None
         slab = np.zeros(self.K * self.cap * self.S, np.uint8)
         sl = np.zeros(self.K * self.cap, np.uint32)
         self.be.f["replay_dump"](self.h, w, occ, ver, slab, sl)

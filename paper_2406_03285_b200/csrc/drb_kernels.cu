@@ -1476,6 +1476,8 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             if (tid == 0)
                 run_mark(rp, rp.i0 + k, 2);
             sel_core(sp, v, flag[0] != 0);
+            if (b.dbg & 2048)  // experiment: the compute warp's own GPU-scope fence
+                __threadfence();
             __syncwarp();
             if (tid == 0) {
                 st_release_cta(seen + 2, k + 1);  // hand sel(k) to the publisher
@@ -1548,6 +1550,8 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
         tl_mark(sp, 1, false);
         trace_at(sp, 5);
         plan_core(sp, v, T, 3);
+        if (rp.base.dbg & 2048)
+            __threadfence();
         cta_bar(3, T);
         if (tid == 0) {
             st_release_cta(seen + 2, k + 1);  // hand plan(k) to the publisher
@@ -1666,10 +1670,17 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         const uint64_t i = rp.i0 + k;
         const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
         const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
-        for (uint32_t x = lane; x < pw; x += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xraw + x)), "l"(xs + x) : "memory");
-        for (uint32_t x = lane; x < ww; x += 32)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wraw + x)), "l"(ws + x) : "memory");
+        if (b.dbg & 4096) {  // experiment: lists through L2 only
+            for (uint32_t x = lane; x < pw; x += 32)
+                xraw[x] = __ldcg(xs + x);
+            for (uint32_t x = lane; x < ww; x += 32)
+                wraw[x] = __ldcg(ws + x);
+        } else {
+            for (uint32_t x = lane; x < pw; x += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xraw + x)), "l"(xs + x) : "memory");
+            for (uint32_t x = lane; x < ww; x += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wraw + x)), "l"(ws + x) : "memory");
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
         copy_parse(sp, xraw, wraw, jsrc, nullptr, misc, ready, true, true, false);
         const uint32_t nj = misc[0], nw = misc[1];
@@ -1695,7 +1706,18 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         if (lane == 0)
             cta_mark(sp, 10);
         // W_{k-1} (the other warp's) for the hazard checks
-        bool push_hz = false, w_hz = false;
+        bool push_hz = false, w_hz = false, own_hz = false;
+        if (k > 1) {  // a slot pushed now that this warp's B(k-2) wrote: its stores land first
+            const uint32_t* wq = wrows + ((k - 2) & 3) * nslot;
+            const uint32_t nq = wq[0];
+            for (uint32_t x = lane; x < nj; x += 32) {
+                const uint32_t s_ = jsrc[x];
+                if (!(s_ >> 31))
+                    for (uint32_t t = 0; t < nq; ++t)
+                        own_hz |= wq[1 + t] == s_;
+            }
+            own_hz = __any_sync(kFull, own_hz);
+        }
         if (k > 0) {
             if (lane == 0)
                 smem_wait_ge(&fl->parsed[(k - 1) & 3], k, rp, 2, k);
@@ -1750,6 +1772,15 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
             prev_k = -1;
             drained = true;
         };
+        if (k > 2) {  // the other warp's B(k-3) complete (its drain precedes every wait of B(k-1))
+            if (lane == 0)
+                smem_wait_ge(&fl->complete[(k - 3) & 1], k - 2, rp, 7, k);
+            __syncwarp();
+        }
+        if (own_hz && !push_hz) {
+            drain();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         if (push_hz) {  // B(k-1)'s W stores land before these loads read the rows. Drain own
                         // k-2 first: the other warp may be waiting for it (no wait cycle).
             drain();
