@@ -19,7 +19,8 @@
  * DRB_ERR_INVALID_ARGUMENT, exception taxonomy -> status (drb_capi.cpp:29-46).
  *
  * No torch types: device buffers are plain device pointers, streams are cudaStream_t
- * passed as void* (NULL = the handle's own stream).
+ * passed as void* (NULL = the handle's own stream, which is not ordered with the caller's
+ * work; pass cudaStreamLegacy for the legacy default stream).
  *
  * Payloads are opaque fixed-size samples of `sample_bytes` bytes (S); labels are uint32.
  * The reference stores float features; any S that is a multiple of 4 is bit-compatible

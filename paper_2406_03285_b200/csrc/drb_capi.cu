@@ -1220,9 +1220,10 @@ drb_status drb_rb_synchronize(drb_rb* h) {
             cudaDeviceSynchronize();
             RunCtl rc{};
             cudaMemcpy(&rc, h->runctl, sizeof rc, cudaMemcpyDeviceToHost);
-            std::fprintf(stderr, "drb run: sel %llu plan %llu b %llu error %u where site %u k %u\n",
+            std::fprintf(stderr, "drb run: sel %llu plan %llu b %llu error %u where site %u k %u check %u/%u first k %u\n",
                          (unsigned long long)rc.sel_done, (unsigned long long)rc.plan_done,
-                         (unsigned long long)rc.b_done, rc.error, rc.where >> 24, rc.where & 0xffffff);
+                         (unsigned long long)rc.b_done, rc.error, rc.where >> 24, rc.where & 0xffffff,
+                         rc.pad[0], rc.pad[2], rc.pad[1]);
         }
         cuda_check(cudaStreamSynchronize(h->stream), "sync");
         cuda_check(cudaStreamSynchronize(h->s_sel), "sync");

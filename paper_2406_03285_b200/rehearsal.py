@@ -36,6 +36,16 @@ class _cai:
         self._owner = owner
 
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
+def _stream_arg(s: torch.cuda.Stream) -> C.c_void_p:
+    """The handle to pass for a torch stream. torch's default stream reports handle 0, which the
+    C ABI reads as "the engine's own stream" (unordered with the caller's work), so the legacy
+    default stream is passed explicitly."""
+    return C.c_void_p(s.cuda_stream or _CUDA_STREAM_LEGACY)
+
+
 def _view(ptr: int, shape, typestr: str, device: int, owner) -> torch.Tensor:
     return torch.as_tensor(_cai(ptr, shape, typestr, owner), device=f"cuda:{device}")
 
@@ -327,7 +337,8 @@ class prepared_run:
         self.g, self._keep = g, keep
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
-        check(lib.drb_rb_graph_launch(self.g, C.c_void_p(stream.cuda_stream) if stream is not None else None))
+        s = stream if stream is not None else torch.cuda.current_stream()
+        check(lib.drb_rb_graph_launch(self.g, _stream_arg(s)))
 
     def close(self) -> None:
         if self.g and self.g.value:
@@ -364,7 +375,11 @@ class engine:
         s = stream if stream is not None else torch.cuda.current_stream(self.buffer.device)
         aug = _lib.drb_aug()
         check(lib.drb_rb_step(self.buffer.h, data.data_ptr() if n else None, labels.data_ptr() if n else None, n,
-                              C.c_void_p(s.cuda_stream), C.byref(aug)))
+                              _stream_arg(s), C.byref(aug)))
+        if n:  # m_i is read until "m'_i ready", which `s` waits for: the caching allocator must
+            # not hand m_i's blocks (or a converted label copy) to anyone before that point
+            data.record_stream(s)
+            labels.record_stream(s)
         self.iteration += 1
         return augmented_batch(self, aug)
 
@@ -389,7 +404,9 @@ class engine:
         if events is not None:
             ev = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
         check(lib.drb_rb_run(self.buffer.h, data_ring.data_ptr(), data_ring.stride(0), label_ring.data_ptr(),
-                             label_ring.stride(0), B, n, steps, first, C.c_void_p(s.cuda_stream), ev))
+                             label_ring.stride(0), B, n, steps, first, _stream_arg(s), ev))
+        data_ring.record_stream(s)  # read until the run completes on `s`
+        label_ring.record_stream(s)
         self.iteration += steps
 
     def prepare_run(self, data_ring: torch.Tensor, label_ring: torch.Tensor, steps: int,

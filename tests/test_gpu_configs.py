@@ -86,6 +86,7 @@ def config_parity(K, cap, S, b, c, r, T, N=1, ring=6, steps=120, post=3, seed=1,
         torch.cuda.synchronize(w)
     del runs
     for w in range(N):
+        engs[w].synchronize()
         assert engs[w].device_error() == 0, ("run failed on the device", w)
     for w in range(N):
         occ, ver, slab, sl = rep.dump(w) if slab_check else rep.dump(w, occupancy_only=True)
@@ -101,7 +102,30 @@ def config_parity(K, cap, S, b, c, r, T, N=1, ring=6, steps=120, post=3, seed=1,
                     "gpu", fp.get(d[k, s_, :16].tobytes()), "oracle", fp.get(slab[k, s_, :16].tobytes()),
                     int((d[k, s_].reshape(-1, 16) != slab[k, s_].reshape(-1, 16)).any(1).sum()))
                    for k in range(K) for s_ in range(occ[k]) if not np.array_equal(d[k, s_], slab[k, s_])]
-            assert not bad, (w, len(bad), bad[:8])
+            if bad:  # per copy-CTA column detail of the first bad slot (diagnostics)
+                k0, s0 = bad[0][0], bad[0][1]
+                parts = torch.cuda.get_device_properties(w).multi_processor_count - 2
+                c16 = S // 16
+                cols = [((c16 * p_ // parts) * 16, (c16 * (p_ + 1) // parts) * 16) for p_ in range(parts)]
+                fpc = lambda a, e, row: next((f"{x},{j}" for x in range(ring) for j in range(b)
+                                              if np.array_equal(rd[w][x, j, a:e], row[a:e])), None)
+                det = [(p_, "pattern" if (d[k0, s0, a:e] == 0xA5).all() else fpc(a, e, d[k0, s0]), fpc(a, e, slab[k0, s0]))
+                       for p_, (a, e) in enumerate(cols) if e > a and not np.array_equal(d[k0, s0, a:e], slab[k0, s0, a:e])]
+                bad.append(("columns of the first", len(det), det[:10]))
+                flat_o = slab.reshape(K * cap, S)
+                flat_g = d.reshape(K * cap, S)
+                bad.append(("gpu row equals oracle rows", [divmod(x, cap) for x in range(K * cap)
+                                                            if np.array_equal(flat_o[x], d[k0, s0])][:6],
+                            "oracle row found at gpu rows", [divmod(x, cap) for x in range(K * cap)
+                                                             if np.array_equal(flat_g[x], slab[k0, s0])][:6],
+                            "gpu row zero", bool((d[k0, s0] == 0).all()),
+                            "gpu first bytes", d[k0, s0, :8].tolist()))
+                import json
+                import os
+                if os.environ.get("DRB_TEST_DIAG"):
+                    with open(os.environ["DRB_TEST_DIAG"], "a") as f:
+                        f.write(json.dumps([str(x) for x in bad]) + "\n")
+            assert not bad, (w, len(bad), bad[:8] + bad[-1:])
             for k in range(K):
                 assert np.array_equal(l[k, :occ[k]], sl[k, :occ[k]]), (w, k)
     streams = [torch.cuda.Stream(device=w) for w in range(N)]
