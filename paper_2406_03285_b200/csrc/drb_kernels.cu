@@ -1721,9 +1721,6 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
                     for (uint32_t t = 0; t < nq; ++t)
                         own_hz |= wq[1 + t] == s_;
             }
-            for (uint32_t t = lane; t < nw; t += 32)  // a W_k row B(k-2) also wrote
-                for (uint32_t u = 0; u < nq; ++u)
-                    own_hz |= wq[1 + u] == wk[1 + t];
             own_hz = __any_sync(kFull, own_hz);
         }
         if (k > 0) {
@@ -1769,16 +1766,9 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         __syncwarp();
         if (lane == 0)
             cta_mark(sp, 12);
-        // This warp's B(k-2) stores drain AFTER B(k)'s stores are issued (their completion —
-        // remote ones are NVLink round trips — overlaps this iteration), except when B(k)
-        // touches a row B(k-2) wrote (own_hz) or before any wait on the other warp: a warp
-        // never blocks on the other one while holding undrained stores, so no wait cycle forms.
         bool drained = false;
-        auto drain = [&](bool all) {  // B(k-2): stores complete, arrive
-            if (all)
-                bulk_wait_all();
-            else  // every bulk group but the newest (B(k)'s single window)
-                asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+        auto drain = [&]() {  // this warp's previous iteration (k-2): stores complete, arrive
+            bulk_wait_all();
             __syncwarp();
             if (lane == 0 && prev_k >= 0) {
                 fl->complete[prev_k & 1] = uint64_t(prev_k) + 1;
@@ -1787,26 +1777,21 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
             prev_k = -1;
             drained = true;
         };
-        auto wait_other = [&](const volatile unsigned long long* f, uint64_t want, uint32_t site) {
-            const bool ready = __shfl_sync(kFull, lane == 0 ? (*f >= want ? 1 : 0) : 0, 0) != 0;
-            if (ready)
-                return;
-            if (!drained)
-                drain(true);
+        if (k > 2) {  // the other warp's B(k-3) complete (its drain precedes every wait of B(k-1))
             if (lane == 0)
-                smem_wait_ge(f, want, rp, site, k);
+                smem_wait_ge(&fl->complete[(k - 3) & 1], k - 2, rp, 7, k);
             __syncwarp();
-        };
-        const bool one_window = pieces <= per_win;
-        const bool eager = !(b.dbg & 8192);  // DRB_DBG bit 13: drain B(k-2) after B(k)'s stores
-        if (own_hz || !one_window) {
-            drain(true);
+        }
+        if (own_hz && !push_hz) {
+            drain();
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        if (k > 2)  // the other warp's B(k-3) complete
-            wait_other(&fl->complete[(k - 3) & 1], k - 2, 7);
-        if (push_hz) {  // B(k-1)'s W stores land before these loads read the rows
-            wait_other(&fl->complete[(k - 1) & 1], k, 3);
+        if (push_hz) {  // B(k-1)'s W stores land before these loads read the rows. Drain own
+                        // k-2 first: the other warp may be waiting for it (no wait cycle).
+            drain();
+            if (lane == 0)
+                smem_wait_ge(&fl->complete[(k - 1) & 1], k, rp, 3, k);
+            __syncwarp();
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         for (uint32_t p0 = 0; p0 < pieces; p0 += per_win) {
@@ -1821,37 +1806,26 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
                 bulk_load(arena + (x - p0) * clen, reinterpret_cast<const void*>(paddr[2 * x]), clen, barB);
             if (lane == 0)
                 cta_mark(sp, 3);
-            if (eager && !drained)  // drain B(k-2) under this iteration's loads
-                drain(true);
+            if (!drained)
+                drain();
             if (!mbar_wait(barB, take_phase(phB, 0), rp.base.timeout_ns))
                 atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
-            if (b.dbg & 16384) {  // debug: the arena holds the W sources' bytes (read-only batch rows)
-                for (uint32_t x = p0 + lane; x < p1; x += 32) {
-                    if (x < nj)
-                        continue;
-                    const uint4 a = *reinterpret_cast<const uint4*>(arena + (x - p0) * clen);
-                    const uint4 g = __ldcg(reinterpret_cast<const uint4*>(paddr[2 * x]));
-                    atomicAdd(&rp.ctl->pad[2], 1u);
-                    if (a.x != g.x || a.y != g.y || a.z != g.z || a.w != g.w) {
-                        if (atomicAdd(&rp.ctl->pad[0], 1u) == 0)
-                            rp.ctl->pad[1] = uint32_t(k);
-                    }
-                }
-            }
             if (p1 == pieces && lane == 0)
                 fl->landed[k & 1] = k + 1;
-            if (lane == 0)
+            if (lane == 0) {
                 cta_mark(sp, 6);
-            if (k > 0)  // B(k-1) finished reading the rows W_k overwrites
-                wait_other(&fl->landed[(k - 1) & 1], k, 4);
-            if (k > 0 && w_hz)  // and its own writes to them land first
-                wait_other(&fl->complete[(k - 1) & 1], k, 5);
+                if (k > 0)  // B(k-1) finished reading the rows W_k overwrites
+                    smem_wait_ge(&fl->landed[(k - 1) & 1], k, rp, 4, k);
+                if (k > 0 && w_hz)  // and its own writes to them land first
+                    smem_wait_ge(&fl->complete[(k - 1) & 1], k, rp, 5, k);
+            }
+            __syncwarp();
             for (uint32_t x = p0 + lane; x < p1; x += 32)
                 bulk_store(reinterpret_cast<void*>(paddr[2 * x + 1]), arena + (x - p0) * clen, clen);
             bulk_commit();
         }
         if (!drained)
-            drain(pieces == 0);
+            drain();
         if (pieces == 0 && lane == 0)
             fl->landed[k & 1] = k + 1;
         prev_k = int64_t(k);

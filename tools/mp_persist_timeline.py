@@ -76,6 +76,15 @@ sel_start = [cta[row, 0, 0] for row in rows]
 plan_start = [cta[row, 1, 0] for row in rows]
 out.append(f"  lead: sel start - B start {np.median(np.array(sel_start) - np.array(bs)) / 1e3:.2f} us, "
            f"plan start - B start {np.median(np.array(plan_start) - np.array(bs)) / 1e3:.2f} us")
+ph = t[:, 8:32]
+
+
+def phase(a, e):
+    return np.median([(ph[row, e] - ph[row, a]) / 1e3 for row in rows])
+
+
+out.append(f"  sel_core phases: select {phase(1, 2):.2f}, assign {phase(2, 3):.2f}, W/state/publish {phase(3, 4):.2f} us")
+out.append(f"  plan phases: rendezvous {phase(5, 6):.2f}, draws+locate {phase(6, 7):.2f}, push list {phase(7, 8):.2f} us")
 allout = [None] * world
 dist.all_gather_object(allout, "\n".join(out))
 if rank == 0:
