@@ -178,7 +178,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--ring", type=int, default=64, help="device input batches (>L2 in total)")
-    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--cpu-iters", type=int, default=300)
     ap.add_argument("--ref-iters", type=int, default=400)
     ap.add_argument("--no-cpu", action="store_true")
