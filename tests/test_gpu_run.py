@@ -106,3 +106,45 @@ def test_run_c2_sample_shape(drb):
 def test_run_graph_captured(drb):
     ring_parity(drb, K=10, cap=6, S=64, b=24, c=14, r=7, seed=8, pre=2, runs=[(25, 1), (7, 0)], post=3, ring=6,
                 graph=True)
+
+
+def test_run_and_step_ordered_after_default_stream_producer(drb):
+    """The batch ring is produced on torch's default stream right before run()/update() with no
+    host synchronisation (a long sleep kernel delays the producer): the engine must order its
+    reads behind it (the default stream's handle is 0, which the C ABI would otherwise read as
+    the engine's own, unordered stream)."""
+    K, cap, S, b, c, r, seed, ring = 10, 3, 4096, 24, 14, 7, 21, 4
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed)
+    eng = drb.engine(buf)
+    eng.start()
+    rep = Backend("port").replay(1, K, cap, S, c, r, seed)
+    spec = stream_spec(K, 1, b, S, steps_per_task=10**9, seed=seed)
+    rd = np.stack([spec.payload(0, x) for x in range(ring)])
+    rl = np.stack([spec.labels(0, x) for x in range(ring)])
+    src_d, src_l = dev(rd, rl)
+    data = torch.zeros_like(src_d)
+    lab = torch.zeros_like(src_l)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)  # ~0.1 s on the default stream before the producer copies
+    data.copy_(src_d)
+    lab.copy_(src_l)
+    eng.run(data, lab, 12, first=0)
+    for k in range(12):
+        rep.step(rd[k % ring][None], rl[k % ring][None])
+    torch.cuda.synchronize()
+    check_state(buf, rep, K, cap, "run after a delayed producer")
+    m_d = torch.zeros((b, S), dtype=torch.uint8, device="cuda")
+    m_l = torch.zeros((b,), dtype=torch.int32, device="cuda")
+    pd, pl = dev(spec.payload(0, 99), spec.labels(0, 99))
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)
+    m_d.copy_(pd)
+    m_l.copy_(pl)
+    aug = eng.update((m_d, m_l))
+    o, ol, oc = rep.step(spec.payload(0, 99)[None], spec.labels(0, 99)[None])
+    d, l = aug.tensors()
+    assert aug.count() == int(oc[0])
+    assert np.array_equal(d.cpu().numpy(), o[0, :aug.count()])
+    assert np.array_equal(l.cpu().numpy().astype(np.uint32), ol[0, :aug.count()])
+    assert eng.device_error() == 0
+    eng.shutdown()
