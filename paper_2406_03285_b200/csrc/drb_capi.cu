@@ -233,6 +233,7 @@ StepParams base_params(drb_rb* h) {
     p.trace = h->trace;
     p.timeline = h->timeline;
     p.timeline_steps = h->timeline_steps ? h->timeline_steps : 1;
+    p.evict_m = ~0ull / h->cfg.per_class_cap;
     p.seq = h->seq++;
     p.tslot_in = uint32_t(h->ver % kTableRing);
     p.tslot_out = uint32_t((h->ver + 1) % kTableRing);
@@ -976,6 +977,7 @@ void enqueue_persistent_run(drb_rb* h, const uint8_t* batches, uint64_t batch_st
     rp.ww = wlist_words(h->cfg.max_batch);
     const uint32_t grid = uint32_t(h->sm_count);
     rp.copy_ctas = grid - 2;
+    rp.first_mod = uint32_t(first % ring);
     cuda_check(cudaMemsetAsync(h->runctl, 0, sizeof(RunCtl), s), "run state reset");
     if (launch_run(rp, grid, s))
         fail(DRB_ERR_INTERNAL, std::string("persistent run launch failed: ") + cudaGetErrorString(cudaGetLastError()));
@@ -1047,7 +1049,7 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
             return;
         const bool vec = (h->cfg.sample_bytes % 16 == 0) && aligned16(batches) && (batch_stride % 16 == 0);
         h->last_run_persistent = false;
-        if (h->use_persist && !step_events && vec && h->sm_count > 2) {
+        if (h->use_persist && !step_events && vec && h->sm_count > 2 && steps < (1ull << 31)) {
             enqueue_persistent_run(h, b, batch_stride, labels, label_stride, ring, n, steps, first, s);
             return;
         }

@@ -146,6 +146,7 @@ struct StepParams {
     unsigned long long* trace;  // optional phase timestamps (CTA 0) + grid min/max, 16 slots
     unsigned long long* timeline;  // optional per-kernel [start, end] per step (kind 0 sel, 1 plan, 2 copy)
     uint32_t timeline_steps;       // ring length of the timeline (entries = steps * 3)
+    uint64_t evict_m;              // floor((2^64-1) / cap): the eviction bound's reciprocal (host-computed)
 };
 
 // Persistent multi-iteration run (drb_rb_run over a device-resident input ring):
@@ -173,7 +174,7 @@ struct RunParams {
     uint32_t* plist_base;
     uint32_t* wlist_base;
     RunCtl* ctl;
-    uint32_t ring, n, sel_par0, plan_par0, pw, ww, copy_ctas, pad;
+    uint32_t ring, n, sel_par0, plan_par0, pw, ww, copy_ctas, first_mod;  // first_mod = first % ring
 };
 constexpr uint32_t kRunThreads = 32 * (kMaxWorld + 2);  // plan_threads(N) + a helper warp, >= kSelThreads
 

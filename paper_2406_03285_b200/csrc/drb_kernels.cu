@@ -55,6 +55,7 @@ __device__ uint64_t bounded_seq(uint64_t key, uint64_t& ctr, uint64_t n) {
 struct reducer {
     uint64_t d, m;
     __device__ explicit reducer(uint64_t d_) : d(d_), m(~0ull / d_) {}
+    __device__ reducer(uint64_t d_, uint64_t m_) : d(d_), m(m_) {}  // m precomputed (= ~0 / d)
     __device__ __forceinline__ uint64_t mod(uint64_t v) const {
         uint64_t r = v - __umul64hi(v, m) * d;
         r = r >= d ? r - d : r;
@@ -170,12 +171,12 @@ __device__ void warp_select(uint64_t key, uint64_t& ctr, uint32_t n, uint32_t k,
 // order (exclusive prefix over the replacement ballot; rejected draws are skipped via
 // __fns over the validity ballot, which is exact because every replacement draws with the
 // same bound cap). occ[] (shared) is updated in place to the post-update occupancy.
-__device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint32_t k,
+__device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint64_t cap_m, uint32_t k,
                             const uint32_t* sel, const uint32_t* lab, uint32_t* occ,
                             uint32_t* cand_l, uint32_t* cand_slot, uint32_t* scratch,
                             uint32_t* kind, uint32_t& appends) {
     const int lane = threadIdx.x & 31;
-    const reducer red(cap);
+    const reducer red = cap_m ? reducer(cap, cap_m) : reducer(cap);
     const uint64_t thr = red.thr();
     const unsigned lt = (1u << lane) - 1u;
     appends = 0;
@@ -458,7 +459,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
     if (k > 0) {
         warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
         trace_at(p, 2);
-        warp_assign(p.evict_key, evict_ctr, cap, k, sel, v.lab, occ, cand_l, cand_slot, v.misc + 32, kind,
+        warp_assign(p.evict_key, evict_ctr, cap, p.evict_m, k, sel, v.lab, occ, cand_l, cand_slot, v.misc + 32, kind,
                     appends);
     }
     trace_at(p, 3);
@@ -1297,6 +1298,8 @@ __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
 
 // *f >= want, or false once the run failed / the wait timed out (then the run is failed).
 __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, bool sys) {
+    if ((sys ? ld_acquire_sys(f) : ld_acquire_gpu(f)) >= want)  // satisfied: no timer read
+        return true;
     const uint64_t t0 = globaltimer();
     for (;;) {
         const uint64_t v = sys ? ld_acquire_sys(f) : ld_acquire_gpu(f);
@@ -1327,7 +1330,7 @@ __device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t k) {
     p.sel_out = rp.sel_base + ((rp.sel_par0 + i + 1) & 1);
     p.plan_in = rp.plan_base + ((rp.plan_par0 + i) & 1);
     p.plan_out = rp.plan_base + ((rp.plan_par0 + i + 1) & 1);
-    const uint64_t slot = (rp.first + k) % rp.ring;
+    const uint64_t slot = (rp.first_mod + uint32_t(k)) % rp.ring;  // 32-bit: steps < 2^31
     p.batch = rp.batches + slot * rp.batch_stride;
     p.labels = rp.labels + slot * rp.label_stride;
     p.n = rp.n;
@@ -1485,7 +1488,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                 tl_mark(sp, 0, true);
             }
         } else if (k + 1 < rp.steps) {  // warps 2-3: labels of m_{k+1}
-            const uint64_t slot = (rp.first + k + 1) % rp.ring;
+            const uint64_t slot = (rp.first_mod + uint32_t(k + 1)) % rp.ring;
             const uint32_t* lp = rp.labels + slot * rp.label_stride;
             int bad = 0;
             for (uint32_t x = tid - 64; x < rp.n; x += kSelThreads - 64) {
@@ -1894,7 +1897,7 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         // m'_i's rows were last written by A(k-6): those stores are complete (every bulk
         // group but the newest — A(k-1)'s last window — has finished)
         asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
-        const uint8_t* batch = rp.batches + ((rp.first + k) % rp.ring) * rp.batch_stride;
+        const uint8_t* batch = rp.batches + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.batch_stride;
         uint8_t* dst = b.region[b.me] + b.off_aug + (i % kAugRing) * b.aug_slot_bytes + uint64_t(row0) * S;
         for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
             const uint32_t w1 = min(nA, w0 + kTmaStagesA);
