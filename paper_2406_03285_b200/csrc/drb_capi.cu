@@ -171,6 +171,7 @@ struct drb_rb {
     bool use_persist = true;          // drb_rb_run as one persistent cooperative launch (DRB_PERSIST=0 off)
     bool last_run_persistent = false; // the latest drb_rb_run was one persistent launch
     RunCtl* runctl = nullptr;         // device counters of the persistent run
+    unsigned long long* prof = nullptr;  // DRB_DBG 65536: sel/plan phase cycle accumulators [64]
     cudaEvent_t run_end = nullptr;
     uint64_t prewaited = 0;           // 1 + the iteration whose sel/plan the copy stream already waited for
     bool use_pdl = true;              // copy(i+1) launched programmatically behind copy(i); DRB_PDL=0 off
@@ -231,6 +232,7 @@ StepParams base_params(drb_rb* h) {
     static const uint32_t dbg = std::getenv("DRB_DBG") ? uint32_t(std::strtoul(std::getenv("DRB_DBG"), nullptr, 0)) : 0u;
     p.dbg = dbg;
     p.trace = h->trace;
+    p.prof = h->prof;
     p.timeline = h->timeline;
     p.timeline_steps = h->timeline_steps ? h->timeline_steps : 1;
     p.evict_m = ~0ull / h->cfg.per_class_cap;
@@ -512,6 +514,10 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         if (const char* pe = std::getenv("DRB_PERSIST"))
             h->use_persist = pe[0] == '1';
         cuda_check(cudaMalloc(&h->runctl, sizeof(RunCtl)), "run state alloc");
+        if (h->dbg_bits & 65536) {
+            cuda_check(cudaMalloc(&h->prof, 64 * 8), "prof alloc");
+            cuda_check(cudaMemset(h->prof, 0, 64 * 8), "prof alloc");
+        }
         cuda_check(cudaEventCreateWithFlags(&h->run_end, cudaEventDisableTiming), "event");
         if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
             cuda_check(cudaMalloc(&h->trace, 32 * 8), "trace alloc");
@@ -567,6 +573,8 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaStreamDestroy(h->s_sel);
         if (h->runctl)
             cudaFree(h->runctl);
+        if (h->prof)
+            cudaFree(h->prof);
         if (h->run_end)
             cudaEventDestroy(h->run_end);
         cudaStreamDestroy(h->s_plan);
@@ -1226,6 +1234,19 @@ drb_status drb_rb_synchronize(drb_rb* h) {
                          (unsigned long long)rc.sel_done, (unsigned long long)rc.plan_done,
                          (unsigned long long)rc.b_done, rc.error, rc.where >> 24, rc.where & 0xffffff,
                          rc.pad[0], rc.pad[2], rc.pad[1]);
+            if (h->prof) {
+                unsigned long long pr[64];
+                cudaMemcpy(pr, h->prof, sizeof pr, cudaMemcpyDeviceToHost);
+                for (int c = 0; c < 2; ++c) {
+                    const double it = pr[32 * c + 31] ? double(pr[32 * c + 31]) : 1.0;
+                    std::fprintf(stderr, "drb prof CTA %d (%llu iterations), cycles/iteration by stamp:", c,
+                                 (unsigned long long)pr[32 * c + 31]);
+                    for (int x = 0; x < 31; ++x)
+                        if (pr[32 * c + x])
+                            std::fprintf(stderr, " [%d] %.0f", x, double(pr[32 * c + x]) / it);
+                    std::fprintf(stderr, "\n");
+                }
+            }
         }
         cuda_check(cudaStreamSynchronize(h->stream), "sync");
         cuda_check(cudaStreamSynchronize(h->s_sel), "sync");

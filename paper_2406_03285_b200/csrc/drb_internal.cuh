@@ -147,6 +147,7 @@ struct StepParams {
     unsigned long long* timeline;  // optional per-kernel [start, end] per step (kind 0 sel, 1 plan, 2 copy)
     uint32_t timeline_steps;       // ring length of the timeline (entries = steps * 3)
     uint64_t evict_m;              // floor((2^64-1) / cap): the eviction bound's reciprocal (host-computed)
+    unsigned long long* prof;      // DRB_DBG 65536: clock64 phase accumulators of the run's sel/plan CTAs [64]
 };
 
 // Persistent multi-iteration run (drb_rb_run over a device-resident input ring):

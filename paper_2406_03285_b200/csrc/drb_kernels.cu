@@ -380,6 +380,16 @@ __device__ __forceinline__ void cta_mark(const StepParams& p, int slot) {
 
 __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
     // CTA 0 (sel, plan and the copy's first CTA); CTA 1 too: the plan role of a persistent run
+    if (p.prof && blockIdx.x <= 1 && threadIdx.x == 0) {  // cycles since this CTA's previous stamp
+        __shared__ unsigned long long prof_prev;
+        const unsigned long long now = clock64();
+        if (slot != 12 && slot != 13)  // 12/13: loop tops (start the chain)
+            atomicAdd(p.prof + 32 * blockIdx.x + slot, now - prof_prev);
+        else
+            atomicAdd(p.prof + 32 * blockIdx.x + slot, prof_prev ? now - prof_prev : 0ull);
+        atomicAdd(p.prof + 32 * blockIdx.x + 31, slot == 12 || slot == 13 ? 1ull : 0ull);
+        prof_prev = now;
+    }
     if (blockIdx.x <= 1 && (threadIdx.x & 31) == 0) {
         if (p.trace)
             p.trace[slot] = globaltimer();
@@ -1451,6 +1461,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
 #pragma unroll 1
     for (uint64_t k = 0; k < rp.steps; ++k) {  // warps 0, 2, 3 (barrier 1, 96 threads)
         if (tid == 0) {
+            trace_at(sp, 12);
             run_mark(rp, rp.i0 + k, 0);
             if (k > 0)
                 run_patch(sp, rp, k);
@@ -1535,6 +1546,7 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
 #pragma unroll 1
     for (uint64_t k = 0; k < rp.steps; ++k) {
         if (tid == 0) {
+            trace_at(sp, 13);
             run_mark(rp, rp.i0 + k, 0);
             if (k > 0)
                 run_patch(sp, rp, k);
