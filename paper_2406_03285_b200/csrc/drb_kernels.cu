@@ -20,6 +20,13 @@
 
 #include "drb_internal.cuh"
 
+// Timeline / trace / phase-profile stamps (DRB_TIMELINE, DRB_TRACE, DRB_DBG 65536) exist only
+// in the instrumented build (-DDRB_INSTRUMENT=1, tools/): every site costs the control chains
+// instruction fetch and issue slots even when switched off at run time.
+#ifndef DRB_INSTRUMENT
+#define DRB_INSTRUMENT 0
+#endif
+
 namespace drb_b200 {
 
 namespace {
@@ -360,6 +367,7 @@ __device__ __forceinline__ V ld_vec(const V* p) {
 // Timeline (DRB_TIMELINE=<steps>): grid-wide first start / last end of each kernel of
 // each step, as globaltimer ns; works inside CUDA graphs.
 __device__ __forceinline__ void tl_mark(const StepParams& p, int kind, bool end) {
+#if DRB_INSTRUMENT
     if (p.timeline && threadIdx.x == 0) {
         unsigned long long* e = p.timeline + (p.step % p.timeline_steps) * kTlStride + 2 * kind;
         if (end)
@@ -367,18 +375,35 @@ __device__ __forceinline__ void tl_mark(const StepParams& p, int kind, bool end)
         else
             atomicMin(e, globaltimer());
     }
+#endif
 }
 
 // per-CTA copy stamps (timeline mode): slot s of this CTA, written by the calling thread
 __device__ __forceinline__ void cta_mark(const StepParams& p, int slot) {
+#if DRB_INSTRUMENT
     if (p.timeline && blockIdx.x < kTlMaxCtas) {
         uint64_t t;  // "memory": not reordered with the surrounding loads / stores
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
         p.timeline[(p.step % p.timeline_steps) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = t;
     }
+#endif
+}
+
+// DRB_DBG 65536: cycles since `t` into prof slot `slot` of this control CTA (lane 0 of the
+// calling warp), then t = now. Free of memory traffic when profiling is off.
+__device__ __forceinline__ void prof_span(const StepParams& p, int slot, unsigned long long& t) {
+#if DRB_INSTRUMENT
+    if (p.prof && blockIdx.x <= 1 && (threadIdx.x & 31) == 0) {
+        const unsigned long long now = clock64();
+        if (t)
+            atomicAdd(p.prof + 32 * blockIdx.x + slot, now - t);
+        t = now;
+    }
+#endif
 }
 
 __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
+#if DRB_INSTRUMENT
     // CTA 0 (sel, plan and the copy's first CTA); CTA 1 too: the plan role of a persistent run
     if (p.prof && blockIdx.x <= 1 && threadIdx.x == 0) {  // cycles since this CTA's previous stamp
         __shared__ unsigned long long prof_prev;
@@ -396,6 +421,7 @@ __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
         if (p.timeline)  // phase stamps of the pipelined run: slots 8.. of the step's record
             p.timeline[(p.step % p.timeline_steps) * kTlStride + 8 + slot] = globaltimer();
     }
+#endif
 }
 
 }  // namespace
@@ -473,6 +499,8 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
                     appends);
     }
     trace_at(p, 3);
+    unsigned long long pt = 0;
+    prof_span(p, 14, pt);
     // W_i: winners = last writer of each (class, slot) in selection order, ballot-ordered
     uint32_t* wl = p.wlist;
     uint32_t n_win = 0;
@@ -502,6 +530,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
     }
     if (lane == 0)
         wl[0] = n_win;
+    prof_span(p, 14, pt);
     // round-(i+1) selection state
     const uint32_t err = dead ? st->error : ((bad && do_update) ? DRB_ERR_USAGE : 0u);
     __syncwarp();
@@ -519,9 +548,11 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
         if (p.mailbox && err)
             reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
     }
+    prof_span(p, 15, pt);
 #pragma unroll 1
     for (uint32_t t = lane; t < k; t += 32)  // stored label == class (class-partitioned)
         p.slab_labels[cand_l[t] * cap + cand_slot[t]] = cand_l[t];
+    prof_span(p, 16, pt);
     if (do_publish && !dead) {  // publish_row(i): version i+1 (engine.cpp:108-136)
         uint64_t* tout = reinterpret_cast<uint64_t*>(p.region[me] + p.off_table) +
                          uint64_t(p.tslot_out) * NK + uint64_t(me) * K;
@@ -550,6 +581,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
             }
         }
     }
+    prof_span(p, 17, pt);
     if (p.mode & kModeReport) {  // insertion_report (rehearsal_buffer.hpp:17-26)
 #pragma unroll 1
         for (uint32_t x = lane; x < 2 * K + 2; x += 32)
@@ -564,6 +596,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
         }
     }
     __syncwarp();
+    prof_span(p, 18, pt);
     trace_at(p, 4);
 }
 
@@ -683,11 +716,17 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         return;
     }
     // S4 plan(i): warps 1..N draw for requester q = warp-1; warp 0 builds the prefix
+    unsigned long long pt = 0;
+    if (warp == 1)
+        prof_span(p, 14, pt);
     if (warp >= 1 && warp <= N) {
         const uint32_t q = warp - 1;
         uint64_t ctr = st->samp_ctr[q];
         const uint32_t total = warp_sum(pre, NK);
+        if (warp == 1)
+        prof_span(p, 14, pt);
         const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
+        prof_span(p, 15, pt);
         if (lane == 0) {
             cnt[q] = c;
             p.plan_out->samp_ctr[q] = ctr;
@@ -697,9 +736,12 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         warp_exclusive_scan(pre, NK, pfx);
     }
     cta_bar(bar, T);
+    if (warp == 1)
+        prof_span(p, 16, pt);
     if (warp >= 1 && warp <= N) {
         const uint32_t q = warp - 1;
         warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
+        prof_span(p, 17, pt);
         if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
             uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
                            uint64_t((p.aslot + 1) % kAugRing) * p.auglab_slot_elems;
@@ -707,8 +749,11 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
             for (uint32_t j = lane; j < cnt[q]; j += 32)
                 al[p.nmax + j] = plan[3 * (q * r + j) + 1];
         }
+        prof_span(p, 18, pt);
     }
     cta_bar(bar, T);
+    if (warp == 1)
+        prof_span(p, 19, pt);
     trace_at(p, 7);
     // Push list X_i for copy(i): every entry (q, j) of plan(i), over all requesters q (own
     // plan included), whose slot this rank owns, in (q, j) order. copy(i) stores the slot's
@@ -1354,9 +1399,11 @@ __device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t k) {
 
 // per-CTA timeline stamp of engine iteration i (timeline mode), any thread
 __device__ __forceinline__ void run_mark(const RunParams& rp, uint64_t i, int slot) {
+#if DRB_INSTRUMENT
     const StepParams& p = rp.base;
     if (p.timeline && blockIdx.x < kTlMaxCtas)
         p.timeline[(i % p.timeline_steps) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = globaltimer();
+#endif
 }
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
@@ -1490,14 +1537,17 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             if (tid == 0)
                 run_mark(rp, rp.i0 + k, 2);
             sel_core(sp, v, flag[0] != 0);
-            if (b.dbg & 2048)  // experiment: the compute warp's own GPU-scope fence
+            if (DRB_INSTRUMENT && (b.dbg & 2048))  // experiment: the compute warp's own GPU-scope fence
                 __threadfence();
             __syncwarp();
+            unsigned long long pt = 0;
+            prof_span(sp, 19, pt);
             if (tid == 0) {
                 st_release_cta(seen + 2, k + 1);  // hand sel(k) to the publisher
                 run_mark(rp, rp.i0 + k, 3);
                 tl_mark(sp, 0, true);
             }
+            prof_span(sp, 19, pt);
         } else if (k + 1 < rp.steps) {  // warps 2-3: labels of m_{k+1}
             const uint64_t slot = (rp.first_mod + uint32_t(k + 1)) % rp.ring;
             const uint32_t* lp = rp.labels + slot * rp.label_stride;
@@ -1510,7 +1560,12 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             if (bad)
                 atomicOr(&flag[3], 1u);
         }
+        unsigned long long pt2 = 0;
+        if (warp == 0)
+            prof_span(sp, 20, pt2);
         named_bar(1, 96);
+        if (warp == 0)
+            prof_span(sp, 20, pt2);
         if (tid == 0) {
             flag[2] = flag[3];
             run_mark(rp, rp.i0 + k, 4);
@@ -1565,7 +1620,7 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
         tl_mark(sp, 1, false);
         trace_at(sp, 5);
         plan_core(sp, v, T, 3);
-        if (rp.base.dbg & 2048)
+        if (DRB_INSTRUMENT && (rp.base.dbg & 2048))
             __threadfence();
         cta_bar(3, T);
         if (tid == 0) {
@@ -1690,7 +1745,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         const uint64_t i = rp.i0 + k;
         const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
         const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
-        if (b.dbg & 4096) {  // experiment: lists through L2 only
+        if (DRB_INSTRUMENT && (b.dbg & 4096)) {  // experiment: lists through L2 only
             for (uint32_t x = lane; x < pw; x += 32)
                 xraw[x] = __ldcg(xs + x);
             for (uint32_t x = lane; x < ww; x += 32)

@@ -1,4 +1,5 @@
-"""Per-phase cycle accounting of the persistent run's sel / plan CTAs (DRB_DBG 65536|1024):
+"""Per-phase cycle accounting of the persistent run's sel / plan CTAs (DRB_DBG 65536|1024; needs the
+instrumented build: DRB_INSTRUMENT=1 python -c "import __graft_entry__ as g; g.build_library(force=True)"):
 one c2-shape run, single rank. Usage: python tools/prof_run.py [config] [steps]"""
 import os, sys
 os.environ["DRB_DBG"] = str(65536 | 1024)
