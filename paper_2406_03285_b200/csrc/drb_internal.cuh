@@ -295,7 +295,7 @@ __host__ __device__ inline RunSmem run_smem(uint32_t N, uint32_t K, uint32_t r, 
     s.arena_bytes = (left / 2) & ~127u;
     s.arena[0] = take(s.arena_bytes, 128);
     s.arena[1] = take(s.arena_bytes, 128);
-    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax + 8) * 4, plan_b = plan_smem(N, K, r).words * 4;
+    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax + 8 + 112) * 4, plan_b = plan_smem(N, K, r).words * 4;
     const uint32_t ctl = sel_b > plan_b ? sel_b : plan_b;
     s.bytes = off > ctl ? off : ctl;
     if (s.bytes < kSoloSmem)

@@ -26,12 +26,25 @@
 #ifndef DRB_INSTRUMENT
 #define DRB_INSTRUMENT 0
 #endif
+// Critical-chain experiment (tools/): -DDRB_DELAY=1/2/3 adds ~1 us per iteration to the sel /
+// plan / B chain of the persistent run; the chain whose delay moves the step time is the bound.
+#ifndef DRB_DELAY
+#define DRB_DELAY 0
+#endif
 
 namespace drb_b200 {
 
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ void delay_exp(int chain) {
+    if (DRB_DELAY == chain) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < 2000) {
+        }
+    }
+}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.cpp:12-17
     z += kPhi;
@@ -114,12 +127,12 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 //          = A(m) for the latest m<j with s_m == j, else j          (pointer jumping)
 //   sel[j] = A(q) for the latest q<j with s_q == s_j, else s_j.
 // Any rejected draw (probability < k*2^-32) falls back to the literal sequential loop.
-__device__ void warp_select(uint64_t key, uint64_t& ctr, uint32_t n, uint32_t k, uint32_t* sel,
-                            uint32_t* idx) {
+// The fast path alone (k <= 32, n < 2^16): sel[0..k) for draws ctr+1..ctr+k; false (sel
+// untouched) if any of them is rejected. `idx` is 32 words of scratch.
+__device__ bool warp_select_fast(uint64_t key, uint64_t ctr, uint32_t n, uint32_t k, uint32_t* sel,
+                                 uint32_t* idx) {
     const int lane = threadIdx.x & 31;
-    if (k == 0)
-        return;
-    if (k <= 32 && n < 65536u) {  // (mod_small needs n < 2^16; max_batch <= 4096)
+    {
         const uint32_t j = lane;
         uint32_t s = 0xffffffffu;
         bool ok = true;
@@ -150,10 +163,22 @@ __device__ void warp_select(uint64_t key, uint64_t& ctr, uint32_t n, uint32_t k,
             const uint32_t aq = __shfl_sync(kFull, static_cast<uint32_t>(par), q < 0 ? 0 : q);
             if (j < k)
                 sel[j] = q >= 0 ? aq : s;
-            ctr += k;
             __syncwarp();
-            return;
+            return true;
         }
+    }
+    return false;
+}
+
+__device__ void warp_select(uint64_t key, uint64_t& ctr, uint32_t n, uint32_t k, uint32_t* sel,
+                            uint32_t* idx) {
+    const int lane = threadIdx.x & 31;
+    if (k == 0)
+        return;
+    // (mod_small needs n < 2^16; max_batch <= 4096)
+    if (k <= 32 && n < 65536u && warp_select_fast(key, ctr, n, k, sel, idx)) {
+        ctr += k;
+        return;
     }
     for (uint32_t i = lane; i < n; i += 32)
         idx[i] = i;
@@ -476,7 +501,10 @@ __device__ __forceinline__ SelView sel_view(uint32_t* sm, const StepParams& p) {
 // in place to version i+1) and lab (labels of m_i, `bad` if any is >= K), the candidate-write
 // list W_i, the round-(i+1) selection state (p.sel_out, and *v.st in place), stored slot
 // labels, the published occupancy row v=i+1 and the insertion report.
-__device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
+// spec (persistent run): a selection computed ahead for the counter spec_ctr (k = min(c, n)
+// draws, no rejection); used when it matches this round's counter and k.
+__device__ void sel_core(const StepParams& p, const SelView& v, bool bad, const uint32_t* spec = nullptr,
+                         uint64_t spec_ctr = ~0ull) {
     const uint32_t lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap;
@@ -493,7 +521,12 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad) {
     uint64_t evict_ctr = (p.mode & kModeCtrParams) ? p.evict_ctr0 : st->evict_ctr;
     uint32_t appends = 0;
     if (k > 0) {
-        warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
+        if (spec && spec_ctr == cand_ctr && k <= 32) {  // S1 already drawn for this counter
+            sel = const_cast<uint32_t*>(spec);
+            cand_ctr += k;
+        } else {
+            warp_select(p.cand_key, cand_ctr, n, k, sel, kind);
+        }
         trace_at(p, 2);
         warp_assign(p.evict_key, evict_ctr, cap, p.evict_m, k, sel, v.lab, occ, cand_l, cand_slot, v.misc + 32, kind,
                     appends);
@@ -1424,6 +1457,13 @@ __device__ __forceinline__ bool wait_seen(SeenFlag& s, uint64_t want, const RunP
     return true;
 }
 
+__device__ __forceinline__ bool poll_seen(SeenFlag& s, uint64_t want) {  // one acquire load at most
+    if (s.seen >= want)
+        return true;
+    s.seen = ld_acquire_gpu(s.f);
+    return s.seen >= want;
+}
+
 __device__ __forceinline__ void st_release_cta(volatile unsigned long long* p, uint64_t v) {
     asm volatile("st.release.cta.shared.u64 [%0], %1;" ::"r"(smem_u32(const_cast<unsigned long long*>(p))), "l"(v)
                  : "memory");
@@ -1477,12 +1517,21 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
     uint32_t* labs[2] = {v.lab, lab2};
     volatile unsigned long long* seen =  // [0] b_done, [1] plan_done as last loaded; [2] ready
         reinterpret_cast<volatile unsigned long long*>(sm + ((sel_smem(b.K, b.nmax).words + b.nmax + 1) & ~1u));
+    // Speculative S1 (warp 2 draws round k+1's selection during round k; it depends only on
+    // the candidate counter, which round k advances by min(c, n) unless a draw is rejected or
+    // the round inserts nothing): sx[0..1] the counter each parity's selection was drawn for
+    // (~0: none), sx[2] the counter at the start of the current round; spec_sel[2][32].
+    unsigned long long* sx = const_cast<unsigned long long*>(seen) + 4;
+    uint32_t* spec_sel = reinterpret_cast<uint32_t*>(sx + 4);
+    uint32_t* spec_tmp = spec_sel + 64;
     if (tid == 0) {
         sp = b;
         run_patch(sp, rp, 0);
         seen[0] = 0;
         seen[1] = 0;
         seen[2] = 0;
+        sx[0] = ~0ull;
+        sx[1] = ~0ull;
     }
     named_bar(1, kSelThreads);
     {  // state and the own occupancy row at the start of the run (written before the launch)
@@ -1526,6 +1575,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             flag[1] = ok ? 0u : 1u;
             flag[0] = flag[2];  // "bad" of m_k's labels
             flag[3] = 0;
+            sx[2] = v.st->cand_ctr;  // written by this thread in sel_core(k-1)
         }
         named_bar(1, 96);
         if (flag[1])
@@ -1536,7 +1586,8 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             trace_at(sp, 0);
             if (tid == 0)
                 run_mark(rp, rp.i0 + k, 2);
-            sel_core(sp, v, flag[0] != 0);
+            sel_core(sp, v, flag[0] != 0, spec_sel + 32 * (k & 1), sx[k & 1]);
+            delay_exp(1);
             if (DRB_INSTRUMENT && (b.dbg & 2048))  // experiment: the compute warp's own GPU-scope fence
                 __threadfence();
             __syncwarp();
@@ -1548,11 +1599,21 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                 tl_mark(sp, 0, true);
             }
             prof_span(sp, 19, pt);
-        } else if (k + 1 < rp.steps) {  // warps 2-3: labels of m_{k+1}
+        } else if (k + 1 < rp.steps && warp == 2) {  // warp 2: S1 of round k+1, ahead
+            const uint32_t kk = min(sp.c, rp.n);
+            uint64_t drawn = ~0ull;
+            if (kk > 0 && kk <= 32 && rp.n < 65536u) {
+                const uint64_t c1 = sx[2] + kk;
+                if (warp_select_fast(sp.cand_key, c1, rp.n, kk, spec_sel + 32 * ((k + 1) & 1), spec_tmp))
+                    drawn = c1;
+            }
+            if (tid == 64)
+                sx[(k + 1) & 1] = drawn;
+        } else if (k + 1 < rp.steps) {  // warp 3: labels of m_{k+1}
             const uint64_t slot = (rp.first_mod + uint32_t(k + 1)) % rp.ring;
             const uint32_t* lp = rp.labels + slot * rp.label_stride;
             int bad = 0;
-            for (uint32_t x = tid - 64; x < rp.n; x += kSelThreads - 64) {
+            for (uint32_t x = tid - 96; x < rp.n; x += 32) {
                 const uint32_t l = __ldg(lp + x);
                 labs[(k + 1) & 1][x] = l;
                 bad |= l >= sp.K;
@@ -1620,6 +1681,7 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
         tl_mark(sp, 1, false);
         trace_at(sp, 5);
         plan_core(sp, v, T, 3);
+        delay_exp(2);
         if (DRB_INSTRUMENT && (rp.base.dbg & 2048))
             __threadfence();
         cta_bar(3, T);
@@ -1727,36 +1789,37 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
     SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0};
     uint32_t phB = 0;
     int64_t prev_k = -1;  // this warp's previous iteration (stores not yet drained)
+    bool fetched = false;  // this iteration's lists already in flight (prefetched by the previous one)
     if (lane == 0)
         sp = b;
+    auto fetch_lists = [&](uint64_t kk) {  // W_kk and X_kk -> wraw / xraw (cp.async, one group)
+        const uint64_t i = rp.i0 + kk;
+        const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
+        const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
+        for (uint32_t x = lane; x < pw; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xraw + x)), "l"(xs + x) : "memory");
+        for (uint32_t x = lane; x < ww; x += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wraw + x)), "l"(ws + x) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 #pragma unroll 1
     for (uint64_t k = wsel; k < rp.steps; k += 2) {
         bool ok = true;
         if (lane == 0) {
             run_patch(sp, rp, k);
-            ok = wait_seen(sdone, k + 1, rp) && wait_seen(pdone, k + 1, rp);
+            if (!fetched)
+                ok = wait_seen(sdone, k + 1, rp) && wait_seen(pdone, k + 1, rp);
         }
         if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
             break;
+        delay_exp(3);
         __syncwarp();
         tl_mark(sp, 2, false);
         if (lane == 0)
             cta_mark(sp, 0);
-        const uint64_t i = rp.i0 + k;
-        const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
-        const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
-        if (DRB_INSTRUMENT && (b.dbg & 4096)) {  // experiment: lists through L2 only
-            for (uint32_t x = lane; x < pw; x += 32)
-                xraw[x] = __ldcg(xs + x);
-            for (uint32_t x = lane; x < ww; x += 32)
-                wraw[x] = __ldcg(ws + x);
-        } else {
-            for (uint32_t x = lane; x < pw; x += 32)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(xraw + x)), "l"(xs + x) : "memory");
-            for (uint32_t x = lane; x < ww; x += 32)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wraw + x)), "l"(ws + x) : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (!fetched)
+            fetch_lists(k);
+        fetched = false;
         copy_parse(sp, xraw, wraw, jsrc, nullptr, misc, ready, true, true, false);
         const uint32_t nj = misc[0], nw = misc[1];
         uint32_t* wk = wrows + (k & 3) * nslot;  // publish W_k's rows for B(k+1)
@@ -1834,6 +1897,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
             }
         }
         __syncwarp();
+
         if (lane == 0)
             cta_mark(sp, 12);
         bool drained = false;
@@ -1866,10 +1930,8 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         }
         for (uint32_t p0 = 0; p0 < pieces; p0 += per_win) {
             const uint32_t p1 = min(pieces, p0 + per_win);
-            if (p0 > 0) {
-                bulk_wait_read_all();  // arena reuse
-                __syncwarp();
-            }
+            bulk_wait_read_all();  // arena reuse (p0 = 0: this warp's previous iteration's stores)
+            __syncwarp();
             if (lane == 0)
                 mbar_expect_tx(barB, (p1 - p0) * clen);
             for (uint32_t x = p0 + lane; x < p1; x += 32)
@@ -1898,13 +1960,21 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
             drain();
         if (pieces == 0 && lane == 0)
             fl->landed[k & 1] = k + 1;
+        // xraw / wraw are free (paddr holds this iteration's addresses): fetch this warp's next
+        // lists now if sel / plan already published them, so the L2 round trip overlaps the
+        // stores in flight instead of starting the next iteration
+        if (k + 2 < rp.steps) {
+            bool pre = false;
+            if (lane == 0)
+                pre = poll_seen(sdone, k + 3) && poll_seen(pdone, k + 3);
+            if (__shfl_sync(kFull, pre ? 1 : 0, 0)) {
+                fetch_lists(k + 2);
+                fetched = true;
+            }
+        }
         prev_k = int64_t(k);
         if (lane == 0)
             cta_mark(sp, 4);
-        bulk_wait_read_all();  // arena free before this warp's next iteration
-        __syncwarp();
-        if (lane == 0)
-            cta_mark(sp, 9);
     }
     if (prev_k >= 0 && !*reinterpret_cast<volatile uint32_t*>(&rp.ctl->error)) {
         bulk_wait_all();
