@@ -1757,6 +1757,14 @@ __device__ bool smem_wait_ge(const volatile unsigned long long* f, uint64_t want
     return true;
 }
 
+// B(k)'s stores are complete (after bulk_wait_all): hand them to the CTA's arrival warp. The
+// proxy fence orders the async-proxy stores before the CTA-scope release; the arrival warp's
+// acquire and its GPU-scope acq_rel ticket atomic carry them on (cumulativity).
+__device__ __forceinline__ void b_complete(volatile BFlags* fl, uint64_t k) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    st_release_cta(&fl->complete[k & 1], k + 1);
+}
+
 // One B engine (a warp) of a copy CTA, for the iterations k = first, first+2, ...: the W_k
 // writes and X_k pushes on this CTA's byte column [c0, c1). The two B warps alternate, so
 // B(k+1) issues its loads while B(k) drains; what must stay ordered between consecutive
@@ -1780,7 +1788,6 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
     volatile uint32_t* ready = misc + 6;
     const uint32_t part = blockIdx.x - 2, parts = rp.copy_ctas;
     const uint64_t S = b.S;
-    const bool multi = (b.mode & kModePeers) && b.N > 1;
     const uint64_t c16 = S >> 4;
     const uint64_t c0 = (c16 * part / parts) << 4, c1 = (c16 * (part + 1) / parts) << 4;
     const uint32_t clen = static_cast<uint32_t>(c1 - c0);
@@ -1904,10 +1911,8 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         auto drain = [&]() {  // this warp's previous iteration (k-2): stores complete, arrive
             bulk_wait_all();
             __syncwarp();
-            if (lane == 0 && prev_k >= 0) {
-                fl->complete[prev_k & 1] = uint64_t(prev_k) + 1;
-                run_b_arrive(rp, sp, uint64_t(prev_k), multi);
-            }
+            if (lane == 0 && prev_k >= 0)
+                b_complete(fl, uint64_t(prev_k));
             prev_k = -1;
             drained = true;
         };
@@ -1979,10 +1984,8 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
     if (prev_k >= 0 && !*reinterpret_cast<volatile uint32_t*>(&rp.ctl->error)) {
         bulk_wait_all();
         __syncwarp();
-        if (lane == 0) {
-            fl->complete[prev_k & 1] = uint64_t(prev_k) + 1;
-            run_b_arrive(rp, sp, uint64_t(prev_k), multi);
-        }
+        if (lane == 0)
+            b_complete(fl, uint64_t(prev_k));
     }
 }
 
@@ -1993,7 +1996,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
 // grid-wide hand-off between iterations.
 __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2) {
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (warp >= 3)
+    if (warp >= 4)
         return;
     const StepParams& b = rp.base;
     const RunSmem R = run_smem(b.N, b.K, b.r, b.nmax);
@@ -2011,9 +2014,36 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    named_bar(2, 96);
+    named_bar(2, 128);
     if (warp == 0 || warp == 2) {
         run_b_warp(rp, sm, R, sp2[warp >> 1], warp >> 1);
+        return;
+    }
+    if (warp == 3) {  // arrival warp: B(k) complete -> ticket / b_done / pushdone, in order, off
+                      // the B engines' own chains (the GPU-scope atomic waits on the memory system)
+        if (lane != 0)
+            return;
+        volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
+        const bool multi = (b.mode & kModePeers) && b.N > 1;
+#pragma unroll 1
+        for (uint64_t k = 0; k < rp.steps; ++k) {
+            uint64_t t0 = 0;
+            for (uint32_t spin = 0; ld_acquire_cta(&fl->complete[k & 1]) < k + 1; ++spin) {
+                if ((spin & 63) == 63) {
+                    if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+                        return;
+                    const uint64_t now = globaltimer();
+                    if (t0 == 0)
+                        t0 = now;
+                    else if (now - t0 > b.timeout_ns) {
+                        if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
+                            rp.ctl->where = (8u << 24) | uint32_t(k & 0xffffff);
+                        return;
+                    }
+                }
+            }
+            run_b_arrive(rp, b, k, multi);
+        }
         return;
     }
     // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
