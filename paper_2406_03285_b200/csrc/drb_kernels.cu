@@ -1732,7 +1732,7 @@ struct BFlags {
     unsigned long long landed[2];    // k+1: B(k)'s loads landed (its reads are done)
     unsigned long long complete[2];  // k+1: B(k)'s stores complete
     unsigned long long parsed[4];    // k+1 in slot k % 4: W_k's slab rows published in wrows[k % 4]
-    unsigned long long counted;      // k+1: m'_i's counts written (part 0)
+    unsigned long long pad;
 };
 // Bounded like every other wait: gives up once the run failed or after timeout_ns (then
 // fails the run, recording `site` and the iteration), so no role can spin forever.
@@ -1838,16 +1838,6 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         __threadfence_block();
         if (lane == 0)
             fl->parsed[k & 3] = k + 1;
-        if (part == 0) {  // m'_i's counts after m'_{i-1}'s (repcnt hand-off)
-            if (lane == 0 && k > 0)
-                smem_wait_ge(&fl->counted, k, rp, 1, k);
-            __syncwarp();
-            copy_counts(sp, xraw);
-            __syncwarp();
-            __threadfence_block();
-            if (lane == 0)
-                fl->counted = k + 1;
-        }
         if (lane == 0)
             cta_mark(sp, 10);
         // W_{k-1} (the other warp's) for the hazard checks
@@ -2021,28 +2011,64 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
     }
     if (warp == 3) {  // arrival warp: B(k) complete -> ticket / b_done / pushdone, in order, off
                       // the B engines' own chains (the GPU-scope atomic waits on the memory system)
-        if (lane != 0)
-            return;
+        // CTA part 0 also writes m'_k's counts and batch labels here (copy_counts' job on the
+        // three-kernel path), in iteration order: |reps(k-1)| stays in a register, and the
+        // X list's |reps(k)| is read before this CTA's arrival lets plan(k+8) reuse its slot.
         volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
         const bool multi = (b.mode & kModePeers) && b.N > 1;
+        RegionHeader* hdr = reinterpret_cast<RegionHeader*>(b.region[b.me]);
+        const uint32_t row0 = b.nmax - rp.n;
+        uint32_t prev = 0;
 #pragma unroll 1
         for (uint64_t k = 0; k < rp.steps; ++k) {
-            uint64_t t0 = 0;
-            for (uint32_t spin = 0; ld_acquire_cta(&fl->complete[k & 1]) < k + 1; ++spin) {
-                if ((spin & 63) == 63) {
-                    if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
-                        return;
-                    const uint64_t now = globaltimer();
-                    if (t0 == 0)
-                        t0 = now;
-                    else if (now - t0 > b.timeout_ns) {
-                        if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
-                            rp.ctl->where = (8u << 24) | uint32_t(k & 0xffffff);
-                        return;
+            bool ok = true;
+            if (lane == 0) {
+                uint64_t t0 = 0;
+                for (uint32_t spin = 0; ok && ld_acquire_cta(&fl->complete[k & 1]) < k + 1; ++spin) {
+                    if ((spin & 63) == 63) {
+                        if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error)) {
+                            ok = false;
+                            break;
+                        }
+                        const uint64_t now = globaltimer();
+                        if (t0 == 0)
+                            t0 = now;
+                        else if (now - t0 > b.timeout_ns) {
+                            if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
+                                rp.ctl->where = (8u << 24) | uint32_t(k & 0xffffff);
+                            ok = false;
+                        }
                     }
                 }
             }
-            run_b_arrive(rp, b, k, multi);
+            if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
+                return;
+            if (part == 0) {
+                const uint64_t i = rp.i0 + k;
+                const uint32_t aslot = static_cast<uint32_t>(i % kAugRing);
+                const uint32_t* lab = rp.labels + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.label_stride;
+                uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
+                               uint64_t(aslot) * b.auglab_slot_elems;
+#pragma unroll 1
+                for (uint32_t x = lane; x < rp.n; x += 32)
+                    al[row0 + x] = __ldg(lab + x);
+                if (lane == 0) {
+                    if (k == 0)
+                        prev = i > 0 ? __ldcg(&hdr->repcnt[aslot]) : 0u;
+                    const uint32_t nrep = __ldcg(rp.plist_base + (i % kListRing) * rp.pw);  // |reps(k)|
+                    hdr->aug_count[aslot] = rp.n + prev;
+                    hdr->repcnt[(aslot + 1) % kAugRing] = nrep;
+                    if (b.mailbox) {
+                        volatile uint32_t* mb = b.mailbox;
+                        mb[aslot] = rp.n + prev;
+                        mb[kAugRing + aslot] = 0;
+                    }
+                    prev = nrep;
+                }
+                __syncwarp();
+            }
+            if (lane == 0)
+                run_b_arrive(rp, b, k, multi);
         }
         return;
     }
