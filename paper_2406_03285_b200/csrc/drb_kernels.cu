@@ -2012,50 +2012,62 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
     if (warp == 3) {  // arrival warp: B(k) complete -> ticket / b_done / pushdone, in order, off
                       // the B engines' own chains (the GPU-scope atomic waits on the memory system)
         // CTA part 0 also writes m'_k's counts and batch labels here (copy_counts' job on the
-        // three-kernel path), in iteration order: |reps(k-1)| stays in a register, and the
-        // X list's |reps(k)| is read before this CTA's arrival lets plan(k+8) reuse its slot.
+        // three-kernel path), in iteration order, while B(k) still runs: they need only plan(k)
+        // (seen through the B engines' `parsed`), |reps(k-1)| stays in a register, and the X
+        // list's |reps(k)| is read before this CTA's arrival lets plan(k+8) reuse its slot.
         volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
         const bool multi = (b.mode & kModePeers) && b.N > 1;
         RegionHeader* hdr = reinterpret_cast<RegionHeader*>(b.region[b.me]);
         const uint32_t row0 = b.nmax - rp.n;
         uint32_t prev = 0;
-#pragma unroll 1
-        for (uint64_t k = 0; k < rp.steps; ++k) {
-            bool ok = true;
-            if (lane == 0) {
-                uint64_t t0 = 0;
-                for (uint32_t spin = 0; ok && ld_acquire_cta(&fl->complete[k & 1]) < k + 1; ++spin) {
-                    if ((spin & 63) == 63) {
-                        if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error)) {
-                            ok = false;
-                            break;
-                        }
-                        const uint64_t now = globaltimer();
-                        if (t0 == 0)
-                            t0 = now;
-                        else if (now - t0 > b.timeout_ns) {
-                            if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
-                                rp.ctl->where = (8u << 24) | uint32_t(k & 0xffffff);
-                            ok = false;
-                        }
+        auto wait_cta = [&](const volatile unsigned long long* f, uint64_t want, uint64_t k) {
+            if (lane != 0)
+                return true;
+            uint64_t t0 = 0;
+            for (uint32_t spin = 0; ld_acquire_cta(f) < want; ++spin) {
+                if ((spin & 63) == 63) {
+                    if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+                        return false;
+                    const uint64_t now = globaltimer();
+                    if (t0 == 0)
+                        t0 = now;
+                    else if (now - t0 > b.timeout_ns) {
+                        if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
+                            rp.ctl->where = (8u << 24) | uint32_t(k & 0xffffff);
+                        return false;
                     }
                 }
             }
-            if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
-                return;
+            return true;
+        };
+#pragma unroll 1
+        for (uint64_t k = 0; k < rp.steps; ++k) {
             if (part == 0) {
+                if (!__shfl_sync(kFull, wait_cta(&fl->parsed[k & 3], k + 1, k) ? 1 : 0, 0))
+                    return;
                 const uint64_t i = rp.i0 + k;
                 const uint32_t aslot = static_cast<uint32_t>(i % kAugRing);
                 const uint32_t* lab = rp.labels + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.label_stride;
                 uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
                                uint64_t(aslot) * b.auglab_slot_elems;
-#pragma unroll 1
-                for (uint32_t x = lane; x < rp.n; x += 32)
-                    al[row0 + x] = __ldg(lab + x);
+                uint32_t nrep = 0;
+                if (lane == 0)
+                    nrep = __ldcg(rp.plist_base + (i % kListRing) * rp.pw);  // |reps(k)|
+                if (rp.n <= 64) {  // both label loads in flight at once
+                    const uint32_t l0 = lane < rp.n ? __ldg(lab + lane) : 0u;
+                    const uint32_t l1 = lane + 32 < rp.n ? __ldg(lab + lane + 32) : 0u;
+                    if (lane < rp.n)
+                        al[row0 + lane] = l0;
+                    if (lane + 32 < rp.n)
+                        al[row0 + lane + 32] = l1;
+                } else {
+#pragma unroll 4
+                    for (uint32_t x = lane; x < rp.n; x += 32)
+                        al[row0 + x] = __ldg(lab + x);
+                }
                 if (lane == 0) {
                     if (k == 0)
                         prev = i > 0 ? __ldcg(&hdr->repcnt[aslot]) : 0u;
-                    const uint32_t nrep = __ldcg(rp.plist_base + (i % kListRing) * rp.pw);  // |reps(k)|
                     hdr->aug_count[aslot] = rp.n + prev;
                     hdr->repcnt[(aslot + 1) % kAugRing] = nrep;
                     if (b.mailbox) {
@@ -2067,6 +2079,9 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                 }
                 __syncwarp();
             }
+            if (!__shfl_sync(kFull, wait_cta(&fl->complete[k & 1], k + 1, k) ? 1 : 0, 0))
+                return;
+            delay_exp(4);
             if (lane == 0)
                 run_b_arrive(rp, b, k, multi);
         }
