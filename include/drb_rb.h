@@ -261,6 +261,51 @@ DRB_RB_API drb_status drb_rb_timeline_read(drb_rb* h, uint64_t* out, uint32_t* s
 DRB_RB_API drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads,
                                          uint32_t* smem);
 
+/* ---- Input side: the producer of m ----------------------------
+ * A DRDS dataset file (proj/src/scenario/dataset.hpp:10-17: "DRDS", u16 version 1,
+ * u64 count, u32 feature_dim, u32 n_classes, count x {feature_dim f32, u32 label}, all LE;
+ * optional "<path>.split" sidecar) resident in HBM as SoA features [count][feature_dim*4 B]
+ * + u32 labels[count]. Sample bytes S = feature_dim*4 match a rehearsal buffer whose
+ * sample_bytes is S, so drb_ds_gather output feeds drb_rb_step / drb_rb_run directly. */
+typedef struct drb_ds drb_ds;
+/* load_dataset (proj/src/scenario/dataset.cpp:102-143): same checks, same order, same
+ * messages; every failure is DRB_ERR_IO (io_error). */
+DRB_RB_API drb_status drb_ds_load(const char* path, int32_t device, drb_ds** out);
+DRB_RB_API drb_status drb_ds_destroy(drb_ds* ds);
+/* dataset::size / feature_dim / n_classes / train_count / eval_count (dataset.hpp:19-27). */
+DRB_RB_API drb_status drb_ds_info(const drb_ds* ds, uint64_t* count, uint32_t* feature_dim,
+                                  uint32_t* n_classes, uint64_t* train_count,
+                                  uint64_t* eval_count);
+DRB_RB_API drb_status drb_ds_device_views(const drb_ds* ds, void** features, uint32_t** labels);
+/* train_indices_of (eval = 0) / eval_indices_of (eval = 1) (dataset.cpp:48-64): ascending
+ * dataset indices whose label is in classes[0..n_classes). *n_out = the full count; at most
+ * cap are written (out = NULL, cap = 0 queries the count). */
+DRB_RB_API drb_status drb_ds_indices_of(const drb_ds* ds, const uint32_t* classes,
+                                        uint32_t n_classes, int32_t eval, uint64_t* out,
+                                        uint64_t cap, uint64_t* n_out);
+/* dataset::gather (dataset.cpp:66-72) on the device, ordered on `stream`: out_batch row j
+ * (S bytes) and out_labels[j] (may be NULL) = record indices[j]. indices is a DEVICE array
+ * of n u64. An index >= count leaves row j untouched and sets bit 0 of the device error
+ * word (drb_ds_device_error). */
+DRB_RB_API drb_status drb_ds_gather(const drb_ds* ds, const uint64_t* indices, uint32_t n,
+                                    void* out_batch, uint32_t* out_labels, void* stream);
+/* Synchronizes the device, returns and clears the gather error word. */
+DRB_RB_API drb_status drb_ds_device_error(const drb_ds* ds, uint32_t* out);
+/* make_schedule (proj/src/scenario/schedule.cpp:10-35): classes[K] = the seeded class
+ * permutation, task t = the next task_sizes[t] entries. T == 0 or T > K -> DRB_ERR_CONFIG. */
+DRB_RB_API drb_status drb_make_schedule(uint32_t n_classes, uint32_t n_tasks, uint64_t seed,
+                                        uint32_t* classes, uint32_t* task_sizes);
+/* shard_batches (schedule.cpp:37-62), flattened: this worker's shard in order; batch b is
+ * entries [b*batch_size, (b+1)*batch_size). *n_out = shard size; at most cap written.
+ * worker >= n_workers -> DRB_ERR_USAGE (usage_error); batch_size 0 -> DRB_ERR_USAGE. */
+DRB_RB_API drb_status drb_shard_batches(const uint64_t* task_data, uint64_t n, uint32_t worker,
+                                        uint32_t n_workers, uint32_t batch_size, uint64_t seed,
+                                        uint64_t task_index, uint64_t epoch, uint64_t* out,
+                                        uint64_t cap, uint64_t* n_out);
+/* lockstep_batches (schedule.cpp:64-69). */
+DRB_RB_API drb_status drb_lockstep_batches(uint64_t task_size, uint32_t n_workers,
+                                           uint32_t batch_size, uint64_t* out);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

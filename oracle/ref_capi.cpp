@@ -22,6 +22,8 @@
 #include "engine/engine.hpp"
 #include "metrics/metrics.hpp"
 #include "runner/mesh.hpp"
+#include "scenario/dataset.hpp"
+#include "scenario/schedule.hpp"
 #include "sampler/sampler.hpp"
 #include "sampler/size_table.hpp"
 #include "transport/socket.hpp"
@@ -364,6 +366,101 @@ int ref_bias_report(const std::uint64_t* counts, std::uint64_t n, std::uint64_t 
     } catch (...) {
         return 8;
     }
+}
+
+// ---- input side: DRDS files, class-incremental schedule, shards ----
+
+// synth_dataset + write_dataset (proj/src/scenario/dataset.cpp): the reference's own writer.
+int ref_write_synth_dataset(const char* path, std::uint32_t n_classes, std::uint32_t per_class,
+                            std::uint32_t feature_dim, double separation, std::uint64_t seed) {
+    try {
+        write_dataset(synth_dataset(n_classes, per_class, feature_dim, separation, seed), path);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// load_dataset: 0 ok, 3 io_error (message into err), -1 other. out_* may be NULL (header only).
+int ref_load_dataset(const char* path, std::uint64_t* count, std::uint32_t* dim,
+                     std::uint32_t* n_classes, std::uint64_t* train, std::uint64_t* eval,
+                     float* out_features, std::uint32_t* out_labels, char* err, std::size_t err_len) {
+    try {
+        const dataset d = load_dataset(path);
+        *count = d.size();
+        *dim = d.feature_dim;
+        *n_classes = d.n_classes;
+        *train = d.train_count;
+        *eval = d.eval_count;
+        if (out_features)
+            std::memcpy(out_features, d.features.data(), d.features.size() * sizeof(float));
+        if (out_labels)
+            std::memcpy(out_labels, d.labels.data(), d.labels.size() * sizeof(std::uint32_t));
+        return 0;
+    } catch (const io_error& e) {
+        if (err && err_len) {
+            std::strncpy(err, e.what(), err_len - 1);
+            err[err_len - 1] = 0;
+        }
+        return 3;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// train_indices_of / eval_indices_of; returns the count, writes up to cap.
+std::uint64_t ref_indices_of(const char* path, const std::uint32_t* classes, std::uint32_t n,
+                             int eval, std::uint64_t* out, std::uint64_t cap) {
+    const dataset d = load_dataset(path);
+    const std::vector<class_id> cls(classes, classes + n);
+    const auto v = eval ? d.eval_indices_of(cls) : d.train_indices_of(cls);
+    for (std::size_t i = 0; i < v.size() && i < cap; ++i)
+        out[i] = v[i];
+    return v.size();
+}
+
+int ref_make_schedule(std::uint32_t K, std::uint32_t T, std::uint64_t seed, std::uint32_t* classes,
+                      std::uint32_t* sizes) {
+    try {
+        const auto s = make_schedule(K, T, seed);
+        std::size_t c = 0;
+        for (std::uint32_t t = 0; t < T; ++t) {
+            sizes[t] = static_cast<std::uint32_t>(s.tasks[t].size());
+            for (const auto k : s.tasks[t])
+                classes[c++] = k;
+        }
+        return 0;
+    } catch (const config_error&) {
+        return 2;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// shard_batches flattened: batches concatenated in order (batch boundaries every `batch`).
+int ref_shard_batches(const std::uint64_t* task_data, std::uint64_t n, std::uint32_t worker,
+                      std::uint32_t n_workers, std::uint32_t batch, std::uint64_t seed,
+                      std::uint64_t task_index, std::uint64_t epoch, std::uint64_t* out,
+                      std::uint64_t* n_out, std::uint64_t* n_batches) {
+    try {
+        const std::vector<std::size_t> td(task_data, task_data + n);
+        const auto b = shard_batches(td, worker, n_workers, batch, seed, task_index, epoch);
+        std::uint64_t c = 0;
+        for (const auto& v : b)
+            for (const auto i : v)
+                out[c++] = i;
+        *n_out = c;
+        *n_batches = b.size();
+        return 0;
+    } catch (const usage_error&) {
+        return 7;
+    } catch (...) {
+        return -1;
+    }
+}
+
+std::uint64_t ref_lockstep_batches(std::uint64_t task_size, std::uint32_t n_workers, std::uint32_t batch) {
+    return lockstep_batches(task_size, n_workers, batch);
 }
 
 } // extern "C"

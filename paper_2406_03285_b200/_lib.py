@@ -49,7 +49,12 @@ class usage_error(drb_error):
     status = DRB_ERR_USAGE
 
 
-_BY_STATUS = {c.status: c for c in (invalid_argument, config_error, transport_error, engine_error, usage_error)}
+class io_error(drb_error):
+    status = DRB_ERR_IO
+
+
+_BY_STATUS = {c.status: c for c in (invalid_argument, config_error, io_error, transport_error, engine_error,
+                                    usage_error)}
 
 
 class drb_rng(C.Structure):
@@ -140,6 +145,16 @@ def _load():
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),
+        "drb_ds_load": (st, [C.c_char_p, i32, P(vp)]),
+        "drb_ds_destroy": (st, [vp]),
+        "drb_ds_info": (st, [vp, P(u64), P(u32), P(u32), P(u64), P(u64)]),
+        "drb_ds_device_views": (st, [vp, P(vp), P(vp)]),
+        "drb_ds_indices_of": (st, [vp, vp, u32, i32, vp, u64, P(u64)]),
+        "drb_ds_gather": (st, [vp, vp, u32, vp, vp, vp]),
+        "drb_ds_device_error": (st, [vp, P(u32)]),
+        "drb_make_schedule": (st, [u32, u32, u64, vp, vp]),
+        "drb_shard_batches": (st, [vp, u64, u32, u32, u32, u64, u64, u64, vp, u64, P(u64)]),
+        "drb_lockstep_batches": (st, [u64, u32, u32, P(u64)]),
         "drb_rb_bias_test": (st, [u32, u32, u32, u64, u64, u64, i32, vp, P(C.c_double), P(C.c_double), i32]),
         "drb_rb_trace_read": (st, [vp, vp]),
         "drb_rb_timeline_read": (st, [vp, vp, P(u32)]),

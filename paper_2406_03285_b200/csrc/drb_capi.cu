@@ -123,6 +123,11 @@ struct dev_tmp {
 
 }  // namespace
 
+namespace drb_b200 {
+// Shared with drb_dataset.cu: one thread-local last error for the whole C ABI.
+void set_last_error(const char* what) { t_last_error = what; }
+}  // namespace drb_b200
+
 struct drb_rb {
     drb_rb_config cfg{};
     RegionLayout layout{};

@@ -1,0 +1,443 @@
+// Input side of the hot path: the producer of m.
+//
+//   DRDS dataset file -> HBM (load_dataset, proj/src/scenario/dataset.cpp:102-143)
+//   class-incremental schedule and per-worker shards (proj/src/scenario/schedule.cpp:10-69)
+//   dataset::gather of a batch of records into m (proj/src/scenario/dataset.cpp:66-72)
+//
+// HBM layout: the file's record-interleaved [count][dim f32 | u32 label] is split on the
+// device into SoA features [count][dim*4 B] (rows 16 B aligned whenever dim % 4 == 0) and
+// labels u32[count], so a batch gather is a straight row copy into the rehearsal buffer's
+// m layout ([b][S] bytes + u32 labels[b], S = dim*4). The file is streamed through two
+// pinned staging buffers; each chunk's H2D copy overlaps the next chunk's read, and the
+// split kernel runs per chunk on the device.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "drb_internal.cuh"
+
+namespace drb_b200 {
+void set_last_error(const char* what);
+}
+
+struct drb_ds {
+    int device = 0;
+    uint64_t count = 0, train = 0, eval = 0;
+    uint32_t dim = 0, n_classes = 0;
+    uint8_t* features = nullptr;  // [count][dim*4]
+    uint32_t* labels = nullptr;   // [count]
+    uint32_t* err = nullptr;      // device error word of gathers (bit 0: index out of range)
+    std::vector<uint32_t> host_labels;
+    ~drb_ds() {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        cudaFree(features);
+        cudaFree(labels);
+        cudaFree(err);
+        if (prev >= 0)
+            cudaSetDevice(prev);
+    }
+};
+
+namespace {
+
+struct ds_error : std::runtime_error {
+    drb_status code;
+    ds_error(drb_status c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+[[noreturn]] void fail(drb_status c, const std::string& w) { throw ds_error(c, w); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(DRB_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+drb_status guarded(F&& f) {
+    try {
+        f();
+        return DRB_OK;
+    } catch (const ds_error& e) {
+        drb_b200::set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        drb_b200::set_last_error("out of memory");
+        return DRB_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        drb_b200::set_last_error(e.what());
+        return DRB_ERR_INTERNAL;
+    }
+}
+
+#define DS_REQUIRE(cond)                                  \
+    do {                                                  \
+        if (!(cond)) {                                    \
+            drb_b200::set_last_error("null argument");    \
+            return DRB_ERR_INVALID_ARGUMENT;              \
+        }                                                 \
+    } while (0)
+
+struct device_scope {
+    int prev = -1;
+    explicit device_scope(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev)
+            cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~device_scope() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev)
+            cudaSetDevice(prev);
+    }
+};
+
+// ---- host splitmix stream (rng.cpp:12-53): shuffles of the input side only ----
+constexpr uint64_t kPhiH = 0x9e3779b97f4a7c15ULL;
+uint64_t mix(uint64_t z) {
+    z += kPhiH;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+struct host_rng {
+    uint64_t key, ctr = 0;
+    // rng_stream::keyed(seed, worker, purpose, k1, k2) (rng.cpp:19-39): k1+1, k2+1 folded in.
+    host_rng(uint64_t seed, uint64_t worker, uint64_t purpose, uint64_t k1, uint64_t k2) {
+        key = mix(seed);
+        key = mix(key ^ (worker * 0xd1342543de82ef95ULL));
+        key = mix(key ^ (purpose * 0xaf251af3b0f025b5ULL));
+        key = mix(key ^ (k1 + 1));
+        key = mix(key ^ (k2 + 1));
+    }
+    uint64_t next() { return mix(key ^ (++ctr * kPhiH)); }
+    uint64_t bounded(uint64_t n) {  // rng.cpp:45-53
+        const uint64_t thr = (0 - n) % n;
+        for (;;) {
+            const uint64_t v = next();
+            if (v >= thr)
+                return v % n;
+        }
+    }
+};
+constexpr uint64_t kDataShuffle = 4;  // rng.hpp purpose::data_shuffle
+
+// ---- kernels ----
+
+// One chunk of records [dim words | label word] -> SoA features rows (labels come from the
+// host pass). Word-granular grid-stride loop: reads fully coalesced, writes coalesced
+// within each row.
+__global__ void ds_split_kernel(const uint32_t* __restrict__ rec, uint64_t n_words, uint32_t dim,
+                                uint32_t* __restrict__ feat) {
+    const uint32_t stride = dim + 1;
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_words;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = w / stride;
+        const uint32_t f = uint32_t(w - r * stride);
+        if (f < dim)
+            feat[r * dim + f] = rec[w];
+    }
+}
+
+// m[j] = features[idx[j]], labels[j] = labels[idx[j]] (dataset.cpp:66-72). blockIdx.y walks
+// the batch rows, blockIdx.x the 16 B (or 4 B) words of a row.
+template <typename V>
+__global__ void ds_gather_kernel(const uint8_t* __restrict__ feat, const uint32_t* __restrict__ labels,
+                                 uint64_t count, uint64_t row_bytes, const uint64_t* __restrict__ idx,
+                                 uint32_t n, uint8_t* __restrict__ out, uint32_t* __restrict__ out_labels,
+                                 uint32_t* err) {
+    const uint64_t row_words = row_bytes / sizeof(V);
+    for (uint32_t j = blockIdx.y; j < n; j += gridDim.y) {
+        const uint64_t i = idx[j];
+        if (i >= count) {
+            if (blockIdx.x == 0 && threadIdx.x == 0)
+                atomicOr(err, 1u);
+            continue;
+        }
+        const V* src = reinterpret_cast<const V*>(feat + i * row_bytes);
+        V* dst = reinterpret_cast<V*>(out + uint64_t(j) * row_bytes);
+        for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < row_words;
+             w += uint64_t(gridDim.x) * blockDim.x)
+            dst[w] = __ldg(src + w);
+        if (out_labels && blockIdx.x == 0 && threadIdx.x == 0)
+            out_labels[j] = labels[i];
+    }
+}
+
+uint64_t read_le(const uint8_t* p, int n) {
+    uint64_t v = 0;
+    for (int i = 0; i < n; ++i)
+        v |= uint64_t(p[i]) << (8 * i);
+    return v;
+}
+
+struct file_closer {
+    void operator()(FILE* f) const {
+        if (f)
+            fclose(f);
+    }
+};
+
+struct pinned {
+    void* p = nullptr;
+    ~pinned() { cudaFreeHost(p); }
+};
+struct devbuf {
+    void* p = nullptr;
+    ~devbuf() { cudaFree(p); }
+};
+
+}  // namespace
+
+extern "C" {
+
+drb_status drb_ds_load(const char* path, int32_t device, drb_ds** out) {
+    DS_REQUIRE(path && out);
+    return guarded([&] {
+        const std::string P(path);
+        std::unique_ptr<FILE, file_closer> f(fopen(path, "rb"));
+        if (!f)
+            fail(DRB_ERR_IO, "cannot open dataset file: " + P);
+        uint8_t hdr[22];
+        const size_t got = fread(hdr, 1, sizeof hdr, f.get());
+        if (got < 4 || std::memcmp(hdr, "DRDS", 4) != 0)
+            fail(DRB_ERR_IO, "not a dataset file (bad magic): " + P);
+        if (got < 6)
+            fail(DRB_ERR_IO, "truncated dataset file: " + P);
+        const uint64_t version = read_le(hdr + 4, 2);
+        if (version != 1)
+            fail(DRB_ERR_IO, "unsupported dataset version " + std::to_string(version) + ": " + P);
+        if (got < sizeof hdr)
+            fail(DRB_ERR_IO, "truncated dataset file: " + P);
+        std::unique_ptr<drb_ds> ds(new drb_ds);
+        ds->device = device;
+        ds->count = read_le(hdr + 6, 8);
+        ds->dim = uint32_t(read_le(hdr + 14, 4));
+        ds->n_classes = uint32_t(read_le(hdr + 18, 4));
+        const uint64_t rec_words = uint64_t(ds->dim) + 1, rec_bytes = rec_words * 4;
+        device_scope g(device);
+        const uint64_t row_bytes = uint64_t(ds->dim) * 4;
+        // an absurd header count fails as truncated before anything is allocated
+        fseek(f.get(), 0, SEEK_END);
+        const uint64_t fsize = uint64_t(ftell(f.get()));
+        fseek(f.get(), long(sizeof hdr), SEEK_SET);
+        const uint64_t avail = (fsize - sizeof hdr) / rec_bytes;
+        const uint64_t alloc_n = std::min(ds->count, avail);
+        ds->host_labels.resize(alloc_n);
+        cuda_check(cudaMalloc(&ds->features, std::max<uint64_t>(alloc_n * row_bytes, 16)), "ds features");
+        cuda_check(cudaMalloc(&ds->labels, std::max<uint64_t>(alloc_n * 4, 4)), "ds labels");
+        cuda_check(cudaMalloc(&ds->err, 4), "ds err");
+        cuda_check(cudaMemset(ds->err, 0, 4), "ds err");
+        cudaStream_t st;
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "ds stream");
+        std::shared_ptr<void> st_guard(nullptr, [&](void*) { cudaStreamDestroy(st); });
+        const uint64_t chunk_recs =
+            std::max<uint64_t>(1, std::min<uint64_t>(alloc_n, (64ull << 20) / rec_bytes));
+        pinned h[2];
+        devbuf d[2];
+        cudaEvent_t ev[2];
+        for (int b = 0; b < 2; ++b) {
+            cuda_check(cudaMallocHost(&h[b].p, chunk_recs * rec_bytes), "ds staging");
+            cuda_check(cudaMalloc(&d[b].p, chunk_recs * rec_bytes), "ds staging");
+            cuda_check(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming), "ds event");
+        }
+        std::shared_ptr<void> ev_guard(nullptr, [&](void*) {
+            cudaEventDestroy(ev[0]);
+            cudaEventDestroy(ev[1]);
+        });
+        int dev_sms = 148;
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+        uint64_t base = 0;
+        for (int b = 0; base < alloc_n; b ^= 1) {
+            const uint64_t nrec = std::min(chunk_recs, alloc_n - base);
+            cuda_check(cudaEventSynchronize(ev[b]), "ds staging reuse");
+            if (fread(h[b].p, rec_bytes, nrec, f.get()) != nrec)
+                fail(DRB_ERR_IO, "truncated dataset file: " + P);
+            const uint32_t* w = static_cast<const uint32_t*>(h[b].p);
+            for (uint64_t r = 0; r < nrec; ++r) {
+                const uint32_t lab = w[r * rec_words + ds->dim];
+                if (lab >= ds->n_classes)
+                    fail(DRB_ERR_IO, "dataset label out of range at record " + std::to_string(base + r) +
+                                         ": " + P);
+                ds->host_labels[base + r] = lab;
+            }
+            cuda_check(cudaMemcpyAsync(d[b].p, h[b].p, nrec * rec_bytes, cudaMemcpyHostToDevice, st), "ds h2d");
+            if (ds->dim)
+                ds_split_kernel<<<dev_sms * 8, 256, 0, st>>>(static_cast<const uint32_t*>(d[b].p),
+                                                            nrec * rec_words, ds->dim,
+                                                            reinterpret_cast<uint32_t*>(ds->features) +
+                                                                base * ds->dim);
+            cuda_check(cudaGetLastError(), "ds split launch");
+            cuda_check(cudaEventRecord(ev[b], st), "ds event");
+            base += nrec;
+        }
+        if (alloc_n < ds->count)  // a record (or its label) is missing
+            fail(DRB_ERR_IO, "truncated dataset file: " + P);
+        cuda_check(cudaMemcpyAsync(ds->labels, ds->host_labels.data(), alloc_n * 4, cudaMemcpyHostToDevice, st),
+                   "ds labels h2d");
+        cuda_check(cudaStreamSynchronize(st), "ds load");
+        // split sidecar (dataset.cpp:129-142)
+        std::ifstream split(P + ".split");
+        if (split) {
+            std::string key;
+            uint64_t train = 0, eval = 0;
+            if (!(split >> key >> train) || key != "train" || !(split >> key >> eval) || key != "eval" ||
+                train + eval != ds->count)
+                fail(DRB_ERR_IO, "bad split sidecar: " + P + ".split");
+            ds->train = train;
+            ds->eval = eval;
+        } else {
+            ds->train = ds->count;
+            ds->eval = 0;
+        }
+        *out = ds.release();
+    });
+}
+
+drb_status drb_ds_destroy(drb_ds* ds) {
+    delete ds;
+    return DRB_OK;
+}
+
+drb_status drb_ds_info(const drb_ds* ds, uint64_t* count, uint32_t* feature_dim, uint32_t* n_classes,
+                       uint64_t* train_count, uint64_t* eval_count) {
+    DS_REQUIRE(ds && count && feature_dim && n_classes && train_count && eval_count);
+    *count = ds->count;
+    *feature_dim = ds->dim;
+    *n_classes = ds->n_classes;
+    *train_count = ds->train;
+    *eval_count = ds->eval;
+    return DRB_OK;
+}
+
+drb_status drb_ds_device_views(const drb_ds* ds, void** features, uint32_t** labels) {
+    DS_REQUIRE(ds && features && labels);
+    *features = ds->features;
+    *labels = ds->labels;
+    return DRB_OK;
+}
+
+drb_status drb_ds_indices_of(const drb_ds* ds, const uint32_t* classes, uint32_t n_classes, int32_t eval,
+                             uint64_t* out, uint64_t cap, uint64_t* n_out) {
+    DS_REQUIRE(ds && n_out && (classes || n_classes == 0) && (out || cap == 0));
+    return guarded([&] {
+        const std::unordered_set<uint32_t> wanted(classes, classes + n_classes);
+        const uint64_t lo = eval ? ds->train : 0, hi = eval ? ds->count : ds->train;
+        uint64_t c = 0;
+        for (uint64_t i = lo; i < hi; ++i)
+            if (wanted.count(ds->host_labels[i])) {
+                if (c < cap)
+                    out[c] = i;
+                ++c;
+            }
+        *n_out = c;
+    });
+}
+
+drb_status drb_ds_gather(const drb_ds* ds, const uint64_t* indices, uint32_t n, void* out_batch,
+                         uint32_t* out_labels, void* stream) {
+    DS_REQUIRE(ds && (n == 0 || (indices && out_batch)));
+    return guarded([&] {
+        if (n == 0)
+            return;
+        device_scope g(ds->device);
+        const uint64_t row_bytes = uint64_t(ds->dim) * 4;
+        if (row_bytes == 0) {
+            if (out_labels)
+                ds_gather_kernel<uint32_t><<<1, 32, 0, cudaStream_t(stream)>>>(
+                    ds->features, ds->labels, ds->count, 0, indices, n, static_cast<uint8_t*>(out_batch),
+                    out_labels, ds->err);
+            cuda_check(cudaGetLastError(), "ds gather launch");
+            return;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ds->device);
+        const bool v16 = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(out_batch) % 16) == 0;
+        const uint64_t words = row_bytes / (v16 ? 16 : 4);
+        // enough CTAs per row that the batch fills every SM several times over
+        const uint64_t per_row = std::min<uint64_t>((words + 255) / 256,
+                                                    std::max<uint64_t>(1, (uint64_t(sms) * 8 + n - 1) / n));
+        dim3 grid(uint32_t(per_row), std::min<uint32_t>(n, 65535));
+        if (v16)
+            ds_gather_kernel<uint4><<<grid, 256, 0, cudaStream_t(stream)>>>(
+                ds->features, ds->labels, ds->count, row_bytes, indices, n, static_cast<uint8_t*>(out_batch),
+                out_labels, ds->err);
+        else
+            ds_gather_kernel<uint32_t><<<grid, 256, 0, cudaStream_t(stream)>>>(
+                ds->features, ds->labels, ds->count, row_bytes, indices, n, static_cast<uint8_t*>(out_batch),
+                out_labels, ds->err);
+        cuda_check(cudaGetLastError(), "ds gather launch");
+    });
+}
+
+drb_status drb_ds_device_error(const drb_ds* ds, uint32_t* out) {
+    DS_REQUIRE(ds && out);
+    return guarded([&] {
+        device_scope g(ds->device);
+        cuda_check(cudaDeviceSynchronize(), "ds sync");
+        cuda_check(cudaMemcpy(out, ds->err, 4, cudaMemcpyDeviceToHost), "ds err read");
+        cuda_check(cudaMemset(ds->err, 0, 4), "ds err clear");
+    });
+}
+
+drb_status drb_make_schedule(uint32_t n_classes, uint32_t n_tasks, uint64_t seed, uint32_t* classes,
+                             uint32_t* task_sizes) {
+    DS_REQUIRE(classes || n_classes == 0);
+    DS_REQUIRE(task_sizes || n_tasks == 0);
+    return guarded([&] {
+        if (n_tasks == 0 || n_tasks > n_classes)
+            fail(DRB_ERR_CONFIG, "make_schedule: need 1 <= T <= K (T=" + std::to_string(n_tasks) +
+                                     ", K=" + std::to_string(n_classes) + ")");
+        for (uint32_t i = 0; i < n_classes; ++i)
+            classes[i] = i;
+        host_rng rng(seed, 0, kDataShuffle, 0xabcd, 0);
+        for (uint64_t i = n_classes; i > 1; --i)
+            std::swap(classes[i - 1], classes[rng.bounded(i)]);
+        for (uint32_t t = 0; t < n_tasks; ++t)
+            task_sizes[t] = n_classes / n_tasks + (t < n_classes % n_tasks ? 1 : 0);
+    });
+}
+
+drb_status drb_shard_batches(const uint64_t* task_data, uint64_t n, uint32_t worker, uint32_t n_workers,
+                             uint32_t batch_size, uint64_t seed, uint64_t task_index, uint64_t epoch,
+                             uint64_t* out, uint64_t cap, uint64_t* n_out) {
+    DS_REQUIRE(n_out && (task_data || n == 0) && (out || cap == 0));
+    return guarded([&] {
+        if (worker >= n_workers)
+            fail(DRB_ERR_USAGE, "shard_batches: worker id out of range");
+        if (batch_size == 0)
+            fail(DRB_ERR_USAGE, "shard_batches: batch_size must be > 0");
+        std::vector<uint64_t> order(task_data, task_data + n);
+        host_rng rng(seed, 0, kDataShuffle, task_index + 1, epoch + 1);
+        for (uint64_t i = order.size(); i > 1; --i)
+            std::swap(order[i - 1], order[rng.bounded(i)]);
+        uint64_t c = 0;
+        for (uint64_t i = worker; i < n; i += n_workers, ++c)
+            if (c < cap)
+                out[c] = order[i];
+        *n_out = c;
+    });
+}
+
+drb_status drb_lockstep_batches(uint64_t task_size, uint32_t n_workers, uint32_t batch_size, uint64_t* out) {
+    DS_REQUIRE(out);
+    if (n_workers == 0 || batch_size == 0) {
+        drb_b200::set_last_error("lockstep_batches: n_workers and batch_size must be > 0");
+        return DRB_ERR_USAGE;
+    }
+    *out = (task_size / n_workers + batch_size - 1) / batch_size;
+    return DRB_OK;
+}
+
+}  // extern "C"
