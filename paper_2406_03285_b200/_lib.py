@@ -148,7 +148,7 @@ def _load():
         "drb_ds_load": (st, [C.c_char_p, i32, P(vp)]),
         "drb_ds_destroy": (st, [vp]),
         "drb_ds_info": (st, [vp, P(u64), P(u32), P(u32), P(u64), P(u64)]),
-        "drb_ds_device_views": (st, [vp, P(vp), P(vp)]),
+        "drb_ds_device_views": (st, [vp, P(vp), P(vp)]),  # uint32_t** as void**
         "drb_ds_indices_of": (st, [vp, vp, u32, i32, vp, u64, P(u64)]),
         "drb_ds_gather": (st, [vp, vp, u32, vp, vp, vp]),
         "drb_ds_device_error": (st, [vp, P(u32)]),

@@ -151,13 +151,17 @@ __global__ void ds_split_kernel(const uint32_t* __restrict__ rec, uint64_t n_wor
 }
 
 // m[j] = features[idx[j]], labels[j] = labels[idx[j]] (dataset.cpp:66-72). blockIdx.y walks
-// the batch rows, blockIdx.x the 16 B (or 4 B) words of a row.
+// the batch rows, blockIdx.x tiles of kUnroll*blockDim words of a row: every thread issues
+// its kUnroll loads before any store, so each SM keeps ~64 KB of reads in flight.
+constexpr int kUnroll = 4;
 template <typename V>
-__global__ void ds_gather_kernel(const uint8_t* __restrict__ feat, const uint32_t* __restrict__ labels,
-                                 uint64_t count, uint64_t row_bytes, const uint64_t* __restrict__ idx,
-                                 uint32_t n, uint8_t* __restrict__ out, uint32_t* __restrict__ out_labels,
-                                 uint32_t* err) {
+__global__ void __launch_bounds__(256) ds_gather_kernel(const uint8_t* __restrict__ feat,
+                                                        const uint32_t* __restrict__ labels, uint64_t count,
+                                                        uint64_t row_bytes, const uint64_t* __restrict__ idx,
+                                                        uint32_t n, uint8_t* __restrict__ out,
+                                                        uint32_t* __restrict__ out_labels, uint32_t* err) {
     const uint64_t row_words = row_bytes / sizeof(V);
+    const uint64_t tile = uint64_t(blockDim.x) * kUnroll;
     for (uint32_t j = blockIdx.y; j < n; j += gridDim.y) {
         const uint64_t i = idx[j];
         if (i >= count) {
@@ -167,9 +171,21 @@ __global__ void ds_gather_kernel(const uint8_t* __restrict__ feat, const uint32_
         }
         const V* src = reinterpret_cast<const V*>(feat + i * row_bytes);
         V* dst = reinterpret_cast<V*>(out + uint64_t(j) * row_bytes);
-        for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < row_words;
-             w += uint64_t(gridDim.x) * blockDim.x)
-            dst[w] = __ldg(src + w);
+        for (uint64_t base = blockIdx.x * tile; base < row_words; base += uint64_t(gridDim.x) * tile) {
+            V v[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint64_t w = base + u * blockDim.x + threadIdx.x;
+                if (w < row_words)
+                    v[u] = __ldcs(src + w);  // streamed once: evict-first in L2
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint64_t w = base + u * blockDim.x + threadIdx.x;
+                if (w < row_words)
+                    dst[w] = v[u];
+            }
+        }
         if (out_labels && blockIdx.x == 0 && threadIdx.x == 0)
             out_labels[j] = labels[i];
     }
@@ -366,8 +382,8 @@ drb_status drb_ds_gather(const drb_ds* ds, const uint64_t* indices, uint32_t n, 
         const bool v16 = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(out_batch) % 16) == 0;
         const uint64_t words = row_bytes / (v16 ? 16 : 4);
         // enough CTAs per row that the batch fills every SM several times over
-        const uint64_t per_row = std::min<uint64_t>((words + 255) / 256,
-                                                    std::max<uint64_t>(1, (uint64_t(sms) * 8 + n - 1) / n));
+        const uint64_t per_row = std::min<uint64_t>((words + 256 * kUnroll - 1) / (256 * kUnroll),
+                                                    std::max<uint64_t>(1, (uint64_t(sms) * 4 + n - 1) / n));
         dim3 grid(uint32_t(per_row), std::min<uint32_t>(n, 65535));
         if (v16)
             ds_gather_kernel<uint4><<<grid, 256, 0, cudaStream_t(stream)>>>(

@@ -60,14 +60,14 @@ class dataset:
 
     def features(self) -> torch.Tensor:
         """Zero-copy view of the device features, f32 [count, feature_dim]."""
-        fp, lp = C.c_void_p(), C.POINTER(C.c_uint32)()
+        fp, lp = C.c_void_p(), C.c_void_p()
         check(lib.drb_ds_device_views(self._h, C.byref(fp), C.byref(lp)))
         return _view(fp.value or 0, (self._count, self.feature_dim), "<f4", self.device, self)
 
     def labels(self) -> torch.Tensor:
-        fp, lp = C.c_void_p(), C.POINTER(C.c_uint32)()
+        fp, lp = C.c_void_p(), C.c_void_p()
         check(lib.drb_ds_device_views(self._h, C.byref(fp), C.byref(lp)))
-        return _view(C.cast(lp, C.c_void_p).value or 0, (self._count,), "<i4", self.device, self)
+        return _view(lp.value or 0, (self._count,), "<i4", self.device, self)
 
     def _indices_of(self, classes: Sequence[int], eval_set: int) -> np.ndarray:
         cls = np.ascontiguousarray(np.asarray(list(classes), dtype=np.uint32))

@@ -47,7 +47,7 @@ def test_load_fixture_and_gather(name):
         m, ml = ds.gather(idx)
         torch.cuda.synchronize()
         of, ol = O.gather(f, lab, idx)
-        assert np.array_equal(m.cpu().numpy().view(np.uint32).reshape(n, -1), of.view(np.uint32).reshape(n, -1))
+        assert np.array_equal(m.cpu().numpy().view(np.uint32).reshape(n, f.shape[1]), of.view(np.uint32).reshape(n, f.shape[1]))
         assert np.array_equal(ml.cpu().numpy().astype(np.uint32), ol)
     assert ds.device_error() == 0
 
@@ -85,7 +85,7 @@ def test_gather_out_of_range_index_sets_the_error_word():
 
 
 def test_load_errors_match_the_oracle(tmp_path):
-    from tests.test_input_cpu import broken_files
+    from test_input_cpu import broken_files
     D = _D()
     for name, path in broken_files(tmp_path):
         with pytest.raises(O.io_error) as mine:
