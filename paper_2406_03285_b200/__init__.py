@@ -10,6 +10,8 @@ from .rehearsal import (augment, augmented_batch, bias_report, bias_test, engine
                         plan, read_entry, rehearsal_buffer, rng_stream, sample_without_replacement,
                         sampling_plan)
 
+from . import dataset  # noqa: E402,F401  (the producer of m: DRDS load, schedule, shards, device gather)
+
 __all__ = [
     "rehearsal_buffer", "engine", "rng_stream", "plan", "augment", "sample_without_replacement", "bias_test",
     "bias_report",

@@ -124,4 +124,7 @@ def test_gathered_batch_drives_the_buffer_like_host_bytes(tmp_path):
     torch.cuda.synchronize()
     assert bufs[0].snapshot().per_class == bufs[1].snapshot().per_class
     s0, s1 = bufs[0].slab(), bufs[1].slab()
-    assert torch.equal(s0[0], s1[0]) and torch.equal(s0[1], s1[1])
+    occ = bufs[0].snapshot().per_class
+    assert sum(occ) > 0
+    for k in range(K):  # slots past occ[k] were never written (uninitialised HBM)
+        assert torch.equal(s0[0][k, :occ[k]], s1[0][k, :occ[k]]) and torch.equal(s0[1][k, :occ[k]], s1[1][k, :occ[k]])
