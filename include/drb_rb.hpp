@@ -23,6 +23,7 @@
 // Device memory is plain device pointers: the caller owns batches, the engine owns m'.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -49,6 +50,9 @@ struct transport_error : drb_error {
 struct engine_error : drb_error {
     using drb_error::drb_error;
 };
+struct io_error : drb_error {
+    using drb_error::drb_error;
+};
 
 inline void check(drb_status s) {
     if (s == DRB_OK)
@@ -59,6 +63,7 @@ inline void check(drb_status s) {
     case DRB_ERR_USAGE: throw usage_error(s, msg);
     case DRB_ERR_TRANSPORT: throw transport_error(s, msg);
     case DRB_ERR_TRAINING: throw engine_error(s, msg);
+    case DRB_ERR_IO: throw io_error(s, msg);
     default: throw drb_error(s, msg);
     }
 }
@@ -279,5 +284,95 @@ private:
     rehearsal_buffer& b_;
     bool started_ = false, shut_ = false;
 };
+
+// ---- input side: the producer of m (proj/src/scenario/dataset.hpp, schedule.hpp) ----
+
+/// dataset (dataset.hpp:19-40), resident in HBM; load_dataset throws io_error like
+/// dataset.cpp:102-143. gather() is dataset::gather on the device: indices is a device array.
+class dataset {
+public:
+    explicit dataset(const std::string& path, int device = 0) {
+        check(drb_ds_load(path.c_str(), device, &h_));
+        check(drb_ds_info(h_, &count_, &feature_dim, &n_classes, &train_count, &eval_count));
+    }
+    ~dataset() { drb_ds_destroy(h_); }
+    dataset(const dataset&) = delete;
+    dataset& operator=(const dataset&) = delete;
+
+    std::size_t size() const { return count_; }
+    std::vector<std::size_t> train_indices_of(const std::vector<std::uint32_t>& classes) const {
+        return indices_of(classes, 0);
+    }
+    std::vector<std::size_t> eval_indices_of(const std::vector<std::uint32_t>& classes) const {
+        return indices_of(classes, 1);
+    }
+    /// rows -> out (n x feature_dim*4 bytes) and labels, ordered on `stream`.
+    device_batch gather(const std::uint64_t* indices, std::uint32_t n, void* out, std::uint32_t* out_labels,
+                        void* stream = nullptr) const {
+        check(drb_ds_gather(h_, indices, n, out, out_labels, stream));
+        return device_batch{out, out_labels, n};
+    }
+    std::uint32_t device_error() const {
+        std::uint32_t e = 0;
+        check(drb_ds_device_error(h_, &e));
+        return e;
+    }
+    drb_ds* raw() const { return h_; }
+
+    std::uint32_t feature_dim = 0, n_classes = 0;
+    std::uint64_t train_count = 0, eval_count = 0;
+
+private:
+    std::vector<std::size_t> indices_of(const std::vector<std::uint32_t>& classes, int eval) const {
+        std::uint64_t n = 0;
+        check(drb_ds_indices_of(h_, classes.data(), std::uint32_t(classes.size()), eval, nullptr, 0, &n));
+        std::vector<std::uint64_t> v(n);
+        check(drb_ds_indices_of(h_, classes.data(), std::uint32_t(classes.size()), eval, v.data(), n, &n));
+        return std::vector<std::size_t>(v.begin(), v.end());
+    }
+    drb_ds* h_ = nullptr;
+    std::uint64_t count_ = 0;
+};
+
+/// task_schedule / make_schedule (schedule.hpp:10-25, schedule.cpp:10-35).
+struct task_schedule {
+    std::vector<std::vector<std::uint32_t>> tasks;
+    unsigned epochs_per_task = 1;
+};
+inline task_schedule make_schedule(std::uint32_t n_classes, std::uint32_t n_tasks, std::uint64_t seed,
+                                   unsigned epochs_per_task = 1) {
+    std::vector<std::uint32_t> cls(n_classes), sizes(n_tasks);
+    check(drb_make_schedule(n_classes, n_tasks, seed, cls.data(), sizes.data()));
+    task_schedule s;
+    s.epochs_per_task = epochs_per_task;
+    std::size_t cur = 0;
+    for (std::uint32_t t = 0; t < n_tasks; ++t) {
+        s.tasks.emplace_back(cls.begin() + cur, cls.begin() + cur + sizes[t]);
+        cur += sizes[t];
+    }
+    return s;
+}
+
+/// shard_batches (schedule.cpp:37-62): this worker's batches for (task, epoch).
+inline std::vector<std::vector<std::size_t>> shard_batches(const std::vector<std::size_t>& task_data,
+                                                           std::uint32_t worker, std::uint32_t n_workers,
+                                                           unsigned batch_size, std::uint64_t seed,
+                                                           std::uint64_t task_index, std::uint64_t epoch) {
+    const std::vector<std::uint64_t> td(task_data.begin(), task_data.end());
+    std::vector<std::uint64_t> out(n_workers ? (td.size() + n_workers - 1) / n_workers : 0);
+    std::uint64_t n = 0;
+    check(drb_shard_batches(td.data(), td.size(), worker, n_workers, batch_size, seed, task_index, epoch,
+                            out.data(), out.size(), &n));
+    std::vector<std::vector<std::size_t>> batches;
+    for (std::uint64_t s = 0; s < n; s += batch_size)
+        batches.emplace_back(out.begin() + s, out.begin() + std::min<std::uint64_t>(n, s + batch_size));
+    return batches;
+}
+
+inline std::size_t lockstep_batches(std::size_t task_size, std::uint32_t n_workers, unsigned batch_size) {
+    std::uint64_t out = 0;
+    check(drb_lockstep_batches(task_size, n_workers, batch_size, &out));
+    return out;
+}
 
 }  // namespace drb::b200

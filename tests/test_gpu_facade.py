@@ -15,3 +15,12 @@ def test_cpp_facade_parity():
     res = subprocess.run([EXE], capture_output=True, text=True, timeout=120)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "bit-exact" in res.stdout
+
+
+def test_cpp_input_facade_parity():
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "input_parity")
+    assert os.path.exists(exe), "build first: python -c 'import __graft_entry__ as g; g.build()'"
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    res = subprocess.run([exe, gold], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "bit-exact" in res.stdout
