@@ -8,10 +8,12 @@
 // device into SoA features [count][dim*4 B] (rows 16 B aligned whenever dim % 4 == 0) and
 // labels u32[count], so a batch gather is a straight row copy into the rehearsal buffer's
 // m layout ([b][S] bytes + u32 labels[b], S = dim*4). The file is streamed through two
-// pinned staging buffers; each chunk's H2D copy overlaps the next chunk's read, and the
+// pinned staging buffers (each chunk read by up to 16 pread threads, which also validate
+// the labels of their slice); each chunk's H2D copy overlaps the next chunk's read, and the
 // split kernel runs per chunk on the device.
 
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -20,6 +22,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -274,19 +277,51 @@ drb_status drb_ds_load(const char* path, int32_t device, drb_ds** out) {
         });
         int dev_sms = 148;
         cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+        const int fd = fileno(f.get());
+        const unsigned reader_threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         uint64_t base = 0;
         for (int b = 0; base < alloc_n; b ^= 1) {
             const uint64_t nrec = std::min(chunk_recs, alloc_n - base);
             cuda_check(cudaEventSynchronize(ev[b]), "ds staging reuse");
-            if (fread(h[b].p, rec_bytes, nrec, f.get()) != nrec)
-                fail(DRB_ERR_IO, "truncated dataset file: " + P);
+            // parallel pread of the chunk into pinned memory + label scan per slice; the first
+            // bad record (lowest index) wins, as in the reference's sequential read
             const uint32_t* w = static_cast<const uint32_t*>(h[b].p);
-            for (uint64_t r = 0; r < nrec; ++r) {
-                const uint32_t lab = w[r * rec_words + ds->dim];
-                if (lab >= ds->n_classes)
-                    fail(DRB_ERR_IO, "dataset label out of range at record " + std::to_string(base + r) +
-                                         ": " + P);
-                ds->host_labels[base + r] = lab;
+            const unsigned nt = unsigned(std::min<uint64_t>(reader_threads, nrec));
+            std::vector<uint64_t> bad(nt, UINT64_MAX);
+            std::vector<char> short_read(nt, 0);
+            auto slice = [&](unsigned t) {
+                const uint64_t r0 = nrec * t / nt, r1 = nrec * (t + 1) / nt;
+                const uint64_t off = sizeof hdr + (base + r0) * rec_bytes, len = (r1 - r0) * rec_bytes;
+                char* dst = static_cast<char*>(h[b].p) + r0 * rec_bytes;
+                for (uint64_t got_b = 0; got_b < len;) {
+                    const ssize_t k = pread(fd, dst + got_b, size_t(std::min<uint64_t>(len - got_b, 1ull << 30)),
+                                            off_t(off + got_b));
+                    if (k <= 0) {
+                        short_read[t] = 1;
+                        return;
+                    }
+                    got_b += uint64_t(k);
+                }
+                for (uint64_t r = r0; r < r1; ++r) {
+                    const uint32_t lab = w[r * rec_words + ds->dim];
+                    if (lab >= ds->n_classes) {
+                        bad[t] = base + r;
+                        return;
+                    }
+                    ds->host_labels[base + r] = lab;
+                }
+            };
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < nt; ++t)
+                pool.emplace_back(slice, t);
+            slice(0);
+            for (auto& th : pool)
+                th.join();
+            for (unsigned t = 0; t < nt; ++t) {
+                if (short_read[t])
+                    fail(DRB_ERR_IO, "truncated dataset file: " + P);
+                if (bad[t] != UINT64_MAX)
+                    fail(DRB_ERR_IO, "dataset label out of range at record " + std::to_string(bad[t]) + ": " + P);
             }
             cuda_check(cudaMemcpyAsync(d[b].p, h[b].p, nrec * rec_bytes, cudaMemcpyHostToDevice, st), "ds h2d");
             if (ds->dim)
