@@ -11,8 +11,19 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle.py_input_oracle import write_dataset  # noqa: E402  (writes the test input file only)
 from paper_2406_03285_b200 import dataset as D  # noqa: E402
+
+
+def write_dataset(path, features, labels, n_classes):
+    """A DRDS file (proj/src/scenario/dataset.hpp:10-17) of the synthetic input, all train."""
+    count, dim = features.shape
+    rec = np.empty((count, dim + 1), dtype="<u4")
+    rec[:, :dim] = features.view(np.uint32)
+    rec[:, dim] = labels
+    with open(path, "wb") as f:
+        f.write(b"DRDS" + (1).to_bytes(2, "little") + count.to_bytes(8, "little") + dim.to_bytes(4, "little") +
+                n_classes.to_bytes(4, "little"))
+        f.write(rec.tobytes())
 
 count, dim, b, iters = 4000, 37632, 56, 200
 rng = np.random.default_rng(0)
