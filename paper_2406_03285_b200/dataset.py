@@ -150,3 +150,21 @@ def lockstep_batches(task_size: int, n_workers: int, batch_size: int) -> int:
     out = C.c_uint64()
     check(lib.drb_lockstep_batches(task_size, n_workers, batch_size, C.byref(out)))
     return out.value
+
+
+def epoch_batches(ds: dataset, task_data, worker: int, n_workers: int, batch_size: int, seed: int,
+                  task_index: int, epoch: int):
+    """The producer side of epoch_driver::run (proj/src/trainer/trainer.cpp:94-106): this
+    worker's shard for (task, epoch), lockstep_batches steps, each yielded as a device m
+    (u8 [n, S], int32 labels [n]) ready for engine.update. The shard's indices go to HBM
+    once per epoch; every step is one device gather into a fresh pair of tensors."""
+    batches = shard_batches(task_data, worker, n_workers, batch_size, seed, task_index, epoch)
+    steps = lockstep_batches(len(task_data), n_workers, batch_size)
+    if steps == 0:
+        return
+    dev = torch.device("cuda", ds.device)
+    flat = torch.as_tensor(np.concatenate(batches[:steps]).astype(np.int64)).to(dev)
+    pos = 0
+    for b in batches[:steps]:
+        yield ds.gather(flat[pos:pos + len(b)])
+        pos += len(b)

@@ -128,3 +128,41 @@ def test_gathered_batch_drives_the_buffer_like_host_bytes(tmp_path):
     assert sum(occ) > 0
     for k in range(K):  # slots past occ[k] were never written (uninitialised HBM)
         assert torch.equal(s0[0][k, :occ[k]], s1[0][k, :occ[k]]) and torch.equal(s0[1][k, :occ[k]], s1[1][k, :occ[k]])
+
+
+def test_epoch_batches_drive_the_engine_like_host_batches(tmp_path):
+    """epoch_batches -> engine.update for a whole epoch gives the same m' sequence as the same
+    records built on the host (trainer.cpp:94-113 with rehearse = true)."""
+    import torch
+    import paper_2406_03285_b200 as P
+    D = _D()
+    K, per_class, dim, b = 10, 80, 32, 16
+    rng = np.random.default_rng(21)
+    feats = rng.standard_normal((K * per_class, dim)).astype(np.float32)
+    labels = np.tile(np.arange(K, dtype=np.uint32), per_class)
+    p = str(tmp_path / "e.drds")
+    O.write_dataset(p, feats, labels, K)
+    ds = D.load_dataset(p, 0)
+    sched = D.make_schedule(K, 2, 3)
+    task = ds.train_indices_of(sched.tasks[1])
+    host_batches = O.shard_batches(task.tolist(), 0, 1, b, 3, 1, 0)[:O.lockstep_batches(len(task), 1, b)]
+    engines = []
+    for _ in range(2):
+        buf = P.rehearsal_buffer(K, 12, dim * 4, max_batch=b, candidate_count=14, rep_count=5, seed=3, device=0)
+        eng = P.engine(buf)
+        eng.start()
+        engines.append((buf, eng))
+    got = []
+    for step, m in enumerate(D.epoch_batches(ds, task, 0, 1, b, 3, 1, 0)):
+        idx = np.asarray(host_batches[step], np.int64)
+        m_host = (torch.from_numpy(feats[idx].view(np.uint8).reshape(len(idx), dim * 4)).cuda(),
+                  torch.from_numpy(labels[idx].astype(np.int32)).cuda())
+        a0 = engines[0][1].update(m)
+        a1 = engines[1][1].update(m_host)
+        x0, y0 = a0.tensors()
+        x1, y1 = a1.tensors()
+        assert torch.equal(x0, x1) and torch.equal(y0, y1), step
+        got.append(len(y0))
+    assert len(got) == len(host_batches) and max(got) > b  # reps arrived after the first round
+    for buf, eng in engines:
+        eng.shutdown()
