@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -155,9 +156,8 @@ __global__ void ds_split_kernel(const uint32_t* __restrict__ rec, uint64_t n_wor
 
 // m[j] = features[idx[j]], labels[j] = labels[idx[j]] (dataset.cpp:66-72). blockIdx.y walks
 // the batch rows, blockIdx.x tiles of kUnroll*blockDim words of a row: every thread issues
-// its kUnroll loads before any store, so each SM keeps ~64 KB of reads in flight.
-constexpr int kUnroll = 4;
-template <typename V>
+// its kUnroll loads before any store (kUnroll 4, 4 CTAs per SM: ~64 KB of reads in flight per SM).
+template <typename V, int kUnroll>
 __global__ void __launch_bounds__(256) ds_gather_kernel(const uint8_t* __restrict__ feat,
                                                         const uint32_t* __restrict__ labels, uint64_t count,
                                                         uint64_t row_bytes, const uint64_t* __restrict__ idx,
@@ -406,7 +406,7 @@ drb_status drb_ds_gather(const drb_ds* ds, const uint64_t* indices, uint32_t n, 
         const uint64_t row_bytes = uint64_t(ds->dim) * 4;
         if (row_bytes == 0) {
             if (out_labels)
-                ds_gather_kernel<uint32_t><<<1, 32, 0, cudaStream_t(stream)>>>(
+                ds_gather_kernel<uint32_t, 1><<<1, 32, 0, cudaStream_t(stream)>>>(
                     ds->features, ds->labels, ds->count, 0, indices, n, static_cast<uint8_t*>(out_batch),
                     out_labels, ds->err);
             cuda_check(cudaGetLastError(), "ds gather launch");
@@ -417,17 +417,27 @@ drb_status drb_ds_gather(const drb_ds* ds, const uint64_t* indices, uint32_t n, 
         const bool v16 = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(out_batch) % 16) == 0;
         const uint64_t words = row_bytes / (v16 ? 16 : 4);
         // enough CTAs per row that the batch fills every SM several times over
-        const uint64_t per_row = std::min<uint64_t>((words + 256 * kUnroll - 1) / (256 * kUnroll),
-                                                    std::max<uint64_t>(1, (uint64_t(sms) * 4 + n - 1) / n));
+        // (DRB_GATHER="unroll,ctas_per_sm" overrides the 4,4 default: tools/input_bench.py sweeps)
+        static const std::pair<int, int> knobs = [] {
+            int u = 4, c = 4;
+            if (const char* e = std::getenv("DRB_GATHER"))
+                std::sscanf(e, "%d,%d", &u, &c);
+            return std::make_pair(u == 2 || u == 8 ? u : 4, c > 0 ? c : 4);
+        }();
+        const int unroll = knobs.first;
+        const uint64_t per_row = std::min<uint64_t>((words + 256 * unroll - 1) / (256 * unroll),
+                                                    std::max<uint64_t>(1, (uint64_t(sms) * knobs.second + n - 1) / n));
         dim3 grid(uint32_t(per_row), std::min<uint32_t>(n, 65535));
+        auto launch = [&](auto kern) {
+            kern<<<grid, 256, 0, cudaStream_t(stream)>>>(ds->features, ds->labels, ds->count, row_bytes, indices, n,
+                                                         static_cast<uint8_t*>(out_batch), out_labels, ds->err);
+        };
         if (v16)
-            ds_gather_kernel<uint4><<<grid, 256, 0, cudaStream_t(stream)>>>(
-                ds->features, ds->labels, ds->count, row_bytes, indices, n, static_cast<uint8_t*>(out_batch),
-                out_labels, ds->err);
+            unroll == 2 ? launch(ds_gather_kernel<uint4, 2>)
+                        : unroll == 8 ? launch(ds_gather_kernel<uint4, 8>) : launch(ds_gather_kernel<uint4, 4>);
         else
-            ds_gather_kernel<uint32_t><<<grid, 256, 0, cudaStream_t(stream)>>>(
-                ds->features, ds->labels, ds->count, row_bytes, indices, n, static_cast<uint8_t*>(out_batch),
-                out_labels, ds->err);
+            unroll == 2 ? launch(ds_gather_kernel<uint32_t, 2>)
+                        : unroll == 8 ? launch(ds_gather_kernel<uint32_t, 8>) : launch(ds_gather_kernel<uint32_t, 4>);
         cuda_check(cudaGetLastError(), "ds gather launch");
     });
 }
