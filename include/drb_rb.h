@@ -271,6 +271,11 @@ typedef struct drb_ds drb_ds;
 /* load_dataset (proj/src/scenario/dataset.cpp:102-143): same checks, same order, same
  * messages; every failure is DRB_ERR_IO (io_error). */
 DRB_RB_API drb_status drb_ds_load(const char* path, int32_t device, drb_ds** out);
+/* synth_dataset (proj/src/scenario/dataset.cpp:145-205): the reference's Gaussian-blob
+ * dataset, bit-identical (same stream, same double arithmetic), placed in HBM.
+ * separation <= 0 -> DRB_ERR_CONFIG. */
+DRB_RB_API drb_status drb_ds_synth(uint32_t n_classes, uint32_t per_class, uint32_t feature_dim,
+                                   double separation, uint64_t seed, int32_t device, drb_ds** out);
 DRB_RB_API drb_status drb_ds_destroy(drb_ds* ds);
 /* dataset::size / feature_dim / n_classes / train_count / eval_count (dataset.hpp:19-27). */
 DRB_RB_API drb_status drb_ds_info(const drb_ds* ds, uint64_t* count, uint32_t* feature_dim,

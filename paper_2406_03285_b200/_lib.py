@@ -146,6 +146,7 @@ def _load():
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),
         "drb_ds_load": (st, [C.c_char_p, i32, P(vp)]),
+        "drb_ds_synth": (st, [u32, u32, u32, C.c_double, u64, i32, P(vp)]),
         "drb_ds_destroy": (st, [vp]),
         "drb_ds_info": (st, [vp, P(u64), P(u32), P(u32), P(u64), P(u64)]),
         "drb_ds_device_views": (st, [vp, P(vp), P(vp)]),  # uint32_t** as void**

@@ -16,10 +16,12 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -118,12 +120,30 @@ uint64_t mix(uint64_t z) {
 struct host_rng {
     uint64_t key, ctr = 0;
     // rng_stream::keyed(seed, worker, purpose, k1, k2) (rng.cpp:19-39): k1+1, k2+1 folded in.
-    host_rng(uint64_t seed, uint64_t worker, uint64_t purpose, uint64_t k1, uint64_t k2) {
+    host_rng(uint64_t seed, uint64_t worker, uint64_t purpose, uint64_t k1, uint64_t k2, bool keyed = true) {
         key = mix(seed);
         key = mix(key ^ (worker * 0xd1342543de82ef95ULL));
         key = mix(key ^ (purpose * 0xaf251af3b0f025b5ULL));
-        key = mix(key ^ (k1 + 1));
-        key = mix(key ^ (k2 + 1));
+        key = mix(key ^ (keyed ? k1 + 1 : 0));  // the plain ctor folds 0, 0 (rng.cpp:33-34)
+        key = mix(key ^ (keyed ? k2 + 1 : 0));
+    }
+    double next_double() { return double(next() >> 11) * 0x1.0p-53; }  // rng.cpp:54-56
+    bool has_spare = false;
+    double spare = 0;
+    double gaussian() {  // Box-Muller with a cached spare (rng.cpp:58-72)
+        if (has_spare) {
+            has_spare = false;
+            return spare;
+        }
+        double u1 = next_double();
+        const double u2 = next_double();
+        if (u1 <= 0.0)
+            u1 = 0x1.0p-53;
+        const double radius = std::sqrt(-2.0 * std::log(u1));
+        const double angle = 2.0 * M_PI * u2;
+        spare = radius * std::sin(angle);
+        has_spare = true;
+        return radius * std::cos(angle);
     }
     uint64_t next() { return mix(key ^ (++ctr * kPhiH)); }
     uint64_t bounded(uint64_t n) {  // rng.cpp:45-53
@@ -136,6 +156,7 @@ struct host_rng {
     }
 };
 constexpr uint64_t kDataShuffle = 4;  // rng.hpp purpose::data_shuffle
+constexpr uint64_t kSynth = 7;        // rng.hpp purpose::synth
 
 // ---- kernels ----
 
@@ -352,6 +373,67 @@ drb_status drb_ds_load(const char* path, int32_t device, drb_ds** out) {
             ds->train = ds->count;
             ds->eval = 0;
         }
+        *out = ds.release();
+    });
+}
+
+// synth_dataset (proj/src/scenario/dataset.cpp:145-205): the Gaussian-blob dataset, drawn on
+// the host with the same double arithmetic and libm, then placed in HBM like a loaded file.
+drb_status drb_ds_synth(uint32_t n_classes, uint32_t per_class, uint32_t feature_dim, double separation,
+                        uint64_t seed, int32_t device, drb_ds** out) {
+    DS_REQUIRE(out);
+    return guarded([&] {
+        if (!(separation > 0.0))
+            fail(DRB_ERR_CONFIG, "synth_dataset: separation must be > 0");
+        host_rng rng(seed, 0, kSynth, 0, 0, /*keyed=*/false);
+        std::vector<std::vector<double>> means(n_classes, std::vector<double>(feature_dim));
+        double min_dist = 0.0;
+        do {
+            for (auto& mean : means)
+                for (auto& v : mean)
+                    v = rng.gaussian();
+            min_dist = std::numeric_limits<double>::infinity();
+            for (uint32_t a = 0; a < n_classes; ++a)
+                for (uint32_t b = a + 1; b < n_classes; ++b) {
+                    double d2 = 0.0;
+                    for (uint32_t f = 0; f < feature_dim; ++f) {
+                        const double diff = means[a][f] - means[b][f];
+                        d2 += diff * diff;
+                    }
+                    min_dist = std::min(min_dist, std::sqrt(d2));
+                }
+        } while (n_classes > 1 && min_dist <= 1e-9);
+        if (n_classes > 1) {
+            const double scale = separation / min_dist;
+            for (auto& mean : means)
+                for (auto& v : mean)
+                    v *= scale;
+        }
+        const uint32_t eval_per = per_class / 5, train_per = per_class - eval_per;
+        std::unique_ptr<drb_ds> ds(new drb_ds);
+        ds->device = device;
+        ds->dim = feature_dim;
+        ds->n_classes = n_classes;
+        ds->train = uint64_t(train_per) * n_classes;
+        ds->eval = uint64_t(eval_per) * n_classes;
+        ds->count = ds->train + ds->eval;
+        std::vector<float> feats;
+        feats.reserve(ds->count * feature_dim);
+        ds->host_labels.reserve(ds->count);
+        for (const uint32_t rows : {train_per, eval_per})  // round-robin over classes per block
+            for (uint32_t row = 0; row < rows; ++row)
+                for (uint32_t c = 0; c < n_classes; ++c) {
+                    for (uint32_t f = 0; f < feature_dim; ++f)
+                        feats.push_back(static_cast<float>(means[c][f] + rng.gaussian()));
+                    ds->host_labels.push_back(c);
+                }
+        device_scope g(device);
+        cuda_check(cudaMalloc(&ds->features, std::max<uint64_t>(feats.size() * 4, 16)), "ds features");
+        cuda_check(cudaMalloc(&ds->labels, std::max<uint64_t>(ds->count * 4, 4)), "ds labels");
+        cuda_check(cudaMalloc(&ds->err, 4), "ds err");
+        cuda_check(cudaMemset(ds->err, 0, 4), "ds err");
+        cuda_check(cudaMemcpy(ds->features, feats.data(), feats.size() * 4, cudaMemcpyHostToDevice), "ds h2d");
+        cuda_check(cudaMemcpy(ds->labels, ds->host_labels.data(), ds->count * 4, cudaMemcpyHostToDevice), "ds h2d");
         *out = ds.release();
     });
 }

@@ -4,6 +4,7 @@ Python mirror of the reference's scenario API over the C ABI (include/drb_rb.h, 
 drb_make_schedule / drb_shard_batches / drb_lockstep_batches):
 
   dataset, load_dataset        proj/src/scenario/dataset.hpp:10-40, dataset.cpp:102-143
+  synth_dataset                proj/src/scenario/dataset.cpp:145-205
   dataset.train_indices_of     proj/src/scenario/dataset.cpp:48-55
   dataset.eval_indices_of      proj/src/scenario/dataset.cpp:57-64
   dataset.gather               proj/src/scenario/dataset.cpp:66-72 (on the device: returns
@@ -114,6 +115,14 @@ class dataset:
 def load_dataset(path: str, device: int = 0) -> dataset:
     h = C.c_void_p()
     check(lib.drb_ds_load(str(path).encode(), device, C.byref(h)))
+    return dataset(h, device)
+
+
+def synth_dataset(n_classes: int, per_class: int, feature_dim: int, separation: float, seed: int,
+                  device: int = 0) -> dataset:
+    """synth_dataset (proj/src/scenario/dataset.cpp:145-205), bit-identical, resident in HBM."""
+    h = C.c_void_p()
+    check(lib.drb_ds_synth(n_classes, per_class, feature_dim, float(separation), seed, device, C.byref(h)))
     return dataset(h, device)
 
 

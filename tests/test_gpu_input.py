@@ -166,3 +166,15 @@ def test_epoch_batches_drive_the_engine_like_host_batches(tmp_path):
     assert len(got) == len(host_batches) and max(got) > b  # reps arrived after the first round
     for buf, eng in engines:
         eng.shutdown()
+
+
+@pytest.mark.parametrize("name,args", [("drds_small", (5, 8, 12, 4.0, 11)), ("drds_odd", (3, 6, 7, 3.0, 12))])
+def test_synth_dataset_is_bit_identical_to_the_reference(name, args):
+    """synth_dataset(K, per_class, dim, separation, seed) in HBM equals the file the reference's
+    own synth_dataset + write_dataset produced for the same arguments (oracle/gen_golden_input.py)."""
+    from paper_2406_03285_b200 import _lib
+    D = _D()
+    ds = D.synth_dataset(*args, device=0)
+    _check_loaded(ds, os.path.join(GOLD, name + ".drds"))
+    with pytest.raises(_lib.config_error):
+        D.synth_dataset(3, 5, 4, 0.0, 1)
