@@ -295,7 +295,22 @@ public:
         check(drb_ds_load(path.c_str(), device, &h_));
         check(drb_ds_info(h_, &count_, &feature_dim, &n_classes, &train_count, &eval_count));
     }
-    ~dataset() { drb_ds_destroy(h_); }
+    /// synth_dataset (dataset.cpp:145-205), bit-identical to the reference's, in HBM.
+    static dataset synth(std::uint32_t n_classes, std::uint32_t per_class, std::uint32_t feature_dim,
+                         double separation, std::uint64_t seed, int device = 0) {
+        drb_ds* h = nullptr;
+        check(drb_ds_synth(n_classes, per_class, feature_dim, separation, seed, device, &h));
+        return dataset(h);
+    }
+    dataset(dataset&& o) noexcept
+        : feature_dim(o.feature_dim), n_classes(o.n_classes), train_count(o.train_count),
+          eval_count(o.eval_count), h_(o.h_), count_(o.count_) {
+        o.h_ = nullptr;
+    }
+    ~dataset() {
+        if (h_)
+            drb_ds_destroy(h_);
+    }
     dataset(const dataset&) = delete;
     dataset& operator=(const dataset&) = delete;
 
@@ -323,6 +338,9 @@ public:
     std::uint64_t train_count = 0, eval_count = 0;
 
 private:
+    explicit dataset(drb_ds* h) : h_(h) {
+        check(drb_ds_info(h_, &count_, &feature_dim, &n_classes, &train_count, &eval_count));
+    }
     std::vector<std::size_t> indices_of(const std::vector<std::uint32_t>& classes, int eval) const {
         std::uint64_t n = 0;
         check(drb_ds_indices_of(h_, classes.data(), std::uint32_t(classes.size()), eval, nullptr, 0, &n));

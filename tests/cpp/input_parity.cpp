@@ -98,9 +98,19 @@ int main(int argc, char** argv) {
         EXPECT(lab[j] == l);
     }
     EXPECT(ds.device_error() == 0);
+    // synth_dataset(5, 8, 12, 4.0, 11) is the fixture's content (written by the reference)
+    const dataset syn = dataset::synth(5, 8, 12, 4.0, 11);
+    EXPECT(syn.size() == ds.size() && syn.train_count == ds.train_count && syn.eval_count == ds.eval_count);
+    void *fa, *fb;
+    std::uint32_t *la, *lb;
+    EXPECT(drb_ds_device_views(syn.raw(), &fa, &la) == DRB_OK && drb_ds_device_views(ds.raw(), &fb, &lb) == DRB_OK);
+    std::vector<unsigned char> a(ds.size() * S), bb(ds.size() * S);
+    EXPECT(cudaMemcpy(a.data(), fa, a.size(), cudaMemcpyDeviceToHost) == cudaSuccess);
+    EXPECT(cudaMemcpy(bb.data(), fb, bb.size(), cudaMemcpyDeviceToHost) == cudaSuccess);
+    EXPECT(a == bb);
     cudaFree(d_idx);
     cudaFree(d_out);
     cudaFree(d_lab);
-    std::printf("input facade: schedule, shards, load, indices, gather bit-exact\n");
+    std::printf("input facade: schedule, shards, load, synth, indices, gather bit-exact\n");
     return 0;
 }
