@@ -178,3 +178,21 @@ def test_copy_of_fixture_keeps_split(tmp_path):
     shutil.copy(os.path.join(GOLD, "drds_small.drds"), p)
     _, lab, _, tr, ev = O.load_dataset(str(p))
     assert (tr, ev) == (len(lab), 0)
+
+
+def test_product_load_header_errors_before_touching_the_gpu(tmp_path):
+    """drb_ds_load rejects a missing file and bad headers before any device work, with the
+    reference's io_error messages (dataset.cpp:103-111) — callable without a GPU."""
+    from paper_2406_03285_b200 import _lib
+    from paper_2406_03285_b200 import dataset as D
+    early = {"missing", "bad_magic", "short_magic", "version2", "short_header"}
+    for name, path in broken_files(tmp_path):
+        if name not in early:
+            continue
+        with pytest.raises(O.io_error) as mine:
+            O.load_dataset(path)
+        with pytest.raises(_lib.io_error) as prod:
+            D.load_dataset(path, 0)
+        assert str(prod.value).split("] ", 1)[1] == str(mine.value), name
+    with pytest.raises(_lib.invalid_argument):
+        _lib.check(_lib.lib.drb_ds_load(None, 0, None))
