@@ -116,24 +116,76 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_baseline_sample(cfg, n_workers: int, iters: int, warmup: int):
-    """Reference engine on the host cores (oracle/_ref), else the C port oracle replay."""
+def load_workload():
+    """paper_2406_03285_b200/workload.py (numpy input generation) loaded by path, so the
+    reference arm never runs the package __init__ (which maps libdrb_b200.so)."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_2406_03285_b200", "workload.py")
+    spec = importlib.util.spec_from_file_location("drb_bench_workload", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["drb_bench_workload"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+STEPS_PER_TASK = 100
+
+
+def bench_config(cfg, n_gpus: int, ring: int):
+    """The one `config` both arms print (same workload, same keys)."""
+    K, cap, S, b = cfg["K"], cfg["cap"], cfg["S"], cfg["b"]
+    return {"workload": cfg["workload"], "K": K, "cap": cap, "b": b, "r": cfg["r"], "c": cfg["c"], "S": S,
+            "tasks": cfg["T"], "steps_per_task": STEPS_PER_TASK,
+            "prefill_steps": cfg["T"] * STEPS_PER_TASK,
+            "parallelism": f"dp{n_gpus}" if n_gpus > 1 else "single",
+            "l2": f"inputs larger than L2: {ring}-batch device ring ({ring * b * S / 2**20:.0f} MiB), "
+                  f"slab {K * cap * S / 2**20:.0f} MiB per GPU"}
+
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": avail, "cpu_count": os.cpu_count()}
+
+
+def cpu_baseline_sample(cfg, n_workers: int, iters: int):
+    """Reference engine on the host cores (oracle/_ref): N in-process workers over loopback
+    TCP, each doing engine.update(m) + augment(m, reps) (proj/tests/test_engine.cpp:57-107,
+    proj/src/runner/overlap.cpp:83-89 with zero train cost), after a prefill of
+    T x steps_per_task steps whose labels cycle through every task, so every class is at
+    capacity (replacements) as in the GPU arm. Falls back to the C port's replay."""
     from oracle.py_oracle import Backend, have_reference
-    from paper_2406_03285_b200.workload import stream_spec
-    spec = stream_spec(cfg["K"], cfg["T"], cfg["b"], cfg["S"], steps_per_task=100, seed=1)
+    wl = load_workload()
+    spec = wl.stream_spec(cfg["K"], cfg["T"], cfg["b"], cfg["S"], steps_per_task=STEPS_PER_TASK, seed=1)
     ring = 8
-    data = np.stack([np.stack([spec.payload(w, i) for i in range(ring)]) for w in range(n_workers)])
-    labels = np.stack([np.stack([spec.labels(w, i) for i in range(ring)]) for w in range(n_workers)])
+    prefill = cfg["T"] * STEPS_PER_TASK
+
+    def step_of(i):  # ring slot i covers task i % T
+        return (i % cfg["T"]) * STEPS_PER_TASK + i
+    data = np.stack([np.stack([spec.payload(w, step_of(i)) for i in range(ring)]) for w in range(n_workers)])
+    labels = np.stack([np.stack([spec.labels(w, step_of(i)) for i in range(ring)]) for w in range(n_workers)])
+    info = host_info()
     if have_reference():
         be = Backend("reference")
         secs, samples = be.engine_bench(n_workers, cfg["K"], cfg["cap"], cfg["S"], cfg["b"], cfg["c"], cfg["r"],
-                                        1, data, labels, warmup, iters)
-        kind, cores = "reference", 2 * n_workers + (3 * n_workers * (n_workers - 1) if n_workers > 1 else 0)
-        cores = min(cores, os.cpu_count() or 1)
+                                        1, data, labels, prefill, iters)
+        # per worker: the training thread and the engine's pipeline thread are the busy ones
+        kind, cores = "reference", min(2 * n_workers, info["nproc"])
     else:
         be = Backend("port")
         rp = be.replay(n_workers, cfg["K"], cfg["cap"], cfg["S"], cfg["c"], cfg["r"], 1)
-        for i in range(warmup):
+        for i in range(prefill):
             rp.step(data[:, i % ring], labels[:, i % ring])
         t0 = time.perf_counter()
         samples = 0
@@ -142,9 +194,11 @@ def cpu_baseline_sample(cfg, n_workers: int, iters: int, warmup: int):
             samples += int(cnt.sum())
         secs = time.perf_counter() - t0
         kind, cores = "port", 1
-    return {"value": samples / secs, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{iters} iterations x {n_workers} worker(s) of {cfg['workload']} after {warmup} warm-up "
-                      f"(f32-packed payload, same byte volume), {samples} augmented samples in {secs:.2f}s"}
+    return {"value": samples / secs, "unit": UNIT, "cores": cores, "kind": kind, **info,
+            "n_workers": n_workers, "seconds": secs,
+            "sample": f"{iters} timed iterations x {n_workers} in-process worker(s) of {cfg['workload']} after a "
+                      f"{prefill}-step prefill to capacity (f32-packed payload, same byte volume), {samples} "
+                      f"augmented samples in {secs:.2f}s"}
 
 
 def run_reference(args, cfg):
@@ -154,18 +208,19 @@ def run_reference(args, cfg):
         return 0
     try:
         iters = max(1, min(args.steps, args.ref_iters))
-        cb = cpu_baseline_sample(cfg, n, iters, min(args.warmup, 50) if args.warmup else 10)
+        cb = cpu_baseline_sample(cfg, n, iters)
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}), flush=True)
         return 0
+    step_samples = (cfg["b"] + cfg["r"]) * n  # steady state: every worker's m' has b + r rows
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": n,
-            "steps": iters, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["b"] * n / cb["value"] if cb["value"] else None,
+            "steps": iters, "warmup": cfg["T"] * STEPS_PER_TASK,
+            "ms_per_step": 1000.0 * step_samples / cb["value"] if cb["value"] else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
-            "data": "synthetic", "config": {"workload": cfg["workload"], "K": cfg["K"], "cap": cfg["cap"],
-                                            "b": cfg["b"], "r": cfg["r"], "c": cfg["c"], "S": cfg["S"],
-                                            "n_workers": n},
+            "data": "synthetic", "config": bench_config(cfg, n, args.ring),
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                                        "d2h_bytes_per_step": 0}}
+                                        "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -179,7 +234,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--ring", type=int, default=64, help="device input batches (>L2 in total)")
     ap.add_argument("--e2e-steps", type=int, default=500)
-    ap.add_argument("--cpu-iters", type=int, default=300)
+    ap.add_argument("--cpu-iters", type=int, default=200)
+    ap.add_argument("--sweep", default="", help="comma-separated step counts: also time one run of each "
+                                                "(fixed per-run cost vs steps; reported as steps_sweep)")
     ap.add_argument("--ref-iters", type=int, default=400)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="issue the timed launches one by one")
@@ -204,7 +261,7 @@ def main():
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device(f"cuda:{local}"))
 
     K, cap, S, b, r, c = cfg["K"], cfg["cap"], cfg["S"], cfg["b"], cfg["r"], cfg["c"]
-    steps_per_task = 100
+    steps_per_task = STEPS_PER_TASK
     spec = stream_spec(K, cfg["T"], b, S, steps_per_task=steps_per_task, seed=1)
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, rank=rank,
                                world=N, device=local)
@@ -272,6 +329,31 @@ def main():
     samples = (b + r) * N * args.steps  # steady state: every rank's m'_i has b + r rows
     value = samples / (t_ms / 1000.0)
     ms_per_step = t_ms / args.steps
+
+    # fixed per-run cost: the same timed region (sync + barrier, one prepared run, events on
+    # its stream) for several run lengths; us_per_step(K) = t(K) / K
+    sweep = []
+    for ks in [int(x) for x in args.sweep.split(",") if x.strip()]:
+        sr = eng.prepare_run(data, lab, ks, first=0) if not args.no_graph else None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        if sr is not None:
+            sr.launch(stream)
+        else:
+            eng.run(data, lab, ks, first=0, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if sr is not None:
+            sr.close()
+        tk = e0.elapsed_time(e1)
+        if N > 1:
+            tt = torch.tensor([tk], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tk = float(tt.item())
+        step += ks
+        sweep.append({"steps": ks, "ms": tk, "us_per_step": 1000.0 * tk / ks})
 
     # per-launch device time of the dominant kernel (drb_copy_kernel: all byte movement of an
     # iteration; sel/plan are 1-CTA kernels running ahead on their own streams), from CUDA
@@ -368,7 +450,7 @@ def main():
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline_sample(cfg, 1, args.cpu_iters, 20)
+            cpu = cpu_baseline_sample(cfg, 1, args.cpu_iters)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)}
 
@@ -377,11 +459,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-            "config": {"workload": cfg["workload"], "K": K, "cap": cap, "b": b, "r": r, "c": c, "S": S,
-                       "tasks": cfg["T"], "steps_per_task": steps_per_task,
-                       "parallelism": f"dp{N}" if N > 1 else "single",
-                       "l2": f"inputs larger than L2: {ring}-batch device ring ({ring * b * S / 2**20:.0f} MiB), "
-                             f"slab {K * cap * S / 2**20:.0f} MiB per GPU"},
+            "config": bench_config(cfg, N, ring),
             "gpu_launches": launches,
             "launch_mode": launch_mode,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
@@ -403,6 +481,7 @@ def main():
                          "bytes_formula": "2*S*(b+r+c) per rank per iteration (SURVEY.md 8d)"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
+            **({"steps_sweep": sweep} if sweep else {}),
         }
         print(json.dumps(line), flush=True)
     if N > 1:

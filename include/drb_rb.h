@@ -91,6 +91,10 @@ typedef struct drb_rb_config {
     uint64_t seed;            /* rng_seed                            (config.hpp:49)     */
     int32_t device;           /* CUDA device ordinal                                     */
     uint32_t flags;           /* reserved, 0                                             */
+    uint32_t aug_ring;        /* m' ring depth: m'_i's slot is rewritten by step i+aug_ring;
+                                 0 = 6 (the default), else >= 6. A deep ring keeps every m'
+                                 of a multi-step run readable (drb_rb_aug_slot)            */
+    uint32_t reserved;        /* 0                                                        */
 } drb_rb_config;
 
 /* Per-class insertion report of one update, replaces insertion_report
@@ -243,6 +247,11 @@ DRB_RB_API drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint6
 DRB_RB_API drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream);
 DRB_RB_API drb_status drb_rb_graph_destroy(drb_rb_graph* g);
 /* Rows of m' for a completed step (blocks on that step's completion). */
+/* m'_step still held by the engine's ring (one of the last aug_ring enqueued steps), for a
+ * step whose batch had n rows: the same views drb_rb_step returned for it. With a deep ring
+ * (drb_rb_config.aug_ring >= steps) every m' of a drb_rb_run stays readable after the run
+ * (step-by-step parity of the benchmarked path). Engine-internal; no reference counterpart. */
+DRB_RB_API drb_status drb_rb_aug_slot(drb_rb* h, uint64_t step, uint32_t n, drb_aug* out);
 DRB_RB_API drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count);
 DRB_RB_API drb_status drb_rb_synchronize(drb_rb* h);
 /* total_wait_ms (engine.hpp:88): host time blocked waiting for round results. */

@@ -22,7 +22,7 @@ DRB_ERR_TRAINING = 6
 DRB_ERR_USAGE = 7
 DRB_ERR_INTERNAL = 8
 MAX_WORLD = 8
-AUG_RING = 3
+AUG_RING = 6  # default m' ring depth (drb_rb_config.aug_ring = 0)
 
 
 class drb_error(RuntimeError):
@@ -74,6 +74,8 @@ class drb_rb_config(C.Structure):
         ("seed", C.c_uint64),
         ("device", C.c_int32),
         ("flags", C.c_uint32),
+        ("aug_ring", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -141,6 +143,7 @@ def _load():
         "drb_rb_graph_launch": (st, [vp, vp]),
         "drb_rb_graph_destroy": (st, [vp]),
         "drb_rb_aug_count": (st, [vp, P(drb_aug), P(u32)]),
+        "drb_rb_aug_slot": (st, [vp, u64, u32, P(drb_aug)]),
         "drb_rb_synchronize": (st, [vp]),
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),

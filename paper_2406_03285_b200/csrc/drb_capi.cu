@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -156,11 +157,12 @@ struct drb_rb {
     uint32_t* report = nullptr;       // [2K+2]
     uint32_t* plist = nullptr;        // [kListRing][plist_words]: P_i, plan(i-1) -> copy(i)
     uint32_t* wlist = nullptr;        // [kListRing][wlist_words]: W_i, sel(i) -> copy(i)
-    uint32_t* mailbox = nullptr;      // host-mapped [4*kAugRing]
+    uint32_t* mailbox = nullptr;      // host-mapped, mb_words(R) (drb_internal.cuh)
     uint32_t* mailbox_dev = nullptr;
     static constexpr int kEv = 16;  // >= kListRing + 1: per-iteration events in flight
     cudaEvent_t ev_user[kEv] = {}, ev_sel[kEv] = {}, ev_plan[kEv] = {}, ev_copy[kEv] = {};
-    cudaEvent_t done[kAugRing] = {};  // completion of the copy that last wrote each m' slot
+    uint32_t aug_ring = kAugRingDefault;  // R: m' ring depth
+    std::vector<cudaEvent_t> done;    // [R] completion of the copy that last wrote each m' slot
     cudaEvent_t in_free[2] = {};      // host path: staging slot reusable
     cudaEvent_t h2d_done[2] = {};
     uint8_t* stage = nullptr;         // host path: device staging [2][max_batch][S]
@@ -178,6 +180,8 @@ struct drb_rb {
     RunCtl* runctl = nullptr;         // device counters of the persistent run
     unsigned long long* prof = nullptr;  // DRB_DBG 65536: sel/plan phase cycle accumulators [64]
     cudaEvent_t run_end = nullptr;
+    cudaEvent_t last_work = nullptr;  // after the handle's latest enqueued iteration (any path)
+    bool last_work_valid = false;
     uint64_t prewaited = 0;           // 1 + the iteration whose sel/plan the copy stream already waited for
     bool use_pdl = true;              // copy(i+1) launched programmatically behind copy(i); DRB_PDL=0 off
     bool started = false, shut_down = false;
@@ -194,7 +198,7 @@ void check_engine_alive(drb_rb* h) {
     // Sticky failure of an earlier round (device-written, host-mapped), observed without
     // blocking. A round whose failure is not yet visible is caught on the device instead
     // (the next launch sees DevState::error and reports it in its own mailbox slot).
-    const uint32_t e = reinterpret_cast<volatile uint32_t*>(h->mailbox)[2 * kAugRing];
+    const uint32_t e = reinterpret_cast<volatile uint32_t*>(h->mailbox)[kMbSticky];
     if (e)
         fail(DRB_ERR_TRAINING, "engine: background pipeline dead: round failed with status " +
                                    std::to_string(e) +
@@ -225,6 +229,8 @@ StepParams base_params(drb_rb* h) {
     p.region[c.rank] = h->region;
     p.slab_peer[c.rank] = h->slab;
     p.off_table = h->layout.off_table;
+    p.off_counts = h->layout.off_counts;
+    p.aug_ring = h->aug_ring;
     p.off_aug = h->layout.off_aug;
     p.off_auglab = h->layout.off_auglab;
     p.aug_slot_bytes = h->layout.aug_slot_bytes;
@@ -434,6 +440,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: max_batch must be in [1, 4096]");
         if (c.rep_count > 4096 || uint64_t(c.world) * c.rep_count > 4096)
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: world * rep_count must be <= 4096");
+        if (c.aug_ring != 0 && (c.aug_ring < kAugRingDefault || c.aug_ring > kAugRingMax))
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: aug_ring must be 0 (default 6) or in [6, 65536]");
         if (uint64_t(c.world) * c.n_classes * c.per_class_cap >= (1ull << 31))
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K*cap must be < 2^31 slots");
         const uint32_t plan_bytes = plan_smem_bytes(c.world, c.n_classes, c.rep_count);
@@ -443,7 +451,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         auto h = new drb_rb();
         std::unique_ptr<drb_rb> guard_h(h);
         h->cfg = c;
-        h->layout = region_layout(c.world, c.n_classes, c.sample_bytes, c.max_batch, c.rep_count);
+        h->aug_ring = c.aug_ring ? c.aug_ring : kAugRingDefault;
+        h->layout = region_layout(c.world, c.n_classes, c.sample_bytes, c.max_batch, c.rep_count, h->aug_ring);
         h->copy_smem = copy_smem(c.world, c.rep_count, c.max_batch).words * 4;
         {
             const char* so = std::getenv("DRB_SOLO");  // DRB_SOLO=0: let the kernels share SMs
@@ -483,9 +492,10 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         cuda_check(cudaMemset(h->plist, 0, uint64_t(kListRing) * plist_words(c.world, c.rep_count) * 4), "memset");
         cuda_check(cudaMalloc(&h->wlist, uint64_t(kListRing) * wlist_words(c.max_batch) * 4), "wlist alloc");
         cuda_check(cudaMemset(h->wlist, 0, uint64_t(kListRing) * wlist_words(c.max_batch) * 4), "memset");
-        cuda_check(cudaHostAlloc(&h->mailbox, 4 * kAugRing * 4, cudaHostAllocMapped), "mailbox");
-        std::memset(h->mailbox, 0, 4 * kAugRing * 4);
+        cuda_check(cudaHostAlloc(&h->mailbox, mb_words(h->aug_ring) * 4, cudaHostAllocMapped), "mailbox");
+        std::memset(h->mailbox, 0, mb_words(h->aug_ring) * 4);
         cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->mailbox_dev), h->mailbox, 0), "mailbox map");
+        h->done.assign(h->aug_ring, nullptr);
         for (auto& e : h->done)
             cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         for (int i = 0; i < drb_rb::kEv; ++i)
@@ -524,6 +534,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             cuda_check(cudaMemset(h->prof, 0, 64 * 8), "prof alloc");
         }
         cuda_check(cudaEventCreateWithFlags(&h->run_end, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&h->last_work, cudaEventDisableTiming), "event");
         if (const char* tr = std::getenv("DRB_TRACE"); tr && tr[0] == '1')
             cuda_check(cudaMalloc(&h->trace, 32 * 8), "trace alloc");
         if (h->dbg_bits & 64) {
@@ -582,6 +593,8 @@ drb_status drb_rb_destroy(drb_rb* h) {
             cudaFree(h->prof);
         if (h->run_end)
             cudaEventDestroy(h->run_end);
+        if (h->last_work)
+            cudaEventDestroy(h->last_work);
         cudaStreamDestroy(h->s_plan);
         cudaStreamDestroy(h->h2d);
         cudaStreamDestroy(h->d2h);
@@ -833,7 +846,7 @@ StepParams iter_params(drb_rb* h, uint64_t i, const void* batch, const uint32_t*
     p.step = i;
     p.seq = i;
     p.mode = kModeUpdate | kModeAssemble | kModePlan | kModePublish | (h->cfg.world > 1 ? kModePeers : 0u);
-    p.aslot = uint32_t(i % kAugRing);
+    p.aslot = uint32_t(i % h->aug_ring);
     const uint64_t pw = plist_words(h->cfg.world, h->cfg.rep_count);
     const uint64_t ww = wlist_words(h->cfg.max_batch);
     p.plist_in = h->plist + (i % kListRing) * pw;   // X_i, built by plan(i), read by copy(i)
@@ -862,8 +875,9 @@ void enqueue_sel(drb_rb* h, uint64_t i, const void* batch, const uint32_t* label
     // and plan(i) of every rank waits for all sel(i) rows. (One rank: stream order.)
     if (i >= h->dep_floor + kListRing)
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - kListRing)], 0), "wait");
-    if (h->cfg.world > 1 && i >= h->dep_floor + kAugRing)
-        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - kAugRing)], 0), "wait");
+    const uint32_t lag = std::min<uint32_t>(h->aug_ring, kTableRing);
+    if (h->cfg.world > 1 && i >= h->dep_floor + lag)
+        cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_copy[ev_of(i - lag)], 0), "wait");
     if (i >= h->dep_floor + 4)
         cuda_check(cudaStreamWaitEvent(h->s_sel, h->ev_plan[ev_of(i - 4)], 0), "wait");
     if (launch_sel(p, h->s_sel, h->use_pdl && (h->dbg_bits & 256)))  // DRB_DBG bit 8: PDL sel chain
@@ -933,6 +947,10 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
     if (ev_end)
         cuda_check(cudaEventRecordWithFlags(ev_end, s, rec_flags), "event");
     cuda_check(cudaEventRecord(h->ev_copy[ev_of(i)], s), "event");
+    if (cap != cudaStreamCaptureStatusActive) {
+        cuda_check(cudaEventRecord(h->last_work, s), "event");
+        h->last_work_valid = true;
+    }
     if (ready_wait && (p.mode & kModePeers) && i > 0) {
         cuda_check(cudaStreamWaitEvent(h->s_wait, h->ev_copy[ev_of(i)], 0), "wait");
         if (launch_peers_wait(p, h->s_wait))
@@ -962,10 +980,19 @@ void enqueue_persistent_run(drb_rb* h, const uint8_t* batches, uint64_t batch_st
                             uint64_t label_stride, uint32_t ring, uint32_t n, uint64_t steps, uint64_t first,
                             cudaStream_t s) {
     const uint64_t i0 = h->step, end = i0 + steps;
-    if (i0 >= h->dep_floor + 1) {
-        cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i0 - 1)], 0), "wait");
-        cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i0 - 1)], 0), "wait");
-        cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i0 - 1)], 0), "wait");
+    cudaStreamCaptureStatus cap0 = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(s, &cap0), "capture query");
+    if (cap0 != cudaStreamCaptureStatusActive) {
+        // every earlier iteration of this handle, whatever path and stream enqueued it (a
+        // persistent run, a launched graph, single steps), completes before this run resets
+        // the run counters and mutates the state (graph_prepare synchronises instead)
+        if (h->last_work_valid)
+            cuda_check(cudaStreamWaitEvent(s, h->last_work, 0), "wait");
+        if (i0 >= h->dep_floor + 1) {
+            cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i0 - 1)], 0), "wait");
+            cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i0 - 1)], 0), "wait");
+            cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i0 - 1)], 0), "wait");
+        }
     }
     RunParams rp{};
     rp.base = iter_params(h, i0, batches, labels, n);
@@ -1003,6 +1030,8 @@ void enqueue_persistent_run(drb_rb* h, const uint8_t* batches, uint64_t batch_st
                 cuda_check(cudaStreamWaitEvent(o, h->run_end, 0), "wait");
         for (auto& e : h->done)
             cuda_check(cudaEventRecord(e, s), "event");
+        cuda_check(cudaEventRecord(h->last_work, s), "event");
+        h->last_work_valid = true;
     }
     h->last_run_persistent = true;
     h->ver = h->ver0 + end;
@@ -1042,7 +1071,7 @@ drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uin
         enqueue_copy(h, i, batch, labels, n, h->stream, !chained, out, nullptr, nullptr, false,
                      h->ev_user[ev_of(i)], true);
         if (s != h->stream || h->cfg.world > 1)
-            cuda_check(cudaStreamWaitEvent(s, h->done[i % kAugRing], 0), "wait");
+            cuda_check(cudaStreamWaitEvent(s, h->done[i % h->aug_ring], 0), "wait");
     });
 }
 
@@ -1130,6 +1159,9 @@ drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_s
         if (const char* dot = std::getenv("DRB_GRAPH_DOT"))  // diagnostics: the captured DAG
             cudaGraphDebugDotPrint(gr->graph, dot, cudaGraphDebugDotFlagsVerbose);
         cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
+        // upload now: the first launch of a never-uploaded graph pays the upload inside it
+        cuda_check(cudaGraphUpload(gr->exec, h->stream), "graph upload");
+        cuda_check(cudaStreamSynchronize(h->stream), "graph upload");
         // events recorded during the capture are graph-internal: later steps must not wait
         // on them (graph_launch orders the handle's streams after the whole graph instead)
         h->dep_floor = h->step;
@@ -1146,6 +1178,10 @@ drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream) {
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->h->stream;
         cuda_check(cudaGraphLaunch(g->exec, s), "graph launch");
         cuda_check(cudaEventRecord(g->h->ev_user[0], s), "event");
+        cuda_check(cudaEventRecord(g->h->last_work, s), "event");
+        g->h->last_work_valid = true;
+        for (auto& e : g->h->done)
+            cuda_check(cudaEventRecord(e, s), "event");
         for (cudaStream_t o : {g->h->stream, g->h->s_sel, g->h->s_plan})
             if (o != s)
                 cuda_check(cudaStreamWaitEvent(o, g->h->ev_user[0], 0), "wait");
@@ -1204,11 +1240,31 @@ drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels
                                    rows * c.sample_bytes, cudaMemcpyDeviceToHost, h->d2h), "d2h");
         cuda_check(cudaMemcpyAsync(out_labels + skip, aug.labels + skip, rows * 4, cudaMemcpyDeviceToHost, h->d2h),
                    "d2h");
-        const auto* hdr = reinterpret_cast<const RegionHeader*>(h->region);
-        cuda_check(cudaMemcpyAsync(out_count, &hdr->aug_count[aug.ring_slot], 4, cudaMemcpyDeviceToHost, h->d2h), "d2h");
+        const auto* counts = reinterpret_cast<const uint32_t*>(h->region + h->layout.off_counts);
+        cuda_check(cudaMemcpyAsync(out_count, counts + aug.ring_slot, 4, cudaMemcpyDeviceToHost, h->d2h), "d2h");
         // The next step may reuse this m' slot only after the copy-out drained.
         cuda_check(cudaEventRecord(h->done[aug.ring_slot], h->d2h), "event");
         cuda_check(cudaStreamWaitEvent(h->stream, h->done[aug.ring_slot], 0), "wait");
+    });
+}
+
+drb_status drb_rb_aug_slot(drb_rb* h, uint64_t step, uint32_t n, drb_aug* out) {
+    DRB_REQUIRE(h && out);
+    return guarded([&] {
+        if (n > h->cfg.max_batch)
+            fail(DRB_ERR_USAGE, "aug_slot: batch larger than max_batch");
+        if (step >= h->step || h->step - step > h->aug_ring)
+            fail(DRB_ERR_USAGE, "aug_slot: step " + std::to_string(step) + " is not among the last " +
+                                    std::to_string(h->aug_ring) + " enqueued steps");
+        const uint32_t slot = uint32_t(step % h->aug_ring);
+        const uint32_t row0 = h->cfg.max_batch - n;
+        out->n = n;
+        out->ring_slot = slot;
+        out->step = step;
+        out->data = h->region + h->layout.off_aug + uint64_t(slot) * h->layout.aug_slot_bytes +
+                    uint64_t(row0) * h->cfg.sample_bytes;
+        out->labels = reinterpret_cast<uint32_t*>(h->region + h->layout.off_auglab) +
+                      uint64_t(slot) * (align_up(h->layout.rows * 4, 256) / 4) + row0;
     });
 }
 
@@ -1220,8 +1276,8 @@ drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count) {
         cuda_check(cudaEventSynchronize(h->done[aug->ring_slot]), "aug wait");
         h->wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         const volatile uint32_t* mb = h->mailbox;
-        const uint32_t e = mb[kAugRing + aug->ring_slot];
-        *count = mb[aug->ring_slot];
+        const uint32_t e = mb[mb_err(aug->ring_slot, h->aug_ring)];
+        *count = mb[mb_count(aug->ring_slot)];
         if (e)
             fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(e));
     });

@@ -27,10 +27,17 @@ constexpr uint32_t kCtaReserved = 1024u;        // per-CTA system reservation
 // CTA 0, then kTlCtaSlots stamps for each of up to kTlMaxCtas copy CTAs.
 constexpr uint32_t kTlCtaSlots = 16, kTlMaxCtas = 160;
 constexpr uint32_t kTlStride = 32 + kTlCtaSlots * kTlMaxCtas;
-// m' buffers per rank. The API promises m'_i until step i+2 is enqueued; the slot is reused
-// by step i+6 (batch rows) and by the pushes of reps(i+5) — a deep ring lets sel(i) order the
-// multi-rank pushes behind copy(i-6) instead of copy(i-3), off the pipeline's critical path.
-constexpr int kAugRing = 6;
+// m' buffers per rank (drb_rb_config.aug_ring, default 6). The API promises m'_i until step
+// i+2 is enqueued; the slot is reused by step i+R (batch rows) and by the pushes of
+// reps(i+R-1). A deep ring (R >= the steps of a run) keeps every m' of the run readable.
+constexpr uint32_t kAugRingDefault = 6;
+constexpr uint32_t kAugRingMax = 1u << 16;
+// Host-mapped mailbox (u32 words): [0] sticky engine error, [1, 64) control words,
+// [64, 64+R) rows of m' per ring slot, [64+R, 64+2R) per-slot round errors.
+constexpr uint32_t kMbSticky = 0, kMbBase = 64;
+__host__ __device__ inline uint32_t mb_count(uint32_t slot) { return kMbBase + slot; }
+__host__ __device__ inline uint32_t mb_err(uint32_t slot, uint32_t R) { return kMbBase + R + slot; }
+__host__ __device__ inline uint32_t mb_words(uint32_t R) { return kMbBase + 2 * R; }
 constexpr int kThreads = 512;  // step kernel CTA size (16 warps)
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
 
@@ -65,19 +72,17 @@ struct alignas(16) PlanState {
 };
 
 // Peer-shareable region header (one cudaMalloc per rank, exported over CUDA IPC).
-static_assert(kAugRing <= 8, "RegionHeader sizes aug_count / repcnt for 8 slots");
 struct alignas(256) RegionHeader {
     uint64_t pushdone[kMaxWorld];  // [w]: 1 + last iteration whose pushes rank w completed
                                    //      (its reps rows of my m'_{i+1} have landed)
-    uint32_t aug_count[8];         // local: rows of m' per ring slot (device copy)
-    uint32_t repcnt[8];            // local: |reps| already written into m' ring slot s
-    uint64_t pad[9];
+    uint64_t pad[24];
 };
 
 struct RegionLayout {
     uint64_t off_table;     // u64 [kTableRing][N][K] occupancy words: version << 32 | occ
-    uint64_t off_aug;       // u8  [kAugRing][rows][S]
-    uint64_t off_auglab;    // u32 [kAugRing][rows]
+    uint64_t off_counts;    // u32 aug_count[R] (rows of m' per ring slot), repcnt[R] (|reps| in slot s)
+    uint64_t off_aug;       // u8  [R][rows][S]
+    uint64_t off_auglab;    // u32 [R][rows]
     uint64_t aug_slot_bytes;
     uint64_t rows;          // max_batch + r
     uint64_t bytes;
@@ -95,17 +100,19 @@ __host__ __device__ inline uint32_t occ_of(uint64_t w) { return uint32_t(w); }
 __host__ __device__ inline bool occ_is(uint64_t w, uint64_t version) { return uint32_t(w >> 32) == uint32_t(version); }
 
 inline RegionLayout region_layout(uint32_t N, uint32_t K, uint64_t S, uint32_t max_batch,
-                                  uint32_t r) {
+                                  uint32_t r, uint32_t R) {
     RegionLayout L{};
     uint64_t off = sizeof(RegionHeader);
     L.off_table = off = align_up(off, 256);
     off += uint64_t(kTableRing) * N * K * 8;
+    L.off_counts = off = align_up(off, 256);
+    off += 2ull * R * 4;
     L.rows = uint64_t(max_batch) + r;
     L.aug_slot_bytes = align_up(L.rows * S, 256);
     L.off_aug = off = align_up(off, 256);
-    off += kAugRing * L.aug_slot_bytes;
+    off += uint64_t(R) * L.aug_slot_bytes;
     L.off_auglab = off = align_up(off, 256);
-    off += uint64_t(kAugRing) * align_up(L.rows * 4, 256);
+    off += uint64_t(R) * align_up(L.rows * 4, 256);
     L.bytes = align_up(off, 4096);
     return L;
 }
@@ -118,6 +125,7 @@ struct StepParams {
     uint64_t seq;                  // launch sequence number of this handle (intra-launch flag)
     uint32_t tslot_in, tslot_out;  // table ring slots of versions i and i+1
     uint32_t aslot;                // m' ring slot of step i
+    uint32_t aug_ring;             // R, m' ring depth
     uint32_t mode;
     uint64_t cand_key, evict_key;
     uint64_t cand_ctr0, evict_ctr0;  // used with kModeCtrParams
@@ -132,12 +140,12 @@ struct StepParams {
     PlanState* plan_out;
     uint8_t* region[kMaxWorld];  // every rank's region base, mapped in this process
     const uint8_t* slab_peer[kMaxWorld];  // every rank's slab, mapped in this process
-    uint64_t off_table, off_aug, off_auglab, aug_slot_bytes, auglab_slot_elems;
+    uint64_t off_table, off_counts, off_aug, off_auglab, aug_slot_bytes, auglab_slot_elems;
     const uint32_t* plist_in;  // copy(i): push list P_i (built by plan(i-1))
     uint32_t* plist_out;       // plan(i): push list P_{i+1}
     uint32_t* wlist;           // sel(i) writes / copy(i) reads the candidate-write list W_i
     uint32_t* report;    // [2K + 2]: appends[K], replacements[K], totals[2]
-    uint32_t* mailbox;   // host-mapped: [kAugRing] counts, [kAugRing] errors
+    uint32_t* mailbox;   // host-mapped, mb_* layout above
     uint64_t timeout_ns;
     uint32_t vec16;      // 16-byte vector path legal (S % 16 == 0, aligned bases)
     uint32_t smem_bytes;

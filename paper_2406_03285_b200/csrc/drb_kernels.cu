@@ -468,6 +468,14 @@ __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
 
 constexpr uint32_t kSelThreads = 128;
 
+// m' ring slot counts of this rank: aug_count[R] then repcnt[R]
+__device__ __forceinline__ uint32_t* counts_of(const StepParams& p) {
+    return reinterpret_cast<uint32_t*>(p.region[p.me] + p.off_counts);
+}
+// How far a rank's sel(i) may run ahead of every peer's pushes (multi-rank): the table slot
+// its row overwrites (kTableRing versions) and the m' slot plan(i) refills (R slots).
+__device__ __forceinline__ uint32_t aug_lag(uint32_t R) { return R < kTableRing ? R : kTableRing; }
+
 // Spin (thread-level) until *flag >= want or the timeout; returns false on timeout.
 __device__ bool wait_flag(const uint64_t* flag, uint64_t want, uint64_t timeout_ns) {
     const uint64_t t0 = globaltimer();
@@ -579,7 +587,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad, const 
         *p.sel_out = o;
         *st = o;
         if (p.mailbox && err)
-            reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = err;
+            reinterpret_cast<volatile uint32_t*>(p.mailbox)[kMbSticky] = err;
     }
     prof_span(p, 15, pt);
 #pragma unroll 1
@@ -596,11 +604,12 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad, const 
             // Every peer finished copy(i-6) (it announced pushdone >= i-5): its plan(i-6) no
             // longer reads the table slot this row overwrites, and its pushes into the m'
             // slot that plan(i) refills have landed. Normally long true: sel runs ahead.
-            if (p.step >= kAugRing && lane < N && lane != me &&
+            const uint32_t lag = aug_lag(p.aug_ring);
+            if (p.step >= lag && lane < N && lane != me &&
                 !wait_flag(&reinterpret_cast<const RegionHeader*>(p.region[me])->pushdone[lane],
-                           p.step - (kAugRing - 1), p.timeout_ns) &&
+                           p.step - (lag - 1), p.timeout_ns) &&
                 p.mailbox)
-                reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = DRB_ERR_TRANSPORT;
+                reinterpret_cast<volatile uint32_t*>(p.mailbox)[kMbSticky] = DRB_ERR_TRANSPORT;
             __syncwarp();
 #pragma unroll 1
             for (uint32_t w = 0; w < N; ++w) {
@@ -777,7 +786,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         prof_span(p, 17, pt);
         if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
             uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
-                           uint64_t((p.aslot + 1) % kAugRing) * p.auglab_slot_elems;
+                           uint64_t((p.aslot + 1) % p.aug_ring) * p.auglab_slot_elems;
 #pragma unroll 1
             for (uint32_t j = lane; j < cnt[q]; j += 32)
                 al[p.nmax + j] = plan[3 * (q * r + j) + 1];
@@ -829,7 +838,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         p.plan_out->error = misc[0];
         st->error = misc[0];
         if (misc[0] && p.mailbox)  // rendezvous failure: the engine is dead from here
-            reinterpret_cast<volatile uint32_t*>(p.mailbox)[2 * kAugRing] = misc[0];
+            reinterpret_cast<volatile uint32_t*>(p.mailbox)[kMbSticky] = misc[0];
     }
     trace_at(p, 8);
 }
@@ -855,8 +864,8 @@ __global__ void drb_plan_next_kernel(const __grid_constant__ StepParams p) {
 __device__ __forceinline__ void mailbox_fail(const StepParams& p, uint32_t err) {
     if (p.mailbox) {
         volatile uint32_t* mb = p.mailbox;
-        mb[kAugRing + p.aslot] = err;
-        mb[2 * kAugRing] = err;
+        mb[mb_err(p.aslot, p.aug_ring)] = err;
+        mb[kMbSticky] = err;
     }
 }
 
@@ -927,20 +936,21 @@ __device__ void copy_parse(const StepParams& p, const uint32_t* xraw, const uint
 // n + |reps(i-1)| (|reps(i-1)| left by copy(i-1) in repcnt) and |reps(i)| for copy(i+1).
 __device__ void copy_counts(const StepParams& p, const uint32_t* xraw) {
     const uint32_t lane = threadIdx.x & 31;
-    RegionHeader* hdr = reinterpret_cast<RegionHeader*>(p.region[p.me]);
     const uint32_t row0 = p.nmax - p.n;
     uint32_t* al = reinterpret_cast<uint32_t*>(p.region[p.me] + p.off_auglab) + uint64_t(p.aslot) * p.auglab_slot_elems;
 #pragma unroll 1
     for (uint32_t x = lane; x < p.n; x += 32)
         al[row0 + x] = __ldg(p.labels + x);
     if (lane == 0) {
-        const uint32_t prev = p.step > 0 ? hdr->repcnt[p.aslot] : 0u;
-        hdr->aug_count[p.aslot] = p.n + prev;
-        hdr->repcnt[(p.aslot + 1) % kAugRing] = xraw[0];
+        uint32_t* aug_count = counts_of(p);
+        uint32_t* repcnt = aug_count + p.aug_ring;
+        const uint32_t prev = p.step > 0 ? repcnt[p.aslot] : 0u;
+        aug_count[p.aslot] = p.n + prev;
+        repcnt[(p.aslot + 1) % p.aug_ring] = xraw[0];
         if (p.mailbox) {
             volatile uint32_t* mb = p.mailbox;
-            mb[p.aslot] = p.n + prev;
-            mb[kAugRing + p.aslot] = 0;
+            mb[mb_count(p.aslot)] = p.n + prev;
+            mb[mb_err(p.aslot, p.aug_ring)] = 0;
         }
     }
 }
@@ -1008,7 +1018,7 @@ __global__ void __launch_bounds__(kThreads, 1) drb_copy_kernel(const __grid_cons
     V* slab = reinterpret_cast<V*>(p.slab);
     V* asm_dst = reinterpret_cast<V*>(p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes) +
                  uint64_t(p.nmax - n) * nvec;
-    const uint32_t next_slot = (p.aslot + 1) % kAugRing;
+    const uint32_t next_slot = (p.aslot + 1) % p.aug_ring;
     const uint32_t* jdst = xraw + 4;
 
     tl_mark(p, 2, false);
@@ -1189,7 +1199,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
     const uint8_t* batch = reinterpret_cast<const uint8_t*>(p.batch);
     uint8_t* slab = reinterpret_cast<uint8_t*>(p.slab);
     uint8_t* my_aug = p.region[me] + p.off_aug + uint64_t(p.aslot) * p.aug_slot_bytes;
-    const uint32_t next_slot = (p.aslot + 1) % kAugRing;
+    const uint32_t next_slot = (p.aslot + 1) % p.aug_ring;
     const uint32_t row0 = p.nmax - n;
     const uint32_t* jdst = xraw + 4;
     volatile uint32_t* ready = misc + 6;
@@ -1400,7 +1410,7 @@ __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, 
                 rp.ctl->where = (9u << 24) | uint32_t(want & 0xffffff);
             if (rp.base.mailbox) {
                 volatile uint32_t* mb = rp.base.mailbox;
-                mb[2 * kAugRing] = DRB_ERR_TRANSPORT;
+                mb[kMbSticky] = DRB_ERR_TRANSPORT;
             }
             return false;
         }
@@ -1424,7 +1434,7 @@ __device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t k) {
     p.n = rp.n;
     p.step = i;
     p.seq = i;
-    p.aslot = static_cast<uint32_t>(i % kAugRing);
+    p.aslot = static_cast<uint32_t>(i % p.aug_ring);
     p.plist_in = rp.plist_base + (i % kListRing) * rp.pw;
     p.plist_out = const_cast<uint32_t*>(p.plist_in);
     p.wlist = rp.wlist_base + (i % kListRing) * rp.ww;
@@ -1562,7 +1572,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             if (k > 0)
                 run_patch(sp, rp, k);
             // W slot (k-8) / m' slot (multi, k-6) / table slot (plan(k-4)) free
-            const uint64_t wb = back(k, multi ? kAugRing - 1 : kListRing - 1), wp = back(k, 3);
+            const uint64_t wb = back(k, multi ? aug_lag(b.aug_ring) - 1 : kListRing - 1), wp = back(k, 3);
             bool ok = true;
             if (seen[0] < wb)
                 ok = run_wait(&rp.ctl->b_done, wb, rp, false);
@@ -1570,8 +1580,8 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                 ok = run_wait(&rp.ctl->plan_done, wp, rp, false);
             run_mark(rp, rp.i0 + k, 1);
             for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-6) complete (m' slot)
-                if (w != me && sp.step >= kAugRing)
-                    ok = run_wait(&hdr->pushdone[w], sp.step - kAugRing + 1, rp, true);
+                if (w != me && sp.step >= aug_lag(b.aug_ring))
+                    ok = run_wait(&hdr->pushdone[w], sp.step - aug_lag(b.aug_ring) + 1, rp, true);
             flag[1] = ok ? 0u : 1u;
             flag[0] = flag[2];  // "bad" of m_k's labels
             flag[3] = 0;
@@ -1877,7 +1887,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         {
             const uint8_t* batch = sp.batch;
             uint8_t* slab = reinterpret_cast<uint8_t*>(sp.slab);
-            const uint32_t next_slot = (sp.aslot + 1) % kAugRing;
+            const uint32_t next_slot = (sp.aslot + 1) % b.aug_ring;
             for (uint32_t x = lane; x < pieces; x += 32) {
                 const uint8_t* src;
                 uint8_t* dst;
@@ -2017,7 +2027,6 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         // list's |reps(k)| is read before this CTA's arrival lets plan(k+8) reuse its slot.
         volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
         const bool multi = (b.mode & kModePeers) && b.N > 1;
-        RegionHeader* hdr = reinterpret_cast<RegionHeader*>(b.region[b.me]);
         const uint32_t row0 = b.nmax - rp.n;
         uint32_t prev = 0;
         auto wait_cta = [&](const volatile unsigned long long* f, uint64_t want, uint64_t k) {
@@ -2046,7 +2055,7 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                 if (!__shfl_sync(kFull, wait_cta(&fl->parsed[k & 3], k + 1, k) ? 1 : 0, 0))
                     return;
                 const uint64_t i = rp.i0 + k;
-                const uint32_t aslot = static_cast<uint32_t>(i % kAugRing);
+                const uint32_t aslot = static_cast<uint32_t>(i % b.aug_ring);
                 const uint32_t* lab = rp.labels + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.label_stride;
                 uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
                                uint64_t(aslot) * b.auglab_slot_elems;
@@ -2066,14 +2075,16 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                         al[row0 + x] = __ldg(lab + x);
                 }
                 if (lane == 0) {
+                    uint32_t* aug_count = counts_of(b);
+                    uint32_t* repcnt = aug_count + b.aug_ring;
                     if (k == 0)
-                        prev = i > 0 ? __ldcg(&hdr->repcnt[aslot]) : 0u;
-                    hdr->aug_count[aslot] = rp.n + prev;
-                    hdr->repcnt[(aslot + 1) % kAugRing] = nrep;
+                        prev = i > 0 ? __ldcg(&repcnt[aslot]) : 0u;
+                    aug_count[aslot] = rp.n + prev;
+                    repcnt[(aslot + 1) % b.aug_ring] = nrep;
                     if (b.mailbox) {
                         volatile uint32_t* mb = b.mailbox;
-                        mb[aslot] = rp.n + prev;
-                        mb[kAugRing + aslot] = 0;
+                        mb[mb_count(aslot)] = rp.n + prev;
+                        mb[mb_err(aslot, b.aug_ring)] = 0;
                     }
                     prev = nrep;
                 }
@@ -2106,7 +2117,7 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         // group but the newest — A(k-1)'s last window — has finished)
         asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
         const uint8_t* batch = rp.batches + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.batch_stride;
-        uint8_t* dst = b.region[b.me] + b.off_aug + (i % kAugRing) * b.aug_slot_bytes + uint64_t(row0) * S;
+        uint8_t* dst = b.region[b.me] + b.off_aug + (i % b.aug_ring) * b.aug_slot_bytes + uint64_t(row0) * S;
         for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
             const uint32_t w1 = min(nA, w0 + kTmaStagesA);
             bulk_wait_read_all();  // the ring's previous window has been stored

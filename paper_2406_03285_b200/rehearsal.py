@@ -194,15 +194,16 @@ class rehearsal_buffer:
 
     def __init__(self, n_classes: int, per_class_cap: int, sample_bytes: int, *, max_batch: int = 64,
                  candidate_count: int = 14, rep_count: int = 7, seed: int = 1, rank: int = 0,
-                 world: int = 1, device: int = 0):
+                 world: int = 1, device: int = 0, aug_ring: int = 0):
         cfg = _lib.drb_rb_config(n_classes=n_classes, per_class_cap=per_class_cap, sample_bytes=sample_bytes,
                                  max_batch=max_batch, candidate_count=candidate_count, rep_count=rep_count,
-                                 rank=rank, world=world, seed=seed, device=device, flags=0)
+                                 rank=rank, world=world, seed=seed, device=device, flags=0, aug_ring=aug_ring)
         self.h = C.c_void_p()
         check(lib.drb_rb_create(C.byref(cfg), C.byref(self.h)))
         self.K, self.cap, self.S = n_classes, per_class_cap, sample_bytes
         self.max_batch, self.c, self.r = max_batch, candidate_count, rep_count
         self.seed, self.rank, self.world, self.device = seed, rank, world, device
+        self.aug_ring = aug_ring or _lib.AUG_RING
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:
@@ -290,6 +291,26 @@ class rehearsal_buffer:
         g, t, s = C.c_uint32(), C.c_uint32(), C.c_uint32()
         check(lib.drb_rb_launch_info(self.h, C.byref(g), C.byref(t), C.byref(s)))
         return int(g.value), int(t.value), int(s.value)
+
+
+def _ring_args(buf: "rehearsal_buffer", data_ring: torch.Tensor, label_ring: torch.Tensor, what: str):
+    """A device input ring as the C ABI takes it: bytes [B, n, S] (any payload dtype, row
+    stride in BYTES) and uint32/int32 labels [B, n]."""
+    if not data_ring.is_cuda or not label_ring.is_cuda:
+        raise _lib.usage_error(f"{what}: rings must be CUDA tensors")
+    if data_ring.dim() < 2 or label_ring.dim() != 2:
+        raise _lib.usage_error(f"{what}: data ring [B, n, ...] and label ring [B, n] expected")
+    B, n = int(data_ring.shape[0]), int(data_ring.shape[1])
+    if tuple(label_ring.shape) != (B, n):
+        raise _lib.usage_error(f"{what}: label ring must be [B, n] = [{B}, {n}]")
+    if n > buf.max_batch:
+        raise _lib.usage_error(f"{what}: batch of {n} rows exceeds max_batch {buf.max_batch}")
+    data = data_ring.contiguous().view(torch.uint8).reshape(B, n, -1)
+    if int(data.shape[2]) != buf.S:
+        raise _lib.usage_error(f"{what}: samples are {int(data.shape[2])} bytes, the buffer holds {buf.S}")
+    labels = label_ring if label_ring.dtype in (torch.int32, torch.uint32) else label_ring.to(torch.int32)
+    labels = labels.contiguous()
+    return data, labels, B, n
 
 
 class augmented_batch:
@@ -393,13 +414,11 @@ class engine:
 
     def run(self, data_ring: torch.Tensor, label_ring: torch.Tensor, steps: int, first: int = 0,
             stream: Optional[torch.cuda.Stream] = None, events=None) -> None:
-        """`steps` iterations over a device ring: data [B, n, S] uint8, labels [B', n] int32;
-        iteration i uses data[(first+i) % B] and labels[(first+i) % B'] (B' multiple of B
-        not required: label rows are indexed by their own ring length)."""
-        B, n = int(data_ring.shape[0]), int(data_ring.shape[1])
+        """`steps` iterations over a device ring: data [B, n, ...] (any dtype; each row is S
+        bytes), labels [B, n] int32/int64/uint32; iteration i uses data[(first+i) % B] and
+        labels[(first+i) % B]."""
+        data_ring, label_ring, B, n = _ring_args(self.buffer, data_ring, label_ring, "run")
         s = stream if stream is not None else torch.cuda.current_stream(self.buffer.device)
-        if label_ring.shape[0] != B:
-            raise _lib.usage_error("run: data and label rings must have the same length")
         ev = None
         if events is not None:
             ev = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
@@ -413,9 +432,7 @@ class engine:
                     first: int = 0, events=None) -> "prepared_run":
         """Capture `steps` iterations (as run()) into a CUDA graph; launch it once, in order.
         events: optional 2*steps torch.cuda.Event (timing) bracketing each copy kernel."""
-        B, n = int(data_ring.shape[0]), int(data_ring.shape[1])
-        if label_ring.shape[0] != B:
-            raise _lib.usage_error("prepare_run: data and label rings must have the same length")
+        data_ring, label_ring, B, n = _ring_args(self.buffer, data_ring, label_ring, "prepare_run")
         ev = None
         if events is not None:
             ev = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
@@ -425,6 +442,13 @@ class engine:
                                        C.byref(g)))
         self.iteration += steps
         return prepared_run(g, (data_ring, label_ring))
+
+    def aug_slot(self, step: int, n: int) -> augmented_batch:
+        """m'_step as the engine's ring still holds it (one of the last aug_ring steps; its
+        batch had n rows). With aug_ring >= steps every m' of a run() stays readable."""
+        aug = _lib.drb_aug()
+        check(lib.drb_rb_aug_slot(self.buffer.h, step, n, C.byref(aug)))
+        return augmented_batch(self, aug)
 
     def synchronize(self) -> None:
         check(lib.drb_rb_synchronize(self.buffer.h))

@@ -23,8 +23,9 @@ def main():
     dist.init_process_group("gloo", init_method="env://")
     K, cap, S, b, c, r, seed, steps = 16, 6, 256, 32, 14, 9, 3, 60
     spec = stream_spec(K, 2, b, S, steps_per_task=20, seed=seed)
+    run_steps = int(os.environ.get("DRB_PIN_RUN", "50"))  # then one run(), every m' of it pinned
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed, rank=rank,
-                               world=world, device=local)
+                               world=world, device=local, aug_ring=max(6, run_steps + 1))
     from paper_2406_03285_b200.dist import connect_world
     connect_world(buf)
     eng = drb.engine(buf)
@@ -44,12 +45,35 @@ def main():
         if not ok:
             bad += 1
             print(f"rank {rank} step {i}: mismatch (count {cnt} vs {oc[rank]})", flush=True)
+    # the benchmarked path: one multi-step run over a device ring, every rank's m'_k read back
+    # from the deep m' ring after the run and compared step by step
+    if run_steps:
+        first = steps
+        rd = np.stack([np.stack([spec.payload(w, first + k) for w in range(world)]) for k in range(run_steps)])
+        rl = np.stack([np.stack([spec.labels(w, first + k) for w in range(world)]) for k in range(run_steps)])
+        d_ring = torch.from_numpy(np.ascontiguousarray(rd[:, rank])).cuda(local)
+        l_ring = torch.from_numpy(rl[:, rank].astype(np.int32)).cuda(local)
+        eng.run(d_ring, l_ring, run_steps)
+        torch.cuda.synchronize()
+        for k in range(run_steps):
+            o, ol, oc = rep.step(rd[k], rl[k])
+            aug = eng.aug_slot(first + k, b)
+            d, l = aug.tensors()
+            cnt = aug.count()
+            ok = cnt == int(oc[rank]) and np.array_equal(l.cpu().numpy().astype(np.uint32), ol[rank, :cnt]) and \
+                np.array_equal(d.cpu().numpy(), o[rank, :cnt])
+            if not ok:
+                bad += 1
+                print(f"rank {rank} run step {first + k}: mismatch (count {cnt} vs {oc[rank]})", flush=True)
+        # every rank is done reading its peers' pushes before any rank tears down
+        dist.barrier()
     eng.shutdown()
     t = torch.tensor([bad])
     dist.all_reduce(t)
     dist.destroy_process_group()
     if rank == 0:
-        print(f"ipc parity: {world} ranks x {steps} steps, mismatching rank-steps: {int(t.item())}", flush=True)
+        print(f"ipc parity: {world} ranks x ({steps} update steps + a {run_steps}-step run), "
+              f"mismatching rank-steps: {int(t.item())}", flush=True)
     sys.exit(1 if int(t.item()) else 0)
 
 
