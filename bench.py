@@ -37,8 +37,12 @@ CONFIGS = {
                b=64, r=8, c=14),
     "c3": dict(workload="imagenet1k-224x224x3-u8-10pct-per-gpu", K=1000, T=4, cap=128, S=224 * 224 * 3,
                dtype="u8", b=56, r=7, c=14),
-    "c4": dict(workload="imagenet100-224x224x3-fp16-b128", K=100, T=4, cap=48, S=224 * 224 * 3 * 2,
+    "c4": dict(workload="imagenet100-224x224x3-fp16-b128-r28", K=100, T=4, cap=48, S=224 * 224 * 3 * 2,
                dtype="f16", b=128, r=28, c=14),
+    "c4r14": dict(workload="imagenet100-224x224x3-fp16-b128-r14", K=100, T=4, cap=48, S=224 * 224 * 3 * 2,
+                  dtype="f16", b=128, r=14, c=14),
+    "c4r7": dict(workload="imagenet100-224x224x3-fp16-b128-r7", K=100, T=4, cap=48, S=224 * 224 * 3 * 2,
+                 dtype="f16", b=128, r=7, c=14),
     "c5": dict(workload="sensor-128x128x1-fp32", K=50, T=1, cap=40, S=128 * 128 * 4, dtype="f32",
                b=256, r=32, c=14),
 }
@@ -263,8 +267,10 @@ def main():
     K, cap, S, b, r, c = cfg["K"], cfg["cap"], cfg["S"], cfg["b"], cfg["r"], cfg["c"]
     steps_per_task = STEPS_PER_TASK
     spec = stream_spec(K, cfg["T"], b, S, steps_per_task=steps_per_task, seed=1)
+    # the whole GPU for the engine: the bench has no training step to share the SMs with
+    engine_ctas = torch.cuda.get_device_properties(local).multi_processor_count
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, rank=rank,
-                               world=N, device=local)
+                               world=N, device=local, engine_ctas=engine_ctas)
     if N > 1:
         from paper_2406_03285_b200.dist import connect_world
         connect_world(buf)
@@ -304,12 +310,14 @@ def main():
     # timed region: K steps, back to back, device-timed (events on the launching stream).
     # The K launches are captured into a CUDA graph beforehand (host launch cost paid
     # outside the timed region, as a training loop would replay a captured step).
+    resident = eng.engine_info()["resident"]
     run = eng.prepare_run(data, lab, args.steps, first=args.warmup) if not args.no_graph else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         barrier()
         torch.cuda.synchronize()
+        inst0 = eng.engine_info()["instances"]
         ev0.record(stream)
         if run is not None:
             run.launch(stream)
@@ -318,6 +326,7 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
+    timed_instances = eng.engine_info()["instances"] - inst0
     if run is not None:
         run.close()
     t_ms = ev0.elapsed_time(ev1)
@@ -355,26 +364,47 @@ def main():
         step += ks
         sweep.append({"steps": ks, "ms": tk, "us_per_step": 1000.0 * tk / ks})
 
-    # per-launch device time of the dominant kernel (drb_copy_kernel: all byte movement of an
-    # iteration; sel/plan are 1-CTA kernels running ahead on their own streams), from CUDA
-    # events recorded inside the captured graph around each copy launch
-    nper = 256
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nper)]
-    for e in evs:  # torch creates the CUDA event lazily on first record
-        e.record(stream)
-    stream.synchronize()
-    barrier()
-    krun = eng.prepare_run(data, lab, nper, first=0, events=evs)
-    krun.launch(stream)
-    torch.cuda.synchronize()
-    krun.close()
-    launch_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(nper)]
-    kernel_ms = float(np.median(launch_ms))
-    step += nper
-    if N > 1:
-        tt = torch.tensor([kernel_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        kernel_ms = float(tt.item())
+    # The drop-in API a trainer calls (trainer.cpp:109-113): update(m_i) on one stream, one call
+    # per step, serial (the next post follows the previous m' on the stream, as in a training
+    # loop with zero train cost), inputs resident in HBM, device-timed like the run above.
+    def time_updates(nsteps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        inst0 = eng.engine_info()["instances"]
+        e0.record(stream)
+        for k in range(nsteps):
+            eng.update((data[k % ring], lab[k % ring]), stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tk = e0.elapsed_time(e1)
+        if N > 1:
+            tt = torch.tensor([tk], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tk = float(tt.item())
+        return 1000.0 * tk / nsteps, eng.engine_info()["instances"] - inst0
+    upd_us, upd_launch = time_updates(args.steps)
+    upd_us_200, _ = time_updates(200)
+    step += args.steps + 200
+    kernel_ms = None
+    if not resident:  # three-kernel path: per-launch copy-kernel times from events in the graph
+        nper = 256
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nper)]
+        for e in evs:  # torch creates the CUDA event lazily on first record
+            e.record(stream)
+        stream.synchronize()
+        barrier()
+        krun = eng.prepare_run(data, lab, nper, first=0, events=evs)
+        krun.launch(stream)
+        torch.cuda.synchronize()
+        krun.close()
+        launch_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(nper)]
+        kernel_ms = float(np.median(launch_ms))
+        step += nper
+        if N > 1:
+            tt = torch.tensor([kernel_ms], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            kernel_ms = float(tt.item())
 
     # e2e through the host-buffer C-ABI call drb_rb_step_host: pinned host m_i in, m'_i
     # assembled in place in the caller's buffer (rows [0, b) are m_i, the r representative
@@ -408,7 +438,6 @@ def main():
     e2e_value = (b + r) * N * e2e_steps / e2e_s
     eng.shutdown()
 
-    persistent = os.environ.get("DRB_PERSIST", "1") != "0" and not args.no_graph
     # PCIe ceiling of the e2e leg: the same H2D + D2H bytes as one step, plain pinned copies
     h2d_b, d2h_b = b * (S + 4), r * (S + 4) + 4
     pin_in = torch.empty(h2d_b, dtype=torch.uint8).pin_memory()
@@ -427,10 +456,11 @@ def main():
         torch.cuda.synchronize()
         pcie_s = time.perf_counter() - t0
     pcie_steps_per_s = e2e_steps / pcie_s
-    # our kernels inside the timed region: sel + plan + copy per step (three-kernel path,
-    # captured in one CUDA graph, DRB_PERSIST=0), or one cooperative launch for the whole run
-    launches = 1 if persistent else 3 * args.steps
-    launch_mode = "persistent-cooperative" if persistent else ("cuda-graph" if not args.no_graph else "direct")
+    # our kernels inside the timed region: the resident engine's instances launched there (one
+    # cooperative kernel per busy period; steps are posted with stream memory operations), or
+    # sel + plan + copy per step on the three-kernel path (DRB_PERSIST=0)
+    launches = timed_instances if resident else 3 * args.steps
+    launch_mode = "resident-cooperative" if resident else ("cuda-graph" if not args.no_graph else "direct")
     peak, peak_kind = peaks()
     bytes_step = hbm_bytes_per_step(cfg)
     # The copy kernel is the only bulk kernel and runs back to back, one launch per step, so
@@ -461,7 +491,14 @@ def main():
             "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
             "config": bench_config(cfg, N, ring),
             "gpu_launches": launches,
+            "engine": eng.engine_info(),
             "launch_mode": launch_mode,
+            "update_us_per_step": upd_us,
+            "update": {"us_per_step": upd_us, "steps": args.steps, "us_per_step_200": upd_us_200,
+                       "instances_launched": upd_launch,
+                       "api": "engine.update(m_i) per step on one stream (drb_rb_step: descriptor post + "
+                              "stream wait for m'_i, no kernel launch per step), inputs resident in HBM, "
+                              "device-timed; serial: each post follows the previous m' on the stream"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
                     "d2h_bytes_per_step": d2h_b, "steps": e2e_steps,
                     "api": "drb_rb_step_host, m' assembled in place in the caller's pinned batch buffer",
@@ -472,12 +509,13 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "algorithmic_bytes_per_step": bytes_step,
-                         "algorithmic_bytes_per_launch": bytes_step * (args.steps if persistent else 1),
+                         "algorithmic_bytes_per_launch": bytes_step * (args.steps if resident else 1),
                          "kernel_ms_per_step": ms_per_step,
-                         "kernel": "drb_run_kernel" if persistent else "drb_copy_tma_kernel",
-                         "timing": ("one persistent launch = the whole timed region (K steps); CUDA events on its "
-                                    "stream / K" if persistent else "CUDA events over the timed region / K steps"),
-                         "three_kernel_copy_ms_event_bracketed": kernel_ms,
+                         "kernel": "drb_run_kernel" if resident else "drb_copy_tma_kernel",
+                         "timing": ("the resident engine processes the K steps of the timed region (its instance "
+                                    "launch, pipeline fill and drain included); CUDA events on the posting stream / K"
+                                    if resident else "CUDA events over the timed region / K steps"),
+                         **({"three_kernel_copy_ms_event_bracketed": kernel_ms} if kernel_ms is not None else {}),
                          "bytes_formula": "2*S*(b+r+c) per rank per iteration (SURVEY.md 8d)"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),

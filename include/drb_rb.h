@@ -94,7 +94,8 @@ typedef struct drb_rb_config {
     uint32_t aug_ring;        /* m' ring depth: m'_i's slot is rewritten by step i+aug_ring;
                                  0 = 6 (the default), else >= 6. A deep ring keeps every m'
                                  of a multi-step run readable (drb_rb_aug_slot)            */
-    uint32_t reserved;        /* 0                                                        */
+    uint32_t engine_ctas;     /* CTAs (one per SM) of the resident engine while busy; 0 = half
+                                 the SMs, leaving the rest to a co-running training step  */
 } drb_rb_config;
 
 /* Per-class insertion report of one update, replaces insertion_report
@@ -251,6 +252,11 @@ DRB_RB_API drb_status drb_rb_graph_destroy(drb_rb_graph* g);
  * step whose batch had n rows: the same views drb_rb_step returned for it. With a deep ring
  * (drb_rb_config.aug_ring >= steps) every m' of a drb_rb_run stays readable after the run
  * (step-by-step parity of the benchmarked path). Engine-internal; no reference counterpart. */
+/* Resident-engine bookkeeping (no reference counterpart): whether the engine runs as a
+ * resident kernel, how many instances have been launched so far (one per busy period; a
+ * step itself launches nothing), descriptors posted, CTAs per instance. */
+DRB_RB_API drb_status drb_rb_engine_info(drb_rb* h, uint32_t* resident, uint64_t* instances,
+                                         uint64_t* posted, uint32_t* grid);
 DRB_RB_API drb_status drb_rb_aug_slot(drb_rb* h, uint64_t step, uint32_t n, drb_aug* out);
 DRB_RB_API drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count);
 DRB_RB_API drb_status drb_rb_synchronize(drb_rb* h);

@@ -192,6 +192,49 @@ int or_update_buffer(uint8_t* slab, uint32_t* slab_labels, uint32_t* occ, uint64
     return 0;
 }
 
+/* read_slots (rehearsal_buffer.cpp:88-142) */
+int or_read_slots(const uint8_t* slab, const uint32_t* slab_labels, const uint32_t* occ, uint32_t K,
+                  uint32_t cap, uint64_t S, const uint32_t* req, uint32_t count, or_stream* sub,
+                  uint8_t* out, uint32_t* out_labels, uint8_t* status) {
+    uint64_t total = 0; /* m_total (rehearsal_buffer.hpp:89) = sum of occupancies */
+    for (uint32_t c = 0; c < K; ++c)
+        total += occ[c];
+    for (uint32_t i = 0; i < count; ++i) {
+        const uint32_t cls = req[2 * i], slot = req[2 * i + 1];
+        int64_t row = -1;
+        uint8_t st = 2;
+        if (cls < K && occ[cls] > 0) { /* :96-103 */
+            if (slot < occ[cls]) {
+                st = 0;
+                row = (int64_t)cls * cap + slot;
+            } else {
+                st = 1;
+                row = (int64_t)cls * cap + (int64_t)or_bounded(sub, occ[cls]);
+            }
+        }
+        if (st == 2 && total > 0) { /* :106-121 flat fallback over the whole buffer */
+            uint64_t flat = or_bounded(sub, total);
+            for (uint32_t c = 0; c < K; ++c) {
+                if (flat < occ[c]) {
+                    st = 1;
+                    row = (int64_t)c * cap + (int64_t)flat;
+                    break;
+                }
+                flat -= occ[c];
+            }
+        }
+        status[i] = st;
+        if (row >= 0) {
+            memcpy(out + (size_t)i * S, slab + (size_t)row * S, S);
+            out_labels[i] = slab_labels[row];
+        } else {
+            memset(out + (size_t)i * S, 0, S);
+            out_labels[i] = 0;
+        }
+    }
+    return 0;
+}
+
 /* ---- S5 synchronous replay --------------------------------------------------------- */
 
 typedef struct replay {

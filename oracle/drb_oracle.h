@@ -53,6 +53,17 @@ int or_update_buffer(uint8_t* slab, uint32_t* slab_labels, uint32_t* occ, uint64
                      const uint32_t* labels, uint32_t n, uint32_t c, or_stream* cand,
                      or_stream* evict, uint32_t* report_appends, uint32_t* report_repl);
 
+/* read_slots on one rank's slab (rehearsal_buffer.cpp:88-142): req = (cls, slot) pairs.
+ * Exact read if slot < occ[cls]; a stale index draws a substitute slot of the class
+ * (sub.bounded(occ)); an empty (or out-of-range) class falls back to a uniform draw over every
+ * stored slot (sub.bounded(total), class-major flat order); nothing stored -> empty (zero
+ * bytes, label 0, as serve_sample sends it, engine.cpp:239-244). status: 0 exact,
+ * 1 substituted, 2 empty. (The reference's retry after a concurrent append cannot occur in a
+ * single-threaded replay.) */
+int or_read_slots(const uint8_t* slab, const uint32_t* slab_labels, const uint32_t* occ, uint32_t K,
+                  uint32_t cap, uint64_t S, const uint32_t* req, uint32_t count, or_stream* sub,
+                  uint8_t* out, uint32_t* out_labels, uint8_t* status);
+
 /* Synchronous multi-rank replay (S5): the bit-exact oracle of SURVEY.md §8c.
  * Same signatures as oracle/ref_capi.cpp's ref_replay_*. */
 void* or_replay_create(uint32_t N, uint32_t K, uint32_t cap, uint64_t S, uint32_t c, uint32_t r,

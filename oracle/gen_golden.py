@@ -11,6 +11,9 @@ Outputs:
                             seed=5, 1e5 draws; N=2 fill 40, N=4 fill 80, local-only control):
                             sha256 of the reference's per-slot counts, its chi-square
                             statistic and p-value (make_bias_report)
+  tests/golden/read_slots.json  read_slots of the reference's rehearsal_buffer after update
+                            rounds: statuses, labels, sha256 of the returned bytes, and the
+                            substitute stream's next draw (exact / substituted / empty paths)
 """
 from __future__ import annotations
 
@@ -126,9 +129,60 @@ def bias(be, draws):
     return out
 
 
+# read_slots (rehearsal_buffer.cpp:88-142) against the reference's own buffer: (name, K, cap, S,
+# rounds, n, c, seed, keyed, purpose, k1, k2). The requests of every scenario mix exact reads,
+# stale indices (slot >= occupancy: a substitute drawn within the class), empty classes and
+# classes >= K (the whole-buffer flat fallback), so every branch consumes the stream. The
+# last field is the task count of the input stream (2: half the classes never stored).
+READ_SLOTS_CONFIGS = [
+    ("serve_subst_keyed", 6, 4, 32, 3, 8, 5, 11, 1, 6, 0x5E, 0, 1),  # engine.cpp:33-35 serve stream
+    ("slot_subst_plain", 10, 3, 16, 6, 12, 9, 4, 0, 6, 0, 0, 1),      # engine.cpp:31 substitute stream
+    ("full_classes", 4, 2, 48, 8, 16, 12, 7, 1, 6, 0x5E, 0, 1),
+    ("half_empty", 8, 4, 32, 4, 8, 6, 13, 1, 6, 0x5E, 0, 2),
+    ("nothing_stored", 5, 3, 16, 0, 8, 4, 2, 1, 6, 0x5E, 0, 1),
+]
+
+
+def read_slots_requests(K, cap, occ, seed):
+    rng = np.random.default_rng(seed)
+    req = []
+    for k in range(K + 2):  # two classes past K
+        for _ in range(3):
+            o = int(occ[k]) if k < K else 0
+            if o and rng.random() < 0.4:
+                req.append((k, int(rng.integers(0, o))))           # exact
+            else:
+                req.append((k, int(rng.integers(o, cap + 3))))     # stale / empty / out of range
+    return req
+
+
+def read_slots_golden():
+    from oracle.py_oracle import reference_read_slots
+    out = {}
+    for name, K, cap, S, rounds, n, c, seed, keyed, purpose, k1, k2, T in READ_SLOTS_CONFIGS:
+        spec = stream_spec(K, T, n, S, steps_per_task=10**9, seed=seed)
+        batches = np.stack([spec.payload(0, i, n) for i in range(rounds)]) if rounds else np.zeros((0, n, S), np.uint8)
+        labels = np.stack([spec.labels(0, i, n) for i in range(rounds)]) if rounds else np.zeros((0, n), np.uint32)
+        # occupancy first (a pass with no requests), then the requests built against it
+        _, _, _, _, occ = reference_read_slots(K, cap, S, batches, labels, c, seed, keyed, purpose, k1, k2, [])
+        req = read_slots_requests(K, cap, occ, seed)
+        d, lab, st, nxt, occ = reference_read_slots(K, cap, S, batches, labels, c, seed, keyed, purpose, k1, k2, req)
+        out[name] = {"config": dict(K=K, cap=cap, S=S, rounds=rounds, n=n, c=c, seed=seed, keyed=keyed,
+                                    purpose=purpose, k1=k1, k2=k2, T=T),
+                     "requests": req, "occ": occ.tolist(), "status": st.tolist(), "labels": lab.tolist(),
+                     "bytes_sha256": hashlib.sha256(np.ascontiguousarray(d).tobytes()).hexdigest(),
+                     "sub_next_u64": hex(nxt)}
+    return out
+
+
 def main():
     be = Backend("reference")
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "read_slots":
+        with open(os.path.join(OUT, "read_slots.json"), "w") as f:
+            json.dump(read_slots_golden(), f, indent=1)
+        print("wrote read_slots.json")
+        return
     with open(os.path.join(OUT, "kat.json"), "w") as f:
         json.dump(kat(be), f)
     rep = {}
@@ -140,6 +194,8 @@ def main():
         json.dump(rep, f)
     with open(os.path.join(OUT, "bias.json"), "w") as f:
         json.dump({"draws_1e5": bias(be, 100000), "draws_2000": bias(be, 2000)}, f, indent=1)
+    with open(os.path.join(OUT, "read_slots.json"), "w") as f:
+        json.dump(read_slots_golden(), f, indent=1)
     print("wrote", os.listdir(OUT))
 
 

@@ -222,6 +222,55 @@ class OracleBuffer:
         return rc, app, rep
 
 
+    def read_slots(self, requests, sub):
+        """read_slots (rehearsal_buffer.cpp:88-142) with the substitute stream `sub`
+        (or_read_slots). Returns (bytes [count, S], labels, status)."""
+        f = self.lib.or_read_slots
+        f.restype = C.c_int
+        f.argtypes = [_u8p, _u32p, _u32p, C.c_uint32, C.c_uint32, C.c_uint64, _u32p, C.c_uint32,
+                      C.POINTER(_or_stream), _u8p, _u32p, _u8p]
+        cnt = len(requests)
+        req = np.ascontiguousarray(np.asarray(requests, np.uint32).reshape(-1)) if cnt else np.zeros(2, np.uint32)
+        out = np.zeros((max(cnt, 1), self.S), np.uint8)
+        out_l = np.zeros(max(cnt, 1), np.uint32)
+        st = np.zeros(max(cnt, 1), np.uint8)
+        f(self.slab.reshape(-1), self.slab_labels.reshape(-1), self.occ, self.K, self.cap, self.S, req, cnt,
+          C.byref(sub), out.reshape(-1), out_l, st)
+        return out[:cnt], out_l[:cnt], st[:cnt]
+
+    def next_u64(self, s):
+        f = self.lib.or_next_u64
+        f.restype = C.c_uint64
+        f.argtypes = [C.POINTER(_or_stream)]
+        return int(f(C.byref(s)))
+
+
+def reference_read_slots(K, cap, S, batches, labels, c, seed, keyed, purpose, k1, k2, requests):
+    """The reference's own rehearsal_buffer: len(batches) update_buffer rounds, then one
+    read_slots with the given substitute stream (ref_read_slots_scenario). Returns (bytes,
+    labels, status, the substitute stream's next draw, occupancy)."""
+    lib = C.CDLL(REF_LIB)
+    f = lib.ref_read_slots_scenario
+    f.restype = C.c_int
+    f.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, _u8p, _u32p, C.c_uint32, C.c_uint32, C.c_uint64,
+                  C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, _u32p, C.c_uint32, _u8p, _u32p, _u8p, _u64p, _u32p]
+    rounds, n = int(labels.shape[0]), int(labels.shape[1])
+    cnt = len(requests)
+    req = np.ascontiguousarray(np.asarray(requests, np.uint32).reshape(-1)) if cnt else np.zeros(2, np.uint32)
+    out = np.zeros((max(cnt, 1), S), np.uint8)
+    out_l = np.zeros(max(cnt, 1), np.uint32)
+    st = np.zeros(max(cnt, 1), np.uint8)
+    nxt = np.zeros(1, np.uint64)
+    occ = np.zeros(K, np.uint32)
+    b = np.ascontiguousarray(batches, np.uint8).reshape(-1) if rounds * n else np.zeros(1, np.uint8)
+    l = np.ascontiguousarray(labels, np.uint32).reshape(-1) if rounds * n else np.zeros(1, np.uint32)
+    rc = f(K, cap, S, rounds, b, l, n, c, seed, int(keyed), purpose, k1, k2, req, cnt, out.reshape(-1), out_l, st,
+           nxt, occ)
+    if rc:
+        raise RuntimeError(f"ref_read_slots_scenario failed rc={rc}")
+    return out[:cnt], out_l[:cnt], st[:cnt], int(nxt[0]), occ
+
+
 # ---- global-sampling bias test (proj/src/runner/bias.cpp:35-154), test infrastructure -----
 def bias_view(N: int, K: int, fill: int) -> np.ndarray:
     """Frozen occupancy after the fill phase (bias.cpp:42-45,84-89): rank w inserts

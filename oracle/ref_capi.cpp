@@ -354,6 +354,51 @@ int ref_engine_bench(std::uint32_t N, std::uint32_t K, std::uint32_t cap, std::u
     }
 }
 
+// rehearsal_buffer(K, cap), `rounds` update_buffer calls (streams (seed, 0, candidate) and
+// (seed, 0, eviction)), then ONE read_slots(req, sub) with sub = keyed or plain
+// (seed, 0, purpose, k1, k2): the exact / substituted / empty branches of
+// proj/src/buffer/rehearsal_buffer.cpp:88-142 and the substitute draws they consume.
+// batches: rounds x n x S, labels rounds x n. out: count x S, out_labels, status[count],
+// *sub_next = the substitute stream's next draw afterwards (its counter position; the
+// counter itself is private), occ_out[K] the occupancy.
+int ref_read_slots_scenario(std::uint32_t K, std::uint32_t cap, std::uint64_t S, std::uint32_t rounds,
+                            const std::uint8_t* batches, const std::uint32_t* labels, std::uint32_t n,
+                            std::uint32_t c, std::uint64_t seed, int keyed, std::uint32_t purpose,
+                            std::uint64_t k1, std::uint64_t k2, const std::uint32_t* req, std::uint32_t count,
+                            std::uint8_t* out, std::uint32_t* out_labels, std::uint8_t* status,
+                            std::uint64_t* sub_next, std::uint32_t* occ_out) {
+    try {
+        rehearsal_buffer buf(K, cap);
+        rng_stream cand(seed, 0, rng_stream::purpose::candidate_selection);
+        rng_stream evict(seed, 0, rng_stream::purpose::eviction);
+        for (std::uint32_t i = 0; i < rounds; ++i)
+            buf.update_buffer(to_batch(batches + std::size_t(i) * n * S, labels + std::size_t(i) * n, n, S), c,
+                              cand, evict);
+        rng_stream sub = make_stream(seed, 0, purpose, keyed, k1, k2);
+        std::vector<read_request> rq(count);
+        for (std::uint32_t i = 0; i < count; ++i)
+            rq[i] = read_request{req[2 * i], req[2 * i + 1]};
+        const auto got = buf.read_slots(rq, sub);
+        for (std::uint32_t i = 0; i < count; ++i) {
+            status[i] = static_cast<std::uint8_t>(got[i].status);
+            if (got[i].status == read_status::empty) {
+                std::memset(out + std::size_t(i) * S, 0, S);
+                out_labels[i] = 0;
+            } else {
+                std::memcpy(out + std::size_t(i) * S, got[i].value.features.data(), S);
+                out_labels[i] = got[i].value.label;
+            }
+        }
+        *sub_next = sub.next_u64();
+        const auto snap = buf.snapshot();
+        for (std::uint32_t k = 0; k < K; ++k)
+            occ_out[k] = snap.per_class[k];
+        return 0;
+    } catch (const std::exception&) {
+        return 8;
+    }
+}
+
 // make_bias_report (proj/src/metrics/metrics.cpp:90-107): Pearson chi-square of per-slot
 // hit counts against uniform, p-value by the reference's gamma_q (stats.cpp:54-96).
 int ref_bias_report(const std::uint64_t* counts, std::uint64_t n, std::uint64_t rep_count,

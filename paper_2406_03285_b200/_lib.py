@@ -75,7 +75,7 @@ class drb_rb_config(C.Structure):
         ("device", C.c_int32),
         ("flags", C.c_uint32),
         ("aug_ring", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("engine_ctas", C.c_uint32),
     ]
 
 
@@ -144,6 +144,7 @@ def _load():
         "drb_rb_graph_destroy": (st, [vp]),
         "drb_rb_aug_count": (st, [vp, P(drb_aug), P(u32)]),
         "drb_rb_aug_slot": (st, [vp, u64, u32, P(drb_aug)]),
+        "drb_rb_engine_info": (st, [vp, P(u32), P(u64), P(u64), P(u32)]),
         "drb_rb_synchronize": (st, [vp]),
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),

@@ -2,10 +2,12 @@
 // wiring, launch sequencing, error mapping. Conventions follow the reference C ABI
 // (proj/src/capi/drb_capi.cpp:15-59): thread-local last error, status codes, guarded calls.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -15,6 +17,7 @@
 #include <stdexcept>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "drb_internal.cuh"
@@ -175,9 +178,23 @@ struct drb_rb {
     uint64_t ver0 = 0;                // engine: table version / state parities at start()
     uint32_t sel_par0 = 0, plan_par0 = 0;
     uint32_t dbg_bits = 0;            // DRB_DBG experiment bits (0 in production)
-    bool use_persist = true;          // drb_rb_run as one persistent cooperative launch (DRB_PERSIST=0 off)
-    bool last_run_persistent = false; // the latest drb_rb_run was one persistent launch
-    RunCtl* runctl = nullptr;         // device counters of the persistent run
+    bool use_persist = true;          // resident engine (DRB_PERSIST=0: three kernels per step)
+    bool last_run_persistent = false; // (three-kernel path) the latest drb_rb_run was persistent
+    RunCtl* runctl = nullptr;         // device counters of the resident engine
+    bool rmode = false;               // this engine runs resident (decided at start())
+    FeedDesc* feed = nullptr;         // [kFeedRing] descriptor mirror (device)
+    FeedDesc* hdesc = nullptr;        // [kFeedRing] descriptors as the host writes them (mapped)
+    FeedDesc* hdesc_dev = nullptr;    // its device address
+    uint64_t* feed_seq = nullptr;     // [kFeedRing] posted sequence words (device)
+    uint64_t posted = 0;              // descriptors posted
+    uint64_t gen = 0;                 // generation of the latest launched instance
+    bool alive = false;               // an instance of generation `gen` may be running or queued
+    cudaStream_t s_run = nullptr;     // where instances run, one behind the other
+    uint32_t run_grid = 0;            // CTAs of an instance (2 control + copy CTAs)
+    uint64_t idle_ns = 100ull * 1000;  // an idle instance leaves after this long (frees its SMs)
+    uint8_t* astage = nullptr;        // staging of unaligned device batches [4][max_batch][S]
+    bool feed_kernels = false;        // post / wait with tiny kernels instead of memory operations
+    bool feeder_last = true;          // feeder + ready warps on the last copy CTA, not the sel CTA
     unsigned long long* prof = nullptr;  // DRB_DBG 65536: sel/plan phase cycle accumulators [64]
     cudaEvent_t run_end = nullptr;
     cudaEvent_t last_work = nullptr;  // after the handle's latest enqueued iteration (any path)
@@ -259,6 +276,149 @@ StepParams base_params(drb_rb* h) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Stream memory operations (driver API, resolved through the runtime: no -lcuda): the
+// resident engine's descriptors are posted and its `ready` word is waited for in stream
+// order on the caller's stream, with no kernel launch.
+struct memops_t {
+    CUresult (*batch)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int) = nullptr;
+    CUresult (*wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+    bool ok = false;
+};
+const memops_t& memops() {
+    static const memops_t m = [] {
+        memops_t r{};
+        cudaDriverEntryPointQueryResult q{};
+        void* f = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            r.batch = reinterpret_cast<decltype(r.batch)>(f);
+        f = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue64", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            r.wait64 = reinterpret_cast<decltype(r.wait64)>(f);
+        cudaGetLastError();
+        r.ok = r.batch && r.wait64;
+        return r;
+    }();
+    return m;
+}
+
+volatile unsigned long long* mb64(drb_rb* h, uint32_t word) {
+    return reinterpret_cast<volatile unsigned long long*>(h->mailbox + word);
+}
+
+// Launch the next instance of the resident engine on s_run (behind the previous one).
+void rmode_launch(drb_rb* h) {
+    RunParams rp{};
+    rp.base = base_params(h);
+    rp.base.mode = kModeUpdate | kModeAssemble | kModePlan | kModePublish | (h->cfg.world > 1 ? kModePeers : 0u);
+    rp.base.vec16 = 1;
+    rp.feed = h->feed;
+    rp.hdesc = h->hdesc_dev;
+    rp.feed_seq = h->feed_seq;
+    rp.desc_done_host = reinterpret_cast<volatile unsigned long long*>(h->mailbox_dev + kMbDescDone);
+    rp.ctl = h->runctl;
+    rp.ver0 = h->ver0;
+    rp.sel_base = h->sel;
+    rp.plan_base = h->plan;
+    rp.plist_base = h->plist;
+    rp.wlist_base = h->wlist;
+    rp.gen = h->gen + 1;
+    rp.idle_ns = h->idle_ns;
+    rp.host_posted = reinterpret_cast<const volatile unsigned long long*>(h->mailbox_dev + kMbHostPosted);
+    rp.exiting = reinterpret_cast<volatile unsigned long long*>(h->mailbox_dev + kMbExiting);
+    rp.quiesce = reinterpret_cast<const volatile uint32_t*>(h->mailbox_dev + kMbQuiesce);
+    rp.sel_par0 = h->sel_par0;
+    rp.plan_par0 = h->plan_par0;
+    rp.pw = plist_words(h->cfg.world, h->cfg.rep_count);
+    rp.ww = wlist_words(h->cfg.max_batch);
+    rp.copy_ctas = h->run_grid - 2;
+    rp.feeder_cta = h->feeder_last ? h->run_grid - 1 : 0;
+    if (launch_run(rp, h->run_grid, h->s_run))
+        fail(DRB_ERR_INTERNAL, std::string("resident engine launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    h->gen = rp.gen;
+    h->alive = true;
+}
+
+// Post one descriptor (steps [i_begin, i_begin + count) over an input ring) in stream order
+// on `s`, launching an instance first if none is resident (or the resident one is leaving).
+// The descriptor goes into mapped host memory; `s` then stores its sequence word (and, with
+// wait_end, waits until m'_{wait_end-1} is ready): one stream memory-operation batch.
+void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
+                uint64_t label_stride, uint32_t ring, uint32_t first, uint32_t n, uint64_t i_begin, uint32_t count,
+                cudaStream_t s, uint64_t wait_end = 0) {
+    const uint64_t j = h->posted;
+    if (j >= kFeedRing) {  // ring slot j % kFeedRing: descriptor j - kFeedRing must be consumed
+        const uint64_t need = j - kFeedRing + 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (*mb64(h, kMbDescDone) < need) {
+            check_engine_alive(h);
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(h->timeout_ns))
+                fail(DRB_ERR_TRAINING, "engine: " + std::to_string(kFeedRing) +
+                                           " posted steps are not consumed (is a posting stream blocked?)");
+            std::this_thread::yield();
+        }
+    }
+    FeedDesc& d = h->hdesc[j % kFeedRing];
+    d.batches = reinterpret_cast<uint64_t>(batches);
+    d.labels = reinterpret_cast<uint64_t>(labels);
+    d.batch_stride = batch_stride;
+    d.label_stride = label_stride;
+    d.i_begin = i_begin;
+    d.count_n = uint64_t(count) | (uint64_t(n) << 32);
+    d.ring_first = uint64_t(ring) | (uint64_t(first) << 32);
+    d.seq = j + 1;
+    *reinterpret_cast<volatile uint32_t*>(h->mailbox + kMbQuiesce) = 0;
+    *mb64(h, kMbHostPosted) = j + 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);  // (Dekker with the leaving feeder)
+    const uint64_t ex = *mb64(h, kMbExiting);
+    if (!h->alive || (ex >> 32) == (h->gen & 0xffffffffull))
+        rmode_launch(h);
+    uint64_t* seq = h->feed_seq + (j % kFeedRing);
+    if (h->feed_kernels) {
+        if (launch_feed_post(seq, j + 1, s) || (wait_end && launch_feed_wait(&h->runctl->ready, wait_end, s)))
+            fail(DRB_ERR_INTERNAL, std::string("feed post failed: ") + cudaGetErrorString(cudaGetLastError()));
+    } else {
+        CUstreamBatchMemOpParams ops[2];
+        std::memset(ops, 0, sizeof ops);
+        ops[0].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+        ops[0].writeValue.address = reinterpret_cast<CUdeviceptr>(seq);
+        ops[0].writeValue.value64 = j + 1;
+        ops[0].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;  // after the stream's prior work
+        uint32_t c = 1;
+        if (wait_end) {
+            ops[1].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+            ops[1].waitValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->ready);
+            ops[1].waitValue.value64 = wait_end;
+            ops[1].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+            c = 2;
+        }
+        const CUresult r = memops().batch(reinterpret_cast<CUstream>(s), c, ops, 0);
+        if (r != CUDA_SUCCESS)
+            fail(DRB_ERR_INTERNAL, "feed post: cuStreamBatchMemOp failed (" + std::to_string(int(r)) + ")");
+    }
+    h->posted = j + 1;
+}
+
+// `s` waits (in stream order) until m'_{end-1} is ready, i.e. every iteration < end is done.
+void rmode_wait(drb_rb* h, uint64_t end, cudaStream_t s) {
+    if (h->feed_kernels) {
+        if (launch_feed_wait(&h->runctl->ready, end, s))
+            fail(DRB_ERR_INTERNAL, std::string("feed wait failed: ") + cudaGetErrorString(cudaGetLastError()));
+        return;
+    }
+    const CUresult r = memops().wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(&h->runctl->ready),
+                                       end, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS)
+        fail(DRB_ERR_INTERNAL, "feed wait: cuStreamWaitValue64 failed (" + std::to_string(int(r)) + ")");
+}
+
+// Ask a resident instance to leave as soon as it is idle (before a device-wide sync).
+void rmode_quiesce(drb_rb* h) {
+    if (h->rmode)
+        *reinterpret_cast<volatile uint32_t*>(h->mailbox + kMbQuiesce) = 1;
+}
+
 }  // namespace
 
 extern "C" {
@@ -325,7 +485,7 @@ drb_status drb_plan(uint32_t want, uint32_t n_workers, uint32_t n_classes, const
         const uint32_t entries = uint32_t(want < total ? want : total);
         dev_tmp d_occ(nk * 4), d_out(size_t(entries) * 12), d_cnt(4), d_ctr(8);
         cuda_check(cudaMemcpy(d_occ.p, occ, nk * 4, cudaMemcpyHostToDevice), "plan occ");
-        if (launch_plan(s->key, s->ctr, want, n_workers, n_classes, d_occ.as<uint32_t>(),
+        if (launch_plan(s->key, s->ctr, want, entries, n_workers, n_classes, d_occ.as<uint32_t>(),
                         d_out.as<uint32_t>(), d_cnt.as<uint32_t>(), d_ctr.as<uint64_t>(), nullptr))
             fail(DRB_ERR_INTERNAL, "plan launch failed");
         uint32_t c = 0;
@@ -477,6 +637,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         cuda_check(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&h->s_wait, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&h->s_run, cudaStreamNonBlocking), "stream");
         const uint64_t slab_bytes = uint64_t(c.n_classes) * c.per_class_cap * c.sample_bytes;
         cuda_check(cudaMalloc(&h->slab, slab_bytes), "slab alloc");
         cuda_check(cudaMalloc(&h->slab_labels, uint64_t(c.n_classes) * c.per_class_cap * 4), "labels alloc");
@@ -529,6 +690,27 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         if (const char* pe = std::getenv("DRB_PERSIST"))
             h->use_persist = pe[0] == '1';
         cuda_check(cudaMalloc(&h->runctl, sizeof(RunCtl)), "run state alloc");
+        cuda_check(cudaMemset(h->runctl, 0, sizeof(RunCtl)), "memset");
+        cuda_check(cudaMalloc(&h->feed, kFeedRing * sizeof(FeedDesc)), "feed alloc");
+        cuda_check(cudaMemset(h->feed, 0, kFeedRing * sizeof(FeedDesc)), "memset");
+        cuda_check(cudaMalloc(&h->feed_seq, kFeedRing * 8), "feed alloc");
+        cuda_check(cudaMemset(h->feed_seq, 0, kFeedRing * 8), "memset");
+        cuda_check(cudaHostAlloc(&h->hdesc, kFeedRing * sizeof(FeedDesc), cudaHostAllocMapped), "feed alloc");
+        std::memset(h->hdesc, 0, kFeedRing * sizeof(FeedDesc));
+        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->hdesc_dev), h->hdesc, 0), "feed map");
+        // engine CTAs: half the GPU by default, so a training step co-runs on the other half
+        h->run_grid = c.engine_ctas ? std::max(3u, std::min(uint32_t(h->sm_count), c.engine_ctas))
+                                    : std::max(4u, uint32_t(h->sm_count) / 2);
+        if (const char* rg = std::getenv("DRB_RUN_GRID"))
+            h->run_grid = std::max(3u, std::min(uint32_t(h->sm_count), uint32_t(std::strtoul(rg, nullptr, 10))));
+        if (const char* iu = std::getenv("DRB_IDLE_US"))
+            h->idle_ns = std::strtoull(iu, nullptr, 10) * 1000ull;
+        if (const char* fl = std::getenv("DRB_FEEDER_LAST"))
+            h->feeder_last = fl[0] != '0';
+        if (const char* fk = std::getenv("DRB_FEED"); fk && std::string(fk) == "kernel")
+            h->feed_kernels = true;
+        if (!memops().ok)
+            h->feed_kernels = true;
         if (h->dbg_bits & 65536) {
             cuda_check(cudaMalloc(&h->prof, 64 * 8), "prof alloc");
             cuda_check(cudaMemset(h->prof, 0, 64 * 8), "prof alloc");
@@ -556,6 +738,7 @@ drb_status drb_rb_destroy(drb_rb* h) {
         return DRB_OK;
     return guarded([&] {
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);
         cudaDeviceSynchronize();
         for (uint32_t w = 0; w < h->cfg.world; ++w) {
             if (h->peer_opened[w])
@@ -589,6 +772,12 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaStreamDestroy(h->s_sel);
         if (h->runctl)
             cudaFree(h->runctl);
+        cudaFree(h->feed);
+        cudaFree(h->feed_seq);
+        if (h->hdesc)
+            cudaFreeHost(h->hdesc);
+        cudaFree(h->astage);
+        cudaStreamDestroy(h->s_run);
         if (h->prof)
             cudaFree(h->prof);
         if (h->run_end)
@@ -666,6 +855,7 @@ drb_status drb_rb_read_slots(drb_rb* h, const drb_read_request* requests, uint32
         const uint64_t* row = reinterpret_cast<const uint64_t*>(h->region + h->layout.off_table) +
                               (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
                               uint64_t(h->cfg.rank) * h->cfg.n_classes;
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "read_slots order");
         dev_tmp d_occ(size_t(h->cfg.n_classes) * 4);  // the counts of the versioned words
         cuda_check(cudaMemcpy2D(d_occ.p, 4, row, 8, 4, h->cfg.n_classes, cudaMemcpyDeviceToDevice), "occ copy");
@@ -685,6 +875,7 @@ drb_status drb_rb_snapshot(drb_rb* h, uint32_t* per_class, uint64_t* version) {
     DRB_REQUIRE(h && per_class && version);
     return guarded([&] {
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "snapshot order");
         const uint64_t* row = reinterpret_cast<const uint64_t*>(h->region + h->layout.off_table) +
                               (h->ver % kTableRing) * uint64_t(h->cfg.world) * h->cfg.n_classes +
@@ -700,6 +891,7 @@ drb_status drb_rb_total_stored(drb_rb* h, uint64_t* out) {
     DRB_REQUIRE(h && out);
     return guarded([&] {
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "order");
         SelState st{};
         cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
@@ -711,6 +903,7 @@ drb_status drb_rb_cross_class_evictions(drb_rb* h, uint64_t* out) {
     DRB_REQUIRE(h && out);
     return guarded([&] {
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "order");
         SelState st{};
         cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
@@ -811,6 +1004,25 @@ drb_status drb_rb_start(drb_rb* h) {
         h->ver0 = h->ver - h->step;  // iteration i uses table version ver0 + i
         h->sel_par0 = h->cur_sel;
         h->plan_par0 = h->cur_plan;
+        // Resident engine unless disabled (DRB_PERSIST=0) or samples are not 16-byte rows
+        // (TMA bulk copies); the three-kernel path serves those.
+        h->rmode = h->use_persist && h->cfg.sample_bytes % 16 == 0 && h->sm_count >= 4 &&
+                   run_smem_bytes(h->cfg.world, h->cfg.n_classes, h->cfg.rep_count, h->cfg.max_batch) <= 227u * 1024u;
+        if (h->rmode) {
+            device_guard g(h->cfg.device);
+            RunCtl rc{};
+            rc.sel_done = rc.plan_done = rc.b_done = rc.admitted = rc.ready = h->step;
+            rc.next_step[1] = h->step;  // the first instance is generation 1
+            rc.next_desc[1] = 0;
+            cuda_check(cudaMemcpy(h->runctl, &rc, sizeof rc, cudaMemcpyHostToDevice), "engine state");
+            h->posted = 0;
+            h->gen = 0;
+            h->alive = false;
+            *mb64(h, kMbHostPosted) = 0;
+            *mb64(h, kMbExiting) = 0;
+            *mb64(h, kMbDescDone) = 0;
+            cuda_check(cudaMemset(h->feed_seq, 0, kFeedRing * 8), "feed reset");
+        }
     });
 }
 
@@ -823,7 +1035,29 @@ drb_status drb_rb_shutdown(drb_rb* h) {
             fail(DRB_ERR_USAGE, "engine: double shutdown");
         h->shut_down = true;
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);  // the resident instance leaves once everything posted is done
         cuda_check(cudaDeviceSynchronize(), "shutdown drain");
+        if (h->cfg.world > 1 && h->step > 0) {
+            // Peers may still be pushing this rank's last reps into its m' ring (they run at
+            // most a step behind): wait, bounded, for every peer's final announcement, so a
+            // drb_rb_destroy after shutdown never frees memory a peer still writes.
+            const auto* hdr = reinterpret_cast<const RegionHeader*>(h->region);
+            const auto t0 = std::chrono::steady_clock::now();
+            for (;;) {
+                uint64_t pd[kMaxWorld] = {};
+                cuda_check(cudaMemcpy(pd, hdr->pushdone, sizeof pd, cudaMemcpyDeviceToHost), "peer drain");
+                bool all = true;
+                for (uint32_t w = 0; w < h->cfg.world; ++w)
+                    if (w != h->cfg.rank && pd[w] < h->step)
+                        all = false;
+                if (all)
+                    break;
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(h->timeout_ns))
+                    fail(DRB_ERR_TRANSPORT, "engine: shutdown: a peer did not finish its last step");
+                std::this_thread::sleep_for(std::chrono::microseconds(50));
+            }
+        }
+        h->alive = false;
     });
 }
 
@@ -973,74 +1207,60 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
     h->step = i + 1;
 }
 
-// drb_rb_run as one persistent cooperative launch: the prior iterations (their
-// sel / plan / copy kernels on any stream) complete first; afterwards every engine stream
-// orders behind the run and later steps wait on no per-iteration event of it.
-void enqueue_persistent_run(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
-                            uint64_t label_stride, uint32_t ring, uint32_t n, uint64_t steps, uint64_t first,
-                            cudaStream_t s) {
-    const uint64_t i0 = h->step, end = i0 + steps;
-    cudaStreamCaptureStatus cap0 = cudaStreamCaptureStatusNone;
-    cuda_check(cudaStreamIsCapturing(s, &cap0), "capture query");
-    if (cap0 != cudaStreamCaptureStatusActive) {
-        // every earlier iteration of this handle, whatever path and stream enqueued it (a
-        // persistent run, a launched graph, single steps), completes before this run resets
-        // the run counters and mutates the state (graph_prepare synchronises instead)
-        if (h->last_work_valid)
-            cuda_check(cudaStreamWaitEvent(s, h->last_work, 0), "wait");
-        if (i0 >= h->dep_floor + 1) {
-            cuda_check(cudaStreamWaitEvent(s, h->ev_sel[ev_of(i0 - 1)], 0), "wait");
-            cuda_check(cudaStreamWaitEvent(s, h->ev_plan[ev_of(i0 - 1)], 0), "wait");
-            cuda_check(cudaStreamWaitEvent(s, h->ev_copy[ev_of(i0 - 1)], 0), "wait");
-        }
+// Host view of the state after h->step iterations (table version, state parities), as the
+// three-kernel path keeps it (snapshot, device_error, read_slots read it).
+void rmode_advance(drb_rb* h) {
+    h->ver = h->ver0 + h->step;
+    h->cur_sel = uint32_t((h->sel_par0 + h->step) & 1);
+    h->cur_plan = uint32_t((h->plan_par0 + h->step) & 1);
+}
+
+// One step through the resident engine: post m_i's descriptor on `s`, then `s`
+// waits for "m'_i ready". An unaligned device batch is first copied into a staging slot.
+void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n, cudaStream_t s, drb_aug* out) {
+    const uint64_t i = h->step;
+    const auto& c = h->cfg;
+    const uint8_t* b = static_cast<const uint8_t*>(batch);
+    if (n > 0 && !aligned16(batch)) {
+        constexpr uint32_t kStage = 4;
+        if (!h->astage)
+            cuda_check(cudaMalloc(&h->astage, uint64_t(kStage) * c.max_batch * c.sample_bytes), "stage alloc");
+        if (i >= kStage)  // the slot's previous batch (step i-4) is no longer read
+            rmode_wait(h, i - kStage + 1, s);
+        uint8_t* slot = h->astage + (i % kStage) * uint64_t(c.max_batch) * c.sample_bytes;
+        cuda_check(cudaMemcpyAsync(slot, batch, uint64_t(n) * c.sample_bytes, cudaMemcpyDeviceToDevice, s), "stage");
+        b = slot;
     }
-    RunParams rp{};
-    rp.base = iter_params(h, i0, batches, labels, n);
-    rp.batches = batches;
-    rp.batch_stride = batch_stride;
-    rp.labels = labels;
-    rp.label_stride = label_stride;
-    rp.first = first;
-    rp.i0 = i0;
-    rp.steps = steps;
-    rp.ver0 = h->ver0;
-    rp.sel_base = h->sel;
-    rp.plan_base = h->plan;
-    rp.plist_base = h->plist;
-    rp.wlist_base = h->wlist;
-    rp.ctl = h->runctl;
-    rp.ring = ring;
-    rp.n = n;
-    rp.sel_par0 = h->sel_par0;
-    rp.plan_par0 = h->plan_par0;
-    rp.pw = plist_words(h->cfg.world, h->cfg.rep_count);
-    rp.ww = wlist_words(h->cfg.max_batch);
-    const uint32_t grid = uint32_t(h->sm_count);
-    rp.copy_ctas = grid - 2;
-    rp.first_mod = uint32_t(first % ring);
-    cuda_check(cudaMemsetAsync(h->runctl, 0, sizeof(RunCtl), s), "run state reset");
-    if (launch_run(rp, grid, s))
-        fail(DRB_ERR_INTERNAL, std::string("persistent run launch failed: ") + cudaGetErrorString(cudaGetLastError()));
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cuda_check(cudaStreamIsCapturing(s, &cap), "capture query");
-    if (cap != cudaStreamCaptureStatusActive) {  // (a captured run: graph_launch orders the streams)
-        cuda_check(cudaEventRecord(h->run_end, s), "event");
-        for (cudaStream_t o : {h->stream, h->s_sel, h->s_plan})
-            if (o != s)
-                cuda_check(cudaStreamWaitEvent(o, h->run_end, 0), "wait");
-        for (auto& e : h->done)
-            cuda_check(cudaEventRecord(e, s), "event");
-        cuda_check(cudaEventRecord(h->last_work, s), "event");
-        h->last_work_valid = true;
+    rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, i + 1);
+    const uint32_t slot = uint32_t(i % h->aug_ring);
+    cuda_check(cudaEventRecord(h->done[slot], s), "event record");
+    const uint32_t row0 = c.max_batch - n;
+    out->n = n;
+    out->ring_slot = slot;
+    out->step = i;
+    out->data = h->region + h->layout.off_aug + uint64_t(slot) * h->layout.aug_slot_bytes + uint64_t(row0) * c.sample_bytes;
+    out->labels = reinterpret_cast<uint32_t*>(h->region + h->layout.off_auglab) +
+                  uint64_t(slot) * (align_up(h->layout.rows * 4, 256) / 4) + row0;
+    h->step = i + 1;
+    rmode_advance(h);
+}
+
+// `steps` steps over a device ring through the resident engine: one descriptor per 2^31
+// steps, then `s` waits until the last m' is ready.
+void rmode_run(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
+               uint64_t label_stride, uint32_t ring, uint32_t n, uint64_t steps, uint64_t first, cudaStream_t s) {
+    uint64_t done = 0;
+    while (done < steps) {
+        const uint32_t cnt = uint32_t(std::min<uint64_t>(steps - done, 1ull << 31));
+        const bool last = done + cnt == steps;
+        rmode_post(h, batches, batch_stride, labels, label_stride, ring, uint32_t((first + done) % ring), n,
+                   h->step, cnt, s, last ? h->step + cnt : 0);
+        h->step += cnt;
+        done += cnt;
     }
-    h->last_run_persistent = true;
-    h->ver = h->ver0 + end;
-    h->cur_sel = uint32_t((h->sel_par0 + end) & 1);
-    h->cur_plan = uint32_t((h->plan_par0 + end) & 1);
-    h->dep_floor = end;
-    h->prewaited = 0;
-    h->last_copy_stream = s;
-    h->step = end;
+    for (auto& e : h->done)
+        cuda_check(cudaEventRecord(e, s), "event");
+    rmode_advance(h);
 }
 
 void check_step_args(drb_rb* h, uint32_t n) {
@@ -1062,6 +1282,10 @@ drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uin
         check_step_args(h, n);
         device_guard g(h->cfg.device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        if (h->rmode) {
+            rmode_step(h, batch, labels, n, s, out);
+            return;
+        }
         const uint64_t i = h->step;
         enqueue_sel(h, i, batch, labels, n, s, true);
         enqueue_plan(h, i);
@@ -1091,8 +1315,16 @@ drb_status drb_rb_run(drb_rb* h, const void* batches, uint64_t batch_stride, con
             return;
         const bool vec = (h->cfg.sample_bytes % 16 == 0) && aligned16(batches) && (batch_stride % 16 == 0);
         h->last_run_persistent = false;
-        if (h->use_persist && !step_events && vec && h->sm_count > 2 && steps < (1ull << 31)) {
-            enqueue_persistent_run(h, b, batch_stride, labels, label_stride, ring, n, steps, first, s);
+        if (h->rmode) {
+            if (step_events)
+                fail(DRB_ERR_USAGE, "run: per-step copy events exist only on the three-kernel path (DRB_PERSIST=0)");
+            if (vec) {
+                rmode_run(h, b, batch_stride, labels, label_stride, ring, n, steps, first, s);
+            } else {  // unaligned ring: step by step through the staging copy
+                drb_aug aug{};
+                for (uint64_t k = 0; k < steps; ++k)
+                    rmode_step(h, bat(k), lab(k), n, s, &aug);
+            }
             return;
         }
         // Skewed issue order (software pipeline over a resident input ring): sel runs two
@@ -1122,6 +1354,13 @@ struct drb_rb_graph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     bool launched = false;
+    // resident engine: nothing to capture (a run is one descriptor post and one stream wait,
+    // no launches); launch() posts the run
+    bool deferred = false;
+    const void* batches = nullptr;
+    const uint32_t* labels = nullptr;
+    uint64_t batch_stride = 0, label_stride = 0, steps = 0, first = 0;
+    uint32_t ring = 0, n = 0;
 };
 
 extern "C" {
@@ -1136,8 +1375,25 @@ drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint64_t batch_s
         device_guard g(h->cfg.device);
         auto gr = std::make_unique<drb_rb_graph>();
         gr->h = h;
+        if (h->rmode) {
+            check_step_args(h, n);
+            if (step_events)
+                fail(DRB_ERR_USAGE, "graph_prepare: per-step copy events exist only on the three-kernel path");
+            gr->deferred = true;
+            gr->batches = batches;
+            gr->labels = labels;
+            gr->batch_stride = batch_stride;
+            gr->label_stride = label_stride;
+            gr->steps = steps;
+            gr->first = first;
+            gr->ring = ring;
+            gr->n = n;
+            *out = gr.release();
+            return;
+        }
         // everything issued so far completes first, so the captured steps depend only on
         // each other (no waits on events recorded outside the capture)
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "capture prologue");
         h->dep_floor = h->step;
         cudaStream_t cs = nullptr;
@@ -1176,6 +1432,14 @@ drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream) {
             fail(DRB_ERR_USAGE, "graph_launch: a prepared run can be launched once");
         device_guard dg(g->h->cfg.device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->h->stream;
+        if (g->deferred) {
+            const drb_status st = drb_rb_run(g->h, g->batches, g->batch_stride, g->labels, g->label_stride, g->ring,
+                                             g->n, g->steps, g->first, s, nullptr);
+            if (st != DRB_OK)
+                fail(st, t_last_error);
+            g->launched = true;
+            return;
+        }
         cuda_check(cudaGraphLaunch(g->exec, s), "graph launch");
         cuda_check(cudaEventRecord(g->h->ev_user[0], s), "event");
         cuda_check(cudaEventRecord(g->h->last_work, s), "event");
@@ -1288,6 +1552,7 @@ drb_status drb_rb_synchronize(drb_rb* h) {
     return guarded([&] {
         device_guard g(h->cfg.device);
         if (h->dbg_bits & 1024) {  // diagnostics of the last persistent run
+            rmode_quiesce(h);
             cudaDeviceSynchronize();
             RunCtl rc{};
             cudaMemcpy(&rc, h->runctl, sizeof rc, cudaMemcpyDeviceToHost);
@@ -1331,6 +1596,7 @@ drb_status drb_rb_device_error(drb_rb* h, uint32_t* out) {
         device_guard g(h->cfg.device);
         SelState st{};
         PlanState pst{};
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "order");
         cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
         cuda_check(cudaMemcpy(&pst, h->plan + h->cur_plan, sizeof pst, cudaMemcpyDeviceToHost), "state");
@@ -1344,6 +1610,7 @@ drb_status drb_rb_trace_read(drb_rb* h, uint64_t* out16) {
         if (!h->trace)
             fail(DRB_ERR_USAGE, "trace_read: run with DRB_TRACE=1");
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "trace sync");
         cuda_check(cudaMemcpy(out16, h->trace, 32 * 8, cudaMemcpyDeviceToHost), "trace copy");
     });
@@ -1356,9 +1623,20 @@ drb_status drb_rb_timeline_read(drb_rb* h, uint64_t* out, uint32_t* steps) {
         if (!h->timeline || !out)
             return;
         device_guard g(h->cfg.device);
+        rmode_quiesce(h);
         cuda_check(cudaDeviceSynchronize(), "timeline sync");
         cuda_check(cudaMemcpy(out, h->timeline, h->timeline_steps * uint64_t(kTlStride) * 8, cudaMemcpyDeviceToHost), "timeline copy");
     });
+}
+
+drb_status drb_rb_engine_info(drb_rb* h, uint32_t* resident, uint64_t* instances, uint64_t* posted,
+                              uint32_t* grid) {
+    DRB_REQUIRE(h && resident && instances && posted && grid);
+    *resident = h->rmode ? 1u : 0u;
+    *instances = h->gen;
+    *posted = h->posted;
+    *grid = h->rmode ? h->run_grid : h->grid;
+    return DRB_OK;
 }
 
 drb_status drb_rb_launch_info(drb_rb* h, uint32_t* grid, uint32_t* threads, uint32_t* smem) {

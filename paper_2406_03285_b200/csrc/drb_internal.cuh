@@ -158,32 +158,75 @@ struct StepParams {
     unsigned long long* prof;      // DRB_DBG 65536: clock64 phase accumulators of the run's sel/plan CTAs [64]
 };
 
-// Persistent multi-iteration run (drb_rb_run over a device-resident input ring):
-// one cooperative launch, CTA 0 runs the sel chain, CTA 1 the plan chain, CTAs 2.. the copies,
-// handing iterations over through these device counters (run-relative k+1, zeroed per run).
+// ---- resident engine -----------------------------------------------------
+// One cooperative kernel per rank stays resident while work is posted: CTA 0 runs the sel
+// chain (+ the feeder and ready warps), CTA 1 the plan chain, CTAs 2.. the copies. Work
+// arrives as descriptors in a device ring, written by stream-ordered memory operations on
+// the caller's stream (update(): one step; run(): a range of steps over an input ring), so
+// a step costs no kernel launch. An instance leaves after an idle period once every
+// admitted step is complete (so device-wide synchronisation still returns); the next post
+// launches the next instance, which resumes from RunCtl.
+constexpr uint32_t kFeedRing = 256;  // descriptors in flight
+// A descriptor is written by the host into mapped host memory; the poster's stream then stores
+// its index + 1 into the device word feed_seq[j % kFeedRing] (one stream memory operation,
+// ordered after the producer of the batch); the feeder copies the descriptor into the device
+// mirror before admitting its steps.
+struct alignas(64) FeedDesc {
+    uint64_t batches;       // const uint8_t*: ring of input batches
+    uint64_t labels;        // const uint32_t*
+    uint64_t batch_stride;  // bytes between ring batches
+    uint64_t label_stride;  // u32 elements between ring label rows
+    uint64_t i_begin;       // engine iteration of the descriptor's first step
+    uint64_t count_n;       // steps (lo 32) | batch rows n (hi 32)
+    uint64_t ring_first;    // ring batches (lo 32) | first batch of the range (hi 32)
+    uint64_t seq;           // descriptor index + 1, written last: the descriptor is complete
+};
+constexpr uint32_t kFeedDescWords = sizeof(FeedDesc) / 8;
+
+// Device counters of the resident engine. Iteration counters are absolute (i+1 once
+// iteration i's role finished) and carry over from one instance to the next.
 struct alignas(64) RunCtl {
-    uint64_t sel_done;   // sel of run iteration k finished (W_i, state, own row v=i+1)
-    uint64_t plan_done;  // plan of k finished (X_i)
-    uint64_t b_done;     // every copy CTA's slab writes and pushes of k are complete (in order)
-    uint32_t error;      // sticky: a wait timed out -> every role leaves its loop
+    uint64_t sel_done;   // sel(i) finished (W_i, state, own row v=i+1)
+    uint64_t plan_done;  // plan(i) finished (X_i)
+    uint64_t b_done;     // A(i) and B(i) of every copy CTA complete (in order)
+    uint64_t admitted;   // iterations whose descriptors the feeder has seen
+    uint64_t ready;      // m'_i ready for the consumer (i+1): the stream waits poll this word
+    uint64_t desc_done;  // descriptors fully consumed (their ring slots may be rewritten)
+    uint64_t stop_at;    // gen << 40 | iteration: every role of instance `gen` leaves there
+    uint64_t next_step[2];  // [gen & 1]: where instance `gen` starts (written by the one before)
+    uint64_t next_desc[2];  // its first descriptor
+    uint32_t error;      // sticky: a wait timed out or a round failed -> every role leaves
     uint32_t where;      // diagnostics: the wait that failed first (site << 24 | k)
-    uint32_t pad[8];
+    uint32_t pad[4];
     uint32_t ticket[8];  // copy-CTA arrivals of iteration k in slot k % 8 (CTAs drift < 8 iterations)
 };
+constexpr uint64_t kStopMask = (1ull << 40) - 1;
+constexpr uint64_t kReadyFailed = 1ull << 62;  // ready after a failure: releases every stream wait
+
+// Host-mapped control words of the resident engine (u32 index into the mailbox; u64 words
+// take two): the host's posted-descriptor count, the leaving instance's announcement, the
+// host's request to leave as soon as idle.
+constexpr uint32_t kMbHostPosted = 2, kMbExiting = 4, kMbQuiesce = 6, kMbDescDone = 8;
 
 struct RunParams {
-    StepParams base;  // iteration i0 (host iter_params); per-iteration fields patched on device
-    const uint8_t* batches;
-    uint64_t batch_stride;
-    const uint32_t* labels;
-    uint64_t label_stride;
-    uint64_t first, i0, steps, ver0;
+    StepParams base;  // per-iteration fields patched on device (run_patch)
+    FeedDesc* feed;                      // [kFeedRing] device mirror of the admitted descriptors
+    const FeedDesc* hdesc;               // [kFeedRing] mapped host ring (written by the host)
+    const uint64_t* feed_seq;            // [kFeedRing] device: j + 1 once descriptor j is posted
+    volatile unsigned long long* desc_done_host;  // mapped mirror of RunCtl::desc_done
+    RunCtl* ctl;
+    uint64_t ver0;
     SelState* sel_base;
     PlanState* plan_base;
     uint32_t* plist_base;
     uint32_t* wlist_base;
-    RunCtl* ctl;
-    uint32_t ring, n, sel_par0, plan_par0, pw, ww, copy_ctas, first_mod;  // first_mod = first % ring
+    uint64_t gen;      // instance generation
+    uint64_t idle_ns;  // leave after this long with nothing admitted and all work done
+    const volatile unsigned long long* host_posted;  // mapped: descriptors the host has posted
+    volatile unsigned long long* exiting;            // mapped: gen << 32 | next descriptor + 1
+    const volatile uint32_t* quiesce;                // mapped: leave as soon as idle
+    uint32_t sel_par0, plan_par0, pw, ww, copy_ctas;
+    uint32_t feeder_cta;  // CTA whose warps 4 and 5 run the feeder and the ready publisher
 };
 constexpr uint32_t kRunThreads = 32 * (kMaxWorld + 2);  // plan_threads(N) + a helper warp, >= kSelThreads
 
@@ -303,7 +346,7 @@ __host__ __device__ inline RunSmem run_smem(uint32_t N, uint32_t K, uint32_t r, 
     s.arena_bytes = (left / 2) & ~127u;
     s.arena[0] = take(s.arena_bytes, 128);
     s.arena[1] = take(s.arena_bytes, 128);
-    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax + 8 + 112) * 4, plan_b = plan_smem(N, K, r).words * 4;
+    const uint32_t sel_b = (sel_smem(K, nmax).words + nmax + 8 + 136) * 4, plan_b = plan_smem(N, K, r).words * 4;
     const uint32_t ctl = sel_b > plan_b ? sel_b : plan_b;
     s.bytes = off > ctl ? off : ctl;
     if (s.bytes < kSoloSmem)
@@ -331,9 +374,12 @@ int copy_kernel_max_ctas_per_sm(uint32_t smem_bytes, int* out);
 // multi-rank: wait (one warp) until every peer's pushes into m'_i landed (pushdone >= i)
 int launch_peers_wait(const StepParams& p, void* stream);
 int copy_tma_occupancy(uint32_t smem_bytes, int* out);  // CTAs per SM of the TMA copy kernel
-// persistent run: dynamic smem, and the cooperative launch (grid = copy_ctas + 2)
+// resident engine: dynamic smem, and the cooperative launch of one instance (grid = copy_ctas + 2)
 uint32_t run_smem_bytes(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax);
 int launch_run(const RunParams& rp, uint32_t grid, void* stream);
+// fallback feed without stream memory operations: one thread stores a descriptor / waits for ready
+int launch_feed_post(uint64_t* seq_word, uint64_t value, void* stream);
+int launch_feed_wait(const uint64_t* word, uint64_t want, void* stream);
 uint32_t sel_smem_bytes(uint32_t K, uint32_t nmax);
 uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r);
 uint32_t plan_threads(uint32_t N);
@@ -343,8 +389,8 @@ int launch_rng_draw(uint64_t key, uint64_t ctr, uint64_t bound, uint64_t n, uint
                     uint64_t* ctr_out_dev, void* stream);
 int launch_swor(uint64_t key, uint64_t ctr, uint32_t n, uint32_t k, uint32_t* out_dev,
                 uint64_t* ctr_out_dev, void* stream);
-int launch_plan(uint64_t key, uint64_t ctr, uint32_t want, uint32_t n_workers, uint32_t n_classes,
-                const uint32_t* occ_dev, uint32_t* out_dev, uint32_t* count_dev,
+int launch_plan(uint64_t key, uint64_t ctr, uint32_t want, uint32_t entries, uint32_t n_workers,
+                uint32_t n_classes, const uint32_t* occ_dev, uint32_t* out_dev, uint32_t* count_dev,
                 uint64_t* ctr_out_dev, void* stream);
 int launch_read_slots(const uint8_t* slab, const uint32_t* slab_labels, const uint32_t* occ_dev,
                       uint32_t K, uint32_t cap, uint64_t S, const uint32_t* req_dev,

@@ -1372,19 +1372,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
     }
 }
 
-// ---- persistent run (drb_rb_run over a resident input ring) --------------------------------
-// One cooperative launch for `steps` iterations (all CTAs co-resident): CTA 0 loops the sel
-// chain, CTA 1 the plan chain, CTAs 2.. the copies; the hand-offs that the three-kernel
-// path expresses as launches and stream events become device counters in RunCtl. The
-// selection / sampling state stays in shared memory across iterations, the next labels are
-// fetched while the current selection runs, and nothing is launched per iteration. Every
-// decision is the same code as the three-kernel path (sel_core, plan_core, copy_parse, the
-// push-at-source copy), so the outputs are bit-identical.
-//   sel(k)   waits B(k-8) (W slot), plan(k-4) (table slot); multi-rank B(k-6) of every rank
-//            (the pushes into the m' slot that plan(k)'s requesters refill)
-//   plan(k)  waits sel(k), B(k-8) (X slot), peers' occupancy rows v=i+1
-//   A(k)     (batch -> m'_i) waits B(k-3) (bounded run-ahead)
-//   B(k)     (W_i writes, X_i pushes, by byte column) waits sel(k), plan(k) only
+// ---- resident engine (drb_rb_step / drb_rb_run) ---------------------------------
+// One cooperative instance (all CTAs co-resident) stays resident while work is posted: CTA 0
+// loops the sel chain (warps 0-3), the feeder (warp 4) and the ready publisher (warp 5); CTA 1
+// the plan chain; CTAs 2.. the copies. The hand-offs that the three-kernel path expresses as
+// launches and stream events are device counters in RunCtl (absolute: i+1 once iteration i's
+// role finished). Work arrives as descriptors (FeedDesc) written by stream-ordered memory
+// operations on the caller's stream; the feeder admits their steps in order, every role
+// follows `admitted`. The selection / sampling state stays in shared memory across
+// iterations, the next labels are fetched while the current selection runs, and nothing is
+// launched per step. Every decision is the same code as the three-kernel path (sel_core,
+// plan_core, copy_parse, the push-at-source copy), so the outputs are bit-identical.
+//   sel(i)   waits B(i-8) (W slot), plan(i-4) (table slot); multi-rank B(i-6) of every rank
+//            (the pushes into the m' slot that plan(i)'s requesters refill)
+//   plan(i)  waits sel(i), B(i-8) (X slot), peers' occupancy rows v=i+1
+//   A(i)     (batch -> m'_i) waits B(i-3) (bounded run-ahead)
+//   B(i)     (W_i writes, X_i pushes, by byte column) waits sel(i), plan(i) only
+//   ready(i) (m'_i complete: the consumer's stream wait) = A(i), B(i) on every copy CTA and,
+//            multi-rank, every peer's B(i-1) (its pushes of reps(i-1) into m'_i)
+// An instance leaves once it has been idle (everything admitted is ready, nothing posted)
+// for idle_ns, after a handshake with the host over mapped memory (the host relaunches when
+// it posts behind a leaving instance); every role stops at the same iteration, and the next
+// instance resumes there.
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
     uint64_t v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1393,8 +1402,21 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
 __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ bool run_failed(const RunParams& rp) {
+    return *reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error) != 0;
+}
+// Fail the engine (first failure wins the diagnostics) and make it visible to the host.
+__device__ void run_fail(const RunParams& rp, uint32_t err, uint32_t where) {
+    if (atomicCAS(&rp.ctl->error, 0u, err) == 0)
+        rp.ctl->where = where;
+    if (rp.base.mailbox) {
+        volatile uint32_t* mb = rp.base.mailbox;
+        mb[kMbSticky] = err;
+    }
+}
 
-// *f >= want, or false once the run failed / the wait timed out (then the run is failed).
+// *f >= want, or false once the engine failed / the wait timed out (then the engine fails).
+// Only waits on admitted iterations use this: those complete unless a peer stalls.
 __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, bool sys) {
     if ((sys ? ld_acquire_sys(f) : ld_acquire_gpu(f)) >= want)  // satisfied: no timer read
         return true;
@@ -1403,15 +1425,10 @@ __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, 
         const uint64_t v = sys ? ld_acquire_sys(f) : ld_acquire_gpu(f);
         if (v >= want)
             return true;
-        if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+        if (run_failed(rp))
             return false;
         if (globaltimer() - t0 > rp.base.timeout_ns) {
-            if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_TRANSPORT)) == 0)
-                rp.ctl->where = (9u << 24) | uint32_t(want & 0xffffff);
-            if (rp.base.mailbox) {
-                volatile uint32_t* mb = rp.base.mailbox;
-                mb[kMbSticky] = DRB_ERR_TRANSPORT;
-            }
+            run_fail(rp, DRB_ERR_TRANSPORT, (9u << 24) | uint32_t(want & 0xffffff));
             return false;
         }
         __nanosleep(20);
@@ -1419,25 +1436,84 @@ __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, 
 }
 __device__ __forceinline__ uint64_t back(uint64_t k, uint64_t d) { return k >= d ? k - d : 0; }
 
-// StepParams of run iteration k (= engine iteration i0 + k), as iter_params() on the host
-__device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t k) {
-    const uint64_t i = rp.i0 + k, v = rp.ver0 + i;
+// Iteration i is admitted (its descriptor is visible), or false: this instance stops at or
+// before i, or the engine failed. Unbounded: an idle engine waits here for the next post.
+__device__ bool wait_admit(const RunParams& rp, uint64_t& seen, uint64_t i) {
+    if (seen > i)
+        return true;
+#pragma unroll 1
+    for (uint32_t spin = 0;; ++spin) {
+        seen = ld_acquire_gpu(&rp.ctl->admitted);
+        if (seen > i)
+            return true;
+        const uint64_t st = *reinterpret_cast<volatile const uint64_t*>(&rp.ctl->stop_at);
+        if ((st >> 40) == (rp.gen & 0xffffffu) && (st & kStopMask) <= i)
+            return false;
+        if (run_failed(rp))
+            return false;
+        __nanosleep(spin < 256 ? 32 : 256);
+    }
+}
+
+// The descriptor holding iteration i (roles advance through the ring in order).
+struct FeedCursor {
+    uint64_t j, ib;
+    uint32_t cnt, n, ring, first;
+    const uint8_t* batches;
+    const uint32_t* labels;
+    uint64_t bstride, lstride;
+};
+__device__ __forceinline__ void cursor_init(FeedCursor& c, uint64_t i0, uint64_t j0) {
+    c.j = j0 - 1;  // (wraps for j0 = 0; the first seek advances to j0)
+    c.ib = i0;
+    c.cnt = 0;
+}
+__device__ void cursor_seek(FeedCursor& c, const RunParams& rp, uint64_t i) {
+    while (i >= c.ib + c.cnt) {
+        ++c.j;
+        const FeedDesc* d = rp.feed + (c.j % kFeedRing);
+        c.batches = reinterpret_cast<const uint8_t*>(__ldcg(&d->batches));
+        c.labels = reinterpret_cast<const uint32_t*>(__ldcg(&d->labels));
+        c.bstride = __ldcg(&d->batch_stride);
+        c.lstride = __ldcg(&d->label_stride);
+        c.ib = __ldcg(&d->i_begin);
+        const uint64_t cn = __ldcg(&d->count_n), rf = __ldcg(&d->ring_first);
+        c.cnt = static_cast<uint32_t>(cn);
+        c.n = static_cast<uint32_t>(cn >> 32);
+        c.ring = static_cast<uint32_t>(rf);
+        c.first = static_cast<uint32_t>(rf >> 32);
+    }
+}
+__device__ __forceinline__ uint64_t cursor_slot(const FeedCursor& c, uint64_t i) {
+    return (c.first + static_cast<uint32_t>(i - c.ib)) % c.ring;
+}
+__device__ __forceinline__ const uint8_t* cursor_batch(const FeedCursor& c, uint64_t i) {
+    return c.batches + cursor_slot(c, i) * c.bstride;
+}
+__device__ __forceinline__ const uint32_t* cursor_labels(const FeedCursor& c, uint64_t i) {
+    return c.labels + cursor_slot(c, i) * c.lstride;
+}
+
+// StepParams of engine iteration i, as iter_params() on the host (batch fields: feed_patch)
+__device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t i) {
+    const uint64_t v = rp.ver0 + i;
     p.tslot_in = static_cast<uint32_t>(v % kTableRing);
     p.tslot_out = static_cast<uint32_t>((v + 1) % kTableRing);
     p.sel_in = rp.sel_base + ((rp.sel_par0 + i) & 1);
     p.sel_out = rp.sel_base + ((rp.sel_par0 + i + 1) & 1);
     p.plan_in = rp.plan_base + ((rp.plan_par0 + i) & 1);
     p.plan_out = rp.plan_base + ((rp.plan_par0 + i + 1) & 1);
-    const uint64_t slot = (rp.first_mod + uint32_t(k)) % rp.ring;  // 32-bit: steps < 2^31
-    p.batch = rp.batches + slot * rp.batch_stride;
-    p.labels = rp.labels + slot * rp.label_stride;
-    p.n = rp.n;
     p.step = i;
     p.seq = i;
     p.aslot = static_cast<uint32_t>(i % p.aug_ring);
     p.plist_in = rp.plist_base + (i % kListRing) * rp.pw;
     p.plist_out = const_cast<uint32_t*>(p.plist_in);
     p.wlist = rp.wlist_base + (i % kListRing) * rp.ww;
+}
+__device__ __forceinline__ void feed_patch(StepParams& p, const FeedCursor& c, uint64_t i) {
+    p.batch = cursor_batch(c, i);
+    p.labels = cursor_labels(c, i);
+    p.n = c.n;
 }
 
 // per-CTA timeline stamp of engine iteration i (timeline mode), any thread
@@ -1487,149 +1563,306 @@ __device__ __forceinline__ uint64_t ld_acquire_cta(const volatile unsigned long 
 
 // A publisher warp (lane 0) for a control CTA: whenever the compute warps hand over
 // iteration k (smem `ready` = k+1, release at CTA scope), it release-stores the run counter
-// (`done` = k+1, GPU scope — this is the store that waits for the compute warps' global
+// (`done` = i0+k+1, GPU scope — this is the store that waits for the compute warps' global
 // writes to be acknowledged, so they don't) and refreshes the counters the compute warps
-// check next (`seen`, acquire).
-__device__ void run_publisher(const RunParams& rp, volatile unsigned long long* ready, uint64_t* done,
-                              volatile unsigned long long* seen, const uint64_t* s0, const uint64_t* s1) {
-    for (uint64_t k = 0; k < rp.steps; ++k) {
-        uint64_t t0 = 0;
+// check next (`seen`, acquire). It leaves when the compute warps raise `stop`.
+__device__ void run_publisher(const RunParams& rp, uint64_t i0, volatile unsigned long long* ready, uint64_t* done,
+                              volatile unsigned long long* seen, const uint64_t* s0, const uint64_t* s1,
+                              volatile const uint32_t* stop) {
+#pragma unroll 1
+    for (uint64_t k = 0;; ++k) {
+#pragma unroll 1
         for (uint32_t spin = 0; ld_acquire_cta(ready) < k + 1; ++spin) {
-            if ((spin & 63) == 63) {
-                if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
-                    return;
-                const uint64_t now = globaltimer();
-                if (t0 == 0)
-                    t0 = now;
-                else if (now - t0 > 2 * rp.base.timeout_ns)
-                    return;
+            if (*stop) {  // the role left: publish a hand-over that raced with the stop, then leave
+                __threadfence_block();
+                if (ld_acquire_cta(ready) >= k + 1)
+                    break;
+                return;
             }
+            if ((spin & 63) == 63 && run_failed(rp))
+                return;
             seen[0] = ld_acquire_gpu(s0);  // keep the compute warps' view fresh while waiting
             seen[1] = ld_acquire_gpu(s1);
+            if (spin > 4096)  // idle engine: back off
+                __nanosleep(256);
         }
-        st_release_gpu(done, k + 1);
+        st_release_gpu(done, i0 + k + 1);
         seen[0] = ld_acquire_gpu(s0);
         seen[1] = ld_acquire_gpu(s1);
     }
 }
 
-// CTA 0: the sel chain. Warp 0 runs sel(k), warps 2-3 fetch the labels of m_{k+1}, warp 1
-// publishes sel_done and keeps b_done / plan_done fresh in shared memory.
-__device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
+// The feeder (one lane): admits posted descriptors in order, and ends the instance when idle.
+__device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
+    uint64_t j = j0, admitted = i0, idle_t0 = 0;
+    bool failed = false;
+#pragma unroll 1
+    for (uint32_t spin = 0;; ++spin) {
+        if (ld_acquire_sys(rp.feed_seq + (j % kFeedRing)) == j + 1) {  // posted (stream order)
+            // the descriptor itself: four 16-byte loads from mapped host memory, in flight
+            // together, then the device mirror the roles read
+            const uint64_t* hs = reinterpret_cast<const uint64_t*>(rp.hdesc + (j % kFeedRing));
+            uint64_t w[kFeedDescWords];
+#pragma unroll
+            for (uint32_t x = 0; x < kFeedDescWords; x += 2)
+                asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];"
+                             : "=l"(w[x]), "=l"(w[x + 1])
+                             : "l"(hs + x)
+                             : "memory");
+            uint64_t* dd = reinterpret_cast<uint64_t*>(rp.feed + (j % kFeedRing));
+#pragma unroll
+            for (uint32_t x = 0; x < kFeedDescWords; ++x)
+                dd[x] = w[x];
+            admitted = w[4] + static_cast<uint32_t>(w[5]);  // i_begin + count
+            st_release_gpu(&rp.ctl->admitted, admitted);
+            ++j;
+            idle_t0 = 0;
+            spin = 0;
+            continue;
+        }
+        if (run_failed(rp)) {
+            failed = true;
+            break;
+        }
+        if (ld_acquire_gpu(&rp.ctl->ready) < admitted) {  // work in flight: not idle
+            idle_t0 = 0;
+            __nanosleep(64);
+            continue;
+        }
+        const uint64_t now = globaltimer();
+        if (idle_t0 == 0)
+            idle_t0 = now;
+        if (*rp.quiesce == 0 && now - idle_t0 < rp.idle_ns) {
+            __nanosleep(spin < 512 ? 64 : 512);
+            continue;
+        }
+        // Leave. Announce it in host memory first, then look for a post already on its way
+        // (the host raises host_posted before it enqueues the descriptor's memory
+        // operations, then reads `exiting`): of the two, at least one sees the other, so
+        // either this instance stays or the host launches the next one behind it.
+        *rp.exiting = (rp.gen << 32) | (j + 1);
+        asm volatile("fence.sc.sys;" ::: "memory");
+        if (*rp.host_posted > j) {
+            *rp.exiting = 0;  // stay (a relaunch the host may already have queued finds no work)
+            idle_t0 = 0;
+            continue;
+        }
+        break;
+    }
+    if (!failed) {
+        rp.ctl->next_step[(rp.gen + 1) & 1] = admitted;
+        rp.ctl->next_desc[(rp.gen + 1) & 1] = j;
+    }
+    st_release_gpu(&rp.ctl->stop_at, ((rp.gen & 0xffffffu) << 40) | admitted);
+}
+
+// CTA 0 warp 5: ready(i) — m'_i complete — in order, for the consumers' stream waits.
+__device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
+    const StepParams& b = rp.base;
+    const bool multi = (b.mode & kModePeers) && b.N > 1;
+    const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(b.region[b.me]);
+    uint64_t adm = 0;
+    SeenFlag bd{&rp.ctl->b_done, 0};
+    FeedCursor c;
+    cursor_init(c, i0, j0);
+#pragma unroll 1
+    for (uint64_t i = i0;; ++i) {
+        if (!wait_admit(rp, adm, i))
+            break;
+        bool ok = wait_seen(bd, i + 1, rp);
+        for (uint32_t w = 0; ok && multi && w < b.N; ++w)
+            if (w != b.me && i > 0)
+                ok = run_wait(&hdr->pushdone[w], i, rp, true);
+        if (!ok) {  // the engine failed: every admitted m' not yet ready reports it
+            if (b.mailbox) {
+                volatile uint32_t* mb = b.mailbox;
+                const uint32_t err = *reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error);
+                for (uint64_t x = i; x < adm && x < i + b.aug_ring; ++x)
+                    mb[mb_err(static_cast<uint32_t>(x % b.aug_ring), b.aug_ring)] = err ? err : DRB_ERR_INTERNAL;
+            }
+            break;
+        }
+        st_release_sys(&rp.ctl->ready, i + 1);
+        cursor_seek(c, rp, i);
+        if (i + 1 == c.ib + c.cnt) {  // the last step of its descriptor: the slot is free
+            st_release_gpu(&rp.ctl->desc_done, c.j + 1);
+            *rp.desc_done_host = c.j + 1;  // the host reuses ring slots behind this
+        }
+    }
+    if (run_failed(rp))  // release every stream still waiting for an m' of this engine
+        st_release_sys(&rp.ctl->ready, kReadyFailed);
+}
+
+// CTA 0: the sel chain. Warp 0 runs sel(i), warp 2 draws round i+1's selection ahead,
+// warp 3 fetches the labels of m_{i+1}; warp 1 publishes sel_done and keeps b_done /
+// plan_done fresh in shared memory; warps 4 and 5 are the feeder and the ready publisher.
+__device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag, uint64_t i0,
+                             uint64_t j0) {
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 4 && rp.feeder_cta == 0) {
+        if ((tid & 31) == 0)
+            run_feeder(rp, i0, j0);
+        return;
+    }
+    if (warp == 5 && rp.feeder_cta == 0) {
+        if ((tid & 31) == 0)
+            run_ready(rp, i0, j0);
+        return;
+    }
     if (tid >= kSelThreads)
         return;
     const StepParams& b = rp.base;
     const uint32_t N = b.N, me = b.me;
     const bool multi = (b.mode & kModePeers) && N > 1;
+    const uint32_t lag = aug_lag(b.aug_ring);
     SelView v = sel_view(sm, b);
     uint32_t* lab2 = sm + sel_smem(b.K, b.nmax).words;  // second label buffer (prefetch)
     uint32_t* labs[2] = {v.lab, lab2};
     volatile unsigned long long* seen =  // [0] b_done, [1] plan_done as last loaded; [2] ready
         reinterpret_cast<volatile unsigned long long*>(sm + ((sel_smem(b.K, b.nmax).words + b.nmax + 1) & ~1u));
     // Speculative S1 (warp 2 draws round k+1's selection during round k; it depends only on
-    // the candidate counter, which round k advances by min(c, n) unless a draw is rejected or
-    // the round inserts nothing): sx[0..1] the counter each parity's selection was drawn for
-    // (~0: none), sx[2] the counter at the start of the current round; spec_sel[2][32].
+    // the candidate counter, which round k advances by min(c, n_k) unless a draw is rejected
+    // or the round inserts nothing): sx[0..1] the counter each parity's selection was drawn
+    // for (~0: none), sx[2] the counter at the start of the current round; spec_sel[2][32].
     unsigned long long* sx = const_cast<unsigned long long*>(seen) + 4;
     uint32_t* spec_sel = reinterpret_cast<uint32_t*>(sx + 4);
     uint32_t* spec_tmp = spec_sel + 64;
+    // step hand-over between tid 0 and the other warps: [0] current n, [1] next n (or ~0:
+    // step k+1 not admitted yet), [2..3] next labels pointer, [4] stop, [5] bad of m_k,
+    // [6] bad of the prefetched m_{k+1}, [7] labels of step k already in labs[k & 1]
+    volatile uint32_t* hx = reinterpret_cast<volatile uint32_t*>(spec_tmp + 32);
+    FeedCursor cur, nxt;  // tid 0's
+    uint64_t adm_seen = 0;
     if (tid == 0) {
         sp = b;
-        run_patch(sp, rp, 0);
+        run_patch(sp, rp, i0);
         seen[0] = 0;
         seen[1] = 0;
         seen[2] = 0;
         sx[0] = ~0ull;
         sx[1] = ~0ull;
+        for (int x = 0; x < 8; ++x)
+            hx[x] = 0;
+        cursor_init(cur, i0, j0);
+        cursor_init(nxt, i0, j0);
     }
     named_bar(1, kSelThreads);
-    {  // state and the own occupancy row at the start of the run (written before the launch)
+    {  // state and the own occupancy row at the start of the instance
         const uint64_t* tin = reinterpret_cast<const uint64_t*>(sp.region[me] + sp.off_table) +
                               uint64_t(sp.tslot_in) * N * sp.K + uint64_t(me) * sp.K;
         if (tid < sizeof(SelState) / 8)
             reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.sel_in) + tid);
         for (uint32_t x = tid; x < sp.K; x += kSelThreads)
             v.occ[x] = occ_of(__ldcg(tin + x));
-        if (tid == 0)
-            flag[2] = 0;
-        named_bar(1, kSelThreads);
-        if (sel_load_labels(sp, v, kSelThreads))
-            atomicOr(&flag[2], 1u);
         named_bar(1, kSelThreads);
     }
     if (warp == 1) {
         if (tid == 32)
-            run_publisher(rp, seen + 2, &rp.ctl->sel_done, seen, &rp.ctl->b_done, &rp.ctl->plan_done);
+            run_publisher(rp, i0, seen + 2, &rp.ctl->sel_done, seen, &rp.ctl->b_done, &rp.ctl->plan_done, hx + 4);
         return;
     }
     const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(b.region[me]);
 #pragma unroll 1
-    for (uint64_t k = 0; k < rp.steps; ++k) {  // warps 0, 2, 3 (barrier 1, 96 threads)
+    for (uint64_t k = 0;; ++k) {  // warps 0, 2, 3 (barrier 1, 96 threads)
+        const uint64_t i = i0 + k;
         if (tid == 0) {
             trace_at(sp, 12);
-            run_mark(rp, rp.i0 + k, 0);
-            if (k > 0)
-                run_patch(sp, rp, k);
-            // W slot (k-8) / m' slot (multi, k-6) / table slot (plan(k-4)) free
-            const uint64_t wb = back(k, multi ? aug_lag(b.aug_ring) - 1 : kListRing - 1), wp = back(k, 3);
-            bool ok = true;
-            if (seen[0] < wb)
-                ok = run_wait(&rp.ctl->b_done, wb, rp, false);
-            if (ok && seen[1] < wp)
-                ok = run_wait(&rp.ctl->plan_done, wp, rp, false);
-            run_mark(rp, rp.i0 + k, 1);
-            for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-6) complete (m' slot)
-                if (w != me && sp.step >= aug_lag(b.aug_ring))
-                    ok = run_wait(&hdr->pushdone[w], sp.step - aug_lag(b.aug_ring) + 1, rp, true);
-            flag[1] = ok ? 0u : 1u;
-            flag[0] = flag[2];  // "bad" of m_k's labels
-            flag[3] = 0;
+            run_mark(rp, i, 0);
+            uint64_t as = adm_seen;
+            bool ok = wait_admit(rp, as, i);
+            if (ok && v.st->error) {  // round i-1 failed (a label >= K): it was still delivered;
+                                      // nothing after it runs (engine.cpp:67-68,74-80)
+                run_fail(rp, v.st->error, (1u << 24) | uint32_t(i & 0xffffff));
+                ok = false;
+            }
+            if (ok) {
+                run_patch(sp, rp, i);
+                cursor_seek(cur, rp, i);
+                feed_patch(sp, cur, i);
+                hx[0] = sp.n;
+                // W slot (i-8) / m' slot (multi, i-6) / table slot (plan(i-4)) free
+                const uint64_t wb = i0 + back(k, multi ? lag - 1 : kListRing - 1), wp = i0 + back(k, 3);
+                if (seen[0] < wb)
+                    ok = run_wait(&rp.ctl->b_done, wb, rp, false);
+                if (ok && seen[1] < wp)
+                    ok = run_wait(&rp.ctl->plan_done, wp, rp, false);
+                run_mark(rp, i, 1);
+                for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-6) complete (m' slot)
+                    if (w != me && i >= lag)
+                        ok = run_wait(&hdr->pushdone[w], i - lag + 1, rp, true);
+                // step i+1 already posted: its batch size and labels for the look-ahead warps
+                hx[1] = ~0u;
+                if (ok && (as > i + 1 || ((as = ld_acquire_gpu(&rp.ctl->admitted)) > i + 1))) {
+                    cursor_seek(nxt, rp, i + 1);
+                    hx[1] = nxt.n;
+                    const uint32_t* lp = cursor_labels(nxt, i + 1);
+                    hx[2] = static_cast<uint32_t>(reinterpret_cast<uint64_t>(lp));
+                    hx[3] = static_cast<uint32_t>(reinterpret_cast<uint64_t>(lp) >> 32);
+                }
+            }
+            adm_seen = as;
+            __threadfence_block();  // sel(k-1)'s hand-over is visible before the stop
+            hx[4] = ok ? 0u : 1u;
             sx[2] = v.st->cand_ctr;  // written by this thread in sel_core(k-1)
         }
         named_bar(1, 96);
-        if (flag[1])
+        if (hx[4])
             return;
         v.lab = labs[k & 1];
+        if (!hx[7]) {  // labels of m_i were not prefetched: load them now (all three warps)
+            const uint32_t n = hx[0];
+            const uint32_t t = tid < 32 ? tid : tid - 32;  // warps 0, 2, 3 -> 0..95
+            int bad = 0;
+            for (uint32_t x = t; x < n; x += 96) {
+                const uint32_t l = __ldg(sp.labels + x);
+                v.lab[x] = l;
+                bad |= l >= sp.K;
+            }
+            if (bad)
+                atomicOr(const_cast<uint32_t*>(hx + 5), 1u);
+            named_bar(1, 96);
+        }
+        const uint32_t nn = hx[1];
         if (warp == 0) {
             tl_mark(sp, 0, false);
             trace_at(sp, 0);
             if (tid == 0)
-                run_mark(rp, rp.i0 + k, 2);
-            sel_core(sp, v, flag[0] != 0, spec_sel + 32 * (k & 1), sx[k & 1]);
+                run_mark(rp, i, 2);
+            sel_core(sp, v, hx[5] != 0, spec_sel + 32 * (k & 1), sx[k & 1]);
             delay_exp(1);
-            if (DRB_INSTRUMENT && (b.dbg & 2048))  // experiment: the compute warp's own GPU-scope fence
-                __threadfence();
             __syncwarp();
             unsigned long long pt = 0;
             prof_span(sp, 19, pt);
             if (tid == 0) {
                 st_release_cta(seen + 2, k + 1);  // hand sel(k) to the publisher
-                run_mark(rp, rp.i0 + k, 3);
+                run_mark(rp, i, 3);
                 tl_mark(sp, 0, true);
             }
             prof_span(sp, 19, pt);
-        } else if (k + 1 < rp.steps && warp == 2) {  // warp 2: S1 of round k+1, ahead
-            const uint32_t kk = min(sp.c, rp.n);
+        } else if (warp == 2) {  // warp 2: S1 of round k+1, ahead
             uint64_t drawn = ~0ull;
-            if (kk > 0 && kk <= 32 && rp.n < 65536u) {
-                const uint64_t c1 = sx[2] + kk;
-                if (warp_select_fast(sp.cand_key, c1, rp.n, kk, spec_sel + 32 * ((k + 1) & 1), spec_tmp))
-                    drawn = c1;
+            const uint32_t kk = min(sp.c, hx[0]);   // round k's draws (counter advance)
+            if (nn != ~0u) {
+                const uint32_t k1 = min(sp.c, nn);  // round k+1's draws
+                if (kk > 0 && k1 > 0 && k1 <= 32 && nn < 65536u) {
+                    const uint64_t c1 = sx[2] + kk;
+                    if (warp_select_fast(sp.cand_key, c1, nn, k1, spec_sel + 32 * ((k + 1) & 1), spec_tmp))
+                        drawn = c1;
+                }
             }
             if (tid == 64)
                 sx[(k + 1) & 1] = drawn;
-        } else if (k + 1 < rp.steps) {  // warp 3: labels of m_{k+1}
-            const uint64_t slot = (rp.first_mod + uint32_t(k + 1)) % rp.ring;
-            const uint32_t* lp = rp.labels + slot * rp.label_stride;
+        } else if (nn != ~0u) {  // warp 3: labels of m_{k+1}
+            const uint32_t* lp =
+                reinterpret_cast<const uint32_t*>(uint64_t(hx[2]) | (uint64_t(hx[3]) << 32));
             int bad = 0;
-            for (uint32_t x = tid - 96; x < rp.n; x += 32) {
+            for (uint32_t x = tid - 96; x < nn; x += 32) {
                 const uint32_t l = __ldg(lp + x);
                 labs[(k + 1) & 1][x] = l;
                 bad |= l >= sp.K;
             }
-            if (bad)
-                atomicOr(&flag[3], 1u);
+            if (__any_sync(kFull, bad) && tid == 96)
+                hx[6] = 1u;
         }
         unsigned long long pt2 = 0;
         if (warp == 0)
@@ -1638,75 +1871,85 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
         if (warp == 0)
             prof_span(sp, 20, pt2);
         if (tid == 0) {
-            flag[2] = flag[3];
-            run_mark(rp, rp.i0 + k, 4);
+            hx[7] = nn != ~0u ? 1u : 0u;  // step k+1's labels are in labs[(k+1) & 1]
+            hx[5] = hx[6];
+            hx[6] = 0;
+            run_mark(rp, i, 4);
         }
     }
 }
 
 // CTA 1: the plan chain. plan_core runs on the first plan_threads(N) threads (named barrier
 // 3); a helper warp publishes plan_done and keeps sel_done / b_done fresh.
-__device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag) {
+__device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp, uint32_t* flag, uint64_t i0) {
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const PlanView v = plan_view(sm, rp.base);
     const uint32_t T = 32 * (rp.base.N + 1 < 3 ? 3 : rp.base.N + 1);  // plan_threads(N) <= kRunThreads - 32
     const uint32_t helper = kRunThreads / 32 - 1;
     volatile unsigned long long* seen = reinterpret_cast<volatile unsigned long long*>(flag + 2);  // [0] sel, [1] b, [2] ready
+    volatile uint32_t* stop = flag;  // [0]
     if (tid == 0) {
         sp = rp.base;
-        run_patch(sp, rp, 0);
+        run_patch(sp, rp, i0);
         seen[0] = 0;
         seen[1] = 0;
         seen[2] = 0;
+        flag[0] = 0;
     }
     __syncthreads();
     if (warp == helper) {
         if ((tid & 31) == 0)
-            run_publisher(rp, seen + 2, &rp.ctl->plan_done, seen, &rp.ctl->sel_done, &rp.ctl->b_done);
+            run_publisher(rp, i0, seen + 2, &rp.ctl->plan_done, seen, &rp.ctl->sel_done, &rp.ctl->b_done, stop);
         return;
     }
     if (tid >= T)
         return;
     if (tid < sizeof(PlanState) / 8)
         reinterpret_cast<uint64_t*>(v.st)[tid] = __ldcg(reinterpret_cast<const uint64_t*>(sp.plan_in) + tid);
+    uint64_t adm = 0;
 #pragma unroll 1
-    for (uint64_t k = 0; k < rp.steps; ++k) {
+    for (uint64_t k = 0;; ++k) {
+        const uint64_t i = i0 + k;
         if (tid == 0) {
             trace_at(sp, 13);
-            run_mark(rp, rp.i0 + k, 0);
-            if (k > 0)
-                run_patch(sp, rp, k);
-            bool ok = true;
-            if (seen[0] < k + 1)  // sel(k)
-                ok = run_wait(&rp.ctl->sel_done, k + 1, rp, false);
-            if (ok && seen[1] < back(k, kListRing - 1))  // X slot: B(k-8) complete
-                ok = run_wait(&rp.ctl->b_done, back(k, kListRing - 1), rp, false);
-            run_mark(rp, rp.i0 + k, 1);
+            run_mark(rp, i, 0);
+            bool ok = wait_admit(rp, adm, i);
+            if (ok) {
+                run_patch(sp, rp, i);
+                if (seen[0] < i + 1)  // sel(i)
+                    ok = run_wait(&rp.ctl->sel_done, i + 1, rp, false);
+                if (ok && seen[1] < i0 + back(k, kListRing - 1))  // X slot: B(i-8) complete
+                    ok = run_wait(&rp.ctl->b_done, i0 + back(k, kListRing - 1), rp, false);
+            }
+            run_mark(rp, i, 1);
             flag[1] = ok ? 0u : 1u;
             v.misc[0] = 0;
         }
         cta_bar(3, T);
-        if (flag[1])
+        if (flag[1]) {
+            if (tid == 0) {
+                __threadfence_block();
+                flag[0] = 1;  // the publisher leaves too
+            }
             return;
+        }
         tl_mark(sp, 1, false);
         trace_at(sp, 5);
         plan_core(sp, v, T, 3);
         delay_exp(2);
-        if (DRB_INSTRUMENT && (rp.base.dbg & 2048))
-            __threadfence();
         cta_bar(3, T);
         if (tid == 0) {
             st_release_cta(seen + 2, k + 1);  // hand plan(k) to the publisher
             tl_mark(sp, 1, true);
-            run_mark(rp, rp.i0 + k, 3);
+            run_mark(rp, i, 3);
         }
     }
 }
 
 // B(k) of a copy CTA is complete: fence, arrive. Copy CTAs are not in lockstep, so arrivals
-// are counted per iteration (slot k % 8); the last arrival of k releases b_done = k+1 once
-// b_done = k (in order) and, multi-rank, pushdone = i+1 at every peer.
-__device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t k, bool multi) {
+// are counted per iteration (slot k % 8); the last arrival of iteration i releases b_done =
+// i+1 once b_done = i (in order) and, multi-rank, pushdone = i+1 at every peer.
+__device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t k, uint64_t i, bool multi) {
     asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk stores, for generic-proxy readers
     uint32_t* t = &rp.ctl->ticket[k & 7];
     uint32_t old;
@@ -1716,7 +1959,7 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
     if (old + 1 == rp.copy_ctas) {
         *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+8
-        if (!run_wait(&rp.ctl->b_done, k, rp, false))
+        if (!run_wait(&rp.ctl->b_done, i, rp, false))
             return;
         if (multi) {
             asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -1724,25 +1967,19 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
                 if (w != p.me)
                     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(
                                      &reinterpret_cast<RegionHeader*>(p.region[w])->pushdone[p.me]),
-                                 "l"(rp.i0 + k + 1)
+                                 "l"(i + 1)
                                  : "memory");
         }
-        st_release_gpu(&rp.ctl->b_done, k + 1);
+        st_release_gpu(&rp.ctl->b_done, i + 1);
     }
 }
 
-// CTAs 2..: copies. Warp 1 lane 0 streams m_i -> m'_i (flat slice of the batch bytes), at
-// most two iterations ahead of the completed B. Warp 0 does B on a fixed COLUMN of every
-// row — bytes [c0, c1) of each slab row it writes (W_i) and each slot it pushes (X_i) — so
-// every read and write of a given slab byte happens in this one CTA, in program order:
-// there is no grid-wide hand-off between iterations. The one cross-iteration hazard (a
-// slot pushed in k that B(k-1) wrote) waits for this CTA's previous stores to complete.
-// Cross-warp progress of a copy CTA's B engines (shared memory, per iteration parity).
+// Cross-warp progress of a copy CTA's engines (shared memory, per iteration parity).
 struct BFlags {
     unsigned long long landed[2];    // k+1: B(k)'s loads landed (its reads are done)
     unsigned long long complete[2];  // k+1: B(k)'s stores complete
     unsigned long long parsed[4];    // k+1 in slot k % 4: W_k's slab rows published in wrows[k % 4]
-    unsigned long long pad;
+    unsigned long long a_done;       // k+1: A(k)'s stores (m_i -> m'_i) complete
 };
 // Bounded like every other wait: gives up once the run failed or after timeout_ns (then
 // fails the run, recording `site` and the iteration), so no role can spin forever.
@@ -1751,14 +1988,13 @@ __device__ bool smem_wait_ge(const volatile unsigned long long* f, uint64_t want
     uint64_t t0 = 0;
     for (uint32_t spin = 0; *f < want; ++spin) {
         if ((spin & 255) == 255) {
-            if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+            if (run_failed(rp))
                 return false;
             const uint64_t now = globaltimer();
             if (t0 == 0)
                 t0 = now;
             else if (now - t0 > rp.base.timeout_ns) {
-                if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
-                    rp.ctl->where = (site << 24) | uint32_t(k & 0xffffff);
+                run_fail(rp, DRB_ERR_INTERNAL, (site << 24) | uint32_t(k & 0xffffff));
                 return false;
             }
         }
@@ -1775,14 +2011,15 @@ __device__ __forceinline__ void b_complete(volatile BFlags* fl, uint64_t k) {
     st_release_cta(&fl->complete[k & 1], k + 1);
 }
 
-// One B engine (a warp) of a copy CTA, for the iterations k = first, first+2, ...: the W_k
-// writes and X_k pushes on this CTA's byte column [c0, c1). The two B warps alternate, so
-// B(k+1) issues its loads while B(k) drains; what must stay ordered between consecutive
-// iterations on the same slab bytes is ordered through BFlags:
+// One B engine (a warp) of a copy CTA, for the instance's iterations k = wsel, wsel+2, ...:
+// the W_i writes and X_i pushes on this CTA's byte column [c0, c1). The two B warps
+// alternate, so B(k+1) issues its loads while B(k) drains; what must stay ordered between
+// consecutive iterations on the same slab bytes is ordered through BFlags:
 //   a slot pushed in k that W_{k-1} wrote        -> B(k-1)'s stores complete first
 //   a W_k row that X_{k-1} read                  -> B(k-1)'s loads landed before k's stores
 //   a W_k row that W_{k-1} also wrote            -> B(k-1)'s stores complete first
-__device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, StepParams& sp, uint32_t wsel) {
+__device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, StepParams& sp, uint32_t wsel,
+                           uint64_t i0, uint64_t j0) {
     const uint32_t lane = threadIdx.x & 31;
     const StepParams& b = rp.base;
     uint8_t* base8 = reinterpret_cast<uint8_t*>(sm);
@@ -1804,13 +2041,15 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
     const uint32_t per_win = clen ? R.arena_bytes / clen : 0;
     const uint32_t pw = plist_words(b.N, b.r), ww = wlist_words(b.nmax), nslot = b.nmax + 1;
     SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0};
+    uint64_t adm = 0;
+    FeedCursor cur;
+    cursor_init(cur, i0, j0);
     uint32_t phB = 0;
     int64_t prev_k = -1;  // this warp's previous iteration (stores not yet drained)
     bool fetched = false;  // this iteration's lists already in flight (prefetched by the previous one)
     if (lane == 0)
         sp = b;
-    auto fetch_lists = [&](uint64_t kk) {  // W_kk and X_kk -> wraw / xraw (cp.async, one group)
-        const uint64_t i = rp.i0 + kk;
+    auto fetch_lists = [&](uint64_t i) {  // W_i and X_i -> wraw / xraw (cp.async, one group)
         const uint32_t* xs = rp.plist_base + (i % kListRing) * rp.pw;
         const uint32_t* ws = rp.wlist_base + (i % kListRing) * rp.ww;
         for (uint32_t x = lane; x < pw; x += 32)
@@ -1820,12 +2059,33 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll 1
-    for (uint64_t k = wsel; k < rp.steps; k += 2) {
+    for (uint64_t k = wsel;; k += 2) {
+        const uint64_t i = i0 + k;
         bool ok = true;
+        // Before waiting for a step that is not posted yet, complete the previous one: its
+        // stores would otherwise stay in flight (and b_done, ready behind them) until the
+        // next post arrives.
+        if (prev_k >= 0) {
+            bool posted = false;
+            if (lane == 0)
+                posted = adm > i || (adm = ld_acquire_gpu(&rp.ctl->admitted)) > i;
+            if (!__shfl_sync(kFull, posted ? 1 : 0, 0)) {
+                bulk_wait_all();
+                __syncwarp();
+                if (lane == 0)
+                    b_complete(fl, uint64_t(prev_k));
+                prev_k = -1;
+            }
+        }
         if (lane == 0) {
-            run_patch(sp, rp, k);
-            if (!fetched)
-                ok = wait_seen(sdone, k + 1, rp) && wait_seen(pdone, k + 1, rp);
+            ok = wait_admit(rp, adm, i);
+            if (ok) {
+                run_patch(sp, rp, i);
+                cursor_seek(cur, rp, i);
+                feed_patch(sp, cur, i);
+                if (!fetched)
+                    ok = wait_seen(sdone, i + 1, rp) && wait_seen(pdone, i + 1, rp);
+            }
         }
         if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
             break;
@@ -1835,7 +2095,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         if (lane == 0)
             cta_mark(sp, 0);
         if (!fetched)
-            fetch_lists(k);
+            fetch_lists(i);
         fetched = false;
         copy_parse(sp, xraw, wraw, jsrc, nullptr, misc, ready, true, true, false);
         const uint32_t nj = misc[0], nw = misc[1];
@@ -1945,8 +2205,8 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
                 cta_mark(sp, 3);
             if (!drained)
                 drain();
-            if (!mbar_wait(barB, take_phase(phB, 0), rp.base.timeout_ns))
-                atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
+            if (!mbar_wait(barB, take_phase(phB, 0), rp.base.timeout_ns) && lane == 0)
+                run_fail(rp, DRB_ERR_INTERNAL, (10u << 24) | uint32_t(k & 0xffffff));
             if (p1 == pieces && lane == 0)
                 fl->landed[k & 1] = k + 1;
             if (lane == 0) {
@@ -1968,12 +2228,12 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         // xraw / wraw are free (paddr holds this iteration's addresses): fetch this warp's next
         // lists now if sel / plan already published them, so the L2 round trip overlaps the
         // stores in flight instead of starting the next iteration
-        if (k + 2 < rp.steps) {
+        {
             bool pre = false;
             if (lane == 0)
-                pre = poll_seen(sdone, k + 3) && poll_seen(pdone, k + 3);
+                pre = poll_seen(sdone, i + 3) && poll_seen(pdone, i + 3);
             if (__shfl_sync(kFull, pre ? 1 : 0, 0)) {
-                fetch_lists(k + 2);
+                fetch_lists(i + 2);
                 fetched = true;
             }
         }
@@ -1981,23 +2241,32 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         if (lane == 0)
             cta_mark(sp, 4);
     }
-    if (prev_k >= 0 && !*reinterpret_cast<volatile uint32_t*>(&rp.ctl->error)) {
+    if (prev_k >= 0 && !run_failed(rp)) {
         bulk_wait_all();
         __syncwarp();
         if (lane == 0)
             b_complete(fl, uint64_t(prev_k));
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // a prefetch issued for an iteration never run
 }
 
 // CTAs 2..: copies. Warp 1 lane 0 streams m_i -> m'_i (flat slice of the batch bytes), at
 // most two iterations ahead of the completed B. Warps 0 and 2 do B (even / odd iterations)
 // on a fixed COLUMN of every row — bytes [c0, c1) of each slab row written (W_i) and each
 // slot pushed (X_i) — so every access to a given slab byte is in this one CTA: there is no
-// grid-wide hand-off between iterations.
-__device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2) {
+// grid-wide hand-off between iterations. Warp 3 arrives for the CTA once A(k) and B(k) are
+// complete.
+__device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2, uint64_t i0, uint64_t j0) {
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (warp >= 4)
+    if (warp >= 4) {  // the feeder and the ready publisher, when they live on this copy CTA
+        if (blockIdx.x == rp.feeder_cta && lane == 0) {
+            if (warp == 4)
+                run_feeder(rp, i0, j0);
+            else if (warp == 5)
+                run_ready(rp, i0, j0);
+        }
         return;
+    }
     const StepParams& b = rp.base;
     const RunSmem R = run_smem(b.N, b.K, b.r, b.nmax);
     uint8_t* base8 = reinterpret_cast<uint8_t*>(sm);
@@ -2015,34 +2284,36 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     named_bar(2, 128);
+    volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
     if (warp == 0 || warp == 2) {
-        run_b_warp(rp, sm, R, sp2[warp >> 1], warp >> 1);
+        run_b_warp(rp, sm, R, sp2[warp >> 1], warp >> 1, i0, j0);
         return;
     }
-    if (warp == 3) {  // arrival warp: B(k) complete -> ticket / b_done / pushdone, in order, off
-                      // the B engines' own chains (the GPU-scope atomic waits on the memory system)
+    if (warp == 3) {  // arrival warp: A(k), B(k) complete -> ticket / b_done / pushdone, in
+                      // order, off the engines' own chains (the GPU-scope atomic waits on the
+                      // memory system)
         // CTA part 0 also writes m'_k's counts and batch labels here (copy_counts' job on the
         // three-kernel path), in iteration order, while B(k) still runs: they need only plan(k)
         // (seen through the B engines' `parsed`), |reps(k-1)| stays in a register, and the X
         // list's |reps(k)| is read before this CTA's arrival lets plan(k+8) reuse its slot.
-        volatile BFlags* fl = reinterpret_cast<volatile BFlags*>(base8 + R.flags);
         const bool multi = (b.mode & kModePeers) && b.N > 1;
-        const uint32_t row0 = b.nmax - rp.n;
         uint32_t prev = 0;
+        uint64_t adm = 0;
+        FeedCursor cur;
+        cursor_init(cur, i0, j0);
         auto wait_cta = [&](const volatile unsigned long long* f, uint64_t want, uint64_t k) {
             if (lane != 0)
                 return true;
             uint64_t t0 = 0;
             for (uint32_t spin = 0; ld_acquire_cta(f) < want; ++spin) {
                 if ((spin & 63) == 63) {
-                    if (*reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error))
+                    if (run_failed(rp))
                         return false;
                     const uint64_t now = globaltimer();
                     if (t0 == 0)
                         t0 = now;
                     else if (now - t0 > b.timeout_ns) {
-                        if (atomicCAS(&rp.ctl->error, 0u, uint32_t(DRB_ERR_INTERNAL)) == 0)
-                            rp.ctl->where = (8u << 24) | uint32_t(k & 0xffffff);
+                        run_fail(rp, DRB_ERR_INTERNAL, (8u << 24) | uint32_t(k & 0xffffff));
                         return false;
                     }
                 }
@@ -2050,28 +2321,44 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
             return true;
         };
 #pragma unroll 1
-        for (uint64_t k = 0; k < rp.steps; ++k) {
+        for (uint64_t k = 0;; ++k) {
+            const uint64_t i = i0 + k;
+            uint64_t lp = 0;
+            uint32_t n = 0;
+            bool ok = true;
+            if (lane == 0) {
+                ok = wait_admit(rp, adm, i);
+                if (ok) {
+                    cursor_seek(cur, rp, i);
+                    lp = reinterpret_cast<uint64_t>(cursor_labels(cur, i));
+                    n = cur.n;
+                }
+            }
+            if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
+                return;
             if (part == 0) {
                 if (!__shfl_sync(kFull, wait_cta(&fl->parsed[k & 3], k + 1, k) ? 1 : 0, 0))
                     return;
-                const uint64_t i = rp.i0 + k;
+                lp = __shfl_sync(kFull, lp, 0);
+                n = __shfl_sync(kFull, n, 0);
+                const uint32_t* lab = reinterpret_cast<const uint32_t*>(lp);
+                const uint32_t row0 = b.nmax - n;
                 const uint32_t aslot = static_cast<uint32_t>(i % b.aug_ring);
-                const uint32_t* lab = rp.labels + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.label_stride;
                 uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
                                uint64_t(aslot) * b.auglab_slot_elems;
                 uint32_t nrep = 0;
                 if (lane == 0)
-                    nrep = __ldcg(rp.plist_base + (i % kListRing) * rp.pw);  // |reps(k)|
-                if (rp.n <= 64) {  // both label loads in flight at once
-                    const uint32_t l0 = lane < rp.n ? __ldg(lab + lane) : 0u;
-                    const uint32_t l1 = lane + 32 < rp.n ? __ldg(lab + lane + 32) : 0u;
-                    if (lane < rp.n)
+                    nrep = __ldcg(rp.plist_base + (i % kListRing) * rp.pw);  // |reps(i)|
+                if (n <= 64) {  // both label loads in flight at once
+                    const uint32_t l0 = lane < n ? __ldg(lab + lane) : 0u;
+                    const uint32_t l1 = lane + 32 < n ? __ldg(lab + lane + 32) : 0u;
+                    if (lane < n)
                         al[row0 + lane] = l0;
-                    if (lane + 32 < rp.n)
+                    if (lane + 32 < n)
                         al[row0 + lane + 32] = l1;
                 } else {
 #pragma unroll 4
-                    for (uint32_t x = lane; x < rp.n; x += 32)
+                    for (uint32_t x = lane; x < n; x += 32)
                         al[row0 + x] = __ldg(lab + x);
                 }
                 if (lane == 0) {
@@ -2079,11 +2366,11 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                     uint32_t* repcnt = aug_count + b.aug_ring;
                     if (k == 0)
                         prev = i > 0 ? __ldcg(&repcnt[aslot]) : 0u;
-                    aug_count[aslot] = rp.n + prev;
+                    aug_count[aslot] = n + prev;
                     repcnt[(aslot + 1) % b.aug_ring] = nrep;
                     if (b.mailbox) {
                         volatile uint32_t* mb = b.mailbox;
-                        mb[mb_count(aslot)] = rp.n + prev;
+                        mb[mb_count(aslot)] = n + prev;
                         mb[mb_err(aslot, b.aug_ring)] = 0;
                     }
                     prev = nrep;
@@ -2092,32 +2379,36 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
             }
             if (!__shfl_sync(kFull, wait_cta(&fl->complete[k & 1], k + 1, k) ? 1 : 0, 0))
                 return;
+            if (!__shfl_sync(kFull, wait_cta(&fl->a_done, k + 1, k) ? 1 : 0, 0))
+                return;
             delay_exp(4);
             if (lane == 0)
-                run_b_arrive(rp, b, k, multi);
+                run_b_arrive(rp, b, k, i, multi);
         }
-        return;
     }
     // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
     if (lane != 0)
         return;
-    const uint64_t a16 = (uint64_t(rp.n) * S) >> 4;
-    const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
-    const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
-    const uint32_t row0 = b.nmax - rp.n;
     uint32_t ph_bits = 0;  // phase of each A barrier
     SeenFlag bdone{&rp.ctl->b_done, 0};
+    uint64_t adm = 0;
+    FeedCursor cur;
+    cursor_init(cur, i0, j0);
 #pragma unroll 1
-    for (uint64_t k = 0; k < rp.steps; ++k) {
-        if (!wait_seen(bdone, back(k, 2), rp))
+    for (uint64_t k = 0;; ++k) {
+        const uint64_t i = i0 + k;
+        if (!wait_admit(rp, adm, i))
             break;
-        const uint64_t i = rp.i0 + k;
+        if (!wait_seen(bdone, i0 + back(k, 2), rp))
+            break;
         run_mark(rp, i, 2);
-        // m'_i's rows were last written by A(k-6): those stores are complete (every bulk
-        // group but the newest — A(k-1)'s last window — has finished)
-        asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
-        const uint8_t* batch = rp.batches + uint64_t((rp.first_mod + uint32_t(k)) % rp.ring) * rp.batch_stride;
-        uint8_t* dst = b.region[b.me] + b.off_aug + (i % b.aug_ring) * b.aug_slot_bytes + uint64_t(row0) * S;
+        cursor_seek(cur, rp, i);
+        const uint32_t n = cur.n;
+        const uint8_t* batch = cursor_batch(cur, i);
+        const uint64_t a16 = (uint64_t(n) * S) >> 4;
+        const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
+        const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
+        uint8_t* dst = b.region[b.me] + b.off_aug + (i % b.aug_ring) * b.aug_slot_bytes + uint64_t(b.nmax - n) * S;
         for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
             const uint32_t w1 = min(nA, w0 + kTmaStagesA);
             bulk_wait_read_all();  // the ring's previous window has been stored
@@ -2131,11 +2422,14 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                 const uint64_t off = alo + uint64_t(x) * CH;
                 const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
                 if (!mbar_wait(bars + (x - w0), take_phase(ph_bits, x - w0), rp.base.timeout_ns))
-                    atomicExch(&rp.ctl->error, DRB_ERR_INTERNAL);
+                    run_fail(rp, DRB_ERR_INTERNAL, (11u << 24) | uint32_t(k & 0xffffff));
                 bulk_store(dst + off, ringA + (x - w0) * CH, len);
             }
             bulk_commit();
         }
+        bulk_wait_all();  // A(k)'s m'_i rows are written: hand them to the arrival warp
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        st_release_cta(&fl->a_done, k + 1);
         run_mark(rp, i, 5);
     }
     bulk_wait_all();
@@ -2145,12 +2439,23 @@ __global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_co
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ StepParams sp[2];
     __shared__ __align__(8) uint32_t flag[8];  // [0..1] role flags, [2..7] the plan role's counters
+    // where this instance starts (written by the previous one when it left, or by start())
+    const uint64_t i0 = __ldcg(&rp.ctl->next_step[rp.gen & 1]);
+    const uint64_t j0 = __ldcg(&rp.ctl->next_desc[rp.gen & 1]);
     if (blockIdx.x == 0)
-        run_sel_role(rp, sm, sp[0], flag);
+        run_sel_role(rp, sm, sp[0], flag, i0, j0);
     else if (blockIdx.x == 1)
-        run_plan_role(rp, sm, sp[0], flag);
+        run_plan_role(rp, sm, sp[0], flag, i0);
     else
-        run_copy_role(rp, sm, sp);
+        run_copy_role(rp, sm, sp, i0, j0);
+}
+
+// Fallback feed (no stream memory operations): one thread stores a descriptor's sequence word;
+// one thread waits for `ready`.
+__global__ void feed_post_kernel(uint64_t* seq_word, uint64_t value) { st_release_sys(seq_word, value); }
+__global__ void feed_wait_kernel(const uint64_t* word, uint64_t want) {
+    while (ld_acquire_sys(word) < want)
+        __nanosleep(100);
 }
 
 // ---- global-sampling bias test (proj/src/runner/bias.cpp:104-133) -----------------------
@@ -2382,6 +2687,16 @@ int launch_run(const RunParams& rp, uint32_t grid, void* stream) {
     return cudaLaunchKernelEx(&cfg, drb_run_kernel, rp) == cudaSuccess ? 0 : -1;
 }
 
+int launch_feed_post(uint64_t* seq_word, uint64_t value, void* stream) {
+    feed_post_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(seq_word, value);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_feed_wait(const uint64_t* word, uint64_t want, void* stream) {
+    feed_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(word, want);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int launch_peers_wait(const StepParams& p, void* stream) {
     peers_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(p);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -2436,11 +2751,13 @@ int launch_swor(uint64_t key, uint64_t ctr, uint32_t n, uint32_t k, uint32_t* ou
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_plan(uint64_t key, uint64_t ctr, uint32_t want, uint32_t n_workers, uint32_t n_classes,
-                const uint32_t* occ_dev, uint32_t* out_dev, uint32_t* count_dev,
+int launch_plan(uint64_t key, uint64_t ctr, uint32_t want, uint32_t entries, uint32_t n_workers,
+                uint32_t n_classes, const uint32_t* occ_dev, uint32_t* out_dev, uint32_t* count_dev,
                 uint64_t* ctr_out_dev, void* stream) {
-    const uint32_t NK = n_workers * n_classes;
-    const size_t smem = (2 * size_t(NK) + 1 + size_t(want + 1) * 4) * 4;
+    // entries = min(want, total) (host-computed): the kernel never holds more draws than that
+    const size_t NK = size_t(n_workers) * n_classes;
+    const size_t m = entries ? entries : 1;
+    const size_t smem = (2 * NK + 1 + 4 * m) * 4;
     if (smem > 200 * 1024)
         return -1;
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -13,8 +13,10 @@ event of m'_i. Everything is timed on the device:
   background_ms      engine alone, device time per update
   train_ms           the training step alone on a resident batch
   iteration_ms       the overlapped loop, per iteration (train stream events)
-  wait_ms            iteration_ms - train_ms: what the trainer lost to the engine
-                     (waiting for m'_i, and SM / HBM contention)
+  wait_ms            the train stream blocked on m'_i (the reference's wait_ms: time
+                     update() blocks, engine.cpp:82-90)
+  slowdown_ms        iteration_ms - train_ms: what the trainer lost overall (waiting for
+                     m'_i, and SM / HBM contention with the engine)
 """
 from __future__ import annotations
 
@@ -28,13 +30,18 @@ import torch.nn as nn
 class overlap_result:  # overlap_stats (proj/include/drb.h:70-77)
     train_cost_ms: float
     background_ms: float
-    mean_wait_ms: float
+    mean_wait_ms: float        # the train stream blocked on m'_i (engine.cpp:82-90 wait_ms)
     mean_iteration_ms: float
     iterations: int
+    mean_slowdown_ms: float = 0.0  # iteration - training alone: blocking + SM / HBM contention
 
     @property
     def wait_fraction(self) -> float:
         return self.mean_wait_ms / self.mean_iteration_ms if self.mean_iteration_ms > 0 else 0.0
+
+    @property
+    def slowdown_fraction(self) -> float:
+        return self.mean_slowdown_ms / self.mean_iteration_ms if self.mean_iteration_ms > 0 else 0.0
 
 
 class conv_classifier(nn.Module):
@@ -122,10 +129,14 @@ def run_overlap_bench(eng, data_ring: torch.Tensor, label_ring: torch.Tensor, tr
 
     pending = enqueue(0)
     torch.cuda.synchronize(dev)
+    w0 = [ev() for _ in range(iterations)]
+    w1 = [ev() for _ in range(iterations)]
     e0.record(s_train)
     for i in range(iterations):
         cur = pending
+        w0[i].record(s_train)  # step i-1 done; from here the train stream waits for m'_i
         s_train.wait_event(ready[i % 3])
+        w1[i].record(s_train)
         # m'_i stays valid until update(m_{i+2}) is enqueued; the next update is i+1, and
         # the one after waits on the train stream (s_eng waits for step i's reads below)
         pending = enqueue(i + 1)
@@ -136,4 +147,6 @@ def run_overlap_bench(eng, data_ring: torch.Tensor, label_ring: torch.Tensor, tr
     e1.record(s_train)
     torch.cuda.synchronize(dev)
     iteration_ms = e0.elapsed_time(e1) / iterations
-    return overlap_result(train_ms, background_ms, max(0.0, iteration_ms - train_ms), iteration_ms, iterations)
+    wait_ms = sum(w0[i].elapsed_time(w1[i]) for i in range(iterations)) / iterations
+    return overlap_result(train_ms, background_ms, wait_ms, iteration_ms, iterations,
+                          max(0.0, iteration_ms - train_ms))

@@ -194,10 +194,11 @@ class rehearsal_buffer:
 
     def __init__(self, n_classes: int, per_class_cap: int, sample_bytes: int, *, max_batch: int = 64,
                  candidate_count: int = 14, rep_count: int = 7, seed: int = 1, rank: int = 0,
-                 world: int = 1, device: int = 0, aug_ring: int = 0):
+                 world: int = 1, device: int = 0, aug_ring: int = 0, engine_ctas: int = 0):
         cfg = _lib.drb_rb_config(n_classes=n_classes, per_class_cap=per_class_cap, sample_bytes=sample_bytes,
                                  max_batch=max_batch, candidate_count=candidate_count, rep_count=rep_count,
-                                 rank=rank, world=world, seed=seed, device=device, flags=0, aug_ring=aug_ring)
+                                 rank=rank, world=world, seed=seed, device=device, flags=0, aug_ring=aug_ring,
+                                 engine_ctas=engine_ctas)
         self.h = C.c_void_p()
         check(lib.drb_rb_create(C.byref(cfg), C.byref(self.h)))
         self.K, self.cap, self.S = n_classes, per_class_cap, sample_bytes
@@ -449,6 +450,15 @@ class engine:
         aug = _lib.drb_aug()
         check(lib.drb_rb_aug_slot(self.buffer.h, step, n, C.byref(aug)))
         return augmented_batch(self, aug)
+
+    def engine_info(self) -> dict:
+        """resident: the engine runs as a resident kernel; instances: launched so far (one per
+        busy period, not per step); posted: work descriptors posted; grid: CTAs per instance."""
+        r, g = C.c_uint32(), C.c_uint32()
+        inst, posted = C.c_uint64(), C.c_uint64()
+        check(lib.drb_rb_engine_info(self.buffer.h, C.byref(r), C.byref(inst), C.byref(posted), C.byref(g)))
+        return {"resident": bool(r.value), "instances": int(inst.value), "posted": int(posted.value),
+                "grid": int(g.value)}
 
     def synchronize(self) -> None:
         check(lib.drb_rb_synchronize(self.buffer.h))

@@ -157,3 +157,40 @@ def test_update_buffer_matches_oracle(drb, K, cap, S, nmax):
         o = orc.occ[k]
         assert np.array_equal(slab[k, :o], orc.slab[k, :o]), k
         assert np.array_equal(slab_labels.cpu().numpy()[k, :o], orc.slab_labels[k, :o])
+
+
+def _read_slots_golden():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "read_slots.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_read_slots_golden()))
+def test_read_slots_substitute_stream_matches_reference(drb, name):
+    """The substitute choices themselves (rehearsal_buffer.cpp:96-121): after the same update
+    rounds, the device read_slots with the serve / slot substitute stream returns, per request,
+    the status, label and bytes the reference's buffer returned, and leaves the stream where
+    the reference left it (tests/golden/read_slots.json, generated from oracle/_ref)."""
+    import hashlib
+
+    from paper_2406_03285_b200.workload import stream_spec
+    g = _read_slots_golden()[name]
+    c = g["config"]
+    buf = drb.rehearsal_buffer(c["K"], c["cap"], c["S"], max_batch=c["n"])
+    spec = stream_spec(c["K"], c["T"], c["n"], c["S"], steps_per_task=10**9, seed=c["seed"])
+    cand = drb.rng_stream(c["seed"], 0, CANDIDATE)
+    evict = drb.rng_stream(c["seed"], 0, EVICTION)
+    for i in range(c["rounds"]):
+        buf.update_buffer(dev_batch(spec.payload(0, i, c["n"]), spec.labels(0, i, c["n"])), c["c"], cand, evict)
+    assert buf.snapshot().per_class == g["occ"]
+    if c["keyed"]:
+        sub = drb.rng_stream.keyed(c["seed"], 0, c["purpose"], c["k1"], c["k2"])
+    else:
+        sub = drb.rng_stream(c["seed"], 0, c["purpose"])
+    got = buf.read_slots([tuple(x) for x in g["requests"]], sub)
+    assert [e.status for e in got] == g["status"]
+    assert [e.label for e in got] == g["labels"]
+    data = np.stack([e.value.cpu().numpy() for e in got])
+    assert hashlib.sha256(np.ascontiguousarray(data).tobytes()).hexdigest() == g["bytes_sha256"]
+    assert hex(int(sub.next_u64()[0])) == g["sub_next_u64"]

@@ -98,3 +98,21 @@ def test_plan_exhaustion_and_empty(drb):
     assert s.counter == 0
     assert len(drb.plan(0, np.array([[4, 6]]), s).entries) == 0
     assert len(drb.plan(7, np.array([[0], [0]]), s).entries) == 0
+
+
+def test_plan_want_beyond_total_and_huge(drb, orc):
+    """want far above the view's total (up to UINT32_MAX) returns every slot in flat order
+    with no draws (sampler.cpp:45-51); the device scratch is sized by min(want, total), not
+    by want. A large want below a larger total draws normally."""
+    occ = np.array([[3, 0, 2], [1, 4, 0]], np.uint32)
+    flat = [[w, k, s] for w in range(2) for k in range(3) for s in range(int(occ[w, k]))]
+    for want in (11, 12, 13000, 2**31, 2**32 - 1):
+        s = drb.rng_stream(9, 1, GLOBAL_SAMPLING)
+        p = drb.plan(want, occ, s)
+        assert p.entries.tolist() == flat, want
+        assert s.counter == 0
+    big = np.full((4, 250), 20, np.uint32)  # total 20000 > want 9000
+    s = drb.rng_stream(3, 2, GLOBAL_SAMPLING)
+    got = drb.plan(9000, big, s)
+    assert got.entries.tolist() == orc.plan(9000, big, 3, 2, GLOBAL_SAMPLING).tolist()
+    assert not got.has_duplicates()

@@ -137,3 +137,34 @@ def test_port_bias_counts_match_reference_golden():
         assert occ.tolist() == g["occ"], name
         c = bias_counts(be, occ, g["r"], g["seed"], g["draws"], g["local_only"])
         assert hashlib.sha256(c.astype("<u8").tobytes()).hexdigest() == g["counts_sha256"], name
+
+
+def _read_slots_golden():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "read_slots.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_read_slots_golden()))
+def test_port_read_slots_matches_reference_golden(name):
+    """read_slots (rehearsal_buffer.cpp:88-142) of the C restatement after the same update
+    rounds: statuses, labels, bytes and the substitute stream's position, as the reference's
+    own buffer produced them (tests/golden/read_slots.json, oracle/gen_golden.py)."""
+    import hashlib
+
+    from oracle.py_oracle import OracleBuffer
+    g = _read_slots_golden()[name]
+    c = g["config"]
+    ob = OracleBuffer(c["K"], c["cap"], c["S"])
+    spec = stream_spec(c["K"], c["T"], c["n"], c["S"], steps_per_task=10**9, seed=c["seed"])
+    cand = ob.stream(c["seed"], 0, CANDIDATE)
+    evict = ob.stream(c["seed"], 0, EVICTION)
+    for i in range(c["rounds"]):
+        rc, _, _ = ob.update_buffer(spec.payload(0, i, c["n"]), spec.labels(0, i, c["n"]), c["c"], cand, evict)
+        assert rc == 0
+    assert ob.occ.tolist() == g["occ"]
+    sub = ob.stream(c["seed"], 0, c["purpose"], bool(c["keyed"]), c["k1"], c["k2"])
+    d, lab, st = ob.read_slots([tuple(x) for x in g["requests"]], sub)
+    assert st.tolist() == g["status"]
+    assert lab.tolist() == g["labels"]
+    assert hashlib.sha256(np.ascontiguousarray(d).tobytes()).hexdigest() == g["bytes_sha256"]
+    assert hex(ob.next_u64(sub)) == g["sub_next_u64"]
