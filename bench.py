@@ -367,14 +367,23 @@ def main():
     # The drop-in API a trainer calls (trainer.cpp:109-113): update(m_i) on one stream, one call
     # per step, serial (the next post follows the previous m' on the stream, as in a training
     # loop with zero train cost), inputs resident in HBM, device-timed like the run above.
-    def time_updates(nsteps):
+    # Also split: the loader's stream posts m_i, the trainer's stream (here: with no training)
+    # releases the m' it used and waits for m'_i (drb_rb_step_split), so posts pipeline.
+    producer = torch.cuda.Stream(device=local)
+
+    def time_updates(nsteps, split=False):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize()
         inst0 = eng.engine_info()["instances"]
         e0.record(stream)
+        if split:
+            producer.wait_stream(stream)  # the timed region starts at e0 for the producer too
         for k in range(nsteps):
-            eng.update((data[k % ring], lab[k % ring]), stream=stream)
+            if split:
+                eng.update((data[k % ring], lab[k % ring]), stream=producer, consumer=stream)
+            else:
+                eng.update((data[k % ring], lab[k % ring]), stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         tk = e0.elapsed_time(e1)
@@ -383,9 +392,22 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tk = float(tt.item())
         return 1000.0 * tk / nsteps, eng.engine_info()["instances"] - inst0
-    upd_us, upd_launch = time_updates(args.steps)
-    upd_us_200, _ = time_updates(200)
-    step += args.steps + 200
+    # the same through the C++ facade (tools/update_bench: the reference's trainer is C++; no
+    # Python in the per-step path), N=1 only
+    cpp_update = None
+    exe = os.path.join(ROOT, "tools", "update_bench")
+    if N == 1 and os.path.exists(exe):
+        try:
+            res = subprocess.run([exe, "200", str(local)], capture_output=True, text=True, timeout=300)
+            cpp_update = json.loads(res.stdout.strip().splitlines()[-1]) if res.returncode == 0 else \
+                {"error": res.stderr[-300:]}
+        except Exception as e:  # noqa: BLE001
+            cpp_update = {"error": f"{type(e).__name__}: {e}"}
+    upd_serial_us, upd_launch = time_updates(args.steps)
+    upd_serial_us_200, _ = time_updates(200)
+    upd_us, upd_split_launch = time_updates(args.steps, split=True)
+    upd_us_200, _ = time_updates(200, split=True)
+    step += 2 * (args.steps + 200)
     kernel_ms = None
     if not resident:  # three-kernel path: per-launch copy-kernel times from events in the graph
         nper = 256
@@ -493,12 +515,19 @@ def main():
             "gpu_launches": launches,
             "engine": eng.engine_info(),
             "launch_mode": launch_mode,
-            "update_us_per_step": upd_us,
-            "update": {"us_per_step": upd_us, "steps": args.steps, "us_per_step_200": upd_us_200,
-                       "instances_launched": upd_launch,
-                       "api": "engine.update(m_i) per step on one stream (drb_rb_step: descriptor post + "
-                              "stream wait for m'_i, no kernel launch per step), inputs resident in HBM, "
-                              "device-timed; serial: each post follows the previous m' on the stream"},
+            "update_us_per_step": (cpp_update["split_us_per_step"] if cpp_update and "split_us_per_step" in cpp_update
+                                   else upd_us),
+            "update": {"cpp_facade": cpp_update,
+                       "us_per_step": upd_us, "steps": args.steps, "us_per_step_200": upd_us_200,
+                       "instances_launched": upd_split_launch,
+                       "api": "engine.update(m_i, stream=loader, consumer=trainer) per step (drb_rb_step_split: "
+                              "the descriptor is posted on the loader's stream, the trainer's stream releases "
+                              "the m' it used and waits for m'_i; no kernel launch per step), inputs resident "
+                              "in HBM, device-timed on the trainer's stream",
+                       "serial": {"us_per_step": upd_serial_us, "us_per_step_200": upd_serial_us_200,
+                                  "instances_launched": upd_launch,
+                                  "api": "engine.update(m_i) on one stream (drb_rb_step): each post follows "
+                                         "the wait for the previous m' — the latency of one round"}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
                     "d2h_bytes_per_step": d2h_b, "steps": e2e_steps,
                     "api": "drb_rb_step_host, m' assembled in place in the caller's pinned batch buffer",

@@ -221,6 +221,14 @@ DRB_RB_API drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* 
  * In place (out == batch and out_labels == labels, capacity n + r rows): m_i's rows are
  * already where m'_i keeps them, so only reps(i-1) (rows [n, n+|reps|)) and their labels
  * come back — `augment(m, reps)` (sampler.cpp:234-240) without the host-side copy of m. */
+/* drb_rb_step with the producer / consumer split of the reference's asynchronous engine
+ * (engine.cpp:62-106: the loader hands m_i over, the trainer consumes m'_i): m_i is posted in
+ * `producer`'s order (after the work that produced it), and `consumer` first releases every
+ * m' it was handed before this call (everything already enqueued on it has used them), then
+ * waits for m'_i. Steps posted back to back on the producer run pipelined in the engine;
+ * the engine refills an m' ring slot only after its consumer released it. */
+DRB_RB_API drb_status drb_rb_step_split(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n,
+                                        void* producer, void* consumer, drb_aug* out);
 DRB_RB_API drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels,
                                        uint32_t n, void* out, uint32_t* out_labels,
                                        uint32_t* out_count);

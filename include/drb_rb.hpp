@@ -269,6 +269,13 @@ public:
         check(drb_rb_step(b_.raw(), m.data, m.labels, m.n, stream, &a));
         return augmented_batch(b_.raw(), a);
     }
+    // the loader / trainer split: m posted in `producer` order, `consumer` releases the m'
+    // it used and waits for m'_i (drb_rb_step_split)
+    augmented_batch update(const device_batch& m, void* producer, void* consumer) {
+        drb_aug a{};
+        check(drb_rb_step_split(b_.raw(), m.data, m.labels, m.n, producer, consumer, &a));
+        return augmented_batch(b_.raw(), a);
+    }
     void shutdown() {
         check(drb_rb_shutdown(b_.raw()));
         shut_ = true;

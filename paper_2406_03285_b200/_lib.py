@@ -137,6 +137,7 @@ def _load():
         "drb_rb_start": (st, [vp]),
         "drb_rb_shutdown": (st, [vp]),
         "drb_rb_step": (st, [vp, vp, vp, u32, vp, P(drb_aug)]),
+        "drb_rb_step_split": (st, [vp, vp, vp, u32, vp, vp, P(drb_aug)]),
         "drb_rb_step_host": (st, [vp, vp, vp, u32, vp, vp, vp]),
         "drb_rb_run": (st, [vp, vp, u64, vp, u64, u32, u32, u64, u64, vp, vp]),
         "drb_rb_graph_prepare": (st, [vp, vp, u64, vp, u64, u32, u32, u64, u64, vp, P(vp)]),

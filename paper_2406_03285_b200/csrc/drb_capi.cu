@@ -164,8 +164,11 @@ struct drb_rb {
     uint32_t* mailbox_dev = nullptr;
     static constexpr int kEv = 16;  // >= kListRing + 1: per-iteration events in flight
     cudaEvent_t ev_user[kEv] = {}, ev_sel[kEv] = {}, ev_plan[kEv] = {}, ev_copy[kEv] = {};
+    cudaEvent_t rel[kEv] = {};  // split steps: the consumer's release at each call
     uint32_t aug_ring = kAugRingDefault;  // R: m' ring depth
     std::vector<cudaEvent_t> done;    // [R] completion of the copy that last wrote each m' slot
+    std::vector<uint8_t> slot_run;    // [R] 1: the slot was last filled by a run (see run_done)
+    cudaEvent_t run_done = nullptr;   // resident run(): one event after the run's last m'
     cudaEvent_t in_free[2] = {};      // host path: staging slot reusable
     cudaEvent_t h2d_done[2] = {};
     uint8_t* stage = nullptr;         // host path: device staging [2][max_batch][S]
@@ -340,13 +343,26 @@ void rmode_launch(drb_rb* h) {
     h->alive = true;
 }
 
+// `s` waits (in stream order) until m'_{end-1} is ready, i.e. every iteration < end is done.
+void rmode_wait(drb_rb* h, uint64_t end, cudaStream_t s) {
+    if (h->feed_kernels) {
+        if (launch_feed_wait(&h->runctl->ready, end, s))
+            fail(DRB_ERR_INTERNAL, std::string("feed wait failed: ") + cudaGetErrorString(cudaGetLastError()));
+        return;
+    }
+    const CUresult r = memops().wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(&h->runctl->ready),
+                                       end, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS)
+        fail(DRB_ERR_INTERNAL, "feed wait: cuStreamWaitValue64 failed (" + std::to_string(int(r)) + ")");
+}
+
 // Post one descriptor (steps [i_begin, i_begin + count) over an input ring) in stream order
 // on `s`, launching an instance first if none is resident (or the resident one is leaving).
 // The descriptor goes into mapped host memory; `s` then stores its sequence word (and, with
 // wait_end, waits until m'_{wait_end-1} is ready): one stream memory-operation batch.
 void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
                 uint64_t label_stride, uint32_t ring, uint32_t first, uint32_t n, uint64_t i_begin, uint32_t count,
-                cudaStream_t s, uint64_t wait_end = 0) {
+                cudaStream_t s, uint64_t wait_end = 0, bool split = false) {
     const uint64_t j = h->posted;
     if (j >= kFeedRing) {  // ring slot j % kFeedRing: descriptor j - kFeedRing must be consumed
         const uint64_t need = j - kFeedRing + 1;
@@ -365,19 +381,37 @@ void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const 
     d.batch_stride = batch_stride;
     d.label_stride = label_stride;
     d.i_begin = i_begin;
-    d.count_n = uint64_t(count) | (uint64_t(n) << 32);
+    d.count_n = uint64_t(count) | (uint64_t(n) << 32) | (split ? kDescSplit : 0ull);
     d.ring_first = uint64_t(ring) | (uint64_t(first) << 32);
     d.seq = j + 1;
     *reinterpret_cast<volatile uint32_t*>(h->mailbox + kMbQuiesce) = 0;
     *mb64(h, kMbHostPosted) = j + 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);  // (Dekker with the leaving feeder)
     const uint64_t ex = *mb64(h, kMbExiting);
-    if (!h->alive || (ex >> 32) == (h->gen & 0xffffffffull))
-        rmode_launch(h);
+    const bool launch = !h->alive || (ex >> 32) == (h->gen & 0xffffffffull);
     uint64_t* seq = h->feed_seq + (j % kFeedRing);
-    if (h->feed_kernels) {
-        if (launch_feed_post(seq, j + 1, s) || (wait_end && launch_feed_wait(&h->runctl->ready, wait_end, s)))
-            fail(DRB_ERR_INTERNAL, std::string("feed post failed: ") + cudaGetErrorString(cudaGetLastError()));
+    if (h->feed_kernels || launch) {
+        // with a launch: the sequence word first, then the instance, then the wait — an
+        // instance launched behind work that waits for it would never start under a tool that
+        // serialises the device (ncu, compute-sanitizer)
+        if (h->feed_kernels) {
+            if (launch_feed_post(seq, j + 1, s))
+                fail(DRB_ERR_INTERNAL, std::string("feed post failed: ") + cudaGetErrorString(cudaGetLastError()));
+        } else {
+            CUstreamBatchMemOpParams op;
+            std::memset(&op, 0, sizeof op);
+            op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+            op.writeValue.address = reinterpret_cast<CUdeviceptr>(seq);
+            op.writeValue.value64 = j + 1;
+            op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+            const CUresult r = memops().batch(reinterpret_cast<CUstream>(s), 1, &op, 0);
+            if (r != CUDA_SUCCESS)
+                fail(DRB_ERR_INTERNAL, "feed post: cuStreamBatchMemOp failed (" + std::to_string(int(r)) + ")");
+        }
+        if (launch)
+            rmode_launch(h);
+        if (wait_end)
+            rmode_wait(h, wait_end, s);
     } else {
         CUstreamBatchMemOpParams ops[2];
         std::memset(ops, 0, sizeof ops);
@@ -398,19 +432,6 @@ void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const 
             fail(DRB_ERR_INTERNAL, "feed post: cuStreamBatchMemOp failed (" + std::to_string(int(r)) + ")");
     }
     h->posted = j + 1;
-}
-
-// `s` waits (in stream order) until m'_{end-1} is ready, i.e. every iteration < end is done.
-void rmode_wait(drb_rb* h, uint64_t end, cudaStream_t s) {
-    if (h->feed_kernels) {
-        if (launch_feed_wait(&h->runctl->ready, end, s))
-            fail(DRB_ERR_INTERNAL, std::string("feed wait failed: ") + cudaGetErrorString(cudaGetLastError()));
-        return;
-    }
-    const CUresult r = memops().wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(&h->runctl->ready),
-                                       end, CU_STREAM_WAIT_VALUE_GEQ);
-    if (r != CUDA_SUCCESS)
-        fail(DRB_ERR_INTERNAL, "feed wait: cuStreamWaitValue64 failed (" + std::to_string(int(r)) + ")");
 }
 
 // Ask a resident instance to leave as soon as it is idle (before a device-wide sync).
@@ -657,10 +678,12 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         std::memset(h->mailbox, 0, mb_words(h->aug_ring) * 4);
         cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->mailbox_dev), h->mailbox, 0), "mailbox map");
         h->done.assign(h->aug_ring, nullptr);
+        h->slot_run.assign(h->aug_ring, 0);
+        cuda_check(cudaEventCreateWithFlags(&h->run_done, cudaEventDisableTiming), "event");
         for (auto& e : h->done)
             cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         for (int i = 0; i < drb_rb::kEv; ++i)
-            for (cudaEvent_t* e : {&h->ev_user[i], &h->ev_sel[i], &h->ev_plan[i], &h->ev_copy[i]})
+            for (cudaEvent_t* e : {&h->ev_user[i], &h->ev_sel[i], &h->ev_plan[i], &h->ev_copy[i], &h->rel[i]})
                 cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
         for (int i = 0; i < 2; ++i) {
             cuda_check(cudaEventCreateWithFlags(&h->in_free[i], cudaEventDisableTiming), "event");
@@ -761,8 +784,10 @@ drb_status drb_rb_destroy(drb_rb* h) {
         cudaFreeHost(h->mailbox);
         for (auto e : h->done)
             cudaEventDestroy(e);
+        if (h->run_done)
+            cudaEventDestroy(h->run_done);
         for (int i = 0; i < drb_rb::kEv; ++i)
-            for (cudaEvent_t e : {h->ev_user[i], h->ev_sel[i], h->ev_plan[i], h->ev_copy[i]})
+            for (cudaEvent_t e : {h->ev_user[i], h->ev_sel[i], h->ev_plan[i], h->ev_copy[i], h->rel[i]})
                 cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
             cudaEventDestroy(h->in_free[i]);
@@ -1190,8 +1215,10 @@ void enqueue_copy(drb_rb* h, uint64_t i, const void* batch, const uint32_t* labe
         if (launch_peers_wait(p, h->s_wait))
             fail(DRB_ERR_INTERNAL, std::string("peers_wait launch failed: ") + cudaGetErrorString(cudaGetLastError()));
         cuda_check(cudaEventRecord(h->done[p.aslot], h->s_wait), "event record");
+        h->slot_run[p.aslot] = 0;
     } else {
         cuda_check(cudaEventRecord(h->done[p.aslot], s), "event record");
+        h->slot_run[p.aslot] = 0;
     }
     h->last_copy_stream = s;
     if (out) {
@@ -1217,7 +1244,8 @@ void rmode_advance(drb_rb* h) {
 
 // One step through the resident engine: post m_i's descriptor on `s`, then `s`
 // waits for "m'_i ready". An unaligned device batch is first copied into a staging slot.
-void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n, cudaStream_t s, drb_aug* out) {
+void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n, cudaStream_t s, drb_aug* out,
+                cudaStream_t consumer = nullptr) {
     const uint64_t i = h->step;
     const auto& c = h->cfg;
     const uint8_t* b = static_cast<const uint8_t*>(batch);
@@ -1231,9 +1259,35 @@ void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n
         cuda_check(cudaMemcpyAsync(slot, batch, uint64_t(n) * c.sample_bytes, cudaMemcpyDeviceToDevice, s), "stage");
         b = slot;
     }
-    rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, i + 1);
     const uint32_t slot = uint32_t(i % h->aug_ring);
-    cuda_check(cudaEventRecord(h->done[slot], s), "event record");
+    if (!consumer) {  // one stream: posting m_i releases every earlier m'; then wait for m'_i
+        rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, i + 1);
+        cuda_check(cudaEventRecord(h->done[slot], s), "event record");
+        h->slot_run[slot] = 0;
+    } else {  // producer / consumer streams: the consumer releases what it used, then waits
+        rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, 0, true);
+        if (h->feed_kernels) {
+            if (launch_feed_post(&h->runctl->consumed, i, consumer) ||
+                launch_feed_wait(&h->runctl->ready, i + 1, consumer))
+                fail(DRB_ERR_INTERNAL, std::string("feed failed: ") + cudaGetErrorString(cudaGetLastError()));
+        } else {
+            CUstreamBatchMemOpParams ops[2];
+            std::memset(ops, 0, sizeof ops);
+            ops[0].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+            ops[0].writeValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->consumed);
+            ops[0].writeValue.value64 = i;  // m'_0 .. m'_{i-1}: everything the consumer was handed
+            ops[0].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+            ops[1].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+            ops[1].waitValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->ready);
+            ops[1].waitValue.value64 = i + 1;
+            ops[1].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+            const CUresult r = memops().batch(reinterpret_cast<CUstream>(consumer), 2, ops, 0);
+            if (r != CUDA_SUCCESS)
+                fail(DRB_ERR_INTERNAL, "consumer wait: cuStreamBatchMemOp failed (" + std::to_string(int(r)) + ")");
+        }
+        cuda_check(cudaEventRecord(h->done[slot], consumer), "event record");
+        h->slot_run[slot] = 0;
+    }
     const uint32_t row0 = c.max_batch - n;
     out->n = n;
     out->ring_slot = slot;
@@ -1258,8 +1312,11 @@ void rmode_run(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const u
         h->step += cnt;
         done += cnt;
     }
-    for (auto& e : h->done)
-        cuda_check(cudaEventRecord(e, s), "event");
+    // one event for the whole run (its m' ring slots alias it): the host cost of recording
+    // R events would sit inside a timed run
+    cuda_check(cudaEventRecord(h->run_done, s), "event");
+    for (auto& f : h->slot_run)
+        f = 1;
     rmode_advance(h);
 }
 
@@ -1296,6 +1353,35 @@ drb_status drb_rb_step(drb_rb* h, const void* batch, const uint32_t* labels, uin
                      h->ev_user[ev_of(i)], true);
         if (s != h->stream || h->cfg.world > 1)
             cuda_check(cudaStreamWaitEvent(s, h->done[i % h->aug_ring], 0), "wait");
+    });
+}
+
+drb_status drb_rb_step_split(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n, void* producer,
+                             void* consumer, drb_aug* out) {
+    DRB_REQUIRE(h && out && consumer && ((batch && labels) || n == 0));
+    return guarded([&] {
+        check_step_args(h, n);
+        device_guard g(h->cfg.device);
+        cudaStream_t sp = producer ? static_cast<cudaStream_t>(producer) : h->stream;
+        cudaStream_t sc = static_cast<cudaStream_t>(consumer);
+        if (h->rmode) {
+            rmode_step(h, batch, labels, n, sp, out, sc);
+            return;
+        }
+        // three-kernel path: a release event per call on the consumer (its use of every m'
+        // handed out before); step i refills m'_{i+1-R}'s slot, so the producer waits for the
+        // release recorded at call i+2-R (a more recent one for rings deeper than the events)
+        const uint64_t i = h->step;
+        cuda_check(cudaEventRecord(h->rel[i % drb_rb::kEv], sc), "event");
+        const uint64_t R = h->aug_ring;
+        if (i + 2 >= R) {
+            const uint64_t k = std::max<uint64_t>(i + 2 - R, i + 1 >= drb_rb::kEv ? i + 1 - drb_rb::kEv : 0);
+            cuda_check(cudaStreamWaitEvent(sp, h->rel[k % drb_rb::kEv], 0), "wait");
+        }
+        const drb_status st = drb_rb_step(h, batch, labels, n, sp, out);
+        if (st != DRB_OK)
+            fail(st, t_last_error);
+        cuda_check(cudaStreamWaitEvent(sc, h->done[out->ring_slot], 0), "wait");
     });
 }
 
@@ -1537,7 +1623,8 @@ drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count) {
     return guarded([&] {
         device_guard g(h->cfg.device);
         const auto t0 = std::chrono::steady_clock::now();
-        cuda_check(cudaEventSynchronize(h->done[aug->ring_slot]), "aug wait");
+        cuda_check(cudaEventSynchronize(h->slot_run[aug->ring_slot] ? h->run_done : h->done[aug->ring_slot]),
+                   "aug wait");
         h->wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         const volatile uint32_t* mb = h->mailbox;
         const uint32_t e = mb[mb_err(aug->ring_slot, h->aug_ring)];
@@ -1581,6 +1668,7 @@ drb_status drb_rb_synchronize(drb_rb* h) {
         cuda_check(cudaStreamSynchronize(h->d2h), "sync");
         for (auto e : h->done)
             cuda_check(cudaEventSynchronize(e), "sync");
+        cuda_check(cudaEventSynchronize(h->run_done), "sync");
     });
 }
 

@@ -177,11 +177,14 @@ struct alignas(64) FeedDesc {
     uint64_t batch_stride;  // bytes between ring batches
     uint64_t label_stride;  // u32 elements between ring label rows
     uint64_t i_begin;       // engine iteration of the descriptor's first step
-    uint64_t count_n;       // steps (lo 32) | batch rows n (hi 32)
+    uint64_t count_n;       // steps (lo 32) | batch rows n (bits 32-62) | kDescSplit
     uint64_t ring_first;    // ring batches (lo 32) | first batch of the range (hi 32)
     uint64_t seq;           // descriptor index + 1, written last: the descriptor is complete
 };
 constexpr uint32_t kFeedDescWords = sizeof(FeedDesc) / 8;
+// The descriptor's m' is consumed on another stream, which releases consumed m' explicitly
+// (RunCtl::consumed); without the flag, posting step i releases every m' before it.
+constexpr uint64_t kDescSplit = 1ull << 63;
 
 // Device counters of the resident engine. Iteration counters are absolute (i+1 once
 // iteration i's role finished) and carry over from one instance to the next.
@@ -195,9 +198,10 @@ struct alignas(64) RunCtl {
     uint64_t stop_at;    // gen << 40 | iteration: every role of instance `gen` leaves there
     uint64_t next_step[2];  // [gen & 1]: where instance `gen` starts (written by the one before)
     uint64_t next_desc[2];  // its first descriptor
+    uint64_t consumed;      // split-stream consumers: m'_0 .. m'_{consumed-1} are released
     uint32_t error;      // sticky: a wait timed out or a round failed -> every role leaves
     uint32_t where;      // diagnostics: the wait that failed first (site << 24 | k)
-    uint32_t pad[4];
+    uint32_t pad[2];
     uint32_t ticket[8];  // copy-CTA arrivals of iteration k in slot k % 8 (CTAs drift < 8 iterations)
 };
 constexpr uint64_t kStopMask = (1ull << 40) - 1;

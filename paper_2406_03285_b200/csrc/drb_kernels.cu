@@ -1479,7 +1479,7 @@ __device__ void cursor_seek(FeedCursor& c, const RunParams& rp, uint64_t i) {
         c.ib = __ldcg(&d->i_begin);
         const uint64_t cn = __ldcg(&d->count_n), rf = __ldcg(&d->ring_first);
         c.cnt = static_cast<uint32_t>(cn);
-        c.n = static_cast<uint32_t>(cn >> 32);
+        c.n = static_cast<uint32_t>(cn >> 32) & 0x7fffffffu;
         c.ring = static_cast<uint32_t>(rf);
         c.first = static_cast<uint32_t>(rf >> 32);
     }
@@ -1595,7 +1595,9 @@ __device__ void run_publisher(const RunParams& rp, uint64_t i0, volatile unsigne
 // The feeder (one lane): admits posted descriptors in order, and ends the instance when idle.
 __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
     uint64_t j = j0, admitted = i0, idle_t0 = 0;
+    uint64_t released = i0;  // m' below this are released by implicit (single-stream) posts
     bool failed = false;
+    const uint32_t R = rp.base.aug_ring;
 #pragma unroll 1
     for (uint32_t spin = 0;; ++spin) {
         if (ld_acquire_sys(rp.feed_seq + (j % kFeedRing)) == j + 1) {  // posted (stream order)
@@ -1609,12 +1611,25 @@ __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
                              : "=l"(w[x]), "=l"(w[x + 1])
                              : "l"(hs + x)
                              : "memory");
+            if (w[5] & kDescSplit) {
+                // plan(i)/B(i) refill m'_{i+1}'s slot, last handed out as m'_{i+1-R}: its
+                // consumer (another stream) must have released it
+                const uint64_t need = w[4] + 2 >= R ? w[4] + 2 - R : 0;
+                if (released < need && ld_acquire_sys(&rp.ctl->consumed) < need) {
+                    idle_t0 = 0;  // posted work is waiting: not idle
+                    __nanosleep(128);
+                    continue;
+                }
+            } else if (w[4] > released) {
+                released = w[4];
+            }
             uint64_t* dd = reinterpret_cast<uint64_t*>(rp.feed + (j % kFeedRing));
 #pragma unroll
             for (uint32_t x = 0; x < kFeedDescWords; ++x)
                 dd[x] = w[x];
             admitted = w[4] + static_cast<uint32_t>(w[5]);  // i_begin + count
             st_release_gpu(&rp.ctl->admitted, admitted);
+            run_mark(rp, w[4], 13);
             ++j;
             idle_t0 = 0;
             spin = 0;
@@ -1683,6 +1698,7 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
             break;
         }
         st_release_sys(&rp.ctl->ready, i + 1);
+        run_mark(rp, i, 14);
         cursor_seek(c, rp, i);
         if (i + 1 == c.ib + c.cnt) {  // the last step of its descriptor: the slot is free
             st_release_gpu(&rp.ctl->desc_done, c.j + 1);
@@ -1971,6 +1987,7 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
                                  : "memory");
         }
         st_release_gpu(&rp.ctl->b_done, i + 1);
+        run_mark(rp, i, 9);
     }
 }
 
@@ -2382,8 +2399,10 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
             if (!__shfl_sync(kFull, wait_cta(&fl->a_done, k + 1, k) ? 1 : 0, 0))
                 return;
             delay_exp(4);
-            if (lane == 0)
+            if (lane == 0) {
+                run_mark(rp, i, 8);
                 run_b_arrive(rp, b, k, i, multi);
+            }
         }
     }
     // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
@@ -2784,3 +2803,18 @@ int launch_read_slots(const uint8_t* slab, const uint32_t* slab_labels, const ui
 }
 
 }  // namespace drb_b200
+
+#if DRB_INSTRUMENT
+// tools/ timeline probes only: one thread stores %globaltimer when the stream reaches it.
+namespace {
+__global__ void dbg_stamp_kernel(unsigned long long* out) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int drb_dbg_stamp(unsigned long long* out, void* stream) {
+    dbg_stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+#endif

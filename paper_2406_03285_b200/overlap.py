@@ -6,10 +6,11 @@ cost, run a training stub of >= 10x that cost after every `engine.update(m)`, an
 mean time the trainer waits for its augmented batch to stay under 5% of the iteration.
 
 Here the trainer is a real GPU training step (forward, backward and SGD update of a small
-convolutional classifier on m'_i, bf16 autocast) on its own CUDA stream, and the engine's
-three kernels run on theirs. update(m_{i+1}) is enqueued one iteration ahead, so round i+1's
-selection, sampling and copy run while step i trains; the train stream only waits on the
-event of m'_i. Everything is timed on the device:
+convolutional classifier on m'_i, bf16 autocast) on its own CUDA stream, next to the
+resident engine on its partition of the SMs. update(m_{i+1}) posts m_{i+1} on the loader's
+stream right after step i is enqueued, so round i+1's selection, sampling and copy run while
+step i trains; the train stream only waits for m'_{i+1} behind step i. Everything is timed on
+the device:
   background_ms      engine alone, device time per update
   train_ms           the training step alone on a resident batch
   iteration_ms       the overlapped loop, per iteration (train stream events)
@@ -119,31 +120,22 @@ def run_overlap_bench(eng, data_ring: torch.Tensor, label_ring: torch.Tensor, tr
     torch.cuda.synchronize(dev)
     train_ms = e0.elapsed_time(e1) / min(iterations, 100)
 
-    # overlapped loop: update(m_{i+1}) is enqueued before step i trains on m'_i
-    ready = [torch.cuda.Event() for _ in range(3)]
-
-    def enqueue(i):
-        a = eng.update((data_ring[i % B], label_ring[i % B]), stream=s_eng)
-        ready[i % 3].record(s_eng)
-        return a
-
-    pending = enqueue(0)
+    # overlapped loop (the reference's trainer, trainer.cpp:109-113, with the loader on its own
+    # stream): after step i is enqueued on the train stream, update(m_{i+1}) posts m_{i+1} on
+    # the engine stream — round i+1 runs on the device while step i trains — and the train
+    # stream releases m'_i and waits for m'_{i+1} behind step i (drb_rb_step_split)
+    aug = eng.update((data_ring[0], label_ring[0]), stream=s_eng, consumer=s_train)
     torch.cuda.synchronize(dev)
     w0 = [ev() for _ in range(iterations)]
     w1 = [ev() for _ in range(iterations)]
     e0.record(s_train)
     for i in range(iterations):
-        cur = pending
-        w0[i].record(s_train)  # step i-1 done; from here the train stream waits for m'_i
-        s_train.wait_event(ready[i % 3])
-        w1[i].record(s_train)
-        # m'_i stays valid until update(m_{i+2}) is enqueued; the next update is i+1, and
-        # the one after waits on the train stream (s_eng waits for step i's reads below)
-        pending = enqueue(i + 1)
         with torch.cuda.stream(s_train):
-            dd, ll = cur.tensors_nowait()
+            dd, ll = aug.tensors_nowait()
             train_step(dd, ll)
-        s_eng.wait_stream(s_train)  # step i read m'_i before update(m_{i+2}) may reuse its slot
+        w0[i].record(s_train)  # step i done; from here the train stream waits for m'_{i+1}
+        aug = eng.update((data_ring[(i + 1) % B], label_ring[(i + 1) % B]), stream=s_eng, consumer=s_train)
+        w1[i].record(s_train)
     e1.record(s_train)
     torch.cuda.synchronize(dev)
     iteration_ms = e0.elapsed_time(e1) / iterations

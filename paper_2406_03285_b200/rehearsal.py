@@ -387,17 +387,27 @@ class engine:
     def shutdown(self) -> None:
         check(lib.drb_rb_shutdown(self.buffer.h))
 
-    def update(self, m, stream: Optional[torch.cuda.Stream] = None) -> augmented_batch:
+    def update(self, m, stream: Optional[torch.cuda.Stream] = None,
+               consumer: Optional[torch.cuda.Stream] = None) -> augmented_batch:
         """Enqueue round i for m_i and return m'_i = m_i ++ reps(i-1) (fused update+augment,
-        trainer.cpp:109-113). Waits are deferred to first use of the result."""
+        trainer.cpp:109-113). Waits are deferred to first use of the result: `stream` waits
+        for m'_i. With `consumer`, m_i is posted in `stream`'s order (its producer) and the
+        consumer stream releases the m' it used so far, then waits for m'_i (drb_rb_step_split:
+        back-to-back updates run pipelined in the engine)."""
         data, labels = m
         n = int(labels.shape[0])
         data = _as_bytes(data) if n else data
         labels = _as_labels(labels) if n else labels
         s = stream if stream is not None else torch.cuda.current_stream(self.buffer.device)
         aug = _lib.drb_aug()
-        check(lib.drb_rb_step(self.buffer.h, data.data_ptr() if n else None, labels.data_ptr() if n else None, n,
-                              _stream_arg(s), C.byref(aug)))
+        if consumer is None:
+            check(lib.drb_rb_step(self.buffer.h, data.data_ptr() if n else None, labels.data_ptr() if n else None,
+                                  n, _stream_arg(s), C.byref(aug)))
+        else:
+            check(lib.drb_rb_step_split(self.buffer.h, data.data_ptr() if n else None,
+                                        labels.data_ptr() if n else None, n, _stream_arg(s), _stream_arg(consumer),
+                                        C.byref(aug)))
+            s = consumer
         if n:  # m_i is read until "m'_i ready", which `s` waits for: the caching allocator must
             # not hand m_i's blocks (or a converted label copy) to anyone before that point
             data.record_stream(s)

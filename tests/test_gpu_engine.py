@@ -14,9 +14,10 @@ from paper_2406_03285_b200.workload import stream_spec
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def drb():
+@pytest.fixture(params=["resident", "three-kernel"])
+def drb(request, monkeypatch):
     import paper_2406_03285_b200 as drb
+    monkeypatch.setenv("DRB_PERSIST", "1" if request.param == "resident" else "0")
     return drb
 
 
@@ -160,3 +161,37 @@ def test_engine_dies_on_bad_label(drb):
     assert a.count() == 8 + 7  # m'_1 = m_1 ++ reps(0) is still delivered (round 0 was fine)
     with pytest.raises(drb.engine_error):
         eng.update(dev(spec.payload(0, 2), spec.labels(0, 2)))
+
+
+@pytest.mark.parametrize("ring", [0, 70])
+def test_split_streams_pipelined_parity(drb, ring):
+    """update(m_i, stream=loader, consumer=trainer) (drb_rb_step_split): every post goes out on
+    the loader stream back to back (the engine pipelines them); the trainer stream copies each
+    m'_i right after its wait. With the default 6-slot m' ring the engine may refill a slot
+    only after the trainer released it — the copies must still equal the oracle's m'."""
+    K, cap, S, b, c, r, steps = 20, 6, 4096, 40, 14, 9, 64
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=21, aug_ring=ring)
+    eng = drb.engine(buf)
+    eng.start()
+    rep = Backend("port").replay(1, K, cap, S, c, r, 21)
+    spec = stream_spec(K, 2, b, S, steps_per_task=25, seed=21)
+    loader, trainer = torch.cuda.Stream(), torch.cuda.Stream()
+    ins = [dev(spec.payload(0, i), spec.labels(0, i)) for i in range(steps)]
+    torch.cuda.synchronize()
+    got = []
+    for i in range(steps):
+        aug = eng.update(ins[i], stream=loader, consumer=trainer)
+        with torch.cuda.stream(trainer):
+            d, lab = aug.tensors_nowait()
+            got.append((d.clone(), lab.clone(), aug))
+    torch.cuda.synchronize()
+    for i in range(steps):
+        o, ol, oc = rep.step(spec.payload(0, i)[None], spec.labels(0, i)[None])
+        d, lab, aug = got[i]
+        cnt = int(oc[0])
+        if ring:  # (a 6-slot ring's row counts are rewritten by later steps by now)
+            assert aug.count() == cnt, i
+        assert np.array_equal(lab[:cnt].cpu().numpy().astype(np.uint32), ol[0, :cnt]), i
+        assert np.array_equal(d[:cnt].cpu().numpy(), o[0, :cnt]), i
+    assert eng.device_error() == 0
+    eng.shutdown()

@@ -1,6 +1,8 @@
 """Engine overlapped with a real training step (acceptance criterion 5,
 proj/tests/acceptance.cpp:229-256): with a training step >= 10x the engine's background cost,
-the trainer loses < 5% of its iteration to the engine."""
+the trainer waits for its augmented batch < 5% of its iteration (the reference's wait_ms: the
+time update() blocks, engine.cpp:82-90). The overall slowdown of the training loop (which also
+counts SM and HBM sharing with the resident engine) is reported beside it."""
 import numpy as np
 import pytest
 import torch
@@ -23,5 +25,6 @@ def test_overlap_wait_under_5_percent():
     model = conv_classifier(224, 3, K, width=64).cuda().to(memory_format=torch.channels_last)
     res = run_overlap_bench(eng, data, lab, make_train_step(model), 200)
     eng.shutdown()
+    print(res, "wait fraction", res.wait_fraction, "slowdown fraction", res.slowdown_fraction)
     assert res.train_cost_ms >= 10 * res.background_ms, res
     assert res.wait_fraction < 0.05, res
