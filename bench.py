@@ -113,6 +113,38 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons, "samples": len(rows)}
 
 
+class NvlinkCounters:
+    """NVLink data bytes sent / received by one GPU (NVML field values, summed over its links):
+    the hardware's count of what the pushes put on the wire, read around the timed region."""
+
+    def __init__(self, device: int, links: int = 18):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.fields = [(f, l) for f in (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                            pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX) for l in range(links)]
+            self.read()
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = f"{type(e).__name__}: {e}"
+
+    def read(self):
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, self.fields)
+        tx = rx = 0
+        for k, v in enumerate(vals):
+            if v.nvmlReturn != 0:
+                continue
+            x = int(v.value.ullVal) * 1024  # KiB
+            if k < len(self.fields) // 2:
+                tx += x
+            else:
+                rx += x
+        return tx, rx
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -269,8 +301,10 @@ def main():
     spec = stream_spec(K, cfg["T"], b, S, steps_per_task=steps_per_task, seed=1)
     # the whole GPU for the engine: the bench has no training step to share the SMs with
     engine_ctas = torch.cuda.get_device_properties(local).multi_processor_count
+    # 16 m' slots: in the split update() form the loader may run 14 steps ahead of the trainer
+    aug_ring = 16
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, rank=rank,
-                               world=N, device=local, engine_ctas=engine_ctas)
+                               world=N, device=local, engine_ctas=engine_ctas, aug_ring=aug_ring)
     if N > 1:
         from paper_2406_03285_b200.dist import connect_world
         connect_world(buf)
@@ -311,6 +345,7 @@ def main():
     # The K launches are captured into a CUDA graph beforehand (host launch cost paid
     # outside the timed region, as a training loop would replay a captured step).
     resident = eng.engine_info()["resident"]
+    nvl = NvlinkCounters(local)
     run = eng.prepare_run(data, lab, args.steps, first=args.warmup) if not args.no_graph else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -318,6 +353,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         inst0 = eng.engine_info()["instances"]
+        nvl0 = nvl.read() if nvl.ok else None
         ev0.record(stream)
         if run is not None:
             run.launch(stream)
@@ -327,6 +363,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
     timed_instances = eng.engine_info()["instances"] - inst0
+    nvl1 = nvl.read() if (nvl.ok and N > 1) else None
     if run is not None:
         run.close()
     t_ms = ev0.elapsed_time(ev1)
@@ -335,6 +372,20 @@ def main():
         tt = torch.tensor([t_ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
+    nvlink = None
+    if N > 1:
+        if nvl.ok:
+            tt = torch.tensor([nvl1[0] - nvl0[0], nvl1[1] - nvl0[1]], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            # algorithmic: every rank receives r*S*(N-1)/N per step (the reps its peers own)
+            nvlink = {"tx_bytes_per_step_per_rank": float(tt[0]) / N / args.steps,
+                      "rx_bytes_per_step_per_rank": float(tt[1]) / N / args.steps,
+                      "algorithmic_bytes_per_step_per_rank": r * S * (N - 1) / N,
+                      "rx_gbs_per_rank": float(tt[1]) / N / (t_ms / 1000.0) / 1e9 if t_ms else None,
+                      "peak_gbs_per_direction": 900.0,
+                      "source": "NVML NVLink data throughput counters, summed over links, around the timed region"}
+        else:
+            nvlink = {"unavailable": nvl.err}
     samples = (b + r) * N * args.steps  # steady state: every rank's m'_i has b + r rows
     value = samples / (t_ms / 1000.0)
     ms_per_step = t_ms / args.steps
@@ -347,6 +398,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize()
+        c0 = nvl.read() if (nvl.ok and N > 1) else None
         e0.record(stream)
         if sr is not None:
             sr.launch(stream)
@@ -354,15 +406,23 @@ def main():
             eng.run(data, lab, ks, first=0, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
+        c1 = nvl.read() if (nvl.ok and N > 1) else None
         if sr is not None:
             sr.close()
         tk = e0.elapsed_time(e1)
+        ent = {"steps": ks}
         if N > 1:
             tt = torch.tensor([tk], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tk = float(tt.item())
+            if c0 is not None:
+                cc = torch.tensor([c1[0] - c0[0], c1[1] - c0[1]], device=f"cuda:{local}", dtype=torch.float64)
+                dist.all_reduce(cc, op=dist.ReduceOp.SUM)
+                ent["nvlink_rx_bytes_per_step_per_rank"] = float(cc[1]) / N / ks
+                ent["nvlink_tx_bytes_per_step_per_rank"] = float(cc[0]) / N / ks
         step += ks
-        sweep.append({"steps": ks, "ms": tk, "us_per_step": 1000.0 * tk / ks})
+        ent.update({"ms": tk, "us_per_step": 1000.0 * tk / ks})
+        sweep.append(ent)
 
     # The drop-in API a trainer calls (trainer.cpp:109-113): update(m_i) on one stream, one call
     # per step, serial (the next post follows the previous m' on the stream, as in a training
@@ -398,7 +458,8 @@ def main():
     exe = os.path.join(ROOT, "tools", "update_bench")
     if N == 1 and os.path.exists(exe):
         try:
-            res = subprocess.run([exe, "200", str(local)], capture_output=True, text=True, timeout=300)
+            res = subprocess.run([exe, "200", str(local), str(aug_ring)], capture_output=True, text=True,
+                                 timeout=300)
             cpp_update = json.loads(res.stdout.strip().splitlines()[-1]) if res.returncode == 0 else \
                 {"error": res.stderr[-300:]}
         except Exception as e:  # noqa: BLE001
@@ -548,6 +609,7 @@ def main():
                          "bytes_formula": "2*S*(b+r+c) per rank per iteration (SURVEY.md 8d)"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
+            **({"nvlink": nvlink} if nvlink else {}),
             **({"steps_sweep": sweep} if sweep else {}),
         }
         print(json.dumps(line), flush=True)

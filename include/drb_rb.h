@@ -79,6 +79,9 @@ typedef struct drb_rng {
 
 typedef struct drb_rb drb_rb; /* one rank: HBM slab + occupancy + engine state */
 
+/* drb_rb_config.flags: record per-round timings on the device (drb_rb_drain_timings) */
+#define DRB_RB_FLAG_TIMINGS 1u
+
 typedef struct drb_rb_config {
     uint32_t n_classes;       /* K                                   (config.hpp:37) */
     uint32_t per_class_cap;   /* floor(S_max / K)                    (capacity.cpp:10-18) */
@@ -90,7 +93,7 @@ typedef struct drb_rb_config {
     uint32_t world;           /* N <= DRB_RB_MAX_WORLD                                   */
     uint64_t seed;            /* rng_seed                            (config.hpp:49)     */
     int32_t device;           /* CUDA device ordinal                                     */
-    uint32_t flags;           /* reserved, 0                                             */
+    uint32_t flags;           /* DRB_RB_FLAG_* bits, 0 by default                         */
     uint32_t aug_ring;        /* m' ring depth: m'_i's slot is rewritten by step i+aug_ring;
                                  0 = 6 (the default), else >= 6. A deep ring keeps every m'
                                  of a multi-step run readable (drb_rb_aug_slot)            */
@@ -256,6 +259,27 @@ DRB_RB_API drb_status drb_rb_graph_prepare(drb_rb* h, const void* batches, uint6
 DRB_RB_API drb_status drb_rb_graph_launch(drb_rb_graph* g, void* stream);
 DRB_RB_API drb_status drb_rb_graph_destroy(drb_rb_graph* g);
 /* Rows of m' for a completed step (blocks on that step's completion). */
+/* Per-round timings, replaces engine::timings / drain_timings() (proj/src/engine/engine.hpp:43-50,
+ * :93; recorded at engine.cpp:139-168). Device timestamps of the resident engine (config flag
+ * DRB_RB_FLAG_TIMINGS; the three-kernel path records none):
+ *   populate_ms  sel(i): update_buffer + publish_row           (engine.cpp:141-144)
+ *   augment_ms   plan(i) start -> round i's pushes complete   (view_at + plan + fetch, :146-163)
+ *   latency_ms   round i admitted -> its pushes complete      (enqueue -> promise, :139,168)
+ *   wait_ms      0: no engine thread blocks (the consumer's stream waits on the device)
+ *   degraded     0: a stalled peer fails the engine instead */
+typedef struct drb_timing {
+    uint64_t iteration;
+    double populate_ms;
+    double augment_ms;
+    double latency_ms;
+    double wait_ms;
+    uint32_t degraded;
+    uint32_t pad;
+} drb_timing;
+/* Moves the timings of the rounds completed since the last drain (at most the last 4096) into
+ * out[0..capacity); *count = records written. Waits for the engine's posted work first. */
+DRB_RB_API drb_status drb_rb_drain_timings(drb_rb* h, drb_timing* out, uint32_t capacity, uint32_t* count);
+
 /* m'_step still held by the engine's ring (one of the last aug_ring enqueued steps), for a
  * step whose batch had n rows: the same views drb_rb_step returned for it. With a deep ring
  * (drb_rb_config.aug_ring >= steps) every m' of a drb_rb_run stays readable after the run

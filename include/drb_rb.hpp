@@ -286,6 +286,14 @@ public:
         return v;
     }
     void synchronize() { check(drb_rb_synchronize(b_.raw())); }
+    // engine::drain_timings (engine.hpp:93); needs DRB_RB_FLAG_TIMINGS in the buffer's config
+    std::vector<drb_timing> drain_timings() {
+        std::vector<drb_timing> out(4096);
+        std::uint32_t n = 0;
+        check(drb_rb_drain_timings(b_.raw(), out.data(), std::uint32_t(out.size()), &n));
+        out.resize(n);
+        return out;
+    }
 
 private:
     rehearsal_buffer& b_;

@@ -22,6 +22,7 @@ DRB_ERR_TRAINING = 6
 DRB_ERR_USAGE = 7
 DRB_ERR_INTERNAL = 8
 MAX_WORLD = 8
+FLAG_TIMINGS = 1  # DRB_RB_FLAG_TIMINGS
 AUG_RING = 6  # default m' ring depth (drb_rb_config.aug_ring = 0)
 
 
@@ -96,6 +97,12 @@ class drb_slot_ref(C.Structure):
     _fields_ = [("owner", C.c_uint32), ("cls", C.c_uint32), ("slot", C.c_uint32)]
 
 
+class drb_timing(C.Structure):
+    _fields_ = [("iteration", C.c_uint64), ("populate_ms", C.c_double), ("augment_ms", C.c_double),
+                ("latency_ms", C.c_double), ("wait_ms", C.c_double), ("degraded", C.c_uint32),
+                ("pad", C.c_uint32)]
+
+
 class drb_aug(C.Structure):
     _fields_ = [
         ("data", C.c_void_p),
@@ -148,6 +155,7 @@ def _load():
         "drb_rb_engine_info": (st, [vp, P(u32), P(u64), P(u64), P(u32)]),
         "drb_rb_synchronize": (st, [vp]),
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
+        "drb_rb_drain_timings": (st, [vp, P(drb_timing), u32, P(u32)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),
         "drb_ds_load": (st, [C.c_char_p, i32, P(vp)]),

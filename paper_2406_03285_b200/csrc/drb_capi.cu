@@ -198,6 +198,13 @@ struct drb_rb {
     uint8_t* astage = nullptr;        // staging of unaligned device batches [4][max_batch][S]
     bool feed_kernels = false;        // post / wait with tiny kernels instead of memory operations
     bool feeder_last = true;          // feeder + ready warps on the last copy CTA, not the sel CTA
+    // Under ncu / compute-sanitizer (CUDA_INJECTION64_PATH set) or DRB_TOOL_MODE=1 kernels run
+    // one at a time: a resident instance would wait forever for a post queued behind it. So every
+    // post launches its own instance (after the post's sequence word) and instances leave as
+    // soon as they are idle.
+    bool tool_mode = false;
+    uint64_t* timings = nullptr;      // DRB_RB_FLAG_TIMINGS: per-round device stamps [kTimingRing][8]
+    uint64_t timings_drained = 0;     // first round not yet returned by drb_rb_drain_timings
     unsigned long long* prof = nullptr;  // DRB_DBG 65536: sel/plan phase cycle accumulators [64]
     cudaEvent_t run_end = nullptr;
     cudaEvent_t last_work = nullptr;  // after the handle's latest enqueued iteration (any path)
@@ -337,6 +344,8 @@ void rmode_launch(drb_rb* h) {
     rp.ww = wlist_words(h->cfg.max_batch);
     rp.copy_ctas = h->run_grid - 2;
     rp.feeder_cta = h->feeder_last ? h->run_grid - 1 : 0;
+    rp.timings = h->timings;
+    rp.tool_mode = h->tool_mode ? 1u : 0u;
     if (launch_run(rp, h->run_grid, h->s_run))
         fail(DRB_ERR_INTERNAL, std::string("resident engine launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     h->gen = rp.gen;
@@ -388,7 +397,7 @@ void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const 
     *mb64(h, kMbHostPosted) = j + 1;
     std::atomic_thread_fence(std::memory_order_seq_cst);  // (Dekker with the leaving feeder)
     const uint64_t ex = *mb64(h, kMbExiting);
-    const bool launch = !h->alive || (ex >> 32) == (h->gen & 0xffffffffull);
+    const bool launch = h->tool_mode || !h->alive || (ex >> 32) == (h->gen & 0xffffffffull);
     uint64_t* seq = h->feed_seq + (j % kFeedRing);
     if (h->feed_kernels || launch) {
         // with a launch: the sequence word first, then the instance, then the wait — an
@@ -728,6 +737,13 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             h->run_grid = std::max(3u, std::min(uint32_t(h->sm_count), uint32_t(std::strtoul(rg, nullptr, 10))));
         if (const char* iu = std::getenv("DRB_IDLE_US"))
             h->idle_ns = std::strtoull(iu, nullptr, 10) * 1000ull;
+        if (c.flags & DRB_RB_FLAG_TIMINGS) {
+            cuda_check(cudaMalloc(&h->timings, uint64_t(kTimingRing) * kTimingWords * 8), "timings alloc");
+            cuda_check(cudaMemset(h->timings, 0, uint64_t(kTimingRing) * kTimingWords * 8), "memset");
+        }
+        if (std::getenv("CUDA_INJECTION64_PATH") || (std::getenv("DRB_TOOL_MODE") &&
+                                                     std::getenv("DRB_TOOL_MODE")[0] == '1'))
+            h->tool_mode = true;
         if (const char* fl = std::getenv("DRB_FEEDER_LAST"))
             h->feeder_last = fl[0] != '0';
         if (const char* fk = std::getenv("DRB_FEED"); fk && std::string(fk) == "kernel")
@@ -799,6 +815,7 @@ drb_status drb_rb_destroy(drb_rb* h) {
             cudaFree(h->runctl);
         cudaFree(h->feed);
         cudaFree(h->feed_seq);
+        cudaFree(h->timings);
         if (h->hdesc)
             cudaFreeHost(h->hdesc);
         cudaFree(h->astage);
@@ -1669,6 +1686,36 @@ drb_status drb_rb_synchronize(drb_rb* h) {
         for (auto e : h->done)
             cuda_check(cudaEventSynchronize(e), "sync");
         cuda_check(cudaEventSynchronize(h->run_done), "sync");
+    });
+}
+
+drb_status drb_rb_drain_timings(drb_rb* h, drb_timing* out, uint32_t capacity, uint32_t* count) {
+    DRB_REQUIRE(h && count && (out || capacity == 0));
+    return guarded([&] {
+        *count = 0;
+        if (!h->timings)
+            return;
+        device_guard g(h->cfg.device);
+        rmode_quiesce(h);
+        cuda_check(cudaDeviceSynchronize(), "timings order");
+        std::vector<uint64_t> t(uint64_t(kTimingRing) * kTimingWords);
+        cuda_check(cudaMemcpy(t.data(), h->timings, t.size() * 8, cudaMemcpyDeviceToHost), "timings copy");
+        uint64_t i = std::max<uint64_t>(h->timings_drained, h->step > kTimingRing ? h->step - kTimingRing : 0);
+        uint32_t n = 0;
+        for (; i < h->step && n < capacity; ++i) {
+            const uint64_t* r = t.data() + (i % kTimingRing) * kTimingWords;
+            auto ms = [](uint64_t a, uint64_t b) { return b >= a && a ? double(b - a) / 1e6 : 0.0; };
+            drb_timing& o = out[n++];
+            o.iteration = i;
+            o.populate_ms = ms(r[1], r[2]);
+            o.augment_ms = ms(r[3], r[4]);
+            o.latency_ms = ms(r[0], r[4]);
+            o.wait_ms = 0.0;
+            o.degraded = 0;
+            o.pad = 0;
+        }
+        h->timings_drained = i;
+        *count = n;
     });
 }
 

@@ -231,7 +231,13 @@ struct RunParams {
     const volatile uint32_t* quiesce;                // mapped: leave as soon as idle
     uint32_t sel_par0, plan_par0, pw, ww, copy_ctas;
     uint32_t feeder_cta;  // CTA whose warps 4 and 5 run the feeder and the ready publisher
+    uint64_t* timings;    // DRB_RB_FLAG_TIMINGS: [kTimingRing][kTimingWords] globaltimer stamps, else null
+    uint32_t tool_mode;   // under a tool that serialises the device: one instance per post, leave when idle
+    uint32_t pad2;
 };
+// Per-round stamps (drb_rb_drain_timings): [0] admitted, [1] sel start, [2] sel handed over,
+// [3] plan start, [4] pushes complete (b_done)
+constexpr uint32_t kTimingRing = 4096, kTimingWords = 8;
 constexpr uint32_t kRunThreads = 32 * (kMaxWorld + 2);  // plan_threads(N) + a helper warp, >= kSelThreads
 
 // Push list X_i, plan(i) -> copy(i). u32 words:

@@ -1529,6 +1529,12 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Per-round timing stamp (drb_rb_drain_timings), one thread, only when enabled.
+__device__ __forceinline__ void tstamp(const RunParams& rp, uint64_t i, uint32_t slot) {
+    if (rp.timings)
+        rp.timings[(i % kTimingRing) * kTimingWords + slot] = globaltimer();
+}
+
 // Waits on run counters keep the last value seen, so a satisfied wait costs no memory trip.
 struct SeenFlag {
     const uint64_t* f;
@@ -1630,6 +1636,9 @@ __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
             admitted = w[4] + static_cast<uint32_t>(w[5]);  // i_begin + count
             st_release_gpu(&rp.ctl->admitted, admitted);
             run_mark(rp, w[4], 13);
+            if (rp.timings)
+                for (uint64_t x = w[4]; x < admitted && x < w[4] + kTimingRing; ++x)
+                    tstamp(rp, x, 0);
             ++j;
             idle_t0 = 0;
             spin = 0;
@@ -1647,6 +1656,8 @@ __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
         const uint64_t now = globaltimer();
         if (idle_t0 == 0)
             idle_t0 = now;
+        if (rp.tool_mode)  // every post launches its own instance: nothing to hand over
+            break;
         if (*rp.quiesce == 0 && now - idle_t0 < rp.idle_ns) {
             __nanosleep(spin < 512 ? 64 : 512);
             continue;
@@ -1842,8 +1853,10 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
         if (warp == 0) {
             tl_mark(sp, 0, false);
             trace_at(sp, 0);
-            if (tid == 0)
+            if (tid == 0) {
                 run_mark(rp, i, 2);
+                tstamp(rp, i, 1);
+            }
             sel_core(sp, v, hx[5] != 0, spec_sel + 32 * (k & 1), sx[k & 1]);
             delay_exp(1);
             __syncwarp();
@@ -1851,6 +1864,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             prof_span(sp, 19, pt);
             if (tid == 0) {
                 st_release_cta(seen + 2, k + 1);  // hand sel(k) to the publisher
+                tstamp(rp, i, 2);
                 run_mark(rp, i, 3);
                 tl_mark(sp, 0, true);
             }
@@ -1951,6 +1965,8 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
         }
         tl_mark(sp, 1, false);
         trace_at(sp, 5);
+        if (tid == 0)
+            tstamp(rp, i, 3);
         plan_core(sp, v, T, 3);
         delay_exp(2);
         cta_bar(3, T);
@@ -1987,6 +2003,7 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
                                  : "memory");
         }
         st_release_gpu(&rp.ctl->b_done, i + 1);
+        tstamp(rp, i, 4);
         run_mark(rp, i, 9);
     }
 }

@@ -194,10 +194,12 @@ class rehearsal_buffer:
 
     def __init__(self, n_classes: int, per_class_cap: int, sample_bytes: int, *, max_batch: int = 64,
                  candidate_count: int = 14, rep_count: int = 7, seed: int = 1, rank: int = 0,
-                 world: int = 1, device: int = 0, aug_ring: int = 0, engine_ctas: int = 0):
+                 world: int = 1, device: int = 0, aug_ring: int = 0, engine_ctas: int = 0,
+                 record_timings: bool = False):
         cfg = _lib.drb_rb_config(n_classes=n_classes, per_class_cap=per_class_cap, sample_bytes=sample_bytes,
                                  max_batch=max_batch, candidate_count=candidate_count, rep_count=rep_count,
-                                 rank=rank, world=world, seed=seed, device=device, flags=0, aug_ring=aug_ring,
+                                 rank=rank, world=world, seed=seed, device=device,
+                                 flags=_lib.FLAG_TIMINGS if record_timings else 0, aug_ring=aug_ring,
                                  engine_ctas=engine_ctas)
         self.h = C.c_void_p()
         check(lib.drb_rb_create(C.byref(cfg), C.byref(self.h)))
@@ -472,6 +474,17 @@ class engine:
 
     def synchronize(self) -> None:
         check(lib.drb_rb_synchronize(self.buffer.h))
+
+    def drain_timings(self) -> List[dict]:
+        """engine::drain_timings (engine.hpp:93): per-round timings since the last drain
+        (device stamps; the buffer must be created with record_timings=True)."""
+        cap = 4096
+        arr = (_lib.drb_timing * cap)()
+        n = C.c_uint32(0)
+        check(lib.drb_rb_drain_timings(self.buffer.h, arr, cap, C.byref(n)))
+        return [{"iteration": int(t.iteration), "populate_ms": t.populate_ms, "augment_ms": t.augment_ms,
+                 "latency_ms": t.latency_ms, "wait_ms": t.wait_ms, "degraded": int(t.degraded)}
+                for t in arr[: n.value]]
 
     def total_wait_ms(self) -> float:
         v = C.c_double(0)

@@ -195,3 +195,32 @@ def test_split_streams_pipelined_parity(drb, ring):
         assert np.array_equal(d[:cnt].cpu().numpy(), o[0, :cnt]), i
     assert eng.device_error() == 0
     eng.shutdown()
+
+
+def test_drain_timings(drb):
+    """engine::drain_timings (engine.hpp:43-50,93): one record per completed round since the
+    last drain, from device stamps (resident engine; the three-kernel path records none)."""
+    K, cap, S, b, c, r = 10, 8, 1024, 32, 14, 8
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=2, record_timings=True)
+    eng = drb.engine(buf)
+    eng.start()
+    spec = stream_spec(K, 1, b, S, steps_per_task=10**9, seed=2)
+    for i in range(30):
+        eng.update(dev(spec.payload(0, i), spec.labels(0, i)))
+    d_ring, l_ring = dev(np.stack([spec.payload(0, 30 + k) for k in range(4)]),
+                         np.stack([spec.labels(0, 30 + k) for k in range(4)]))
+    eng.run(d_ring, l_ring, 20)
+    t = eng.drain_timings()
+    resident = eng.engine_info()["resident"]
+    if not resident:
+        assert t == []
+    else:
+        assert [x["iteration"] for x in t] == list(range(50))
+        for x in t:
+            assert x["populate_ms"] > 0 and x["augment_ms"] > 0, x
+            assert x["latency_ms"] >= x["augment_ms"], x
+            assert x["latency_ms"] < 1000 and x["wait_ms"] == 0 and x["degraded"] == 0, x
+        assert eng.drain_timings() == []
+        eng.update(dev(spec.payload(0, 60), spec.labels(0, 60)))
+        assert [x["iteration"] for x in eng.drain_timings()] == [50]
+    eng.shutdown()

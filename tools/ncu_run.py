@@ -1,0 +1,33 @@
+"""ncu target (tools/, not product): the resident engine at the c2 shape on the whole GPU —
+instance 1 is a 400-step prefill, instance 2 the measured run of argv[1] steps (capture it with
+`ncu -k regex:drb_run_kernel --launch-skip 1 -c 1`). DRB_IDLE_US defaults to 5 here so the
+instance leaves right after its last step (the idle tail is not part of the run)."""
+import os
+import sys
+
+os.environ.setdefault("DRB_IDLE_US", "5")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2406_03285_b200 as drb  # noqa: E402
+from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E402
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+K, cap, S, b, r, c = 100, 48, 150528, 56, 7, 14
+spec = stream_spec(K, 4, b, S, steps_per_task=100, seed=1)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, engine_ctas=sms)
+eng = drb.engine(buf)
+eng.start()
+data, lab = device_ring(spec, 0, 64, "cuda:0")
+s = torch.cuda.Stream()
+eng.run(data, lab, 400, stream=s)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(s)
+eng.run(data, lab, steps, stream=s)
+e1.record(s)
+torch.cuda.synchronize()
+print(f"run of {steps} steps: {e0.elapsed_time(e1) * 1000 / steps:.2f} us/step, instances {eng.engine_info()}")
+assert eng.device_error() == 0
+eng.shutdown()

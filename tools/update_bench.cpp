@@ -30,6 +30,7 @@ using namespace drb::b200;
 int main(int argc, char** argv) {
     const int steps = argc > 1 ? std::atoi(argv[1]) : 200;
     const int device = argc > 2 ? std::atoi(argv[2]) : 0;
+    const uint32_t aug_ring = argc > 3 ? uint32_t(std::atoi(argv[3])) : 0;  // 0: the default 6 slots
     CK(cudaSetDevice(device));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -47,6 +48,7 @@ int main(int argc, char** argv) {
     cfg.seed = 1;
     cfg.device = device;
     cfg.engine_ctas = uint32_t(sms);  // no training step to share the SMs with
+    cfg.aug_ring = aug_ring;          // split form: the loader runs up to aug_ring - 2 steps ahead
     rehearsal_buffer buf(cfg);
     engine eng(buf);
     eng.start();
@@ -101,8 +103,8 @@ int main(int argc, char** argv) {
     eng.shutdown();
     std::printf("{\"split_us_per_step\": %.3f, \"serial_us_per_step\": %.3f, \"split_us_per_step_20\": %.3f, "
                 "\"serial_us_per_step_20\": %.3f, \"host_us_per_call_split\": %.3f, \"host_us_per_call_serial\": %.3f, "
-                "\"steps\": %d, \"engine_ctas\": %d}\n",
-                split, serial, split20, serial20, h_split, h_serial, steps, sms);
+                "\"steps\": %d, \"engine_ctas\": %d, \"aug_ring\": %u}\n",
+                split, serial, split20, serial20, h_split, h_serial, steps, sms, aug_ring ? aug_ring : 6u);
     cudaFree(data);
     cudaFree(labels);
     return 0;
