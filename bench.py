@@ -134,6 +134,9 @@ class NvlinkCounters:
     def read(self):
         vals = self.nv.nvmlDeviceGetFieldValues(self.h, self.fields)
         tx = rx = 0
+        bad = [int(v.nvmlReturn) for v in vals if v.nvmlReturn != 0]
+        if len(bad) == len(vals):
+            raise RuntimeError(f"NVML field values unsupported (return {bad[0]})")
         for k, v in enumerate(vals):
             if v.nvmlReturn != 0:
                 continue
@@ -350,10 +353,11 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        # NVML counters before the barrier: a slow NVML query must not skew the ranks' starts
+        nvl0 = nvl.read() if (nvl.ok and N > 1) else None
         barrier()
         torch.cuda.synchronize()
         inst0 = eng.engine_info()["instances"]
-        nvl0 = nvl.read() if nvl.ok else None
         ev0.record(stream)
         if run is not None:
             run.launch(stream)
@@ -396,9 +400,9 @@ def main():
     for ks in [int(x) for x in args.sweep.split(",") if x.strip()]:
         sr = eng.prepare_run(data, lab, ks, first=0) if not args.no_graph else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0 = nvl.read() if (nvl.ok and N > 1) else None  # (before the barrier: no rank skew)
         barrier()
         torch.cuda.synchronize()
-        c0 = nvl.read() if (nvl.ok and N > 1) else None
         e0.record(stream)
         if sr is not None:
             sr.launch(stream)

@@ -1079,10 +1079,13 @@ drb_status drb_rb_shutdown(drb_rb* h) {
         device_guard g(h->cfg.device);
         rmode_quiesce(h);  // the resident instance leaves once everything posted is done
         cuda_check(cudaDeviceSynchronize(), "shutdown drain");
-        if (h->cfg.world > 1 && h->step > 0) {
+        const bool failed = reinterpret_cast<volatile uint32_t*>(h->mailbox)[kMbSticky] != 0;
+        if (h->rmode && h->cfg.world > 1 && h->step > 0 && !failed) {
             // Peers may still be pushing this rank's last reps into its m' ring (they run at
             // most a step behind): wait, bounded, for every peer's final announcement, so a
-            // drb_rb_destroy after shutdown never frees memory a peer still writes.
+            // drb_rb_destroy after shutdown never frees memory a peer still writes. (Not after
+            // a failure: a stalled peer never announces; the three-kernel path announces a
+            // step late and keeps the old contract — shut down every rank before destroying.)
             const auto* hdr = reinterpret_cast<const RegionHeader*>(h->region);
             const auto t0 = std::chrono::steady_clock::now();
             for (;;) {
@@ -1693,7 +1696,7 @@ drb_status drb_rb_drain_timings(drb_rb* h, drb_timing* out, uint32_t capacity, u
     DRB_REQUIRE(h && count && (out || capacity == 0));
     return guarded([&] {
         *count = 0;
-        if (!h->timings)
+        if (!h->timings || !h->rmode)  // (the three-kernel path records no timings)
             return;
         device_guard g(h->cfg.device);
         rmode_quiesce(h);

@@ -27,21 +27,33 @@ from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E40
 
 ctas = int(sys.argv[1]) if len(sys.argv) > 1 else 148
 mode = sys.argv[2] if len(sys.argv) > 2 else "serial"
+world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+if world > 1:
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method="env://")
 K, cap, S, b, r, c = 100, 48, 150528, 56, 7, 14
 spec = stream_spec(K, 4, b, S, steps_per_task=100, seed=1)
-buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, engine_ctas=ctas)
+buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, engine_ctas=ctas,
+                           rank=rank, world=world, device=local)
+if world > 1:
+    from paper_2406_03285_b200.dist import connect_world
+    connect_world(buf)
 eng = drb.engine(buf)
 eng.start()
-data, lab = device_ring(spec, 0, 16, "cuda:0")
+data, lab = device_ring(spec, rank, 16, f"cuda:{local}")
 s = torch.cuda.Stream()
 eng.run(data, lab, 400, stream=s)
 torch.cuda.synchronize()
 stamp = _lib.lib.drb_dbg_stamp
 stamp.argtypes = [C.c_void_p, C.c_void_p]
 N = 40 if mode == "serial" else 200
-pre = torch.zeros(N, dtype=torch.int64, device="cuda")
-post = torch.zeros(N, dtype=torch.int64, device="cuda")
+pre = torch.zeros(N, dtype=torch.int64, device=f"cuda:{local}")
+post = torch.zeros(N, dtype=torch.int64, device=f"cuda:{local}")
 first = eng.iteration
+if world > 1:
+    dist.barrier()
 if mode == "serial":
     for k in range(N):
         stamp(pre.data_ptr() + 8 * k, C.c_void_p(s.cuda_stream))
@@ -90,6 +102,7 @@ for k in range(8, N):
     rec["ready published"] = rel(cta[row, G - 1, 14])
     rows.append(rec)
 keys = list(rows[0].keys())
+print(f"== rank {rank} of {world}")
 if mode != "serial":
     tops = [cta[(first + k) % n.value, 0, 0] for k in range(8, N)]
     print(f"pipelined run: sel loop-top period {np.median(np.diff(tops)) / 1e3:.2f} us")
@@ -102,4 +115,8 @@ if mode != "serial":
 print(f"grid {G}, {len(rows)} {mode} steps; us after {'the posting stream reached update()' if mode == 'serial' else 'the sel loop top'} (median):")
 for kname in keys:
     print(f"  {kname:34s} {np.nanmedian([r_[kname] for r_ in rows]):8.2f}")
+if world > 1:
+    dist.barrier()
 eng.shutdown()
+if world > 1:
+    dist.barrier()
