@@ -560,7 +560,11 @@ def main():
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            # DRAM bytes of the dominant kernel per launch, like `achieved`: the timed launch runs
+            # K steps, the capture holds the per-step figure of a 200-step instance
+            traffic = tj["dram_bytes_per_step"] * (args.steps if resident else 1) if "dram_bytes_per_step" in tj \
+                else tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 

@@ -203,6 +203,8 @@ struct drb_rb {
     // post launches its own instance (after the post's sequence word) and instances leave as
     // soon as they are idle.
     bool tool_mode = false;
+    uint64_t released = 0;            // split steps: the last m' release written (step index)
+    uint64_t release_every = 1;       // split steps: release cadence, max(1, (R - 2) / 4)
     uint64_t* timings = nullptr;      // DRB_RB_FLAG_TIMINGS: per-round device stamps [kTimingRing][8]
     uint64_t timings_drained = 0;     // first round not yet returned by drb_rb_drain_timings
     unsigned long long* prof = nullptr;  // DRB_DBG 65536: sel/plan phase cycle accumulators [64]
@@ -327,6 +329,7 @@ void rmode_launch(drb_rb* h) {
     rp.hdesc = h->hdesc_dev;
     rp.feed_seq = h->feed_seq;
     rp.desc_done_host = reinterpret_cast<volatile unsigned long long*>(h->mailbox_dev + kMbDescDone);
+    rp.ready_host = reinterpret_cast<volatile unsigned long long*>(h->mailbox_dev + kMbReady);
     rp.ctl = h->runctl;
     rp.ver0 = h->ver0;
     rp.sel_base = h->sel;
@@ -642,6 +645,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         std::unique_ptr<drb_rb> guard_h(h);
         h->cfg = c;
         h->aug_ring = c.aug_ring ? c.aug_ring : kAugRingDefault;
+        h->release_every = std::max<uint64_t>(1, (h->aug_ring - 2) / 4);
         h->layout = region_layout(c.world, c.n_classes, c.sample_bytes, c.max_batch, c.rep_count, h->aug_ring);
         h->copy_smem = copy_smem(c.world, c.rep_count, c.max_batch).words * 4;
         {
@@ -706,6 +710,12 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         h->slab_peers[c.rank] = h->slab;
         if (const char* tl = std::getenv("DRB_TIMELINE")) {
             h->timeline_steps = uint32_t(std::strtoul(tl, nullptr, 10));
+            if (h->timeline_steps) {  // a power of two: stamps index the ring with a mask
+                uint32_t p2 = 1;
+                while (p2 < h->timeline_steps)
+                    p2 <<= 1;
+                h->timeline_steps = p2;
+            }
             if (h->timeline_steps) {
                 cuda_check(cudaMalloc(&h->timeline, h->timeline_steps * uint64_t(kTlStride) * 8), "timeline alloc");
                 std::vector<unsigned long long> init(h->timeline_steps * uint64_t(kTlStride), 0ull);
@@ -1060,9 +1070,11 @@ drb_status drb_rb_start(drb_rb* h) {
             h->posted = 0;
             h->gen = 0;
             h->alive = false;
+            h->released = h->step;
             *mb64(h, kMbHostPosted) = 0;
             *mb64(h, kMbExiting) = 0;
             *mb64(h, kMbDescDone) = 0;
+            *mb64(h, kMbReady) = h->step;
             cuda_check(cudaMemset(h->feed_seq, 0, kFeedRing * 8), "feed reset");
         }
     });
@@ -1282,31 +1294,38 @@ void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n
     const uint32_t slot = uint32_t(i % h->aug_ring);
     if (!consumer) {  // one stream: posting m_i releases every earlier m'; then wait for m'_i
         rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, i + 1);
-        cuda_check(cudaEventRecord(h->done[slot], s), "event record");
-        h->slot_run[slot] = 0;
     } else {  // producer / consumer streams: the consumer releases what it used, then waits
         rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, 0, true);
+        // the release of consumed m' every `release_every` steps (each stream memory operation
+        // costs the consumer stream time; the ring keeps aug_ring - 2 - release_every steps of
+        // run-ahead), then the wait for m'_i
+        const bool rel = i >= h->released + h->release_every;
+        if (rel)
+            h->released = i;
         if (h->feed_kernels) {
-            if (launch_feed_post(&h->runctl->consumed, i, consumer) ||
+            if ((rel && launch_feed_post(&h->runctl->consumed, i, consumer)) ||
                 launch_feed_wait(&h->runctl->ready, i + 1, consumer))
                 fail(DRB_ERR_INTERNAL, std::string("feed failed: ") + cudaGetErrorString(cudaGetLastError()));
         } else {
             CUstreamBatchMemOpParams ops[2];
             std::memset(ops, 0, sizeof ops);
-            ops[0].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
-            ops[0].writeValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->consumed);
-            ops[0].writeValue.value64 = i;  // m'_0 .. m'_{i-1}: everything the consumer was handed
-            ops[0].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-            ops[1].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
-            ops[1].waitValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->ready);
-            ops[1].waitValue.value64 = i + 1;
-            ops[1].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
-            const CUresult r = memops().batch(reinterpret_cast<CUstream>(consumer), 2, ops, 0);
+            uint32_t nop = 0;
+            if (rel) {
+                ops[nop].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+                ops[nop].writeValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->consumed);
+                ops[nop].writeValue.value64 = i;  // m'_0 .. m'_{i-1}: everything the consumer was handed
+                ops[nop].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+                ++nop;
+            }
+            ops[nop].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+            ops[nop].waitValue.address = reinterpret_cast<CUdeviceptr>(&h->runctl->ready);
+            ops[nop].waitValue.value64 = i + 1;
+            ops[nop].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+            ++nop;
+            const CUresult r = memops().batch(reinterpret_cast<CUstream>(consumer), nop, ops, 0);
             if (r != CUDA_SUCCESS)
                 fail(DRB_ERR_INTERNAL, "consumer wait: cuStreamBatchMemOp failed (" + std::to_string(int(r)) + ")");
         }
-        cuda_check(cudaEventRecord(h->done[slot], consumer), "event record");
-        h->slot_run[slot] = 0;
     }
     const uint32_t row0 = c.max_batch - n;
     out->n = n;
@@ -1598,6 +1617,8 @@ drb_status drb_rb_step_host(drb_rb* h, const void* batch, const uint32_t* labels
         const drb_status st = drb_rb_step(h, st_b, st_l, n, h->stream, &aug);
         if (st != DRB_OK)
             fail(st, t_last_error);
+        if (h->rmode)  // (the resident step records no event: the copy-out orders behind this one)
+            cuda_check(cudaEventRecord(h->done[aug.ring_slot], h->stream), "event record");
         cuda_check(cudaEventRecord(h->in_free[si], h->stream), "event");
         cuda_check(cudaStreamWaitEvent(h->d2h, h->done[aug.ring_slot], 0), "wait");
         // in place: the caller's batch rows already are m'_i's first n rows; only the
@@ -1643,14 +1664,24 @@ drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count) {
     return guarded([&] {
         device_guard g(h->cfg.device);
         const auto t0 = std::chrono::steady_clock::now();
-        cuda_check(cudaEventSynchronize(h->slot_run[aug->ring_slot] ? h->run_done : h->done[aug->ring_slot]),
-                   "aug wait");
+        if (h->rmode) {  // the ready publisher mirrors `ready` into host memory: no event per step
+            while (*mb64(h, kMbReady) < aug->step + 1) {
+                if (reinterpret_cast<volatile uint32_t*>(h->mailbox)[kMbSticky])
+                    break;
+                std::this_thread::yield();
+            }
+        } else {
+            cuda_check(cudaEventSynchronize(h->slot_run[aug->ring_slot] ? h->run_done : h->done[aug->ring_slot]),
+                       "aug wait");
+        }
         h->wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         const volatile uint32_t* mb = h->mailbox;
         const uint32_t e = mb[mb_err(aug->ring_slot, h->aug_ring)];
         *count = mb[mb_count(aug->ring_slot)];
         if (e)
             fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(e));
+        if (h->rmode && *mb64(h, kMbReady) < aug->step + 1)  // (the sticky error ended the wait)
+            fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(mb[kMbSticky]));
     });
 }
 
@@ -1681,6 +1712,9 @@ drb_status drb_rb_synchronize(drb_rb* h) {
                 }
             }
         }
+        if (h->rmode)  // every posted step's m' ready (the streams that posted them progressed)
+            while (*mb64(h, kMbReady) < h->step && !reinterpret_cast<volatile uint32_t*>(h->mailbox)[kMbSticky])
+                std::this_thread::yield();
         cuda_check(cudaStreamSynchronize(h->stream), "sync");
         cuda_check(cudaStreamSynchronize(h->s_sel), "sync");
         cuda_check(cudaStreamSynchronize(h->s_plan), "sync");

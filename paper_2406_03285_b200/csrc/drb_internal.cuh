@@ -210,7 +210,7 @@ constexpr uint64_t kReadyFailed = 1ull << 62;  // ready after a failure: release
 // Host-mapped control words of the resident engine (u32 index into the mailbox; u64 words
 // take two): the host's posted-descriptor count, the leaving instance's announcement, the
 // host's request to leave as soon as idle.
-constexpr uint32_t kMbHostPosted = 2, kMbExiting = 4, kMbQuiesce = 6, kMbDescDone = 8;
+constexpr uint32_t kMbHostPosted = 2, kMbExiting = 4, kMbQuiesce = 6, kMbDescDone = 8, kMbReady = 10;
 
 struct RunParams {
     StepParams base;  // per-iteration fields patched on device (run_patch)
@@ -218,6 +218,7 @@ struct RunParams {
     const FeedDesc* hdesc;               // [kFeedRing] mapped host ring (written by the host)
     const uint64_t* feed_seq;            // [kFeedRing] device: j + 1 once descriptor j is posted
     volatile unsigned long long* desc_done_host;  // mapped mirror of RunCtl::desc_done
+    volatile unsigned long long* ready_host;      // mapped mirror of RunCtl::ready (host-side waits)
     RunCtl* ctl;
     uint64_t ver0;
     SelState* sel_base;

@@ -90,6 +90,9 @@ __device__ __forceinline__ uint32_t mod_small(uint64_t v, uint32_t d) {
     const uint32_t hi = static_cast<uint32_t>(v >> 32) % d, lo = static_cast<uint32_t>(v) % d;
     return ((hi * c) % d + lo) % d;
 }
+// i mod R for the m' ring (R <= 2^16) in 32-bit arithmetic: no 64-bit division routine on the
+// per-step paths
+__device__ __forceinline__ uint32_t ring_slot(uint64_t i, uint32_t R) { return mod_small(i, R); }
 __device__ __forceinline__ uint32_t thr_small(uint32_t d) {  // 2^64 mod d = (2^32 mod d)^2 mod d
     const uint32_t c = (0u - d) % d;
     return (c * c) % d;
@@ -394,7 +397,7 @@ __device__ __forceinline__ V ld_vec(const V* p) {
 __device__ __forceinline__ void tl_mark(const StepParams& p, int kind, bool end) {
 #if DRB_INSTRUMENT
     if (p.timeline && threadIdx.x == 0) {
-        unsigned long long* e = p.timeline + (p.step % p.timeline_steps) * kTlStride + 2 * kind;
+        unsigned long long* e = p.timeline + (p.step & (p.timeline_steps - 1)) * kTlStride + 2 * kind;
         if (end)
             atomicMax(e + 1, globaltimer());
         else
@@ -409,7 +412,7 @@ __device__ __forceinline__ void cta_mark(const StepParams& p, int slot) {
     if (p.timeline && blockIdx.x < kTlMaxCtas) {
         uint64_t t;  // "memory": not reordered with the surrounding loads / stores
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
-        p.timeline[(p.step % p.timeline_steps) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = t;
+        p.timeline[(p.step & (p.timeline_steps - 1)) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = t;
     }
 #endif
 }
@@ -444,7 +447,7 @@ __device__ __forceinline__ void trace_at(const StepParams& p, int slot) {
         if (p.trace)
             p.trace[slot] = globaltimer();
         if (p.timeline)  // phase stamps of the pipelined run: slots 8.. of the step's record
-            p.timeline[(p.step % p.timeline_steps) * kTlStride + 8 + slot] = globaltimer();
+            p.timeline[(p.step & (p.timeline_steps - 1)) * kTlStride + 8 + slot] = globaltimer();
     }
 #endif
 }
@@ -1505,7 +1508,7 @@ __device__ void run_patch(StepParams& p, const RunParams& rp, uint64_t i) {
     p.plan_out = rp.plan_base + ((rp.plan_par0 + i + 1) & 1);
     p.step = i;
     p.seq = i;
-    p.aslot = static_cast<uint32_t>(i % p.aug_ring);
+    p.aslot = ring_slot(i, p.aug_ring);
     p.plist_in = rp.plist_base + (i % kListRing) * rp.pw;
     p.plist_out = const_cast<uint32_t*>(p.plist_in);
     p.wlist = rp.wlist_base + (i % kListRing) * rp.ww;
@@ -1521,7 +1524,7 @@ __device__ __forceinline__ void run_mark(const RunParams& rp, uint64_t i, int sl
 #if DRB_INSTRUMENT
     const StepParams& p = rp.base;
     if (p.timeline && blockIdx.x < kTlMaxCtas)
-        p.timeline[(i % p.timeline_steps) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = globaltimer();
+        p.timeline[(i & (p.timeline_steps - 1)) * kTlStride + 32 + blockIdx.x * kTlCtaSlots + slot] = globaltimer();
 #endif
 }
 
@@ -1704,11 +1707,12 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
                 volatile uint32_t* mb = b.mailbox;
                 const uint32_t err = *reinterpret_cast<volatile const uint32_t*>(&rp.ctl->error);
                 for (uint64_t x = i; x < adm && x < i + b.aug_ring; ++x)
-                    mb[mb_err(static_cast<uint32_t>(x % b.aug_ring), b.aug_ring)] = err ? err : DRB_ERR_INTERNAL;
+                    mb[mb_err(ring_slot(x, b.aug_ring), b.aug_ring)] = err ? err : DRB_ERR_INTERNAL;
             }
             break;
         }
         st_release_sys(&rp.ctl->ready, i + 1);
+        *rp.ready_host = i + 1;  // (after the system-scope release: the host sees m'_i complete)
         run_mark(rp, i, 14);
         cursor_seek(c, rp, i);
         if (i + 1 == c.ib + c.cnt) {  // the last step of its descriptor: the slot is free
@@ -1716,8 +1720,10 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
             *rp.desc_done_host = c.j + 1;  // the host reuses ring slots behind this
         }
     }
-    if (run_failed(rp))  // release every stream still waiting for an m' of this engine
+    if (run_failed(rp)) {  // release every stream (and host) still waiting for an m' of this engine
         st_release_sys(&rp.ctl->ready, kReadyFailed);
+        *rp.ready_host = kReadyFailed;
+    }
 }
 
 // CTA 0: the sel chain. Warp 0 runs sel(i), warp 2 draws round i+1's selection ahead,
@@ -2377,7 +2383,7 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                 n = __shfl_sync(kFull, n, 0);
                 const uint32_t* lab = reinterpret_cast<const uint32_t*>(lp);
                 const uint32_t row0 = b.nmax - n;
-                const uint32_t aslot = static_cast<uint32_t>(i % b.aug_ring);
+                const uint32_t aslot = ring_slot(i, b.aug_ring);
                 uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
                                uint64_t(aslot) * b.auglab_slot_elems;
                 uint32_t nrep = 0;
@@ -2444,7 +2450,8 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         const uint64_t a16 = (uint64_t(n) * S) >> 4;
         const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
         const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
-        uint8_t* dst = b.region[b.me] + b.off_aug + (i % b.aug_ring) * b.aug_slot_bytes + uint64_t(b.nmax - n) * S;
+        uint8_t* dst = b.region[b.me] + b.off_aug + uint64_t(ring_slot(i, b.aug_ring)) * b.aug_slot_bytes +
+                       uint64_t(b.nmax - n) * S;
         for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
             const uint32_t w1 = min(nA, w0 + kTmaStagesA);
             bulk_wait_read_all();  // the ring's previous window has been stored
