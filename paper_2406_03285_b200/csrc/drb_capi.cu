@@ -162,7 +162,7 @@ struct drb_rb {
     uint32_t* wlist = nullptr;        // [kListRing][wlist_words]: W_i, sel(i) -> copy(i)
     uint32_t* mailbox = nullptr;      // host-mapped, mb_words(R) (drb_internal.cuh)
     uint32_t* mailbox_dev = nullptr;
-    static constexpr int kEv = 16;  // >= kListRing + 1: per-iteration events in flight
+    static constexpr int kEv = 40;  // > kListRing (and > the multi-rank lag): per-iteration events in flight
     cudaEvent_t ev_user[kEv] = {}, ev_sel[kEv] = {}, ev_plan[kEv] = {}, ev_copy[kEv] = {};
     cudaEvent_t rel[kEv] = {};  // split steps: the consumer's release at each call
     uint32_t aug_ring = kAugRingDefault;  // R: m' ring depth
@@ -203,6 +203,7 @@ struct drb_rb {
     // post launches its own instance (after the post's sequence word) and instances leave as
     // soon as they are idle.
     bool tool_mode = false;
+    uint32_t a_ahead = 4;             // A's run-ahead over the completed B (DRB_A_AHEAD)
     uint64_t released = 0;            // split steps: the last m' release written (step index)
     uint64_t release_every = 1;       // split steps: release cadence, max(1, (R - 2) / 4)
     uint64_t* timings = nullptr;      // DRB_RB_FLAG_TIMINGS: per-round device stamps [kTimingRing][8]
@@ -349,6 +350,7 @@ void rmode_launch(drb_rb* h) {
     rp.feeder_cta = h->feeder_last ? h->run_grid - 1 : 0;
     rp.timings = h->timings;
     rp.tool_mode = h->tool_mode ? 1u : 0u;
+    rp.a_ahead = h->a_ahead;
     if (launch_run(rp, h->run_grid, h->s_run))
         fail(DRB_ERR_INTERNAL, std::string("resident engine launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     h->gen = rp.gen;
@@ -633,8 +635,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: max_batch must be in [1, 4096]");
         if (c.rep_count > 4096 || uint64_t(c.world) * c.rep_count > 4096)
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: world * rep_count must be <= 4096");
-        if (c.aug_ring != 0 && (c.aug_ring < kAugRingDefault || c.aug_ring > kAugRingMax))
-            fail(DRB_ERR_CONFIG, "rehearsal_buffer: aug_ring must be 0 (default 6) or in [6, 65536]");
+        if (c.aug_ring != 0 && (c.aug_ring < kAugRingMin || c.aug_ring > kAugRingMax))
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: aug_ring must be 0 (default 16) or in [6, 65536]");
         if (uint64_t(c.world) * c.n_classes * c.per_class_cap >= (1ull << 31))
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K*cap must be < 2^31 slots");
         const uint32_t plan_bytes = plan_smem_bytes(c.world, c.n_classes, c.rep_count);
@@ -754,6 +756,8 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         if (std::getenv("CUDA_INJECTION64_PATH") || (std::getenv("DRB_TOOL_MODE") &&
                                                      std::getenv("DRB_TOOL_MODE")[0] == '1'))
             h->tool_mode = true;
+        if (const char* aa = std::getenv("DRB_A_AHEAD"))
+            h->a_ahead = std::max(2u, uint32_t(std::strtoul(aa, nullptr, 10)));
         if (const char* fl = std::getenv("DRB_FEEDER_LAST"))
             h->feeder_last = fl[0] != '0';
         if (const char* fk = std::getenv("DRB_FEED"); fk && std::string(fk) == "kernel")

@@ -12,8 +12,8 @@
 namespace drb_b200 {
 
 constexpr int kMaxWorld = DRB_RB_MAX_WORLD;
-constexpr int kTableRing = 6;  // occupancy-row versions kept per rank (v % 6); see DESIGN.md §4
-constexpr int kListRing = 8;   // W_i / X_i slots: sel and plan may run up to 8 iterations ahead
+constexpr int kTableRing = 16;  // occupancy-row versions kept per rank (v % 16); see DESIGN.md §3
+constexpr int kListRing = 32;  // W_i / X_i slots: sel and plan may run up to 32 iterations ahead of B
 // sel and plan reserve at least this much dynamic shared memory, so neither is ever resident
 // next to a copy CTA: they are latency-bound single-CTA kernels and, next to a copy CTA,
 // their shared/global instructions queue behind the copy's memory traffic. The copy grid
@@ -27,10 +27,12 @@ constexpr uint32_t kCtaReserved = 1024u;        // per-CTA system reservation
 // CTA 0, then kTlCtaSlots stamps for each of up to kTlMaxCtas copy CTAs.
 constexpr uint32_t kTlCtaSlots = 16, kTlMaxCtas = 160;
 constexpr uint32_t kTlStride = 32 + kTlCtaSlots * kTlMaxCtas;
-// m' buffers per rank (drb_rb_config.aug_ring, default 6). The API promises m'_i until step
+// m' buffers per rank (drb_rb_config.aug_ring, default 16). The API promises m'_i until step
 // i+2 is enqueued; the slot is reused by step i+R (batch rows) and by the pushes of
 // reps(i+R-1). A deep ring (R >= the steps of a run) keeps every m' of the run readable.
-constexpr uint32_t kAugRingDefault = 6;
+constexpr uint32_t kAugRingDefault = 16;
+constexpr uint32_t kAugRingMin = 6;
+constexpr uint32_t kTicketRing = 32;  // copy-CTA arrivals per iteration slot (CTAs drift < kListRing)
 constexpr uint32_t kAugRingMax = 1u << 16;
 // Host-mapped mailbox (u32 words): [0] sticky engine error, [1, 64) control words,
 // [64, 64+R) rows of m' per ring slot, [64+R, 64+2R) per-slot round errors.
@@ -202,7 +204,7 @@ struct alignas(64) RunCtl {
     uint32_t error;      // sticky: a wait timed out or a round failed -> every role leaves
     uint32_t where;      // diagnostics: the wait that failed first (site << 24 | k)
     uint32_t pad[2];
-    uint32_t ticket[8];  // copy-CTA arrivals of iteration k in slot k % 8 (CTAs drift < 8 iterations)
+    uint32_t ticket[kTicketRing];  // copy-CTA arrivals of iteration k in slot k % 32 (drift < kListRing)
 };
 constexpr uint64_t kStopMask = (1ull << 40) - 1;
 constexpr uint64_t kReadyFailed = 1ull << 62;  // ready after a failure: releases every stream wait
@@ -234,7 +236,7 @@ struct RunParams {
     uint32_t feeder_cta;  // CTA whose warps 4 and 5 run the feeder and the ready publisher
     uint64_t* timings;    // DRB_RB_FLAG_TIMINGS: [kTimingRing][kTimingWords] globaltimer stamps, else null
     uint32_t tool_mode;   // under a tool that serialises the device: one instance per post, leave when idle
-    uint32_t pad2;
+    uint32_t a_ahead;     // A(i) runs at most this many iterations ahead of the completed B
 };
 // Per-round stamps (drb_rb_drain_timings): [0] admitted, [1] sel start, [2] sel handed over,
 // [3] plan start, [4] pushes complete (b_done)

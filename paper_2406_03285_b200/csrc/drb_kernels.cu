@@ -1389,7 +1389,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) drb_copy_tma_kernel(const __gr
 //   sel(i)   waits B(i-8) (W slot), plan(i-4) (table slot); multi-rank B(i-6) of every rank
 //            (the pushes into the m' slot that plan(i)'s requesters refill)
 //   plan(i)  waits sel(i), B(i-8) (X slot), peers' occupancy rows v=i+1
-//   A(i)     (batch -> m'_i) waits B(i-3) (bounded run-ahead)
+//   A(i)     (batch -> m'_i) waits B(i-R+1) (its ring slot's previous m' is complete)
 //   B(i)     (W_i writes, X_i pushes, by byte column) waits sel(i), plan(i) only
 //   ready(i) (m'_i complete: the consumer's stream wait) = A(i), B(i) on every copy CTA and,
 //            multi-rank, every peer's B(i-1) (its pushes of reps(i-1) into m'_i)
@@ -1814,7 +1814,8 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                 feed_patch(sp, cur, i);
                 hx[0] = sp.n;
                 // W slot (i-8) / m' slot (multi, i-6) / table slot (plan(i-4)) free
-                const uint64_t wb = i0 + back(k, multi ? lag - 1 : kListRing - 1), wp = i0 + back(k, 3);
+                // W slot: B(i-32) complete (multi-rank: the m' / table lag); table slot: plan(i-15)
+                const uint64_t wb = i0 + back(k, multi ? lag - 1 : kListRing - 1), wp = i0 + back(k, kTableRing - 2);
                 if (seen[0] < wb)
                     ok = run_wait(&rp.ctl->b_done, wb, rp, false);
                 if (ok && seen[1] < wp)
@@ -1954,7 +1955,7 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
                 run_patch(sp, rp, i);
                 if (seen[0] < i + 1)  // sel(i)
                     ok = run_wait(&rp.ctl->sel_done, i + 1, rp, false);
-                if (ok && seen[1] < i0 + back(k, kListRing - 1))  // X slot: B(i-8) complete
+                if (ok && seen[1] < i0 + back(k, kListRing - 1))  // X slot: B(i-32) complete
                     ok = run_wait(&rp.ctl->b_done, i0 + back(k, kListRing - 1), rp, false);
             }
             run_mark(rp, i, 1);
@@ -1989,14 +1990,14 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
 // i+1 once b_done = i (in order) and, multi-rank, pushdone = i+1 at every peer.
 __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t k, uint64_t i, bool multi) {
     asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk stores, for generic-proxy readers
-    uint32_t* t = &rp.ctl->ticket[k & 7];
+    uint32_t* t = &rp.ctl->ticket[k % kTicketRing];
     uint32_t old;
     // acq_rel at GPU scope: the last arrival observes every arrival's (completed) stores, local
     // and remote; its one system-scope fence below makes them all visible to the peers before
     // the pushdone words (cumulativity), so no arrival pays a system-scope atomic
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
     if (old + 1 == rp.copy_ctas) {
-        *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+8
+        *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+32
         if (!run_wait(&rp.ctl->b_done, i, rp, false))
             return;
         if (multi) {
@@ -2436,12 +2437,16 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
     uint64_t adm = 0;
     FeedCursor cur;
     cursor_init(cur, i0, j0);
+    // A(i) writes m'_i's batch rows into the ring slot m'_{i-R} held: that m' was complete (its
+    // pushes, B(i-R-1), done) and released (admission), so A could run R-2 iterations ahead of
+    // B; DRB_A_AHEAD (default 4) bounds it: A's streaming traffic far ahead delays B's loads
+    const uint32_t ahead = min(b.aug_ring - 2, rp.a_ahead);
 #pragma unroll 1
     for (uint64_t k = 0;; ++k) {
         const uint64_t i = i0 + k;
         if (!wait_admit(rp, adm, i))
             break;
-        if (!wait_seen(bdone, i0 + back(k, 2), rp))
+        if (!wait_seen(bdone, i0 + back(k, ahead), rp))
             break;
         run_mark(rp, i, 2);
         cursor_seek(cur, rp, i);

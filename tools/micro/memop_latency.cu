@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
@@ -52,6 +53,44 @@ int main(int argc, char** argv) {
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
     printf("memop ping-pong: %.2f us per round trip (%d)\n", 1000.0 * ms / n, n);
 
+    // 3. back-to-back stream memory operations on one stream (no kernel involved): GPU time per op
+    {
+        typedef CUresult (*bt_t)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+        bt_t bt = nullptr;
+        CK(cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", (void**)&bt, 12000, cudaEnableDefault, &q));
+        const int m = 2000;
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(e0, s));
+        for (int i = 1; i <= m; ++i)
+            wr(s, (CUdeviceptr)flag, i, 0);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        printf("writeValue64 back to back: %.3f us per op\n", 1000.0 * ms / m);
+        CK(cudaEventRecord(e0, s));
+        for (int i = 1; i <= m; ++i)
+            wt(s, (CUdeviceptr)flag, 1, CU_STREAM_WAIT_VALUE_GEQ);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        printf("waitValue64 (already satisfied) back to back: %.3f us per op\n", 1000.0 * ms / m);
+        CUstreamBatchMemOpParams op[2];
+        memset(op, 0, sizeof op);
+        op[0].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+        op[0].writeValue.address = (CUdeviceptr)ack;
+        op[0].writeValue.value64 = 7;
+        op[1].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+        op[1].waitValue.address = (CUdeviceptr)flag;
+        op[1].waitValue.value64 = 1;
+        op[1].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+        CK(cudaEventRecord(e0, s));
+        for (int i = 1; i <= m; ++i)
+            bt(s, 2, op, 0);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        printf("batch [write, satisfied wait] back to back: %.3f us per batch\n", 1000.0 * ms / m);
+    }
     int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     CK(cudaFuncSetAttribute(empty_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (int G : {76, 148}) {

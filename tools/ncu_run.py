@@ -16,7 +16,9 @@ steps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 K, cap, S, b, r, c = 100, 48, 150528, 56, 7, 14
 spec = stream_spec(K, 4, b, S, steps_per_task=100, seed=1)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, engine_ctas=sms)
+ring = int(os.environ.get("AUG_RING", "0"))
+buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=1, engine_ctas=sms,
+                           aug_ring=ring)
 eng = drb.engine(buf)
 eng.start()
 data, lab = device_ring(spec, 0, 64, "cuda:0")
@@ -28,6 +30,7 @@ e0.record(s)
 eng.run(data, lab, steps, stream=s)
 e1.record(s)
 torch.cuda.synchronize()
-print(f"run of {steps} steps: {e0.elapsed_time(e1) * 1000 / steps:.2f} us/step, instances {eng.engine_info()}")
+print(f"run of {steps} steps (aug_ring {ring or 16}, A ahead {os.environ.get('DRB_A_AHEAD', 4)}): "
+      f"{e0.elapsed_time(e1) * 1000 / steps:.2f} us/step, instances {eng.engine_info()}")
 assert eng.device_error() == 0
 eng.shutdown()
