@@ -1603,28 +1603,40 @@ __device__ void run_publisher(const RunParams& rp, uint64_t i0, volatile unsigne
 
 // The feeder (one lane): admits posted descriptors in order, and ends the instance when idle.
 __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
+    // The whole warp runs this loop in lockstep (every value below is warp-uniform); lane 0
+    // does the control loads and stores, lanes 0-3 fetch the descriptor.
+    const uint32_t lane = threadIdx.x & 31;
     uint64_t j = j0, admitted = i0, idle_t0 = 0;
     uint64_t released = i0;  // m' below this are released by implicit (single-stream) posts
     bool failed = false;
     const uint32_t R = rp.base.aug_ring;
 #pragma unroll 1
     for (uint32_t spin = 0;; ++spin) {
-        if (ld_acquire_sys(rp.feed_seq + (j % kFeedRing)) == j + 1) {  // posted (stream order)
-            // the descriptor itself: four 16-byte loads from mapped host memory, in flight
-            // together, then the device mirror the roles read
+        uint32_t posted = 0;
+        if (lane == 0)
+            posted = ld_acquire_sys(rp.feed_seq + (j % kFeedRing)) == j + 1;  // posted (stream order)
+        if (__shfl_sync(kFull, posted, 0)) {
+            // the descriptor itself from mapped host memory: four 16-byte reads on four lanes,
+            // in flight together (one PCIe round trip), then the device mirror the roles read
             const uint64_t* hs = reinterpret_cast<const uint64_t*>(rp.hdesc + (j % kFeedRing));
+            uint64_t lo = 0, hi = 0;
+            if (lane < kFeedDescWords / 2)
+                asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(hs + 2 * lane)
+                             : "memory");
             uint64_t w[kFeedDescWords];
 #pragma unroll
-            for (uint32_t x = 0; x < kFeedDescWords; x += 2)
-                asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];"
-                             : "=l"(w[x]), "=l"(w[x + 1])
-                             : "l"(hs + x)
-                             : "memory");
+            for (uint32_t x = 0; x < kFeedDescWords / 2; ++x) {
+                w[2 * x] = __shfl_sync(kFull, lo, x);
+                w[2 * x + 1] = __shfl_sync(kFull, hi, x);
+            }
             if (w[5] & kDescSplit) {
                 // plan(i)/B(i) refill m'_{i+1}'s slot, last handed out as m'_{i+1-R}: its
                 // consumer (another stream) must have released it
                 const uint64_t need = w[4] + 2 >= R ? w[4] + 2 - R : 0;
-                if (released < need && ld_acquire_sys(&rp.ctl->consumed) < need) {
+                uint32_t blocked = 0;
+                if (lane == 0)
+                    blocked = released < need && ld_acquire_sys(&rp.ctl->consumed) < need;
+                if (__shfl_sync(kFull, blocked, 0)) {
                     idle_t0 = 0;  // posted work is waiting: not idle
                     __nanosleep(128);
                     continue;
@@ -1632,57 +1644,68 @@ __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
             } else if (w[4] > released) {
                 released = w[4];
             }
-            uint64_t* dd = reinterpret_cast<uint64_t*>(rp.feed + (j % kFeedRing));
-#pragma unroll
-            for (uint32_t x = 0; x < kFeedDescWords; ++x)
-                dd[x] = w[x];
             admitted = w[4] + static_cast<uint32_t>(w[5]);  // i_begin + count
-            st_release_gpu(&rp.ctl->admitted, admitted);
-            run_mark(rp, w[4], 13);
-            if (rp.timings)
-                for (uint64_t x = w[4]; x < admitted && x < w[4] + kTimingRing; ++x)
-                    tstamp(rp, x, 0);
+            if (lane == 0) {
+                uint64_t* dd = reinterpret_cast<uint64_t*>(rp.feed + (j % kFeedRing));
+#pragma unroll
+                for (uint32_t x = 0; x < kFeedDescWords; ++x)
+                    dd[x] = w[x];
+                st_release_gpu(&rp.ctl->admitted, admitted);
+                run_mark(rp, w[4], 13);
+                if (rp.timings)
+                    for (uint64_t x = w[4]; x < admitted && x < w[4] + kTimingRing; ++x)
+                        tstamp(rp, x, 0);
+            }
             ++j;
             idle_t0 = 0;
             spin = 0;
             continue;
         }
-        if (run_failed(rp)) {
+        uint32_t act = 0;  // 0: keep polling, 1: failed, 2: leave
+        if (lane == 0) {
+            if (run_failed(rp)) {
+                act = 1;
+            } else if (ld_acquire_gpu(&rp.ctl->ready) < admitted) {  // work in flight: not idle
+                idle_t0 = 0;
+            } else {
+                const uint64_t now = globaltimer();
+                if (idle_t0 == 0)
+                    idle_t0 = now;
+                if (rp.tool_mode) {  // every post launches its own instance: nothing to hand over
+                    act = 2;
+                } else if (*rp.quiesce != 0 || now - idle_t0 >= rp.idle_ns) {
+                    // Leave. Announce it in host memory first, then look for a post already on
+                    // its way (the host raises host_posted before it enqueues the descriptor's
+                    // memory operations, then reads `exiting`): of the two, at least one sees
+                    // the other, so either this instance stays or the host launches the next
+                    // one behind it.
+                    *rp.exiting = (rp.gen << 32) | (j + 1);
+                    asm volatile("fence.sc.sys;" ::: "memory");
+                    if (*rp.host_posted > j) {
+                        *rp.exiting = 0;  // stay (a relaunch the host may already have queued finds no work)
+                        idle_t0 = 0;
+                    } else {
+                        act = 2;
+                    }
+                }
+            }
+        }
+        act = __shfl_sync(kFull, act, 0);
+        if (act == 1) {
             failed = true;
             break;
         }
-        if (ld_acquire_gpu(&rp.ctl->ready) < admitted) {  // work in flight: not idle
-            idle_t0 = 0;
-            __nanosleep(64);
-            continue;
-        }
-        const uint64_t now = globaltimer();
-        if (idle_t0 == 0)
-            idle_t0 = now;
-        if (rp.tool_mode)  // every post launches its own instance: nothing to hand over
+        if (act == 2)
             break;
-        if (*rp.quiesce == 0 && now - idle_t0 < rp.idle_ns) {
-            __nanosleep(spin < 512 ? 64 : 512);
-            continue;
-        }
-        // Leave. Announce it in host memory first, then look for a post already on its way
-        // (the host raises host_posted before it enqueues the descriptor's memory
-        // operations, then reads `exiting`): of the two, at least one sees the other, so
-        // either this instance stays or the host launches the next one behind it.
-        *rp.exiting = (rp.gen << 32) | (j + 1);
-        asm volatile("fence.sc.sys;" ::: "memory");
-        if (*rp.host_posted > j) {
-            *rp.exiting = 0;  // stay (a relaunch the host may already have queued finds no work)
-            idle_t0 = 0;
-            continue;
-        }
-        break;
+        __nanosleep(spin < 512 ? 64 : 512);
     }
-    if (!failed) {
-        rp.ctl->next_step[(rp.gen + 1) & 1] = admitted;
-        rp.ctl->next_desc[(rp.gen + 1) & 1] = j;
+    if (lane == 0) {
+        if (!failed) {
+            rp.ctl->next_step[(rp.gen + 1) & 1] = admitted;
+            rp.ctl->next_desc[(rp.gen + 1) & 1] = j;
+        }
+        st_release_gpu(&rp.ctl->stop_at, ((rp.gen & 0xffffffu) << 40) | admitted);
     }
-    st_release_gpu(&rp.ctl->stop_at, ((rp.gen & 0xffffffu) << 40) | admitted);
 }
 
 // CTA 0 warp 5: ready(i) — m'_i complete — in order, for the consumers' stream waits.
@@ -1733,8 +1756,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                              uint64_t j0) {
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     if (warp == 4 && rp.feeder_cta == 0) {
-        if ((tid & 31) == 0)
-            run_feeder(rp, i0, j0);
+        run_feeder(rp, i0, j0);  // (the whole warp)
         return;
     }
     if (warp == 5 && rp.feeder_cta == 0) {
@@ -2300,10 +2322,10 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
 __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2, uint64_t i0, uint64_t j0) {
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp >= 4) {  // the feeder and the ready publisher, when they live on this copy CTA
-        if (blockIdx.x == rp.feeder_cta && lane == 0) {
+        if (blockIdx.x == rp.feeder_cta) {
             if (warp == 4)
-                run_feeder(rp, i0, j0);
-            else if (warp == 5)
+                run_feeder(rp, i0, j0);  // (the whole warp)
+            else if (warp == 5 && lane == 0)
                 run_ready(rp, i0, j0);
         }
         return;

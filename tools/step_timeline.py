@@ -59,6 +59,10 @@ if mode == "serial":
         stamp(pre.data_ptr() + 8 * k, C.c_void_p(s.cuda_stream))
         eng.update((data[k % 16], lab[k % 16]), stream=s)
         stamp(post.data_ptr() + 8 * k, C.c_void_p(s.cuda_stream))
+elif mode == "split":  # update(m, loader, trainer) back to back (the pipelined trainer form)
+    loader = torch.cuda.Stream()
+    for k in range(N):
+        eng.update((data[k % 16], lab[k % 16]), stream=loader, consumer=s)
 else:  # one run of N pipelined steps: stamps relative to each step's admission
     eng.run(data, lab, N, stream=s)
 torch.cuda.synchronize()
@@ -105,6 +109,9 @@ keys = list(rows[0].keys())
 print(f"== rank {rank} of {world}")
 if mode != "serial":
     tops = [cta[(first + k) % n.value, 0, 0] for k in range(8, N)]
+    adm = [cta[(first + k) % n.value, G - 1, 13] for k in range(8, N)]
+    rdy = [cta[(first + k) % n.value, G - 1, 14] for k in range(8, N)]
+    print(f"feeder admission period {np.median(np.diff(adm)) / 1e3:.2f} us; ready period {np.median(np.diff(rdy)) / 1e3:.2f} us")
     print(f"pipelined run: sel loop-top period {np.median(np.diff(tops)) / 1e3:.2f} us")
     for nm, sl, cc in (("plan top", 0, 1), ("B start", 0, None), ("arrival", 8, None)):
         if cc is not None:
