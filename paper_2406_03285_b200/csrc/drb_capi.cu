@@ -376,7 +376,7 @@ void rmode_wait(drb_rb* h, uint64_t end, cudaStream_t s) {
 // wait_end, waits until m'_{wait_end-1} is ready): one stream memory-operation batch.
 void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
                 uint64_t label_stride, uint32_t ring, uint32_t first, uint32_t n, uint64_t i_begin, uint32_t count,
-                cudaStream_t s, uint64_t wait_end = 0, bool split = false) {
+                cudaStream_t s, uint64_t wait_end = 0, bool split = false, bool early = false) {
     const uint64_t j = h->posted;
     if (j >= kFeedRing) {  // ring slot j % kFeedRing: descriptor j - kFeedRing must be consumed
         const uint64_t need = j - kFeedRing + 1;
@@ -395,7 +395,7 @@ void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const 
     d.batch_stride = batch_stride;
     d.label_stride = label_stride;
     d.i_begin = i_begin;
-    d.count_n = uint64_t(count) | (uint64_t(n) << 32) | (split ? kDescSplit : 0ull);
+    d.count_n = uint64_t(count) | (uint64_t(n) << 32) | (split ? kDescSplit : 0ull) | (early ? kDescEarly : 0ull);
     d.ring_first = uint64_t(ring) | (uint64_t(first) << 32);
     d.seq = j + 1;
     *reinterpret_cast<volatile uint32_t*>(h->mailbox + kMbQuiesce) = 0;
@@ -1067,7 +1067,7 @@ drb_status drb_rb_start(drb_rb* h) {
         if (h->rmode) {
             device_guard g(h->cfg.device);
             RunCtl rc{};
-            rc.sel_done = rc.plan_done = rc.b_done = rc.admitted = rc.ready = h->step;
+            rc.sel_done = rc.plan_done = rc.b_done = rc.a_done = rc.admitted = rc.ready = h->step;
             rc.next_step[1] = h->step;  // the first instance is generation 1
             rc.next_desc[1] = 0;
             cuda_check(cudaMemcpy(h->runctl, &rc, sizeof rc, cudaMemcpyHostToDevice), "engine state");
@@ -1297,7 +1297,7 @@ void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n
     }
     const uint32_t slot = uint32_t(i % h->aug_ring);
     if (!consumer) {  // one stream: posting m_i releases every earlier m'; then wait for m'_i
-        rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, i + 1);
+        rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, i + 1, false, true);
     } else {  // producer / consumer streams: the consumer releases what it used, then waits
         rmode_post(h, b, 0, labels, 0, 1, 0, n, i, 1, s, 0, true);
         // the release of consumed m' every `release_every` steps (each stream memory operation

@@ -179,7 +179,7 @@ struct alignas(64) FeedDesc {
     uint64_t batch_stride;  // bytes between ring batches
     uint64_t label_stride;  // u32 elements between ring label rows
     uint64_t i_begin;       // engine iteration of the descriptor's first step
-    uint64_t count_n;       // steps (lo 32) | batch rows n (bits 32-62) | kDescSplit
+    uint64_t count_n;       // steps (lo 32) | batch rows n (bits 32-61) | kDescEarly | kDescSplit
     uint64_t ring_first;    // ring batches (lo 32) | first batch of the range (hi 32)
     uint64_t seq;           // descriptor index + 1, written last: the descriptor is complete
 };
@@ -187,13 +187,19 @@ constexpr uint32_t kFeedDescWords = sizeof(FeedDesc) / 8;
 // The descriptor's m' is consumed on another stream, which releases consumed m' explicitly
 // (RunCtl::consumed); without the flag, posting step i releases every m' before it.
 constexpr uint64_t kDescSplit = 1ull << 63;
+// Single-stream update(): m'_i is ready as soon as A(i) and the previous round are (B(i) then
+// sources round i's winners from m'_i, so m_i is free at that point). Without the flag B(i)
+// reads the winners from m_i and m'_i is ready after B(i): the B engines never wait for the
+// A engines (the throughput form, runs and split updates).
+constexpr uint64_t kDescEarly = 1ull << 62;
 
 // Device counters of the resident engine. Iteration counters are absolute (i+1 once
 // iteration i's role finished) and carry over from one instance to the next.
 struct alignas(64) RunCtl {
     uint64_t sel_done;   // sel(i) finished (W_i, state, own row v=i+1)
     uint64_t plan_done;  // plan(i) finished (X_i)
-    uint64_t b_done;     // A(i) and B(i) of every copy CTA complete (in order)
+    uint64_t b_done;     // B(i) of every copy CTA complete (in order): W_i writes, X_i pushes
+    uint64_t a_done;     // A(i) of every copy CTA complete (in order): m_i's rows and labels in m'_i
     uint64_t admitted;   // iterations whose descriptors the feeder has seen
     uint64_t ready;      // m'_i ready for the consumer (i+1): the stream waits poll this word
     uint64_t desc_done;  // descriptors fully consumed (their ring slots may be rewritten)
@@ -204,7 +210,8 @@ struct alignas(64) RunCtl {
     uint32_t error;      // sticky: a wait timed out or a round failed -> every role leaves
     uint32_t where;      // diagnostics: the wait that failed first (site << 24 | k)
     uint32_t pad[2];
-    uint32_t ticket[kTicketRing];  // copy-CTA arrivals of iteration k in slot k % 32 (drift < kListRing)
+    uint32_t ticket[kTicketRing];   // copy-CTA B arrivals of iteration k in slot k % 32 (drift < kListRing)
+    uint32_t aticket[kTicketRing];  // copy-CTA A arrivals
 };
 constexpr uint64_t kStopMask = (1ull << 40) - 1;
 constexpr uint64_t kReadyFailed = 1ull << 62;  // ready after a failure: releases every stream wait

@@ -788,11 +788,14 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
         prof_span(p, 17, pt);
         if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
+            const uint32_t nslot = (p.aslot + 1) % p.aug_ring;
             uint32_t* al = reinterpret_cast<uint32_t*>(p.region[me] + p.off_auglab) +
-                           uint64_t((p.aslot + 1) % p.aug_ring) * p.auglab_slot_elems;
+                           uint64_t(nslot) * p.auglab_slot_elems;
 #pragma unroll 1
             for (uint32_t j = lane; j < cnt[q]; j += 32)
                 al[p.nmax + j] = plan[3 * (q * r + j) + 1];
+            if (lane == 0)  // |reps(i)|: the rows m'_{i+1} gets after its batch (repcnt, counts_of)
+                counts_of(p)[p.aug_ring + nslot] = cnt[q];
         }
         prof_span(p, 18, pt);
     }
@@ -1462,6 +1465,7 @@ __device__ bool wait_admit(const RunParams& rp, uint64_t& seen, uint64_t i) {
 struct FeedCursor {
     uint64_t j, ib;
     uint32_t cnt, n, ring, first;
+    bool early;  // kDescEarly
     const uint8_t* batches;
     const uint32_t* labels;
     uint64_t bstride, lstride;
@@ -1482,7 +1486,8 @@ __device__ void cursor_seek(FeedCursor& c, const RunParams& rp, uint64_t i) {
         c.ib = __ldcg(&d->i_begin);
         const uint64_t cn = __ldcg(&d->count_n), rf = __ldcg(&d->ring_first);
         c.cnt = static_cast<uint32_t>(cn);
-        c.n = static_cast<uint32_t>(cn >> 32) & 0x7fffffffu;
+        c.n = static_cast<uint32_t>(cn >> 32) & 0x3fffffffu;
+        c.early = (cn & kDescEarly) != 0;
         c.ring = static_cast<uint32_t>(rf);
         c.first = static_cast<uint32_t>(rf >> 32);
     }
@@ -1710,18 +1715,27 @@ __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
 
 // CTA 0 warp 5: ready(i) — m'_i complete — in order, for the consumers' stream waits.
 __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
+    // m'_i = m_i ++ reps(i-1) is complete once A(i) (its batch rows and labels, every CTA),
+    // B(i-1) (the reps this rank owns; plan(i-1) wrote their labels and |reps(i-1)|) and every
+    // peer's B(i-1) (the reps it owns) are. The caller's m_i is free once sel(i) has read its
+    // labels and B(i) no longer reads it: for early-ready steps B(i) sources the winners from
+    // m'_i, so B(i) may still run; otherwise ready(i) also waits for B(i).
     const StepParams& b = rp.base;
     const bool multi = (b.mode & kModePeers) && b.N > 1;
     const RegionHeader* hdr = reinterpret_cast<const RegionHeader*>(b.region[b.me]);
+    const uint32_t* repcnt = reinterpret_cast<const uint32_t*>(b.region[b.me] + b.off_counts) + b.aug_ring;
+    uint32_t* aug_count = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_counts);
     uint64_t adm = 0;
-    SeenFlag bd{&rp.ctl->b_done, 0};
+    SeenFlag ad{&rp.ctl->a_done, 0}, bd{&rp.ctl->b_done, 0}, sd{&rp.ctl->sel_done, 0};
     FeedCursor c;
     cursor_init(c, i0, j0);
 #pragma unroll 1
     for (uint64_t i = i0;; ++i) {
         if (!wait_admit(rp, adm, i))
             break;
-        bool ok = wait_seen(bd, i + 1, rp);
+        cursor_seek(c, rp, i);
+        // early-ready steps: A(i), the previous round and sel(i); otherwise B(i) as well
+        bool ok = wait_seen(ad, i + 1, rp) && wait_seen(bd, c.early ? i : i + 1, rp) && wait_seen(sd, i + 1, rp);
         for (uint32_t w = 0; ok && multi && w < b.N; ++w)
             if (w != b.me && i > 0)
                 ok = run_wait(&hdr->pushdone[w], i, rp, true);
@@ -1734,13 +1748,23 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
             }
             break;
         }
+        const uint32_t slot = ring_slot(i, b.aug_ring);
+        const uint32_t cnt = c.n + (i > 0 ? __ldcg(repcnt + slot) : 0u);  // n + |reps(i-1)|
+        aug_count[slot] = cnt;
+        if (b.mailbox) {
+            volatile uint32_t* mb = b.mailbox;
+            mb[mb_count(slot)] = cnt;
+            mb[mb_err(slot, b.aug_ring)] = 0;
+        }
         st_release_sys(&rp.ctl->ready, i + 1);
         *rp.ready_host = i + 1;  // (after the system-scope release: the host sees m'_i complete)
         run_mark(rp, i, 14);
-        cursor_seek(c, rp, i);
-        if (i + 1 == c.ib + c.cnt) {  // the last step of its descriptor: the slot is free
+        if (i + 1 == c.ib + c.cnt) {  // a descriptor's last step: once its B is done too, no role
+                                      // reads the descriptor again and the host may reuse its slot
+            if (!wait_seen(bd, i + 1, rp))
+                break;
             st_release_gpu(&rp.ctl->desc_done, c.j + 1);
-            *rp.desc_done_host = c.j + 1;  // the host reuses ring slots behind this
+            *rp.desc_done_host = c.j + 1;
         }
     }
     if (run_failed(rp)) {  // release every stream (and host) still waiting for an m' of this engine
@@ -2010,7 +2034,16 @@ __device__ void run_plan_role(const RunParams& rp, uint32_t* sm, StepParams& sp,
 // B(k) of a copy CTA is complete: fence, arrive. Copy CTAs are not in lockstep, so arrivals
 // are counted per iteration (slot k % 8); the last arrival of iteration i releases b_done =
 // i+1 once b_done = i (in order) and, multi-rank, pushdone = i+1 at every peer.
-__device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t k, uint64_t i, bool multi) {
+// a_done = max(a_done, v) with release semantics: A(i) of every CTA is complete. Two chains
+// raise it — the A ticket of early-ready steps, the B arrivals of the others (whose CTA
+// arrivals wait for their own A(i)) — and A is in order per CTA, so the maximum is exact.
+__device__ __forceinline__ void raise_a_done(const RunParams& rp, uint64_t v) {
+    asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(&rp.ctl->a_done), "l"(v) : "memory");
+}
+// Returns true for the last arrival (b_done = i+1 published). a_too: every arrival of this
+// iteration also waited for its CTA's A(i), so the last one raises a_done too.
+__device__ bool run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t k, uint64_t i, bool multi,
+                             bool a_too) {
     asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk stores, for generic-proxy readers
     uint32_t* t = &rp.ctl->ticket[k % kTicketRing];
     uint32_t old;
@@ -2021,7 +2054,7 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
     if (old + 1 == rp.copy_ctas) {
         *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+32
         if (!run_wait(&rp.ctl->b_done, i, rp, false))
-            return;
+            return false;
         if (multi) {
             asm volatile("fence.acq_rel.sys;" ::: "memory");
             for (uint32_t w = 0; w < p.N; ++w)
@@ -2031,10 +2064,14 @@ __device__ void run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
                                  "l"(i + 1)
                                  : "memory");
         }
+        if (a_too)
+            raise_a_done(rp, i + 1);
         st_release_gpu(&rp.ctl->b_done, i + 1);
         tstamp(rp, i, 4);
         run_mark(rp, i, 9);
+        return true;
     }
+    return false;
 }
 
 // Cross-warp progress of a copy CTA's engines (shared memory, per iteration parity).
@@ -2042,7 +2079,7 @@ struct BFlags {
     unsigned long long landed[2];    // k+1: B(k)'s loads landed (its reads are done)
     unsigned long long complete[2];  // k+1: B(k)'s stores complete
     unsigned long long parsed[4];    // k+1 in slot k % 4: W_k's slab rows published in wrows[k % 4]
-    unsigned long long a_done;       // k+1: A(k)'s stores (m_i -> m'_i) complete
+    unsigned long long a_local;      // k+1: this CTA's A(k) complete (m_i's slice and labels in m'_i)
 };
 // Bounded like every other wait: gives up once the run failed or after timeout_ns (then
 // fails the run, recording `site` and the iteration), so no role can spin forever.
@@ -2103,7 +2140,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
     const uint32_t clen = static_cast<uint32_t>(c1 - c0);
     const uint32_t per_win = clen ? R.arena_bytes / clen : 0;
     const uint32_t pw = plist_words(b.N, b.r), ww = wlist_words(b.nmax), nslot = b.nmax + 1;
-    SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0};
+    SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0}, adone{&rp.ctl->a_done, 0};
     uint64_t adm = 0;
     FeedCursor cur;
     cursor_init(cur, i0, j0);
@@ -2207,8 +2244,24 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
             w_hz = __any_sync(kFull, w_hz);
         }
         const uint32_t pieces = clen ? nj + nw : 0;
+        // early-ready steps: the winning batch rows come from m'_i (the A engines copied m_i
+        // there): wait for every CTA's A(i), then order its stores before these TMA loads
+        const bool early = __shfl_sync(kFull, cur.early ? 1 : 0, 0) != 0;
+        bool from_batch = early && nw > 0;
+        for (uint32_t x = lane; early && x < nj && !from_batch; x += 32)
+            from_batch = (jsrc[x] >> 31) != 0;
+        if (__any_sync(kFull, from_batch) && pieces) {  // every CTA's A(i) (a flat slice each)
+            bool ok_a = true;
+            if (lane == 0)
+                ok_a = wait_seen(adone, i + 1, rp);
+            if (!__shfl_sync(kFull, ok_a ? 1 : 0, 0))
+                break;
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         {
-            const uint8_t* batch = sp.batch;
+            const uint8_t* batch = early ? b.region[b.me] + b.off_aug + uint64_t(sp.aslot) * b.aug_slot_bytes +
+                                               uint64_t(b.nmax - sp.n) * S  // m_i's rows inside m'_i
+                                         : sp.batch;
             uint8_t* slab = reinterpret_cast<uint8_t*>(sp.slab);
             const uint32_t next_slot = (sp.aslot + 1) % b.aug_ring;
             for (uint32_t x = lane; x < pieces; x += 32) {
@@ -2319,6 +2372,26 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
 // slot pushed (X_i) — so every access to a given slab byte is in this one CTA: there is no
 // grid-wide hand-off between iterations. Warp 3 arrives for the CTA once A(k) and B(k) are
 // complete.
+// A(k) of a copy CTA is complete (its m'_i rows stored, and for CTA part 0 m_i's labels), for
+// an early-ready step: arrive on the A ticket; the last arrival raises a_done to i+1.
+__device__ void run_a_arrive(const RunParams& rp, uint64_t k, uint64_t i) {
+    uint32_t* t = &rp.ctl->aticket[k % kTicketRing];
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    if (old + 1 == rp.copy_ctas) {
+        *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+32
+        raise_a_done(rp, i + 1);
+    }
+}
+
+// CTAs 2..: copies. The B engines work on a fixed byte COLUMN [c0, c1) of every row — so every
+// slab access to a given byte happens in this one CTA, in program order, and there is no
+// grid-wide hand-off between their iterations:
+//   warp 1   A(k): a flat slice of m_i's bytes -> m'_i (TMA through the A ring); CTA part 0
+//            also copies m_i's labels. m_i is not read after A(i): m'_i is ready without B(i).
+//   warps 0, 2   B (even / odd iterations): W_i writes and X_i pushes, sourced from the slab
+//            or, for winning batch rows, from m'_i's rows (after every CTA's A(i): a_done)
+//   warp 3   arrival: B(k) complete -> ticket / b_done / pushdone (and descriptor retirement)
 __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2, uint64_t i0, uint64_t j0) {
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp >= 4) {  // the feeder and the ready publisher, when they live on this copy CTA
@@ -2337,7 +2410,6 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
     uint8_t* ringA = base8 + R.ring_a;
     const uint32_t part = blockIdx.x - 2, parts = rp.copy_ctas;
     const uint64_t S = b.S;
-    const uint32_t CH = kTmaChunk;
     if (tid < sizeof(BFlags) / 8)
         reinterpret_cast<unsigned long long*>(base8 + R.flags)[tid] = 0;
     if (tid == 32) {
@@ -2352,157 +2424,127 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         run_b_warp(rp, sm, R, sp2[warp >> 1], warp >> 1, i0, j0);
         return;
     }
-    if (warp == 3) {  // arrival warp: A(k), B(k) complete -> ticket / b_done / pushdone, in
-                      // order, off the engines' own chains (the GPU-scope atomic waits on the
+    if (warp == 3) {  // arrival warp (lane 0): B(k) complete -> ticket / b_done / pushdone, in
+                      // order, off the B engines' own chains (the GPU-scope atomic waits on the
                       // memory system)
-        // CTA part 0 also writes m'_k's counts and batch labels here (copy_counts' job on the
-        // three-kernel path), in iteration order, while B(k) still runs: they need only plan(k)
-        // (seen through the B engines' `parsed`), |reps(k-1)| stays in a register, and the X
-        // list's |reps(k)| is read before this CTA's arrival lets plan(k+8) reuse its slot.
+        if (lane != 0)
+            return;
         const bool multi = (b.mode & kModePeers) && b.N > 1;
-        uint32_t prev = 0;
         uint64_t adm = 0;
         FeedCursor cur;
         cursor_init(cur, i0, j0);
-        auto wait_cta = [&](const volatile unsigned long long* f, uint64_t want, uint64_t k) {
-            if (lane != 0)
-                return true;
+#pragma unroll 1
+        for (uint64_t k = 0;; ++k) {
+            const uint64_t i = i0 + k;
+            if (!wait_admit(rp, adm, i))
+                return;
+            cursor_seek(cur, rp, i);
+            const bool a_too = !cur.early;  // this arrival also stands for the CTA's A(i)
             uint64_t t0 = 0;
-            for (uint32_t spin = 0; ld_acquire_cta(f) < want; ++spin) {
+            for (uint32_t spin = 0; ld_acquire_cta(&fl->complete[k & 1]) < k + 1 ||
+                                    (a_too && ld_acquire_cta(&fl->a_local) < k + 1);
+                 ++spin) {
                 if ((spin & 63) == 63) {
                     if (run_failed(rp))
-                        return false;
+                        return;
                     const uint64_t now = globaltimer();
                     if (t0 == 0)
                         t0 = now;
                     else if (now - t0 > b.timeout_ns) {
                         run_fail(rp, DRB_ERR_INTERNAL, (8u << 24) | uint32_t(k & 0xffffff));
-                        return false;
+                        return;
                     }
                 }
             }
-            return true;
-        };
-#pragma unroll 1
-        for (uint64_t k = 0;; ++k) {
-            const uint64_t i = i0 + k;
-            uint64_t lp = 0;
-            uint32_t n = 0;
-            bool ok = true;
-            if (lane == 0) {
-                ok = wait_admit(rp, adm, i);
-                if (ok) {
-                    cursor_seek(cur, rp, i);
-                    lp = reinterpret_cast<uint64_t>(cursor_labels(cur, i));
-                    n = cur.n;
-                }
-            }
-            if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
-                return;
-            if (part == 0) {
-                if (!__shfl_sync(kFull, wait_cta(&fl->parsed[k & 3], k + 1, k) ? 1 : 0, 0))
-                    return;
-                lp = __shfl_sync(kFull, lp, 0);
-                n = __shfl_sync(kFull, n, 0);
-                const uint32_t* lab = reinterpret_cast<const uint32_t*>(lp);
-                const uint32_t row0 = b.nmax - n;
-                const uint32_t aslot = ring_slot(i, b.aug_ring);
-                uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
-                               uint64_t(aslot) * b.auglab_slot_elems;
-                uint32_t nrep = 0;
-                if (lane == 0)
-                    nrep = __ldcg(rp.plist_base + (i % kListRing) * rp.pw);  // |reps(i)|
-                if (n <= 64) {  // both label loads in flight at once
-                    const uint32_t l0 = lane < n ? __ldg(lab + lane) : 0u;
-                    const uint32_t l1 = lane + 32 < n ? __ldg(lab + lane + 32) : 0u;
-                    if (lane < n)
-                        al[row0 + lane] = l0;
-                    if (lane + 32 < n)
-                        al[row0 + lane + 32] = l1;
-                } else {
-#pragma unroll 4
-                    for (uint32_t x = lane; x < n; x += 32)
-                        al[row0 + x] = __ldg(lab + x);
-                }
-                if (lane == 0) {
-                    uint32_t* aug_count = counts_of(b);
-                    uint32_t* repcnt = aug_count + b.aug_ring;
-                    if (k == 0)
-                        prev = i > 0 ? __ldcg(&repcnt[aslot]) : 0u;
-                    aug_count[aslot] = n + prev;
-                    repcnt[(aslot + 1) % b.aug_ring] = nrep;
-                    if (b.mailbox) {
-                        volatile uint32_t* mb = b.mailbox;
-                        mb[mb_count(aslot)] = n + prev;
-                        mb[mb_err(aslot, b.aug_ring)] = 0;
-                    }
-                    prev = nrep;
-                }
-                __syncwarp();
-            }
-            if (!__shfl_sync(kFull, wait_cta(&fl->complete[k & 1], k + 1, k) ? 1 : 0, 0))
-                return;
-            if (!__shfl_sync(kFull, wait_cta(&fl->a_done, k + 1, k) ? 1 : 0, 0))
-                return;
             delay_exp(4);
-            if (lane == 0) {
-                run_mark(rp, i, 8);
-                run_b_arrive(rp, b, k, i, multi);
-            }
+            run_mark(rp, i, 8);
+            run_b_arrive(rp, b, k, i, multi, a_too);
         }
     }
-    // ---- A engine: m_i -> m'_i rows, iteration after iteration --------------------------
-    if (lane != 0)
-        return;
-    uint32_t ph_bits = 0;  // phase of each A barrier
-    SeenFlag bdone{&rp.ctl->b_done, 0};
+    // ---- A engine (warp 1): m_i -> m'_i rows (a flat slice of the batch bytes per CTA, 8 KB
+    // TMA chunks), iteration after iteration ---------------------------------------------
+    const uint32_t CH = kTmaChunk;
+    uint32_t ph_bits = 0;  // phase of each A barrier (lane 0)
+    SeenFlag bdone{&rp.ctl->b_done, 0}, adone{&rp.ctl->a_done, 0};
     uint64_t adm = 0;
     FeedCursor cur;
     cursor_init(cur, i0, j0);
     // A(i) writes m'_i's batch rows into the ring slot m'_{i-R} held: that m' was complete (its
-    // pushes, B(i-R-1), done) and released (admission), so A could run R-2 iterations ahead of
-    // B; DRB_A_AHEAD (default 4) bounds it: A's streaming traffic far ahead delays B's loads
+    // pushes, B(i-R-1), done), read by B(i-R) (sourcing winners) and released (admission), so A
+    // could run R-2 iterations ahead of B; DRB_A_AHEAD (default 4) bounds it: A's streaming
+    // traffic far ahead delays B's loads
     const uint32_t ahead = min(b.aug_ring - 2, rp.a_ahead);
 #pragma unroll 1
     for (uint64_t k = 0;; ++k) {
         const uint64_t i = i0 + k;
-        if (!wait_admit(rp, adm, i))
-            break;
-        if (!wait_seen(bdone, i0 + back(k, ahead), rp))
-            break;
-        run_mark(rp, i, 2);
-        cursor_seek(cur, rp, i);
-        const uint32_t n = cur.n;
-        const uint8_t* batch = cursor_batch(cur, i);
-        const uint64_t a16 = (uint64_t(n) * S) >> 4;
-        const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
-        const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
-        uint8_t* dst = b.region[b.me] + b.off_aug + uint64_t(ring_slot(i, b.aug_ring)) * b.aug_slot_bytes +
-                       uint64_t(b.nmax - n) * S;
-        for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
-            const uint32_t w1 = min(nA, w0 + kTmaStagesA);
-            bulk_wait_read_all();  // the ring's previous window has been stored
-            for (uint32_t x = w0; x < w1; ++x) {
-                const uint64_t off = alo + uint64_t(x) * CH;
-                const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
-                mbar_expect_tx(bars + (x - w0), len);
-                bulk_load(ringA + (x - w0) * CH, batch + off, len, bars + (x - w0));
+        bool ok = true;
+        uint32_t n = 0;
+        uint64_t bp = 0, lp = 0;
+        bool early = false;
+        if (lane == 0) {
+            // (and within kTicketRing/2 iterations of the slowest CTA's A: the A ticket slots)
+            ok = wait_admit(rp, adm, i) && wait_seen(bdone, i0 + back(k, ahead), rp) &&
+                 wait_seen(adone, i0 + back(k, kTicketRing / 2), rp);
+            if (ok) {
+                cursor_seek(cur, rp, i);
+                early = cur.early;
+                n = cur.n;
+                bp = reinterpret_cast<uint64_t>(cursor_batch(cur, i));
+                lp = reinterpret_cast<uint64_t>(cursor_labels(cur, i));
             }
-            for (uint32_t x = w0; x < w1; ++x) {
-                const uint64_t off = alo + uint64_t(x) * CH;
-                const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
-                if (!mbar_wait(bars + (x - w0), take_phase(ph_bits, x - w0), rp.base.timeout_ns))
-                    run_fail(rp, DRB_ERR_INTERNAL, (11u << 24) | uint32_t(k & 0xffffff));
-                bulk_store(dst + off, ringA + (x - w0) * CH, len);
-            }
-            bulk_commit();
         }
-        bulk_wait_all();  // A(k)'s m'_i rows are written: hand them to the arrival warp
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        st_release_cta(&fl->a_done, k + 1);
-        run_mark(rp, i, 5);
+        if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
+            break;
+        n = __shfl_sync(kFull, n, 0);
+        lp = __shfl_sync(kFull, lp, 0);
+        run_mark(rp, i, 2);
+        const uint32_t slot = ring_slot(i, b.aug_ring);
+        const uint32_t row0 = b.nmax - n;
+        if (part == 0) {  // m_i's labels -> m'_i's batch rows' labels (the whole warp)
+            const uint32_t* lab = reinterpret_cast<const uint32_t*>(lp);
+            uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
+                           uint64_t(slot) * b.auglab_slot_elems + row0;
+#pragma unroll 4
+            for (uint32_t x = lane; x < n; x += 32)
+                al[x] = __ldg(lab + x);
+        }
+        if (lane == 0) {
+            const uint64_t a16 = (uint64_t(n) * S) >> 4;
+            const uint64_t alo = (a16 * part / parts) << 4, ahi = (a16 * (part + 1) / parts) << 4;
+            const uint32_t nA = static_cast<uint32_t>((ahi - alo + CH - 1) / CH);
+            const uint8_t* batch = reinterpret_cast<const uint8_t*>(bp);
+            uint8_t* dst = b.region[b.me] + b.off_aug + uint64_t(slot) * b.aug_slot_bytes + uint64_t(row0) * S;
+            for (uint32_t w0 = 0; w0 < nA; w0 += kTmaStagesA) {
+                const uint32_t w1 = min(nA, w0 + kTmaStagesA);
+                bulk_wait_read_all();  // the ring's previous window has been stored
+                for (uint32_t x = w0; x < w1; ++x) {
+                    const uint64_t off = alo + uint64_t(x) * CH;
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                    mbar_expect_tx(bars + (x - w0), len);
+                    bulk_load(ringA + (x - w0) * CH, batch + off, len, bars + (x - w0));
+                }
+                for (uint32_t x = w0; x < w1; ++x) {
+                    const uint64_t off = alo + uint64_t(x) * CH;
+                    const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
+                    if (!mbar_wait(bars + (x - w0), take_phase(ph_bits, x - w0), rp.base.timeout_ns))
+                        run_fail(rp, DRB_ERR_INTERNAL, (11u << 24) | uint32_t(k & 0xffffff));
+                    bulk_store(dst + off, ringA + (x - w0) * CH, len);
+                }
+                bulk_commit();
+            }
+            bulk_wait_all();  // A(k)'s m'_i rows are written
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();  // (the other lanes' label stores are ordered before lane 0's release)
+        if (lane == 0) {
+            st_release_cta(&fl->a_local, k + 1);  // for this CTA's arrival (the B ticket)
+            if (early)
+                run_a_arrive(rp, k, i);  // m'_i's batch part is complete: ready(i), and every B(i)
+            run_mark(rp, i, 5);
+        }
     }
-    bulk_wait_all();
+    if (lane == 0)
+        bulk_wait_all();
 }
 
 __global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_constant__ RunParams rp) {

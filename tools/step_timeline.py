@@ -9,8 +9,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "tools", "ablib", "libdrb_inst.so")
-if not os.path.exists(LIB) or os.environ.get("REBUILD"):
+LIB = os.environ.get("INST_LIB") or os.path.join(ROOT, "tools", "ablib", "libdrb_inst.so")
+if not os.environ.get("INST_LIB") and (not os.path.exists(LIB) or os.environ.get("REBUILD")):
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     src = [os.path.join(ROOT, "paper_2406_03285_b200", "csrc", f) for f in ("drb_kernels.cu", "drb_capi.cu", "drb_dataset.cu")]
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
