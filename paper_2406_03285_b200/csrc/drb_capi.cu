@@ -1346,15 +1346,21 @@ void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n
 // steps, then `s` waits until the last m' is ready.
 void rmode_run(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const uint32_t* labels,
                uint64_t label_stride, uint32_t ring, uint32_t n, uint64_t steps, uint64_t first, cudaStream_t s) {
+    // The run's last step goes out as its own early-ready descriptor: the stream's wait then ends
+    // when m'_{end-1} is complete, without waiting for B(end-1) (which sources its winners
+    // from m'_{end-1}, so the caller's ring is free once the wait is over).
+    const uint64_t body = steps - 1;
     uint64_t done = 0;
-    while (done < steps) {
-        const uint32_t cnt = uint32_t(std::min<uint64_t>(steps - done, 1ull << 31));
-        const bool last = done + cnt == steps;
+    while (done < body) {
+        const uint32_t cnt = uint32_t(std::min<uint64_t>(body - done, 1ull << 31));
         rmode_post(h, batches, batch_stride, labels, label_stride, ring, uint32_t((first + done) % ring), n,
-                   h->step, cnt, s, last ? h->step + cnt : 0);
+                   h->step, cnt, s);
         h->step += cnt;
         done += cnt;
     }
+    rmode_post(h, batches, batch_stride, labels, label_stride, ring, uint32_t((first + done) % ring), n, h->step, 1, s,
+               h->step + 1, false, true);
+    h->step += 1;
     // one event for the whole run (its m' ring slots alias it): the host cost of recording
     // R events would sit inside a timed run
     cuda_check(cudaEventRecord(h->run_done, s), "event");

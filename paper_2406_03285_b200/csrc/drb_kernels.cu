@@ -2500,12 +2500,13 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         run_mark(rp, i, 2);
         const uint32_t slot = ring_slot(i, b.aug_ring);
         const uint32_t row0 = b.nmax - n;
-        if (part == 0) {  // m_i's labels -> m'_i's batch rows' labels (the whole warp)
+        if (part == 0 && lane > 0) {  // m_i's labels -> m'_i's batch rows' labels (lanes 1-31,
+                                      // while lane 0 drives the TMA copy)
             const uint32_t* lab = reinterpret_cast<const uint32_t*>(lp);
             uint32_t* al = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_auglab) +
                            uint64_t(slot) * b.auglab_slot_elems + row0;
 #pragma unroll 4
-            for (uint32_t x = lane; x < n; x += 32)
+            for (uint32_t x = lane - 1; x < n; x += 31)
                 al[x] = __ldg(lab + x);
         }
         if (lane == 0) {

@@ -148,3 +148,37 @@ def test_run_and_step_ordered_after_default_stream_producer(drb):
     assert np.array_equal(l.cpu().numpy().astype(np.uint32), ol[0, :aug.count()])
     assert eng.device_error() == 0
     eng.shutdown()
+
+
+def test_runs_on_different_streams_and_graph_then_run(drb):
+    """a run() on one stream, another run() on a second stream and a prepared run
+    launched on a third, back to back with no host synchronisation, still apply in call order
+    (the resident engine admits posts in order; the three-kernel path orders every run behind
+    the handle's latest work)."""
+    K, cap, S, b, c, r, seed, ring = 10, 4, 256, 24, 14, 7, 33, 5
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed)
+    eng = drb.engine(buf)
+    eng.start()
+    rep = Backend("port").replay(1, K, cap, S, c, r, seed)
+    spec = stream_spec(K, 1, b, S, steps_per_task=10**9, seed=seed)
+    rings = []
+    for x in range(3):
+        rd = np.stack([spec.payload(0, 100 * x + k) for k in range(ring)])
+        rl = np.stack([spec.labels(0, 100 * x + k) for k in range(ring)])
+        rings.append((rd, rl, dev(rd, rl)))
+    torch.cuda.synchronize()
+    s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    eng.run(rings[0][2][0], rings[0][2][1], 9, stream=s1)
+    eng.run(rings[1][2][0], rings[1][2][1], 7, first=2, stream=s2)
+    g = eng.prepare_run(rings[2][2][0], rings[2][2][1], 11, first=1)
+    g.launch(s3)
+    for x, (steps, first) in enumerate(((9, 0), (7, 2), (11, 1))):
+        rd, rl, _ = rings[x]
+        for k in range(steps):
+            rep.step(rd[(first + k) % ring][None], rl[(first + k) % ring][None])
+    torch.cuda.synchronize()
+    g.close()
+    check_state(buf, rep, K, cap, "three runs on three streams")
+    check_step(eng, rep, spec.payload(0, 999), spec.labels(0, 999), "step after")
+    assert eng.device_error() == 0
+    eng.shutdown()

@@ -25,12 +25,17 @@ data, lab = device_ring(spec, 0, 64, "cuda:0")
 s = torch.cuda.Stream()
 eng.run(data, lab, 400, stream=s)
 torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record(s)
-eng.run(data, lab, steps, stream=s)
-e1.record(s)
-torch.cuda.synchronize()
+reps = int(os.environ.get("REPS", "1"))
+ts = []
+for _ in range(reps):  # each rep: synchronise (the instance leaves), then one timed run
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    eng.run(data, lab, steps, stream=s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) * 1000 / steps)
+ts.sort()
 print(f"run of {steps} steps (aug_ring {ring or 16}, A ahead {os.environ.get('DRB_A_AHEAD', 4)}): "
-      f"{e0.elapsed_time(e1) * 1000 / steps:.2f} us/step, instances {eng.engine_info()}")
+      f"{ts[len(ts) // 2]:.2f} us/step (median of {reps}, min {ts[0]:.2f}), instances {eng.engine_info()}")
 assert eng.device_error() == 0
 eng.shutdown()
