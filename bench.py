@@ -249,7 +249,7 @@ def run_reference(args, cfg):
         iters = max(1, min(args.steps, args.ref_iters))
         cb = cpu_baseline_sample(cfg, n, iters)
     except Exception as e:  # noqa: BLE001
-        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}), flush=True)
+        emit({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"})
         return 0
     step_samples = (cfg["b"] + cfg["r"]) * n  # steady state: every worker's m' has b + r rows
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": n,
@@ -260,11 +260,28 @@ def run_reference(args, cfg):
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
+_JSON_FD = 1
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout (library chatter such as NCCL's version
+    banner is routed to stderr by quiet_stdout)."""
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
+
+
+def quiet_stdout():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
 def main():
+    quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=0)
     ap.add_argument("--steps", type=int, default=20000)
@@ -620,7 +637,7 @@ def main():
             **({"nvlink": nvlink} if nvlink else {}),
             **({"steps_sweep": sweep} if sweep else {}),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if N > 1:
         dist.destroy_process_group()
     return 0

@@ -1734,8 +1734,10 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
         if (!wait_admit(rp, adm, i))
             break;
         cursor_seek(c, rp, i);
-        // early-ready steps: A(i), the previous round and sel(i); otherwise B(i) as well
-        bool ok = wait_seen(ad, i + 1, rp) && wait_seen(bd, c.early ? i : i + 1, rp) && wait_seen(sd, i + 1, rp);
+        // early-ready steps: A(i), the previous round and sel(i); otherwise B(i), which implies
+        // them (every CTA's arrival for B(i) waited for its A(i); B(i) followed sel(i))
+        bool ok = c.early ? wait_seen(ad, i + 1, rp) && wait_seen(bd, i, rp) && wait_seen(sd, i + 1, rp)
+                          : wait_seen(bd, i + 1, rp);
         for (uint32_t w = 0; ok && multi && w < b.N; ++w)
             if (w != b.me && i > 0)
                 ok = run_wait(&hdr->pushdone[w], i, rp, true);
@@ -2482,12 +2484,14 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         uint64_t bp = 0, lp = 0;
         bool early = false;
         if (lane == 0) {
-            // (and within kTicketRing/2 iterations of the slowest CTA's A: the A ticket slots)
-            ok = wait_admit(rp, adm, i) && wait_seen(bdone, i0 + back(k, ahead), rp) &&
-                 wait_seen(adone, i0 + back(k, kTicketRing / 2), rp);
+            ok = wait_admit(rp, adm, i) && wait_seen(bdone, i0 + back(k, ahead), rp);
             if (ok) {
                 cursor_seek(cur, rp, i);
                 early = cur.early;
+                // an early step's A ticket: within kTicketRing/2 iterations of the slowest CTA's A
+                // (otherwise b_done, which the B arrivals raise only after their CTA's A, bounds it)
+                if (early)
+                    ok = wait_seen(adone, i0 + back(k, kTicketRing / 2), rp);
                 n = cur.n;
                 bp = reinterpret_cast<uint64_t>(cursor_batch(cur, i));
                 lp = reinterpret_cast<uint64_t>(cursor_labels(cur, i));

@@ -1,5 +1,5 @@
 """Multi-rank wiring over torch.distributed (plumbing only: the data path is the CUDA
-kernels pulling over NVLink). Replaces the reference's worker_mesh roster/connect step
+kernels pushing over NVLink). Replaces the reference's worker_mesh roster/connect step
 (proj/src/runner/mesh.cpp:12-81): every rank all-gathers the opaque handle blobs of the
 peer-shareable regions (CUDA IPC) and maps them."""
 from __future__ import annotations

@@ -101,7 +101,7 @@ def test_multi_process_ipc_parity(N):
 def test_stalled_peer_times_out_without_hanging(monkeypatch):
     """A peer that stops calling update: the reference degrades after its
     rendezvous timeout (size_table.cpp:66-100); here every cross-rank wait is bounded
-    (DRB_TIMEOUT_MS), the round fails with a sticky transport error, the augmented batch
+    (DRB_TIMEOUT_MS), the round fails with a sticky transport error, the next augmented batch
     reports it, the engine is dead for later updates (engine.cpp:67-68,74-80), and shutdown
     still drains — the GPU is not left spinning."""
     if ngpu() < 2:
@@ -124,12 +124,18 @@ def test_stalled_peer_times_out_without_hanging(monkeypatch):
         a = [upd(w, i) for w in range(2)]
         assert [x.count() for x in a] == [b + r if i else b] * 2
     t0 = time.time()
-    lone = upd(0, 4)  # rank 1 stalls: never enqueues round 4
+    # rank 1 stalls: never enqueues round 4. update(m_4) returns m_4 ++ reps(3), which the
+    # peer's round 3 already delivered — as the reference's update(m_4) returns the reps
+    # fetched in round 3 (engine.cpp:62-106) — so it completes; round 4's rendezvous (the
+    # peer's occupancy row 5) is what times out, and update(m_5) reports it.
+    lone = upd(0, 4)
+    assert lone.count() == b + r
+    nxt = upd(0, 5)
     with pytest.raises(drb.engine_error):
-        lone.count()
+        nxt.count()
     assert time.time() - t0 < 30
     with pytest.raises(drb.engine_error):
-        upd(0, 5)
+        upd(0, 6)
     assert engs[0].device_error() != 0
     for e in engs:
         e.shutdown()
