@@ -474,12 +474,13 @@ def main():
             tk = float(tt.item())
         return 1000.0 * tk / nsteps, eng.engine_info()["instances"] - inst0
     # the same through the C++ facade (tools/update_bench: the reference's trainer is C++; no
-    # Python in the per-step path), N=1 only
+    # Python in the per-step path), N=1 only: 2000 steps (the steady state of a training loop;
+    # it also reports 20 steps)
     cpp_update = None
     exe = os.path.join(ROOT, "tools", "update_bench")
     if N == 1 and os.path.exists(exe):
         try:
-            res = subprocess.run([exe, "200", str(local), str(aug_ring)], capture_output=True, text=True,
+            res = subprocess.run([exe, "2000", str(local), str(aug_ring)], capture_output=True, text=True,
                                  timeout=300)
             cpp_update = json.loads(res.stdout.strip().splitlines()[-1]) if res.returncode == 0 else \
                 {"error": res.stderr[-300:]}

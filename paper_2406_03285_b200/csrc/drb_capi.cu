@@ -1351,8 +1351,10 @@ void rmode_run(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const u
     // from m'_{end-1}, so the caller's ring is free once the wait is over).
     const uint64_t body = steps - 1;
     uint64_t done = 0;
+    // DRB_RUN_CHUNK: steps per descriptor (experiments: the per-descriptor cost of the feed)
+    static const uint64_t chunk = std::getenv("DRB_RUN_CHUNK") ? std::max<uint64_t>(1, std::strtoull(std::getenv("DRB_RUN_CHUNK"), nullptr, 10)) : (1ull << 31);
     while (done < body) {
-        const uint32_t cnt = uint32_t(std::min<uint64_t>(body - done, 1ull << 31));
+        const uint32_t cnt = uint32_t(std::min<uint64_t>(body - done, chunk));
         rmode_post(h, batches, batch_stride, labels, label_stride, ring, uint32_t((first + done) % ring), n,
                    h->step, cnt, s);
         h->step += cnt;

@@ -1608,63 +1608,83 @@ __device__ void run_publisher(const RunParams& rp, uint64_t i0, volatile unsigne
 
 // The feeder (one lane): admits posted descriptors in order, and ends the instance when idle.
 __device__ void run_feeder(const RunParams& rp, uint64_t i0, uint64_t j0) {
-    // The whole warp runs this loop in lockstep (every value below is warp-uniform); lane 0
-    // does the control loads and stores, lanes 0-3 fetch the descriptor.
+    // The whole warp runs this loop in lockstep (every value below is warp-uniform). Lanes 0-7
+    // poll the sequence words of the next eight descriptors together; the posted prefix of them
+    // is fetched in one PCIe round trip (four 16-byte reads per descriptor, on lanes 4d..4d+3)
+    // and admitted in order, so a producer that runs ahead is admitted a batch at a time.
     const uint32_t lane = threadIdx.x & 31;
     uint64_t j = j0, admitted = i0, idle_t0 = 0;
     uint64_t released = i0;  // m' below this are released by implicit (single-stream) posts
     bool failed = false;
     const uint32_t R = rp.base.aug_ring;
+    constexpr uint32_t kBatch = 32 / (kFeedDescWords / 2);  // descriptors per round trip
 #pragma unroll 1
     for (uint32_t spin = 0;; ++spin) {
         uint32_t posted = 0;
-        if (lane == 0)
-            posted = ld_acquire_sys(rp.feed_seq + (j % kFeedRing)) == j + 1;  // posted (stream order)
-        if (__shfl_sync(kFull, posted, 0)) {
-            // the descriptor itself from mapped host memory: four 16-byte reads on four lanes,
-            // in flight together (one PCIe round trip), then the device mirror the roles read
-            const uint64_t* hs = reinterpret_cast<const uint64_t*>(rp.hdesc + (j % kFeedRing));
+        if (lane < kBatch)
+            posted = ld_acquire_sys(rp.feed_seq + ((j + lane) % kFeedRing)) == j + lane + 1;  // stream order
+        const uint32_t cnt = __ffs(~__ballot_sync(kFull, posted)) - 1;  // posted prefix j .. j+cnt-1
+        if (cnt > 0) {
+            __syncwarp();  // (the polling lanes' acquires order every lane's descriptor reads)
+            // the descriptors from mapped host memory, then the device mirror the roles read
+            const uint32_t d = lane / (kFeedDescWords / 2), part = lane % (kFeedDescWords / 2);
             uint64_t lo = 0, hi = 0;
-            if (lane < kFeedDescWords / 2)
-                asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(hs + 2 * lane)
+            if (d < cnt) {
+                const uint64_t* hs = reinterpret_cast<const uint64_t*>(rp.hdesc + ((j + d) % kFeedRing));
+                asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(hs + 2 * part)
                              : "memory");
-            uint64_t w[kFeedDescWords];
-#pragma unroll
-            for (uint32_t x = 0; x < kFeedDescWords / 2; ++x) {
-                w[2 * x] = __shfl_sync(kFull, lo, x);
-                w[2 * x + 1] = __shfl_sync(kFull, hi, x);
             }
-            if (w[5] & kDescSplit) {
-                // plan(i)/B(i) refill m'_{i+1}'s slot, last handed out as m'_{i+1-R}: its
-                // consumer (another stream) must have released it
-                const uint64_t need = w[4] + 2 >= R ? w[4] + 2 - R : 0;
-                uint32_t blocked = 0;
-                if (lane == 0)
-                    blocked = released < need && ld_acquire_sys(&rp.ctl->consumed) < need;
-                if (__shfl_sync(kFull, blocked, 0)) {
-                    idle_t0 = 0;  // posted work is waiting: not idle
-                    __nanosleep(128);
-                    continue;
+            uint64_t consumed = 0;
+            if (lane == 0)
+                consumed = ld_acquire_sys(&rp.ctl->consumed);
+            consumed = __shfl_sync(kFull, consumed, 0);
+            uint32_t took = 0;
+            bool blocked = false;
+#pragma unroll 1
+            for (; took < cnt; ++took) {
+                uint64_t w[kFeedDescWords];
+#pragma unroll
+                for (uint32_t x = 0; x < kFeedDescWords / 2; ++x) {
+                    w[2 * x] = __shfl_sync(kFull, lo, took * (kFeedDescWords / 2) + x);
+                    w[2 * x + 1] = __shfl_sync(kFull, hi, took * (kFeedDescWords / 2) + x);
                 }
-            } else if (w[4] > released) {
-                released = w[4];
-            }
-            admitted = w[4] + static_cast<uint32_t>(w[5]);  // i_begin + count
-            if (lane == 0) {
-                uint64_t* dd = reinterpret_cast<uint64_t*>(rp.feed + (j % kFeedRing));
+                if (w[5] & kDescSplit) {
+                    // plan(i)/B(i) refill m'_{i+1}'s slot, last handed out as m'_{i+1-R}: its
+                    // consumer (another stream) must have released it
+                    const uint64_t need = w[4] + 2 >= R ? w[4] + 2 - R : 0;
+                    if (released < need && consumed < need) {
+                        blocked = true;
+                        break;
+                    }
+                } else if (w[4] > released) {
+                    released = w[4];
+                }
+                admitted = w[4] + static_cast<uint32_t>(w[5]);  // i_begin + count
+                if (lane == 0) {
+                    uint64_t* dd = reinterpret_cast<uint64_t*>(rp.feed + ((j + took) % kFeedRing));
 #pragma unroll
-                for (uint32_t x = 0; x < kFeedDescWords; ++x)
-                    dd[x] = w[x];
-                st_release_gpu(&rp.ctl->admitted, admitted);
-                run_mark(rp, w[4], 13);
-                if (rp.timings)
-                    for (uint64_t x = w[4]; x < admitted && x < w[4] + kTimingRing; ++x)
-                        tstamp(rp, x, 0);
+                    for (uint32_t x = 0; x < kFeedDescWords; ++x)
+                        dd[x] = w[x];
+                    if (rp.timings)
+                        for (uint64_t x = w[4]; x < admitted && x < w[4] + kTimingRing; ++x)
+                            tstamp(rp, x, 0);
+                    run_mark(rp, w[4], 13);
+                }
             }
-            ++j;
-            idle_t0 = 0;
-            spin = 0;
-            continue;
+            if (took > 0) {
+                if (lane == 0) {
+                    st_release_gpu(&rp.ctl->admitted, admitted);
+                }
+                j += took;
+                idle_t0 = 0;
+                spin = 0;
+                continue;
+            }
+            if (blocked) {  // posted work is waiting for its consumer: not idle
+                idle_t0 = 0;
+                __nanosleep(128);
+                continue;
+            }
         }
         uint32_t act = 0;  // 0: keep polling, 1: failed, 2: leave
         if (lane == 0) {
@@ -1858,7 +1878,10 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
             }
             if (ok) {
                 run_patch(sp, rp, i);
-                cursor_seek(cur, rp, i);
+                if (nxt.cnt != 0 && i >= nxt.ib && i < nxt.ib + nxt.cnt)
+                    cur = nxt;  // looked ahead in round i-1 (no second descriptor load)
+                else
+                    cursor_seek(cur, rp, i);
                 feed_patch(sp, cur, i);
                 hx[0] = sp.n;
                 // W slot (i-8) / m' slot (multi, i-6) / table slot (plan(i-4)) free

@@ -63,6 +63,15 @@ elif mode == "split":  # update(m, loader, trainer) back to back (the pipelined 
     loader = torch.cuda.Stream()
     for k in range(N):
         eng.update((data[k % 16], lab[k % 16]), stream=loader, consumer=s)
+elif mode == "splitraw":  # the same through raw ctypes calls (the Python wrapper is slower than a step)
+    loader = torch.cuda.Stream()
+    loader.wait_stream(s)
+    fn = _lib.lib.drb_rb_step_split
+    out = _lib.drb_aug()
+    ptrs = [(C.c_void_p(data[k].data_ptr()), C.c_void_p(lab[k].data_ptr())) for k in range(16)]
+    hl, hs, hb = C.c_void_p(loader.cuda_stream), C.c_void_p(s.cuda_stream), buf.h
+    for k in range(N):
+        fn(hb, ptrs[k % 16][0], ptrs[k % 16][1], b, hl, hs, C.byref(out))
 else:  # one run of N pipelined steps: stamps relative to each step's admission
     eng.run(data, lab, N, stream=s)
 torch.cuda.synchronize()

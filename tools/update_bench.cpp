@@ -76,8 +76,14 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    // UB_TRACE=1: an event after every step's wait, per-step times by step range on stderr
+    const bool trace = std::getenv("UB_TRACE") != nullptr;
+    std::vector<cudaEvent_t> evs;
     auto timed = [&](bool split, int n, double* host_us) {
         CK(cudaDeviceSynchronize());
+        if (trace)
+            while (evs.size() < size_t(n))
+                CK(cudaEventCreate(&evs.emplace_back()));
         CK(cudaEventRecord(e0, trainer));
         if (split)
             CK(cudaStreamWaitEvent(loader, e0, 0));
@@ -87,6 +93,23 @@ int main(int argc, char** argv) {
                 eng.update(batch(k), loader, trainer);
             else
                 eng.update(batch(k), trainer);
+            if (trace)
+                CK(cudaEventRecord(evs[k], trainer));
+        }
+        if (trace) {
+            CK(cudaDeviceSynchronize());
+            int lo = 0;
+            for (int hi : {1, 5, 20, 50, 100, 200, 400, 800, 1600, 3200}) {
+                if (hi > n)
+                    hi = n;
+                if (hi <= lo)
+                    break;
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, lo ? evs[lo - 1] : e0, evs[hi - 1]));
+                std::fprintf(stderr, "%s steps [%d,%d): %.2f us/step\n", split ? "split" : "serial", lo, hi,
+                             1000.0 * ms / (hi - lo));
+                lo = hi;
+            }
         }
         *host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / n;
         CK(cudaEventRecord(e1, trainer));
