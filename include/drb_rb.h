@@ -294,6 +294,17 @@ DRB_RB_API drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* 
 DRB_RB_API drb_status drb_rb_synchronize(drb_rb* h);
 /* total_wait_ms (engine.hpp:88): host time blocked waiting for round results. */
 DRB_RB_API drb_status drb_rb_total_wait_ms(drb_rb* h, double* out);
+/* engine::iterations / queue_depth / degraded_rounds / replanned_entries (engine.hpp:87-92), any
+ * pointer may be NULL. iterations = steps enqueued; queue_depth = enqueued steps whose m' is not
+ * ready yet (the reference holds at most one queued job; here several rounds may be in flight);
+ * degraded_rounds and replanned_entries are always 0: a stalled peer fails the engine
+ * (DRB_ERR_TRANSPORT) instead of degrading to stale rows. */
+DRB_RB_API drb_status drb_rb_engine_counters(drb_rb* h, uint64_t* iterations, uint64_t* queue_depth,
+                                             uint64_t* degraded_rounds, uint64_t* replanned_entries);
+/* engine::broadcast_sizes (engine.hpp:82, engine.cpp:256-265): re-publish the freshest occupancy
+ * row at a task boundary. A no-op here: every round already stores the row into every peer's
+ * table. */
+DRB_RB_API drb_status drb_rb_broadcast_sizes(drb_rb* h);
 /* Device-side error word of the last completed step (0 = none). */
 DRB_RB_API drb_status drb_rb_device_error(drb_rb* h, uint32_t* out);
 /* Diagnostics (DRB_TRACE=1 at create): globaltimer stamps of the last step's phases in

@@ -286,6 +286,13 @@ public:
         return v;
     }
     void synchronize() { check(drb_rb_synchronize(b_.raw())); }
+    // engine::iterations / queue_depth / degraded_rounds / replanned_entries (engine.hpp:87-92)
+    std::uint64_t iterations() const { return counter(0); }
+    std::size_t queue_depth() const { return std::size_t(counter(1)); }
+    std::uint64_t degraded_rounds() const { return counter(2); }
+    std::uint64_t replanned_entries() const { return counter(3); }
+    // engine::broadcast_sizes (engine.hpp:82): a no-op, rows are published every round
+    void broadcast_sizes() { check(drb_rb_broadcast_sizes(b_.raw())); }
     // engine::drain_timings (engine.hpp:93); needs DRB_RB_FLAG_TIMINGS in the buffer's config
     std::vector<drb_timing> drain_timings() {
         std::vector<drb_timing> out(4096);
@@ -296,6 +303,11 @@ public:
     }
 
 private:
+    std::uint64_t counter(int which) const {
+        std::uint64_t v[4] = {0, 0, 0, 0};
+        check(drb_rb_engine_counters(b_.raw(), &v[0], &v[1], &v[2], &v[3]));
+        return v[which];
+    }
     rehearsal_buffer& b_;
     bool started_ = false, shut_ = false;
 };

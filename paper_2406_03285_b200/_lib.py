@@ -155,6 +155,8 @@ def _load():
         "drb_rb_engine_info": (st, [vp, P(u32), P(u64), P(u64), P(u32)]),
         "drb_rb_synchronize": (st, [vp]),
         "drb_rb_total_wait_ms": (st, [vp, P(C.c_double)]),
+        "drb_rb_engine_counters": (st, [vp, P(u64), P(u64), P(u64), P(u64)]),
+        "drb_rb_broadcast_sizes": (st, [vp]),
         "drb_rb_drain_timings": (st, [vp, P(drb_timing), u32, P(u32)]),
         "drb_rb_device_error": (st, [vp, P(u32)]),
         "drb_rb_launch_info": (st, [vp, P(u32), P(u32), P(u32)]),

@@ -1774,6 +1774,40 @@ drb_status drb_rb_total_wait_ms(drb_rb* h, double* out) {
     return DRB_OK;
 }
 
+drb_status drb_rb_engine_counters(drb_rb* h, uint64_t* iterations, uint64_t* queue_depth, uint64_t* degraded_rounds,
+                                  uint64_t* replanned_entries) {
+    DRB_REQUIRE(h);
+    return guarded([&] {
+        device_guard g(h->cfg.device);
+        uint64_t pending = 0;  // enqueued rounds whose m' is not ready yet (a non-blocking look)
+        if (h->rmode) {
+            const uint64_t rd = *mb64(h, kMbReady);
+            pending = rd >= kReadyFailed ? 0 : h->step - std::min(h->step, rd);
+        } else if (!h->done.empty()) {
+            const uint64_t R = h->done.size();
+            for (uint64_t x = h->step > R ? h->step - R : 0; x < h->step; ++x)
+                pending += cudaEventQuery(h->done[x % R]) == cudaErrorNotReady ? 1 : 0;
+            cudaGetLastError();
+        }
+        if (iterations)
+            *iterations = h->step;
+        if (queue_depth)
+            *queue_depth = pending;
+        if (degraded_rounds)  // fail-stop: a round completes on the exact view or fails the engine
+            *degraded_rounds = 0;
+        if (replanned_entries)  // every owner is reachable over peer memory: nothing is re-planned
+            *replanned_entries = 0;
+    });
+}
+
+drb_status drb_rb_broadcast_sizes(drb_rb* h) {
+    DRB_REQUIRE(h);
+    // Every round's sel already stored this rank's occupancy row (version i+1) into every
+    // peer's table as self-validating words, so the freshest row is always published; the
+    // reference's re-broadcast at task boundaries (engine.cpp:256-265) has nothing to resend.
+    return DRB_OK;
+}
+
 drb_status drb_rb_device_error(drb_rb* h, uint32_t* out) {
     DRB_REQUIRE(h && out);
     return guarded([&] {

@@ -486,6 +486,31 @@ class engine:
                  "latency_ms": t.latency_ms, "wait_ms": t.wait_ms, "degraded": int(t.degraded)}
                 for t in arr[: n.value]]
 
+    def _counters(self):
+        v = [C.c_uint64(0) for _ in range(4)]
+        check(lib.drb_rb_engine_counters(self.buffer.h, *[C.byref(x) for x in v]))
+        return [int(x.value) for x in v]
+
+    def iterations(self) -> int:
+        """engine::iterations (engine.hpp:88): steps enqueued."""
+        return self._counters()[0]
+
+    def queue_depth(self) -> int:
+        """engine::queue_depth (engine.hpp:89): enqueued steps whose m' is not ready yet."""
+        return self._counters()[1]
+
+    def degraded_rounds(self) -> int:
+        """engine::degraded_rounds (engine.hpp:90): always 0 (fail-stop, DESIGN.md §8)."""
+        return self._counters()[2]
+
+    def replanned_entries(self) -> int:
+        """engine::replanned_entries (engine.hpp:91): always 0 (no unreachable owners)."""
+        return self._counters()[3]
+
+    def broadcast_sizes(self) -> None:
+        """engine::broadcast_sizes (engine.hpp:82): a no-op, every round publishes the row."""
+        check(lib.drb_rb_broadcast_sizes(self.buffer.h))
+
     def total_wait_ms(self) -> float:
         v = C.c_double(0)
         check(lib.drb_rb_total_wait_ms(self.buffer.h, C.byref(v)))

@@ -224,3 +224,30 @@ def test_drain_timings(drb):
         eng.update(dev(spec.payload(0, 60), spec.labels(0, 60)))
         assert [x["iteration"] for x in eng.drain_timings()] == [50]
     eng.shutdown()
+
+
+def test_instrumentation_counters_and_broadcast_sizes(drb):
+    """engine::iterations / queue_depth / degraded_rounds / replanned_entries and
+    broadcast_sizes (engine.hpp:82-92): iterations counts enqueued steps, queue_depth drains to
+    0 once every m' is ready, nothing degrades or re-plans on a healthy engine, and
+    broadcast_sizes (a no-op: rows are published every round) changes nothing."""
+    K, cap, S, b, c, r, seed = 10, 4, 256, 24, 14, 7, 12
+    buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=seed)
+    eng = drb.engine(buf)
+    eng.start()
+    rep = Backend("port").replay(1, K, cap, S, c, r, seed)
+    spec = stream_spec(K, 2, b, S, steps_per_task=5, seed=seed)
+    assert eng.iterations() == 0 and eng.queue_depth() == 0
+    for i in range(12):
+        if i == 5:
+            eng.broadcast_sizes()  # task boundary
+        o, ol, oc = rep.step(spec.payload(0, i)[None], spec.labels(0, i)[None])
+        aug = eng.update(dev(spec.payload(0, i), spec.labels(0, i)))
+        assert eng.iterations() == i + 1
+        d, l = aug.tensors()
+        assert aug.count() == int(oc[0])
+        assert np.array_equal(d.cpu().numpy(), o[0, :aug.count()])
+    eng.synchronize()
+    assert eng.queue_depth() == 0
+    assert eng.degraded_rounds() == 0 and eng.replanned_entries() == 0
+    eng.shutdown()
