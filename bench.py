@@ -73,6 +73,8 @@ class ClockSampler:
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_dev{device}_{os.getpid()}.csv")
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):  # (experiments: the timed region without the sampler)
+            return self
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -356,6 +358,14 @@ def main():
         step += cnt
         stream.synchronize()
     lab = labels_for(step)
+    # The clock sampler starts before the warm-up steps (it needs ~0.3 s to produce samples): the
+    # GPUs then go from the warm-up straight into the timed region instead of idling while it
+    # starts, which would time the first microseconds of the region at ramping clocks.
+    nvl = NvlinkCounters(local)  # (NVML init here, not between the warm-up and the timed region)
+    clocks = ClockSampler(local)
+    late_clocks = bool(os.environ.get("BENCH_CLOCKS_LATE"))  # (experiments: the old order)
+    if not late_clocks:
+        clocks.__enter__()
     eng.run(data, lab, args.warmup, first=0, stream=stream)
     step += args.warmup
     stream.synchronize()
@@ -365,11 +375,12 @@ def main():
     # The K launches are captured into a CUDA graph beforehand (host launch cost paid
     # outside the timed region, as a training loop would replay a captured step).
     resident = eng.engine_info()["resident"]
-    nvl = NvlinkCounters(local)
     run = eng.prepare_run(data, lab, args.steps, first=args.warmup) if not args.no_graph else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    if late_clocks:
+        clocks.__enter__()
+    try:
         # NVML counters before the barrier: a slow NVML query must not skew the ranks' starts
         nvl0 = nvl.read() if (nvl.ok and N > 1) else None
         barrier()
@@ -383,6 +394,8 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
+    finally:
+        clocks.__exit__(None, None, None)
     timed_instances = eng.engine_info()["instances"] - inst0
     nvl1 = nvl.read() if (nvl.ok and N > 1) else None
     if run is not None:
@@ -478,7 +491,7 @@ def main():
     # it also reports 20 steps)
     cpp_update = None
     exe = os.path.join(ROOT, "tools", "update_bench")
-    if N == 1 and os.path.exists(exe):
+    if N == 1 and os.path.exists(exe) and not os.environ.get("BENCH_NO_CPP"):
         try:
             res = subprocess.run([exe, "2000", str(local), str(aug_ring)], capture_output=True, text=True,
                                  timeout=300)

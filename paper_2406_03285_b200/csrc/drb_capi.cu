@@ -1688,12 +1688,16 @@ drb_status drb_rb_aug_count(drb_rb* h, const drb_aug* aug, uint32_t* count) {
         }
         h->wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         const volatile uint32_t* mb = h->mailbox;
+        // `ready` first: the ready publisher writes a slot's error word before it publishes
+        // `ready` (failed or not), so an error of this step is visible once `ready` covers it
+        const uint64_t rd = h->rmode ? *mb64(h, kMbReady) : ~0ull;
+        std::atomic_thread_fence(std::memory_order_acquire);
         const uint32_t e = mb[mb_err(aug->ring_slot, h->aug_ring)];
         *count = mb[mb_count(aug->ring_slot)];
+        if (rd < aug->step + 1 || (h->rmode && rd >= kReadyFailed && aug->step >= *mb64(h, kMbFailedAt)))
+            fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(mb[kMbSticky]));
         if (e)
             fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(e));
-        if (h->rmode && *mb64(h, kMbReady) < aug->step + 1)  // (the sticky error ended the wait)
-            fail(DRB_ERR_TRAINING, "engine: round failed with status " + std::to_string(mb[kMbSticky]));
     });
 }
 
@@ -1818,7 +1822,10 @@ drb_status drb_rb_device_error(drb_rb* h, uint32_t* out) {
         cuda_check(cudaDeviceSynchronize(), "order");
         cuda_check(cudaMemcpy(&st, h->sel + h->cur_sel, sizeof st, cudaMemcpyDeviceToHost), "state");
         cuda_check(cudaMemcpy(&pst, h->plan + h->cur_plan, sizeof pst, cudaMemcpyDeviceToHost), "state");
-        *out = st.error ? st.error : pst.error;
+        // the mailbox's sticky word first: the resident engine stops at the failing role, so the
+        // state parity the host expects after its posted steps may predate the failure
+        const uint32_t sticky = reinterpret_cast<volatile uint32_t*>(h->mailbox)[kMbSticky];
+        *out = sticky ? sticky : (st.error ? st.error : pst.error);
     });
 }
 

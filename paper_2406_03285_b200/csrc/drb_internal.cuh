@@ -220,6 +220,9 @@ constexpr uint64_t kReadyFailed = 1ull << 62;  // ready after a failure: release
 // take two): the host's posted-descriptor count, the leaving instance's announcement, the
 // host's request to leave as soon as idle.
 constexpr uint32_t kMbHostPosted = 2, kMbExiting = 4, kMbQuiesce = 6, kMbDescDone = 8, kMbReady = 10;
+// the first step the ready publisher did not make ready when the engine failed (written before
+// `ready` turns kReadyFailed, so a waiter that sees the failure also sees where it began)
+constexpr uint32_t kMbFailedAt = 12;
 
 struct RunParams {
     StepParams base;  // per-iteration fields patched on device (run_patch)

@@ -1749,8 +1749,9 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
     SeenFlag ad{&rp.ctl->a_done, 0}, bd{&rp.ctl->b_done, 0}, sd{&rp.ctl->sel_done, 0};
     FeedCursor c;
     cursor_init(c, i0, j0);
+    uint64_t i = i0;
 #pragma unroll 1
-    for (uint64_t i = i0;; ++i) {
+    for (;; ++i) {
         if (!wait_admit(rp, adm, i))
             break;
         cursor_seek(c, rp, i);
@@ -1790,6 +1791,9 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
         }
     }
     if (run_failed(rp)) {  // release every stream (and host) still waiting for an m' of this engine
+        if (b.mailbox)
+            *reinterpret_cast<volatile unsigned long long*>(b.mailbox + kMbFailedAt) = i;
+        __threadfence_system();
         st_release_sys(&rp.ctl->ready, kReadyFailed);
         *rp.ready_host = kReadyFailed;
     }

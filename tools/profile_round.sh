@@ -6,8 +6,8 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 R=${1:-r2}
-ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
-    --log-file gpurun_out/ncu_launches_$R.csv python bench.py --steps 20 --warmup 5 --no-cpu --e2e-steps 10 \
+BENCH_NO_CPP=1 ncu --target-processes application-only --metrics gpu__time_duration.sum --clock-control none \
+    -c 4000 --csv --log-file gpurun_out/ncu_launches_$R.csv python bench.py --steps 20 --warmup 5 --no-cpu --e2e-steps 10 \
     > gpurun_out/ncu_launches_$R.log 2>&1
 echo "launch list rc $?"
 ncu --set full --import-source on --clock-control none -k regex:drb_run_kernel --launch-skip 1 -c 1 \
