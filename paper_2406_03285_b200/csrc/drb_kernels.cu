@@ -730,21 +730,34 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
     const uint64_t* tv1 = reinterpret_cast<const uint64_t*>(p.region[me] + p.off_table) +
                           uint64_t(p.tslot_out) * NK;
     {
+        // kU words per thread in flight per pass (each word validates itself: no ordering
+        // between them), then a spin only on the words that have not landed yet — one round
+        // trip for the whole view instead of one per NK/T words (K = 1000 at c3)
+        constexpr uint32_t kU = 8;
         uint64_t t0 = 0;
 #pragma unroll 1
-        for (uint32_t x = tid; x < NK; x += T) {
-            uint64_t w = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
-            while (!occ_is(w, p.step + 1)) {
-                if (t0 == 0)
-                    t0 = globaltimer();
-                else if (globaltimer() - t0 > p.timeout_ns) {
-                    misc[0] = DRB_ERR_TRANSPORT;
+        for (uint32_t base = tid; base < NK; base += T * kU) {
+            uint64_t w[kU];
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u)
+                w[u] = base + u * T < NK ? *reinterpret_cast<const volatile uint64_t*>(tv1 + base + u * T) : 0;
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u) {
+                const uint32_t x = base + u * T;
+                if (x >= NK)
                     break;
+                while (!occ_is(w[u], p.step + 1)) {
+                    if (t0 == 0)
+                        t0 = globaltimer();
+                    else if (globaltimer() - t0 > p.timeout_ns) {
+                        misc[0] = DRB_ERR_TRANSPORT;
+                        break;
+                    }
+                    __nanosleep(32);
+                    w[u] = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
                 }
-                __nanosleep(32);
-                w = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
+                pre[x] = occ_of(w[u]);
             }
-            pre[x] = occ_of(w);
         }
     }
     cta_bar(bar, T);

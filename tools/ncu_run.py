@@ -14,6 +14,7 @@ from paper_2406_03285_b200.workload import device_ring, stream_spec  # noqa: E40
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 K, cap, S, b, r, c = 100, 48, 150528, 56, 7, 14
+K, cap = int(os.environ.get("NCU_K", K)), int(os.environ.get("NCU_CAP", cap))  # c3: NCU_K=1000 NCU_CAP=128
 spec = stream_spec(K, 4, b, S, steps_per_task=100, seed=1)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 ring = int(os.environ.get("AUG_RING", "0"))
