@@ -1436,14 +1436,21 @@ __device__ void run_fail(const RunParams& rp, uint32_t err, uint32_t where) {
 
 // *f >= want, or false once the engine failed / the wait timed out (then the engine fails).
 // Only waits on admitted iterations use this: those complete unless a peer stalls.
-__device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, bool sys) {
-    if ((sys ? ld_acquire_sys(f) : ld_acquire_gpu(f)) >= want)  // satisfied: no timer read
+__device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, bool sys, uint64_t* got = nullptr) {
+    uint64_t v = sys ? ld_acquire_sys(f) : ld_acquire_gpu(f);
+    if (v >= want) {  // satisfied: no timer read
+        if (got)
+            *got = v;
         return true;
+    }
     const uint64_t t0 = globaltimer();
     for (;;) {
-        const uint64_t v = sys ? ld_acquire_sys(f) : ld_acquire_gpu(f);
-        if (v >= want)
+        v = sys ? ld_acquire_sys(f) : ld_acquire_gpu(f);
+        if (v >= want) {
+            if (got)
+                *got = v;
             return true;
+        }
         if (run_failed(rp))
             return false;
         if (globaltimer() - t0 > rp.base.timeout_ns) {
@@ -1454,6 +1461,37 @@ __device__ bool run_wait(const uint64_t* f, uint64_t want, const RunParams& rp, 
     }
 }
 __device__ __forceinline__ uint64_t back(uint64_t k, uint64_t d) { return k >= d ? k - d : 0; }
+
+// Every peer's word words[w] >= want (w != me, w < N), one thread. `seen` caches the smallest
+// value observed (peers advance in lockstep, so one look usually covers many later waits). The
+// words are read with relaxed loads issued together (one round trip for all peers, not one
+// acquire each); a word still short is then waited for (bounded, acquire). With `fence`, one
+// fence.acq_rel.sys after a fresh look is the acquire for the relaxed reads (a system fence
+// costs microseconds: callers that publish with a system-scope release next pass false — the
+// release's fence follows the reads).
+__device__ bool wait_peers(const uint64_t* words, uint32_t N, uint32_t me, uint64_t want, const RunParams& rp,
+                           uint64_t& seen, bool fence) {
+    if (seen >= want)
+        return true;
+    uint64_t v[kMaxWorld];
+#pragma unroll
+    for (uint32_t w = 0; w < kMaxWorld; ++w) {
+        v[w] = ~0ull;
+        if (w < N && w != me)
+            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[w]) : "l"(words + w) : "memory");
+    }
+    uint64_t lo = ~0ull;
+#pragma unroll
+    for (uint32_t w = 0; w < kMaxWorld; ++w) {
+        if (v[w] < want && !run_wait(words + w, want, rp, true, &v[w]))
+            return false;
+        lo = v[w] < lo ? v[w] : lo;
+    }
+    if (fence)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    seen = lo;
+    return true;
+}
 
 // Iteration i is admitted (its descriptor is visible), or false: this instance stops at or
 // before i, or the engine failed. Unbounded: an idle engine waits here for the next post.
@@ -1564,10 +1602,7 @@ struct SeenFlag {
 __device__ __forceinline__ bool wait_seen(SeenFlag& s, uint64_t want, const RunParams& rp, bool sys = false) {
     if (s.seen >= want)
         return true;
-    if (!run_wait(s.f, want, rp, sys))
-        return false;
-    s.seen = sys ? ld_acquire_sys(s.f) : ld_acquire_gpu(s.f);
-    return true;
+    return run_wait(s.f, want, rp, sys, &s.seen);  // (the value that satisfied the wait: no second load)
 }
 
 __device__ __forceinline__ bool poll_seen(SeenFlag& s, uint64_t want) {  // one acquire load at most
@@ -1760,6 +1795,7 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
     uint32_t* aug_count = reinterpret_cast<uint32_t*>(b.region[b.me] + b.off_counts);
     uint64_t adm = 0;
     SeenFlag ad{&rp.ctl->a_done, 0}, bd{&rp.ctl->b_done, 0}, sd{&rp.ctl->sel_done, 0};
+    uint64_t peers_seen = 0;
     FeedCursor c;
     cursor_init(c, i0, j0);
     uint64_t i = i0;
@@ -1772,9 +1808,8 @@ __device__ void run_ready(const RunParams& rp, uint64_t i0, uint64_t j0) {
         // them (every CTA's arrival for B(i) waited for its A(i); B(i) followed sel(i))
         bool ok = c.early ? wait_seen(ad, i + 1, rp) && wait_seen(bd, i, rp) && wait_seen(sd, i + 1, rp)
                           : wait_seen(bd, i + 1, rp);
-        for (uint32_t w = 0; ok && multi && w < b.N; ++w)
-            if (w != b.me && i > 0)
-                ok = run_wait(&hdr->pushdone[w], i, rp, true);
+        if (ok && multi && i > 0)
+            ok = wait_peers(hdr->pushdone, b.N, b.me, i, rp, peers_seen, false);
         if (!ok) {  // the engine failed: every admitted m' not yet ready reports it
             if (b.mailbox) {
                 volatile uint32_t* mb = b.mailbox;
@@ -1850,7 +1885,7 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
     // [6] bad of the prefetched m_{k+1}, [7] labels of step k already in labs[k & 1]
     volatile uint32_t* hx = reinterpret_cast<volatile uint32_t*>(spec_tmp + 32);
     FeedCursor cur, nxt;  // tid 0's
-    uint64_t adm_seen = 0;
+    uint64_t adm_seen = 0, peers_seen = 0;
     if (tid == 0) {
         sp = b;
         run_patch(sp, rp, i0);
@@ -1909,9 +1944,8 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                 if (ok && seen[1] < wp)
                     ok = run_wait(&rp.ctl->plan_done, wp, rp, false);
                 run_mark(rp, i, 1);
-                for (uint32_t w = 0; ok && multi && w < N; ++w)  // peers' B(i-6) complete (m' slot)
-                    if (w != me && i >= lag)
-                        ok = run_wait(&hdr->pushdone[w], i - lag + 1, rp, true);
+                if (ok && multi && i >= lag)  // peers' B(i-lag) complete (m' slot)
+                    ok = wait_peers(hdr->pushdone, N, me, i - lag + 1, rp, peers_seen, true);
                 // step i+1 already posted: its batch size and labels for the look-ahead warps
                 hx[1] = ~0u;
                 if (ok && (as > i + 1 || ((as = ld_acquire_gpu(&rp.ctl->admitted)) > i + 1))) {
@@ -2182,7 +2216,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
     const uint32_t clen = static_cast<uint32_t>(c1 - c0);
     const uint32_t per_win = clen ? R.arena_bytes / clen : 0;
     const uint32_t pw = plist_words(b.N, b.r), ww = wlist_words(b.nmax), nslot = b.nmax + 1;
-    SeenFlag sdone{&rp.ctl->sel_done, 0}, pdone{&rp.ctl->plan_done, 0}, adone{&rp.ctl->a_done, 0};
+    SeenFlag pdone{&rp.ctl->plan_done, 0}, adone{&rp.ctl->a_done, 0};  // (plan_done > i implies sel_done > i)
     uint64_t adm = 0;
     FeedCursor cur;
     cursor_init(cur, i0, j0);
@@ -2226,7 +2260,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
                 cursor_seek(cur, rp, i);
                 feed_patch(sp, cur, i);
                 if (!fetched)
-                    ok = wait_seen(sdone, i + 1, rp) && wait_seen(pdone, i + 1, rp);
+                    ok = wait_seen(pdone, i + 1, rp);  // plan(i) followed sel(i): implies sel_done > i
             }
         }
         if (!__shfl_sync(kFull, ok ? 1 : 0, 0))
@@ -2389,7 +2423,7 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
         {
             bool pre = false;
             if (lane == 0)
-                pre = poll_seen(sdone, i + 3) && poll_seen(pdone, i + 3);
+                pre = poll_seen(pdone, i + 3);  // (implies sel(i+2))
             if (__shfl_sync(kFull, pre ? 1 : 0, 0)) {
                 fetch_lists(i + 2);
                 fetched = true;
