@@ -515,7 +515,7 @@ __device__ __forceinline__ SelView sel_view(uint32_t* sm, const StepParams& p) {
 // spec (persistent run): a selection computed ahead for the counter spec_ctr (k = min(c, n)
 // draws, no rejection); used when it matches this round's counter and k.
 __device__ void sel_core(const StepParams& p, const SelView& v, bool bad, const uint32_t* spec = nullptr,
-                         uint64_t spec_ctr = ~0ull) {
+                         uint64_t spec_ctr = ~0ull, bool peers_checked = false) {
     const uint32_t lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t N = p.N, K = p.K, me = p.me, n = p.n, cap = p.cap;
@@ -608,7 +608,7 @@ __device__ void sel_core(const StepParams& p, const SelView& v, bool bad, const 
             // longer reads the table slot this row overwrites, and its pushes into the m'
             // slot that plan(i) refills have landed. Normally long true: sel runs ahead.
             const uint32_t lag = aug_lag(p.aug_ring);
-            if (p.step >= lag && lane < N && lane != me &&
+            if (!peers_checked && p.step >= lag && lane < N && lane != me &&
                 !wait_flag(&reinterpret_cast<const RegionHeader*>(p.region[me])->pushdone[lane],
                            p.step - (lag - 1), p.timeout_ns) &&
                 p.mailbox)
@@ -1986,7 +1986,8 @@ __device__ void run_sel_role(const RunParams& rp, uint32_t* sm, StepParams& sp, 
                 run_mark(rp, i, 2);
                 tstamp(rp, i, 1);
             }
-            sel_core(sp, v, hx[5] != 0, spec_sel + 32 * (k & 1), sx[k & 1]);
+            // (the peers' pushdone for the table / m' slot was checked before the hand-over)
+            sel_core(sp, v, hx[5] != 0, spec_sel + 32 * (k & 1), sx[k & 1], true);
             delay_exp(1);
             __syncwarp();
             unsigned long long pt = 0;
