@@ -306,7 +306,8 @@ __device__ uint32_t warp_plan_draw(uint64_t key, uint64_t& ctr, uint32_t want, u
         if (c >= need) {
             if (!dup && rank < need)
                 acc[got + rank] = f;
-            ctr += __fns(nm, 0, need) + 1;
+            // the lane holding the need-th new flat (one ballot, not __fns)
+            ctr += __ffs(__ballot_sync(kFull, !dup && rank == need - 1));
             got = want;
         } else {
             if (!dup)
@@ -339,18 +340,6 @@ __device__ void warp_locate(const uint32_t* acc, uint32_t cnt, const uint32_t* p
         plan[3 * j + 2] = f - pfx[lo];
     }
     __syncwarp();
-}
-
-// Sum of a[0..n) by one warp.
-__device__ uint32_t warp_sum(const uint32_t* a, uint32_t n) {
-    const int lane = threadIdx.x & 31;
-    uint32_t s = 0;
-    for (uint32_t i = lane; i < n; i += 32)
-        s += a[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        s += __shfl_xor_sync(kFull, s, o);
-    return s;
 }
 
 // Exclusive prefix of a[0..n) into out[0..n] (out[n] = total), one warp: each lane scans a
@@ -735,6 +724,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         // trip for the whole view instead of one per NK/T words (K = 1000 at c3)
         constexpr uint32_t kU = 8;
         uint64_t t0 = 0;
+        uint32_t part = 0;  // this thread's share of the view's total (no separate sum pass)
 #pragma unroll 1
         for (uint32_t base = tid; base < NK; base += T * kU) {
             uint64_t w[kU];
@@ -757,8 +747,12 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
                     w[u] = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
                 }
                 pre[x] = occ_of(w[u]);
+                part += occ_of(w[u]);
             }
         }
+        part = __reduce_add_sync(kFull, part);  // T is a multiple of 32
+        if (lane == 0)
+            misc[2 + warp] = part;  // misc[2 .. 2 + T/32): per-warp totals (T/32 <= 9)
     }
     cta_bar(bar, T);
     trace_at(p, 6);
@@ -780,7 +774,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
     if (warp >= 1 && warp <= N) {
         const uint32_t q = warp - 1;
         uint64_t ctr = st->samp_ctr[q];
-        const uint32_t total = warp_sum(pre, NK);
+        const uint32_t total = __reduce_add_sync(kFull, lane < T / 32 ? misc[2 + lane] : 0u);
         if (warp == 1)
         prof_span(p, 14, pt);
         const uint32_t c = warp_plan_draw(p.samp_key[q], ctr, r, total, acc + q * r);
@@ -917,17 +911,28 @@ __device__ void copy_parse(const StepParams& p, const uint32_t* xraw, const uint
     const uint32_t nj = do_push ? xraw[1] : 0;
     const uint32_t n_win = do_update ? wraw[0] : 0;
     const uint32_t* jrow = xraw + 4 + MJ;
+    if (n_win <= 32) {  // lane t holds winner t's slot; one ballot per job (winners hold distinct slots)
+        const uint32_t wslot = lane < n_win ? wraw[3 + 2 * lane] : ~0u;
 #pragma unroll 1
-    for (uint32_t x = lane; x < nj; x += 32) {
-        const uint32_t row = jrow[x];
-        uint32_t src = row;
+        for (uint32_t x = 0; x < nj; ++x) {
+            const uint32_t row = jrow[x];
+            const unsigned hit = __ballot_sync(kFull, wslot == row);
+            if (lane == 0)
+                jsrc[x] = hit ? 0x80000000u | wraw[2 + 2 * (__ffs(hit) - 1)] : row;
+        }
+    } else {
 #pragma unroll 1
-        for (uint32_t t = 0; t < n_win; ++t)  // winners hold distinct slots
-            if (wraw[3 + 2 * t] == row) {
-                src = 0x80000000u | wraw[2 + 2 * t];
-                break;
-            }
-        jsrc[x] = src;
+        for (uint32_t x = lane; x < nj; x += 32) {
+            const uint32_t row = jrow[x];
+            uint32_t src = row;
+#pragma unroll 1
+            for (uint32_t t = 0; t < n_win; ++t)
+                if (wraw[3 + 2 * t] == row) {
+                    src = 0x80000000u | wraw[2 + 2 * t];
+                    break;
+                }
+            jsrc[x] = src;
+        }
     }
     if (fuse) {
 #pragma unroll 1
