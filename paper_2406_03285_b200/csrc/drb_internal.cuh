@@ -293,8 +293,8 @@ __host__ __device__ inline PlanSmem plan_smem(uint32_t N, uint32_t K, uint32_t r
     PlanSmem s{};
     uint32_t w = 0;
     const uint32_t mj = plist_mj(N, r);
-    s.pre = DRB_TAKE(N * K);
-    s.pfx = DRB_TAKE(N * K + 1);
+    s.pre = DRB_TAKE(N * K + (N * K) / 32 + 1);  // padded: one word per 32 (plan_core's scan stripes)
+    s.pfx = DRB_TAKE(N * K + 1 + (N * K + 1) / 32 + 1);
     s.plan = DRB_TAKE(3 * mj);
     s.cnt = DRB_TAKE(N);
     s.acc = DRB_TAKE(mj);

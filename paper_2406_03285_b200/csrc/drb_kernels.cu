@@ -322,6 +322,12 @@ __device__ uint32_t warp_plan_draw(uint64_t key, uint64_t& ctr, uint32_t want, u
 
 // locate (size_table.cpp:29-39): flat -> (owner, class, slot) by binary search over the
 // exclusive prefix pfx[0..NK] (largest i with pfx[i] <= f), one warp.
+// Shared-memory index with one pad word per 32: a lane's contiguous stripe of a prefix array
+// (lane * per + i) then falls on distinct banks (K = 1000 puts 32 words in every stripe).
+template <bool kPad>
+__device__ __forceinline__ uint32_t pidx(uint32_t x) { return kPad ? x + (x >> 5) : x; }
+
+template <bool kPad = false>
 __device__ void warp_locate(const uint32_t* acc, uint32_t cnt, const uint32_t* pfx, uint32_t NK,
                             uint32_t K, uint32_t* plan) {
     const int lane = threadIdx.x & 31;
@@ -330,27 +336,28 @@ __device__ void warp_locate(const uint32_t* acc, uint32_t cnt, const uint32_t* p
         uint32_t lo = 0, hi = NK;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (pfx[mid] <= f)
+            if (pfx[pidx<kPad>(mid)] <= f)
                 lo = mid;
             else
                 hi = mid;
         }
         plan[3 * j] = lo / K;
         plan[3 * j + 1] = lo % K;
-        plan[3 * j + 2] = f - pfx[lo];
+        plan[3 * j + 2] = f - pfx[pidx<kPad>(lo)];
     }
     __syncwarp();
 }
 
 // Exclusive prefix of a[0..n) into out[0..n] (out[n] = total), one warp: each lane scans a
 // contiguous stripe, then a warp scan of the stripe totals.
+template <bool kPad = false>
 __device__ uint32_t warp_exclusive_scan(const uint32_t* a, uint32_t n, uint32_t* out) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t per = (n + 31) / 32;
     const uint32_t b0 = min(n, lane * per), b1 = min(n, b0 + per);
     uint32_t s = 0;
     for (uint32_t i = b0; i < b1; ++i)
-        s += a[i];
+        s += a[pidx<kPad>(i)];
     uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -360,12 +367,12 @@ __device__ uint32_t warp_exclusive_scan(const uint32_t* a, uint32_t n, uint32_t*
     }
     uint32_t excl = x - s;
     for (uint32_t i = b0; i < b1; ++i) {
-        out[i] = excl;
-        excl += a[i];
+        out[pidx<kPad>(i)] = excl;
+        excl += a[pidx<kPad>(i)];
     }
     const uint32_t total = __shfl_sync(kFull, x, 31);
     if (lane == 0)
-        out[n] = total;
+        out[pidx<kPad>(n)] = total;
     __syncwarp();
     return total;
 }
@@ -746,7 +753,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
                     __nanosleep(32);
                     w[u] = *reinterpret_cast<const volatile uint64_t*>(tv1 + x);
                 }
-                pre[x] = occ_of(w[u]);
+                pre[pidx<true>(x)] = occ_of(w[u]);  // (padded: the scan reads stripes)
                 part += occ_of(w[u]);
             }
         }
@@ -785,14 +792,14 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
             st->samp_ctr[q] = ctr;
         }
     } else if (warp == 0) {
-        warp_exclusive_scan(pre, NK, pfx);
+        warp_exclusive_scan<true>(pre, NK, pfx);
     }
     cta_bar(bar, T);
     if (warp == 1)
         prof_span(p, 16, pt);
     if (warp >= 1 && warp <= N) {
         const uint32_t q = warp - 1;
-        warp_locate(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
+        warp_locate<true>(acc + q * r, cnt[q], pfx, NK, K, plan + 3 * q * r);
         prof_span(p, 17, pt);
         if (q == me && (p.mode & kModeAssemble)) {  // labels of m'_{i+1}'s reps (stored label == class)
             const uint32_t nslot = (p.aslot + 1) % p.aug_ring;
