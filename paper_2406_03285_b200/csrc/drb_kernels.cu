@@ -729,7 +729,7 @@ __device__ void plan_core(const StepParams& p, const PlanView& v, uint32_t T, ui
         // kU words per thread in flight per pass (each word validates itself: no ordering
         // between them), then a spin only on the words that have not landed yet — one round
         // trip for the whole view instead of one per NK/T words (K = 1000 at c3)
-        constexpr uint32_t kU = 8;
+        constexpr uint32_t kU = 16;
         uint64_t t0 = 0;
         uint32_t part = 0;  // this thread's share of the view's total (no separate sum pass)
 #pragma unroll 1
@@ -2301,16 +2301,32 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
             cta_mark(sp, 10);
         // W_{k-1} (the other warp's) for the hazard checks
         bool push_hz = false, w_hz = false, own_hz = false;
+        // slot-set intersections: with <= 32 slots on one side, lane t holds slot t and every
+        // probe is one vote (no per-lane scan of the other list)
+        auto hits_any = [&](const uint32_t* list, uint32_t nl, const uint32_t* probe, uint32_t np_, bool skip_batch) {
+            bool hz = false;
+            if (nl <= 32) {
+                const uint32_t mine = lane < nl ? list[1 + lane] : ~0u;
+#pragma unroll 1
+                for (uint32_t x = 0; x < np_ && !hz; ++x) {
+                    const uint32_t s_ = probe[x];
+                    if (!(skip_batch && (s_ >> 31)))
+                        hz = __any_sync(kFull, mine == s_);
+                }
+            } else {
+                for (uint32_t x = lane; x < np_; x += 32) {
+                    const uint32_t s_ = probe[x];
+                    if (!(skip_batch && (s_ >> 31)))
+                        for (uint32_t t = 0; t < nl; ++t)
+                            hz |= list[1 + t] == s_;
+                }
+                hz = __any_sync(kFull, hz);
+            }
+            return hz;
+        };
         if (k > 1) {  // a slot pushed now that this warp's B(k-2) wrote: its stores land first
             const uint32_t* wq = wrows + ((k - 2) & 3) * nslot;
-            const uint32_t nq = wq[0];
-            for (uint32_t x = lane; x < nj; x += 32) {
-                const uint32_t s_ = jsrc[x];
-                if (!(s_ >> 31))
-                    for (uint32_t t = 0; t < nq; ++t)
-                        own_hz |= wq[1 + t] == s_;
-            }
-            own_hz = __any_sync(kFull, own_hz);
+            own_hz = hits_any(wq, wq[0], jsrc, nj, true);
         }
         if (k > 0) {
             if (lane == 0)
@@ -2320,17 +2336,8 @@ __device__ void run_b_warp(const RunParams& rp, uint32_t* sm, const RunSmem& R, 
                 cta_mark(sp, 11);
             const uint32_t* wp = wrows + ((k - 1) & 3) * nslot;
             const uint32_t np = wp[0];
-            for (uint32_t x = lane; x < nj; x += 32) {
-                const uint32_t s_ = jsrc[x];
-                if (!(s_ >> 31))
-                    for (uint32_t t = 0; t < np; ++t)
-                        push_hz |= wp[1 + t] == s_;
-            }
-            for (uint32_t t = lane; t < nw; t += 32)
-                for (uint32_t u = 0; u < np; ++u)
-                    w_hz |= wp[1 + u] == wk[1 + t];
-            push_hz = __any_sync(kFull, push_hz);
-            w_hz = __any_sync(kFull, w_hz);
+            push_hz = hits_any(wp, np, jsrc, nj, true);
+            w_hz = hits_any(wp, np, wk + 1, nw, false);
         }
         const uint32_t pieces = clen ? nj + nw : 0;
         // early-ready steps: the winning batch rows come from m'_i (the A engines copied m_i
