@@ -196,7 +196,6 @@ struct drb_rb {
     uint32_t run_grid = 0;            // CTAs of an instance (2 control + copy CTAs)
     uint64_t idle_ns = 100ull * 1000;  // an idle instance leaves after this long (frees its SMs)
     uint8_t* astage = nullptr;        // staging of unaligned device batches [4][max_batch][S]
-    bool feed_kernels = false;        // post / wait with tiny kernels instead of memory operations
     bool feeder_last = true;          // feeder + ready warps on the last copy CTA, not the sel CTA
     // Under ncu / compute-sanitizer (CUDA_INJECTION64_PATH set) or DRB_TOOL_MODE=1 kernels run
     // one at a time: a resident instance would wait forever for a post queued behind it. So every
@@ -359,11 +358,6 @@ void rmode_launch(drb_rb* h) {
 
 // `s` waits (in stream order) until m'_{end-1} is ready, i.e. every iteration < end is done.
 void rmode_wait(drb_rb* h, uint64_t end, cudaStream_t s) {
-    if (h->feed_kernels) {
-        if (launch_feed_wait(&h->runctl->ready, end, s))
-            fail(DRB_ERR_INTERNAL, std::string("feed wait failed: ") + cudaGetErrorString(cudaGetLastError()));
-        return;
-    }
     const CUresult r = memops().wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(&h->runctl->ready),
                                        end, CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS)
@@ -404,14 +398,11 @@ void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const 
     const uint64_t ex = *mb64(h, kMbExiting);
     const bool launch = h->tool_mode || !h->alive || (ex >> 32) == (h->gen & 0xffffffffull);
     uint64_t* seq = h->feed_seq + (j % kFeedRing);
-    if (h->feed_kernels || launch) {
+    if (launch) {
         // with a launch: the sequence word first, then the instance, then the wait — an
         // instance launched behind work that waits for it would never start under a tool that
         // serialises the device (ncu, compute-sanitizer)
-        if (h->feed_kernels) {
-            if (launch_feed_post(seq, j + 1, s))
-                fail(DRB_ERR_INTERNAL, std::string("feed post failed: ") + cudaGetErrorString(cudaGetLastError()));
-        } else {
+        {
             CUstreamBatchMemOpParams op;
             std::memset(&op, 0, sizeof op);
             op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
@@ -422,8 +413,7 @@ void rmode_post(drb_rb* h, const uint8_t* batches, uint64_t batch_stride, const 
             if (r != CUDA_SUCCESS)
                 fail(DRB_ERR_INTERNAL, "feed post: cuStreamBatchMemOp failed (" + std::to_string(int(r)) + ")");
         }
-        if (launch)
-            rmode_launch(h);
+        rmode_launch(h);
         if (wait_end)
             rmode_wait(h, wait_end, s);
     } else {
@@ -760,10 +750,6 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
             h->a_ahead = std::max(2u, uint32_t(std::strtoul(aa, nullptr, 10)));
         if (const char* fl = std::getenv("DRB_FEEDER_LAST"))
             h->feeder_last = fl[0] != '0';
-        if (const char* fk = std::getenv("DRB_FEED"); fk && std::string(fk) == "kernel")
-            h->feed_kernels = true;
-        if (!memops().ok)
-            h->feed_kernels = true;
         if (h->dbg_bits & 65536) {
             cuda_check(cudaMalloc(&h->prof, 64 * 8), "prof alloc");
             cuda_check(cudaMemset(h->prof, 0, 64 * 8), "prof alloc");
@@ -1060,9 +1046,10 @@ drb_status drb_rb_start(drb_rb* h) {
         h->ver0 = h->ver - h->step;  // iteration i uses table version ver0 + i
         h->sel_par0 = h->cur_sel;
         h->plan_par0 = h->cur_plan;
-        // Resident engine unless disabled (DRB_PERSIST=0) or samples are not 16-byte rows
-        // (TMA bulk copies); the three-kernel path serves those.
-        h->rmode = h->use_persist && h->cfg.sample_bytes % 16 == 0 && h->sm_count >= 4 &&
+        // Resident engine unless disabled (DRB_PERSIST=0), samples are not 16-byte rows (TMA
+        // bulk copies) or the driver has no stream memory operations (its feed); the
+        // three-kernel path serves those.
+        h->rmode = h->use_persist && memops().ok && h->cfg.sample_bytes % 16 == 0 && h->sm_count >= 4 &&
                    run_smem_bytes(h->cfg.world, h->cfg.n_classes, h->cfg.rep_count, h->cfg.max_batch) <= 227u * 1024u;
         if (h->rmode) {
             device_guard g(h->cfg.device);
@@ -1306,11 +1293,7 @@ void rmode_step(drb_rb* h, const void* batch, const uint32_t* labels, uint32_t n
         const bool rel = i >= h->released + h->release_every;
         if (rel)
             h->released = i;
-        if (h->feed_kernels) {
-            if ((rel && launch_feed_post(&h->runctl->consumed, i, consumer)) ||
-                launch_feed_wait(&h->runctl->ready, i + 1, consumer))
-                fail(DRB_ERR_INTERNAL, std::string("feed failed: ") + cudaGetErrorString(cudaGetLastError()));
-        } else {
+        {
             CUstreamBatchMemOpParams ops[2];
             std::memset(ops, 0, sizeof ops);
             uint32_t nop = 0;

@@ -401,8 +401,6 @@ int copy_tma_occupancy(uint32_t smem_bytes, int* out);  // CTAs per SM of the TM
 uint32_t run_smem_bytes(uint32_t N, uint32_t K, uint32_t r, uint32_t nmax);
 int launch_run(const RunParams& rp, uint32_t grid, void* stream);
 // fallback feed without stream memory operations: one thread stores a descriptor / waits for ready
-int launch_feed_post(uint64_t* seq_word, uint64_t value, void* stream);
-int launch_feed_wait(const uint64_t* word, uint64_t want, void* stream);
 uint32_t sel_smem_bytes(uint32_t K, uint32_t nmax);
 uint32_t plan_smem_bytes(uint32_t N, uint32_t K, uint32_t r);
 uint32_t plan_threads(uint32_t N);

@@ -2661,14 +2661,6 @@ __global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_co
         run_copy_role(rp, sm, sp, i0, j0);
 }
 
-// Fallback feed (no stream memory operations): one thread stores a descriptor's sequence word;
-// one thread waits for `ready`.
-__global__ void feed_post_kernel(uint64_t* seq_word, uint64_t value) { st_release_sys(seq_word, value); }
-__global__ void feed_wait_kernel(const uint64_t* word, uint64_t want) {
-    while (ld_acquire_sys(word) < want)
-        __nanosleep(100);
-}
-
 // ---- global-sampling bias test (proj/src/runner/bias.cpp:104-133) -----------------------
 // One warp replays rank 0's global-sampling stream plan after plan — each plan's first
 // counter is where the previous one stopped, so the draws are inherently sequential — and
@@ -2896,16 +2888,6 @@ int launch_run(const RunParams& rp, uint32_t grid, void* stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, drb_run_kernel, rp) == cudaSuccess ? 0 : -1;
-}
-
-int launch_feed_post(uint64_t* seq_word, uint64_t value, void* stream) {
-    feed_post_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(seq_word, value);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-
-int launch_feed_wait(const uint64_t* word, uint64_t want, void* stream) {
-    feed_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(word, want);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_peers_wait(const StepParams& p, void* stream) {

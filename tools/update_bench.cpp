@@ -70,7 +70,8 @@ int main(int argc, char** argv) {
         const uint32_t j = uint32_t(k) % ring;
         return device_batch{data + uint64_t(j) * b * S, labels + uint64_t(j) * b, b};
     };
-    for (int k = 0; k < 400; ++k)  // fill every class to capacity (replacements from here)
+    const int prefill = std::getenv("UB_PREFILL") ? std::atoi(std::getenv("UB_PREFILL")) : 400;
+    for (int k = 0; k < prefill; ++k)  // fill every class to capacity (replacements from here)
         eng.update(batch(k), loader, trainer);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
