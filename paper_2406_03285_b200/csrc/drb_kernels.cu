@@ -233,14 +233,19 @@ __device__ void warp_assign(uint64_t ekey, uint64_t& ectr, uint32_t cap, uint64_
         uint32_t slot = o + rho;
         if (R) {
             const uint64_t v = draw_at(ekey, ectr + 1 + lane);
-            const unsigned vmask = __ballot_sync(kFull, v >= thr);
+            const bool valid = v >= thr;
+            const unsigned vmask = __ballot_sync(kFull, valid);
             if (static_cast<uint32_t>(__popc(vmask)) >= R) {
-                const uint32_t val = static_cast<uint32_t>(red.mod(v));
-                const int pos = rep ? static_cast<int>(__fns(vmask, 0, e + 1)) : 0;
-                const uint32_t got = __shfl_sync(kFull, val, pos);
+                // the e-th replacement takes the e-th valid draw: valid lanes deposit their value
+                // by valid-rank, replacements pick theirs up (no per-lane __fns)
+                const uint32_t vr = __popc(vmask & lt);
+                if (valid && vr < R)
+                    scratch[vr] = static_cast<uint32_t>(red.mod(v));
+                __syncwarp();
                 if (rep)
-                    slot = got;
-                ectr += __fns(vmask, 0, R) + 1;
+                    slot = scratch[e];
+                ectr += __ffs(__ballot_sync(kFull, valid && vr == R - 1));  // past the R-th valid draw
+                __syncwarp();
             } else {
                 if (lane == 0)
                     for (uint32_t x = 0; x < R; ++x)
@@ -2570,6 +2575,21 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
     // could run R-2 iterations ahead of B; DRB_A_AHEAD (default 4) bounds it: A's streaming
     // traffic far ahead delays B's loads
     const uint32_t ahead = min(b.aug_ring - 2, rp.a_ahead);
+    // A(k)'s stores complete while A(k+1)'s loads are in flight: its completion (a_local, and the
+    // A ticket of an early step) is signalled from the next iteration, or at once when no next
+    // step is posted (lane 0's state)
+    int64_t pend_k = -1;
+    uint64_t pend_i = 0;
+    bool pend_early = false;
+    auto flush = [&]() {
+        bulk_wait_all();  // A(pend)'s m'_i rows are written
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        st_release_cta(&fl->a_local, uint64_t(pend_k) + 1);  // for this CTA's arrival (the B ticket)
+        if (pend_early)
+            run_a_arrive(rp, uint64_t(pend_k), pend_i);  // m'_i's batch part is complete
+        run_mark(rp, pend_i, 5);
+        pend_k = -1;
+    };
 #pragma unroll 1
     for (uint64_t k = 0;; ++k) {
         const uint64_t i = i0 + k;
@@ -2577,6 +2597,8 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
         uint32_t n = 0;
         uint64_t bp = 0, lp = 0;
         bool early = false;
+        if (lane == 0 && pend_k >= 0 && !(adm > i || (adm = ld_acquire_gpu(&rp.ctl->admitted)) > i))
+            flush();  // nothing to overlap with: complete the previous step now
         if (lane == 0) {
             ok = wait_admit(rp, adm, i) && wait_seen(bdone, i0 + back(k, ahead), rp);
             if (ok) {
@@ -2622,6 +2644,8 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                     mbar_expect_tx(bars + (x - w0), len);
                     bulk_load(ringA + (x - w0) * CH, batch + off, len, bars + (x - w0));
                 }
+                if (pend_k >= 0)
+                    flush();  // the previous step's stores finish under these loads
                 for (uint32_t x = w0; x < w1; ++x) {
                     const uint64_t off = alo + uint64_t(x) * CH;
                     const uint32_t len = static_cast<uint32_t>(min64(CH, ahi - off));
@@ -2631,19 +2655,19 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
                 }
                 bulk_commit();
             }
-            bulk_wait_all();  // A(k)'s m'_i rows are written
-            asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (pend_k >= 0)
+                flush();  // (an empty batch: no window)
+            pend_k = int64_t(k);
+            pend_i = i;
+            pend_early = early;
         }
-        __syncwarp();  // (the other lanes' label stores are ordered before lane 0's release)
-        if (lane == 0) {
-            st_release_cta(&fl->a_local, k + 1);  // for this CTA's arrival (the B ticket)
-            if (early)
-                run_a_arrive(rp, k, i);  // m'_i's batch part is complete: ready(i), and every B(i)
-            run_mark(rp, i, 5);
-        }
+        __syncwarp();  // (the other lanes' label stores are ordered before lane 0's later release)
     }
-    if (lane == 0)
+    if (lane == 0) {
+        if (pend_k >= 0 && !run_failed(rp))
+            flush();
         bulk_wait_all();
+    }
 }
 
 __global__ void __launch_bounds__(kRunThreads, 1) drb_run_kernel(const __grid_constant__ RunParams rp) {
