@@ -202,7 +202,7 @@ struct drb_rb {
     // post launches its own instance (after the post's sequence word) and instances leave as
     // soon as they are idle.
     bool tool_mode = false;
-    uint32_t a_ahead = 4;             // A's run-ahead over the completed B (DRB_A_AHEAD)
+    uint32_t a_ahead = 8;             // A's run-ahead over the completed B (DRB_A_AHEAD)
     uint64_t released = 0;            // split steps: the last m' release written (step index)
     uint64_t release_every = 1;       // split steps: release cadence, max(1, (R - 2) / 4)
     uint64_t* timings = nullptr;      // DRB_RB_FLAG_TIMINGS: per-round device stamps [kTimingRing][8]

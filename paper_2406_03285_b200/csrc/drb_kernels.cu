@@ -2572,7 +2572,7 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
     cursor_init(cur, i0, j0);
     // A(i) writes m'_i's batch rows into the ring slot m'_{i-R} held: that m' was complete (its
     // pushes, B(i-R-1), done), read by B(i-R) (sourcing winners) and released (admission), so A
-    // could run R-2 iterations ahead of B; DRB_A_AHEAD (default 4) bounds it: A's streaming
+    // could run R-2 iterations ahead of B; DRB_A_AHEAD (default 8) bounds it: A's streaming
     // traffic far ahead delays B's loads
     const uint32_t ahead = min(b.aug_ring - 2, rp.a_ahead);
     // A(k)'s stores complete while A(k+1)'s loads are in flight: its completion (a_local, and the
