@@ -95,7 +95,7 @@ typedef struct drb_rb_config {
     int32_t device;           /* CUDA device ordinal                                     */
     uint32_t flags;           /* DRB_RB_FLAG_* bits, 0 by default                         */
     uint32_t aug_ring;        /* m' ring depth: m'_i's slot is rewritten by step i+aug_ring;
-                                 0 = 16 (the default), else >= 6. A deep ring keeps every m'
+                                 0 = 32 (the default), else >= 6. A deep ring keeps every m'
                                  of a multi-step run readable (drb_rb_aug_slot)            */
     uint32_t engine_ctas;     /* CTAs (one per SM) of the resident engine while busy; 0 = half
                                  the SMs, leaving the rest to a co-running training step  */

@@ -23,7 +23,7 @@ DRB_ERR_USAGE = 7
 DRB_ERR_INTERNAL = 8
 MAX_WORLD = 8
 FLAG_TIMINGS = 1  # DRB_RB_FLAG_TIMINGS
-AUG_RING = 16  # default m' ring depth (drb_rb_config.aug_ring = 0)
+AUG_RING = 32  # default m' ring depth (drb_rb_config.aug_ring = 0)
 
 
 class drb_error(RuntimeError):

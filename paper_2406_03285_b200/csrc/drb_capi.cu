@@ -626,7 +626,7 @@ drb_status drb_rb_create(const drb_rb_config* cfg, drb_rb** out) {
         if (c.rep_count > 4096 || uint64_t(c.world) * c.rep_count > 4096)
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: world * rep_count must be <= 4096");
         if (c.aug_ring != 0 && (c.aug_ring < kAugRingMin || c.aug_ring > kAugRingMax))
-            fail(DRB_ERR_CONFIG, "rehearsal_buffer: aug_ring must be 0 (default 16) or in [6, 65536]");
+            fail(DRB_ERR_CONFIG, "rehearsal_buffer: aug_ring must be 0 (default 32) or in [6, 65536]");
         if (uint64_t(c.world) * c.n_classes * c.per_class_cap >= (1ull << 31))
             fail(DRB_ERR_CONFIG, "rehearsal_buffer: N*K*cap must be < 2^31 slots");
         const uint32_t plan_bytes = plan_smem_bytes(c.world, c.n_classes, c.rep_count);

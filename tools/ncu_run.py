@@ -36,7 +36,7 @@ for _ in range(reps):  # each rep: synchronise (the instance leaves), then one t
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1) * 1000 / steps)
 ts.sort()
-print(f"run of {steps} steps (aug_ring {ring or 16}, A ahead {os.environ.get('DRB_A_AHEAD', 8)}): "
+print(f"run of {steps} steps (aug_ring {ring or 32}, A ahead {os.environ.get('DRB_A_AHEAD', 8)}): "
       f"{ts[len(ts) // 2]:.2f} us/step (median of {reps}, min {ts[0]:.2f}), instances {eng.engine_info()}")
 assert eng.device_error() == 0
 eng.shutdown()

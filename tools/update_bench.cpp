@@ -30,7 +30,7 @@ using namespace drb::b200;
 int main(int argc, char** argv) {
     const int steps = argc > 1 ? std::atoi(argv[1]) : 200;
     const int device = argc > 2 ? std::atoi(argv[2]) : 0;
-    const uint32_t aug_ring = argc > 3 ? uint32_t(std::atoi(argv[3])) : 0;  // 0: the default 6 slots
+    const uint32_t aug_ring = argc > 3 ? uint32_t(std::atoi(argv[3])) : 0;  // 0: the default (32 slots)
     CK(cudaSetDevice(device));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -128,7 +128,7 @@ int main(int argc, char** argv) {
     std::printf("{\"split_us_per_step\": %.3f, \"serial_us_per_step\": %.3f, \"split_us_per_step_20\": %.3f, "
                 "\"serial_us_per_step_20\": %.3f, \"host_us_per_call_split\": %.3f, \"host_us_per_call_serial\": %.3f, "
                 "\"steps\": %d, \"engine_ctas\": %d, \"aug_ring\": %u}\n",
-                split, serial, split20, serial20, h_split, h_serial, steps, sms, aug_ring ? aug_ring : 6u);
+                split, serial, split20, serial20, h_split, h_serial, steps, sms, aug_ring ? aug_ring : 32u);
     cudaFree(data);
     cudaFree(labels);
     return 0;
