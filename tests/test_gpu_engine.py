@@ -167,7 +167,7 @@ def test_engine_dies_on_bad_label(drb):
 def test_split_streams_pipelined_parity(drb, ring):
     """update(m_i, stream=loader, consumer=trainer) (drb_rb_step_split): every post goes out on
     the loader stream back to back (the engine pipelines them); the trainer stream copies each
-    m'_i right after its wait. With the default 6-slot m' ring the engine may refill a slot
+    m'_i right after its wait. With the smallest m' ring (6 slots) the engine may refill a slot
     only after the trainer released it — the copies must still equal the oracle's m'."""
     K, cap, S, b, c, r, steps = 20, 6, 4096, 40, 14, 9, 64
     buf = drb.rehearsal_buffer(K, cap, S, max_batch=b, candidate_count=c, rep_count=r, seed=21, aug_ring=ring)
