@@ -2149,15 +2149,7 @@ __device__ bool run_b_arrive(const RunParams& rp, const StepParams& p, uint64_t 
         *reinterpret_cast<volatile uint32_t*>(t) = 0;  // slot reused by iteration k+32
         if (!run_wait(&rp.ctl->b_done, i, rp, false))
             return false;
-        if (multi) {
-            asm volatile("fence.acq_rel.sys;" ::: "memory");
-            for (uint32_t w = 0; w < p.N; ++w)
-                if (w != p.me)
-                    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(
-                                     &reinterpret_cast<RegionHeader*>(p.region[w])->pushdone[p.me]),
-                                 "l"(i + 1)
-                                 : "memory");
-        }
+        (void)multi;  // pushdone at the peers: run_peer_publisher, off this chain
         if (a_too)
             raise_a_done(rp, i + 1);
         st_release_gpu(&rp.ctl->b_done, i + 1);
@@ -2485,6 +2477,39 @@ __device__ void run_a_arrive(const RunParams& rp, uint64_t k, uint64_t i) {
     }
 }
 
+// Multi-rank: pushdone[me] = b_done at every peer, one thread, in order. The system-scope fence
+// that makes this rank's pushes visible to the peers before the word costs microseconds; here it
+// is off the arrivals' b_done chain (the last arrival's GPU-scope release of b_done covers every
+// CTA's completed B stores; this thread acquires it, fences at system scope, then stores). It
+// leaves once everything this instance admitted is B-complete and announced.
+__device__ void run_peer_publisher(const RunParams& rp, uint64_t i0) {
+    const StepParams& b = rp.base;
+    uint64_t pub = i0;
+#pragma unroll 1
+    for (uint32_t spin = 0;; ++spin) {
+        const uint64_t bd = ld_acquire_gpu(&rp.ctl->b_done);
+        if (bd > pub) {
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (uint32_t w = 0; w < b.N; ++w)
+                if (w != b.me)
+                    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(
+                                     &reinterpret_cast<RegionHeader*>(b.region[w])->pushdone[b.me]),
+                                 "l"(bd)
+                                 : "memory");
+            pub = bd;
+            spin = 0;
+            continue;
+        }
+        if (run_failed(rp))
+            return;
+        const uint64_t st = *reinterpret_cast<volatile const uint64_t*>(&rp.ctl->stop_at);
+        if ((st >> 40) == (rp.gen & 0xffffffu) && bd >= (st & kStopMask))
+            return;
+        if (spin > 64)
+            __nanosleep(spin < 4096 ? 32 : 256);
+    }
+}
+
 // CTAs 2..: copies. The B engines work on a fixed byte COLUMN [c0, c1) of every row — so every
 // slab access to a given byte happens in this one CTA, in program order, and there is no
 // grid-wide hand-off between their iterations:
@@ -2502,6 +2527,8 @@ __device__ void run_copy_role(const RunParams& rp, uint32_t* sm, StepParams* sp2
             else if (warp == 5 && lane == 0)
                 run_ready(rp, i0, j0);
         }
+        if (blockIdx.x == gridDim.x - 1 && warp == 6 && lane == 0 && (rp.base.mode & kModePeers) && rp.base.N > 1)
+            run_peer_publisher(rp, i0);
         return;
     }
     const StepParams& b = rp.base;
